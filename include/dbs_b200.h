@@ -1,0 +1,290 @@
+/*
+ * dbs_b200.h -- C ABI of the B200-native Dynamic Batch Size (DBS) hot path.
+ *
+ * One shared library (paper_2007_11831_b200/libdbs_b200.so) exports every symbol
+ * below.  Plain pointers, sizes and status codes only: no torch or CUDA types in
+ * the signatures (streams are passed as `void*` = cudaStream_t, NULL = legacy
+ * default stream).  Each entry point names the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/dbsim/).  The Python host mirror
+ * (the paper_2007_11831_b200 package) binds these with ctypes; INTEGRATION.md shows
+ * the binding the reference's own package would add.
+ *
+ * Two calling conventions:
+ *   dbs_*            HOST buffers in/out.  The call copies inputs to the device,
+ *                    runs the kernel, copies results back and synchronises.  This
+ *                    is the drop-in for the reference's pure functions.
+ *   dbs_dev_*        DEVICE buffers, asynchronous on `stream`; errors that the
+ *                    reference raises are written to a device status word so the
+ *                    epoch loop never leaves the GPU.
+ *
+ * Every function returns a dbs_status.  The codes map 1:1 onto the reference
+ * exception classes of errors.py:4-53 (see dbs_status below).
+ */
+#ifndef DBS_B200_H
+#define DBS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* Status codes  (errors.py:4-53)                                            */
+/* ------------------------------------------------------------------------ */
+typedef enum {
+  DBS_OK = 0,
+  DBS_ERR_INVALID_MEASUREMENT = 1, /* InvalidMeasurementError  errors.py:8  */
+  DBS_ERR_INVALID_PERFORMANCE = 2, /* InvalidPerformanceError  errors.py:12 */
+  DBS_ERR_BUDGET_TOO_SMALL = 3,    /* BudgetTooSmallError      errors.py:16 */
+  DBS_ERR_INVALID_BATCH = 4,       /* InvalidBatchError        errors.py:20 */
+  DBS_ERR_EMPTY_PARTITION = 5,     /* EmptyPartitionError      errors.py:24 */
+  DBS_ERR_DATASET_TOO_SMALL = 6,   /* DatasetTooSmallError     errors.py:28 */
+  DBS_ERR_CONFIGURATION = 7,       /* ConfigurationError       errors.py:32 */
+  DBS_ERR_EMPTY_BATCH = 9,         /* EmptyBatchError          errors.py:40 */
+  DBS_ERR_INVALID_STEP_SIZE = 10,  /* InvalidStepSizeError     errors.py:44 */
+  DBS_ERR_FSUM_OVERFLOW = 20,      /* math.fsum OverflowError ("intermediate overflow") */
+  DBS_ERR_FSUM_INF_NAN = 21,       /* math.fsum ValueError ("-inf + inf in fsum")       */
+  DBS_ERR_INT_OVERFLOW = 22,       /* value outside int64 where Python has big ints      */
+  DBS_ERR_ARGUMENT = 30,           /* NULL pointer / unsupported size                    */
+  DBS_ERR_CUDA = 40,               /* CUDA runtime / driver failure (dbs_last_error())   */
+  DBS_ERR_UNSUPPORTED = 41         /* hardware feature missing (not sm_100)              */
+} dbs_status;
+
+/* Human-readable detail of the last error on the calling thread. */
+const char* dbs_last_error(void);
+/* Library version and the SM architecture the kernels were built for (100). */
+int dbs_version(int* major, int* minor, int* sm_arch);
+/* 1 when a CUDA device with compute capability 10.x is visible. */
+int dbs_device_ok(void);
+
+/* ------------------------------------------------------------------------ */
+/* (3) Epoch-end DBS controller  -- allocation.py, single-CTA fp64 kernel   */
+/* All fp64 arithmetic is IEEE round-to-nearest with no FMA contraction, the */
+/* correctly-rounded sum of math.fsum, and exact int64/int128 rationals, so  */
+/* results are bit-identical to the reference.                               */
+/* ------------------------------------------------------------------------ */
+
+/* allocation.evaluate_performance (allocation.py:78-88), applied to n pairs. */
+int dbs_evaluate_performance(const double* shares, const double* times, int64_t n,
+                             double* perf_out, int64_t* bad_index);
+
+/* allocation.compute_batch_fractions (allocation.py:91-102). */
+int dbs_compute_batch_fractions(const double* perfs, int64_t n, double* fractions_out,
+                                int64_t* bad_index);
+
+/* allocation.scale_to_real_batches (allocation.py:105-113). */
+int dbs_scale_to_real_batches(const double* fractions, int64_t n, int64_t total_budget,
+                              double* real_out);
+
+/* allocation.round_twice (allocation.py:116-137). */
+int dbs_round_twice(const double* real_batches, int64_t n, int64_t total_budget,
+                    int64_t* int_out);
+
+/* allocation._raise_zero_batches (allocation.py:191-204). */
+int dbs_raise_zero_batches(const int64_t* int_batches, int64_t n, int64_t* out);
+
+/* allocation.partition_ranges (allocation.py:140-155): range i is
+ * [cum[i]/cum[n], cum[i+1]/cum[n]) as exact rationals; cum has n+1 entries. */
+int dbs_partition_ranges(const int64_t* int_batches, int64_t n, int64_t* cum_out);
+
+/* A range bound as the reference may receive it: an exact rational
+ * (Fraction or int: kind 0, num/den with den > 0) or an IEEE double (kind 1). */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  int64_t num;
+  int64_t den;
+  double value;
+} dbs_bound;
+
+/* allocation.spans_from_ranges (allocation.py:158-188): spans_out[2i],
+ * spans_out[2i+1] = half-open sample span of worker i. */
+int dbs_spans_from_ranges(const dbs_bound* lo, const dbs_bound* hi, int64_t n,
+                          int64_t dataset_size, int64_t* spans_out);
+
+/* allocation.plan_next_epoch (allocation.py:207-244), whole pipeline in one
+ * launch.  Outputs: int_batches[n], cum[n+1] (ranges), spans[2n]. */
+int dbs_plan_next_epoch(const double* prev_shares, const double* prev_times, int64_t n,
+                        int64_t total_budget, int64_t dataset_size, int64_t epoch,
+                        int64_t* int_batches_out, int64_t* cum_out, int64_t* spans_out,
+                        int64_t* bad_index);
+
+/* Device-resident re-plan: cluster.run_training's DBS branch
+ * (cluster.py:253-271) followed by plan_next_epoch, with the previous
+ * epoch's measured per-worker compute seconds in d_times.
+ *   d_prev_spans [2n]  previous plan's spans (shares = width / D, allocation.py:72-75)
+ *   d_smoothed   [n]   EMA state (cluster.py:263-266), updated in place
+ *   d_flags      [2]   [0] = EMA state valid, [1] = status (dbs_status) out
+ * epoch == 0 or kind != dbs gives the even plan (cluster.py:254-255, 223-231).
+ * Outputs land in d_int_batches[n], d_cum[n+1], d_spans[2n], d_iters[1]
+ * (iterations_for_plan, cluster.py:159-170). */
+int dbs_dev_replan(const int64_t* d_prev_spans, const double* d_times, int64_t n,
+                   int64_t total_budget, int64_t dataset_size, int64_t epoch, int32_t adaptive,
+                   double perf_smoothing, double* d_smoothed, int32_t* d_flags,
+                   int64_t* d_int_batches, int64_t* d_cum, int64_t* d_spans, int64_t* d_iters,
+                   void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Sample assignment  -- sgdlab.py:358, 372-374                              */
+/* numpy Generator(PCG64) semantics: SeedSequence seeding, PCG64 XSL-RR      */
+/* 128/64, buffered next_uint32, masked-rejection random_interval, reversed  */
+/* Fisher-Yates (numpy 2.3 Generator.permutation).                           */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t state_hi, state_lo; /* 128-bit LCG state */
+  uint64_t inc_hi, inc_lo;     /* 128-bit odd increment */
+  uint32_t has_uint32;         /* buffered upper half pending */
+  uint32_t uinteger;           /* the buffered upper half */
+} dbs_pcg64;
+
+/* numpy.random.default_rng(seed) for a non-negative integer seed given as
+ * little-endian 32-bit words (SeedSequence entropy). Host-side setup. */
+int dbs_pcg64_seed(const uint32_t* seed_words, int32_t n_words, dbs_pcg64* out);
+
+/* Host-buffer drop-in: for each span i (in order, one generator),
+ * perm_out[off_i + k] = start_i + rng.permutation(end_i - start_i)[k],
+ * off_i = sum of earlier span widths.  rng is advanced in place. */
+int dbs_permute_spans(dbs_pcg64* rng, const int64_t* spans, int64_t n, int64_t* perm_out);
+
+/* Device version.  d_rng is device-resident and advanced in place.
+ * only_span = -1 materialises every span; otherwise only that span's
+ * indices are written (the draws of every span are still consumed, so all
+ * ranks stay in lock-step with the reference's single generator).
+ * d_draws is scratch of at least sum(widths) int32. */
+int dbs_dev_permute_spans(dbs_pcg64* d_rng, const int64_t* d_spans, int64_t n,
+                          int64_t total_width, int64_t only_span, int64_t* d_perm_out,
+                          int32_t* d_draws, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Repartition gather  -- the row gathers offsets[idx] / features[idx]       */
+/* (sgdlab.py:82, 144) done once per epoch as a coalesced shard repack.      */
+/* ------------------------------------------------------------------------ */
+/* dst[r, :] = src[idx[r], :] for r < rows; rows of row_bytes bytes. */
+int dbs_dev_gather_rows(const void* d_src, const int64_t* d_idx, int64_t rows,
+                        int64_t row_bytes, void* d_dst, void* stream);
+/* Same, converting fp32 rows of `cols` elements to bf16 (model input staging). */
+int dbs_dev_gather_rows_f32_bf16(const float* d_src, const int64_t* d_idx, int64_t rows,
+                                 int64_t cols, void* d_dst_bf16, void* stream);
+/* Same for int32 labels. */
+int dbs_dev_gather_i32(const int32_t* d_src, const int64_t* d_idx, int64_t rows,
+                       int32_t* d_dst, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* (2) Batch-weighted aggregation + momentum SGD  -- sgdlab.py:208-238       */
+/* ------------------------------------------------------------------------ */
+enum { DBS_AGG_UNIFORM = 0, DBS_AGG_BATCH_WEIGHTED = 1 };
+
+/* sgdlab.aggregate_gradients (sgdlab.py:208-227) over n device gradient
+ * buffers of P doubles: out = sum_i w_i g_i, w_i = b_i / sum(b) or 1/n. */
+int dbs_dev_aggregate_f64(const double* const* d_grads, const int64_t* batch_sizes, int64_t n,
+                          int32_t mode, int64_t P, double* d_out, void* stream);
+/* sgdlab.sgd_step (sgdlab.py:230-238), out of place:
+ * v' = momentum v + g ; x' = x - step v'. */
+int dbs_dev_sgd_step_f64(const double* d_x, const double* d_g, const double* d_v, int64_t P,
+                         double step, double momentum, double* d_x_out, double* d_v_out,
+                         void* stream);
+/* Fused single-device aggregate + step, in place (the per-iteration update
+ * of run_parallel_sgd, sgdlab.py:385-386), fp64. */
+int dbs_dev_aggregate_sgd_f64(const double* const* d_grads, const int64_t* batch_sizes, int64_t n,
+                              int32_t mode, int64_t P, double step, double momentum,
+                              double* d_x, double* d_v, void* stream);
+/* fp32 model-parameter variant: grads fp32, params/velocity fp32 master,
+ * optional bf16 shadow of the params (GEMM operand) written in the same pass. */
+int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* batch_sizes, int64_t n,
+                              int32_t mode, int64_t P, float step, float momentum, float* d_x,
+                              float* d_v, uint16_t* d_x_bf16, void* stream);
+
+/* Multi-GPU: one process per GPU.  A communicator holds the peer-mapped
+ * (CUDA IPC over NVLink/NVSwitch) symmetric buffers:
+ *   grad[P] fp32, param[P] fp32, param_bf16[P], signal words.
+ * dbs_comm_alloc allocates this rank's symmetric block and returns its IPC
+ * handle bytes; dbs_comm_open maps every peer's block (handles gathered by the
+ * host with any transport, e.g. torch.distributed). */
+typedef struct dbs_comm dbs_comm;
+int dbs_comm_handle_size(void);
+int dbs_comm_alloc(int32_t rank, int32_t world, int64_t P, dbs_comm** out, void* handle_out);
+int dbs_comm_open(dbs_comm* comm, const void* all_handles /* world * handle_size */);
+int dbs_comm_buffers(dbs_comm* comm, float** d_grad, float** d_param, uint16_t** d_param_bf16);
+int dbs_comm_destroy(dbs_comm* comm);
+/* The fused per-iteration kernel: each rank owns shard [r*P/W, (r+1)*P/W);
+ * it loads the shard of every peer's gradient over NVLink, forms
+ * sum_j w_j g_j (w_j = b_j / sum b), applies v' = mom v + g, x' = x - lr v',
+ * and stores x' (fp32 + bf16) into every peer's parameter buffer; in-kernel
+ * signal barriers order the exchange.  d_velocity is this rank's shard.
+ * mode DBS_AGG_* ; batch_sizes is a host array of W entries. */
+int dbs_comm_allreduce_sgd(dbs_comm* comm, const int64_t* batch_sizes, int32_t mode, float step,
+                           float momentum, float* d_velocity_shard, void* stream);
+/* Model averaging (cluster.py:185-186 cadence): params <- sum_j w_j param_j,
+ * same kernel skeleton without the momentum step. */
+int dbs_comm_average_params(dbs_comm* comm, const int64_t* batch_sizes, int32_t mode,
+                            void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* (1) Variable-batch forward/backward  -- per_sample_gradients + mean      */
+/* (sgdlab.py:200-205, 81-82, 143-148) and the named models.                 */
+/* ------------------------------------------------------------------------ */
+/* ConvexProblem (sgdlab.py:33-95): out[w] = mean_k mu (x - opt - offsets[idx_w[k]])
+ * for n_workers index lists concatenated in d_idx with offsets d_off[n+1]. */
+int dbs_dev_quadratic_grads(const double* d_x, const double* d_opt, const double* d_offsets,
+                            int64_t dim, const int64_t* d_idx, const int64_t* d_off,
+                            int64_t n_workers, double mu, double* d_grads_out, void* stream);
+/* LogisticProblem (sgdlab.py:98-159): mean_k (coeff_k feats_k + mu x),
+ * coeff = -y / (1 + exp(y feats.x)). */
+int dbs_dev_logistic_grads(const double* d_x, const double* d_features, const double* d_labels,
+                           int64_t dim, const int64_t* d_idx, const int64_t* d_off,
+                           int64_t n_workers, double mu, double* d_grads_out, void* stream);
+/* ||x - opt||^2 into d_out[slot] (run_parallel_sgd's squared_distances,
+ * sgdlab.py:387-388). */
+int dbs_dev_sq_dist(const double* d_x, const double* d_opt, int64_t dim, double* d_out,
+                    int64_t slot, void* stream);
+
+/* tcgen05 GEMM:  D[M,N] (+)= A[M,K] * B[N,K]^T, bf16 operands, fp32 accumulate
+ * in TMEM.  a_major/b_major: 0 = K contiguous, 1 = M (resp. N) contiguous; lda/ldb
+ * are leading-dimension strides in elements.  epilogue selects the fused tail. */
+enum {
+  DBS_EPI_F32 = 0,           /* D fp32 = acc                                    */
+  DBS_EPI_F32_ACCUM = 1,     /* D fp32 += acc                                   */
+  DBS_EPI_BIAS_RELU_BF16 = 2,/* D bf16 = relu(acc + bias[n]); aux bf16 = acc+bias */
+  DBS_EPI_BIAS_F32 = 3,      /* D fp32 = acc + bias[n]                          */
+  DBS_EPI_BF16 = 4           /* D bf16 = acc                                    */
+};
+int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, const void* d_b,
+                      int32_t b_major, int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N,
+                      int64_t K, int32_t epilogue, const float* d_bias, void* d_aux, void* stream);
+
+/* 2-layer MLP (784 -> H -> C, ReLU, softmax cross-entropy): one variable-batch
+ * forward + backward of a worker's batch.  Params live in one flat fp32
+ * buffer laid out [W1 (H x IN) | b1 (H) | W2 (C x H) | b2 (C)], with a bf16
+ * shadow of the same layout; the flat fp32 gradient of the batch-mean loss is
+ * written to d_grad and the batch-mean loss to d_loss[0]. */
+typedef struct dbs_mlp dbs_mlp;
+int dbs_mlp_create(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch,
+                   dbs_mlp** out);
+int dbs_mlp_destroy(dbs_mlp* m);
+int dbs_mlp_param_count(const dbs_mlp* m, int64_t* out);
+int dbs_mlp_forward_backward(dbs_mlp* m, const uint16_t* d_params_bf16, const float* d_params,
+                             const uint16_t* d_x_bf16, const int32_t* d_labels, int64_t batch,
+                             float* d_grad, float* d_loss, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Worker heterogeneity (cluster.py:25-79 DisturbanceEvent) and timing       */
+/* ------------------------------------------------------------------------ */
+/* Occupy `num_ctas` SMs (one resident CTA per SM, max shared memory) until
+ * *d_stop becomes non-zero: the co-running disturbance of the paper's
+ * robustness experiments.  Launch it on its own stream. */
+int dbs_dev_spin_until(int32_t num_ctas, const volatile int32_t* d_stop, void* stream);
+/* Occupy `num_ctas` SMs for `nanoseconds` (fixed extra work). */
+int dbs_dev_spin_for(int32_t num_ctas, int64_t nanoseconds, void* stream);
+/* Write the device %globaltimer (ns) into d_stamps[slot]. */
+int dbs_dev_stamp(int64_t* d_stamps, int64_t slot, void* stream);
+/* d_seconds[w] += (d_stamps[end] - d_stamps[begin]) * 1e-9 : per-worker
+ * compute time accumulated on the device for the controller. */
+int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, int64_t end,
+                            double* d_seconds, int64_t worker, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DBS_B200_H */
