@@ -176,7 +176,7 @@ int dbs_dev_gather_i32(const int32_t* d_src, const int64_t* d_idx, int64_t rows,
 enum { DBS_AGG_UNIFORM = 0, DBS_AGG_BATCH_WEIGHTED = 1 };
 
 /* sgdlab.aggregate_gradients (sgdlab.py:208-227) over n device gradient
- * buffers of P doubles: out = sum_i w_i g_i, w_i = b_i / sum(b) or 1/n. */
+ * buffers of P doubles (d_grads: HOST array of n device pointers): out = sum_i w_i g_i, w_i = b_i / sum(b) or 1/n. */
 int dbs_dev_aggregate_f64(const double* const* d_grads, const int64_t* batch_sizes, int64_t n,
                           int32_t mode, int64_t P, double* d_out, void* stream);
 /* sgdlab.sgd_step (sgdlab.py:230-238), out of place:
@@ -234,6 +234,18 @@ int dbs_dev_quadratic_grads(const double* d_x, const double* d_opt, const double
 int dbs_dev_logistic_grads(const double* d_x, const double* d_features, const double* d_labels,
                            int64_t dim, const int64_t* d_idx, const int64_t* d_off,
                            int64_t n_workers, double mu, double* d_grads_out, void* stream);
+/* One whole epoch of run_parallel_sgd's hot loop (sgdlab.py:380-391) for the
+ * reference problems in ONE single-CTA launch: for t < iters, every worker's
+ * batch-mean gradient on perm[span_off[w] + t*b_w ...], aggregation
+ * (DBS_AGG_*), heavy-ball step on d_x/d_v in place, and ||x - opt||^2 into
+ * d_sq_out[t].  kind 0 = ConvexProblem (d_data = offsets, bit-exact order),
+ * 1 = LogisticProblem (d_data = features, d_labels = +/-1).  span_off and
+ * batches are HOST arrays; d_grads holds n*dim, d_coeff sum(b) doubles. */
+int dbs_dev_sgd_epoch(int32_t kind, const double* d_data, const double* d_labels, const double* d_opt,
+                      int64_t dim, double mu, const int64_t* d_perm, const int64_t* span_off,
+                      const int64_t* batches, int64_t n_workers, int32_t mode, int64_t iters, double step,
+                      double momentum, double* d_x, double* d_v, double* d_grads, double* d_coeff,
+                      double* d_sq_out, void* stream);
 /* ||x - opt||^2 into d_out[slot] (run_parallel_sgd's squared_distances,
  * sgdlab.py:387-388). */
 int dbs_dev_sq_dist(const double* d_x, const double* d_opt, int64_t dim, double* d_out,

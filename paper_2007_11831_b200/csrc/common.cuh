@@ -1,0 +1,53 @@
+// common.cuh -- shared helpers of libdbs_b200 (status plumbing, launch checks).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/dbs_b200.h"
+
+namespace dbs {
+
+// Thread-local detail string behind dbs_last_error().
+void set_error(const char* fmt, ...);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define DBS_CUDA_TRY(expr)                                                             \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      ::dbs::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return DBS_ERR_CUDA;                                                             \
+    }                                                                                  \
+  } while (0)
+
+#define DBS_LAUNCH_CHECK() DBS_CUDA_TRY(cudaGetLastError())
+
+#define DBS_REQUIRE(cond, code, ...)  \
+  do {                                \
+    if (!(cond)) {                    \
+      ::dbs::set_error(__VA_ARGS__);  \
+      return (code);                  \
+    }                                 \
+  } while (0)
+
+// Grow-only device scratch owned by the library (one per calling thread).
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+};
+int scratch_get(Scratch& s, size_t bytes, void** out);
+
+// Pinned host staging buffer (one per calling thread) for the host-buffer
+// entry points, so H2D/D2H copies are asynchronous and small.
+int pinned_get(size_t bytes, void** out);
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+int num_sms();
+
+}  // namespace dbs

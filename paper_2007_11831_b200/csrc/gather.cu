@@ -1,0 +1,141 @@
+// gather.cu -- coalesced repartition gather (HBM-bound).
+//
+// The reference gathers sample rows by index inside every gradient call
+// (offsets[idx] sgdlab.py:82, features[idx] sgdlab.py:144).  On the B200 the
+// epoch's permuted sample order is applied ONCE per epoch: each worker's shard
+// is repacked contiguously in HBM so every iteration reads a dense slice.
+//
+// Algorithmic bytes per row: 2 * row_bytes (+ 8 B of index).  Mapping: one warp
+// per row (several rows per CTA, grid-stride over rows), 16-byte vector loads
+// and stores with 4 independent requests in flight per lane; rows that are not
+// 16-byte aligned fall back to 4-byte or byte copies.
+#include "common.cuh"
+
+namespace dbs {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kUnroll = 4;
+
+template <typename V>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    gather_rows_kernel(const V* __restrict__ src, const int64_t* __restrict__ idx, int64_t rows,
+                       int64_t vec_per_row, V* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const V* s = src + __ldg(&idx[r]) * vec_per_row;
+    V* d = dst + r * vec_per_row;
+    int64_t c = lane;
+    for (; c + 32 * (kUnroll - 1) < vec_per_row; c += 32 * kUnroll) {
+      V v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) v[u] = __ldcs(s + c + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) __stcs(d + c + 32 * u, v[u]);
+    }
+    for (; c < vec_per_row; c += 32) __stcs(d + c, __ldcs(s + c));
+  }
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    gather_bytes_kernel(const unsigned char* __restrict__ src, const int64_t* __restrict__ idx,
+                        int64_t rows, int64_t row_bytes, unsigned char* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const unsigned char* s = src + idx[r] * row_bytes;
+    unsigned char* d = dst + r * row_bytes;
+    for (int64_t c = lane; c < row_bytes; c += 32) d[c] = s[c];
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  // round-to-nearest-even, like __float2bfloat16_rn
+  uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  ua = (ua + 0x7FFFu + ((ua >> 16) & 1u)) >> 16;
+  ub = (ub + 0x7FFFu + ((ub >> 16) & 1u)) >> 16;
+  return ua | (ub << 16);
+}
+
+// fp32 rows of `cols` (cols % 4 == 0) -> bf16 rows.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    gather_f32_bf16_kernel(const float4* __restrict__ src, const int64_t* __restrict__ idx,
+                           int64_t rows, int64_t vec_per_row, uint2* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float4* s = src + __ldg(&idx[r]) * vec_per_row;
+    uint2* d = dst + r * vec_per_row;
+    for (int64_t c = lane; c < vec_per_row; c += 32) {
+      float4 v = __ldcs(s + c);
+      d[c] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    }
+  }
+}
+
+__global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ idx,
+                                  int64_t rows, int32_t* __restrict__ dst) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    dst[r] = src[idx[r]];
+}
+
+int grid_for_rows(int64_t rows) {
+  int64_t blocks = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int64_t cap = (int64_t)num_sms() * 8;  // 8 CTAs x 8 warps = 64 warps per SM
+  return (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+}  // namespace
+}  // namespace dbs
+
+using namespace dbs;
+
+extern "C" int dbs_dev_gather_rows(const void* d_src, const int64_t* d_idx, int64_t rows,
+                                   int64_t row_bytes, void* d_dst, void* stream) {
+  DBS_REQUIRE(rows >= 0 && row_bytes >= 0 && (rows == 0 || (d_src && d_idx && d_dst)),
+              DBS_ERR_ARGUMENT, "dbs_dev_gather_rows: bad arguments");
+  if (rows == 0 || row_bytes == 0) return DBS_OK;
+  cudaStream_t s = as_stream(stream);
+  const int grid = grid_for_rows(rows);
+  const uintptr_t align = (uintptr_t)d_src | (uintptr_t)d_dst;
+  if (row_bytes % 16 == 0 && align % 16 == 0) {
+    gather_rows_kernel<int4><<<grid, kWarpsPerBlock * 32, 0, s>>>(
+        (const int4*)d_src, d_idx, rows, row_bytes / 16, (int4*)d_dst);
+  } else if (row_bytes % 4 == 0 && align % 4 == 0) {
+    gather_rows_kernel<int><<<grid, kWarpsPerBlock * 32, 0, s>>>((const int*)d_src, d_idx, rows,
+                                                                 row_bytes / 4, (int*)d_dst);
+  } else {
+    gather_bytes_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(
+        (const unsigned char*)d_src, d_idx, rows, row_bytes, (unsigned char*)d_dst);
+  }
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_gather_rows_f32_bf16(const float* d_src, const int64_t* d_idx, int64_t rows,
+                                            int64_t cols, void* d_dst, void* stream) {
+  DBS_REQUIRE(rows >= 0 && cols % 4 == 0 && ((uintptr_t)d_src % 16 == 0) &&
+                  ((uintptr_t)d_dst % 8 == 0),
+              DBS_ERR_ARGUMENT, "dbs_dev_gather_rows_f32_bf16: cols must be a multiple of 4, aligned");
+  if (rows == 0 || cols == 0) return DBS_OK;
+  gather_f32_bf16_kernel<<<grid_for_rows(rows), kWarpsPerBlock * 32, 0, as_stream(stream)>>>(
+      (const float4*)d_src, d_idx, rows, cols / 4, (uint2*)d_dst);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_gather_i32(const int32_t* d_src, const int64_t* d_idx, int64_t rows,
+                                  int32_t* d_dst, void* stream) {
+  DBS_REQUIRE(rows >= 0, DBS_ERR_ARGUMENT, "dbs_dev_gather_i32: bad rows");
+  if (rows == 0) return DBS_OK;
+  int grid = (int)((rows + 255) / 256);
+  if (grid > num_sms() * 4) grid = num_sms() * 4;
+  gather_i32_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_src, d_idx, rows, d_dst);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}

@@ -1,0 +1,175 @@
+// sgd.cu -- batch-weighted gradient aggregation + heavy-ball SGD on one device.
+//
+// sgdlab.aggregate_gradients (sgdlab.py:208-227):
+//   batch_weighted: g = sum_i w_i g_i with w = b / sum(b) in fp64,
+//   uniform_average: g = mean_i g_i;
+// sgdlab.sgd_step (sgdlab.py:230-238): v' = momentum * v + g, x' = x - step * v'
+// (no FMA contraction in the fp64 step, so it is bit-identical to numpy's
+// separate multiply/add; the aggregation order is worker 0..n-1).
+//
+// These kernels serve the single-device paths: the drop-in aggregate/step
+// functions, and the per-iteration update when several simulated workers share
+// one GPU.  The multi-GPU fused kernel lives in comm.cu.  Everything is
+// HBM-bound: (n + 4) * P * sizeof(T) bytes per fused launch, 16-byte vectors,
+// grid = a few waves of 148 SMs.
+#include "common.cuh"
+
+namespace dbs {
+namespace {
+
+constexpr int kMaxWorkers = 64;
+
+struct AggArgs {
+  const void* g[kMaxWorkers];
+  double w[kMaxWorkers];
+  int n;
+  int mode;
+};
+
+int make_args(AggArgs& a, const void* const* grads, const int64_t* b, int64_t n, int32_t mode) {
+  DBS_REQUIRE(n >= 1 && n <= kMaxWorkers, DBS_ERR_ARGUMENT, "aggregate: 1..%d workers supported", kMaxWorkers);
+  DBS_REQUIRE(mode == DBS_AGG_UNIFORM || mode == DBS_AGG_BATCH_WEIGHTED, DBS_ERR_CONFIGURATION,
+              "unknown aggregation mode %d", mode);
+  double tot = 0.0;
+  for (int64_t i = 0; i < n; i++) {
+    DBS_REQUIRE(b[i] > 0, DBS_ERR_CONFIGURATION, "batch sizes must be positive");
+    tot += (double)b[i];
+  }
+  a.n = (int)n;
+  a.mode = mode;
+  for (int64_t i = 0; i < n; i++) {
+    a.g[i] = grads[i];
+    a.w[i] = (mode == DBS_AGG_BATCH_WEIGHTED) ? (double)b[i] / tot : 1.0;
+  }
+  return DBS_OK;
+}
+
+__device__ __forceinline__ double agg_f64(const AggArgs& a, int64_t p) {
+  double acc;
+  if (a.mode == DBS_AGG_BATCH_WEIGHTED) {
+    acc = __dmul_rn(a.w[0], ((const double*)a.g[0])[p]);
+    for (int i = 1; i < a.n; i++) acc = __fma_rn(a.w[i], ((const double*)a.g[i])[p], acc);
+  } else {
+    acc = ((const double*)a.g[0])[p];
+    for (int i = 1; i < a.n; i++) acc = __dadd_rn(acc, ((const double*)a.g[i])[p]);
+    acc = __ddiv_rn(acc, (double)a.n);
+  }
+  return acc;
+}
+
+__global__ void aggregate_f64_kernel(AggArgs a, int64_t P, double* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = agg_f64(a, p);
+}
+
+__global__ void sgd_step_f64_kernel(const double* __restrict__ x, const double* __restrict__ g,
+                                    const double* __restrict__ v, int64_t P, double step, double mom,
+                                    double* __restrict__ xo, double* __restrict__ vo) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const double nv = __dadd_rn(__dmul_rn(mom, v[p]), g[p]);
+    xo[p] = __dsub_rn(x[p], __dmul_rn(step, nv));
+    vo[p] = nv;
+  }
+}
+
+__global__ void aggregate_sgd_f64_kernel(AggArgs a, int64_t P, double step, double mom,
+                                         double* __restrict__ x, double* __restrict__ v) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const double g = agg_f64(a, p);
+    const double nv = __dadd_rn(__dmul_rn(mom, v[p]), g);
+    x[p] = __dsub_rn(x[p], __dmul_rn(step, nv));
+    v[p] = nv;
+  }
+}
+
+__device__ __forceinline__ uint32_t bf16_bits(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+
+// fp32 fused aggregate + step, 4 elements per thread (float4).
+__global__ void __launch_bounds__(256) aggregate_sgd_f32_kernel(AggArgs a, int64_t P4, float step, float mom,
+                                                                float4* __restrict__ x, float4* __restrict__ v,
+                                                                uint2* __restrict__ xb) {
+  // weights straight from the parameter bank (no local-memory array)
+#define W(i) ((a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[i] : 1.0f / (float)a.n)
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x) {
+    float4 g = __ldcs(((const float4*)a.g[0]) + p);
+    const float w0 = W(0);
+    g.x *= w0; g.y *= w0; g.z *= w0; g.w *= w0;
+    for (int i = 1; i < a.n; i++) {
+      const float4 h = __ldcs(((const float4*)a.g[i]) + p);
+      const float wi = W(i);
+      g.x = fmaf(wi, h.x, g.x); g.y = fmaf(wi, h.y, g.y);
+      g.z = fmaf(wi, h.z, g.z); g.w = fmaf(wi, h.w, g.w);
+    }
+    float4 vv = v[p], xx = x[p];
+    vv.x = fmaf(mom, vv.x, g.x); vv.y = fmaf(mom, vv.y, g.y);
+    vv.z = fmaf(mom, vv.z, g.z); vv.w = fmaf(mom, vv.w, g.w);
+    xx.x = fmaf(-step, vv.x, xx.x); xx.y = fmaf(-step, vv.y, xx.y);
+    xx.z = fmaf(-step, vv.z, xx.z); xx.w = fmaf(-step, vv.w, xx.w);
+    v[p] = vv;
+    x[p] = xx;
+    if (xb) xb[p] = make_uint2(bf16_bits(xx.x) | (bf16_bits(xx.y) << 16), bf16_bits(xx.z) | (bf16_bits(xx.w) << 16));
+  }
+#undef W
+}
+
+int grid_for(int64_t P, int threads) {
+  int64_t blocks = (P + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
+}
+
+}  // namespace
+}  // namespace dbs
+
+using namespace dbs;
+
+extern "C" int dbs_dev_aggregate_f64(const double* const* d_grads, const int64_t* b, int64_t n,
+                                     int32_t mode, int64_t P, double* d_out, void* stream) {
+  AggArgs a;
+  int st = make_args(a, (const void* const*)d_grads, b, n, mode);
+  if (st) return st;
+  if (P <= 0) return DBS_OK;
+  aggregate_f64_kernel<<<grid_for(P, 256), 256, 0, as_stream(stream)>>>(a, P, d_out);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_sgd_step_f64(const double* d_x, const double* d_g, const double* d_v, int64_t P,
+                                    double step, double mom, double* d_xo, double* d_vo, void* stream) {
+  if (P <= 0) return DBS_OK;
+  sgd_step_f64_kernel<<<grid_for(P, 256), 256, 0, as_stream(stream)>>>(d_x, d_g, d_v, P, step, mom, d_xo, d_vo);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_aggregate_sgd_f64(const double* const* d_grads, const int64_t* b, int64_t n,
+                                         int32_t mode, int64_t P, double step, double mom, double* d_x,
+                                         double* d_v, void* stream) {
+  AggArgs a;
+  int st = make_args(a, (const void* const*)d_grads, b, n, mode);
+  if (st) return st;
+  if (P <= 0) return DBS_OK;
+  aggregate_sgd_f64_kernel<<<grid_for(P, 256), 256, 0, as_stream(stream)>>>(a, P, step, mom, d_x, d_v);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* b, int64_t n,
+                                         int32_t mode, int64_t P, float step, float mom, float* d_x,
+                                         float* d_v, uint16_t* d_x_bf16, void* stream) {
+  AggArgs a;
+  int st = make_args(a, (const void* const*)d_grads, b, n, mode);
+  if (st) return st;
+  DBS_REQUIRE(P % 4 == 0, DBS_ERR_ARGUMENT, "fp32 aggregate: P must be a multiple of 4 (pad the flat buffer)");
+  for (int64_t i = 0; i < n; i++)
+    DBS_REQUIRE(((uintptr_t)d_grads[i] % 16) == 0, DBS_ERR_ARGUMENT, "gradient buffers must be 16-byte aligned");
+  if (P <= 0) return DBS_OK;
+  const int64_t P4 = P / 4;
+  aggregate_sgd_f32_kernel<<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
+      a, P4, step, mom, (float4*)d_x, (float4*)d_v, (uint2*)d_x_bf16);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}

@@ -1,0 +1,114 @@
+// spin.cu -- worker heterogeneity and device-side timing.
+//
+// The reference models a slow worker with DisturbanceEvent (cluster.py:25-56):
+// a multiplicative per-sample cost or flat extra seconds per epoch, applied in
+// effective_cost / epoch_gpu_time (cluster.py:123-145).  On the B200 the
+// disturbance is REAL: a co-running spin kernel that pins whole SMs (one
+// 1024-thread CTA holding ~all shared memory per SM), so the worker's training
+// kernels get only the remaining SMs -- cost_multiplier ~ 1 / (1 - f) for an SM
+// fraction f -- or that burns a fixed number of nanoseconds of device time
+// (extra_epoch_seconds).
+//
+// Per-worker compute time for the controller (cluster.py:259-262 uses the
+// previous epoch's per_worker_gpu) is read from %globaltimer by 1-thread stamp
+// kernels in the worker's stream and accumulated on the device, so the
+// controller never waits for the host.
+#include "common.cuh"
+
+namespace dbs {
+namespace {
+
+constexpr int kSpinThreads = 1024;
+constexpr int kSpinSmem = 200 * 1024;
+constexpr long long kSpinSafetyNs = 600LL * 1000 * 1000 * 1000;  // never spin past 10 minutes
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kSpinThreads, 1) spin_until_kernel(const volatile int32_t* stop) {
+  extern __shared__ float buf[];
+  const long long t0 = globaltimer();
+  float acc = threadIdx.x;
+  for (int it = 0;; it++) {
+    // keep the FMA pipes and the shared-memory port busy
+#pragma unroll 8
+    for (int k = 0; k < 64; k++) acc = fmaf(acc, 1.0000001f, 0.5f);
+    buf[threadIdx.x + (it & 31) * kSpinThreads] = acc;  // 128 KB footprint
+    if ((it & 15) == 0) {
+      if (*stop) break;
+      if (globaltimer() - t0 > kSpinSafetyNs) break;
+    }
+  }
+  if (acc == 12345.0f) buf[0] = acc;  // keep acc live
+}
+
+__global__ void __launch_bounds__(kSpinThreads, 1) spin_for_kernel(long long ns) {
+  extern __shared__ float buf[];
+  const long long t0 = globaltimer();
+  float acc = threadIdx.x;
+  for (int it = 0;; it++) {
+#pragma unroll 8
+    for (int k = 0; k < 64; k++) acc = fmaf(acc, 1.0000001f, 0.5f);
+    buf[(threadIdx.x + it) & 1023] = acc;
+    if ((it & 15) == 0 && globaltimer() - t0 > ns) break;
+  }
+  if (acc == 12345.0f) buf[0] = acc;
+}
+
+__global__ void stamp_kernel(int64_t* stamps, int64_t slot) { stamps[slot] = globaltimer(); }
+
+__global__ void accumulate_kernel(const int64_t* stamps, int64_t b, int64_t e, double* secs, int64_t w) {
+  secs[w] += (double)(stamps[e] - stamps[b]) * 1e-9;
+}
+
+int set_spin_attrs() {
+  static bool done = false;
+  if (!done) {
+    DBS_CUDA_TRY(cudaFuncSetAttribute(spin_until_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpinSmem));
+    DBS_CUDA_TRY(cudaFuncSetAttribute(spin_for_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpinSmem));
+    done = true;
+  }
+  return DBS_OK;
+}
+
+}  // namespace
+}  // namespace dbs
+
+using namespace dbs;
+
+extern "C" int dbs_dev_spin_until(int32_t num_ctas, const volatile int32_t* d_stop, void* stream) {
+  DBS_REQUIRE(num_ctas >= 0 && num_ctas < num_sms() && d_stop, DBS_ERR_ARGUMENT,
+              "spin_until: need 0 <= num_ctas < SM count (%d)", num_sms());
+  if (num_ctas == 0) return DBS_OK;
+  int st = set_spin_attrs();
+  if (st) return st;
+  spin_until_kernel<<<num_ctas, kSpinThreads, kSpinSmem, as_stream(stream)>>>(d_stop);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_spin_for(int32_t num_ctas, int64_t ns, void* stream) {
+  DBS_REQUIRE(num_ctas >= 0 && num_ctas <= num_sms() && ns >= 0, DBS_ERR_ARGUMENT, "spin_for: bad arguments");
+  if (num_ctas == 0 || ns == 0) return DBS_OK;
+  int st = set_spin_attrs();
+  if (st) return st;
+  spin_for_kernel<<<num_ctas, kSpinThreads, kSpinSmem, as_stream(stream)>>>(ns);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_stamp(int64_t* d_stamps, int64_t slot, void* stream) {
+  stamp_kernel<<<1, 1, 0, as_stream(stream)>>>(d_stamps, slot);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, int64_t end, double* d_seconds,
+                                       int64_t worker, void* stream) {
+  accumulate_kernel<<<1, 1, 0, as_stream(stream)>>>(d_stamps, begin, end, d_seconds, worker);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
