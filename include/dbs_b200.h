@@ -259,7 +259,8 @@ enum {
   DBS_EPI_F32_ACCUM = 1,     /* D fp32 += acc                                   */
   DBS_EPI_BIAS_RELU_BF16 = 2,/* D bf16 = relu(acc + bias[n]); aux bf16 = acc+bias */
   DBS_EPI_BIAS_F32 = 3,      /* D fp32 = acc + bias[n]                          */
-  DBS_EPI_BF16 = 4           /* D bf16 = acc                                    */
+  DBS_EPI_BF16 = 4,          /* D bf16 = acc                                    */
+  DBS_EPI_RELU_GRAD_BF16 = 5 /* D bf16 = acc * (aux bf16 [M][ldd] > 0)          */
 };
 int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, const void* d_b,
                       int32_t b_major, int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N,
