@@ -280,6 +280,33 @@ int dbs_mlp_forward_backward(dbs_mlp* m, const uint16_t* d_params_bf16, const fl
                              const uint16_t* d_x_bf16, const int32_t* d_labels, int64_t batch,
                              float* d_grad, float* d_loss, void* stream);
 
+/* One worker of a synchronous iteration (simulated worker on a shared GPU or
+ * one rank's local worker).  Device pointers unless noted. */
+typedef struct {
+  dbs_mlp* model;            /* per-worker activation scratch                      */
+  void* stream;              /* the worker's cudaStream_t (may be a green context) */
+  const uint16_t* x_shard;   /* bf16 [span][in]: this epoch's repacked sample rows */
+  const int32_t* y_shard;    /* int32 [span] labels in the same order              */
+  int64_t batch;             /* b_i of the current plan                            */
+  float* grad;               /* [P] flat gradient of the batch-mean loss           */
+  float* loss;               /* [iters] per-iteration batch loss, or NULL          */
+  float* loss_scratch;       /* [1] used when loss == NULL                         */
+  int64_t* stamps;           /* [2] %globaltimer scratch, NULL = no timing         */
+  double* seconds;           /* device accumulator array of compute seconds        */
+  int64_t worker_index;      /* slot in `seconds`                                  */
+  int64_t spin_ns;           /* disturbance: extra device ns per iteration (0=off) */
+  int32_t spin_ctas;         /* SMs the per-iteration disturbance occupies         */
+  int32_t reserved;
+} dbs_worker_slot;
+
+/* Iterations [t0, t1) of one epoch of run_parallel_sgd's loop (sgdlab.py:380-391)
+ * for the MLP: every worker's forward/backward on its stream, then the fused
+ * aggregate + momentum-SGD update (mode DBS_AGG_*) on agg_stream, ordered with
+ * events; skip_update = 1 measures compute only. */
+int dbs_mlp_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                           float lr, float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                           int32_t skip_update, void* agg_stream);
+
 /* ------------------------------------------------------------------------ */
 /* Worker heterogeneity (cluster.py:25-79 DisturbanceEvent) and timing       */
 /* ------------------------------------------------------------------------ */

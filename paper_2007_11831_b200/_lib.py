@@ -55,6 +55,16 @@ class Pcg64(ctypes.Structure):
                 "has_uint32": int(self.has_uint32), "uinteger": int(self.uinteger)}
 
 
+class WorkerSlot(ctypes.Structure):
+    """dbs_worker_slot (include/dbs_b200.h)."""
+
+    _fields_ = [("model", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("x_shard", ctypes.c_void_p),
+                ("y_shard", ctypes.c_void_p), ("batch", ctypes.c_int64), ("grad", ctypes.c_void_p),
+                ("loss", ctypes.c_void_p), ("loss_scratch", ctypes.c_void_p), ("stamps", ctypes.c_void_p),
+                ("seconds", ctypes.c_void_p), ("worker_index", ctypes.c_int64), ("spin_ns", ctypes.c_int64),
+                ("spin_ctas", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "dbs_last_error": (ctypes.c_char_p, []),
@@ -100,6 +110,8 @@ SIGNATURES = {
     "dbs_mlp_destroy": (c_i32, [c_vp]),
     "dbs_mlp_param_count": (c_i32, [c_vp, P_i64]),
     "dbs_mlp_forward_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "dbs_mlp_run_iterations": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp,
+                                       c_vp, c_vp, c_i32, c_vp]),
     "dbs_dev_spin_until": (c_i32, [c_i32, c_vp, c_vp]),
     "dbs_dev_spin_for": (c_i32, [c_i32, c_i64, c_vp]),
     "dbs_dev_stamp": (c_i32, [c_vp, c_i64, c_vp]),

@@ -42,6 +42,7 @@ struct GemmParams {
   int64_t ldd;
   const float* bias;
   const uint16_t* aux;  // bf16 [M][ldd] for the ReLU-backward epilogue
+  float* colsum_part;   // optional [ceil(M/32)][N] per-warp column sums of the epilogue output
 };
 
 __device__ __forceinline__ uint16_t f2bf(float f) {
@@ -61,7 +62,7 @@ struct Cfg {
 
 template <int BN>
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row, int64_t n_base, const float* v,
-                                               int cnt) {
+                                               int cnt, float* v_out) {
   const int64_t N = p.N;
   const bool full = (n_base + cnt <= N);
   switch (p.epi) {
@@ -107,6 +108,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
           x = (n_base + j < N && bf2f(aux[j]) > 0.0f) ? x : 0.0f;
         }
         o[j] = f2bf(x);
+        v_out[j] = x;
       }
       const bool vec = full && cnt == 32 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0);
       if (vec) {
@@ -218,12 +220,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_32x32b_x32(lane_addr + c * 32, r);
       tmem_ld_wait();
       const int64_t n_base = n0 + c * 32;
-      if (row < p.M && n_base < p.N) {
-        float v[32];
+      if (n_base >= p.N) continue;  // warp-uniform
+      float v[32], vo[32];
 #pragma unroll
-        for (int j = 0; j < 32; j++) v[j] = __uint_as_float(r[j]);
-        const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
-        epilogue_chunk<BN>(p, row, n_base, v, cnt);
+      for (int j = 0; j < 32; j++) {
+        v[j] = __uint_as_float(r[j]);
+        vo[j] = 0.0f;
+      }
+      const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
+      if (row < p.M) epilogue_chunk<BN>(p, row, n_base, v, cnt, vo);
+      if (p.colsum_part != nullptr) {
+        // deterministic per-warp column sums of the stored values (e.g. the bias
+        // gradient sum_b dH): transpose-reduce 32 rows x 32 columns across lanes
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+          float s = vo[j];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          vo[j] = s;
+        }
+        const int64_t g = (m0 >> 5) + warp;
+        if (lane < cnt && m0 + warp * 32 < p.M) p.colsum_part[g * p.N + n_base + lane] = vo[lane];
       }
     }
   } else {
@@ -231,11 +248,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_ld_32x32b_x16(lane_addr, r);
     tmem_ld_wait();
     if (row < p.M && n0 < p.N) {
-      float v[32];
+      float v[32], vo[32];
 #pragma unroll
       for (int j = 0; j < 16; j++) v[j] = __uint_as_float(r[j]);
       const int cnt = (int)((p.N - n0) < 16 ? (p.N - n0) : 16);
-      epilogue_chunk<BN>(p, row, n0, v, cnt);
+      epilogue_chunk<BN>(p, row, n0, v, cnt, vo);
     }
   }
   tc_fence_before();
@@ -299,7 +316,8 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cu
 
 // Entry used by the MLP driver too.
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
-              int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s) {
+              int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
+              float* colsum_part) {
   DBS_REQUIRE(M > 0 && N > 0 && K > 0 && a && b && d, DBS_ERR_ARGUMENT, "gemm: bad shape/pointers");
   DBS_REQUIRE(epi >= DBS_EPI_F32 && epi <= DBS_EPI_RELU_GRAD_BF16, DBS_ERR_ARGUMENT, "gemm: bad epilogue %d", epi);
   DBS_REQUIRE(!((epi == DBS_EPI_BIAS_RELU_BF16 || epi == DBS_EPI_BIAS_F32) && !bias), DBS_ERR_ARGUMENT,
@@ -320,7 +338,8 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
   st = b_mn ? make_tmap(&tb, b, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 64, 64)
             : make_tmap(&tb, b, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, 64, (uint32_t)bn);
   if (st) return st;
-  GemmParams p{M, N, K, a_mn, b_mn, epi, d, ldd, bias, reinterpret_cast<const uint16_t*>(aux)};
+  DBS_REQUIRE(!(colsum_part && bn < 32), DBS_ERR_ARGUMENT, "gemm: column sums need N > 16");
+  GemmParams p{M, N, K, a_mn, b_mn, epi, d, ldd, bias, reinterpret_cast<const uint16_t*>(aux), colsum_part};
   switch (bn) {
     case 16: return launch<16>(ta, tb, p, s);
     case 64: return launch<64>(ta, tb, p, s);
@@ -335,5 +354,5 @@ extern "C" int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, 
                                  int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N, int64_t K,
                                  int32_t epilogue, const float* d_bias, void* d_aux, void* stream) {
   return dbs::gemm_bf16(d_a, a_major, lda, d_b, b_major, ldb, d_d, ldd, M, N, K, epilogue, d_bias, d_aux,
-                        dbs::as_stream(stream));
+                        dbs::as_stream(stream), nullptr);
 }

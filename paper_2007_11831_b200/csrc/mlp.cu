@@ -1,0 +1,288 @@
+// mlp.cu -- variable-batch forward/backward of the 784-H-C MLP on tcgen05, and
+// the native per-epoch iteration driver of synchronous DBS S-SGD.
+//
+// Reference loop being accelerated: sgdlab.run_parallel_sgd (sgdlab.py:380-391):
+//   for t in iterations: for each worker, mean gradient on batch t of its
+//   permuted span -> aggregate_gradients(batch_weighted) -> sgd_step.
+// Per worker and iteration (7 launches, all on the worker's stream):
+//   1. H   = relu(X W1^T + b1)        tcgen05 GEMM, fused bias+ReLU, bf16 out
+//   2. Z   = H W2^T + b2              tcgen05 GEMM (N = C <= 16), fp32 logits
+//   3. softmax cross-entropy          dZ = (softmax - onehot) / b, db2, loss
+//   4. dW2 = dZ^T H                   tcgen05 GEMM, both operands MN-major
+//   5. dH  = (dZ W2) * [H > 0]        tcgen05 GEMM, fused ReLU-backward, + per-warp
+//                                     column sums for db1 (deterministic)
+//   6. db1 = sum of the column-sum partials
+//   7. dW1 = dH^T X                   tcgen05 GEMM, both operands MN-major
+// The flat fp32 gradient [W1 | b1 | W2 | b2] (each block padded to 8 elements)
+// is then combined across workers by the fused aggregate+SGD kernel, which also
+// refreshes the bf16 parameter shadow the GEMMs read.
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dbs {
+int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
+              int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
+              float* colsum_part);
+int stamp(int64_t* d_stamps, int64_t slot, cudaStream_t s);
+}  // namespace dbs
+
+struct dbs_mlp {
+  int64_t in, hid, cls, max_b;
+  int64_t off_w1, off_b1, off_w2, off_b2, P;
+  uint16_t* act = nullptr;      // [max_b][hid]
+  float* logits = nullptr;      // [max_b][16]
+  uint16_t* dz = nullptr;       // [max_b][16]
+  uint16_t* dh = nullptr;       // [max_b][hid]
+  float* colsum = nullptr;      // [ceil(max_b/32)][hid]
+};
+
+namespace dbs {
+namespace {
+
+constexpr int64_t kLdZ = 16;
+
+int64_t pad8(int64_t x) { return (x + 7) & ~int64_t(7); }
+
+__device__ __forceinline__ uint16_t f2bf(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+// One CTA: mean cross-entropy over b rows, dZ = (softmax - onehot)/b (bf16),
+// db2 = sum_rows dZ (fp32, deterministic block reduction), loss.
+__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ z, const int32_t* __restrict__ y,
+                                                         int64_t b, int cls, uint16_t* __restrict__ dz,
+                                                         float* __restrict__ db2, float* __restrict__ loss) {
+  __shared__ float red[8][17];
+  float acc[16];
+  float lsum = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 16; c++) acc[c] = 0.0f;
+  const float inv_b = 1.0f / (float)b;
+  for (int64_t r = threadIdx.x; r < b; r += blockDim.x) {
+    const float* zr = z + r * kLdZ;
+    float mx = -INFINITY;
+    for (int c = 0; c < cls; c++) mx = fmaxf(mx, zr[c]);
+    float se = 0.0f;
+    float e[16];
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      e[c] = (c < cls) ? __expf(zr[c] - mx) : 0.0f;
+      se += e[c];
+    }
+    const int yr = y[r];
+    lsum += (mx + __logf(se)) - zr[yr];
+    const float inv = 1.0f / se;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      float g = (c < cls) ? (e[c] * inv - (c == yr ? 1.0f : 0.0f)) * inv_b : 0.0f;
+      acc[c] += g;
+      dz[r * kLdZ + c] = f2bf(g);
+    }
+  }
+  // block reduction of acc[0..cls) and lsum
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    float s = acc[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp][c] = s;
+  }
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if (lane == 0) red[warp][16] = lsum;
+  __syncthreads();
+  if (threadIdx.x < 17) {
+    float s = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w][threadIdx.x];
+    if (threadIdx.x < cls) db2[threadIdx.x] = s;
+    if (threadIdx.x == 16) *loss = s * inv_b;
+  }
+}
+
+// db1[n] = sum_g part[g][n] over g < groups (fixed order => deterministic)
+__global__ void colsum_reduce_kernel(const float* __restrict__ part, int64_t groups, int64_t n,
+                                     float* __restrict__ out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int64_t g = 0; g < groups; g++) s += part[g * n + j];
+    out[j] = s;
+  }
+}
+
+}  // namespace
+
+int mlp_fwd_bwd(dbs_mlp* m, const uint16_t* pb, const float* pf, const uint16_t* x, const int32_t* y, int64_t b,
+                float* grad, float* loss, cudaStream_t s) {
+  DBS_REQUIRE(m && pb && pf && x && y && grad && loss, DBS_ERR_ARGUMENT, "mlp: null argument");
+  DBS_REQUIRE(b >= 1 && b <= m->max_b, DBS_ERR_ARGUMENT, "mlp: batch %lld outside [1, %lld]", (long long)b,
+              (long long)m->max_b);
+  int st;
+  const int64_t I = m->in, H = m->hid, C = m->cls;
+  // 1. forward layer 1
+  st = gemm_bf16(x, 0, I, pb + m->off_w1, 0, I, m->act, H, b, H, I, DBS_EPI_BIAS_RELU_BF16, pf + m->off_b1,
+                 nullptr, s, nullptr);
+  if (st) return st;
+  // 2. logits
+  st = gemm_bf16(m->act, 0, H, pb + m->off_w2, 0, H, m->logits, kLdZ, b, C, H, DBS_EPI_BIAS_F32, pf + m->off_b2,
+                 nullptr, s, nullptr);
+  if (st) return st;
+  // 3. softmax cross-entropy + db2
+  softmax_ce_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, m->dz, grad + m->off_b2, loss);
+  DBS_LAUNCH_CHECK();
+  // 4. dW2 = dZ^T H
+  st = gemm_bf16(m->dz, 1, kLdZ, m->act, 1, H, grad + m->off_w2, H, C, H, b, DBS_EPI_F32, nullptr, nullptr, s,
+                 nullptr);
+  if (st) return st;
+  // 5. dH = (dZ W2) * [H > 0], with db1 partial column sums
+  st = gemm_bf16(m->dz, 0, kLdZ, pb + m->off_w2, 1, H, m->dh, H, b, H, C, DBS_EPI_RELU_GRAD_BF16, nullptr, m->act,
+                 s, m->colsum);
+  if (st) return st;
+  // 6. db1
+  {
+    int grid = (int)((H + 255) / 256);
+    colsum_reduce_kernel<<<grid, 256, 0, s>>>(m->colsum, (b + 31) / 32, H, grad + m->off_b1);
+    DBS_LAUNCH_CHECK();
+  }
+  // 7. dW1 = dH^T X
+  st = gemm_bf16(m->dh, 1, H, x, 1, I, grad + m->off_w1, I, H, I, b, DBS_EPI_F32, nullptr, nullptr, s, nullptr);
+  return st;
+}
+
+}  // namespace dbs
+
+using namespace dbs;
+
+extern "C" int dbs_mlp_create(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch, dbs_mlp** out) {
+  DBS_REQUIRE(out && in_dim > 0 && hidden > 16 && classes >= 2 && classes <= 16 && max_batch > 0, DBS_ERR_ARGUMENT,
+              "mlp_create: need in>0, hidden>16, 2<=classes<=16");
+  DBS_REQUIRE(in_dim % 8 == 0 && hidden % 8 == 0, DBS_ERR_ARGUMENT, "mlp_create: in/hidden must be multiples of 8");
+  dbs_mlp* m = new dbs_mlp();
+  m->in = in_dim;
+  m->hid = hidden;
+  m->cls = classes;
+  m->max_b = max_batch;
+  m->off_w1 = 0;
+  m->off_b1 = pad8(hidden * in_dim);
+  m->off_w2 = m->off_b1 + pad8(hidden);
+  m->off_b2 = m->off_w2 + pad8(classes * hidden);
+  m->P = m->off_b2 + pad8(classes);
+  const int64_t groups = (max_batch + 31) / 32 + 4;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMalloc(&m->act, sizeof(uint16_t) * max_batch * hidden);
+  e = e ? e : cudaMalloc(&m->logits, sizeof(float) * max_batch * kLdZ);
+  e = e ? e : cudaMalloc(&m->dz, sizeof(uint16_t) * max_batch * kLdZ);
+  e = e ? e : cudaMalloc(&m->dh, sizeof(uint16_t) * max_batch * hidden);
+  e = e ? e : cudaMalloc(&m->colsum, sizeof(float) * groups * hidden);
+  if (e != cudaSuccess) {
+    set_error("mlp_create: %s", cudaGetErrorString(e));
+    dbs_mlp_destroy(m);
+    return DBS_ERR_CUDA;
+  }
+  *out = m;
+  return DBS_OK;
+}
+
+extern "C" int dbs_mlp_destroy(dbs_mlp* m) {
+  if (!m) return DBS_OK;
+  cudaFree(m->act);
+  cudaFree(m->logits);
+  cudaFree(m->dz);
+  cudaFree(m->dh);
+  cudaFree(m->colsum);
+  delete m;
+  return DBS_OK;
+}
+
+extern "C" int dbs_mlp_param_count(const dbs_mlp* m, int64_t* out) {
+  DBS_REQUIRE(m && out, DBS_ERR_ARGUMENT, "mlp_param_count: null");
+  *out = m->P;
+  return DBS_OK;
+}
+
+extern "C" int dbs_mlp_forward_backward(dbs_mlp* m, const uint16_t* d_params_bf16, const float* d_params,
+                                        const uint16_t* d_x_bf16, const int32_t* d_labels, int64_t batch,
+                                        float* d_grad, float* d_loss, void* stream) {
+  return mlp_fwd_bwd(m, d_params_bf16, d_params, d_x_bf16, d_labels, batch, d_grad, d_loss, as_stream(stream));
+}
+
+// ---------------------------------------------------------------------------
+// Native iteration driver: iterations [t0, t1) of one epoch for n workers.
+// Each worker runs on its own stream (optionally an SM-partitioned green
+// context); the aggregation + SGD kernel joins them on agg_stream.  Per-worker
+// compute time is accumulated on the device from %globaltimer stamps.
+// ---------------------------------------------------------------------------
+namespace {
+std::vector<cudaEvent_t> g_events;
+std::mutex g_ev_mu;
+int events(int n, cudaEvent_t** out) {
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  while ((int)g_events.size() < n) {
+    cudaEvent_t e;
+    DBS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g_events.push_back(e);
+  }
+  *out = g_events.data();
+  return DBS_OK;
+}
+}  // namespace
+
+extern "C" int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode,
+                                         int64_t P, float step, float mom, float* d_x, float* d_v, uint16_t* d_x_bf16,
+                                         void* stream);
+extern "C" int dbs_dev_spin_for(int32_t num_ctas, int64_t ns, void* stream);
+extern "C" int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, int64_t end, double* d_seconds,
+                                       int64_t worker, void* stream);
+
+extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                      float lr, float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                                      int32_t skip_update, void* agg_stream) {
+  DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "mlp_run_iterations: bad arguments");
+  cudaEvent_t* ev;
+  int st = events(n + 1, &ev);
+  if (st) return st;
+  cudaStream_t agg = as_stream(agg_stream);
+  const float* grads[64];
+  int64_t batches[64];
+  for (int i = 0; i < n; i++) {
+    grads[i] = w[i].grad;
+    batches[i] = w[i].batch;
+  }
+  const int64_t P = w[0].model->P;
+  DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
+  for (int64_t t = t0; t < t1; t++) {
+    for (int i = 0; i < n; i++) {
+      cudaStream_t s = as_stream(w[i].stream);
+      DBS_CUDA_TRY(cudaStreamWaitEvent(s, ev[n], 0));  // parameters of iteration t ready
+      if (w[i].stamps) {
+        st = stamp(w[i].stamps, 0, s);
+        if (st) return st;
+      }
+      if (w[i].spin_ns > 0 && w[i].spin_ctas > 0) {  // extra_epoch_seconds disturbance
+        st = dbs_dev_spin_for(w[i].spin_ctas, w[i].spin_ns, s);
+        if (st) return st;
+      }
+      const dbs_mlp* m = w[i].model;
+      const int64_t b = w[i].batch;
+      st = mlp_fwd_bwd(w[i].model, d_params_bf16, d_params, w[i].x_shard + t * b * m->in, w[i].y_shard + t * b, b,
+                       w[i].grad, w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
+      if (st) return st;
+      if (w[i].stamps) {
+        st = stamp(w[i].stamps, 1, s);
+        if (st) return st;
+        st = dbs_dev_accumulate_time(w[i].stamps, 0, 1, w[i].seconds, w[i].worker_index, s);
+        if (st) return st;
+      }
+      DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
+    }
+    for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
+    if (!skip_update) {
+      st = dbs_dev_aggregate_sgd_f32(grads, batches, n, mode, P, lr, mom, d_params, d_velocity, d_params_bf16,
+                                     agg_stream);
+      if (st) return st;
+    }
+    DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
+  }
+  return DBS_OK;
+}

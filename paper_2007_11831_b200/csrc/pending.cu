@@ -12,9 +12,4 @@ int dbs_comm_buffers(dbs_comm*, float**, float**, uint16_t**) { PENDING(dbs_comm
 int dbs_comm_destroy(dbs_comm*) { PENDING(dbs_comm_destroy); }
 int dbs_comm_allreduce_sgd(dbs_comm*, const int64_t*, int32_t, float, float, float*, void*) { PENDING(x); }
 int dbs_comm_average_params(dbs_comm*, const int64_t*, int32_t, void*) { PENDING(x); }
-int dbs_mlp_create(int64_t, int64_t, int64_t, int64_t, dbs_mlp**) { PENDING(mlp); }
-int dbs_mlp_destroy(dbs_mlp*) { PENDING(mlp); }
-int dbs_mlp_param_count(const dbs_mlp*, int64_t*) { PENDING(mlp); }
-int dbs_mlp_forward_backward(dbs_mlp*, const uint16_t*, const float*, const uint16_t*, const int32_t*, int64_t,
-                             float*, float*, void*) { PENDING(mlp); }
 }

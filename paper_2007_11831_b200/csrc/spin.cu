@@ -75,6 +75,13 @@ int set_spin_attrs() {
 }
 
 }  // namespace
+
+int stamp(int64_t* d_stamps, int64_t slot, cudaStream_t s) {
+  stamp_kernel<<<1, 1, 0, s>>>(d_stamps, slot);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
 }  // namespace dbs
 
 using namespace dbs;
