@@ -320,6 +320,9 @@ int dbs_dev_spin_for(int32_t num_ctas, int64_t nanoseconds, void* stream);
 int dbs_dev_stamp(int64_t* d_stamps, int64_t slot, void* stream);
 /* d_seconds[w] += (d_stamps[end] - d_stamps[begin]) * 1e-9 : per-worker
  * compute time accumulated on the device for the controller. */
+/* *d_flag = value (0/1) with a memset on `stream`: stops dbs_dev_spin_until
+ * without launching a kernel while the spin owns SMs. */
+int dbs_dev_set_flag(int32_t* d_flag, int32_t value, void* stream);
 int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, int64_t end,
                             double* d_seconds, int64_t worker, void* stream);
 

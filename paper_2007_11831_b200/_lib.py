@@ -115,6 +115,7 @@ SIGNATURES = {
     "dbs_dev_spin_until": (c_i32, [c_i32, c_vp, c_vp]),
     "dbs_dev_spin_for": (c_i32, [c_i32, c_i64, c_vp]),
     "dbs_dev_stamp": (c_i32, [c_vp, c_i64, c_vp]),
+    "dbs_dev_set_flag": (c_i32, [c_vp, c_i32, c_vp]),
     "dbs_dev_accumulate_time": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
 }
 

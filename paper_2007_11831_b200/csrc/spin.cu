@@ -119,3 +119,18 @@ extern "C" int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, i
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
+
+// Set a device int32 flag with a copy-engine transfer from pinned host memory:
+// no kernel (not even the driver's memset kernels) is involved, so it is safe
+// to issue while a spin kernel owns SMs and a lazily loaded module could stall.
+extern "C" int dbs_dev_set_flag(int32_t* d_flag, int32_t value, void* stream) {
+  DBS_REQUIRE(d_flag && (value == 0 || value == 1), DBS_ERR_ARGUMENT, "set_flag: value must be 0 or 1");
+  static int32_t* host_vals = nullptr;
+  if (host_vals == nullptr) {
+    DBS_CUDA_TRY(cudaMallocHost(&host_vals, 2 * sizeof(int32_t)));
+    host_vals[0] = 0;
+    host_vals[1] = 1;
+  }
+  DBS_CUDA_TRY(cudaMemcpyAsync(d_flag, host_vals + value, sizeof(int32_t), cudaMemcpyHostToDevice, as_stream(stream)));
+  return DBS_OK;
+}

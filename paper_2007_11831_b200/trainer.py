@@ -128,6 +128,35 @@ class SimulatedTrainer:
             self.scratch[w] = cur
         return cur
 
+    def _prime(self, slots, iters: int, mode: int):
+        """Run one throw-away iteration (scratch parameters) before a spin kernel
+        starts, so every kernel of the epoch is resident: a lazily loaded module
+        must never be needed while a spinning kernel owns SMs."""
+        if getattr(self, "_primed", False) or iters <= 0:
+            return
+        torch = self.torch
+        p = self.model.params.clone()
+        v = torch.zeros_like(p)
+        pb = self.model.params_bf16.clone()
+        cur = torch.cuda.current_stream()
+        self.agg.wait_stream(cur)
+        for wk in self.workers:
+            wk.stream.wait_stream(cur)
+        saved = [(slots[w].loss, slots[w].stamps, slots[w].seconds) for w in range(self.n)]
+        st_scratch = torch.zeros(2 * self.n, dtype=torch.int64, device=self.dev)
+        sec_scratch = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
+        for w in range(self.n):
+            # same kernel set as a real iteration (incl. the timing stamps), scratch outputs
+            slots[w].loss = None
+            slots[w].stamps = st_scratch[2 * w:].data_ptr()
+            slots[w].seconds = sec_scratch.data_ptr()
+        _lib.check(_lib.lib().dbs_mlp_run_iterations(slots, self.n, 0, 1, mode, 0.0, 0.0, p.data_ptr(), v.data_ptr(),
+                                                      pb.data_ptr(), 0, int(self.agg.cuda_stream)), "prime")
+        for w in range(self.n):
+            slots[w].loss, slots[w].stamps, slots[w].seconds = saved[w]
+        torch.cuda.synchronize()
+        self._primed = True
+
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
@@ -185,10 +214,11 @@ class SimulatedTrainer:
                 sl.worker_index = w
                 sl.spin_ns, sl.spin_ctas = 0, 0
             self.seconds.zero_()
-            self.stop.zero_()
+            _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 0, s_main), "set_flag")
             # disturbances of this epoch
             spinning = []
-            if profiles is not None:
+            if profiles is not None and any(p.active_disturbance(epoch) for p in profiles):
+                self._prime(slots, iters, mode)
                 for w, prof in enumerate(profiles):
                     ev = prof.active_disturbance(epoch)
                     if ev is None:
@@ -219,9 +249,8 @@ class SimulatedTrainer:
                     int(self.agg.cuda_stream))
                 _lib.check(st, "mlp_run_iterations")
             end.record(self.agg)
-            # stop the disturbance once the epoch's work is done
-            with torch.cuda.stream(self.agg):
-                self.stop.fill_(1)
+            # stop the disturbance once the epoch's work is done (memset: no kernel launch)
+            _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 1, int(self.agg.cuda_stream)), "set_flag")
             for wk in spinning:
                 self.agg.wait_stream(wk.spin_stream)
             cur.wait_stream(self.agg)
