@@ -73,6 +73,32 @@ class ClockSampler:
         self._t = None
 
     def start(self):
+        try:  # in-process NVML: no nvidia-smi processes contending for the driver
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+
+            def run_nvml():
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append([str(sm), str(mx), "0"] +
+                                            ["Active" if r & b else "Not Active" for b in bits])
+                    except Exception:
+                        pass
+                    self._stop.wait(0.25)
+
+            self._t = threading.Thread(target=run_nvml, daemon=True)
+            self._t.start()
+            return
+        except Exception:
+            pass
+
         def run():
             q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -176,12 +202,24 @@ def kernel_roofline(tr, peaks):
 
     for _ in range(20):
         launch()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record(s)
-    for _ in range(200):
-        launch()
-    e1.record(s)
+    # 200 back-to-back launches captured in a CUDA graph, so the events time the
+    # kernels on the device, not the host launch rate
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.stream(cs):
+        g.capture_begin()
+        s = torch.cuda.current_stream()
+        for _ in range(200):
+            launch()
+        g.capture_end()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
+    g.replay()
+    e1.record(cs)
     torch.cuda.synchronize()
     dur = e0.elapsed_time(e1) / 1e3 / 200
     flops = 2.0 * b * HIDDEN * IN_DIM

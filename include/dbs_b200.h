@@ -206,7 +206,14 @@ int dbs_comm_handle_size(void);
 int dbs_comm_alloc(int32_t rank, int32_t world, int64_t P, dbs_comm** out, void* handle_out);
 int dbs_comm_open(dbs_comm* comm, const void* all_handles /* world * handle_size */);
 int dbs_comm_buffers(dbs_comm* comm, float** d_grad, float** d_param, uint16_t** d_param_bf16);
+/* padded parameter count (multiple of 4 * world) and the per-rank shard length */
+int dbs_comm_info(const dbs_comm* comm, int64_t* padded_P, int64_t* shard);
+/* unmap the IPC-opened peer blocks (before dbs_comm_destroy) */
+int dbs_comm_close_peers(dbs_comm* comm);
 int dbs_comm_destroy(dbs_comm* comm);
+/* single-process form: `world` communicators over plain local blocks of the
+ * current device (simulated ranks; used by the tests on one GPU) */
+int dbs_comm_create_local(int32_t world, int64_t P, dbs_comm** comms_out);
 /* The fused per-iteration kernel: each rank owns shard [r*P/W, (r+1)*P/W);
  * it loads the shard of every peer's gradient over NVLink, forms
  * sum_j w_j g_j (w_j = b_j / sum b), applies v' = mom v + g, x' = x - lr v',

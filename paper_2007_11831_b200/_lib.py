@@ -97,6 +97,9 @@ SIGNATURES = {
     "dbs_comm_open": (c_i32, [c_vp, c_vp]),
     "dbs_comm_buffers": (c_i32, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     "dbs_comm_destroy": (c_i32, [c_vp]),
+    "dbs_comm_info": (c_i32, [c_vp, P_i64, P_i64]),
+    "dbs_comm_close_peers": (c_i32, [c_vp]),
+    "dbs_comm_create_local": (c_i32, [c_i32, c_i64, ctypes.POINTER(c_vp)]),
     "dbs_comm_allreduce_sgd": (c_i32, [c_vp, P_i64, c_i32, c_flt, c_flt, c_vp, c_vp]),
     "dbs_comm_average_params": (c_i32, [c_vp, P_i64, c_i32, c_vp]),
     "dbs_dev_quadratic_grads": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
