@@ -267,7 +267,9 @@ enum {
   DBS_EPI_BIAS_RELU_BF16 = 2,/* D bf16 = relu(acc + bias[n]); aux bf16 = acc+bias */
   DBS_EPI_BIAS_F32 = 3,      /* D fp32 = acc + bias[n]                          */
   DBS_EPI_BF16 = 4,          /* D bf16 = acc                                    */
-  DBS_EPI_RELU_GRAD_BF16 = 5 /* D bf16 = acc * (aux bf16 [M][ldd] > 0)          */
+  DBS_EPI_RELU_GRAD_BF16 = 5,/* D bf16 = acc * (aux bf16 [M][ldd] > 0)          */
+  DBS_EPI_F32_ATOMIC = 6,    /* D fp32 += acc with atomics (split-K reduction)  */
+  DBS_EPI_BF16_ACCUM = 7     /* D bf16 = D + acc (gradient accumulation)        */
 };
 int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, const void* d_b,
                       int32_t b_major, int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N,
@@ -287,12 +289,44 @@ int dbs_mlp_forward_backward(dbs_mlp* m, const uint16_t* d_params_bf16, const fl
                              const uint16_t* d_x_bf16, const int32_t* d_labels, int64_t batch,
                              float* d_grad, float* d_loss, void* stream);
 
+/* ResNet-18, CIFAR variant (3x3 stem, no max-pool; 11,173,962 weights): one
+ * variable-batch forward + backward of a worker's batch on the implicit-GEMM
+ * tcgen05 convolution.  Input fp32 [B][3][32][32] rows of the repacked shard
+ * (iteration t reads rows t*B.., t = *d_iter or 0), labels int32; the flat fp32
+ * gradient (layout from dbs_resnet_param_table) and the batch-mean loss
+ * (d_loss[t]) are written.  Local (per-worker) BatchNorm statistics. */
+typedef struct dbs_resnet dbs_resnet;
+int dbs_resnet_create(int64_t max_batch, int32_t classes, dbs_resnet** out);
+int dbs_resnet_destroy(dbs_resnet* m);
+int dbs_resnet_param_count(const dbs_resnet* m, int64_t* P);
+/* torchvision parameter order; kind 0 conv weight [Cout][R][S][Cin] (stem
+ * [64][32], 27 used), 1 BN gamma, 2 BN beta, 3 FC weight [C][512], 4 FC bias */
+int dbs_resnet_param_table(const dbs_resnet* m, int64_t* off, int64_t* len, int32_t* kind, int32_t capacity,
+                           int32_t* count);
+int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, const float* d_params,
+                                const float* d_x, const int32_t* d_labels, int64_t batch, const int64_t* d_iter,
+                                float* d_grad, float* d_loss, void* stream);
+
+/* Implicit-GEMM convolutions (NHWC bf16, weights [Cout][k][k][Cin] bf16) on the
+ * tcgen05 GEMM with 4-D TMA operand loads: y = conv(x, w); dx = dgrad(dy, w)
+ * (scratch >= 2*(Cout*k*k*Cin + 64) + 8*N*H*W*Cout bytes); dw += wgrad(dy, x)
+ * (fp32, atomically accumulated -- zero it first). */
+int dbs_dev_conv2d_fwd(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w, int32_t Cout,
+                       int32_t k, int32_t stride, int32_t pad, void* d_y, void* stream);
+int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
+                         int32_t Cout, int32_t k, int32_t stride, int32_t pad, void* d_dx, void* d_scratch,
+                         void* stream);
+int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                         int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw, void* stream);
+
 /* One worker of a synchronous iteration (simulated worker on a shared GPU or
  * one rank's local worker).  Device pointers unless noted. */
+enum { DBS_MODEL_MLP = 0, DBS_MODEL_RESNET18 = 1 };
 typedef struct {
-  dbs_mlp* model;            /* per-worker activation scratch                      */
+  void* model;               /* dbs_mlp* or dbs_resnet* (per-worker scratch)       */
   void* stream;              /* the worker's cudaStream_t (may be a green context) */
-  const uint16_t* x_shard;   /* bf16 [span][in]: this epoch's repacked sample rows */
+  const void* x_shard;       /* this epoch's repacked sample rows (MLP: bf16 [span][in];
+                                ResNet: fp32 [span][3][32][32])                    */
   const int32_t* y_shard;    /* int32 [span] labels in the same order              */
   int64_t batch;             /* b_i of the current plan                            */
   float* grad;               /* [P] flat gradient of the batch-mean loss           */
@@ -303,13 +337,18 @@ typedef struct {
   int64_t worker_index;      /* slot in `seconds`                                  */
   int64_t spin_ns;           /* disturbance: extra device ns per iteration (0=off) */
   int32_t spin_ctas;         /* SMs the per-iteration disturbance occupies         */
-  int32_t reserved;
+  int32_t model_kind;        /* DBS_MODEL_*                                        */
 } dbs_worker_slot;
 
-/* Iterations [t0, t1) of one epoch of run_parallel_sgd's loop (sgdlab.py:380-391)
- * for the MLP: every worker's forward/backward on its stream, then the fused
- * aggregate + momentum-SGD update (mode DBS_AGG_*) on agg_stream, ordered with
- * events; skip_update = 1 measures compute only. */
+/* Iterations [t0, t1) of one epoch of run_parallel_sgd's loop (sgdlab.py:380-391):
+ * every worker's forward/backward on its stream, then the fused aggregate +
+ * momentum-SGD update (mode DBS_AGG_*) on agg_stream, ordered with events;
+ * skip_update = 1 measures compute only.  With d_iter != NULL (ResNet only) the
+ * kernels read the iteration index from *d_iter and the update increments it,
+ * so every iteration is the same launch sequence (CUDA-graph capturable). */
+int dbs_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                       float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                       int32_t skip_update, void* agg_stream, int64_t* d_iter);
 int dbs_mlp_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                            float lr, float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
                            int32_t skip_update, void* agg_stream);

@@ -62,7 +62,7 @@ class WorkerSlot(ctypes.Structure):
                 ("y_shard", ctypes.c_void_p), ("batch", ctypes.c_int64), ("grad", ctypes.c_void_p),
                 ("loss", ctypes.c_void_p), ("loss_scratch", ctypes.c_void_p), ("stamps", ctypes.c_void_p),
                 ("seconds", ctypes.c_void_p), ("worker_index", ctypes.c_int64), ("spin_ns", ctypes.c_int64),
-                ("spin_ctas", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("spin_ctas", ctypes.c_int32), ("model_kind", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes)
@@ -115,6 +115,17 @@ SIGNATURES = {
     "dbs_mlp_forward_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "dbs_mlp_run_iterations": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp,
                                        c_vp, c_vp, c_i32, c_vp]),
+    "dbs_run_iterations": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp, c_vp,
+                                   c_vp, c_i32, c_vp, c_vp]),
+    "dbs_resnet_create": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_resnet_destroy": (c_i32, [c_vp]),
+    "dbs_resnet_param_count": (c_i32, [c_vp, P_i64]),
+    "dbs_resnet_param_table": (c_i32, [c_vp, P_i64, P_i64, P_i32, c_i32, P_i32]),
+    "dbs_resnet_forward_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "dbs_dev_conv2d_fwd": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "dbs_dev_conv2d_dgrad": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp,
+                                     c_vp]),
+    "dbs_dev_conv2d_wgrad": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "dbs_dev_spin_until": (c_i32, [c_i32, c_vp, c_vp]),
     "dbs_dev_spin_for": (c_i32, [c_i32, c_i64, c_vp]),
     "dbs_dev_stamp": (c_i32, [c_vp, c_i64, c_vp]),

@@ -1,28 +1,38 @@
-// gemm.cu -- tcgen05 tensor-core GEMM for the variable-batch forward/backward.
+// gemm.cu -- tcgen05 tensor-core GEMM / implicit-GEMM convolution.
 //
 //   D[M, N] (+)= A[M, K] * B[N, K]^T      bf16 operands, fp32 accumulation in TMEM
 //
-// Either operand may be K-major (row-major over K) or MN-major (the transpose
-// stored row-major), so the forward (X W^T), the input gradient (dY W) and the
-// weight gradient (dY^T X) all read the activations in place -- no transposes.
+// Operand modes (TMA, 128-byte swizzle):
+//   0 K-major   : row-major over K                       (X W^T, conv weights)
+//   1 MN-major  : the transpose stored row-major         (dY^T X, dZ W, ...)
+//   2 conv      : a 4-D NHWC activation read as an implicit im2col matrix --
+//                 A: rows = 128 output pixels, K = (r, s, c) with c fastest, one
+//                    TMA box per K block at the (r, s)-shifted, strided input
+//                    window (zero padding = TMA out-of-bounds fill);
+//                 B: (weight gradient) rows = K = 64 output pixels, N = (r, s, c),
+//                    MN-major boxes of 64 channels.
+// so the variable-batch forward (conv / X W^T), the input gradient (conv of dY
+// with the flipped filter / dZ W) and the weight gradient (dY^T im2col(X))
+// all read activations in place -- no im2col buffers, no transposes.
 //
 // Structure (one 128 x BN output tile per CTA, 4 warps):
-//   warp 0 / lane 0 : TMA producer -- 128B-swizzled boxes into a STAGES-deep
-//                     shared-memory ring, mbarrier expect_tx per stage;
-//   warp 1 / lane 0 : MMA issuer  -- 4 x tcgen05.mma (UMMA_K = 16) per 64-wide
-//                     K block, tcgen05.commit frees the ring slot;
+//   warp 0 / lane 0 : TMA producer into a STAGES-deep shared-memory ring;
+//   warp 1 / lane 0 : MMA issuer (4 x tcgen05.mma, UMMA_K = 16, per 64-wide K
+//                     block; tcgen05.commit frees the ring slot);
 //   warp 2          : TMEM allocator (BN fp32 columns);
-//   all 4 warps     : epilogue -- tcgen05.ld 32x32b (thread = output row),
-//                     fused bias / ReLU / ReLU-backward / bf16 cast, stores.
-// Variable batch: M (the per-rank batch b_i) is a runtime value; rows past M
-// are zero-filled by TMA (OOB fill) and masked in the epilogue, so a batch size
-// that changes every epoch needs no recompilation and no padding copies.
+//   all 4 warps     : epilogue -- tcgen05.ld 32x32b (thread = output row), fused
+//                     bias / ReLU / ReLU-backward / bf16 cast / accumulate /
+//                     split-K atomic reduction, and per-warp column partial sums
+//                     (bias gradients, BatchNorm batch statistics).
+// Variable batch: M (the per-rank batch b_i, or b_i x H x W pixels) is a runtime
+// value; rows past M are zero-filled by TMA and masked in the epilogue, so a
+// batch size that changes every epoch needs no recompilation and no padding.
 #include <cuda.h>
 
 #include <mutex>
-#include <unordered_map>
 
 #include "common.cuh"
+#include "gemm.cuh"
 #include "tcgen05.cuh"
 
 namespace dbs {
@@ -36,13 +46,17 @@ constexpr int kThreads = 128;
 
 struct GemmParams {
   int64_t M, N, K;
-  int a_mn, b_mn;
+  int a_mode, b_mode;
   int epi;
   void* d;
   int64_t ldd;
   const float* bias;
   const uint16_t* aux;  // bf16 [M][ldd] for the ReLU-backward epilogue
-  float* colsum_part;   // optional [ceil(M/32)][N] per-warp column sums of the epilogue output
+  float* colsum_part;   // [ceil(M/32)][N] per-warp column sums of the stored values
+  float* sum_part;      // [ceil(M/32)][N] per-warp column sums of the accumulator
+  float* sq_part;       // [ceil(M/32)][N] per-warp column sums of accumulator^2
+  ConvGeom ga, gb;      // implicit-GEMM geometry of A / B in conv mode
+  int kb_per_split;     // K blocks per CTA along grid.z (split-K)
 };
 
 __device__ __forceinline__ uint16_t f2bf(float f) {
@@ -53,12 +67,20 @@ __device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float(((uin
 
 template <int BN>
 struct Cfg {
-  static constexpr uint32_t kABytes = kBM * kBK * 2;                 // 16 KB
+  static constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + 256;
 };
+
+__device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int& n, int& oh, int& ow) {
+  const int64_t hw = (int64_t)g.OH * g.OW;
+  n = (int)(pix / hw);
+  const int rem = (int)(pix - (int64_t)n * hw);
+  oh = rem / g.OW;
+  ow = rem - oh * g.OW;
+}
 
 template <int BN>
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row, int64_t n_base, const float* v,
@@ -68,7 +90,8 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
   switch (p.epi) {
     case DBS_EPI_F32:
     case DBS_EPI_F32_ACCUM:
-    case DBS_EPI_BIAS_F32: {
+    case DBS_EPI_BIAS_F32:
+    case DBS_EPI_F32_ATOMIC: {
       float* d = reinterpret_cast<float*>(p.d) + row * p.ldd + n_base;
       float o[32];
 #pragma unroll
@@ -77,11 +100,21 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
         float x = v[j];
         if (p.epi == DBS_EPI_BIAS_F32 && n_base + j < N) x += p.bias[n_base + j];
         o[j] = x;
+        v_out[j] = x;
       }
       const bool vec = full && cnt == 32 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0);
       if (p.epi == DBS_EPI_F32_ACCUM) {
         for (int j = 0; j < cnt; j++)
           if (n_base + j < N) d[j] += o[j];
+      } else if (p.epi == DBS_EPI_F32_ATOMIC) {
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            atomicAdd(reinterpret_cast<float4*>(d + j), make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]));
+        } else {
+          for (int j = 0; j < cnt; j++)
+            if (n_base + j < N) atomicAdd(d + j, o[j]);
+        }
       } else if (vec) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
@@ -93,9 +126,26 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
     }
     case DBS_EPI_BIAS_RELU_BF16:
     case DBS_EPI_BF16:
-    case DBS_EPI_RELU_GRAD_BF16: {
+    case DBS_EPI_RELU_GRAD_BF16:
+    case DBS_EPI_BF16_ACCUM: {
       uint16_t* d = reinterpret_cast<uint16_t*>(p.d) + row * p.ldd + n_base;
       const uint16_t* aux = p.aux ? p.aux + row * p.ldd + n_base : nullptr;
+      const bool vec = full && cnt == 32 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0);
+      float prev[32];
+      if (p.epi == DBS_EPI_BF16_ACCUM) {
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            const uint4 q = *reinterpret_cast<const uint4*>(d + j);
+            prev[j + 0] = bf2f(q.x & 0xFFFF); prev[j + 1] = bf2f(q.x >> 16);
+            prev[j + 2] = bf2f(q.y & 0xFFFF); prev[j + 3] = bf2f(q.y >> 16);
+            prev[j + 4] = bf2f(q.z & 0xFFFF); prev[j + 5] = bf2f(q.z >> 16);
+            prev[j + 6] = bf2f(q.w & 0xFFFF); prev[j + 7] = bf2f(q.w >> 16);
+          }
+        } else {
+          for (int j = 0; j < cnt; j++) prev[j] = (n_base + j < N) ? bf2f(d[j]) : 0.0f;
+        }
+      }
       uint16_t o[32];
 #pragma unroll
       for (int j = 0; j < 32; j++) {
@@ -106,11 +156,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
           x = fmaxf(x, 0.0f);
         } else if (p.epi == DBS_EPI_RELU_GRAD_BF16) {
           x = (n_base + j < N && bf2f(aux[j]) > 0.0f) ? x : 0.0f;
+        } else if (p.epi == DBS_EPI_BF16_ACCUM) {
+          x += prev[j];
         }
         o[j] = f2bf(x);
         v_out[j] = x;
       }
-      const bool vec = full && cnt == 32 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0);
       if (vec) {
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
@@ -132,6 +183,19 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
   }
 }
 
+// transpose-reduce 32 rows x 32 columns across the warp: lane j gets column j's sum
+__device__ __forceinline__ float warp_colsum(float (&x)[32], int lane) {
+  float mine = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 32; j++) {
+    float s = x[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == j) mine = s;
+  }
+  return mine;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
@@ -147,7 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m0 = (int64_t)blockIdx.x * kBM, n0 = (int64_t)blockIdx.y * BN;
-  const int num_k = (int)((p.K + kBK - 1) / kBK);
+  const int num_k_total = (int)((p.K + kBK - 1) / kBK);
+  const int kb_begin = (int)blockIdx.z * p.kb_per_split;
+  int kb_end = kb_begin + p.kb_per_split;
+  if (kb_end > num_k_total) kb_end = num_k_total;
+  const int num_k = kb_end > kb_begin ? kb_end - kb_begin : 0;
+  const int a_mn = (p.a_mode == 1) ? 1 : 0;
+  const int b_mn = (p.b_mode >= 1) ? 1 : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -167,92 +237,123 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    for (int kb = 0; kb < num_k; kb++) {
-      const int s = kb % C::kStages;
-      if (kb >= C::kStages) mbar_wait(&empty[s], ((kb / C::kStages) & 1) ^ 1);
+    int a_n = 0, a_oh = 0, a_ow = 0;
+    if (p.a_mode == 2) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
+    int b_r = 0, b_s = 0, b_c0 = 0;
+    if (p.b_mode == 2) {
+      const int rs = (int)(n0 / p.gb.Cin);
+      b_c0 = (int)(n0 - (int64_t)rs * p.gb.Cin);
+      b_r = rs / p.gb.S;
+      b_s = rs - b_r * p.gb.S;
+    }
+    for (int i = 0; i < num_k; i++) {
+      const int kb = kb_begin + i;
+      const int s = i % C::kStages;
+      if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], C::kABytes + C::kBBytes);
       const int32_t k0 = kb * kBK;
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
-      if (!p.a_mn) {
+      if (p.a_mode == 0) {
         tma_load_2d(a, &tmA, &full[s], k0, (int32_t)m0);
-      } else {
+      } else if (p.a_mode == 1) {
         tma_load_2d(a, &tmA, &full[s], (int32_t)m0, k0);
         tma_load_2d(a + 8192, &tmA, &full[s], (int32_t)m0 + 64, k0);
-      }
-      if (!p.b_mn) {
-        tma_load_2d(b, &tmB, &full[s], k0, (int32_t)n0);
       } else {
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        const int r = rs / g.S, sx = rs - r * g.S;
+        tma_load_4d(a, &tmA, &full[s], cb * 64, a_ow * g.stride + sx - g.pad, a_oh * g.stride + r - g.pad, a_n);
+      }
+      if (p.b_mode == 0) {
+        tma_load_2d(b, &tmB, &full[s], k0, (int32_t)n0);
+      } else if (p.b_mode == 1) {
 #pragma unroll
         for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, k0);
+      } else {
+        const ConvGeom& g = p.gb;
+        int bn_, boh, bow;
+        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
+                      boh * g.stride + b_r - g.pad, bn_);
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = make_idesc_bf16(kBM, BN, p.a_mn, p.b_mn);
-    for (int kb = 0; kb < num_k; kb++) {
-      const int s = kb % C::kStages;
-      mbar_wait(&full[s], (kb / C::kStages) & 1);
+    const uint32_t idesc = make_idesc_bf16(kBM, BN, a_mn, b_mn);
+    for (int i = 0; i < num_k; i++) {
+      const int s = i % C::kStages;
+      mbar_wait(&full[s], (i / C::kStages) & 1);
       tc_fence_after();
       const uint32_t a_base = smem_u32(sA + s * C::kABytes);
       const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
 #pragma unroll
       for (int k = 0; k < kBK / 16; k++) {
-        const uint64_t ad = p.a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
-        const uint64_t bd = p.b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
-        mma_bf16_ss(tmem_base, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+        const uint64_t ad = a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+        const uint64_t bd = b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+        mma_bf16_ss(tmem_base, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
       }
       mma_commit(&empty[s]);
     }
-    mma_commit(tmem_full);
+    if (num_k > 0) mma_commit(tmem_full);
   }
   __syncwarp();
 
   // ---------------- epilogue (all 4 warps) ----------------
-  mbar_wait(tmem_full, 0);
-  tc_fence_after();
-  const int64_t row = m0 + warp * 32 + lane;
-  const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
-  if (BN >= 32) {
+  if (num_k > 0) {
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int64_t row = m0 + warp * 32 + lane;
+    const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
+    const bool stats = (p.sum_part != nullptr);
+    if (BN >= 32) {
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; c++) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(lane_addr + c * 32, r);
-      tmem_ld_wait();
-      const int64_t n_base = n0 + c * 32;
-      if (n_base >= p.N) continue;  // warp-uniform
-      float v[32], vo[32];
-#pragma unroll
-      for (int j = 0; j < 32; j++) {
-        v[j] = __uint_as_float(r[j]);
-        vo[j] = 0.0f;
-      }
-      const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
-      if (row < p.M) epilogue_chunk<BN>(p, row, n_base, v, cnt, vo);
-      if (p.colsum_part != nullptr) {
-        // deterministic per-warp column sums of the stored values (e.g. the bias
-        // gradient sum_b dH): transpose-reduce 32 rows x 32 columns across lanes
+      for (int c = 0; c < BN / 32; c++) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(lane_addr + c * 32, r);
+        tmem_ld_wait();
+        const int64_t n_base = n0 + c * 32;
+        if (n_base >= p.N) continue;  // warp-uniform
+        float v[32], vo[32];
 #pragma unroll
         for (int j = 0; j < 32; j++) {
-          float s = vo[j];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          vo[j] = s;
+          v[j] = (row < p.M) ? __uint_as_float(r[j]) : 0.0f;
+          vo[j] = 0.0f;
         }
+        const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
+        if (row < p.M) epilogue_chunk<BN>(p, row, n_base, v, cnt, vo);
         const int64_t g = (m0 >> 5) + warp;
-        if (lane < cnt && m0 + warp * 32 < p.M) p.colsum_part[g * p.N + n_base + lane] = vo[lane];
-      }
-    }
-  } else {
-    uint32_t r[16];
-    tmem_ld_32x32b_x16(lane_addr, r);
-    tmem_ld_wait();
-    if (row < p.M && n0 < p.N) {
-      float v[32], vo[32];
+        const bool group_live = (m0 + warp * 32 < p.M);
+        if (p.colsum_part != nullptr) {
+          const float s = warp_colsum(vo, lane);
+          if (lane < cnt && group_live) p.colsum_part[g * p.N + n_base + lane] = s;
+        }
+        if (stats) {
+          const float s = warp_colsum(v, lane);
+          float sq[32];
 #pragma unroll
-      for (int j = 0; j < 16; j++) v[j] = __uint_as_float(r[j]);
-      const int cnt = (int)((p.N - n0) < 16 ? (p.N - n0) : 16);
-      epilogue_chunk<BN>(p, row, n0, v, cnt, vo);
+          for (int j = 0; j < 32; j++) sq[j] = v[j] * v[j];
+          const float q = warp_colsum(sq, lane);
+          if (lane < cnt && group_live) {
+            p.sum_part[g * p.N + n_base + lane] = s;
+            p.sq_part[g * p.N + n_base + lane] = q;
+          }
+        }
+      }
+    } else {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(lane_addr, r);
+      tmem_ld_wait();
+      if (row < p.M && n0 < p.N) {
+        float v[32], vo[32];
+#pragma unroll
+        for (int j = 0; j < 16; j++) v[j] = __uint_as_float(r[j]);
+        const int cnt = (int)((p.N - n0) < 16 ? (p.N - n0) : 16);
+        epilogue_chunk<BN>(p, row, n0, v, cnt, vo);
+      }
     }
   }
   tc_fence_before();
@@ -298,36 +399,99 @@ int make_tmap(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t rows, 
   return DBS_OK;
 }
 
+// 4-D NHWC bf16 tensor [N][H][W][C]: box {64 c, bw*stride, bh*stride, bn}, traversal stride on W/H
+int make_tmap_nhwc(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride) {
+  EncodeTiledFn fn = encode_fn();
+  DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 64 == 0, DBS_ERR_ARGUMENT,
+              "conv TMA: 16-byte aligned base and C %% 64 == 0 required");
+  DBS_REQUIRE(bw * stride <= 256 && bh * stride <= 256 && bn <= 256, DBS_ERR_ARGUMENT, "conv TMA: box too large");
+  cuuint64_t dims[4] = {(cuuint64_t)t.C, (cuuint64_t)t.W, (cuuint64_t)t.H, (cuuint64_t)t.N};
+  cuuint64_t strides[3] = {(cuuint64_t)t.C * 2, (cuuint64_t)t.W * t.C * 2, (cuuint64_t)t.H * t.W * t.C * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (4d) failed (%d)", (int)r);
+  return DBS_OK;
+}
+
+// pixels of one box: `rows` consecutive output pixels in NHWC order -> (bw, bh, bn)
+int pixel_box(int OH, int OW, int rows, int& bw, int& bh, int& bn) {
+  const int hw = OH * OW;
+  if (hw >= rows) {
+    DBS_REQUIRE(hw % rows == 0 && (rows % OW == 0 || OW % rows == 0), DBS_ERR_ARGUMENT,
+                "conv tile of %d pixels does not align with a %dx%d feature map", rows, OH, OW);
+    if (OW >= rows) {
+      bw = rows;
+      bh = 1;
+    } else {
+      bw = OW;
+      bh = rows / OW;
+    }
+    bn = 1;
+  } else {
+    DBS_REQUIRE(rows % hw == 0, DBS_ERR_ARGUMENT, "conv tile of %d pixels does not align with %dx%d", rows, OH, OW);
+    bw = OW;
+    bh = OH;
+    bn = rows / hw;
+  }
+  return DBS_OK;
+}
+
 template <int BN>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t s) {
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits, cudaStream_t s) {
   using C = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
     DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
     attr = true;
   }
-  dim3 grid((unsigned)((p.M + kBM - 1) / kBM), (unsigned)((p.N + BN - 1) / BN));
+  dim3 grid((unsigned)((p.M + kBM - 1) / kBM), (unsigned)((p.N + BN - 1) / BN), (unsigned)splits);
   gemm_bf16_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, p);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
 
+int pick_bn(int64_t N, int b_mode) {
+  if (N <= 16 && b_mode == 0) return 16;
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  return 256;
+}
+
+int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int bn, int splits, cudaStream_t s) {
+  switch (bn) {
+    case 16: return launch<16>(ta, tb, p, splits, s);
+    case 64: return launch<64>(ta, tb, p, splits, s);
+    case 128: return launch<128>(ta, tb, p, splits, s);
+    default: return launch<256>(ta, tb, p, splits, s);
+  }
+}
+
 }  // namespace
 
-// Entry used by the MLP driver too.
+int preload_gemm() {
+  // force-load every instantiation (lazy module loading must never happen while
+  // a disturbance kernel owns SMs); also sets the shared-memory attribute
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<16>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<64>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<256>::kSmem));
+  return DBS_OK;
+}
+
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
               int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
               float* colsum_part) {
   DBS_REQUIRE(M > 0 && N > 0 && K > 0 && a && b && d, DBS_ERR_ARGUMENT, "gemm: bad shape/pointers");
-  DBS_REQUIRE(epi >= DBS_EPI_F32 && epi <= DBS_EPI_RELU_GRAD_BF16, DBS_ERR_ARGUMENT, "gemm: bad epilogue %d", epi);
+  DBS_REQUIRE(epi >= DBS_EPI_F32 && epi <= DBS_EPI_BF16_ACCUM, DBS_ERR_ARGUMENT, "gemm: bad epilogue %d", epi);
   DBS_REQUIRE(!((epi == DBS_EPI_BIAS_RELU_BF16 || epi == DBS_EPI_BIAS_F32) && !bias), DBS_ERR_ARGUMENT,
               "gemm: epilogue needs bias");
   DBS_REQUIRE(!(epi == DBS_EPI_RELU_GRAD_BF16 && !aux), DBS_ERR_ARGUMENT, "gemm: epilogue needs aux");
-  int bn;
-  if (N <= 16 && !b_mn) bn = 16;
-  else if (N <= 64) bn = 64;
-  else if (N <= 128) bn = 128;
-  else bn = 256;
+  const int bn = pick_bn(N, b_mn);
+  DBS_REQUIRE(!(colsum_part && bn < 32), DBS_ERR_ARGUMENT, "gemm: column sums need N > 16");
   CUtensorMap ta, tb;
   int st;
   // A: K-major [M][lda] -> box {64 K, 128 M};  MN-major [K][lda] -> box {64 M, 64 K}
@@ -338,14 +502,77 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
   st = b_mn ? make_tmap(&tb, b, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 64, 64)
             : make_tmap(&tb, b, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, 64, (uint32_t)bn);
   if (st) return st;
-  DBS_REQUIRE(!(colsum_part && bn < 32), DBS_ERR_ARGUMENT, "gemm: column sums need N > 16");
-  GemmParams p{M, N, K, a_mn, b_mn, epi, d, ldd, bias, reinterpret_cast<const uint16_t*>(aux), colsum_part};
-  switch (bn) {
-    case 16: return launch<16>(ta, tb, p, s);
-    case 64: return launch<64>(ta, tb, p, s);
-    case 128: return launch<128>(ta, tb, p, s);
-    default: return launch<256>(ta, tb, p, s);
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.a_mode = a_mn;
+  p.b_mode = b_mn;
+  p.epi = epi;
+  p.d = d;
+  p.ldd = ldd;
+  p.bias = bias;
+  p.aux = reinterpret_cast<const uint16_t*>(aux);
+  p.colsum_part = colsum_part;
+  p.kb_per_split = (int)((K + kBK - 1) / kBK);
+  return dispatch(ta, tb, p, bn, 1, s);
+}
+
+// Implicit-GEMM convolution family (see gemm.cuh).
+int conv_gemm(const ConvCall& c, cudaStream_t s) {
+  DBS_REQUIRE(c.d && c.M > 0 && c.N > 0 && c.K > 0, DBS_ERR_ARGUMENT, "conv_gemm: bad call");
+  CUtensorMap ta, tb;
+  GemmParams p{};
+  p.M = c.M;
+  p.N = c.N;
+  p.K = c.K;
+  p.epi = c.epi;
+  p.d = c.d;
+  p.ldd = c.ldd;
+  p.bias = c.bias;
+  p.aux = c.aux;
+  p.sum_part = c.sum_part;
+  p.sq_part = c.sq_part;
+  p.colsum_part = nullptr;
+  int st;
+  const int bn = (c.bn_override > 0) ? c.bn_override : pick_bn(c.N, c.b_mode);
+  // ---- A ----
+  p.a_mode = c.a_mode;
+  if (c.a_mode == 2) {
+    int bw, bh, bnn;
+    st = pixel_box(c.ga.OH, c.ga.OW, kBM, bw, bh, bnn);
+    if (st) return st;
+    st = make_tmap_nhwc(&ta, c.a, c.ta, bw, bh, bnn, c.ga.stride);
+    if (st) return st;
+    p.ga = c.ga;
+  } else {
+    st = c.a_mode ? make_tmap(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 64, 64)
+                  : make_tmap(&ta, c.a, (uint64_t)c.K, (uint64_t)c.M, (uint64_t)c.lda, 64, 128);
+    if (st) return st;
   }
+  // ---- B ----
+  p.b_mode = c.b_mode;
+  if (c.b_mode == 2) {
+    int bw, bh, bnn;
+    st = pixel_box(c.gb.OH, c.gb.OW, kBK, bw, bh, bnn);
+    if (st) return st;
+    st = make_tmap_nhwc(&tb, c.b, c.tb, bw, bh, bnn, c.gb.stride);
+    if (st) return st;
+    p.gb = c.gb;
+    DBS_REQUIRE(c.gb.Cin % bn == 0 || bn % c.gb.Cin == 0, DBS_ERR_ARGUMENT, "wgrad: tile must not straddle (r,s)");
+    DBS_REQUIRE(bn <= c.gb.Cin, DBS_ERR_ARGUMENT, "wgrad: BN %d > Cin %d", bn, c.gb.Cin);
+  } else {
+    st = c.b_mode ? make_tmap(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, 64, 64)
+                  : make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, (uint32_t)bn);
+    if (st) return st;
+  }
+  const int num_k = (int)((c.K + kBK - 1) / kBK);
+  int splits = c.splits > 0 ? c.splits : 1;
+  if (splits > num_k) splits = num_k;
+  p.kb_per_split = (num_k + splits - 1) / splits;
+  splits = (num_k + p.kb_per_split - 1) / p.kb_per_split;
+  DBS_REQUIRE(splits == 1 || c.epi == DBS_EPI_F32_ATOMIC, DBS_ERR_ARGUMENT, "split-K needs the atomic epilogue");
+  return dispatch(ta, tb, p, bn, splits, s);
 }
 
 }  // namespace dbs

@@ -235,10 +235,22 @@ extern "C" int dbs_dev_spin_for(int32_t num_ctas, int64_t ns, void* stream);
 extern "C" int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, int64_t end, double* d_seconds,
                                        int64_t worker, void* stream);
 
-extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
-                                      float lr, float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
-                                      int32_t skip_update, void* agg_stream) {
-  DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "mlp_run_iterations: bad arguments");
+namespace dbs {
+int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const float* x_base, const int32_t* y_base,
+                   const int64_t* d_iter, int64_t B, float* grad, float* loss, cudaStream_t s);
+int resnet_param_count(const dbs_resnet* m);
+int iter_increment(int64_t* d_iter, cudaStream_t s);
+}  // namespace dbs
+
+extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                                  float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                                  int32_t skip_update, void* agg_stream, int64_t* d_iter) {
+  DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "run_iterations: bad arguments");
+  for (int i = 0; i < n; i++)
+    DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18) &&
+                    !(d_iter && w[i].model_kind == DBS_MODEL_MLP),
+                DBS_ERR_ARGUMENT, "run_iterations: worker %d has a bad model (device iteration index is ResNet-only)",
+                i);
   cudaEvent_t* ev;
   int st = events(n + 1, &ev);
   if (st) return st;
@@ -249,7 +261,8 @@ extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64
     grads[i] = w[i].grad;
     batches[i] = w[i].batch;
   }
-  const int64_t P = w[0].model->P;
+  const int64_t P = (w[0].model_kind == DBS_MODEL_MLP) ? static_cast<const dbs_mlp*>(w[0].model)->P
+                                                       : resnet_param_count(static_cast<const dbs_resnet*>(w[0].model));
   DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
   for (int64_t t = t0; t < t1; t++) {
     for (int i = 0; i < n; i++) {
@@ -263,10 +276,24 @@ extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64
         st = dbs_dev_spin_for(w[i].spin_ctas, w[i].spin_ns, s);
         if (st) return st;
       }
-      const dbs_mlp* m = w[i].model;
       const int64_t b = w[i].batch;
-      st = mlp_fwd_bwd(w[i].model, d_params_bf16, d_params, w[i].x_shard + t * b * m->in, w[i].y_shard + t * b, b,
-                       w[i].grad, w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
+      if (w[i].model_kind == DBS_MODEL_MLP) {
+        dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
+        const uint16_t* x = static_cast<const uint16_t*>(w[i].x_shard) + t * b * m->in;
+        st = mlp_fwd_bwd(m, d_params_bf16, d_params, x, w[i].y_shard + t * b, b, w[i].grad,
+                         w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
+      } else {
+        dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
+        const float* x = static_cast<const float*>(w[i].x_shard);
+        const int32_t* y = w[i].y_shard;
+        float* loss = w[i].loss;
+        if (!d_iter) {  // host-indexed iteration
+          x += t * b * 3072;
+          y += t * b;
+          loss = loss ? loss + t : nullptr;
+        }
+        st = resnet_fwd_bwd(m, d_params_bf16, d_params, x, y, d_iter, b, w[i].grad, loss, s);
+      }
       if (st) return st;
       if (w[i].stamps) {
         st = stamp(w[i].stamps, 1, s);
@@ -282,7 +309,18 @@ extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64
                                      agg_stream);
       if (st) return st;
     }
+    if (d_iter) {
+      st = iter_increment(d_iter, agg);
+      if (st) return st;
+    }
     DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
   }
   return DBS_OK;
+}
+
+extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                      float lr, float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                                      int32_t skip_update, void* agg_stream) {
+  return dbs_run_iterations(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_bf16, skip_update,
+                            agg_stream, nullptr);
 }

@@ -1,0 +1,863 @@
+// resnet.cu -- ResNet-18 (CIFAR stem: 3x3 conv, no max-pool) forward/backward
+// of one worker's variable batch, on the tcgen05 implicit-GEMM convolution.
+//
+// This is the named model of configs 3-4 (BASELINE.json): the per-worker
+// gradient of sgdlab.minibatch_gradient (sgdlab.py:200-205) for a network the
+// reference only models by its cost (cluster.py:132-145).
+//
+// Layout: activations NHWC bf16; conv weights [Cout][R][S][Cin] (K-major, c
+// fastest) in one flat fp32 parameter vector with a bf16 shadow (the GEMM
+// operand), BN gamma/beta fp32, FC fp32.  Per conv (all on the worker stream):
+//   forward : implicit-GEMM conv (4-D TMA) -> bf16 y + per-warp BN partial sums
+//             -> bn_stats (fp64 reduce) -> bn_apply (+ReLU, +residual/+BN(ds))
+//   backward: bn_bwd_reduce / bn_bwd_apply (ReLU mask recomputed from the saved
+//             output) -> dgrad = conv(dY, flipped W) (stride-2: dY dilated) with
+//             bf16 accumulation of the shortcut gradient -> wgrad = dY^T im2col(X)
+//             (split-K, fp32 atomics into the flat gradient)
+// BatchNorm uses the worker's own batch statistics (local BN, as in DDP without
+// SyncBN); running statistics are not tracked (training throughput path).
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace dbs {
+
+namespace {
+
+constexpr float kBnEps = 1e-5f;
+constexpr int kStemK = 32;  // 27 = 3x3x3 padded to 32
+
+__device__ __forceinline__ uint16_t f2bf(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+__device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
+
+struct Conv {
+  int cin, cout, k, stride, pad;
+  int H, W, OH, OW;         // input / output spatial
+  int64_t w_off, w_len;     // weight block in the flat parameter vector
+  int64_t g_off, b_off;     // BN gamma / beta
+};
+
+struct Block {
+  int c1, c2, ds;  // indices into convs (ds = -1 when identity shortcut)
+};
+
+// ----------------------------- kernels ------------------------------------
+
+// stem im2col: x fp32 [B][3][32][32] (CHW per sample, the repacked shard row
+// t*B .. ) -> A bf16 [B*1024][32], K = (r, s, c) with c fastest, zero padded.
+__global__ void im2col_stem_kernel(const float* __restrict__ x_base, const int64_t* __restrict__ iter, int64_t B,
+                                   uint16_t* __restrict__ out) {
+  const int64_t t = iter ? *iter : 0;
+  const float* x = x_base + t * B * 3072;
+  const int64_t total = B * 1024;
+  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < total;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = pix >> 10;
+    const int h = (int)((pix >> 5) & 31), w = (int)(pix & 31);
+    const float* xs = x + n * 3072;
+    uint32_t packed[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) packed[q] = 0;
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+      for (int s = 0; s < 3; s++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const int hh = h + r - 1, ww = w + s - 1;
+          const float v = (hh >= 0 && hh < 32 && ww >= 0 && ww < 32) ? xs[c * 1024 + hh * 32 + ww] : 0.0f;
+          const int k = (r * 3 + s) * 3 + c;
+          packed[k >> 1] |= (uint32_t)f2bf(v) << ((k & 1) * 16);
+        }
+    uint4* o = reinterpret_cast<uint4*>(out + pix * kStemK);
+#pragma unroll
+    for (int q = 0; q < 4; q++) o[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+  }
+}
+
+// BN batch statistics: partial sums over 32-row groups -> mean, 1/sqrt(var+eps)
+__global__ void bn_stats_kernel(const float* __restrict__ sum_part, const float* __restrict__ sq_part, int64_t groups,
+                                int C, int64_t M, float* __restrict__ mean, float* __restrict__ invstd) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0, q = 0.0;
+  for (int64_t g = 0; g < groups; g++) {
+    s += (double)sum_part[g * C + c];
+    q += (double)sq_part[g * C + c];
+  }
+  const double mu = s / (double)M;
+  double var = q / (double)M - mu * mu;
+  if (var < 0.0) var = 0.0;
+  mean[c] = (float)mu;
+  invstd[c] = (float)(1.0 / sqrt(var + (double)kBnEps));
+}
+
+// out = act( gamma*(y-mean)*invstd + beta  [+ res | + BN_ds(yd)] ), 8 channels / thread
+__global__ void bn_apply_kernel(const uint16_t* __restrict__ y, const float* __restrict__ mean,
+                                const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, const uint16_t* __restrict__ res,
+                                const uint16_t* __restrict__ yd, const float* __restrict__ mean_d,
+                                const float* __restrict__ invstd_d, const float* __restrict__ gamma_d,
+                                const float* __restrict__ beta_d, int relu, int C, int64_t M,
+                                uint16_t* __restrict__ out) {
+  const int cv = C / 8;
+  const int64_t total = M * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % cv) * 8;
+    const uint4 q = reinterpret_cast<const uint4*>(y)[i];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t rw[4] = {0, 0, 0, 0}, dw[4] = {0, 0, 0, 0};
+    if (res) {
+      const uint4 r = reinterpret_cast<const uint4*>(res)[i];
+      rw[0] = r.x; rw[1] = r.y; rw[2] = r.z; rw[3] = r.w;
+    }
+    if (yd) {
+      const uint4 r = reinterpret_cast<const uint4*>(yd)[i];
+      dw[0] = r.x; dw[1] = r.y; dw[2] = r.z; dw[3] = r.w;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int c = c0 + k;
+      const float v = bf2f((uint16_t)(w[k >> 1] >> ((k & 1) * 16)));
+      float z = fmaf(gamma[c] * invstd[c], v - mean[c], beta[c]);
+      if (res) z += bf2f((uint16_t)(rw[k >> 1] >> ((k & 1) * 16)));
+      if (yd) {
+        const float vd = bf2f((uint16_t)(dw[k >> 1] >> ((k & 1) * 16)));
+        z += fmaf(gamma_d[c] * invstd_d[c], vd - mean_d[c], beta_d[c]);
+      }
+      if (relu) z = fmaxf(z, 0.0f);
+      const uint32_t h = f2bf(z);
+      if (k & 1)
+        o[k >> 1] |= h << 16;
+      else
+        o[k >> 1] = h;
+    }
+    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// BN backward, pass 1: dbeta[c] += sum g, dgamma[c] += sum g*yhat,
+// g = gin * [mask > 0] (mask = saved post-ReLU output, nullable)
+template <int C8>
+__global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __restrict__ gin,
+                                                            const uint16_t* __restrict__ mask,
+                                                            const uint16_t* __restrict__ y,
+                                                            const float* __restrict__ mean,
+                                                            const float* __restrict__ invstd, int C, int64_t M,
+                                                            float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  // each thread owns 8 channels (c0 = 8 * (tid % cv)) over rows tid / cv, +rows_per_pass
+  __shared__ float red_g[2048], red_b[2048];
+  const int cv = C / 8;
+  const int rows_per_pass = blockDim.x / cv;
+  const int lane_c = threadIdx.x % cv, lane_r = threadIdx.x / cv;
+  float sg[8], sb[8], mu[8], is[8];
+  const int c0 = lane_c * 8;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    sg[k] = 0.f;
+    sb[k] = 0.f;
+    mu[k] = mean[c0 + k];
+    is[k] = invstd[c0 + k];
+  }
+  if (lane_r < rows_per_pass) {
+    for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + lane_r; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
+      const int64_t i = r * cv + lane_c;
+      const uint4 qg = reinterpret_cast<const uint4*>(gin)[i];
+      const uint4 qy = reinterpret_cast<const uint4*>(y)[i];
+      uint4 qm = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      if (mask) qm = reinterpret_cast<const uint4*>(mask)[i];
+      const uint32_t gw[4] = {qg.x, qg.y, qg.z, qg.w}, yw[4] = {qy.x, qy.y, qy.z, qy.w},
+                     mw[4] = {qm.x, qm.y, qm.z, qm.w};
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int sh = (k & 1) * 16;
+        float g = bf2f((uint16_t)(gw[k >> 1] >> sh));
+        if (mask && !(bf2f((uint16_t)(mw[k >> 1] >> sh)) > 0.0f)) g = 0.0f;
+        const float yh = (bf2f((uint16_t)(yw[k >> 1] >> sh)) - mu[k]) * is[k];
+        sb[k] += g;
+        sg[k] = fmaf(g, yh, sg[k]);
+      }
+    }
+  }
+  // block reduction over lane_r for each channel
+  for (int idx = threadIdx.x; idx < C; idx += blockDim.x) {
+    red_g[idx] = 0.f;
+    red_b[idx] = 0.f;
+  }
+  __syncthreads();
+  if (lane_r < rows_per_pass) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      atomicAdd(&red_g[c0 + k], sg[k]);
+      atomicAdd(&red_b[c0 + k], sb[k]);
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < C; idx += blockDim.x) {
+    atomicAdd(&dgamma[idx], red_g[idx]);
+    atomicAdd(&dbeta[idx], red_b[idx]);
+  }
+}
+
+// BN backward, pass 2: dy = gamma*invstd*(g - dbeta/M - yhat*dgamma/M), bf16;
+// optionally also stores g (the masked incoming gradient, for the shortcut).
+__global__ void bn_bwd_apply_kernel(const uint16_t* __restrict__ gin, const uint16_t* __restrict__ mask,
+                                    const uint16_t* __restrict__ y, const float* __restrict__ mean,
+                                    const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                    const float* __restrict__ dgamma, const float* __restrict__ dbeta, int C,
+                                    int64_t M, uint16_t* __restrict__ dy, uint16_t* __restrict__ g_out) {
+  const int cv = C / 8;
+  const int64_t total = M * cv;
+  const float invM = 1.0f / (float)M;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % cv) * 8;
+    const uint4 qg = reinterpret_cast<const uint4*>(gin)[i];
+    const uint4 qy = reinterpret_cast<const uint4*>(y)[i];
+    uint4 qm = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (mask) qm = reinterpret_cast<const uint4*>(mask)[i];
+    const uint32_t gw[4] = {qg.x, qg.y, qg.z, qg.w}, yw[4] = {qy.x, qy.y, qy.z, qy.w},
+                   mw[4] = {qm.x, qm.y, qm.z, qm.w};
+    uint32_t o[4] = {0, 0, 0, 0}, go[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int c = c0 + k, sh = (k & 1) * 16;
+      float g = bf2f((uint16_t)(gw[k >> 1] >> sh));
+      if (mask && !(bf2f((uint16_t)(mw[k >> 1] >> sh)) > 0.0f)) g = 0.0f;
+      const float yh = (bf2f((uint16_t)(yw[k >> 1] >> sh)) - mean[c]) * invstd[c];
+      const float d = gamma[c] * invstd[c] * (g - dbeta[c] * invM - yh * dgamma[c] * invM);
+      o[k >> 1] |= (uint32_t)f2bf(d) << sh;
+      go[k >> 1] |= (uint32_t)f2bf(g) << sh;
+    }
+    reinterpret_cast<uint4*>(dy)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    if (g_out) reinterpret_cast<uint4*>(g_out)[i] = make_uint4(go[0], go[1], go[2], go[3]);
+  }
+}
+
+// dilate a stride-2 output gradient: u[n][2i][2j][c] = dy[n][i][j][c], 0 elsewhere
+__global__ void dilate2_kernel(const uint16_t* __restrict__ dy, int64_t N, int OH, int OW, int C,
+                               uint16_t* __restrict__ u) {
+  const int H = 2 * OH, W = 2 * OW, cv = C / 8;
+  const int64_t total = N * H * W * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(i % cv);
+    const int64_t pix = i / cv;
+    const int w = (int)(pix % W), h = (int)((pix / W) % H);
+    const int64_t n = pix / ((int64_t)H * W);
+    uint4 q = make_uint4(0, 0, 0, 0);
+    if (!(h & 1) && !(w & 1)) q = reinterpret_cast<const uint4*>(dy)[((n * OH + (h >> 1)) * OW + (w >> 1)) * cv + v];
+    reinterpret_cast<uint4*>(u)[i] = q;
+  }
+}
+
+// dgrad filter: Wt[c][r][s][k] = W[k][R-1-r][S-1-s][c]  (bf16)
+__global__ void flip_weights_kernel(const uint16_t* __restrict__ w, int Cout, int R, int S, int Cin,
+                                    uint16_t* __restrict__ wt) {
+  const int64_t total = (int64_t)Cout * R * S * Cin;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    // i indexes the output Wt[c][r][s][k] with k fastest
+    const int k = (int)(i % Cout);
+    int64_t rest = i / Cout;
+    const int s = (int)(rest % S);
+    rest /= S;
+    const int r = (int)(rest % R);
+    const int c = (int)(rest / R);
+    wt[i] = w[(((int64_t)k * R + (R - 1 - r)) * S + (S - 1 - s)) * Cin + c];
+  }
+}
+
+// head forward+backward, one CTA per sample: global average pool of the 4x4x512
+// map, FC 512 -> C, softmax cross-entropy; writes dlogits/B, feat, the pooled-
+// map gradient dOut = (dlogits W)/16, and the per-sample loss.
+__global__ void __launch_bounds__(256) head_kernel(const uint16_t* __restrict__ a4, const float* __restrict__ Wfc,
+                                                   const float* __restrict__ bfc, const int32_t* __restrict__ y_base,
+                                                   const int64_t* __restrict__ iter, int64_t B, int classes,
+                                                   float* __restrict__ feat, float* __restrict__ dlog,
+                                                   float* __restrict__ loss_per, uint16_t* __restrict__ dout) {
+  __shared__ float f[512];
+  __shared__ float logit[16];
+  const int64_t n = blockIdx.x;
+  const int64_t t = iter ? *iter : 0;
+  const int32_t label = y_base[t * B + n];
+  for (int c = threadIdx.x; c < 512; c += blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < 16; p++) s += bf2f(a4[(n * 16 + p) * 512 + c]);
+    f[c] = s * (1.0f / 16.0f);
+    feat[n * 512 + c] = f[c];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < classes; k += blockDim.x >> 5) {
+    float s = 0.f;
+    for (int c = lane; c < 512; c += 32) s = fmaf(f[c], Wfc[k * 512 + c], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) logit[k] = s + bfc[k];
+  }
+  __syncthreads();
+  __shared__ float dl[16];
+  if (threadIdx.x == 0) {
+    float mx = -INFINITY;
+    for (int k = 0; k < classes; k++) mx = fmaxf(mx, logit[k]);
+    float se = 0.f;
+    for (int k = 0; k < classes; k++) se += __expf(logit[k] - mx);
+    loss_per[n] = (mx + __logf(se)) - logit[label];
+    const float inv = 1.0f / se, invB = 1.0f / (float)B;
+    for (int k = 0; k < classes; k++) {
+      const float g = (__expf(logit[k] - mx) * inv - (k == label ? 1.f : 0.f)) * invB;
+      dl[k] = g;
+      dlog[n * 16 + k] = g;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 512; c += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < classes; k++) s = fmaf(dl[k], Wfc[k * 512 + c], s);
+    const uint16_t h = f2bf(s * (1.0f / 16.0f));
+    for (int p = 0; p < 16; p++) dout[(n * 16 + p) * 512 + c] = h;
+  }
+}
+
+// dWfc[k][c] = sum_n dlog[n][k] feat[n][c], dbfc[k] = sum_n dlog[n][k]; loss mean
+__global__ void head_wgrad_kernel(const float* __restrict__ feat, const float* __restrict__ dlog,
+                                  const float* __restrict__ loss_per, int64_t B, int classes, float* __restrict__ dW,
+                                  float* __restrict__ db, float* __restrict__ loss_out, const int64_t* __restrict__ iter) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < classes * 512) {
+    const int k = idx / 512, c = idx % 512;
+    float s = 0.f;
+    for (int64_t n = 0; n < B; n++) s = fmaf(dlog[n * 16 + k], feat[n * 512 + c], s);
+    dW[idx] = s;
+  }
+  if (idx < classes) {
+    float s = 0.f;
+    for (int64_t n = 0; n < B; n++) s += dlog[n * 16 + idx];
+    db[idx] = s;
+  }
+  if (idx == 0 && loss_out) {
+    float s = 0.f;
+    for (int64_t n = 0; n < B; n++) s += loss_per[n];
+    loss_out[iter ? *iter : 0] = s / (float)B;
+  }
+}
+
+__global__ void iter_inc_kernel(int64_t* it) { *it += 1; }
+
+int grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+}  // namespace
+}  // namespace dbs
+
+using namespace dbs;
+
+struct dbs_resnet {
+  int64_t max_b = 0;
+  int classes = 10;
+  std::vector<Conv> convs;
+  std::vector<Block> blocks;
+  int stem = 0;
+  int64_t fc_w = 0, fc_b = 0, P = 0;
+  // parameter table (torchvision order): offset, length, kind (0 conv w, 1 bn g, 2 bn b, 3 fc w, 4 fc b)
+  std::vector<int64_t> t_off, t_len;
+  std::vector<int32_t> t_kind;
+  // activations
+  uint16_t* stem_cols = nullptr;           // [B*1024][32]
+  std::vector<uint16_t*> y, a;             // per conv: pre-BN output, post-BN(+ReLU) output
+  std::vector<uint16_t*> blk_out;          // per block output (post residual ReLU)
+  std::vector<float*> mean, invstd;        // per conv
+  float* sum_part = nullptr;               // [max groups][512]
+  float* sq_part = nullptr;
+  uint16_t* g0 = nullptr;                  // gradient ping-pong buffers (largest activation)
+  uint16_t* g1 = nullptr;
+  uint16_t* g2 = nullptr;
+  uint16_t* g3 = nullptr;
+  uint16_t* dil = nullptr;                 // dilated gradient (stride-2 dgrad)
+  uint16_t* wflip = nullptr;               // flipped weights (largest conv)
+  float* feat = nullptr;                   // [B][512]
+  float* dlog = nullptr;                   // [B][16]
+  float* loss_per = nullptr;               // [B]
+  float* loss_scratch = nullptr;
+};
+
+namespace {
+
+int64_t pad8(int64_t x) { return (x + 7) & ~int64_t(7); }
+
+void build_layers(dbs_resnet* m) {
+  int64_t off = 0;
+  auto add_param = [&](int64_t len, int kind) {
+    const int64_t o = off;
+    m->t_off.push_back(o);
+    m->t_len.push_back(len);
+    m->t_kind.push_back(kind);
+    off += pad8(len);
+    return o;
+  };
+  auto add_conv = [&](int cin, int cout, int k, int stride, int pad, int H, int W) {
+    Conv c{};
+    c.cin = cin;
+    c.cout = cout;
+    c.k = k;
+    c.stride = stride;
+    c.pad = pad;
+    c.H = H;
+    c.W = W;
+    c.OH = (H + 2 * pad - k) / stride + 1;
+    c.OW = (W + 2 * pad - k) / stride + 1;
+    // stem weights are stored [64][32] (27 padded to 32 so the row pitch is TMA-legal)
+    c.w_len = (cin == 3) ? (int64_t)cout * kStemK : (int64_t)cout * k * k * cin;
+    c.w_off = add_param(c.w_len, 0);
+    c.g_off = add_param(cout, 1);
+    c.b_off = add_param(cout, 2);
+    m->convs.push_back(c);
+    return (int)m->convs.size() - 1;
+  };
+  m->stem = add_conv(3, 64, 3, 1, 1, 32, 32);
+  int H = 32, cin = 64;
+  const int widths[4] = {64, 128, 256, 512};
+  for (int L = 0; L < 4; L++) {
+    for (int bI = 0; bI < 2; bI++) {
+      const int cout = widths[L];
+      const int stride = (L > 0 && bI == 0) ? 2 : 1;
+      Block b{};
+      b.c1 = add_conv(cin, cout, 3, stride, 1, H, H);
+      const int OH = m->convs[b.c1].OH;
+      b.c2 = add_conv(cout, cout, 3, 1, 1, OH, OH);
+      b.ds = (stride != 1 || cin != cout) ? add_conv(cin, cout, 1, stride, 0, H, H) : -1;
+      m->blocks.push_back(b);
+      cin = cout;
+      H = OH;
+    }
+  }
+  m->fc_w = add_param((int64_t)m->classes * 512, 3);
+  m->fc_b = add_param(m->classes, 4);
+  m->P = (off + 31) & ~int64_t(31);
+}
+
+int alloc_all(dbs_resnet* m) {
+  const int64_t B = m->max_b;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+  };
+  A((void**)&m->stem_cols, (size_t)B * 1024 * kStemK * 2);
+  int64_t max_act = 0;
+  for (auto& c : m->convs) {
+    const int64_t n = B * c.OH * c.OW * c.cout;
+    uint16_t *y, *a;
+    A((void**)&y, n * 2);
+    A((void**)&a, n * 2);
+    m->y.push_back(y);
+    m->a.push_back(a);
+    float *mu, *is;
+    A((void**)&mu, c.cout * 4);
+    A((void**)&is, c.cout * 4);
+    m->mean.push_back(mu);
+    m->invstd.push_back(is);
+    if (n > max_act) max_act = n;
+    const int64_t nin = B * c.H * c.W * c.cin;
+    if (nin > max_act) max_act = nin;
+  }
+  for (size_t i = 0; i < m->blocks.size(); i++) {
+    const Conv& c = m->convs[m->blocks[i].c2];
+    uint16_t* o;
+    A((void**)&o, (size_t)B * c.OH * c.OW * c.cout * 2);
+    m->blk_out.push_back(o);
+  }
+  const int64_t groups = (B * 1024 + 31) / 32 + 8;
+  A((void**)&m->sum_part, (size_t)groups * 512 * 4);
+  A((void**)&m->sq_part, (size_t)groups * 512 * 4);
+  A((void**)&m->g0, max_act * 2);
+  A((void**)&m->g1, max_act * 2);
+  A((void**)&m->g2, max_act * 2);
+  A((void**)&m->g3, max_act * 2);
+  A((void**)&m->dil, max_act * 2 * 4);
+  A((void**)&m->wflip, (size_t)512 * 9 * 512 * 2);
+  A((void**)&m->feat, (size_t)B * 512 * 4);
+  A((void**)&m->dlog, (size_t)B * 16 * 4);
+  A((void**)&m->loss_per, (size_t)B * 4);
+  A((void**)&m->loss_scratch, 64);
+  if (e != cudaSuccess) {
+    set_error("resnet alloc: %s", cudaGetErrorString(e));
+    return DBS_ERR_CUDA;
+  }
+  return DBS_OK;
+}
+
+ConvTensor nhwc(int64_t N, int H, int W, int C) { return ConvTensor{(int)N, H, W, C}; }
+
+// forward conv -> y (bf16) + BN statistics -> mean/invstd
+int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64_t B, cudaStream_t s) {
+  const Conv& c = m->convs[ci];
+  const int64_t M = B * c.OH * c.OW;
+  ConvCall call{};
+  call.M = M;
+  call.N = c.cout;
+  call.epi = DBS_EPI_BF16;
+  call.d = m->y[ci];
+  call.ldd = c.cout;
+  call.sum_part = m->sum_part;
+  call.sq_part = m->sq_part;
+  call.b = wb + c.w_off;
+  call.b_mode = 0;
+  if (c.cin == 3) {  // stem: explicit im2col columns [M][32]
+    call.K = kStemK;
+    call.a_mode = 0;
+    call.a = m->stem_cols;
+    call.lda = kStemK;
+    call.ldb = kStemK;
+  } else {
+    call.K = (int64_t)c.k * c.k * c.cin;
+    call.a_mode = 2;
+    call.a = x;
+    call.ta = nhwc(B, c.H, c.W, c.cin);
+    call.ga = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
+    call.ldb = call.K;
+  }
+  int st = conv_gemm(call, s);
+  if (st) return st;
+  const int64_t groups = (M + 31) / 32;
+  bn_stats_kernel<<<(c.cout + 127) / 128, 128, 0, s>>>(m->sum_part, m->sq_part, groups, c.cout, M, m->mean[ci],
+                                                        m->invstd[ci]);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds, int relu, int64_t B,
+             uint16_t* out, cudaStream_t s) {
+  const Conv& c = m->convs[ci];
+  const int64_t M = B * c.OH * c.OW;
+  const int64_t total = M * (c.cout / 8);
+  const Conv* d = ds >= 0 ? &m->convs[ds] : nullptr;
+  bn_apply_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+      m->y[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res, d ? m->y[ds] : nullptr,
+      d ? m->mean[ds] : nullptr, d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
+      d ? pf + d->b_off : nullptr, relu, c.cout, M, out);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+// BN backward for conv ci: gin (masked by `mask` > 0 when given) -> dy; gamma/beta grads into grad
+int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* gin, const uint16_t* mask, int64_t B,
+           uint16_t* dy, uint16_t* g_out, cudaStream_t s) {
+  const Conv& c = m->convs[ci];
+  const int64_t M = B * c.OH * c.OW;
+  const int cv = c.cout / 8;
+  const int rows_per_pass = 256 / cv;
+  int blocks = (int)((M + rows_per_pass * 16 - 1) / (rows_per_pass * 16));
+  if (blocks > num_sms() * 4) blocks = num_sms() * 4;
+  if (blocks < 1) blocks = 1;
+  bn_bwd_reduce_kernel<8><<<blocks, 256, 0, s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci], c.cout, M,
+                                                  grad + c.g_off, grad + c.b_off);
+  DBS_LAUNCH_CHECK();
+  const int64_t total = M * cv;
+  bn_bwd_apply_kernel<<<grid_for(total, 256), 256, 0, s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
+                                                            pf + c.g_off, grad + c.g_off, grad + c.b_off, c.cout, M,
+                                                            dy, g_out);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+// dX (+)= dgrad of conv c from dy; accumulate selects the bf16 accumulate epilogue.
+// wflip: [Cin][k][k][Cout] scratch; dil: dilated-gradient scratch (stride 2)
+int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t B, uint16_t* dx, int accumulate,
+                  uint16_t* wflip, uint16_t* dil, cudaStream_t s) {
+  const int64_t wn = (int64_t)c.cout * c.k * c.k * c.cin;
+  flip_weights_kernel<<<grid_for(wn, 256), 256, 0, s>>>(w, c.cout, c.k, c.k, c.cin, wflip);
+  DBS_LAUNCH_CHECK();
+  const uint16_t* src = dy;
+  int gh = c.OH, gw = c.OW;
+  if (c.stride == 2) {
+    const int64_t total = B * (2 * c.OH) * (2 * c.OW) * (c.cout / 8);
+    dilate2_kernel<<<grid_for(total, 256), 256, 0, s>>>(dy, B, c.OH, c.OW, c.cout, dil);
+    DBS_LAUNCH_CHECK();
+    src = dil;
+    gh = 2 * c.OH;
+    gw = 2 * c.OW;
+  }
+  ConvCall call{};
+  call.M = B * c.H * c.W;
+  call.N = c.cin;
+  call.K = (int64_t)c.k * c.k * c.cout;
+  call.a_mode = 2;
+  call.a = src;
+  call.ta = nhwc(B, gh, gw, c.cout);
+  // 3x3 pad 1 -> flipped 3x3 pad 1; 1x1 pad 0 -> 1x1 pad 0 (stride 1 over the dilated map)
+  call.ga = ConvGeom{c.k, c.k, c.cout / 64, 1, c.k / 2, c.H, c.W, c.cout};
+  call.b_mode = 0;
+  call.b = wflip;
+  call.ldb = call.K;
+  call.epi = accumulate ? DBS_EPI_BF16_ACCUM : DBS_EPI_BF16;
+  call.d = dx;
+  call.ldd = c.cin;
+  return conv_gemm(call, s);
+}
+
+int conv_dgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* wb, int64_t B, uint16_t* dx, int accumulate,
+               cudaStream_t s) {
+  const Conv& c = m->convs[ci];
+  return conv_dgrad_ex(c, dy, wb + c.w_off, B, dx, accumulate, m->wflip, m->dil, s);
+}
+
+// dW of conv c (fp32 atomics into dw) from dy and the conv input x (stem: im2col columns)
+int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t B, float* dw, cudaStream_t s) {
+  const int64_t pixels = B * c.OH * c.OW;
+  ConvCall call{};
+  call.a_mode = 1;  // dY^T: dY stored [pixels][Cout]
+  call.a = dy;
+  call.lda = c.cout;
+  call.M = c.cout;
+  call.epi = DBS_EPI_F32_ATOMIC;
+  call.d = dw;
+  int bn;
+  if (c.cin == 3) {  // stem: columns [pixels][32]
+    call.N = kStemK;
+    call.K = pixels;
+    call.b_mode = 1;
+    call.b = x;
+    call.ldb = kStemK;
+    call.ldd = kStemK;
+    bn = 64;
+  } else {
+    call.N = (int64_t)c.k * c.k * c.cin;
+    call.K = pixels;
+    call.b_mode = 2;
+    call.b = x;
+    call.tb = nhwc(B, c.H, c.W, c.cin);
+    call.gb = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
+    call.ldd = call.N;
+    bn = c.cin >= 256 ? 256 : c.cin;
+    call.bn_override = bn;
+  }
+  // split the long pixel reduction so ~2 waves of CTAs are in flight
+  const int64_t tiles = ((call.M + 127) / 128) * ((call.N + bn - 1) / bn);
+  const int64_t kblocks = (call.K + 63) / 64;
+  int64_t splits = (2 * num_sms() + tiles - 1) / tiles;
+  if (splits > kblocks) splits = kblocks;
+  if (splits < 1) splits = 1;
+  call.splits = (int)splits;
+  return conv_gemm(call, s);
+}
+
+int conv_wgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* x, int64_t B, float* grad, cudaStream_t s) {
+  const Conv& c = m->convs[ci];
+  return conv_wgrad_ex(c, dy, c.cin == 3 ? m->stem_cols : x, B, grad + c.w_off, s);
+}
+
+}  // namespace
+
+namespace dbs {
+
+int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const float* x_base, const int32_t* y_base,
+                   const int64_t* d_iter, int64_t B, float* grad, float* loss, cudaStream_t s) {
+  DBS_REQUIRE(m && wb && pf && x_base && y_base && grad, DBS_ERR_ARGUMENT, "resnet: null argument");
+  DBS_REQUIRE(B >= 1 && B <= m->max_b, DBS_ERR_ARGUMENT, "resnet: batch %lld outside [1, %lld]", (long long)B,
+              (long long)m->max_b);
+  int st;
+  DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
+  // ---------------- forward ----------------
+  im2col_stem_kernel<<<grid_for(B * 1024, 256), 256, 0, s>>>(x_base, d_iter, B, m->stem_cols);
+  DBS_LAUNCH_CHECK();
+  if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
+  if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
+  const uint16_t* x = m->a[m->stem];
+  std::vector<const uint16_t*> blk_in(m->blocks.size());
+  for (size_t i = 0; i < m->blocks.size(); i++) {
+    const Block& b = m->blocks[i];
+    blk_in[i] = x;
+    if ((st = conv_fwd(m, b.c1, x, wb, B, s))) return st;
+    if ((st = bn_apply(m, b.c1, pf, nullptr, -1, 1, B, m->a[b.c1], s))) return st;
+    if ((st = conv_fwd(m, b.c2, m->a[b.c1], wb, B, s))) return st;
+    if (b.ds >= 0) {
+      if ((st = conv_fwd(m, b.ds, x, wb, B, s))) return st;
+    }
+    if ((st = bn_apply(m, b.c2, pf, b.ds >= 0 ? nullptr : x, b.ds, 1, B, m->blk_out[i], s))) return st;
+    x = m->blk_out[i];
+  }
+  // ---------------- head ----------------
+  uint16_t* gcur = m->g0;  // gradient w.r.t. the current block output
+  head_kernel<<<(unsigned)B, 256, 0, s>>>(x, pf + m->fc_w, pf + m->fc_b, y_base, d_iter, B, m->classes, m->feat,
+                                          m->dlog, m->loss_per, gcur);
+  DBS_LAUNCH_CHECK();
+  head_wgrad_kernel<<<(m->classes * 512 + 255) / 256, 256, 0, s>>>(m->feat, m->dlog, m->loss_per, B, m->classes,
+                                                                    grad + m->fc_w, grad + m->fc_b,
+                                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr);
+  DBS_LAUNCH_CHECK();
+  // ---------------- backward through the blocks ----------------
+  uint16_t* bufs[3] = {m->g1, m->g2, m->g3};
+  for (int i = (int)m->blocks.size() - 1; i >= 0; i--) {
+    const Block& b = m->blocks[i];
+    const uint16_t* out = m->blk_out[i];
+    // gradient w.r.t. the block input accumulates in gx (shortcut path first)
+    uint16_t* gx = bufs[0];
+    uint16_t* dy2 = bufs[1];
+    uint16_t* tmp = bufs[2];
+    // BN2 backward with the output ReLU mask; masked gradient g -> gx (identity) or tmp (ds)
+    if ((st = bn_bwd(m, b.c2, pf, grad, gcur, out, B, dy2, b.ds >= 0 ? tmp : gx, s))) return st;
+    if (b.ds >= 0) {
+      // BN_ds backward on the same masked gradient, dgrad of the 1x1 stride-2 conv -> gx
+      uint16_t* dyd = gcur;  // gcur is free once tmp holds the masked gradient
+      if ((st = bn_bwd(m, b.ds, pf, grad, tmp, nullptr, B, dyd, nullptr, s))) return st;
+      if ((st = conv_wgrad(m, b.ds, dyd, blk_in[i], B, grad, s))) return st;
+      if ((st = conv_dgrad(m, b.ds, dyd, wb, B, gx, 0, s))) return st;
+    }
+    // conv2: wgrad (input a1) and dgrad -> da1 (tmp)
+    if ((st = conv_wgrad(m, b.c2, dy2, m->a[b.c1], B, grad, s))) return st;
+    if ((st = conv_dgrad(m, b.c2, dy2, wb, B, tmp, 0, s))) return st;
+    // BN1 backward with the ReLU mask of a1 -> dy1 (dy2 buffer is free now)
+    uint16_t* dy1 = dy2;
+    if ((st = bn_bwd(m, b.c1, pf, grad, tmp, m->a[b.c1], B, dy1, nullptr, s))) return st;
+    if ((st = conv_wgrad(m, b.c1, dy1, blk_in[i], B, grad, s))) return st;
+    if ((st = conv_dgrad(m, b.c1, dy1, wb, B, gx, 1, s))) return st;  // accumulate onto the shortcut gradient
+    // rotate: gx becomes the next gcur
+    uint16_t* old = gcur;
+    gcur = gx;
+    bufs[0] = old;
+  }
+  // stem: BN backward with its ReLU mask, then the weight gradient only
+  if ((st = bn_bwd(m, m->stem, pf, grad, gcur, m->a[m->stem], B, bufs[1], nullptr, s))) return st;
+  if ((st = conv_wgrad(m, m->stem, bufs[1], nullptr, B, grad, s))) return st;
+  return DBS_OK;
+}
+
+int resnet_param_count(const dbs_resnet* m) { return (int)m->P; }
+
+int iter_increment(int64_t* d_iter, cudaStream_t s) {
+  iter_inc_kernel<<<1, 1, 0, s>>>(d_iter);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+}  // namespace dbs
+
+extern "C" int dbs_resnet_create(int64_t max_batch, int32_t classes, dbs_resnet** out) {
+  DBS_REQUIRE(out && max_batch > 0 && classes >= 2 && classes <= 16, DBS_ERR_ARGUMENT,
+              "resnet_create: need max_batch > 0 and 2 <= classes <= 16");
+  dbs_resnet* m = new dbs_resnet();
+  m->max_b = max_batch;
+  m->classes = classes;
+  build_layers(m);
+  int st = alloc_all(m);
+  if (st) {
+    dbs_resnet_destroy(m);
+    return st;
+  }
+  *out = m;
+  return DBS_OK;
+}
+
+extern "C" int dbs_resnet_destroy(dbs_resnet* m) {
+  if (!m) return DBS_OK;
+  cudaFree(m->stem_cols);
+  for (auto p : m->y) cudaFree(p);
+  for (auto p : m->a) cudaFree(p);
+  for (auto p : m->blk_out) cudaFree(p);
+  for (auto p : m->mean) cudaFree(p);
+  for (auto p : m->invstd) cudaFree(p);
+  cudaFree(m->sum_part);
+  cudaFree(m->sq_part);
+  cudaFree(m->g0);
+  cudaFree(m->g1);
+  cudaFree(m->g2);
+  cudaFree(m->g3);
+  cudaFree(m->dil);
+  cudaFree(m->wflip);
+  cudaFree(m->feat);
+  cudaFree(m->dlog);
+  cudaFree(m->loss_per);
+  cudaFree(m->loss_scratch);
+  delete m;
+  return DBS_OK;
+}
+
+extern "C" int dbs_resnet_param_count(const dbs_resnet* m, int64_t* P) {
+  DBS_REQUIRE(m && P, DBS_ERR_ARGUMENT, "resnet_param_count: null");
+  *P = m->P;
+  return DBS_OK;
+}
+
+extern "C" int dbs_resnet_param_table(const dbs_resnet* m, int64_t* off, int64_t* len, int32_t* kind,
+                                      int32_t capacity, int32_t* count) {
+  DBS_REQUIRE(m && count, DBS_ERR_ARGUMENT, "resnet_param_table: null");
+  *count = (int32_t)m->t_off.size();
+  DBS_REQUIRE(capacity >= *count && off && len && kind, DBS_ERR_ARGUMENT, "resnet_param_table: capacity %d < %d",
+              capacity, *count);
+  for (size_t i = 0; i < m->t_off.size(); i++) {
+    off[i] = m->t_off[i];
+    len[i] = m->t_len[i];
+    kind[i] = m->t_kind[i];
+  }
+  return DBS_OK;
+}
+
+extern "C" int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, const float* d_params,
+                                           const float* d_x, const int32_t* d_labels, int64_t batch,
+                                           const int64_t* d_iter, float* d_grad, float* d_loss, void* stream) {
+  return resnet_fwd_bwd(m, d_params_bf16, d_params, d_x, d_labels, d_iter, batch, d_grad, d_loss, as_stream(stream));
+}
+
+// ---- standalone convolution entry points (unit tests / other models) ----
+static Conv make_conv(int N, int H, int W, int Cin, int Cout, int k, int stride, int pad) {
+  (void)N;
+  Conv c{};
+  c.cin = Cin;
+  c.cout = Cout;
+  c.k = k;
+  c.stride = stride;
+  c.pad = pad;
+  c.H = H;
+  c.W = W;
+  c.OH = (H + 2 * pad - k) / stride + 1;
+  c.OW = (W + 2 * pad - k) / stride + 1;
+  return c;
+}
+
+extern "C" int dbs_dev_conv2d_fwd(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
+                                  int32_t Cout, int32_t k, int32_t stride, int32_t pad, void* d_y, void* stream) {
+  DBS_REQUIRE(Cin % 64 == 0 && Cout % 8 == 0, DBS_ERR_ARGUMENT, "conv2d_fwd: Cin %% 64 and Cout %% 8 required");
+  const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
+  ConvCall call{};
+  call.M = (int64_t)N * c.OH * c.OW;
+  call.N = Cout;
+  call.K = (int64_t)k * k * Cin;
+  call.a_mode = 2;
+  call.a = d_x;
+  call.ta = nhwc(N, H, W, Cin);
+  call.ga = ConvGeom{k, k, Cin / 64, stride, pad, c.OH, c.OW, Cin};
+  call.b_mode = 0;
+  call.b = d_w;
+  call.ldb = call.K;
+  call.epi = DBS_EPI_BF16;
+  call.d = d_y;
+  call.ldd = Cout;
+  return conv_gemm(call, as_stream(stream));
+}
+
+extern "C" int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
+                                    int32_t Cout, int32_t k, int32_t stride, int32_t pad, void* d_dx, void* d_scratch,
+                                    void* stream) {
+  DBS_REQUIRE(Cin % 8 == 0 && Cout % 64 == 0 && (stride == 1 || stride == 2) && pad == k / 2, DBS_ERR_ARGUMENT,
+              "conv2d_dgrad: Cout %% 64, stride 1/2, same padding required");
+  const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
+  uint16_t* wflip = static_cast<uint16_t*>(d_scratch);
+  uint16_t* dil = wflip + (((int64_t)Cout * k * k * Cin + 63) & ~int64_t(63));
+  return conv_dgrad_ex(c, static_cast<const uint16_t*>(d_dy), static_cast<const uint16_t*>(d_w), N,
+                       static_cast<uint16_t*>(d_dx), 0, wflip, dil, as_stream(stream));
+}
+
+extern "C" int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                                    int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw, void* stream) {
+  DBS_REQUIRE(Cin % 64 == 0 && Cout % 8 == 0, DBS_ERR_ARGUMENT, "conv2d_wgrad: Cin %% 64 required");
+  const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
+  return conv_wgrad_ex(c, static_cast<const uint16_t*>(d_dy), static_cast<const uint16_t*>(d_x), N, d_dw,
+                       as_stream(stream));
+}

@@ -1,0 +1,179 @@
+"""ResNet-18 (CIFAR variant) -- the named model of configs 3/4 -- on tcgen05.
+
+Host side of csrc/resnet.cu: the flat parameter layout (queried from the
+library's parameter table, torchvision order), host initialisation
+(kaiming-normal fan-out for convolutions, BN gamma=1 beta=0, PyTorch-default
+uniform for the classifier), conversion to / from PyTorch OIHW tensors for the
+parity tests, and per-worker activation scratch.
+
+Data: synthetic CIFAR-shaped samples, fp32 [D][3][32][32] rows, labels 0..9
+(SURVEY.md 8d, C3/C4 inputs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+
+KIND_CONV, KIND_BN_G, KIND_BN_B, KIND_FC_W, KIND_FC_B = 0, 1, 2, 3, 4
+STEM_K = 32
+
+
+class ResnetLayout:
+    """Offsets of every parameter tensor in the flat vector (torchvision order)."""
+
+    _cache = {}
+
+    def __init__(self, classes: int = 10):
+        key = classes
+        if key not in ResnetLayout._cache:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().dbs_resnet_create(1, classes, ctypes.byref(h)), "resnet_create")
+            try:
+                P = ctypes.c_int64()
+                _lib.check(_lib.lib().dbs_resnet_param_count(h, ctypes.byref(P)), "resnet_param_count")
+                cap = 256
+                off = (ctypes.c_int64 * cap)()
+                ln = (ctypes.c_int64 * cap)()
+                kd = (ctypes.c_int32 * cap)()
+                cnt = ctypes.c_int32()
+                _lib.check(_lib.lib().dbs_resnet_param_table(h, off, ln, kd, cap, ctypes.byref(cnt)), "param_table")
+                ResnetLayout._cache[key] = (P.value, [(off[i], ln[i], kd[i]) for i in range(cnt.value)])
+            finally:
+                _lib.lib().dbs_resnet_destroy(h)
+        self.P, self.table = ResnetLayout._cache[key]
+        self.classes = classes
+        self.shapes = self._shapes()
+
+    def _shapes(self):
+        """PyTorch (OIHW) shape of each table entry, in torchvision order."""
+        shapes = []
+        convs = [(3, 64, 3)]
+        cin = 64
+        for L, w in enumerate((64, 128, 256, 512)):
+            for b in range(2):
+                stride = 2 if (L > 0 and b == 0) else 1
+                convs.append((cin, w, 3))
+                convs.append((w, w, 3))
+                if stride != 1 or cin != w:
+                    convs.append((cin, w, 1))
+                cin = w
+        for ci, co, k in convs:
+            shapes += [(co, ci, k, k), (co,), (co,)]
+        shapes += [(self.classes, 512), (self.classes,)]
+        assert len(shapes) == len(self.table), (len(shapes), len(self.table))
+        return shapes
+
+    @property
+    def n_weights(self) -> int:
+        return int(sum(int(np.prod(s)) for s in self.shapes))
+
+    def pack(self, tensors) -> np.ndarray:
+        """PyTorch-layout arrays (torchvision order) -> flat device layout (fp32)."""
+        flat = np.zeros(self.P, dtype=np.float32)
+        for (off, ln, kind), shp, t in zip(self.table, self.shapes, tensors):
+            a = np.asarray(t, dtype=np.float32).reshape(shp)
+            if kind == KIND_CONV:
+                w = a.transpose(0, 2, 3, 1)  # OIHW -> OHWI (c fastest)
+                if shp[1] == 3:  # stem: [64][27] padded to [64][32]
+                    w2 = np.zeros((shp[0], STEM_K), dtype=np.float32)
+                    w2[:, :27] = w.reshape(shp[0], 27)
+                    w = w2
+                flat[off:off + ln] = w.reshape(-1)
+            else:
+                flat[off:off + ln] = a.reshape(-1)
+        return flat
+
+    def unpack(self, flat) -> list:
+        """Flat device layout -> PyTorch-layout arrays (torchvision order)."""
+        flat = np.asarray(flat).reshape(-1)
+        out = []
+        for (off, ln, kind), shp in zip(self.table, self.shapes):
+            v = flat[off:off + ln]
+            if kind == KIND_CONV:
+                if shp[1] == 3:
+                    v = v.reshape(shp[0], STEM_K)[:, :27]
+                out.append(v.reshape(shp[0], shp[2], shp[3], shp[1]).transpose(0, 3, 1, 2).copy())
+            else:
+                out.append(v.reshape(shp).copy())
+        return out
+
+
+def init_params(classes: int = 10, seed: int = 0) -> list:
+    """Host initialisation in torchvision order (kaiming fan-out / BN 1, 0 / FC uniform)."""
+    rng = np.random.default_rng(seed)
+    L = ResnetLayout(classes)
+    out = []
+    for shp, (_, _, kind) in zip(L.shapes, L.table):
+        if kind == KIND_CONV:
+            fan_out = shp[0] * shp[2] * shp[3]
+            out.append(rng.normal(0.0, math.sqrt(2.0 / fan_out), shp).astype(np.float32))
+        elif kind == KIND_BN_G:
+            out.append(np.ones(shp, dtype=np.float32))
+        elif kind == KIND_BN_B:
+            out.append(np.zeros(shp, dtype=np.float32))
+        else:
+            bound = 1.0 / math.sqrt(512)
+            out.append(rng.uniform(-bound, bound, shp).astype(np.float32))
+    return out
+
+
+def synthetic_cifar(n_samples=50000, classes=10, seed=0):
+    """C3 inputs: fp32 [D][3][32][32] ~ N(0,1), labels integers(0, classes)."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n_samples, 3, 32, 32), dtype=np.float32)
+    y = rng.integers(0, classes, size=n_samples).astype(np.int32)
+    return X, y
+
+
+class ResnetModel:
+    """Device parameters (fp32 master, bf16 shadow, momentum) of one replica."""
+
+    def __init__(self, classes=10, seed=0, device=None, params=None):
+        import torch
+
+        _lib.require_device()
+        self.layout = L = ResnetLayout(classes)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        tensors = init_params(classes, seed) if params is None else params
+        self.params = torch.as_tensor(L.pack(tensors), device=self.device)
+        self.params_bf16 = self.params.to(torch.bfloat16)
+        self.velocity = torch.zeros_like(self.params)
+
+    @property
+    def P(self) -> int:
+        return self.layout.P
+
+    def host_tensors(self) -> list:
+        return self.layout.unpack(self.params.cpu().numpy())
+
+
+class ResnetScratch:
+    """Per-worker activation scratch (dbs_resnet) sized for the largest batch."""
+
+    def __init__(self, max_batch: int, classes: int = 10):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().dbs_resnet_create(int(max_batch), classes, ctypes.byref(h)), "resnet_create")
+        self.handle = h
+        self.max_batch = int(max_batch)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().dbs_resnet_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def forward_backward(model: ResnetModel, scratch: ResnetScratch, x, labels, grad, loss, stream=None, d_iter=None):
+    """One worker's batch: flat fp32 gradient of the batch-mean cross-entropy."""
+    b = int(labels.shape[0]) if d_iter is None else int(scratch.max_batch)
+    st = _lib.lib().dbs_resnet_forward_backward(
+        scratch.handle, model.params_bf16.data_ptr(), model.params.data_ptr(), x.data_ptr(), labels.data_ptr(), b,
+        d_iter.data_ptr() if d_iter is not None else None, grad.data_ptr(), loss.data_ptr() if loss is not None else None,
+        _lib.stream_handle(stream))
+    _lib.check(st, "resnet_forward_backward")

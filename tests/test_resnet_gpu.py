@@ -1,0 +1,164 @@
+"""ResNet-18 on tcgen05 implicit-GEMM convolutions vs plain PyTorch fp32.
+
+Unit level: forward / input-gradient / weight-gradient of every conv shape of
+the network against torch.nn.functional.conv2d on the same bf16-rounded
+operands (fp32 accumulation both sides; tolerance 1e-2 relative to the
+operand magnitude).  Network level: loss and per-tensor gradients of the whole
+network (local BatchNorm, bf16 activations) against torch autograd in fp32:
+loss within 2%, every large gradient tensor with cosine similarity >= 0.98 and
+relative L2 error <= 0.2 (bf16 activations through 20 layers)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # N, H, Cin, Cout, k, stride
+    (4, 32, 64, 64, 3, 1),
+    (4, 32, 64, 128, 3, 2),
+    (4, 32, 64, 128, 1, 2),
+    (4, 16, 128, 128, 3, 1),
+    (8, 16, 128, 256, 3, 2),
+    (8, 8, 256, 512, 3, 2),
+    (16, 4, 512, 512, 3, 1),
+    (3, 8, 256, 256, 3, 1),
+]
+
+
+def _conv_ref(torch, x_nhwc, w_ohwi, stride, pad):
+    x = x_nhwc.float().permute(0, 3, 1, 2)
+    w = w_ohwi.float().permute(0, 3, 1, 2)
+    return torch.nn.functional.conv2d(x, w, stride=stride, padding=pad)
+
+
+def _close(torch, got, want, scale):
+    err = (got.float() - want.float()).abs().max().item()
+    assert err <= 1e-2 * scale + 1e-3, (err, scale)
+
+
+@pytest.mark.parametrize("N,H,Cin,Cout,k,stride", SHAPES)
+def test_conv_fwd_dgrad_wgrad(dev, N, H, Cin, Cout, k, stride):
+    import torch
+
+    from paper_2007_11831_b200 import _lib
+
+    pad = k // 2
+    g = torch.Generator(device=dev).manual_seed(N * H + Cin + k)
+    x = torch.randn(N, H, H, Cin, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(Cout, k, k, Cin, device=dev, generator=g) / (k * k * Cin) ** 0.5).to(torch.bfloat16)
+    OH = (H + 2 * pad - k) // stride + 1
+    s = _lib.stream_handle()
+    L = _lib.lib()
+    # forward
+    y = torch.empty(N, OH, OH, Cout, dtype=torch.bfloat16, device=dev)
+    assert L.dbs_dev_conv2d_fwd(x.data_ptr(), N, H, H, Cin, w.data_ptr(), Cout, k, stride, pad, y.data_ptr(), s) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    ref = _conv_ref(torch, x, w, stride, pad).permute(0, 2, 3, 1)
+    _close(torch, y, ref, ref.abs().max().item())
+    # input gradient
+    xr = x.float().permute(0, 3, 1, 2).requires_grad_(True)
+    yr = torch.nn.functional.conv2d(xr, w.float().permute(0, 3, 1, 2), stride=stride, padding=pad)
+    dy = torch.randn(N, OH, OH, Cout, device=dev, generator=g).to(torch.bfloat16)
+    yr.backward(dy.float().permute(0, 3, 1, 2))
+    dx = torch.empty(N, H, H, Cin, dtype=torch.bfloat16, device=dev)
+    scratch = torch.empty(2 * (Cout * k * k * Cin + 64) + 8 * N * H * H * Cout + 1024, dtype=torch.uint8, device=dev)
+    assert L.dbs_dev_conv2d_dgrad(dy.data_ptr(), N, H, H, Cin, w.data_ptr(), Cout, k, stride, pad, dx.data_ptr(),
+                                  scratch.data_ptr(), s) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    want_dx = xr.grad.permute(0, 2, 3, 1)
+    _close(torch, dx, want_dx, want_dx.abs().max().item())
+    # weight gradient
+    wr = w.float().permute(0, 3, 1, 2).requires_grad_(True)
+    yr = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), wr, stride=stride, padding=pad)
+    yr.backward(dy.float().permute(0, 3, 1, 2))
+    dw = torch.zeros(Cout, k, k, Cin, dtype=torch.float32, device=dev)
+    assert L.dbs_dev_conv2d_wgrad(dy.data_ptr(), x.data_ptr(), N, H, H, Cin, Cout, k, stride, pad, dw.data_ptr(),
+                                  s) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    want_dw = wr.grad.permute(0, 2, 3, 1)
+    err = (dw - want_dw).abs().max().item()
+    assert err <= 1e-3 * want_dw.abs().max().item() + 1e-4, err
+
+
+def torch_resnet18(torch, tensors, classes=10):
+    """Reference ResNet-18 (CIFAR stem) as pure functional torch with the same tensors."""
+    import torch.nn.functional as F
+
+    it = iter([torch.as_tensor(t, device="cuda", dtype=torch.float32).requires_grad_(True) for t in tensors])
+    params = []
+
+    def nxt():
+        p = next(it)
+        params.append(p)
+        return p
+
+    def conv_bn(x, stride, pad, relu=True):
+        w, gm, bt = nxt(), nxt(), nxt()
+        y = F.conv2d(x, w, stride=stride, padding=pad)
+        y = F.batch_norm(y, None, None, gm, bt, training=True, eps=1e-5)
+        return F.relu(y) if relu else y
+
+    def build(x):
+        x = conv_bn(x, 1, 1)
+        cin = 64
+        for L, wdt in enumerate((64, 128, 256, 512)):
+            for b in range(2):
+                stride = 2 if (L > 0 and b == 0) else 1
+                h = conv_bn(x, stride, 1)
+                h = conv_bn(h, 1, 1, relu=False)
+                sc = conv_bn(x, stride, 0, relu=False) if (stride != 1 or cin != wdt) else x
+                x = F.relu(h + sc)
+                cin = wdt
+        feat = x.mean(dim=(2, 3))
+        wf, bf = nxt(), nxt()
+        return feat @ wf.t() + bf
+
+    return build, params
+
+
+def test_resnet_forward_backward_vs_torch(dev):
+    import torch
+
+    from paper_2007_11831_b200 import resnet
+
+    B = 32
+    model = resnet.ResnetModel(seed=1)
+    sc = resnet.ResnetScratch(64)
+    X, y = resnet.synthetic_cifar(B, seed=3)
+    x = torch.as_tensor(X, device=dev)
+    yl = torch.as_tensor(y, device=dev)
+    grad = torch.zeros(model.P, device=dev)
+    loss = torch.zeros(1, device=dev)
+    resnet.forward_backward(model, sc, x, yl, grad, loss)
+    torch.cuda.synchronize()
+    tensors = model.host_tensors()
+    build, params = torch_resnet18(torch, tensors)
+    xr = x.to(torch.bfloat16).float()  # the stem reads bf16-rounded pixels
+    logits = build(xr)
+    ref_loss = torch.nn.functional.cross_entropy(logits, yl.long())
+    ref_loss.backward()
+    assert float(loss) == pytest.approx(float(ref_loss), rel=2e-2)
+    got = model.layout.unpack(grad.cpu().numpy())
+    worst = []
+    for p, g in zip(params, got):
+        r = p.grad.detach().cpu().numpy().astype(np.float64)
+        g = g.astype(np.float64)
+        if r.size < 64:
+            continue
+        cos = float((r * g).sum() / (np.linalg.norm(r) * np.linalg.norm(g) + 1e-30))
+        rel = float(np.linalg.norm(g - r) / (np.linalg.norm(r) + 1e-30))
+        worst.append((cos, rel, r.shape))
+        assert cos >= 0.98 and rel <= 0.2, (r.shape, cos, rel)
+
+
+def test_param_layout_roundtrip(dev):
+    from paper_2007_11831_b200 import resnet
+
+    L = resnet.ResnetLayout()
+    assert L.n_weights == 11_173_962
+    t = resnet.init_params(seed=2)
+    back = L.unpack(L.pack(t))
+    for a, b in zip(t, back):
+        np.testing.assert_array_equal(a, b)
