@@ -6,13 +6,20 @@ controller), but `per_worker_gpu` is MEASURED -- per-worker compute seconds
 accumulated on the device from %globaltimer stamps around each worker's
 forward/backward -- and the epoch wall time is a CUDA-event interval.  The
 records are the reference's EpochStats (cluster.py:111-120), so
-cumulative_times / the report schema apply unchanged.
+cumulative_times and the report schema apply unchanged.
+
+Per epoch: controller plan -> device permutation of every span (sgdlab.py:
+372-374) -> coalesced repack of each worker's rows into its HBM shard -> T
+iterations of [every worker's forward/backward on its own stream || fused
+batch-weighted aggregation + momentum SGD].  For ResNet-18 one iteration is
+captured once per distinct plan as a CUDA graph (every kernel reads the
+iteration index from device memory) and replayed T times.
 
 Workers
-  * one process, W simulated workers (config 1): each worker is a CUDA stream,
-    optionally confined to its own SM partition with a green context;
-  * one process per GPU (torchrun): worker = rank, gradients combined by the
-    fused NVLink kernel of comm.py (see DistributedTrainer).
+  * one process, W simulated workers: each worker is a CUDA stream, confined
+    to its own SM partition with a green context when ``partition=True``;
+  * one process per GPU (torchrun): worker = rank (DistributedTrainer), the
+    update is the fused NVLink kernel of comm.py.
 
 Disturbance (DisturbanceEvent, cluster.py:25-56), realised on the device:
   * cost_multiplier m  -> a co-running spin kernel pins a fraction 1 - 1/m of
@@ -24,21 +31,17 @@ Disturbance (DisturbanceEvent, cluster.py:25-56), realised on the device:
 
 from __future__ import annotations
 
-import ctypes
-import math
-import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
 import numpy as np
 
 from . import _lib, cluster
-from .allocation import PartitionPlan
 from .cluster import EpochStats, StrategyConfig, WorkerProfile
-from .mlp import MlpModel, MlpScratch
 from .sgdlab import DeviceRng
 
 _MODE = {"uniform_average": 0, "batch_weighted": 1}
+MODEL_MLP, MODEL_RESNET18 = 0, 1
 
 
 @dataclass
@@ -50,7 +53,16 @@ class Worker:
     green: object = None
 
 
-def make_workers(n: int, partition: bool = True) -> list[Worker]:
+def _green_supported() -> bool:
+    try:
+        import torch
+
+        return bool(torch.cuda.green_contexts.SUPPORTED)
+    except Exception:
+        return False
+
+
+def make_workers(n: int, partition: bool = True) -> list:
     """W simulated workers on the current device; SM partitions via green contexts."""
     import torch
 
@@ -74,15 +86,6 @@ def make_workers(n: int, partition: bool = True) -> list[Worker]:
     return workers
 
 
-def _green_supported() -> bool:
-    try:
-        import torch
-
-        return bool(torch.cuda.green_contexts.SUPPORTED)
-    except Exception:
-        return False
-
-
 @dataclass
 class RunResult:
     stats: list
@@ -93,46 +96,87 @@ class RunResult:
 
 
 class SimulatedTrainer:
-    """W simulated workers of synchronous S-SGD on one GPU (config 1)."""
+    """W simulated workers of synchronous S-SGD on one GPU.
 
-    def __init__(self, X, y, n_workers: int, hidden: int = 256, classes: int = 10, seed: int = 0,
-                 partition: bool = True, params=None, max_batch: Optional[int] = None):
+    model = "mlp" (config 1: X fp32 [D][784]) or "resnet18" (configs 3/4:
+    X fp32 [D][3][32][32]).
+    """
+
+    def __init__(self, X, y, n_workers: int, model: str = "mlp", hidden: int = 256, classes: int = 10,
+                 seed: int = 0, partition: bool = True, params=None, max_batch: Optional[int] = None,
+                 graphs: Optional[bool] = None):
         import torch
 
         _lib.require_device()
         self.torch = torch
         self.dev = torch.device("cuda", torch.cuda.current_device())
-        self.X = torch.as_tensor(X, device=self.dev) if not isinstance(X, torch.Tensor) else X.to(self.dev)
-        self.y = torch.as_tensor(y, device=self.dev) if not isinstance(y, torch.Tensor) else y.to(self.dev)
-        self.X = self.X.to(torch.float32).contiguous()
-        self.y = self.y.to(torch.int32).contiguous()
-        self.D, self.in_dim = self.X.shape
+        X = X if isinstance(X, torch.Tensor) else torch.as_tensor(X)
+        y = y if isinstance(y, torch.Tensor) else torch.as_tensor(y)
+        self.X = X.to(self.dev, torch.float32).contiguous()
+        self.y = y.to(self.dev, torch.int32).contiguous()
+        self.D = int(self.X.shape[0])
+        self.row_elems = int(np.prod(self.X.shape[1:]))
         self.n = n_workers
-        self.model = MlpModel(self.in_dim, hidden, classes, seed, self.dev, params=params)
+        self.kind = MODEL_MLP if model == "mlp" else MODEL_RESNET18
+        if self.kind == MODEL_MLP:
+            from .mlp import MlpModel
+
+            self.model = MlpModel(self.row_elems, hidden, classes, seed, self.dev, params=params)
+        else:
+            from .resnet import ResnetModel
+
+            assert tuple(self.X.shape[1:]) == (3, 32, 32), "resnet18 expects CIFAR-shaped [D][3][32][32] rows"
+            self.model = ResnetModel(classes, seed, self.dev, params=params)
+        self.graphs = (self.kind == MODEL_RESNET18) if graphs is None else bool(graphs and self.kind == MODEL_RESNET18)
         self.workers = make_workers(n_workers, partition)
         self.max_batch = max_batch
         self.scratch = {}
-        self.grads = [torch.zeros(self.model.P, dtype=torch.float32, device=self.dev) for _ in range(n_workers)]
+        P = self.model.P
+        self.grads = [torch.zeros(P, dtype=torch.float32, device=self.dev) for _ in range(n_workers)]
         self.seconds = torch.zeros(n_workers, dtype=torch.float64, device=self.dev)
         self.stamps = [torch.zeros(2, dtype=torch.int64, device=self.dev) for _ in range(n_workers)]
         self.loss_scratch = torch.zeros(n_workers, dtype=torch.float32, device=self.dev)
         self.stop = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.d_iter = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.agg = torch.cuda.Stream()
         self.rng = None
+        # fixed-address shards (graph replays need stable pointers)
+        shard_dtype = torch.bfloat16 if self.kind == MODEL_MLP else torch.float32
+        self.shard_x = [torch.empty((self.D, self.row_elems), dtype=shard_dtype, device=self.dev) for _ in
+                        range(n_workers)]
+        self.shard_y = [torch.empty(self.D, dtype=torch.int32, device=self.dev) for _ in range(n_workers)]
+        self.loss_buf = torch.zeros((n_workers, self.D + 1), dtype=torch.float32, device=self.dev)
+        self._graph_cache = {}
+        self._primed = False
 
-    def _scratch(self, w: int, b: int) -> MlpScratch:
+    # -- helpers --------------------------------------------------------------
+    def _scratch(self, w: int, b: int):
         cur = self.scratch.get(w)
         if cur is None or cur.max_batch < b:
             cap = max(b, self.max_batch or 0)
-            cur = MlpScratch(self.model.layout, cap)
+            if self.kind == MODEL_MLP:
+                from .mlp import MlpScratch
+
+                cur = MlpScratch(self.model.layout, cap)
+            else:
+                from .resnet import ResnetScratch
+
+                cur = ResnetScratch(cap)
             self.scratch[w] = cur
+            self._graph_cache.clear()  # scratch pointers changed
         return cur
 
-    def _prime(self, slots, iters: int, mode: int):
-        """Run one throw-away iteration (scratch parameters) before a spin kernel
-        starts, so every kernel of the epoch is resident: a lazily loaded module
-        must never be needed while a spinning kernel owns SMs."""
-        if getattr(self, "_primed", False) or iters <= 0:
+    def _run_iters(self, slots, t0, t1, mode, lr, mom, params, vel, pb, skip, d_iter=None):
+        st = _lib.lib().dbs_run_iterations(slots, self.n, t0, t1, mode, float(lr), float(mom), params.data_ptr(),
+                                           vel.data_ptr(), pb.data_ptr(), int(skip), int(self.agg.cuda_stream),
+                                           d_iter.data_ptr() if d_iter is not None else None)
+        _lib.check(st, "run_iterations")
+
+    def _prime(self, slots, mode: int):
+        """One throw-away iteration on scratch parameters before the first spin
+        kernel or graph capture: every kernel of an iteration gets loaded (a lazily
+        loaded module must never be needed while a spinning kernel owns SMs)."""
+        if self._primed:
             return
         torch = self.torch
         p = self.model.params.clone()
@@ -145,18 +189,30 @@ class SimulatedTrainer:
         saved = [(slots[w].loss, slots[w].stamps, slots[w].seconds) for w in range(self.n)]
         st_scratch = torch.zeros(2 * self.n, dtype=torch.int64, device=self.dev)
         sec_scratch = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
+        it_scratch = torch.zeros(1, dtype=torch.int64, device=self.dev)
         for w in range(self.n):
-            # same kernel set as a real iteration (incl. the timing stamps), scratch outputs
             slots[w].loss = None
             slots[w].stamps = st_scratch[2 * w:].data_ptr()
             slots[w].seconds = sec_scratch.data_ptr()
-        _lib.check(_lib.lib().dbs_mlp_run_iterations(slots, self.n, 0, 1, mode, 0.0, 0.0, p.data_ptr(), v.data_ptr(),
-                                                      pb.data_ptr(), 0, int(self.agg.cuda_stream)), "prime")
+        self._run_iters(slots, 0, 1, mode, 0.0, 0.0, p, v, pb, 0, it_scratch if self.graphs else None)
         for w in range(self.n):
             slots[w].loss, slots[w].stamps, slots[w].seconds = saved[w]
         torch.cuda.synchronize()
         self._primed = True
 
+    def _graph(self, key, slots, mode, lr, mom, skip):
+        g = self._graph_cache.get(key)
+        if g is None:
+            torch = self.torch
+            g = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=self.agg):
+                self._run_iters(slots, 0, 1, mode, lr, mom, self.model.params, self.model.velocity,
+                                self.model.params_bf16, skip, self.d_iter)
+            self._graph_cache[key] = g
+        return g
+
+    # -- the epoch loop -----------------------------------------------------------
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
@@ -164,14 +220,11 @@ class SimulatedTrainer:
         torch = self.torch
         n, D = self.n, self.D
         self.rng = DeviceRng(seed, self.dev)
-        stats: list[EpochStats] = []
+        stats: list = []
         smoothed = None
-        losses = []
-        samples = 0
-        wall = 0.0
-        plans = []
+        losses, plans = [], []
+        samples, wall, done = 0, 0.0, 0
         mode = _MODE[aggregation]
-        done = 0
         for epoch in range(n_epochs):
             plan, smoothed = cluster.next_plan(config, epoch, n, D, stats[-1] if stats else None, smoothed)
             plans.append(plan)
@@ -180,45 +233,46 @@ class SimulatedTrainer:
             iters = cluster.iterations_for_plan(plan)
             if max_iters is not None:
                 iters = min(iters, max_iters - done)
-            # sample assignment: device permutation of every span (sgdlab.py:372-374)
+            # sample assignment (device) and the per-worker shard repack
             perm, _ = self.rng.permute_spans(spans)
-            # repartition gather: each worker's used rows, in epoch order, fp32 -> bf16
-            slots = (_lib.WorkerSlot * n)()
-            shards = []
             offs = np.cumsum([0] + [e - s for s, e in spans[:-1]])
-            loss_buf = torch.zeros((n, max(iters, 1)), dtype=torch.float32, device=self.dev)
             s_main = _lib.stream_handle()
+            slots = (_lib.WorkerSlot * n)()
             for w in range(n):
                 rows = iters * batches[w]
-                xs = torch.empty((max(rows, 1), self.in_dim), dtype=torch.bfloat16, device=self.dev)
-                ys = torch.empty(max(rows, 1), dtype=torch.int32, device=self.dev)
                 idx = perm[int(offs[w]):int(offs[w]) + rows]
+                xs, ys = self.shard_x[w], self.shard_y[w]
                 if rows:
-                    _lib.check(_lib.lib().dbs_dev_gather_rows_f32_bf16(self.X.data_ptr(), idx.data_ptr(), rows,
-                                                                        self.in_dim, xs.data_ptr(), s_main), "gather")
+                    if self.kind == MODEL_MLP:
+                        st = _lib.lib().dbs_dev_gather_rows_f32_bf16(self.X.data_ptr(), idx.data_ptr(), rows,
+                                                                     self.row_elems, xs.data_ptr(), s_main)
+                    else:
+                        st = _lib.lib().dbs_dev_gather_rows(self.X.data_ptr(), idx.data_ptr(), rows,
+                                                            self.row_elems * 4, xs.data_ptr(), s_main)
+                    _lib.check(st, "gather")
                     _lib.check(_lib.lib().dbs_dev_gather_i32(self.y.data_ptr(), idx.data_ptr(), rows, ys.data_ptr(),
                                                               s_main), "gather labels")
-                shards.append((xs, ys))
                 sc = self._scratch(w, batches[w])
                 sl = slots[w]
                 sl.model = sc.handle.value
+                sl.model_kind = self.kind
                 sl.stream = int(self.workers[w].stream.cuda_stream)
                 sl.x_shard = xs.data_ptr()
                 sl.y_shard = ys.data_ptr()
                 sl.batch = batches[w]
                 sl.grad = self.grads[w].data_ptr()
-                sl.loss = loss_buf[w].data_ptr() if record_loss else None
+                sl.loss = self.loss_buf[w].data_ptr() if record_loss else None
                 sl.loss_scratch = self.loss_scratch[w:].data_ptr()
                 sl.stamps = self.stamps[w].data_ptr()
                 sl.seconds = self.seconds.data_ptr()
                 sl.worker_index = w
                 sl.spin_ns, sl.spin_ctas = 0, 0
             self.seconds.zero_()
+            self.d_iter.zero_()
             _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 0, s_main), "set_flag")
             # disturbances of this epoch
-            spinning = []
-            if profiles is not None and any(p.active_disturbance(epoch) for p in profiles):
-                self._prime(slots, iters, mode)
+            spinning, spin_key = [], []
+            if profiles is not None:
                 for w, prof in enumerate(profiles):
                     ev = prof.active_disturbance(epoch)
                     if ev is None:
@@ -228,14 +282,24 @@ class SimulatedTrainer:
                         ctas = int(round(wk.sm_count * (1.0 - 1.0 / ev.cost_multiplier)))
                         ctas = max(0, min(ctas, wk.sm_count - 1))
                         if ctas:
-                            wk.spin_stream.wait_stream(torch.cuda.current_stream())
-                            _lib.check(_lib.lib().dbs_dev_spin_until(ctas, self.stop.data_ptr(),
-                                                                     int(wk.spin_stream.cuda_stream)), "spin")
-                            spinning.append(wk)
+                            spinning.append((wk, ctas))
                     elif ev.extra_epoch_seconds:
                         slots[w].spin_ns = int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
                         slots[w].spin_ctas = wk.sm_count
+                        spin_key.append((w, slots[w].spin_ns))
+            if iters > 0 and (spinning or self.graphs):
+                self._prime(slots, mode)
+            graph = None
+            if self.graphs and iters > 0:
+                key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
+                       bool(record_loss))
+                graph = self._graph(key, slots, mode, lr, momentum, skip_update)
+                self.d_iter.zero_()
             cur = torch.cuda.current_stream()
+            for wk, ctas in spinning:
+                wk.spin_stream.wait_stream(cur)
+                _lib.check(_lib.lib().dbs_dev_spin_until(ctas, self.stop.data_ptr(), int(wk.spin_stream.cuda_stream)),
+                           "spin")
             self.agg.wait_stream(cur)
             for wk in self.workers:
                 wk.stream.wait_stream(cur)
@@ -243,26 +307,27 @@ class SimulatedTrainer:
             end = torch.cuda.Event(enable_timing=True)
             start.record(self.agg)
             if iters > 0:
-                st = _lib.lib().dbs_mlp_run_iterations(
-                    slots, n, 0, iters, mode, float(lr), float(momentum), self.model.params.data_ptr(),
-                    self.model.velocity.data_ptr(), self.model.params_bf16.data_ptr(), int(skip_update),
-                    int(self.agg.cuda_stream))
-                _lib.check(st, "mlp_run_iterations")
+                if graph is not None:
+                    with torch.cuda.stream(self.agg):
+                        for _ in range(iters):
+                            graph.replay()
+                else:
+                    self._run_iters(slots, 0, iters, mode, lr, momentum, self.model.params, self.model.velocity,
+                                    self.model.params_bf16, skip_update)
             end.record(self.agg)
-            # stop the disturbance once the epoch's work is done (memset: no kernel launch)
+            # stop the disturbance once the epoch's work is done (copy engine, no kernel)
             _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 1, int(self.agg.cuda_stream)), "set_flag")
-            for wk in spinning:
+            for wk, _ in spinning:
                 self.agg.wait_stream(wk.spin_stream)
             cur.wait_stream(self.agg)
             torch.cuda.synchronize()
             ep_wall = start.elapsed_time(end) / 1e3
             secs = tuple(float(x) for x in self.seconds.cpu().tolist())
             slowest = max(secs) if secs else 0.0
-            stat = EpochStats(epoch=epoch, per_worker_gpu=secs, per_worker_wait=tuple(slowest - s for s in secs),
-                              sync_time=max(0.0, ep_wall - slowest), epoch_wall_time=ep_wall, plan=plan)
-            stats.append(stat)
+            stats.append(EpochStats(epoch=epoch, per_worker_gpu=secs, per_worker_wait=tuple(slowest - s for s in secs),
+                                    sync_time=max(0.0, ep_wall - slowest), epoch_wall_time=ep_wall, plan=plan))
             if record_loss and iters > 0:
-                lb = loss_buf[:, :iters].double().cpu().numpy()
+                lb = self.loss_buf[:, :iters].double().cpu().numpy()
                 bw = np.asarray(batches, dtype=np.float64)[:, None]
                 losses.append((lb * bw).sum(axis=0) / bw.sum())
             samples += iters * sum(batches)
