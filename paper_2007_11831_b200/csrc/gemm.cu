@@ -53,8 +53,8 @@ struct GemmParams {
   const float* bias;
   const uint16_t* aux;  // bf16 [M][ldd] for the ReLU-backward epilogue
   float* colsum_part;   // [ceil(M/32)][N] per-warp column sums of the stored values
-  float* sum_part;      // [ceil(M/32)][N] per-warp column sums of the accumulator
-  float* sq_part;       // [ceil(M/32)][N] per-warp column sums of accumulator^2
+  double* sum_part;     // [N] column sums of the accumulator (fp64 atomics, BN statistics)
+  double* sq_part;      // [N] column sums of accumulator^2
   ConvGeom ga, gb;      // implicit-GEMM geometry of A / B in conv mode
   int kb_per_split;     // K blocks per CTA along grid.z (split-K)
 };
@@ -332,15 +332,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane < cnt && group_live) p.colsum_part[g * p.N + n_base + lane] = s;
         }
         if (stats) {
+          // BN batch statistics: warp column sums -> CTA sums (smem) -> one fp64
+          // atomic per column and CTA into the [N] accumulators
+          __shared__ float red_s[4][32], red_q[4][32];
           const float s = warp_colsum(v, lane);
           float sq[32];
 #pragma unroll
           for (int j = 0; j < 32; j++) sq[j] = v[j] * v[j];
           const float q = warp_colsum(sq, lane);
-          if (lane < cnt && group_live) {
-            p.sum_part[g * p.N + n_base + lane] = s;
-            p.sq_part[g * p.N + n_base + lane] = q;
+          red_s[warp][lane] = s;
+          red_q[warp][lane] = q;
+          __syncthreads();
+          if (warp == 0 && lane < cnt) {
+            const double ts = (double)red_s[0][lane] + red_s[1][lane] + red_s[2][lane] + red_s[3][lane];
+            const double tq = (double)red_q[0][lane] + red_q[1][lane] + red_q[2][lane] + red_q[3][lane];
+            atomicAdd(p.sum_part + n_base + lane, ts);
+            atomicAdd(p.sq_part + n_base + lane, tq);
           }
+          __syncthreads();
         }
       }
     } else {

@@ -37,8 +37,8 @@ struct ConvCall {
   int64_t ldd;
   const float* bias;
   const uint16_t* aux;
-  float* sum_part;           // BN batch statistics partials (per 32-row group)
-  float* sq_part;
+  double* sum_part;          // BN batch statistics: [N] fp64 accumulators of sum / sum of squares
+  double* sq_part;
   int splits;                // split-K CTAs along grid.z (atomic epilogue)
   int bn_override;           // force the N tile (0 = auto)
 };

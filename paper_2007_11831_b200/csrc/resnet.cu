@@ -81,16 +81,15 @@ __global__ void im2col_stem_kernel(const float* __restrict__ x_base, const int64
   }
 }
 
-// BN batch statistics: partial sums over 32-row groups -> mean, 1/sqrt(var+eps)
-__global__ void bn_stats_kernel(const float* __restrict__ sum_part, const float* __restrict__ sq_part, int64_t groups,
-                                int C, int64_t M, float* __restrict__ mean, float* __restrict__ invstd) {
+// BN batch statistics: the conv epilogue's fp64 column sums -> mean,
+// 1/sqrt(var+eps); the accumulators are re-zeroed for the next convolution.
+__global__ void bn_stats_kernel(double* __restrict__ sum_acc, double* __restrict__ sq_acc, int C, int64_t M,
+                                float* __restrict__ mean, float* __restrict__ invstd) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
-  double s = 0.0, q = 0.0;
-  for (int64_t g = 0; g < groups; g++) {
-    s += (double)sum_part[g * C + c];
-    q += (double)sq_part[g * C + c];
-  }
+  const double s = sum_acc[c], q = sq_acc[c];
+  sum_acc[c] = 0.0;
+  sq_acc[c] = 0.0;
   const double mu = s / (double)M;
   double var = q / (double)M - mu * mu;
   if (var < 0.0) var = 0.0;
@@ -374,8 +373,8 @@ struct dbs_resnet {
   std::vector<uint16_t*> y, a;             // per conv: pre-BN output, post-BN(+ReLU) output
   std::vector<uint16_t*> blk_out;          // per block output (post residual ReLU)
   std::vector<float*> mean, invstd;        // per conv
-  float* sum_part = nullptr;               // [max groups][512]
-  float* sq_part = nullptr;
+  double* sum_part = nullptr;              // [512] fp64 BN sum accumulators (kept zeroed)
+  double* sq_part = nullptr;               // [512] sum of squares
   uint16_t* g0 = nullptr;                  // gradient ping-pong buffers (largest activation)
   uint16_t* g1 = nullptr;
   uint16_t* g2 = nullptr;
@@ -473,9 +472,10 @@ int alloc_all(dbs_resnet* m) {
     A((void**)&o, (size_t)B * c.OH * c.OW * c.cout * 2);
     m->blk_out.push_back(o);
   }
-  const int64_t groups = (B * 1024 + 31) / 32 + 8;
-  A((void**)&m->sum_part, (size_t)groups * 512 * 4);
-  A((void**)&m->sq_part, (size_t)groups * 512 * 4);
+  A((void**)&m->sum_part, 512 * sizeof(double));
+  A((void**)&m->sq_part, 512 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(m->sum_part, 0, 512 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(m->sq_part, 0, 512 * sizeof(double));
   A((void**)&m->g0, max_act * 2);
   A((void**)&m->g1, max_act * 2);
   A((void**)&m->g2, max_act * 2);
@@ -525,8 +525,7 @@ int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64
   }
   int st = conv_gemm(call, s);
   if (st) return st;
-  const int64_t groups = (M + 31) / 32;
-  bn_stats_kernel<<<(c.cout + 127) / 128, 128, 0, s>>>(m->sum_part, m->sq_part, groups, c.cout, M, m->mean[ci],
+  bn_stats_kernel<<<(c.cout + 127) / 128, 128, 0, s>>>(m->sum_part, m->sq_part, c.cout, M, m->mean[ci],
                                                         m->invstd[ci]);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
