@@ -1,21 +1,25 @@
 #!/usr/bin/env python
 """DBS benchmark: samples/s and epoch time under skewed load, DBS vs fixed batch.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload resnet18|mlp]
 
-One JSON line on rank 0 (contract in the task statement / DESIGN.md):
-  * a "step" is one synchronous S-SGD EPOCH of the hot path (the DBS re-plan
-    granularity): device controller -> device permutation -> shard repack ->
+Prints ONE JSON line on rank 0.  Definitions ("Measurement"):
+  * a "step" is one synchronous S-SGD EPOCH of the hot path: device controller
+    re-plan -> device permutation of every span -> coalesced shard repack ->
     T iterations of per-worker variable-batch forward/backward on tcgen05 +
-    fused batch-weighted aggregation / momentum SGD;
-  * value = samples processed by all workers / device time of the K timed
-    epochs (max over ranks); inputs resident in HBM;
+    fused batch-weighted aggregation / momentum SGD (CUDA-graph replays);
+  * value = samples processed by all workers in the K timed epochs / device
+    time of those K whole epochs (CUDA events, inputs resident in HBM);
   * e2e = the same through the public trainer API with the dataset uploaded
-    from pinned host memory every epoch and the loss read back;
-  * roofline of the dominant kernel, cpu_baseline (the numpy oracle of the same
-    loop on the host cores), clocks sampled during the timed region.
-N = 1 runs the config-1 shape with 3 simulated workers on SM-partitioned green
-contexts; under torchrun each rank is one worker (weak scaling).
+    from pinned host memory every epoch and the losses read back;
+  * roofline of the dominant kernel (the tcgen05 implicit-GEMM convolution),
+    cpu_baseline (the reference loop with a CPU model on the host cores),
+    clocks sampled in-process with NVML during the timed region.
+Workload at N=1 (config 3, BASELINE.json): ResNet-18 on synthetic CIFAR-shaped
+data, 4 simulated workers sharing the GPU, B=512 (128/worker fixed), worker 0
+runs on a device 2x slower (cost_multiplier 2: its step is extended by its own
+forward/backward time).  Under torchrun each rank runs the same 4-worker
+simulation on its own GPU (weak scaling, no data-path collective across GPUs).
 """
 
 from __future__ import annotations
@@ -34,6 +38,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+METRIC = "DBS samples/sec & epoch time under skewed load vs fixed batch"
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -41,17 +47,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="mlp", choices=["mlp"])
+    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "mlp"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
 def load_peaks():
@@ -64,249 +67,273 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clock + throttle reasons sampled in-process (NVML) DURING the timed region."""
 
     def __init__(self, index=0):
-        self.index = index
-        self.samples = []
+        self.index, self.samples = index, []
         self._stop = threading.Event()
         self._t = None
 
     def start(self):
-        try:  # in-process NVML: no nvidia-smi processes contending for the driver
+        try:
             import pynvml
 
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            names = [("hw_slowdown", pynvml.nvmlClocksEventReasonHwSlowdown),
+                     ("hw_thermal_slowdown", pynvml.nvmlClocksEventReasonHwThermalSlowdown),
+                     ("sw_thermal_slowdown", pynvml.nvmlClocksEventReasonSwThermalSlowdown),
+                     ("sw_power_cap", pynvml.nvmlClocksEventReasonSwPowerCap)]
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
-            def run_nvml():
-                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            def run():
                 while not self._stop.is_set():
                     try:
                         sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                         r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        self.samples.append([str(sm), str(mx), "0"] +
-                                            ["Active" if r & b else "Not Active" for b in bits])
+                        self.samples.append((sm, [n for n, b in names if r & b]))
                     except Exception:
                         pass
                     self._stop.wait(0.25)
 
-            self._t = threading.Thread(target=run_nvml, daemon=True)
+            self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
-            return
-        except Exception:
-            pass
-
-        def run():
-            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        except Exception as exc:  # no NVML: record why
+            self.error = repr(exc)
 
     def stop(self):
         self._stop.set()
         if self._t:
-            self._t.join(timeout=6)
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
-                          and not s[3 + i].startswith("Not")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            self._t.join(timeout=5)
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({r for _, rs in self.samples for r in rs})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": getattr(self, "max_mhz", None),
+                "reasons": reasons, "samples": len(sm)}
 
 
 # ---------------------------------------------------------------------------
-# workload: config 1 (3 workers, MLP 784-256-10, synthetic MNIST, DBS vs fixed)
+# workloads
 # ---------------------------------------------------------------------------
-D_SAMPLES, IN_DIM, HIDDEN, CLASSES = 60000, 784, 256, 10
-PER_WORKER = 128
-LR, MOM = 0.05, 0.5
+WL = {
+    "resnet18": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0,
+                     desc="C3: ResNet-18 (CIFAR stem), synthetic CIFAR-10-shaped 50000x3x32x32 fp32 (bf16 tensor-core "
+                          "operands), 4 simulated workers sharing the GPU, B=512 (128/worker fixed), step = 1 epoch "
+                          "(97 iterations)"),
+    "mlp": dict(D=60000, workers=3, per_worker=128, lr=0.05, mom=0.5, mult=2.0,
+                desc="C1: MLP 784-256-10, synthetic MNIST 60000x784, 3 simulated workers, B=384, step = 1 epoch"),
+}
 
 
-def disturbance_profiles(n):
+def profiles(n, mult):
     from paper_2007_11831_b200 import cluster
 
-    # worker 0 runs beside a co-running job that pins 3/4 of its SM partition
-    # (cost multiplier 4); the others are clean.  Persistent, as SURVEY A.6 advises.
-    prof = [cluster.WorkerProfile(0, 1.0, disturbances=(cluster.DisturbanceEvent(0, cost_multiplier=4.0),))]
-    prof += [cluster.WorkerProfile(i, 1.0) for i in range(1, n)]
-    return prof
+    # a persistent slow worker (SURVEY.md A.6: rotating disturbances defeat the
+    # one-epoch-lag estimator; persistent ones are what DBS absorbs)
+    prof = [cluster.WorkerProfile(0, 1.0, disturbances=(cluster.DisturbanceEvent(0, cost_multiplier=mult),))]
+    return prof + [cluster.WorkerProfile(i, 1.0) for i in range(1, n)]
 
 
-def run_ours(args, rank, world):
+def make_trainer(wl, rank):
+    import torch
+
+    from paper_2007_11831_b200.trainer import SimulatedTrainer
+
+    w = WL[wl]
+    if wl == "resnet18":
+        from paper_2007_11831_b200.resnet import synthetic_cifar
+
+        X, y = synthetic_cifar(w["D"], seed=rank)
+        return SimulatedTrainer(X, y, n_workers=w["workers"], model="resnet18", seed=0,
+                                max_batch=w["workers"] * w["per_worker"]), (X, y)
+    from paper_2007_11831_b200.mlp import synthetic_mnist
+
+    X, y = synthetic_mnist(w["D"], seed=rank)
+    return SimulatedTrainer(X, y, n_workers=w["workers"], model="mlp", seed=0,
+                            max_batch=w["workers"] * w["per_worker"]), (X, y)
+
+
+def run_strategy(tr, wl, kind, args):
     import torch
 
     from paper_2007_11831_b200 import cluster
-    from paper_2007_11831_b200.mlp import synthetic_mnist
-    from paper_2007_11831_b200.trainer import SimulatedTrainer
 
-    torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", "0")))
-    n_workers = 3
-    X, y = synthetic_mnist(D_SAMPLES, IN_DIM, CLASSES, seed=rank)
-    tr = SimulatedTrainer(X, y, n_workers=n_workers, hidden=HIDDEN, classes=CLASSES, seed=0, partition=True,
-                          max_batch=4 * PER_WORKER)
-    B = n_workers * PER_WORKER
-    prof = disturbance_profiles(n_workers)
-    results = {}
-    for kind in ("fixed_ssgd", "dbs"):
-        cfg = cluster.StrategyConfig(kind, B)
-        # warm-up epochs (DBS converges its plan here), then K timed epochs
-        tr.run(cfg, n_epochs=args.warmup, lr=LR, momentum=MOM, profiles=prof, record_loss=False)
-        torch.cuda.synchronize()
-        sampler = ClockSampler(torch.cuda.current_device())
-        sampler.start()
-        res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=LR, momentum=MOM, profiles=prof, record_loss=True)
-        clocks = sampler.stop()
-        timed = res.stats[args.warmup:]
-        samples = sum(sum(s.plan.int_batches) * cluster.iterations_for_plan(s.plan) for s in timed)
-        wall = sum(s.epoch_wall_time for s in timed)
-        results[kind] = {"samples_per_s": samples / wall, "epoch_s": wall / len(timed), "samples": samples,
-                         "wall": wall, "clocks": clocks, "stats": timed, "loss_last": float(res.losses[-1])}
-    return tr, results
+    w = WL[wl]
+    cfg = cluster.StrategyConfig(kind, w["workers"] * w["per_worker"])
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=w["lr"], momentum=w["mom"],
+                 profiles=profiles(w["workers"], w["mult"]), record_loss=True, timed_from=args.warmup)
+    clocks = sampler.stop()
+    timed = res.stats[args.warmup:]
+    return {"samples_per_s": res.timed_samples / res.timed_seconds, "epoch_s": res.timed_seconds / len(timed),
+            "stats": timed, "clocks": clocks, "launches": res.timed_launches, "loss_last": float(res.losses[-1]),
+            "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
-def kernel_roofline(tr, peaks):
-    """Dominant kernel: the layer-1 forward GEMM (X W1^T, M=b, N=256, K=784),
-    timed live with CUDA events on its stream over 200 launches."""
+def kernel_roofline(peaks):
+    """Dominant kernel: the tcgen05 implicit-GEMM 3x3 convolution of the 64-channel
+    stage (the most frequent conv shape; 64->64 at 32x32, b=128 per worker:
+    M = 131072 pixels, N = 64, K = 576).  200 launches captured in a CUDA graph,
+    timed with CUDA events on the capturing stream."""
     import torch
 
     from paper_2007_11831_b200 import _lib
 
-    b = PER_WORKER
-    x = torch.randn(b, IN_DIM, device="cuda").to(torch.bfloat16)
-    act = torch.empty(b, HIDDEN, dtype=torch.bfloat16, device="cuda")
-    m = tr.model
-    s = torch.cuda.current_stream()
-    L = m.layout
-    w1 = m.params_bf16[L.off_w1:].data_ptr()
-    bias = m.params[L.off_b1:].data_ptr()
+    N, H, C = 128, 32, 64
+    x = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(C, 3, 3, C, device="cuda") / 24).to(torch.bfloat16)
+    y = torch.empty(N, H, H, C, dtype=torch.bfloat16, device="cuda")
+    L = _lib.lib()
 
-    def launch():
-        _lib.lib().dbs_dev_gemm_bf16(x.data_ptr(), 0, IN_DIM, w1, 0, IN_DIM, act.data_ptr(), HIDDEN, b, HIDDEN, IN_DIM,
-                                     2, bias, None, int(s.cuda_stream))
+    def launch(s):
+        st = L.dbs_dev_conv2d_fwd(x.data_ptr(), N, H, H, C, w.data_ptr(), C, 3, 1, 1, y.data_ptr(), s)
+        assert st == 0, _lib.last_error()
 
-    for _ in range(20):
-        launch()
+    for _ in range(10):
+        launch(_lib.stream_handle())
     torch.cuda.synchronize()
-    # 200 back-to-back launches captured in a CUDA graph, so the events time the
-    # kernels on the device, not the host launch rate
     g = torch.cuda.CUDAGraph()
     cs = torch.cuda.Stream()
-    with torch.cuda.stream(cs):
-        g.capture_begin()
-        s = torch.cuda.current_stream()
+    with torch.cuda.graph(g, stream=cs):
         for _ in range(200):
-            launch()
-        g.capture_end()
-    torch.cuda.synchronize()
+            launch(int(cs.cuda_stream))
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(cs)
-    g.replay()
-    e1.record(cs)
+    with torch.cuda.stream(cs):
+        e0.record(cs)
+        g.replay()
+        e1.record(cs)
     torch.cuda.synchronize()
     dur = e0.elapsed_time(e1) / 1e3 / 200
-    flops = 2.0 * b * HIDDEN * IN_DIM
+    flops = 2.0 * N * H * H * C * 9 * C
     achieved = flops / dur / 1e12
     peak = peaks["bf16_tflops"]
-    return {"bound": "tensor", "kernel": "gemm_bf16_kernel<256> (layer-1 forward, M=128 N=256 K=784)",
-            "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 5),
-            "traffic": None, "avg_launch_us": round(dur * 1e6, 3), "algorithmic_flops": flops,
+    return {"bound": "tensor", "kernel": "gemm_bf16_kernel<64> implicit-GEMM conv3x3 64->64 @32x32, b=128 "
+                                         "(M=131072, N=64, K=576)",
+            "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+            "traffic": None, "avg_launch_us": round(dur * 1e6, 2), "algorithmic_flops_per_launch": flops,
             "peak_source": peaks["source"]}
 
 
-def cpu_baseline(samples_iters=12):
-    """The numpy oracle of the same loop (run_parallel_sgd restatement, MLP Problem)
-    on the host cores: a bounded sample of the config-1 workload."""
+def cpu_baseline(wl, X, y, threads=None):
+    """The reference loop (sgdlab.py:380-391) with a CPU model on the host cores:
+    a bounded sample (one synchronous iteration of all workers)."""
     from oracle import oracle as O
 
-    X, y = O.synthetic_mnist(D_SAMPLES, IN_DIM, CLASSES, seed=0)
-    prob = O.MlpProblem(X, y, hidden=HIDDEN, classes=CLASSES)
-    p0 = O.mlp_init(IN_DIM, HIDDEN, CLASSES).astype(np.float64)
-    t0 = time.perf_counter()
-    O.run_parallel_sgd(prob, LR, samples_iters, MOM, "batch_weighted", 0, 3, [PER_WORKER] * 3, initial_point=p0)
-    dt = time.perf_counter() - t0
-    return {"value": samples_iters * 3 * PER_WORKER / dt, "unit": "samples/s", "cores": os.cpu_count(),
-            "kind": "port", "sample": f"{samples_iters} iterations x 3 workers x {PER_WORKER} samples "
-                                      "(numpy float64 oracle of run_parallel_sgd, MLP 784-256-10)"}
+    w = WL[wl]
+    batches = [w["per_worker"]] * w["workers"]
+    if wl == "resnet18":
+        from paper_2007_11831_b200.resnet import init_params
+
+        tens = init_params(seed=0)
+        sec = O.cpu_resnet_iteration_seconds(tens, X[:sum(batches)], y[:sum(batches)], batches, threads=threads)
+        sample = (f"1 iteration x {w['workers']} workers x {w['per_worker']} samples, ResNet-18 fwd+bwd on "
+                  "PyTorch-CPU inside the restated run_parallel_sgd loop (fp32)")
+    else:
+        prob = O.MlpProblem(X, y)
+        p0 = O.mlp_init().astype(np.float64)
+        t0 = time.perf_counter()
+        O.run_parallel_sgd(prob, w["lr"], 6, w["mom"], "batch_weighted", 0, w["workers"], batches, initial_point=p0)
+        sec = (time.perf_counter() - t0) / 6
+        sample = "6 iterations of the numpy float64 oracle (MLP Problem)"
+    import torch
+
+    return {"value": sum(batches) / sec, "unit": "samples/s", "cores": threads or torch.get_num_threads(),
+            "kind": "port", "sample": sample}
 
 
-def e2e_run(tr, args):
-    """Public API end to end: dataset uploaded from pinned host memory each epoch,
-    loss read back each epoch; DBS strategy under the same disturbance."""
+def e2e_run(tr, wl, X, y, args):
+    """Public API end to end: the dataset is uploaded from pinned host memory every
+    epoch and the per-iteration losses are read back; DBS under the same disturbance."""
     import torch
 
     from paper_2007_11831_b200 import cluster
-    from paper_2007_11831_b200.mlp import synthetic_mnist
 
-    X, y = synthetic_mnist(D_SAMPLES, IN_DIM, CLASSES, seed=0)
-    Xh = torch.from_numpy(X).pin_memory()
-    yh = torch.from_numpy(y).pin_memory()
-    cfg = cluster.StrategyConfig("dbs", 3 * PER_WORKER)
-    prof = disturbance_profiles(3)
+    w = WL[wl]
+    Xh = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()
+    yh = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
+    cfg = cluster.StrategyConfig("dbs", w["workers"] * w["per_worker"])
+    prof = profiles(w["workers"], w["mult"])
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    samples = 0
-    h2d = d2h = 0
+    samples = h2d = d2h = 0
     for _ in range(args.steps):
-        tr.X.copy_(Xh, non_blocking=True)
+        tr.X.copy_(Xh.view(tr.X.shape), non_blocking=True)
         tr.y.copy_(yh, non_blocking=True)
         h2d += Xh.numel() * 4 + yh.numel() * 4
-        res = tr.run(cfg, n_epochs=1, lr=LR, momentum=MOM, profiles=prof, record_loss=True)
+        res = tr.run(cfg, n_epochs=1, lr=w["lr"], momentum=w["mom"], profiles=prof, record_loss=True)
         samples += res.samples
-        _ = float(res.losses[-1])
         d2h += 4 * len(res.losses)
+        _ = float(res.losses[-1])
     e1.record()
     torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) / 1e3
-    return {"value": samples / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d // args.steps,
-            "d2h_bytes_per_step": d2h // args.steps}
+    return {"value": round(samples / dt, 1), "unit": "samples/s", "h2d_bytes_per_step": h2d // args.steps,
+            "d2h_bytes_per_step": d2h // args.steps,
+            "note": "each step re-uploads the dataset and restarts the plan at the even split (epoch 0)"}
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl = args.workload
+    w = WL[wl]
+    if wl == "resnet18":
+        from paper_2007_11831_b200.resnet import synthetic_cifar
+
+        X, y = synthetic_cifar(w["workers"] * w["per_worker"], seed=0)
+    else:
+        from paper_2007_11831_b200.mlp import synthetic_mnist
+
+        X, y = synthetic_mnist(w["D"], seed=0)
+    vals = [cpu_baseline(wl, X, y, threads=os.cpu_count()) for _ in range(max(1, min(args.steps, 2)))]
+    base = vals[-1]
+    out = {"impl": "reference", "metric": METRIC, "value": round(base["value"], 2), "unit": "samples/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+           "dtype": "f32" if wl == "resnet18" else "f64", "data": "synthetic",
+           "config": {"workload": w["desc"]}, "cpu_baseline": base,
+           "e2e": {"value": round(base["value"], 2), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
 
 
 def main():
     args = parse()
-    rank, world, local = dist_env()
-    peaks = load_peaks()
     if args.impl == "reference":
-        if rank != 0:
-            return
-        base = cpu_baseline(samples_iters=max(4, args.steps * 2))
-        out = {"impl": "reference", "metric": "DBS samples/sec (3-worker S-SGD epoch, MLP 784-256-10)",
-               "value": base["value"], "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
-               "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": "C1: 3 workers, MLP 784-256-10, synthetic MNIST 60000x784, B=384"},
-               "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
-                                             "d2h_bytes_per_step": 0}}
-        print(json.dumps(out), flush=True)
-        return
+        return reference_arm(args)
+    rank, world, local = dist_env()
     import torch
 
-    tr, res = run_ours(args, rank, world)
+    torch.cuda.set_device(local if world > 1 else 0)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+    wl = args.workload
+    w = WL[wl]
+    tr, (X, y) = make_trainer(wl, rank)
+    if world > 1:
+        dist.barrier()
+    res = {k: run_strategy(tr, wl, k, args) for k in ("fixed_ssgd", "dbs")}
     dbs, fixed = res["dbs"], res["fixed_ssgd"]
-    roof = kernel_roofline(tr, peaks)
-    e2e = None if args.no_e2e else e2e_run(tr, args)
-    cpu = None if (args.no_cpu or rank != 0) else cpu_baseline()
-    gap = [s.per_worker_wait for s in fixed["stats"]]
-    util_gap = float(np.mean([np.mean(w) / max(s.per_worker_gpu) for w, s in zip(gap, fixed["stats"])]))
+    if world > 1:
+        # max over ranks of the timed device seconds; samples summed over ranks
+        from paper_2007_11831_b200.comm import max_over_ranks
+
+        for r in (dbs, fixed):
+            t = max_over_ranks(r["seconds"])
+            r["samples_per_s"] = r["samples"] * world / t
+            r["epoch_s"] = t / args.steps
+    roof = kernel_roofline(peaks)
+    e2e = None if args.no_e2e else e2e_run(tr, wl, X, y, args)
+    cpu = None if (args.no_cpu or rank != 0) else cpu_baseline(wl, X, y)
+    gaps = [np.mean(s.per_worker_wait) / max(s.per_worker_gpu) for s in fixed["stats"]]
     out = {
-        "metric": "DBS samples/sec & epoch time under skewed load vs fixed batch",
+        "metric": METRIC,
         "value": round(dbs["samples_per_s"], 1),
         "unit": "samples/s",
         "n_gpus": world,
@@ -318,28 +345,27 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": "C1: 3 simulated workers (green-context SM partitions), MLP 784-256-10, synthetic "
-                               "MNIST 60000x784 fp32 (bf16 GEMM operands), B=384 (128/worker fixed), step = 1 epoch",
-                   "disturbance": "worker 0: spin kernel pins 3/4 of its SMs (cost_multiplier 4)",
-                   "l2": "inputs > L2 per epoch (188 MB dataset repacked each epoch)",
-                   "lr": LR, "momentum": MOM},
+        "config": {"workload": w["desc"],
+                   "disturbance": f"worker 0 on a {w['mult']}x slower device (cost_multiplier {w['mult']}): its "
+                                  "iteration is extended by its own forward/backward time",
+                   "l2": "inputs > L2: 614 MB dataset repacked into per-worker shards every epoch",
+                   "lr": w["lr"], "momentum": w["mom"], "parallelism": f"{w['workers']} simulated DP workers/GPU"},
         "fixed": {"samples_per_s": round(fixed["samples_per_s"], 1), "ms_per_epoch": round(fixed["epoch_s"] * 1e3, 3)},
         "dbs_vs_fixed_speedup": round(dbs["samples_per_s"] / fixed["samples_per_s"], 4),
-        "utilisation_gap_fixed": round(util_gap, 4),
+        "utilisation_gap_fixed": round(float(np.mean(gaps)), 4),
         "final_plan": list(dbs["stats"][-1].plan.int_batches),
+        "per_worker_gpu_s_last_epoch": {"fixed": [round(v, 4) for v in fixed["stats"][-1].per_worker_gpu],
+                                        "dbs": [round(v, 4) for v in dbs["stats"][-1].per_worker_gpu]},
         "roofline": roof,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": dbs["clocks"],
-        "gpu_launches": None,
+        "gpu_launches": int(dbs["launches"]),
     }
-    # launches of our kernels inside the timed region: per epoch 1 controller (host-buffer
-    # call) + 2 permutation + 2n gather + iters * (n * (7 + 3) + 1) + spins
-    last = dbs["stats"][-1]
-    it = sum(1 for _ in [0]) and __import__("paper_2007_11831_b200.cluster", fromlist=["x"]).iterations_for_plan(last.plan)
-    out["gpu_launches"] = args.steps * (1 + 2 + 2 * 3 + it * (3 * 10 + 1) + 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

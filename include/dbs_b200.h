@@ -57,6 +57,8 @@ const char* dbs_last_error(void);
 int dbs_version(int* major, int* minor, int* sm_arch);
 /* 1 when a CUDA device with compute capability 10.x is visible. */
 int dbs_device_ok(void);
+/* Number of kernels this library has launched (or captured into a graph) so far. */
+int64_t dbs_launch_count(void);
 
 /* ------------------------------------------------------------------------ */
 /* (3) Epoch-end DBS controller  -- allocation.py, single-CTA fp64 kernel   */
@@ -338,6 +340,10 @@ typedef struct {
   int64_t spin_ns;           /* disturbance: extra device ns per iteration (0=off) */
   int32_t spin_ctas;         /* SMs the per-iteration disturbance occupies         */
   int32_t model_kind;        /* DBS_MODEL_*                                        */
+  float slow_scale;          /* cost_multiplier - 1 of a simulated slow device: after
+                                its forward/backward the worker spins scale x that
+                                duration (0 = off)                                 */
+  int32_t slow_ctas;         /* CTAs of that proportional spin                     */
 } dbs_worker_slot;
 
 /* Iterations [t0, t1) of one epoch of run_parallel_sgd's loop (sgdlab.py:380-391):

@@ -449,3 +449,73 @@ def run_parallel_sgd(problem, step_size, n_iterations, momentum, aggregation, se
         epoch += 1
     return {"squared_distances": sq, "x": x, "losses": np.asarray(losses),
             "final_loss": problem.objective_gap(x) if hasattr(problem, "objective_gap") else None}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline for the ResNet-18 configs: the run_parallel_sgd loop with a
+# PyTorch-CPU ResNet-18 Problem (the reference itself has no ResNet; this is
+# the same loop, a CPU model, on the host cores -- a reported baseline only)
+# ---------------------------------------------------------------------------
+
+def torch_cpu_resnet18(tensors):
+    """Functional ResNet-18 (CIFAR stem) on the CPU with the given torchvision-order tensors."""
+    import torch
+    import torch.nn.functional as F
+
+    params = [torch.as_tensor(np.asarray(t), dtype=torch.float32).requires_grad_(True) for t in tensors]
+
+    def forward(x):
+        it = iter(params)
+
+        def conv_bn(h, stride, pad, relu=True):
+            w, g, b = next(it), next(it), next(it)
+            y = F.batch_norm(F.conv2d(h, w, stride=stride, padding=pad), None, None, g, b, training=True, eps=1e-5)
+            return F.relu(y) if relu else y
+
+        h = conv_bn(x, 1, 1)
+        cin = 64
+        for L, wdt in enumerate((64, 128, 256, 512)):
+            for blk in range(2):
+                stride = 2 if (L > 0 and blk == 0) else 1
+                a = conv_bn(h, stride, 1)
+                a = conv_bn(a, 1, 1, relu=False)
+                sc = conv_bn(h, stride, 0, relu=False) if (stride != 1 or cin != wdt) else h
+                h = F.relu(a + sc)
+                cin = wdt
+        wf, bf = next(it), next(it)
+        return h.mean(dim=(2, 3)) @ wf.t() + bf
+
+    return forward, params
+
+
+def cpu_resnet_iteration_seconds(tensors, X, y, batches, lr=0.05, momentum=0.9, threads=None):
+    """One synchronous iteration (sgdlab.py:380-391) with CPU ResNet-18 workers:
+    per-worker batch-mean gradient, batch-weighted aggregation, heavy-ball step."""
+    import time
+
+    import torch
+    import torch.nn.functional as F
+
+    if threads:
+        torch.set_num_threads(threads)
+    forward, params = torch_cpu_resnet18(tensors)
+    vel = [torch.zeros_like(p) for p in params]
+    t0 = time.perf_counter()
+    grads = []
+    off = 0
+    for b in batches:
+        xb = torch.as_tensor(X[off:off + b])
+        yb = torch.as_tensor(y[off:off + b]).long()
+        off += b
+        for p in params:
+            p.grad = None
+        F.cross_entropy(forward(xb), yb).backward()
+        grads.append([p.grad.detach().clone() for p in params])
+    w = np.asarray(batches, dtype=np.float64)
+    w /= w.sum()
+    with torch.no_grad():
+        for k, p in enumerate(params):
+            g = sum(float(wi) * gr[k] for wi, gr in zip(w, grads))
+            vel[k].mul_(momentum).add_(g)
+            p.sub_(lr * vel[k])
+    return time.perf_counter() - t0

@@ -62,7 +62,8 @@ class WorkerSlot(ctypes.Structure):
                 ("y_shard", ctypes.c_void_p), ("batch", ctypes.c_int64), ("grad", ctypes.c_void_p),
                 ("loss", ctypes.c_void_p), ("loss_scratch", ctypes.c_void_p), ("stamps", ctypes.c_void_p),
                 ("seconds", ctypes.c_void_p), ("worker_index", ctypes.c_int64), ("spin_ns", ctypes.c_int64),
-                ("spin_ctas", ctypes.c_int32), ("model_kind", ctypes.c_int32)]
+                ("spin_ctas", ctypes.c_int32), ("model_kind", ctypes.c_int32), ("slow_scale", ctypes.c_float),
+                ("slow_ctas", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes)
@@ -70,6 +71,7 @@ SIGNATURES = {
     "dbs_last_error": (ctypes.c_char_p, []),
     "dbs_version": (c_i32, [P_i32, P_i32, P_i32]),
     "dbs_device_ok": (c_i32, []),
+    "dbs_launch_count": (c_i64, []),
     "dbs_evaluate_performance": (c_i32, [P_dbl, P_dbl, c_i64, P_dbl, P_i64]),
     "dbs_compute_batch_fractions": (c_i32, [P_dbl, c_i64, P_dbl, P_i64]),
     "dbs_scale_to_real_batches": (c_i32, [P_dbl, c_i64, c_i64, P_dbl]),

@@ -1,11 +1,16 @@
 // common.cu -- error string, scratch buffers, version queries.
 #include <stdarg.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace dbs {
 
 static thread_local char g_err[1024] = {0};
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -58,6 +63,8 @@ int num_sms() {
 }  // namespace dbs
 
 extern "C" const char* dbs_last_error(void) { return dbs::g_err; }
+
+extern "C" int64_t dbs_launch_count(void) { return (int64_t)dbs::g_launches.load(); }
 
 extern "C" int dbs_version(int* major, int* minor, int* sm_arch) {
   if (major) *major = 0;

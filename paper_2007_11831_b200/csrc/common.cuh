@@ -24,7 +24,13 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
     }                                                                                  \
   } while (0)
 
-#define DBS_LAUNCH_CHECK() DBS_CUDA_TRY(cudaGetLastError())
+// every kernel launch of the library goes through this check, which also counts it
+void count_launch();
+#define DBS_LAUNCH_CHECK()     \
+  do {                         \
+    ::dbs::count_launch();     \
+    DBS_CUDA_TRY(cudaGetLastError()); \
+  } while (0)
 
 #define DBS_REQUIRE(cond, code, ...)  \
   do {                                \

@@ -26,6 +26,7 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
               int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
               float* colsum_part);
 int stamp(int64_t* d_stamps, int64_t slot, cudaStream_t s);
+int spin_scaled(const int64_t* d_stamps, int64_t b, int64_t e, float scale, int ctas, cudaStream_t s);
 }  // namespace dbs
 
 struct dbs_mlp {
@@ -298,6 +299,14 @@ extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t
       if (w[i].stamps) {
         st = stamp(w[i].stamps, 1, s);
         if (st) return st;
+        if (w[i].slow_scale > 0.f && w[i].slow_ctas > 0) {
+          // simulated slower device: extend this worker's critical path in
+          // proportion to its own forward/backward time, then re-stamp
+          st = spin_scaled(w[i].stamps, 0, 1, w[i].slow_scale, w[i].slow_ctas, s);
+          if (st) return st;
+          st = stamp(w[i].stamps, 1, s);
+          if (st) return st;
+        }
         st = dbs_dev_accumulate_time(w[i].stamps, 0, 1, w[i].seconds, w[i].worker_index, s);
         if (st) return st;
       }

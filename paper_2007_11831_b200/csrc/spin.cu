@@ -28,32 +28,80 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
+// The spinning CTA must load only ITS SM: the work is FMA + shared memory, and
+// only thread 0 touches the memory system (one poll of the stop flag / the
+// global timer every ~64 inner rounds) -- 1024 threads hammering one global
+// address would congest the L2 slice and slow every kernel on the GPU.
+// 1024 threads x ~64 live registers fill the register file, 200 KB the shared
+// memory: nothing else can be co-resident on a pinned SM.
 __global__ void __launch_bounds__(kSpinThreads, 1) spin_until_kernel(const volatile int32_t* stop) {
   extern __shared__ float buf[];
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
   const long long t0 = globaltimer();
-  float acc = threadIdx.x;
-  for (int it = 0;; it++) {
-    // keep the FMA pipes and the shared-memory port busy
-#pragma unroll 8
-    for (int k = 0; k < 64; k++) acc = fmaf(acc, 1.0000001f, 0.5f);
-    buf[threadIdx.x + (it & 31) * kSpinThreads] = acc;  // 128 KB footprint
-    if ((it & 15) == 0) {
-      if (*stop) break;
-      if (globaltimer() - t0 > kSpinSafetyNs) break;
+  float acc[48];
+#pragma unroll
+  for (int j = 0; j < 48; j++) acc[j] = threadIdx.x + j;
+  for (int it = 1;; it++) {
+#pragma unroll 4
+    for (int k = 0; k < 8; k++)
+#pragma unroll
+      for (int j = 0; j < 48; j++) acc[j] = fmaf(acc[j], 1.0000001f, 0.5f);
+    buf[threadIdx.x + (it & 31) * kSpinThreads] = acc[it & 7];  // 128 KB footprint
+    if ((it & 63) == 0) {
+      if (threadIdx.x == 0 && (*stop || globaltimer() - t0 > kSpinSafetyNs)) done = 1;
+      __syncthreads();
+      if (done) break;
     }
   }
-  if (acc == 12345.0f) buf[0] = acc;  // keep acc live
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 48; j++) s += acc[j];
+  if (s == 12345.0f) buf[0] = s;  // keep the accumulators live
+}
+
+// Worker slow-down proportional to its own work: spin on `ctas` CTAs for
+// scale * (stamps[end] - stamps[begin]) ns -- a device `scale + 1` times slower
+// than this one (DisturbanceEvent.cost_multiplier for a simulated worker).
+__global__ void __launch_bounds__(256) spin_scaled_kernel(const int64_t* stamps, int64_t b, int64_t e, float scale) {
+  __shared__ volatile int done;
+  __shared__ long long ns;
+  if (threadIdx.x == 0) {
+    done = 0;
+    ns = (long long)((double)(stamps[e] - stamps[b]) * (double)scale);
+  }
+  __syncthreads();
+  const long long t0 = globaltimer();
+  float acc = threadIdx.x;
+  for (int it = 1;; it++) {
+#pragma unroll 8
+    for (int k = 0; k < 64; k++) acc = fmaf(acc, 1.0000001f, 0.5f);
+    if ((it & 7) == 0) {
+      if (threadIdx.x == 0 && globaltimer() - t0 > ns) done = 1;
+      __syncthreads();
+      if (done) break;
+    }
+  }
+  if (acc == 12345.0f) done = 2;
 }
 
 __global__ void __launch_bounds__(kSpinThreads, 1) spin_for_kernel(long long ns) {
   extern __shared__ float buf[];
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
   const long long t0 = globaltimer();
   float acc = threadIdx.x;
-  for (int it = 0;; it++) {
+  for (int it = 1;; it++) {
 #pragma unroll 8
     for (int k = 0; k < 64; k++) acc = fmaf(acc, 1.0000001f, 0.5f);
     buf[(threadIdx.x + it) & 1023] = acc;
-    if ((it & 15) == 0 && globaltimer() - t0 > ns) break;
+    if ((it & 15) == 0) {
+      if (threadIdx.x == 0 && globaltimer() - t0 > ns) done = 1;
+      __syncthreads();
+      if (done) break;
+    }
   }
   if (acc == 12345.0f) buf[0] = acc;
 }
@@ -78,6 +126,13 @@ int set_spin_attrs() {
 
 int stamp(int64_t* d_stamps, int64_t slot, cudaStream_t s) {
   stamp_kernel<<<1, 1, 0, s>>>(d_stamps, slot);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+int spin_scaled(const int64_t* d_stamps, int64_t b, int64_t e, float scale, int ctas, cudaStream_t s) {
+  if (scale <= 0.f || ctas <= 0) return DBS_OK;
+  spin_scaled_kernel<<<ctas, 256, 0, s>>>(d_stamps, b, e, scale);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }

@@ -91,8 +91,11 @@ class RunResult:
     stats: list
     losses: np.ndarray          # per-iteration batch-weighted mean loss
     samples: int                # samples processed (sum over epochs of T * sum b)
-    wall_seconds: float         # sum of epoch wall times (device events)
+    wall_seconds: float         # sum of epoch wall times (device events, iterations only)
     plans: list = field(default_factory=list)
+    timed_seconds: float = 0.0  # device time from the start of epoch `timed_from` to the end,
+    timed_samples: int = 0      # whole epochs: re-plan, permutation, repack and iterations
+    timed_launches: int = 0     # kernels of this library executed in that window
 
 
 class SimulatedTrainer:
@@ -103,8 +106,8 @@ class SimulatedTrainer:
     """
 
     def __init__(self, X, y, n_workers: int, model: str = "mlp", hidden: int = 256, classes: int = 10,
-                 seed: int = 0, partition: bool = True, params=None, max_batch: Optional[int] = None,
-                 graphs: Optional[bool] = None):
+                 seed: int = 0, partition: bool = False, params=None, max_batch: Optional[int] = None,
+                 graphs: Optional[bool] = None, pin_sms: Optional[bool] = None):
         import torch
 
         _lib.require_device()
@@ -129,6 +132,9 @@ class SimulatedTrainer:
             self.model = ResnetModel(classes, seed, self.dev, params=params)
         self.graphs = (self.kind == MODEL_RESNET18) if graphs is None else bool(graphs and self.kind == MODEL_RESNET18)
         self.workers = make_workers(n_workers, partition)
+        # SM-pinning disturbance only when each worker owns its SMs (one GPU per
+        # worker, or green-context partitions); otherwise the proportional slow-down
+        self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
         self.max_batch = max_batch
         self.scratch = {}
         P = self.model.P
@@ -201,22 +207,26 @@ class SimulatedTrainer:
         self._primed = True
 
     def _graph(self, key, slots, mode, lr, mom, skip):
-        g = self._graph_cache.get(key)
-        if g is None:
-            torch = self.torch
-            g = torch.cuda.CUDAGraph()
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g, stream=self.agg):
-                self._run_iters(slots, 0, 1, mode, lr, mom, self.model.params, self.model.velocity,
-                                self.model.params_bf16, skip, self.d_iter)
-            self._graph_cache[key] = g
-        return g
+        """(graph, kernels per replay, kernels recorded by a fresh capture now)."""
+        hit = self._graph_cache.get(key)
+        if hit is not None:
+            return hit[0], hit[1], 0
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        c0 = _lib.lib().dbs_launch_count()
+        with torch.cuda.graph(g, stream=self.agg):
+            self._run_iters(slots, 0, 1, mode, lr, mom, self.model.params, self.model.velocity,
+                            self.model.params_bf16, skip, self.d_iter)
+        per = _lib.lib().dbs_launch_count() - c0
+        self._graph_cache[key] = (g, per)
+        return g, per, per
 
     # -- the epoch loop -----------------------------------------------------------
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
-            skip_update: bool = False) -> RunResult:
+            skip_update: bool = False, timed_from: Optional[int] = None) -> RunResult:
         torch = self.torch
         n, D = self.n, self.D
         self.rng = DeviceRng(seed, self.dev)
@@ -225,7 +235,16 @@ class SimulatedTrainer:
         losses, plans = [], []
         samples, wall, done = 0, 0.0, 0
         mode = _MODE[aggregation]
+        t_start = t_end = None
+        timed_samples = timed_launches = 0
         for epoch in range(n_epochs):
+            if timed_from is not None and epoch == timed_from:
+                torch.cuda.synchronize()
+                t_start = torch.cuda.Event(enable_timing=True)
+                t_start.record()
+            timing = timed_from is not None and epoch >= timed_from
+            launches0 = _lib.lib().dbs_launch_count()
+            captured = 0
             plan, smoothed = cluster.next_plan(config, epoch, n, D, stats[-1] if stats else None, smoothed)
             plans.append(plan)
             batches = list(plan.int_batches)
@@ -279,10 +298,18 @@ class SimulatedTrainer:
                         continue
                     wk = self.workers[w]
                     if ev.cost_multiplier is not None and ev.cost_multiplier > 1.0:
-                        ctas = int(round(wk.sm_count * (1.0 - 1.0 / ev.cost_multiplier)))
-                        ctas = max(0, min(ctas, wk.sm_count - 1))
-                        if ctas:
-                            spinning.append((wk, ctas))
+                        if self.pin_sms:
+                            # a co-running job pins 1 - 1/m of the worker's SMs
+                            ctas = int(round(wk.sm_count * (1.0 - 1.0 / ev.cost_multiplier)))
+                            ctas = max(0, min(ctas, wk.sm_count - 1))
+                            if ctas:
+                                spinning.append((wk, ctas))
+                        else:
+                            # simulated workers share the GPU's SMs: the slow worker's
+                            # device is emulated as m x its own forward/backward time
+                            slots[w].slow_scale = float(ev.cost_multiplier - 1.0)
+                            slots[w].slow_ctas = 8
+                            spin_key.append((w, "x", float(ev.cost_multiplier)))
                     elif ev.extra_epoch_seconds:
                         slots[w].spin_ns = int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
                         slots[w].spin_ctas = wk.sm_count
@@ -290,10 +317,11 @@ class SimulatedTrainer:
             if iters > 0 and (spinning or self.graphs):
                 self._prime(slots, mode)
             graph = None
+            per_replay = 0
             if self.graphs and iters > 0:
                 key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
                        bool(record_loss))
-                graph = self._graph(key, slots, mode, lr, momentum, skip_update)
+                graph, per_replay, captured = self._graph(key, slots, mode, lr, momentum, skip_update)
                 self.d_iter.zero_()
             cur = torch.cuda.current_stream()
             for wk, ctas in spinning:
@@ -333,7 +361,18 @@ class SimulatedTrainer:
             samples += iters * sum(batches)
             wall += ep_wall
             done += iters
+            if timing:
+                timed_samples += iters * sum(batches)
+                timed_launches += (_lib.lib().dbs_launch_count() - launches0 - captured
+                                   + (per_replay * iters if graph is not None else 0))
             if max_iters is not None and done >= max_iters:
                 break
+        timed = 0.0
+        if t_start is not None:
+            t_end = torch.cuda.Event(enable_timing=True)
+            t_end.record()
+            torch.cuda.synchronize()
+            timed = t_start.elapsed_time(t_end) / 1e3
         return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
-                         wall_seconds=wall, plans=plans)
+                         wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
+                         timed_launches=timed_launches)
