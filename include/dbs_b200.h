@@ -344,7 +344,18 @@ typedef struct {
                                 its forward/backward the worker spins scale x that
                                 duration (0 = off)                                 */
   int32_t slow_ctas;         /* CTAs of that proportional spin                     */
+  void* ctx;                 /* CUcontext of the worker's SM partition (green
+                                context, dbs_partition_get), NULL = current         */
 } dbs_worker_slot;
+
+/* SM partitions for simulated workers: n_groups green contexts of
+ * sms_per_group SMs each (rounded by the driver; actual count returned), each
+ * with a worker stream and a side stream (for the disturbance). */
+typedef struct dbs_partition dbs_partition;
+int dbs_partition_create(int32_t n_groups, int32_t sms_per_group, dbs_partition** out, int32_t* actual_sms);
+int dbs_partition_get(const dbs_partition* p, int32_t group, void** ctx, void** stream, void** side_stream);
+/* dbs_dev_spin_until launched inside a partition's context (ctx may be NULL). */
+int dbs_dev_spin_until_ctx(int32_t num_ctas, const volatile int32_t* d_stop, void* stream, void* ctx);
 
 /* Iterations [t0, t1) of one epoch of run_parallel_sgd's loop (sgdlab.py:380-391):
  * every worker's forward/backward on its stream, then the fused aggregate +

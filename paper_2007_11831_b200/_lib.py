@@ -63,7 +63,7 @@ class WorkerSlot(ctypes.Structure):
                 ("loss", ctypes.c_void_p), ("loss_scratch", ctypes.c_void_p), ("stamps", ctypes.c_void_p),
                 ("seconds", ctypes.c_void_p), ("worker_index", ctypes.c_int64), ("spin_ns", ctypes.c_int64),
                 ("spin_ctas", ctypes.c_int32), ("model_kind", ctypes.c_int32), ("slow_scale", ctypes.c_float),
-                ("slow_ctas", ctypes.c_int32)]
+                ("slow_ctas", ctypes.c_int32), ("ctx", ctypes.c_void_p)]
 
 
 # name -> (restype, argtypes)
@@ -129,6 +129,9 @@ SIGNATURES = {
                                      c_vp]),
     "dbs_dev_conv2d_wgrad": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "dbs_dev_spin_until": (c_i32, [c_i32, c_vp, c_vp]),
+    "dbs_dev_spin_until_ctx": (c_i32, [c_i32, c_vp, c_vp, c_vp]),
+    "dbs_partition_create": (c_i32, [c_i32, c_i32, ctypes.POINTER(c_vp), P_i32]),
+    "dbs_partition_get": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     "dbs_dev_spin_for": (c_i32, [c_i32, c_i64, c_vp]),
     "dbs_dev_stamp": (c_i32, [c_vp, c_i64, c_vp]),
     "dbs_dev_set_flag": (c_i32, [c_vp, c_i32, c_vp]),

@@ -449,13 +449,35 @@ int pixel_box(int OH, int OW, int rows, int& bw, int& bh, int& bn) {
   return DBS_OK;
 }
 
+// Kernel attributes are per context (workers may launch from their own green
+// context): remember the contexts in which each instantiation was configured.
+void* current_ctx() {
+  typedef CUresult (*GetCur)(CUcontext*);
+  static GetCur fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<GetCur>(p);
+  });
+  CUcontext c = nullptr;
+  if (fn) fn(&c);
+  return c;
+}
+
 template <int BN>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits, cudaStream_t s) {
   using C = Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
+  static thread_local void* seen[16] = {nullptr};
+  static thread_local int nseen = 0;
+  void* ctx = current_ctx();
+  bool known = false;
+  for (int i = 0; i < nseen; i++) known |= (seen[i] == ctx);
+  if (!known) {
     DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
-    attr = true;
+    if (nseen < 16) seen[nseen++] = ctx;
   }
   dim3 grid((unsigned)((p.M + kBM - 1) / kBM), (unsigned)((p.N + BN - 1) / BN), (unsigned)splits);
   gemm_bf16_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, p);

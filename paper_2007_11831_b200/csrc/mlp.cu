@@ -27,6 +27,8 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
               float* colsum_part);
 int stamp(int64_t* d_stamps, int64_t slot, cudaStream_t s);
 int spin_scaled(const int64_t* d_stamps, int64_t b, int64_t e, float scale, int ctas, cudaStream_t s);
+int ctx_push(void* ctx);
+int ctx_pop(void* ctx);
 }  // namespace dbs
 
 struct dbs_mlp {
@@ -268,6 +270,10 @@ extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t
   for (int64_t t = t0; t < t1; t++) {
     for (int i = 0; i < n; i++) {
       cudaStream_t s = as_stream(w[i].stream);
+      // the worker's launches happen with its SM partition's context current
+      st = ctx_push(w[i].ctx);
+      if (st) return st;
+      st = [&]() -> int {
       DBS_CUDA_TRY(cudaStreamWaitEvent(s, ev[n], 0));  // parameters of iteration t ready
       if (w[i].stamps) {
         st = stamp(w[i].stamps, 0, s);
@@ -311,6 +317,11 @@ extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t
         if (st) return st;
       }
       DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
+      return DBS_OK;
+      }();
+      const int st_pop = ctx_pop(w[i].ctx);
+      if (st) return st;
+      if (st_pop) return st_pop;
     }
     for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
     if (!skip_update) {

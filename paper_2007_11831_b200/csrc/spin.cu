@@ -112,13 +112,11 @@ __global__ void accumulate_kernel(const int64_t* stamps, int64_t b, int64_t e, d
   secs[w] += (double)(stamps[e] - stamps[b]) * 1e-9;
 }
 
+// set on every call: the attribute is per context, and workers may run in
+// their own (green) contexts
 int set_spin_attrs() {
-  static bool done = false;
-  if (!done) {
-    DBS_CUDA_TRY(cudaFuncSetAttribute(spin_until_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpinSmem));
-    DBS_CUDA_TRY(cudaFuncSetAttribute(spin_for_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpinSmem));
-    done = true;
-  }
+  DBS_CUDA_TRY(cudaFuncSetAttribute(spin_until_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpinSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(spin_for_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpinSmem));
   return DBS_OK;
 }
 
@@ -150,6 +148,19 @@ extern "C" int dbs_dev_spin_until(int32_t num_ctas, const volatile int32_t* d_st
   spin_until_kernel<<<num_ctas, kSpinThreads, kSpinSmem, as_stream(stream)>>>(d_stop);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
+}
+
+namespace dbs {
+int ctx_push(void* ctx);
+int ctx_pop(void* ctx);
+}  // namespace dbs
+
+extern "C" int dbs_dev_spin_until_ctx(int32_t num_ctas, const volatile int32_t* d_stop, void* stream, void* ctx) {
+  int st = ctx_push(ctx);
+  if (st) return st;
+  st = dbs_dev_spin_until(num_ctas, d_stop, stream);
+  int st2 = ctx_pop(ctx);
+  return st ? st : st2;
 }
 
 extern "C" int dbs_dev_spin_for(int32_t num_ctas, int64_t ns, void* stream) {

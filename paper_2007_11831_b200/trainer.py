@@ -51,6 +51,7 @@ class Worker:
     spin_stream: object
     sm_count: int
     green: object = None
+    ctx: int = 0  # CUcontext of the worker's SM partition (0 = the current context)
 
 
 def _green_supported() -> bool:
@@ -62,27 +63,35 @@ def _green_supported() -> bool:
         return False
 
 
+_PARTITIONS = []  # keep green contexts alive for the process
+
+
 def make_workers(n: int, partition: bool = True) -> list:
-    """W simulated workers on the current device; SM partitions via green contexts."""
+    """W simulated workers on the current device.  partition=True gives each
+    worker a disjoint SM set (a green context created by the library, whose
+    launches the iteration driver issues with that context current)."""
+    import ctypes
+
     import torch
 
     dev = torch.cuda.current_device()
     total = torch.cuda.get_device_properties(dev).multi_processor_count
     workers = []
-    use_green = partition and n > 1 and _green_supported()
-    per = max(8, (total // n) // 8 * 8) if use_green else total
+    if partition and n > 1:
+        per = max(8, (total // n) // 8 * 8)
+        h = ctypes.c_void_p()
+        actual = ctypes.c_int32()
+        _lib.check(_lib.lib().dbs_partition_create(n, per, ctypes.byref(h), ctypes.byref(actual)), "partition")
+        _PARTITIONS.append(h)
+        for i in range(n):
+            ctx, st, side = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(_lib.lib().dbs_partition_get(h, i, ctypes.byref(ctx), ctypes.byref(st), ctypes.byref(side)),
+                       "partition_get")
+            workers.append(Worker(i, torch.cuda.ExternalStream(st.value), torch.cuda.ExternalStream(side.value),
+                                  actual.value, h, ctx.value))
+        return workers
     for i in range(n):
-        if use_green:
-            g = torch.cuda.green_contexts.GreenContext.create(per, dev)
-            s = g.Stream()
-            g.set_context()
-            try:
-                spin = torch.cuda.Stream()
-            finally:
-                g.pop_context()
-            workers.append(Worker(i, s, spin, per, g))
-        else:
-            workers.append(Worker(i, torch.cuda.Stream(), torch.cuda.Stream(), total, None))
+        workers.append(Worker(i, torch.cuda.Stream(), torch.cuda.Stream(), total, None))
     return workers
 
 
@@ -130,8 +139,12 @@ class SimulatedTrainer:
 
             assert tuple(self.X.shape[1:]) == (3, 32, 32), "resnet18 expects CIFAR-shaped [D][3][32][32] rows"
             self.model = ResnetModel(classes, seed, self.dev, params=params)
-        self.graphs = (self.kind == MODEL_RESNET18) if graphs is None else bool(graphs and self.kind == MODEL_RESNET18)
         self.workers = make_workers(n_workers, partition)
+        partitioned = any(w.ctx for w in self.workers)
+        # iteration graphs for ResNet (one context); partitioned workers launch eagerly
+        # from their own contexts (a graph cannot span contexts)
+        default_graphs = self.kind == MODEL_RESNET18 and not partitioned
+        self.graphs = default_graphs if graphs is None else bool(graphs and default_graphs)
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
         self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
@@ -286,6 +299,7 @@ class SimulatedTrainer:
                 sl.seconds = self.seconds.data_ptr()
                 sl.worker_index = w
                 sl.spin_ns, sl.spin_ctas = 0, 0
+                sl.ctx = self.workers[w].ctx or None
             self.seconds.zero_()
             self.d_iter.zero_()
             _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 0, s_main), "set_flag")
@@ -326,8 +340,8 @@ class SimulatedTrainer:
             cur = torch.cuda.current_stream()
             for wk, ctas in spinning:
                 wk.spin_stream.wait_stream(cur)
-                _lib.check(_lib.lib().dbs_dev_spin_until(ctas, self.stop.data_ptr(), int(wk.spin_stream.cuda_stream)),
-                           "spin")
+                _lib.check(_lib.lib().dbs_dev_spin_until_ctx(ctas, self.stop.data_ptr(), int(wk.spin_stream.cuda_stream),
+                                                             wk.ctx or None), "spin")
             self.agg.wait_stream(cur)
             for wk in self.workers:
                 wk.stream.wait_stream(cur)
