@@ -16,9 +16,10 @@ Prints ONE JSON line on rank 0.  Definitions ("Measurement"):
     cpu_baseline (the reference loop with a CPU model on the host cores),
     clocks sampled in-process with NVML during the timed region.
 Workload at N=1 (config 3, BASELINE.json): ResNet-18 on synthetic CIFAR-shaped
-data, 4 simulated workers sharing the GPU, B=512 (128/worker fixed), worker 0
-runs on a device 2x slower (cost_multiplier 2: its step is extended by its own
-forward/backward time).  Under torchrun each rank runs the same 4-worker
+data, 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the
+B200, B=512 (128/worker fixed); worker 0 shares its partition with a co-running
+spin kernel that pins half of its SMs (cost_multiplier 2, the paper's SM
+disturbance).  Under torchrun each rank runs the same 4-worker
 simulation on its own GPU (weak scaling, no data-path collective across GPUs).
 """
 
@@ -117,8 +118,8 @@ class ClockSampler:
 WL = {
     "resnet18": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0,
                      desc="C3: ResNet-18 (CIFAR stem), synthetic CIFAR-10-shaped 50000x3x32x32 fp32 (bf16 tensor-core "
-                          "operands), 4 simulated workers sharing the GPU, B=512 (128/worker fixed), step = 1 epoch "
-                          "(97 iterations)"),
+                          "operands), 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the B200, "
+                          "B=512 (128/worker fixed), step = 1 epoch (97 iterations)"),
     "mlp": dict(D=60000, workers=3, per_worker=128, lr=0.05, mom=0.5, mult=2.0,
                 desc="C1: MLP 784-256-10, synthetic MNIST 60000x784, 3 simulated workers, B=384, step = 1 epoch"),
 }
@@ -143,7 +144,7 @@ def make_trainer(wl, rank):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
         X, y = synthetic_cifar(w["D"], seed=rank)
-        return SimulatedTrainer(X, y, n_workers=w["workers"], model="resnet18", seed=0,
+        return SimulatedTrainer(X, y, n_workers=w["workers"], model="resnet18", seed=0, partition=True,
                                 max_batch=w["workers"] * w["per_worker"]), (X, y)
     from paper_2007_11831_b200.mlp import synthetic_mnist
 
@@ -346,8 +347,9 @@ def main():
         "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": w["desc"],
-                   "disturbance": f"worker 0 on a {w['mult']}x slower device (cost_multiplier {w['mult']}): its "
-                                  "iteration is extended by its own forward/backward time",
+                   "disturbance": (f"worker 0: a co-running spin kernel pins {1 - 1 / w['mult']:.0%} of its SM "
+                                   f"partition for every epoch (cost_multiplier {w['mult']})" if wl == "resnet18" else
+                                   f"worker 0 on a {w['mult']}x slower device (proportional spin)"),
                    "l2": "inputs > L2: 614 MB dataset repacked into per-worker shards every epoch",
                    "lr": w["lr"], "momentum": w["mom"], "parallelism": f"{w['workers']} simulated DP workers/GPU"},
         "fixed": {"samples_per_s": round(fixed["samples_per_s"], 1), "ms_per_epoch": round(fixed["epoch_s"] * 1e3, 3)},
