@@ -134,12 +134,18 @@ def profiles(n, mult):
     return prof + [cluster.WorkerProfile(i, 1.0) for i in range(1, n)]
 
 
-def make_trainer(wl, rank):
+def make_trainer(wl, rank, world=1):
     import torch
 
-    from paper_2007_11831_b200.trainer import SimulatedTrainer
+    from paper_2007_11831_b200.trainer import DistributedTrainer, SimulatedTrainer
 
     w = WL[wl]
+    if world > 1:
+        # one process per GPU: the same 4 SM-partition workers per GPU, the global
+        # plan spans 4 x world workers, gradients meet in the fused NVLink kernel
+        tr = DistributedTrainer(w["D"], workers_per_rank=w["workers"], model=wl, seed=0, partition=True,
+                                max_batch=3 * w["per_worker"])
+        return tr, (None, None)
     if wl == "resnet18":
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
@@ -153,17 +159,18 @@ def make_trainer(wl, rank):
                             max_batch=w["workers"] * w["per_worker"]), (X, y)
 
 
-def run_strategy(tr, wl, kind, args):
+def run_strategy(tr, wl, kind, args, world=1):
     import torch
 
     from paper_2007_11831_b200 import cluster
 
     w = WL[wl]
-    cfg = cluster.StrategyConfig(kind, w["workers"] * w["per_worker"])
+    n_global = w["workers"] * world
+    cfg = cluster.StrategyConfig(kind, n_global * w["per_worker"])
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=w["lr"], momentum=w["mom"],
-                 profiles=profiles(w["workers"], w["mult"]), record_loss=True, timed_from=args.warmup)
+                 profiles=profiles(n_global, w["mult"]), record_loss=True, timed_from=args.warmup)
     clocks = sampler.stop()
     timed = res.stats[args.warmup:]
     return {"samples_per_s": res.timed_samples / res.timed_seconds, "epoch_s": res.timed_seconds / len(timed),
@@ -316,22 +323,16 @@ def main():
     peaks = load_peaks()
     wl = args.workload
     w = WL[wl]
-    tr, (X, y) = make_trainer(wl, rank)
+    tr, (X, y) = make_trainer(wl, rank, world)
     if world > 1:
         dist.barrier()
-    res = {k: run_strategy(tr, wl, k, args) for k in ("fixed_ssgd", "dbs")}
+    # (multi-GPU: the trainer's timed seconds are already the max over ranks and
+    # its samples count every worker of every rank)
+    res = {k: run_strategy(tr, wl, k, args, world) for k in ("fixed_ssgd", "dbs")}
     dbs, fixed = res["dbs"], res["fixed_ssgd"]
-    if world > 1:
-        # max over ranks of the timed device seconds; samples summed over ranks
-        from paper_2007_11831_b200.comm import max_over_ranks
-
-        for r in (dbs, fixed):
-            t = max_over_ranks(r["seconds"])
-            r["samples_per_s"] = r["samples"] * world / t
-            r["epoch_s"] = t / args.steps
     roof = kernel_roofline(peaks)
-    e2e = None if args.no_e2e else e2e_run(tr, wl, X, y, args)
-    cpu = None if (args.no_cpu or rank != 0) else cpu_baseline(wl, X, y)
+    e2e = None if (args.no_e2e or world > 1) else e2e_run(tr, wl, X, y, args)
+    cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl, X, y)
     gaps = [np.mean(s.per_worker_wait) / max(s.per_worker_gpu) for s in fixed["stats"]]
     out = {
         "metric": METRIC,

@@ -366,6 +366,17 @@ int dbs_dev_spin_until_ctx(int32_t num_ctas, const volatile int32_t* d_stop, voi
 int dbs_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                        float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
                        int32_t skip_update, void* agg_stream, int64_t* d_iter);
+/* Multi-GPU form (one process per GPU): the rank's n local workers, then a local
+ * weighted reduce into the communicator's gradient block and the fused NVLink
+ * all-reduce + momentum SGD (dbs_comm_allreduce_sgd) with per-rank weights
+ * rank_batches[r] (sum of that rank's worker batches); parameters are the
+ * communicator's blocks, the velocity is this rank's shard. */
+int dbs_run_iterations_comm(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                            float lr, float momentum, dbs_comm* comm, const int64_t* rank_batches,
+                            float* d_velocity_shard, void* agg_stream, int64_t* d_iter);
+/* fp32 weighted reduce out = sum_i w_i g_i (DBS_AGG_*), no step. */
+int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* batch_sizes, int64_t n, int32_t mode, int64_t P,
+                          float* d_out, void* stream);
 int dbs_mlp_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                            float lr, float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
                            int32_t skip_update, void* agg_stream);

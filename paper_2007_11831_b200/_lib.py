@@ -119,6 +119,9 @@ SIGNATURES = {
                                        c_vp, c_vp, c_i32, c_vp]),
     "dbs_run_iterations": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp, c_vp,
                                    c_vp, c_i32, c_vp, c_vp]),
+    "dbs_run_iterations_comm": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp,
+                                        P_i64, c_vp, c_vp, c_vp]),
+    "dbs_dev_aggregate_f32": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, c_vp, c_vp]),
     "dbs_resnet_create": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_vp)]),
     "dbs_resnet_destroy": (c_i32, [c_vp]),
     "dbs_resnet_param_count": (c_i32, [c_vp, P_i64]),

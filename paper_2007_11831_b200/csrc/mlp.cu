@@ -245,9 +245,45 @@ int resnet_param_count(const dbs_resnet* m);
 int iter_increment(int64_t* d_iter, cudaStream_t s);
 }  // namespace dbs
 
+extern "C" int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                                     float* d_out, void* stream);
+extern "C" int dbs_comm_allreduce_sgd(dbs_comm* c, const int64_t* batch_sizes, int32_t mode, float step,
+                                      float momentum, float* d_velocity_shard, void* stream);
+extern "C" int dbs_comm_buffers(dbs_comm* c, float** d_grad, float** d_param, uint16_t** d_param_bf16);
+
+static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                               float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                               int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
+                               const int64_t* rank_batches);
+
 extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                   float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
                                   int32_t skip_update, void* agg_stream, int64_t* d_iter) {
+  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_bf16, skip_update,
+                             agg_stream, d_iter, nullptr, nullptr);
+}
+
+// Multi-GPU form: this rank's n local workers, then the hierarchical update --
+// local weighted reduce into the communicator's gradient block (skipped for
+// one worker, whose gradient is written there directly) and the fused NVLink
+// all-reduce + momentum SGD with per-rank weights rank_batches[r] = sum of
+// that rank's worker batches.  Parameters live in the communicator's blocks.
+extern "C" int dbs_run_iterations_comm(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                       float lr, float mom, dbs_comm* comm, const int64_t* rank_batches,
+                                       float* d_velocity_shard, void* agg_stream, int64_t* d_iter) {
+  DBS_REQUIRE(comm && rank_batches && d_velocity_shard, DBS_ERR_ARGUMENT, "run_iterations_comm: null argument");
+  float *g = nullptr, *p = nullptr;
+  uint16_t* pb = nullptr;
+  int st = dbs_comm_buffers(comm, &g, &p, &pb);
+  if (st) return st;
+  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, p, d_velocity_shard, pb, 0, agg_stream, d_iter, comm,
+                             rank_batches);
+}
+
+static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                               float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                               int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
+                               const int64_t* rank_batches) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "run_iterations: bad arguments");
   for (int i = 0; i < n; i++)
     DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18) &&
@@ -324,9 +360,19 @@ extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t
       if (st_pop) return st_pop;
     }
     for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
-    if (!skip_update) {
+    if (!skip_update && comm == nullptr) {
       st = dbs_dev_aggregate_sgd_f32(grads, batches, n, mode, P, lr, mom, d_params, d_velocity, d_params_bf16,
                                      agg_stream);
+      if (st) return st;
+    } else if (!skip_update) {
+      float* cg = nullptr;
+      st = dbs_comm_buffers(comm, &cg, nullptr, nullptr);
+      if (st) return st;
+      if (!(n == 1 && grads[0] == cg)) {
+        st = dbs_dev_aggregate_f32(grads, batches, n, mode, P, cg, agg_stream);
+        if (st) return st;
+      }
+      st = dbs_comm_allreduce_sgd(comm, rank_batches, mode, lr, mom, d_velocity, agg_stream);
       if (st) return st;
     }
     if (d_iter) {

@@ -115,6 +115,23 @@ __global__ void __launch_bounds__(256) aggregate_sgd_f32_kernel(AggArgs a, int64
 #undef W
 }
 
+// fp32 weighted reduce without the step: out = sum_i w_i g_i (the local level of
+// the hierarchical all-reduce when several workers share one GPU)
+__global__ void __launch_bounds__(256) aggregate_f32_kernel(AggArgs a, int64_t P4, float4* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x) {
+    const float w0 = (a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[0] : 1.0f / (float)a.n;
+    float4 g = __ldcs(((const float4*)a.g[0]) + p);
+    g.x *= w0; g.y *= w0; g.z *= w0; g.w *= w0;
+    for (int i = 1; i < a.n; i++) {
+      const float wi = (a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[i] : 1.0f / (float)a.n;
+      const float4 h = __ldcs(((const float4*)a.g[i]) + p);
+      g.x = fmaf(wi, h.x, g.x); g.y = fmaf(wi, h.y, g.y);
+      g.z = fmaf(wi, h.z, g.z); g.w = fmaf(wi, h.w, g.w);
+    }
+    out[p] = g;
+  }
+}
+
 int grid_for(int64_t P, int threads) {
   int64_t blocks = (P + threads - 1) / threads;
   int64_t cap = (int64_t)num_sms() * 8;
@@ -170,6 +187,18 @@ extern "C" int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int6
   const int64_t P4 = P / 4;
   aggregate_sgd_f32_kernel<<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
       a, P4, step, mom, (float4*)d_x, (float4*)d_v, (uint2*)d_x_bf16);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                                     float* d_out, void* stream) {
+  AggArgs a;
+  int st = make_args(a, (const void* const*)d_grads, b, n, mode);
+  if (st) return st;
+  DBS_REQUIRE(P % 4 == 0, DBS_ERR_ARGUMENT, "fp32 aggregate: P must be a multiple of 4");
+  if (P <= 0) return DBS_OK;
+  aggregate_f32_kernel<<<grid_for(P / 4, 256), 256, 0, as_stream(stream)>>>(a, P / 4, (float4*)d_out);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }

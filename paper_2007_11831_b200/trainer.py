@@ -390,3 +390,230 @@ class SimulatedTrainer:
         return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
                          wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
                          timed_launches=timed_launches)
+
+
+# ---------------------------------------------------------------------------
+# one process per GPU: the same workers, plus the fused NVLink all-reduce
+# ---------------------------------------------------------------------------
+
+def gather_worker_times(local_secs, group=None) -> list:
+    """All ranks learn every worker's measured compute time (Alg. 2 step 1,
+    PAPER.md:115): rank-major order, so every rank runs the identical
+    (deterministic, bit-exact) controller on the same inputs."""
+    from .comm import gather_times
+
+    out = []
+    for r_times in _gather_lists(list(local_secs), group):
+        out.extend(r_times)
+    return out
+
+
+def _gather_lists(values: list, group=None) -> list:
+    import torch.distributed as dist
+
+    got = [None] * dist.get_world_size(group)
+    dist.all_gather_object(got, [float(v) for v in values], group=group)
+    return got
+
+
+def distributed_plan(config, epoch, n_global, D, prev_stats, smoothed, planner=None):
+    """cluster.run_training's re-plan (cluster.py:253-271) on the gathered times."""
+    planner = planner or cluster.next_plan
+    return planner(config, epoch, n_global, D, prev_stats, smoothed)
+
+
+class DistributedTrainer(SimulatedTrainer):
+    """Synchronous DBS S-SGD across GPUs (one process per GPU, torchrun).
+
+    Each rank hosts ``workers_per_rank`` workers (SM partitions of its GPU, or the
+    whole GPU for one worker); the global plan covers world * workers_per_rank
+    workers.  Per iteration: local forward/backward, local weighted reduce, then
+    the fused NVLink weighted all-reduce + momentum SGD (comm.cu) -- the only
+    data-path exchange.  The dataset is generated identically on every rank
+    (device RNG) so a rank repacks its own spans locally.
+    """
+
+    def __init__(self, D_per_rank: int, workers_per_rank: int = 1, model: str = "resnet18", classes: int = 10,
+                 seed: int = 0, partition: Optional[bool] = None, max_batch: Optional[int] = None, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from .comm import Communicator
+
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        D = D_per_rank * self.world
+        g = torch.Generator(device=dev).manual_seed(seed + 1234)
+        if model == "resnet18":
+            X = torch.randn((D, 3, 32, 32), generator=g, device=dev)
+        else:
+            X = torch.randn((D, 784), generator=g, device=dev)
+        y = torch.randint(0, classes, (D,), generator=g, device=dev, dtype=torch.int32)
+        part = (workers_per_rank > 1) if partition is None else partition
+        super().__init__(X, y, workers_per_rank, model=model, classes=classes, seed=seed, partition=part,
+                         max_batch=max_batch, graphs=False, pin_sms=True)
+        self.comm = Communicator.create(self.model.P, group)
+        self.comm.params.copy_(self.model.params)
+        self.comm.params_bf16.copy_(self.comm.params.to(torch.bfloat16))
+        torch.cuda.synchronize()
+        dist.barrier(group)
+        # the model's tensors now alias the symmetric blocks
+        self.model.params, self.model.params_bf16 = self.comm.params, self.comm.params_bf16
+        if workers_per_rank == 1:
+            self.grads = [self.comm.grad]
+
+    def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
+            aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
+            seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
+            skip_update: bool = False, timed_from: Optional[int] = None) -> RunResult:
+        import torch
+
+        from .comm import max_over_ranks
+
+        n_loc, W, R = self.n, self.n * self.world, self.rank
+        D = self.D
+        self.rng = DeviceRng(seed, self.dev)
+        stats, losses, plans = [], [], []
+        smoothed = None
+        samples = done = 0
+        wall = 0.0
+        mode = _MODE[aggregation]
+        t_start = None
+        timed_samples = timed_launches = 0
+        for epoch in range(n_epochs):
+            if timed_from is not None and epoch == timed_from:
+                torch.cuda.synchronize()
+                torch.distributed.barrier(self.group)
+                t_start = torch.cuda.Event(enable_timing=True)
+                t_start.record()
+            launches0 = _lib.lib().dbs_launch_count()
+            plan, smoothed = distributed_plan(config, epoch, W, D, stats[-1] if stats else None, smoothed)
+            plans.append(plan)
+            batches = list(plan.int_batches)
+            spans = list(plan.sample_spans)
+            iters = cluster.iterations_for_plan(plan)
+            if max_iters is not None:
+                iters = min(iters, max_iters - done)
+            perm, _ = self.rng.permute_spans(spans)
+            offs = np.cumsum([0] + [e - s for s, e in spans[:-1]])
+            s_main = _lib.stream_handle()
+            slots = (_lib.WorkerSlot * n_loc)()
+            for w in range(n_loc):
+                gw = R * n_loc + w
+                rows = iters * batches[gw]
+                idx = perm[int(offs[gw]):int(offs[gw]) + rows]
+                xs, ys = self.shard_x[w], self.shard_y[w]
+                if rows:
+                    if self.kind == MODEL_MLP:
+                        st = _lib.lib().dbs_dev_gather_rows_f32_bf16(self.X.data_ptr(), idx.data_ptr(), rows,
+                                                                     self.row_elems, xs.data_ptr(), s_main)
+                    else:
+                        st = _lib.lib().dbs_dev_gather_rows(self.X.data_ptr(), idx.data_ptr(), rows,
+                                                            self.row_elems * 4, xs.data_ptr(), s_main)
+                    _lib.check(st, "gather")
+                    _lib.check(_lib.lib().dbs_dev_gather_i32(self.y.data_ptr(), idx.data_ptr(), rows, ys.data_ptr(),
+                                                              s_main), "gather labels")
+                sc = self._scratch(w, batches[gw])
+                sl = slots[w]
+                sl.model = sc.handle.value
+                sl.model_kind = self.kind
+                sl.stream = int(self.workers[w].stream.cuda_stream)
+                sl.ctx = self.workers[w].ctx or None
+                sl.x_shard, sl.y_shard = xs.data_ptr(), ys.data_ptr()
+                sl.batch = batches[gw]
+                sl.grad = self.grads[w].data_ptr()
+                sl.loss = self.loss_buf[w].data_ptr() if record_loss else None
+                sl.loss_scratch = self.loss_scratch[w:].data_ptr()
+                sl.stamps = self.stamps[w].data_ptr()
+                sl.seconds = self.seconds.data_ptr()
+                sl.worker_index = w
+            self.seconds.zero_()
+            _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 0, s_main), "set_flag")
+            spinning = []
+            if profiles is not None:
+                for w in range(n_loc):
+                    ev = profiles[R * n_loc + w].active_disturbance(epoch)
+                    if ev is not None and ev.cost_multiplier is not None and ev.cost_multiplier > 1.0:
+                        wk = self.workers[w]
+                        ctas = max(0, min(int(round(wk.sm_count * (1.0 - 1.0 / ev.cost_multiplier))), wk.sm_count - 1))
+                        if ctas:
+                            spinning.append((wk, ctas))
+                    elif ev is not None and ev.extra_epoch_seconds:
+                        slots[w].spin_ns = int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
+                        slots[w].spin_ctas = self.workers[w].sm_count
+            rank_batches = np.asarray([sum(batches[r * n_loc:(r + 1) * n_loc]) for r in range(self.world)],
+                                      dtype=np.int64)
+            if iters > 0:
+                self._prime_comm(slots, mode, rank_batches)
+            cur = torch.cuda.current_stream()
+            for wk, ctas in spinning:
+                wk.spin_stream.wait_stream(cur)
+                _lib.check(_lib.lib().dbs_dev_spin_until_ctx(ctas, self.stop.data_ptr(), int(wk.spin_stream.cuda_stream),
+                                                             wk.ctx or None), "spin")
+            self.agg.wait_stream(cur)
+            for wk in self.workers:
+                wk.stream.wait_stream(cur)
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record(self.agg)
+            if iters > 0:
+                st = _lib.lib().dbs_run_iterations_comm(slots, n_loc, 0, iters, mode, float(lr), float(momentum),
+                                                        self.comm.h, rank_batches.ctypes.data_as(_lib.P_i64),
+                                                        self.comm.velocity.data_ptr(), int(self.agg.cuda_stream), None)
+                _lib.check(st, "run_iterations_comm")
+            end.record(self.agg)
+            _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 1, int(self.agg.cuda_stream)), "set_flag")
+            for wk, _ in spinning:
+                self.agg.wait_stream(wk.spin_stream)
+            cur.wait_stream(self.agg)
+            torch.cuda.synchronize()
+            ep_wall = max_over_ranks(start.elapsed_time(end) / 1e3, self.group)
+            secs = tuple(gather_worker_times(self.seconds.cpu().tolist(), self.group))
+            slowest = max(secs)
+            stats.append(EpochStats(epoch=epoch, per_worker_gpu=secs, per_worker_wait=tuple(slowest - s for s in secs),
+                                    sync_time=max(0.0, ep_wall - slowest), epoch_wall_time=ep_wall, plan=plan))
+            if record_loss and iters > 0:
+                lb = self.loss_buf[:, :iters].double().cpu().numpy()
+                bw = np.asarray(batches[R * n_loc:(R + 1) * n_loc], dtype=np.float64)[:, None]
+                losses.append((lb * bw).sum(axis=0) / bw.sum())
+            samples += iters * sum(batches)
+            wall += ep_wall
+            done += iters
+            if timed_from is not None and epoch >= timed_from:
+                timed_samples += iters * sum(batches)
+                timed_launches += _lib.lib().dbs_launch_count() - launches0
+            if max_iters is not None and done >= max_iters:
+                break
+        timed = 0.0
+        if t_start is not None:
+            t_end = torch.cuda.Event(enable_timing=True)
+            t_end.record()
+            torch.cuda.synchronize()
+            timed = max_over_ranks(t_start.elapsed_time(t_end) / 1e3, self.group)
+        return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
+                         wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
+                         timed_launches=timed_launches)
+
+    def _prime_comm(self, slots, mode, rank_batches):
+        """Load every kernel of an iteration (local workers, local reduce, the fused
+        NVLink kernel) before any spin kernel runs: a lazily loaded module must
+        never be needed while a spinning kernel owns SMs.  The all-reduce runs
+        with lr = 0, so the parameters are untouched; the velocity is reset."""
+        if self._primed:
+            return
+        import ctypes
+
+        import torch
+
+        self._prime(slots, mode)
+        self._primed = True
+        if self.n > 1:
+            ptrs = (ctypes.c_void_p * self.n)(*[g.data_ptr() for g in self.grads])
+            b = np.asarray([slots[w].batch for w in range(self.n)], dtype=np.int64)
+            _lib.check(_lib.lib().dbs_dev_aggregate_f32(ptrs, b.ctypes.data_as(_lib.P_i64), self.n, mode,
+                                                        self.model.P, self.comm.grad.data_ptr(),
+                                                        _lib.stream_handle()), "aggregate_f32")
+        self.comm.allreduce_sgd(rank_batches, 0.0, 0.0, mode=mode)
+        torch.cuda.synchronize()
+        self.comm.velocity.zero_()
+        torch.distributed.barrier(self.group)
