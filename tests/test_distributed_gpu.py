@@ -1,0 +1,31 @@
+"""Two real processes (torchrun, gloo host collectives) driving DistributedTrainer:
+CUDA IPC handle exchange, the fused weighted all-reduce + SGD kernel across
+process boundaries, identical plans and identical parameters on every rank.
+Both ranks may share one GPU (the kernels time-slice; the in-kernel barrier
+has a timeout so a missing peer can never wedge the device)."""
+
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def test_two_process_distributed_trainer(dev):
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", str(ROOT / "scripts" / "dist_smoke.py"), "mlp"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=str(ROOT))
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-3000:]
+    lines = re.findall(r"rank (\d): plans (.*?) losses (.*?) param-sum agree (True|False)", out)
+    assert len(lines) == 2, out[-2000:]
+    assert all(agree == "True" for _, _, _, agree in lines)
+    assert lines[0][1] == lines[1][1]  # same plan on both ranks
