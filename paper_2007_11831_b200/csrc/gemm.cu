@@ -69,7 +69,9 @@ template <int BN>
 struct Cfg {
   static constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
   static constexpr uint32_t kBBytes = BN * kBK * 2;
-  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  // shallow rings so 2-3 CTAs share an SM: one CTA's epilogue (and prologue)
+  // then overlaps another's TMA/MMA main loop
+  static constexpr int kStages = (BN >= 256) ? 2 : (BN >= 128 ? 3 : (BN >= 64 ? 3 : 4));
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + 256;
 };
