@@ -273,6 +273,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (p.b_mode == 1) {
 #pragma unroll
         for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, k0);
+      } else if (p.b_mode == 3) {
+        // input gradient: the filter W[k][r][s][c] read in place as the flipped,
+        // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        const int r = rs / g.S, sx = rs - r * g.S;
+        const int rs_flip = (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
       } else {
         const ConvGeom& g = p.gb;
         int bn_, boh, bow;
@@ -568,7 +578,13 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   p.sq_part = c.sq_part;
   p.colsum_part = nullptr;
   int st;
-  const int bn = (c.bn_override > 0) ? c.bn_override : pick_bn(c.N, c.b_mode);
+  int bn = (c.bn_override > 0) ? c.bn_override : pick_bn(c.N, c.b_mode);
+  if (c.bn_override <= 0 && c.b_mode != 2) {
+    // narrower N tiles when the grid would not cover the SMs this launch can use
+    const int sms = current_sm_count();
+    const int64_t mt = (c.M + kBM - 1) / kBM;
+    while (bn > 64 && mt * ((c.N + bn - 1) / bn) < sms) bn /= 2;
+  }
   // ---- A ----
   p.a_mode = c.a_mode;
   if (c.a_mode == 2) {
@@ -594,6 +610,21 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     p.gb = c.gb;
     DBS_REQUIRE(c.gb.Cin % bn == 0 || bn % c.gb.Cin == 0, DBS_ERR_ARGUMENT, "wgrad: tile must not straddle (r,s)");
     DBS_REQUIRE(bn <= c.gb.Cin, DBS_ERR_ARGUMENT, "wgrad: BN %d > Cin %d", bn, c.gb.Cin);
+  } else if (c.b_mode == 3) {
+    // filter [Cout][R*S][Cin] viewed as 3-D {Cin, R*S, Cout}: box {64 c, 1 rs, 64 k}
+    EncodeTiledFn fn = encode_fn();
+    DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    DBS_REQUIRE(c.tb.C % 64 == 0 && c.tb.N % 64 == 0 && ((uintptr_t)c.b & 15) == 0, DBS_ERR_ARGUMENT,
+                "dgrad filter view: Cin, Cout multiples of 64 required");
+    cuuint64_t dims[3] = {(cuuint64_t)c.tb.C, (cuuint64_t)c.tb.W, (cuuint64_t)c.tb.N};
+    cuuint64_t strides[2] = {(cuuint64_t)c.tb.C * 2, (cuuint64_t)c.tb.W * c.tb.C * 2};
+    cuuint32_t box[3] = {64, 1, 64};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.b), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (3d filter) failed (%d)", (int)r);
+    DBS_REQUIRE(c.a_mode == 2, DBS_ERR_ARGUMENT, "flipped-filter B needs a conv-mode A");
   } else {
     st = c.b_mode ? make_tmap(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, 64, 64)
                   : make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, (uint32_t)bn);

@@ -26,6 +26,8 @@ struct DriverApi {
   CUresult (*greenStream)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
   CUresult (*pushCtx)(CUcontext) = nullptr;
   CUresult (*popCtx)(CUcontext*) = nullptr;
+  CUresult (*getCurrent)(CUcontext*) = nullptr;
+  CUresult (*ctxGetResource)(CUcontext, CUdevResource*, CUdevResourceType) = nullptr;
   bool ok = false;
 };
 
@@ -47,6 +49,8 @@ DriverApi& api() {
     ok &= get("cuGreenCtxStreamCreate", (void**)&a.greenStream);
     ok &= get("cuCtxPushCurrent", (void**)&a.pushCtx);
     ok &= get("cuCtxPopCurrent", (void**)&a.popCtx);
+    get("cuCtxGetCurrent", (void**)&a.getCurrent);
+    get("cuCtxGetDevResource", (void**)&a.ctxGetResource);
     a.ok = ok;
   });
   return a;
@@ -63,6 +67,25 @@ int ctx_push(void* ctx) {
   CUresult r = a.pushCtx(reinterpret_cast<CUcontext>(ctx));
   DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuCtxPushCurrent failed (%d)", (int)r);
   return DBS_OK;
+}
+
+// SMs available to work launched now: the current (green) context's SM
+// resource, cached per context; the whole device when unknown.
+int current_sm_count() {
+  DriverApi& a = api();
+  static thread_local CUcontext last = nullptr;
+  static thread_local int last_sms = 0;
+  if (!a.getCurrent || !a.ctxGetResource) return num_sms();
+  CUcontext c = nullptr;
+  if (a.getCurrent(&c) != CUDA_SUCCESS || c == nullptr) return num_sms();
+  if (c == last && last_sms > 0) return last_sms;
+  CUdevResource r;
+  memset(&r, 0, sizeof(r));
+  int sms = num_sms();
+  if (a.ctxGetResource(c, &r, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS && r.sm.smCount > 0) sms = (int)r.sm.smCount;
+  last = c;
+  last_sms = sms;
+  return sms;
 }
 
 int ctx_pop(void* ctx) {

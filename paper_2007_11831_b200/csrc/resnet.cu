@@ -570,9 +570,7 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
 // wflip: [Cin][k][k][Cout] scratch; dil: dilated-gradient scratch (stride 2)
 int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t B, uint16_t* dx, int accumulate,
                   uint16_t* wflip, uint16_t* dil, cudaStream_t s) {
-  const int64_t wn = (int64_t)c.cout * c.k * c.k * c.cin;
-  flip_weights_kernel<<<grid_for(wn, 256), 256, 0, s>>>(w, c.cout, c.k, c.k, c.cin, wflip);
-  DBS_LAUNCH_CHECK();
+  (void)wflip;  // the GEMM reads the filter flipped in place (B mode 3): no transpose kernel
   const uint16_t* src = dy;
   int gh = c.OH, gw = c.OW;
   if (c.stride == 2) {
@@ -592,9 +590,9 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
   call.ta = nhwc(B, gh, gw, c.cout);
   // 3x3 pad 1 -> flipped 3x3 pad 1; 1x1 pad 0 -> 1x1 pad 0 (stride 1 over the dilated map)
   call.ga = ConvGeom{c.k, c.k, c.cout / 64, 1, c.k / 2, c.H, c.W, c.cout};
-  call.b_mode = 0;
-  call.b = wflip;
-  call.ldb = call.K;
+  call.b_mode = 3;
+  call.b = w;
+  call.tb = ConvTensor{c.cout, 1, c.k * c.k, c.cin};  // {N=Cout, -, W=R*S, C=Cin} filter view
   call.epi = accumulate ? DBS_EPI_BF16_ACCUM : DBS_EPI_BF16;
   call.d = dx;
   call.ldd = c.cin;
@@ -640,7 +638,7 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
   // split the long pixel reduction so ~2 waves of CTAs are in flight
   const int64_t tiles = ((call.M + 127) / 128) * ((call.N + bn - 1) / bn);
   const int64_t kblocks = (call.K + 63) / 64;
-  int64_t splits = (2 * num_sms() + tiles - 1) / tiles;
+  int64_t splits = (2 * current_sm_count() + tiles - 1) / tiles;
   if (splits > kblocks) splits = kblocks;
   if (splits < 1) splits = 1;
   call.splits = (int)splits;
