@@ -347,11 +347,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           // BN batch statistics: warp column sums -> CTA sums (smem) -> one fp64
           // atomic per column and CTA into the [N] accumulators
           __shared__ float red_s[4][32], red_q[4][32];
-          const float s = warp_colsum(v, lane);
-          float sq[32];
+          // transpose through the (now idle) pipeline shared memory: 32 stores +
+          // 32 loads per statistic instead of 160 shuffles
+          float* tr = reinterpret_cast<float*>(sA) + warp * (32 * 33);
 #pragma unroll
-          for (int j = 0; j < 32; j++) sq[j] = v[j] * v[j];
-          const float q = warp_colsum(sq, lane);
+          for (int j = 0; j < 32; j++) tr[lane * 33 + j] = v[j];
+          __syncwarp();
+          float s = 0.f;
+#pragma unroll
+          for (int r2 = 0; r2 < 32; r2++) s += tr[r2 * 33 + lane];
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; j++) tr[lane * 33 + j] = v[j] * v[j];
+          __syncwarp();
+          float q = 0.f;
+#pragma unroll
+          for (int r2 = 0; r2 < 32; r2++) q += tr[r2 * 33 + lane];
+          __syncwarp();
           red_s[warp][lane] = s;
           red_q[warp][lane] = q;
           __syncthreads();

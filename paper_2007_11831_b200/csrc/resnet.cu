@@ -108,7 +108,7 @@ __global__ void bn_apply_kernel(const uint16_t* __restrict__ y, const float* __r
   const int cv = C / 8;
   const int64_t total = M * cv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % cv) * 8;
+    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;  // C is a power of two (64..512)
     const uint4 q = reinterpret_cast<const uint4*>(y)[i];
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t rw[4] = {0, 0, 0, 0}, dw[4] = {0, 0, 0, 0};
@@ -185,23 +185,24 @@ __global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __re
       }
     }
   }
-  // block reduction over lane_r for each channel
-  for (int idx = threadIdx.x; idx < C; idx += blockDim.x) {
-    red_g[idx] = 0.f;
-    red_b[idx] = 0.f;
-  }
-  __syncthreads();
+  // block reduction over lane_r for each channel: [rows_per_pass][C] partials in
+  // shared memory (no shared-memory atomics), then one global atomic per channel
   if (lane_r < rows_per_pass) {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      atomicAdd(&red_g[c0 + k], sg[k]);
-      atomicAdd(&red_b[c0 + k], sb[k]);
+      red_g[lane_r * C + c0 + k] = sg[k];
+      red_b[lane_r * C + c0 + k] = sb[k];
     }
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < C; idx += blockDim.x) {
-    atomicAdd(&dgamma[idx], red_g[idx]);
-    atomicAdd(&dbeta[idx], red_b[idx]);
+    float a = 0.f, b = 0.f;
+    for (int r = 0; r < rows_per_pass; r++) {
+      a += red_g[r * C + idx];
+      b += red_b[r * C + idx];
+    }
+    atomicAdd(&dgamma[idx], a);
+    atomicAdd(&dbeta[idx], b);
   }
 }
 
@@ -216,7 +217,7 @@ __global__ void bn_bwd_apply_kernel(const uint16_t* __restrict__ gin, const uint
   const int64_t total = M * cv;
   const float invM = 1.0f / (float)M;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % cv) * 8;
+    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;  // C is a power of two (64..512)
     const uint4 qg = reinterpret_cast<const uint4*>(gin)[i];
     const uint4 qy = reinterpret_cast<const uint4*>(y)[i];
     uint4 qm = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
