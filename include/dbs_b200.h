@@ -311,8 +311,9 @@ int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, co
 
 /* Implicit-GEMM convolutions (NHWC bf16, weights [Cout][k][k][Cin] bf16) on the
  * tcgen05 GEMM with 4-D TMA operand loads: y = conv(x, w); dx = dgrad(dy, w)
- * (scratch >= 2*(Cout*k*k*Cin + 64) + 8*N*H*W*Cout bytes); dw += wgrad(dy, x)
- * (fp32, atomically accumulated -- zero it first). */
+ * (d_scratch is unused and may be NULL; stride 2 runs one GEMM per output
+ * parity class); dw += wgrad(dy, x) (fp32, atomically accumulated -- zero it
+ * first). */
 int dbs_dev_conv2d_fwd(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w, int32_t Cout,
                        int32_t k, int32_t stride, int32_t pad, void* d_y, void* stream);
 int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,

@@ -15,12 +15,17 @@
 // with the flipped filter / dZ W) and the weight gradient (dY^T im2col(X))
 // all read activations in place -- no im2col buffers, no transposes.
 //
-// Structure (one 128 x BN output tile per CTA, 4 warps):
-//   warp 0 / lane 0 : TMA producer into a STAGES-deep shared-memory ring;
-//   warp 1 / lane 0 : MMA issuer (4 x tcgen05.mma, UMMA_K = 16, per 64-wide K
-//                     block; tcgen05.commit frees the ring slot);
-//   warp 2          : TMEM allocator (BN fp32 columns);
-//   all 4 warps     : epilogue -- tcgen05.ld 32x32b (thread = output row), fused
+// Structure: a persistent kernel, one CTA per SM, 6 warps, walking the output
+// tiles (128 x BN, x split-K slice) in a static stride over the grid:
+//   warp 0 / lane 0 : TMA producer into a STAGES-deep shared-memory ring that
+//                     runs continuously across tiles;
+//   warp 1          : TMEM allocator (2 x BN fp32 columns: two accumulators);
+//     lane 0        : MMA issuer (4 x tcgen05.mma, UMMA_K = 16, per 64-wide K
+//                     block; tcgen05.commit frees the ring slot / hands the
+//                     accumulator to the epilogue);
+//   warps 2..5      : epilogue of tile t (TMEM lane quadrant = warp % 4) while
+//                     the MMA warp already accumulates tile t+1 into the other
+//                     buffer -- tcgen05.ld 32x32b (thread = output row), fused
 //                     bias / ReLU / ReLU-backward / bf16 cast / accumulate /
 //                     split-K atomic reduction, and per-warp column partial sums
 //                     (bias gradients, BatchNorm batch statistics).
@@ -42,7 +47,21 @@ using namespace sm100;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
-constexpr int kThreads = 128;
+constexpr int kThreads = 192;  // producer warp, MMA warp, 4 epilogue warps
+
+// Development-only timeline probe (-DDBS_GEMM_TRACE, scripts/gemm_trace.cu):
+// per-CTA clock64 stamps of the producer / MMA / epilogue hand-offs.
+#ifdef DBS_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[1024 * 128];
+#define GEMM_TRACE(slot)                                                                    \
+  do {                                                                                      \
+    if ((slot) < 128) g_gemm_trace[blockIdx.x * 128 + (slot)] = (unsigned long long)clock64(); \
+  } while (0)
+#else
+#define GEMM_TRACE(slot) \
+  do {                   \
+  } while (0)
+#endif
 
 struct GemmParams {
   int64_t M, N, K;
@@ -56,7 +75,10 @@ struct GemmParams {
   double* sum_part;     // [N] column sums of the accumulator (fp64 atomics, BN statistics)
   double* sq_part;      // [N] column sums of accumulator^2
   ConvGeom ga, gb;      // implicit-GEMM geometry of A / B in conv mode
-  int kb_per_split;     // K blocks per CTA along grid.z (split-K)
+  int kb_per_split;     // K blocks per split-K slice
+  int splits;           // split-K slices (atomic epilogue when > 1)
+  ConvTaps taps;        // explicit conv taps of A (n = 0: R x S window)
+  OutMap omap;          // strided output rows (on = 0: row-major)
 };
 
 __device__ __forceinline__ uint16_t f2bf(float f) {
@@ -69,11 +91,14 @@ template <int BN>
 struct Cfg {
   static constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
   static constexpr uint32_t kBBytes = BN * kBK * 2;
-  // shallow rings so 2-3 CTAs share an SM: one CTA's epilogue (and prologue)
-  // then overlaps another's TMA/MMA main loop
-  static constexpr int kStages = (BN >= 256) ? 2 : (BN >= 128 ? 3 : (BN >= 64 ? 3 : 4));
-  static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + 256;
+  static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;  // fp32 TMEM columns of one accumulator
+  static constexpr uint32_t kTmemCols = 2 * kAccCols;      // double-buffered: epilogue(t) || MMA(t+1)
+  static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;   // per-epilogue-warp 32x33 transpose scratch
+  // one persistent CTA per SM: the ring takes what is left of the 227 KB
+  static constexpr int kRing = (int)((212u * 1024u - kEpiBytes) / (kABytes + kBBytes));
+  static constexpr int kStages = kRing > 8 ? 8 : kRing;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiBytes + 256;
+  static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int& n, int& oh, int& ow) {
@@ -84,9 +109,106 @@ __device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int
   ow = rem - oh * g.OW;
 }
 
+__device__ __forceinline__ void ld_bf16x32(const uint16_t* src, float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const uint4 q = *reinterpret_cast<const uint4*>(src + j);
+    x[j + 0] = bf2f(q.x & 0xFFFF); x[j + 1] = bf2f(q.x >> 16);
+    x[j + 2] = bf2f(q.y & 0xFFFF); x[j + 3] = bf2f(q.y >> 16);
+    x[j + 4] = bf2f(q.z & 0xFFFF); x[j + 5] = bf2f(q.z >> 16);
+    x[j + 6] = bf2f(q.w & 0xFFFF); x[j + 7] = bf2f(q.w >> 16);
+  }
+}
+__device__ __forceinline__ void ld_f32x32(const float* src, float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 4) {
+    const float4 q = *reinterpret_cast<const float4*>(src + j);
+    x[j] = q.x; x[j + 1] = q.y; x[j + 2] = q.z; x[j + 3] = q.w;
+  }
+}
+
 template <int BN>
-__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row, int64_t n_base, const float* v,
-                                               int cnt, float* v_out) {
+__device__ void epilogue_chunk_generic(const GemmParams& p, int64_t row, int64_t n_base, const float* v, int cnt,
+                                       float* v_out);
+
+// One thread's 32 consecutive outputs of one row.  Full, aligned chunks take a
+// branch-free vector path per epilogue kind (the common case: every conv / MLP
+// hidden layer); ragged or unaligned chunks fall back to the per-element path.
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row, int64_t n_base, float (&v)[32],
+                                               int cnt, float (&vo)[32]) {
+  const int epi = p.epi;
+  const bool f32_out = (epi == DBS_EPI_F32 || epi == DBS_EPI_F32_ACCUM || epi == DBS_EPI_BIAS_F32 ||
+                        epi == DBS_EPI_F32_ATOMIC);
+  const int align_elems = f32_out ? 4 : 8;
+  const bool fast = (cnt == 32) && (p.ldd % align_elems == 0) &&
+                    ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0) && (p.aux == nullptr || ((reinterpret_cast<uintptr_t>(p.aux) & 15) == 0)) &&
+                    (p.bias == nullptr || ((reinterpret_cast<uintptr_t>(p.bias) & 15) == 0));
+  if (!fast) {
+    epilogue_chunk_generic<BN>(p, row, n_base, v, cnt, vo);
+    return;
+  }
+  float x[32];
+#pragma unroll
+  for (int j = 0; j < 32; j++) x[j] = v[j];
+  if (epi == DBS_EPI_BIAS_F32 || epi == DBS_EPI_BIAS_RELU_BF16) {
+    float bb[32];
+    ld_f32x32(p.bias + n_base, bb);
+#pragma unroll
+    for (int j = 0; j < 32; j++) x[j] += bb[j];
+  }
+  if (f32_out) {
+    float* d = reinterpret_cast<float*>(p.d) + row * p.ldd + n_base;
+    if (epi == DBS_EPI_F32_ACCUM) {
+      float prev[32];
+      ld_f32x32(d, prev);
+#pragma unroll
+      for (int j = 0; j < 32; j++) x[j] += prev[j];
+    }
+    if (epi == DBS_EPI_F32_ATOMIC) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        atomicAdd(reinterpret_cast<float4*>(d + j), make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+    }
+  } else {
+    uint16_t* d = reinterpret_cast<uint16_t*>(p.d) + row * p.ldd + n_base;
+    if (epi == DBS_EPI_BIAS_RELU_BF16) {
+#pragma unroll
+      for (int j = 0; j < 32; j++) x[j] = fmaxf(x[j], 0.0f);
+    } else if (epi == DBS_EPI_RELU_GRAD_BF16) {
+      float a[32];
+      ld_bf16x32(p.aux + row * p.ldd + n_base, a);
+#pragma unroll
+      for (int j = 0; j < 32; j++) x[j] = a[j] > 0.0f ? x[j] : 0.0f;
+    } else if (epi == DBS_EPI_BF16_ACCUM) {
+      float prev[32];
+      ld_bf16x32(d, prev);
+#pragma unroll
+      for (int j = 0; j < 32; j++) x[j] += prev[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 q;
+      q.x = f2bf(x[j + 0]) | ((uint32_t)f2bf(x[j + 1]) << 16);
+      q.y = f2bf(x[j + 2]) | ((uint32_t)f2bf(x[j + 3]) << 16);
+      q.z = f2bf(x[j + 4]) | ((uint32_t)f2bf(x[j + 5]) << 16);
+      q.w = f2bf(x[j + 6]) | ((uint32_t)f2bf(x[j + 7]) << 16);
+#ifdef DBS_GEMM_NOSTORE
+      if (q.x == 0x12345678u && q.y == 0x9abcdef0u)
+#endif
+      *reinterpret_cast<uint4*>(d + j) = q;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; j++) vo[j] = x[j];
+}
+
+template <int BN>
+__device__ void epilogue_chunk_generic(const GemmParams& p, int64_t row, int64_t n_base, const float* v, int cnt,
+                                       float* v_out) {
   const int64_t N = p.N;
   const bool full = (n_base + cnt <= N);
   switch (p.epi) {
@@ -106,23 +228,26 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
       }
       const bool vec = full && cnt == 32 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0);
       if (p.epi == DBS_EPI_F32_ACCUM) {
-        for (int j = 0; j < cnt; j++)
-          if (n_base + j < N) d[j] += o[j];
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+          if (j < cnt && n_base + j < N) d[j] += o[j];
       } else if (p.epi == DBS_EPI_F32_ATOMIC) {
         if (vec) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             atomicAdd(reinterpret_cast<float4*>(d + j), make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]));
         } else {
-          for (int j = 0; j < cnt; j++)
-            if (n_base + j < N) atomicAdd(d + j, o[j]);
+#pragma unroll
+          for (int j = 0; j < 32; j++)
+            if (j < cnt && n_base + j < N) atomicAdd(d + j, o[j]);
         }
       } else if (vec) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
       } else {
-        for (int j = 0; j < cnt; j++)
-          if (n_base + j < N) d[j] = o[j];
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+          if (j < cnt && n_base + j < N) d[j] = o[j];
       }
       break;
     }
@@ -145,7 +270,8 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
             prev[j + 6] = bf2f(q.w & 0xFFFF); prev[j + 7] = bf2f(q.w >> 16);
           }
         } else {
-          for (int j = 0; j < cnt; j++) prev[j] = (n_base + j < N) ? bf2f(d[j]) : 0.0f;
+#pragma unroll
+          for (int j = 0; j < 32; j++) prev[j] = (j < cnt && n_base + j < N) ? bf2f(d[j]) : 0.0f;
         }
       }
       uint16_t o[32];
@@ -175,8 +301,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
           *reinterpret_cast<uint4*>(d + j) = q;
         }
       } else {
-        for (int j = 0; j < cnt; j++)
-          if (n_base + j < N) d[j] = o[j];
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+          if (j < cnt && n_base + j < N) d[j] = o[j];
       }
       break;
     }
@@ -184,6 +311,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
       break;
   }
 }
+
+// named barrier over the 4 epilogue warps (the producer / MMA warps never join)
+__device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // transpose-reduce 32 rows x 32 columns across the warp: lane j gets column j's sum
 __device__ __forceinline__ float warp_colsum(float (&x)[32], int lane) {
@@ -206,20 +336,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  float* sEpi = reinterpret_cast<float*>(sB + C::kStages * C::kBBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + C::kEpiBytes);
   uint64_t* empty = full + C::kStages;
-  uint64_t* tmem_full = empty + C::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + C::kStages;  // [2] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2;       // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * kBM, n0 = (int64_t)blockIdx.y * BN;
+  if (threadIdx.x == 0) GEMM_TRACE(0);
+  const int64_t m_tiles = (p.M + kBM - 1) / kBM;
+  const int64_t n_tiles = (p.N + BN - 1) / BN;
+  const int64_t num_tiles = m_tiles * n_tiles * p.splits;
   const int num_k_total = (int)((p.K + kBK - 1) / kBK);
-  const int kb_begin = (int)blockIdx.z * p.kb_per_split;
-  int kb_end = kb_begin + p.kb_per_split;
-  if (kb_end > num_k_total) kb_end = num_k_total;
-  const int num_k = kb_end > kb_begin ? kb_end - kb_begin : 0;
   const int a_mn = (p.a_mode == 1) ? 1 : 0;
   const int b_mn = (p.b_mode >= 1) ? 1 : 0;
+  // tile t -> (m tile fastest, then n tile, then split-K slice): the tiles
+  // resident at one time share their B block (and neighbouring A windows) in L2
+  auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& kb_begin) -> int {
+    const int64_t rest = t / m_tiles;
+    m0 = (t - rest * m_tiles) * kBM;
+    const int64_t split = rest / n_tiles;
+    n0 = (rest - split * n_tiles) * BN;
+    kb_begin = (int)split * p.kb_per_split;
+    const int kb_end = min(kb_begin + p.kb_per_split, num_k_total);
+    return kb_end > kb_begin ? kb_end - kb_begin : 0;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -228,17 +370,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_TRACE(1);
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
+  if (warp == 0) {
+    if (lane == 0) {
+   // ---------------- TMA producer ----------------
+   uint32_t it = 0;  // ring position, continuous across tiles
+   uint32_t pt = 0;
+   (void)pt;
+   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    int64_t m0, n0;
+    int kb_begin;
+    const int num_k = decode(t, m0, n0, kb_begin);
     int a_n = 0, a_oh = 0, a_ow = 0;
     if (p.a_mode == 2) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
     int b_r = 0, b_s = 0, b_c0 = 0;
@@ -248,10 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       b_r = rs / p.gb.S;
       b_s = rs - b_r * p.gb.S;
     }
-    for (int i = 0; i < num_k; i++) {
+    if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
+    for (int i = 0; i < num_k; i++, it++) {
       const int kb = kb_begin + i;
-      const int s = i % C::kStages;
-      if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
+      const int s = (int)(it % C::kStages);
+      mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], C::kABytes + C::kBBytes);
       const int32_t k0 = kb * kBK;
       uint8_t* a = sA + s * C::kABytes;
@@ -265,8 +420,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const ConvGeom& g = p.ga;
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
-        const int r = rs / g.S, sx = rs - r * g.S;
-        tma_load_4d(a, &tmA, &full[s], cb * 64, a_ow * g.stride + sx - g.pad, a_oh * g.stride + r - g.pad, a_n);
+        int ah, aw;
+        if (p.taps.n > 0) {
+          ah = a_oh + p.taps.dh[rs];
+          aw = a_ow + p.taps.dw[rs];
+        } else {
+          const int r = rs / g.S, sx = rs - r * g.S;
+          ah = a_oh * g.stride + r - g.pad;
+          aw = a_ow * g.stride + sx - g.pad;
+        }
+        tma_load_4d(a, &tmA, &full[s], cb * 64, aw, ah, a_n);
       }
       if (p.b_mode == 0) {
         tma_load_2d(b, &tmB, &full[s], k0, (int32_t)n0);
@@ -280,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         const int r = rs / g.S, sx = rs - r * g.S;
-        const int rs_flip = (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+        const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
 #pragma unroll
         for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
       } else {
@@ -293,33 +456,67 @@ __global__ void __launch_bounds__(kThreads, 1)
                       boh * g.stride + b_r - g.pad, bn_);
       }
     }
-  } else if (warp == 1 && lane == 0) {
+   }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = make_idesc_bf16(kBM, BN, a_mn, b_mn);
-    for (int i = 0; i < num_k; i++) {
-      const int s = i % C::kStages;
-      mbar_wait(&full[s], (i / C::kStages) & 1);
+    uint32_t it = 0, j = 0;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int64_t m0, n0;
+      int kb_begin;
+      const int num_k = decode(t, m0, n0, kb_begin);
+      if (num_k == 0) continue;
+      const int b = (int)(j & 1);
+      mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+      GEMM_TRACE(12 + j);
       tc_fence_after();
-      const uint32_t a_base = smem_u32(sA + s * C::kABytes);
-      const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
+      const uint32_t d_tmem = tmem_base + b * C::kAccCols;
+      for (int i = 0; i < num_k; i++, it++) {
+        const int s = (int)(it % C::kStages);
+        mbar_wait(&full[s], (it / C::kStages) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sA + s * C::kABytes);
+        const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
 #pragma unroll
-      for (int k = 0; k < kBK / 16; k++) {
-        const uint64_t ad = a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
-        const uint64_t bd = b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
-        mma_bf16_ss(tmem_base, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
+        for (int k = 0; k < kBK / 16; k++) {
+          const uint64_t ad = a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+          const uint64_t bd = b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+          mma_bf16_ss(d_tmem, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
       }
-      mma_commit(&empty[s]);
+      mma_commit(&acc_full[b]);
+      GEMM_TRACE(22 + j);
+      j++;
     }
-    if (num_k > 0) mma_commit(tmem_full);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue (all 4 warps) ----------------
-  if (num_k > 0) {
-    mbar_wait(tmem_full, 0);
+    }
+    __syncwarp();
+  } else {
+  // ---------------- epilogue (warps 2..5) ----------------
+  const int q = warp & 3;  // the TMEM lane quadrant this warp may access
+  float* tr = sEpi + (warp - 2) * (32 * 33);
+  uint32_t tj = 0;
+  for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    int64_t m0, n0;
+    int kb_begin;
+    if (decode(t, m0, n0, kb_begin) == 0) continue;
+    const int b = (int)(tj & 1);
+    mbar_wait(&acc_full[b], (tj >> 1) & 1);
+    if (warp == 2 && lane == 0) GEMM_TRACE(32 + tj);
     tc_fence_after();
-    const int64_t row = m0 + warp * 32 + lane;
-    const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
+    const int64_t row = m0 + q * 32 + lane;
+    int64_t orow = row;  // the output row this thread writes
+    if (p.omap.on && row < p.M) {
+      const int64_t hw = (int64_t)p.omap.OH * p.omap.OW;
+      const int64_t img = row / hw;
+      const int rem = (int)(row - img * hw);
+      const int i = rem / p.omap.OW, jj = rem - i * p.omap.OW;
+      orow = (img * p.omap.H + 2 * i + p.omap.a) * p.omap.W + 2 * jj + p.omap.b;
+    }
+    const uint32_t lane_addr = tmem_base + b * C::kAccCols + ((uint32_t)(q * 32) << 16);
     const bool stats = (p.sum_part != nullptr);
     if (BN >= 32) {
 #pragma unroll 1
@@ -327,71 +524,85 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(lane_addr + c * 32, r);
         tmem_ld_wait();
+        if (warp == 2 && lane == 0 && tj < 8) GEMM_TRACE(64 + 4 * tj + 2 * c);
+        if (c == BN / 32 - 1) {
+          // accumulator fully in registers: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[b]);
+          if (warp == 2 && lane == 0) GEMM_TRACE(42 + tj);
+        }
         const int64_t n_base = n0 + c * 32;
         if (n_base >= p.N) continue;  // warp-uniform
         float v[32], vo[32];
 #pragma unroll
-        for (int j = 0; j < 32; j++) {
-          v[j] = (row < p.M) ? __uint_as_float(r[j]) : 0.0f;
-          vo[j] = 0.0f;
+        for (int k = 0; k < 32; k++) {
+          v[k] = (row < p.M) ? __uint_as_float(r[k]) : 0.0f;
+          vo[k] = 0.0f;
         }
         const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
-        if (row < p.M) epilogue_chunk<BN>(p, row, n_base, v, cnt, vo);
-        const int64_t g = (m0 >> 5) + warp;
-        const bool group_live = (m0 + warp * 32 < p.M);
+        if (row < p.M) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
+        if (warp == 2 && lane == 0 && tj < 8) GEMM_TRACE(64 + 4 * tj + 2 * c + 1);
         if (p.colsum_part != nullptr) {
+          const int64_t g = (m0 >> 5) + q;
+          const bool group_live = (m0 + q * 32 < p.M);
           const float s = warp_colsum(vo, lane);
           if (lane < cnt && group_live) p.colsum_part[g * p.N + n_base + lane] = s;
         }
         if (stats) {
-          // BN batch statistics: warp column sums -> CTA sums (smem) -> one fp64
-          // atomic per column and CTA into the [N] accumulators
+          // BN batch statistics: warp column sums (a 32x33 transpose in shared
+          // memory: 32 stores + 32 loads instead of 160 shuffles) -> tile sums
+          // over the 4 epilogue warps -> one fp64 atomic per column and tile
           __shared__ float red_s[4][32], red_q[4][32];
-          // transpose through the (now idle) pipeline shared memory: 32 stores +
-          // 32 loads per statistic instead of 160 shuffles
-          float* tr = reinterpret_cast<float*>(sA) + warp * (32 * 33);
 #pragma unroll
-          for (int j = 0; j < 32; j++) tr[lane * 33 + j] = v[j];
+          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = v[k];
           __syncwarp();
           float s = 0.f;
 #pragma unroll
           for (int r2 = 0; r2 < 32; r2++) s += tr[r2 * 33 + lane];
           __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; j++) tr[lane * 33 + j] = v[j] * v[j];
+          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = v[k] * v[k];
           __syncwarp();
-          float q = 0.f;
+          float sq = 0.f;
 #pragma unroll
-          for (int r2 = 0; r2 < 32; r2++) q += tr[r2 * 33 + lane];
+          for (int r2 = 0; r2 < 32; r2++) sq += tr[r2 * 33 + lane];
           __syncwarp();
-          red_s[warp][lane] = s;
-          red_q[warp][lane] = q;
-          __syncthreads();
-          if (warp == 0 && lane < cnt) {
+          red_s[q][lane] = s;
+          red_q[q][lane] = sq;
+          epilogue_bar();
+          if (warp == 2 && lane < cnt) {
             const double ts = (double)red_s[0][lane] + red_s[1][lane] + red_s[2][lane] + red_s[3][lane];
             const double tq = (double)red_q[0][lane] + red_q[1][lane] + red_q[2][lane] + red_q[3][lane];
             atomicAdd(p.sum_part + n_base + lane, ts);
             atomicAdd(p.sq_part + n_base + lane, tq);
           }
-          __syncthreads();
+          epilogue_bar();
         }
       }
     } else {
       uint32_t r[16];
       tmem_ld_32x32b_x16(lane_addr, r);
       tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
       if (row < p.M && n0 < p.N) {
         float v[32], vo[32];
 #pragma unroll
-        for (int j = 0; j < 16; j++) v[j] = __uint_as_float(r[j]);
+        for (int k = 0; k < 16; k++) v[k] = __uint_as_float(r[k]);
         const int cnt = (int)((p.N - n0) < 16 ? (p.N - n0) : 16);
-        epilogue_chunk<BN>(p, row, n0, v, cnt, vo);
+        epilogue_chunk<BN>(p, orow, n0, v, cnt, vo);
       }
     }
+    if (warp == 2 && lane == 0) GEMM_TRACE(52 + tj);
+    tj++;
+  }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem_base);
+  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem_base);
+  if (threadIdx.x == 0) GEMM_TRACE(63);
 }
 
 // ---------------------------------------------------------------------------
@@ -503,8 +714,13 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
     DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
     if (nseen < 16) seen[nseen++] = ctx;
   }
-  dim3 grid((unsigned)((p.M + kBM - 1) / kBM), (unsigned)((p.N + BN - 1) / BN), (unsigned)splits);
-  gemm_bf16_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, p);
+  GemmParams q = p;
+  q.splits = splits;
+  // persistent: one CTA per SM of the current (possibly green) context
+  const int64_t tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
+  const int64_t sms = current_sm_count();
+  const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  gemm_bf16_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, q);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -588,14 +804,27 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   p.aux = c.aux;
   p.sum_part = c.sum_part;
   p.sq_part = c.sq_part;
+  p.taps = c.taps;
+  p.omap = c.omap;
   p.colsum_part = nullptr;
   int st;
   int bn = (c.bn_override > 0) ? c.bn_override : pick_bn(c.N, c.b_mode);
-  if (c.bn_override <= 0 && c.b_mode != 2) {
-    // narrower N tiles when the grid would not cover the SMs this launch can use
-    const int sms = current_sm_count();
+  if (c.bn_override <= 0 && c.b_mode != 2 && bn >= 64) {
+    // N tile from a load-bound cost model of the persistent kernel: rounds of
+    // tiles over the SMs this launch can use x shared-memory bytes per tile
+    const int64_t sms = current_sm_count();
     const int64_t mt = (c.M + kBM - 1) / kBM;
-    while (bn > 64 && mt * ((c.N + bn - 1) / bn) < sms) bn /= 2;
+    int64_t best = -1;
+    int pick = bn;
+    for (int cand = bn; cand >= 64; cand /= 2) {
+      const int64_t tiles = mt * ((c.N + cand - 1) / cand);
+      const int64_t cost = ((tiles + sms - 1) / sms) * (int64_t)(kBM * kBK * 2 + cand * kBK * 2);
+      if (best < 0 || cost < best) {
+        best = cost;
+        pick = cand;
+      }
+    }
+    bn = pick;
   }
   // ---- A ----
   p.a_mode = c.a_mode;
@@ -652,6 +881,12 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
 }
 
 }  // namespace dbs
+
+#ifdef DBS_GEMM_TRACE
+extern "C" int dbs_gemm_trace_copy(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, dbs::g_gemm_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, const void* d_b, int32_t b_major,
                                  int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N, int64_t K,

@@ -21,6 +21,23 @@ struct ConvTensor {
   int N, H, W, C;
 };
 
+// Explicit tap list of a conv-mode A operand (the stride-2 input gradient,
+// one GEMM per output parity class): per tap the A window offset on the input
+// grid and the filter slice (r * S + s) read by B mode 3.  n = 0: the R x S
+// window of ConvGeom.
+struct ConvTaps {
+  int n;
+  int8_t dh[9], dw[9];
+  uint8_t rs[9];
+};
+
+// Strided output rows: GEMM row (img, i, j) of an OH x OW grid is written to
+// output pixel (img, 2i + a, 2j + b) of an H x W map.  on = 0: row-major rows.
+struct OutMap {
+  int on;
+  int H, W, a, b, OH, OW;
+};
+
 struct ConvCall {
   int64_t M, N, K;
   int a_mode, b_mode;        // 0 K-major 2-D, 1 MN-major 2-D, 2 conv 4-D
@@ -39,8 +56,10 @@ struct ConvCall {
   const uint16_t* aux;
   double* sum_part;          // BN batch statistics: [N] fp64 accumulators of sum / sum of squares
   double* sq_part;
-  int splits;                // split-K CTAs along grid.z (atomic epilogue)
+  int splits;                // split-K slices (atomic epilogue)
   int bn_override;           // force the N tile (0 = auto)
+  ConvTaps taps;
+  OutMap omap;
 };
 
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,

@@ -240,38 +240,6 @@ __global__ void bn_bwd_apply_kernel(const uint16_t* __restrict__ gin, const uint
   }
 }
 
-// dilate a stride-2 output gradient: u[n][2i][2j][c] = dy[n][i][j][c], 0 elsewhere
-__global__ void dilate2_kernel(const uint16_t* __restrict__ dy, int64_t N, int OH, int OW, int C,
-                               uint16_t* __restrict__ u) {
-  const int H = 2 * OH, W = 2 * OW, cv = C / 8;
-  const int64_t total = N * H * W * cv;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)(i % cv);
-    const int64_t pix = i / cv;
-    const int w = (int)(pix % W), h = (int)((pix / W) % H);
-    const int64_t n = pix / ((int64_t)H * W);
-    uint4 q = make_uint4(0, 0, 0, 0);
-    if (!(h & 1) && !(w & 1)) q = reinterpret_cast<const uint4*>(dy)[((n * OH + (h >> 1)) * OW + (w >> 1)) * cv + v];
-    reinterpret_cast<uint4*>(u)[i] = q;
-  }
-}
-
-// dgrad filter: Wt[c][r][s][k] = W[k][R-1-r][S-1-s][c]  (bf16)
-__global__ void flip_weights_kernel(const uint16_t* __restrict__ w, int Cout, int R, int S, int Cin,
-                                    uint16_t* __restrict__ wt) {
-  const int64_t total = (int64_t)Cout * R * S * Cin;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    // i indexes the output Wt[c][r][s][k] with k fastest
-    const int k = (int)(i % Cout);
-    int64_t rest = i / Cout;
-    const int s = (int)(rest % S);
-    rest /= S;
-    const int r = (int)(rest % R);
-    const int c = (int)(rest / R);
-    wt[i] = w[(((int64_t)k * R + (R - 1 - r)) * S + (S - 1 - s)) * Cin + c];
-  }
-}
-
 // head forward+backward, one CTA per sample: global average pool of the 4x4x512
 // map, FC 512 -> C, softmax cross-entropy; writes dlogits/B, feat, the pooled-
 // map gradient dOut = (dlogits W)/16, and the per-sample loss.
@@ -380,8 +348,6 @@ struct dbs_resnet {
   uint16_t* g1 = nullptr;
   uint16_t* g2 = nullptr;
   uint16_t* g3 = nullptr;
-  uint16_t* dil = nullptr;                 // dilated gradient (stride-2 dgrad)
-  uint16_t* wflip = nullptr;               // flipped weights (largest conv)
   float* feat = nullptr;                   // [B][512]
   float* dlog = nullptr;                   // [B][16]
   float* loss_per = nullptr;               // [B]
@@ -481,8 +447,6 @@ int alloc_all(dbs_resnet* m) {
   A((void**)&m->g1, max_act * 2);
   A((void**)&m->g2, max_act * 2);
   A((void**)&m->g3, max_act * 2);
-  A((void**)&m->dil, max_act * 2 * 4);
-  A((void**)&m->wflip, (size_t)512 * 9 * 512 * 2);
   A((void**)&m->feat, (size_t)B * 512 * 4);
   A((void**)&m->dlog, (size_t)B * 16 * 4);
   A((void**)&m->loss_per, (size_t)B * 4);
@@ -568,42 +532,73 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
 }
 
 // dX (+)= dgrad of conv c from dy; accumulate selects the bf16 accumulate epilogue.
-// wflip: [Cin][k][k][Cout] scratch; dil: dilated-gradient scratch (stride 2)
 int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t B, uint16_t* dx, int accumulate,
-                  uint16_t* wflip, uint16_t* dil, cudaStream_t s) {
-  (void)wflip;  // the GEMM reads the filter flipped in place (B mode 3): no transpose kernel
-  const uint16_t* src = dy;
-  int gh = c.OH, gw = c.OW;
-  if (c.stride == 2) {
-    const int64_t total = B * (2 * c.OH) * (2 * c.OW) * (c.cout / 8);
-    dilate2_kernel<<<grid_for(total, 256), 256, 0, s>>>(dy, B, c.OH, c.OW, c.cout, dil);
-    DBS_LAUNCH_CHECK();
-    src = dil;
-    gh = 2 * c.OH;
-    gw = 2 * c.OW;
-  }
+                  cudaStream_t s) {
+  // the GEMM reads the filter flipped and transposed in place (B mode 3)
   ConvCall call{};
-  call.M = B * c.H * c.W;
   call.N = c.cin;
-  call.K = (int64_t)c.k * c.k * c.cout;
   call.a_mode = 2;
-  call.a = src;
-  call.ta = nhwc(B, gh, gw, c.cout);
-  // 3x3 pad 1 -> flipped 3x3 pad 1; 1x1 pad 0 -> 1x1 pad 0 (stride 1 over the dilated map)
-  call.ga = ConvGeom{c.k, c.k, c.cout / 64, 1, c.k / 2, c.H, c.W, c.cout};
+  call.a = dy;
+  call.ta = nhwc(B, c.OH, c.OW, c.cout);
   call.b_mode = 3;
   call.b = w;
   call.tb = ConvTensor{c.cout, 1, c.k * c.k, c.cin};  // {N=Cout, -, W=R*S, C=Cin} filter view
   call.epi = accumulate ? DBS_EPI_BF16_ACCUM : DBS_EPI_BF16;
   call.d = dx;
   call.ldd = c.cin;
-  return conv_gemm(call, s);
+  if (c.stride == 1) {
+    // stride 1: the flipped filter over dY, same padding
+    call.M = B * c.H * c.W;
+    call.K = (int64_t)c.k * c.k * c.cout;
+    call.ga = ConvGeom{c.k, c.k, c.cout / 64, 1, c.k / 2, c.H, c.W, c.cout};
+    return conv_gemm(call, s);
+  }
+  // stride 2: one GEMM per output parity class (a, b).  dX(2i+a, 2j+b) gathers
+  // only the taps with r = a + pad (mod 2), s = b + pad (mod 2), each reading
+  // dY at (i + (a + pad - r) / 2, j + (b + pad - s) / 2): no zero-dilated dY,
+  // no multiplications by the zeros of the dilation.
+  DBS_REQUIRE(c.stride == 2 && c.H == 2 * c.OH && c.W == 2 * c.OW, DBS_ERR_ARGUMENT,
+              "conv dgrad: stride 2 needs even input extents");
+  const int pad = c.k / 2;
+  bool empty_class = false;
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++) {
+      int n = 0;
+      for (int r = 0; r < c.k; r++)
+        for (int q = 0; q < c.k; q++)
+          if (((a + pad - r) & 1) == 0 && ((b + pad - q) & 1) == 0) n++;
+      if (n == 0) empty_class = true;
+    }
+  if (empty_class && !accumulate)
+    DBS_CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(uint16_t) * (size_t)(B * c.H * c.W * c.cin), s));
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++) {
+      ConvTaps t{};
+      for (int r = 0; r < c.k; r++)
+        for (int q = 0; q < c.k; q++) {
+          if (((a + pad - r) & 1) != 0 || ((b + pad - q) & 1) != 0) continue;
+          t.dh[t.n] = (int8_t)((a + pad - r) / 2);
+          t.dw[t.n] = (int8_t)((b + pad - q) / 2);
+          t.rs[t.n] = (uint8_t)(r * c.k + q);
+          t.n++;
+        }
+      if (t.n == 0) continue;
+      ConvCall cc = call;
+      cc.M = B * c.OH * c.OW;
+      cc.K = (int64_t)t.n * c.cout;
+      cc.ga = ConvGeom{1, t.n, c.cout / 64, 1, 0, c.OH, c.OW, c.cout};
+      cc.taps = t;
+      cc.omap = OutMap{1, c.H, c.W, a, b, c.OH, c.OW};
+      int st = conv_gemm(cc, s);
+      if (st) return st;
+    }
+  return DBS_OK;
 }
 
 int conv_dgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* wb, int64_t B, uint16_t* dx, int accumulate,
                cudaStream_t s) {
   const Conv& c = m->convs[ci];
-  return conv_dgrad_ex(c, dy, wb + c.w_off, B, dx, accumulate, m->wflip, m->dil, s);
+  return conv_dgrad_ex(c, dy, wb + c.w_off, B, dx, accumulate, s);
 }
 
 // dW of conv c (fp32 atomics into dw) from dy and the conv input x (stem: im2col columns)
@@ -636,10 +631,11 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
     bn = c.cin >= 256 ? 256 : c.cin;
     call.bn_override = bn;
   }
-  // split the long pixel reduction so ~2 waves of CTAs are in flight
+  // split the long pixel reduction so the persistent GEMM's one round of
+  // tiles x splits just fits the SMs this launch can use
   const int64_t tiles = ((call.M + 127) / 128) * ((call.N + bn - 1) / bn);
   const int64_t kblocks = (call.K + 63) / 64;
-  int64_t splits = (2 * current_sm_count() + tiles - 1) / tiles;
+  int64_t splits = current_sm_count() / tiles;
   if (splits > kblocks) splits = kblocks;
   if (splits < 1) splits = 1;
   call.splits = (int)splits;
@@ -701,12 +697,11 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const flo
     uint16_t* tmp = bufs[2];
     // BN2 backward with the output ReLU mask; masked gradient g -> gx (identity) or tmp (ds)
     if ((st = bn_bwd(m, b.c2, pf, grad, gcur, out, B, dy2, b.ds >= 0 ? tmp : gx, s))) return st;
+    uint16_t* dyd = gcur;  // gcur is free once tmp holds the masked gradient
     if (b.ds >= 0) {
-      // BN_ds backward on the same masked gradient, dgrad of the 1x1 stride-2 conv -> gx
-      uint16_t* dyd = gcur;  // gcur is free once tmp holds the masked gradient
+      // BN_ds backward on the same masked gradient and the 1x1 stride-2 conv's weight gradient
       if ((st = bn_bwd(m, b.ds, pf, grad, tmp, nullptr, B, dyd, nullptr, s))) return st;
       if ((st = conv_wgrad(m, b.ds, dyd, blk_in[i], B, grad, s))) return st;
-      if ((st = conv_dgrad(m, b.ds, dyd, wb, B, gx, 0, s))) return st;
     }
     // conv2: wgrad (input a1) and dgrad -> da1 (tmp)
     if ((st = conv_wgrad(m, b.c2, dy2, m->a[b.c1], B, grad, s))) return st;
@@ -715,7 +710,14 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const flo
     uint16_t* dy1 = dy2;
     if ((st = bn_bwd(m, b.c1, pf, grad, tmp, m->a[b.c1], B, dy1, nullptr, s))) return st;
     if ((st = conv_wgrad(m, b.c1, dy1, blk_in[i], B, grad, s))) return st;
-    if ((st = conv_dgrad(m, b.c1, dy1, wb, B, gx, 1, s))) return st;  // accumulate onto the shortcut gradient
+    if (b.ds >= 0) {
+      // the 3x3 stride-2 dgrad covers every input pixel; the 1x1 stride-2
+      // shortcut dgrad (even pixels only) then accumulates onto it
+      if ((st = conv_dgrad(m, b.c1, dy1, wb, B, gx, 0, s))) return st;
+      if ((st = conv_dgrad(m, b.ds, dyd, wb, B, gx, 1, s))) return st;
+    } else {
+      if ((st = conv_dgrad(m, b.c1, dy1, wb, B, gx, 1, s))) return st;  // accumulate onto the shortcut gradient
+    }
     // rotate: gx becomes the next gcur
     uint16_t* old = gcur;
     gcur = gx;
@@ -767,8 +769,6 @@ extern "C" int dbs_resnet_destroy(dbs_resnet* m) {
   cudaFree(m->g1);
   cudaFree(m->g2);
   cudaFree(m->g3);
-  cudaFree(m->dil);
-  cudaFree(m->wflip);
   cudaFree(m->feat);
   cudaFree(m->dlog);
   cudaFree(m->loss_per);
@@ -846,10 +846,9 @@ extern "C" int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int3
   DBS_REQUIRE(Cin % 8 == 0 && Cout % 64 == 0 && (stride == 1 || stride == 2) && pad == k / 2, DBS_ERR_ARGUMENT,
               "conv2d_dgrad: Cout %% 64, stride 1/2, same padding required");
   const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
-  uint16_t* wflip = static_cast<uint16_t*>(d_scratch);
-  uint16_t* dil = wflip + (((int64_t)Cout * k * k * Cin + 63) & ~int64_t(63));
+  (void)d_scratch;  // no scratch since the stride-2 path runs per parity class
   return conv_dgrad_ex(c, static_cast<const uint16_t*>(d_dy), static_cast<const uint16_t*>(d_w), N,
-                       static_cast<uint16_t*>(d_dx), 0, wflip, dil, as_stream(stream));
+                       static_cast<uint16_t*>(d_dx), 0, as_stream(stream));
 }
 
 extern "C" int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin,

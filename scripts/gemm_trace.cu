@@ -1,0 +1,36 @@
+// Dev probe: timeline of the persistent tcgen05 GEMM (build with scripts/build_gemm_trace.sh).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <vector>
+#include "dbs_b200.h"
+extern "C" int dbs_gemm_trace_copy(unsigned long long* host, int n);
+int main(int argc, char** argv) {
+  long M = argc > 1 ? atol(argv[1]) : 131072, N = argc > 2 ? atol(argv[2]) : 64, K = argc > 3 ? atol(argv[3]) : 64;
+  void *a, *b, *d;
+  cudaMalloc(&a, M * K * 2); cudaMalloc(&b, N * K * 2); cudaMalloc(&d, M * N * 2);
+  cudaMemset(a, 0x3c, M * K * 2); cudaMemset(b, 0x3c, N * K * 2);
+  for (int i = 0; i < 5; i++)
+    if (dbs_dev_gemm_bf16(a, 0, K, b, 0, K, d, N, M, N, K, DBS_EPI_BF16, nullptr, nullptr, nullptr)) { printf("err %s\n", dbs_last_error()); return 1; }
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  dbs_dev_gemm_bf16(a, 0, K, b, 0, K, d, N, M, N, K, DBS_EPI_BF16, nullptr, nullptr, nullptr);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  printf("M=%ld N=%ld K=%ld: %.1f us  err=%s\n", M, N, K, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
+  std::vector<unsigned long long> t(1024 * 128);
+  dbs_gemm_trace_copy(t.data(), 1024 * 128);
+  for (int c : {0, 147}) {
+    unsigned long long* r = &t[c * 128];
+    unsigned long long t0 = r[0];
+    printf("CTA %d: setup %llu  end %llu\n", c, r[1] - t0, r[63] - t0);
+    for (int j = 0; j < 10; j++)
+      printf("  tile %d: load %7lld  mma_acq %7lld  mma_commit %7lld  epi_acq %7lld  epi_rel %7lld  epi_done %7lld\n", j,
+             (long long)(r[2 + j] - t0), (long long)(r[12 + j] - t0), (long long)(r[22 + j] - t0), (long long)(r[32 + j] - t0),
+             (long long)(r[42 + j] - t0), (long long)(r[52 + j] - t0));
+    for (int j = 0; j < 8; j++)
+      printf("  epi tile %d: ldtm0 %lld chunk0 %lld ldtm1 %lld chunk1 %lld\n", j, (long long)(r[64 + 4 * j] - t0),
+             (long long)(r[65 + 4 * j] - t0), (long long)(r[66 + 4 * j] - t0), (long long)(r[67 + 4 * j] - t0));
+  }
+  return 0;
+}
