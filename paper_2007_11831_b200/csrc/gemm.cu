@@ -47,7 +47,7 @@ using namespace sm100;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
-constexpr int kThreads = 192;  // producer warp, MMA warp, 4 epilogue warps
+constexpr int kThreads = 224;  // producer warp, MMA warp, 4 epilogue warps, halo fix-up warp
 
 // Development-only timeline probe (-DDBS_GEMM_TRACE, scripts/gemm_trace.cu):
 // per-CTA clock64 stamps of the producer / MMA / epilogue hand-offs.
@@ -98,6 +98,30 @@ struct Cfg {
   static constexpr int kRing = (int)((212u * 1024u - kEpiBytes) / (kABytes + kBBytes));
   static constexpr int kStages = kRing > 8 ? 8 : kRing;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiBytes + 256;
+  static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+// Halo variant (3x3 stride-1 conv with 64 input channels, 64 output columns):
+// the 9 filter taps stay resident in shared memory for the CTA's lifetime and
+// each output tile of TR = 128 / W whole rows streams only three column-shifted
+// copies of its (TR + 2)-row input halo -- 3 x 24 KB instead of 9 x (16 + 8) KB
+// per tile, so the L2 -> SM traffic drops ~3x; tap (r, s) is the copy for s
+// viewed from row r * W (a 1 KB-aligned start in the 128-byte swizzle).
+// Each copy is ONE 2-D TMA box over the [pixels][64] view of the activation
+// (measured: a 2-D box costs the TMA unit ~300 cycles, a 4-D box ~560, nearly
+// independent of size -- scripts/tma_bench.cu); the rows that view gets wrong
+// (the column wrap-around of the shifted copies, the zero-padding rows above /
+// below the image) are zeroed in shared memory by a fix-up warp before the
+// MMA warp may read the slot.
+struct HaloCfg {
+  static constexpr uint32_t kSlotBytes = 24 * 1024;  // (TR + 2) * W rows of 128 B, W <= 32
+  static constexpr uint32_t kTapBytes = 64 * 128;    // one 64 x 64 bf16 filter tap
+  static constexpr uint32_t kBResBytes = 9 * kTapBytes;
+  static constexpr int kStages = 5;
+  static constexpr uint32_t kAccCols = 64;
+  static constexpr uint32_t kTmemCols = 128;
+  static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kSlotBytes + kBResBytes + kEpiBytes + 256;
   static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
 };
 
@@ -196,9 +220,6 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
       q.y = f2bf(x[j + 2]) | ((uint32_t)f2bf(x[j + 3]) << 16);
       q.z = f2bf(x[j + 4]) | ((uint32_t)f2bf(x[j + 5]) << 16);
       q.w = f2bf(x[j + 6]) | ((uint32_t)f2bf(x[j + 7]) << 16);
-#ifdef DBS_GEMM_NOSTORE
-      if (q.x == 0x12345678u && q.y == 0x9abcdef0u)
-#endif
       *reinterpret_cast<uint4*>(d + j) = q;
     }
   }
@@ -328,20 +349,30 @@ __device__ __forceinline__ float warp_colsum(float (&x)[32], int lane) {
   return mine;
 }
 
-template <int BN>
+template <int BN, bool kHalo>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   using C = Cfg<BN>;
+  using H = HaloCfg;
+  static_assert(!kHalo || BN == 64, "halo variant: 64 output columns");
+  constexpr int kStages = kHalo ? H::kStages : C::kStages;
+  constexpr uint32_t kAccCols = kHalo ? H::kAccCols : C::kAccCols;
+  constexpr uint32_t kTmemCols = kHalo ? H::kTmemCols : C::kTmemCols;
+  constexpr uint32_t kSlotA = kHalo ? H::kSlotBytes : C::kABytes;
+  constexpr uint32_t kSlotB = kHalo ? 0u : C::kBBytes;
+  constexpr uint32_t kBRes = kHalo ? H::kBResBytes : 0u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::kStages * C::kABytes;
-  float* sEpi = reinterpret_cast<float*>(sB + C::kStages * C::kBBytes);
+  uint8_t* sB = smem + kStages * kSlotA;  // ring B slots, or the resident filter (halo)
+  float* sEpi = reinterpret_cast<float*>(sB + kStages * kSlotB + kBRes);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + C::kEpiBytes);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* acc_full = empty + C::kStages;  // [2] MMA -> epilogue
-  uint64_t* acc_empty = acc_full + 2;       // [2] epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;  // [2] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2;    // [2] epilogue -> MMA
+  uint64_t* bres_full = acc_empty + 2;   // resident filter landed (halo)
+  uint64_t* ready = bres_full + 1;       // [kStages] halo slot fixed up (halo)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GEMM_TRACE(0);
@@ -366,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < C::kStages; s++) {
+    for (int s = 0; s < kStages; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -374,9 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
     }
+    mbar_init(bres_full, 1);
+    for (int s = 0; s < kStages; s++) mbar_init(&ready[s], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -389,6 +422,32 @@ __global__ void __launch_bounds__(kThreads, 1)
    uint32_t it = 0;  // ring position, continuous across tiles
    uint32_t pt = 0;
    (void)pt;
+   if constexpr (kHalo) {
+    // the 9 filter taps, once per CTA
+    mbar_arrive_expect_tx(bres_full, H::kBResBytes);
+    for (int tap = 0; tap < 9; tap++) {
+      uint8_t* b = sB + tap * H::kTapBytes;
+      if (p.b_mode == 0) {
+        tma_load_2d(b, &tmB, bres_full, tap * 64, 0);
+      } else {  // mode 3: flipped, transposed filter of the input gradient
+        tma_load_3d(b, &tmB, bres_full, 0, 8 - tap, 0);
+      }
+    }
+    const ConvGeom& g = p.ga;
+    const uint32_t halo_bytes = (uint32_t)(kBM + 2 * g.OW) * 128u;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      if (pt < 10) GEMM_TRACE(2 + pt);
+      pt++;
+      // first halo pixel: one row above the tile, shifted by sx - 1 columns
+      const int32_t row0 = (int32_t)(t * kBM) - g.OW - 1;
+      for (int sx = 0; sx < 3; sx++, it++) {
+        const int s = (int)(it % kStages);
+        mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], halo_bytes);
+        tma_load_2d(sA + s * kSlotA, &tmA, &full[s], 0, row0 + sx);
+      }
+    }
+   } else {
    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     int64_t m0, n0;
     int kb_begin;
@@ -405,8 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
     for (int i = 0; i < num_k; i++, it++) {
       const int kb = kb_begin + i;
-      const int s = (int)(it % C::kStages);
-      mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+      const int s = (int)(it % kStages);
+      mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], C::kABytes + C::kBBytes);
       const int32_t k0 = kb * kBK;
       uint8_t* a = sA + s * C::kABytes;
@@ -457,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
    }
+   }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -464,6 +524,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = make_idesc_bf16(kBM, BN, a_mn, b_mn);
     uint32_t it = 0, j = 0;
+    if constexpr (kHalo) {
+      mbar_wait(bres_full, 0);
+      tc_fence_after();
+      // descriptors by arithmetic on the 16-byte address field (no per-MMA
+      // re-encoding: the MMA thread's issue rate, not the tensor pipe, was the limit)
+      const uint32_t row16 = (uint32_t)p.ga.OW * 8u;  // one input row of the halo, in 16 B units
+      const uint64_t a_desc0 = make_sdesc(smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 1024) : make_sdesc(smem_u32(sB), 16, 1024);
+      const uint32_t b_kstep = b_mn ? 128u : 2u;
+      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int b = (int)(j & 1);
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        GEMM_TRACE(12 + j);
+        const uint32_t d_tmem = tmem_base + b * kAccCols;
+        for (int sx = 0; sx < 3; sx++, it++) {
+          const int s = (int)(it % kStages);
+          mbar_wait(&ready[s], (it / kStages) & 1);
+          if (j < 8) GEMM_TRACE(96 + 3 * j + sx);
+          tc_fence_after();
+          const uint64_t a_slot = a_desc0 + (uint64_t)((s * kSlotA) >> 4);
+#pragma unroll
+          for (int r = 0; r < 3; r++) {
+            const uint64_t a_r = a_slot + (uint64_t)(r * row16);
+            const uint64_t b_r = b_desc0 + (uint64_t)((r * 3 + sx) * (H::kTapBytes >> 4));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; k++)
+              mma_bf16_ss(d_tmem, a_r + (uint64_t)(k * 2), b_r + (uint64_t)(k * b_kstep), idesc,
+                          (sx | r | k) != 0 ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[b]);
+        GEMM_TRACE(22 + j);
+        j++;
+      }
+    } else {
+    const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), 8192, 1024) : make_sdesc(smem_u32(sA), 16, 1024);
+    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 1024) : make_sdesc(smem_u32(sB), 16, 1024);
+    const uint32_t a_kstep = a_mn ? 128u : 2u, b_kstep = b_mn ? 128u : 2u;  // one UMMA_K step, 16 B units
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int64_t m0, n0;
       int kb_begin;
@@ -473,19 +573,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
       GEMM_TRACE(12 + j);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + b * C::kAccCols;
+      const uint32_t d_tmem = tmem_base + b * kAccCols;
       for (int i = 0; i < num_k; i++, it++) {
-        const int s = (int)(it % C::kStages);
-        mbar_wait(&full[s], (it / C::kStages) & 1);
+        const int s = (int)(it % kStages);
+        mbar_wait(&full[s], (it / kStages) & 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + s * C::kABytes);
-        const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
+        const uint64_t a_s = a_desc0 + (uint64_t)((s * C::kABytes) >> 4);
+        const uint64_t b_s = b_desc0 + (uint64_t)((s * C::kBBytes) >> 4);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; k++) {
-          const uint64_t ad = a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
-          const uint64_t bd = b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
-          mma_bf16_ss(d_tmem, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
-        }
+        for (int k = 0; k < kBK / 16; k++)
+          mma_bf16_ss(d_tmem, a_s + (uint64_t)(k * a_kstep), b_s + (uint64_t)(k * b_kstep), idesc,
+                      (i | k) != 0 ? 1u : 0u);
         mma_commit(&empty[s]);
       }
       mma_commit(&acc_full[b]);
@@ -493,7 +591,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       j++;
     }
     }
+    }
     __syncwarp();
+  } else if (warp == 6) {
+    // ---------------- halo fix-up (halo variant only) ----------------
+    if constexpr (kHalo) {
+      const ConvGeom& g = p.ga;
+      const int W = g.OW, TR = kBM / g.OW, HW = g.OH * g.OW;
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int h0 = (int)((t * kBM) % HW) / W;
+        const bool top = (h0 == 0), bottom = (h0 + TR == g.OH);
+        for (int sx = 0; sx < 3; sx++, it++) {
+          const int s = (int)(it % kStages);
+          mbar_wait(&full[s], (it / kStages) & 1);
+          uint8_t* slot = sA + s * kSlotA;
+          // row j = hh * W + w of the copy is padding when hh is the row above /
+          // below the image, or when the shifted column w + sx - 1 leaves [0, W);
+          // each lane zeroes 16-byte chunks (a row is 8 chunks, swizzle-agnostic)
+          const uint4 z = make_uint4(0, 0, 0, 0);
+          if (sx != 1) {
+            const int w = (sx == 0) ? 0 : W - 1;
+            for (int k = lane; k < (TR + 2) * 8; k += 32)
+              *reinterpret_cast<uint4*>(slot + ((k >> 3) * W + w) * 128 + (k & 7) * 16) = z;
+          }
+          if (top)
+            for (int k = lane; k < W * 8; k += 32) *reinterpret_cast<uint4*>(slot + k * 16) = z;
+          if (bottom)
+            for (int k = lane; k < W * 8; k += 32) *reinterpret_cast<uint4*>(slot + (TR + 1) * W * 128 + k * 16) = z;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ready[s]);
+        }
+      }
+    }
   } else {
   // ---------------- epilogue (warps 2..5) ----------------
   const int q = warp & 3;  // the TMEM lane quadrant this warp may access
@@ -516,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i = rem / p.omap.OW, jj = rem - i * p.omap.OW;
       orow = (img * p.omap.H + 2 * i + p.omap.a) * p.omap.W + 2 * jj + p.omap.b;
     }
-    const uint32_t lane_addr = tmem_base + b * C::kAccCols + ((uint32_t)(q * 32) << 16);
+    const uint32_t lane_addr = tmem_base + b * kAccCols + ((uint32_t)(q * 32) << 16);
     const bool stats = (p.sum_part != nullptr);
     if (BN >= 32) {
 #pragma unroll 1
@@ -601,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem_base);
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
   if (threadIdx.x == 0) GEMM_TRACE(63);
 }
 
@@ -702,16 +833,17 @@ void* current_ctx() {
   return c;
 }
 
-template <int BN>
+template <int BN, bool kHalo = false>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits, cudaStream_t s) {
-  using C = Cfg<BN>;
+  constexpr size_t kSmem = kHalo ? HaloCfg::kSmem : Cfg<BN>::kSmem;
   static thread_local void* seen[16] = {nullptr};
   static thread_local int nseen = 0;
   void* ctx = current_ctx();
   bool known = false;
   for (int i = 0; i < nseen; i++) known |= (seen[i] == ctx);
   if (!known) {
-    DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
+    DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN, kHalo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSmem));
     if (nseen < 16) seen[nseen++] = ctx;
   }
   GemmParams q = p;
@@ -720,7 +852,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   const int64_t tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
   const int64_t sms = current_sm_count();
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  gemm_bf16_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, q);
+  gemm_bf16_kernel<BN, kHalo><<<grid, kThreads, kSmem, s>>>(ta, tb, q);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -732,7 +864,9 @@ int pick_bn(int64_t N, int b_mode) {
   return 256;
 }
 
-int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int bn, int splits, cudaStream_t s) {
+int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int bn, int splits, cudaStream_t s,
+             bool halo = false) {
+  if (halo) return launch<64, true>(ta, tb, p, 1, s);
   switch (bn) {
     case 16: return launch<16>(ta, tb, p, splits, s);
     case 64: return launch<64>(ta, tb, p, splits, s);
@@ -746,10 +880,11 @@ int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, 
 int preload_gemm() {
   // force-load every instantiation (lazy module loading must never happen while
   // a disturbance kernel owns SMs); also sets the shared-memory attribute
-  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<16>::kSmem));
-  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<64>::kSmem));
-  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::kSmem));
-  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<256>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<16>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<64>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<256>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg::kSmem));
   return DBS_OK;
 }
 
@@ -825,6 +960,37 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
       }
     }
     bn = pick;
+  }
+  // ---- halo variant: 3x3 / stride 1 / 64 -> 64 channels, whole-row tiles of one image ----
+  if (c.halo) {
+    const ConvGeom& g = c.ga;
+    DBS_REQUIRE(c.a_mode == 2 && (c.b_mode == 0 || c.b_mode == 3) && g.R == 3 && g.S == 3 && g.stride == 1 &&
+                    g.pad == 1 && g.cblocks == 1 && c.N == 64 && c.K == 576 && c.taps.n == 0 && !c.omap.on &&
+                    g.OW <= 32 && kBM % g.OW == 0 && (g.OH * g.OW) % kBM == 0 && c.ta.H == g.OH && c.ta.W == g.OW,
+                DBS_ERR_ARGUMENT, "conv halo variant: unsupported geometry");
+    // 2-D [pixels][64] view of the NHWC activation, boxes of (TR + 2) * W pixel rows
+    st = make_tmap(&ta, c.a, 64, (uint64_t)c.ta.N * c.ta.H * c.ta.W, 64, 64, (uint32_t)(kBM + 2 * g.OW));
+    if (st) return st;
+    if (c.b_mode == 0) {
+      st = make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, 64);
+      if (st) return st;
+    } else {
+      EncodeTiledFn fn = encode_fn();
+      DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+      cuuint64_t dims[3] = {(cuuint64_t)c.tb.C, (cuuint64_t)c.tb.W, (cuuint64_t)c.tb.N};
+      cuuint64_t strides[2] = {(cuuint64_t)c.tb.C * 2, (cuuint64_t)c.tb.W * c.tb.C * 2};
+      cuuint32_t box[3] = {64, 1, 64};
+      cuuint32_t es[3] = {1, 1, 1};
+      CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.b), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (3d filter) failed (%d)", (int)r);
+    }
+    p.a_mode = 2;
+    p.b_mode = c.b_mode;
+    p.ga = g;
+    p.kb_per_split = 9;
+    return dispatch(ta, tb, p, 64, 1, s, true);
   }
   // ---- A ----
   p.a_mode = c.a_mode;

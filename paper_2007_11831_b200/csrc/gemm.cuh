@@ -60,6 +60,7 @@ struct ConvCall {
   int bn_override;           // force the N tile (0 = auto)
   ConvTaps taps;
   OutMap omap;
+  int halo;                  // 3x3 stride-1 64->64 conv: resident filter + halo rows (gemm.cu HaloCfg)
 };
 
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,

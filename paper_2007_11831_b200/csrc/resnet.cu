@@ -17,6 +17,7 @@
 // BatchNorm uses the worker's own batch statistics (local BN, as in DDP without
 // SyncBN); running statistics are not tracked (training throughput path).
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -461,6 +462,18 @@ int alloc_all(dbs_resnet* m) {
 ConvTensor nhwc(int64_t N, int H, int W, int C) { return ConvTensor{(int)N, H, W, C}; }
 
 // forward conv -> y (bf16) + BN statistics -> mean/invstd
+// 3x3 / stride 1 / 64 -> 64 channels on whole-row tiles: the GEMM's halo
+// variant (resident filter, 3 shifted input halos per tile; gemm.cu HaloCfg).
+// DBS_CONV_HALO=0 turns it off (A/B measurements).
+bool halo_ok(const Conv& c) {
+  static const bool enabled = [] {
+    const char* e = getenv("DBS_CONV_HALO");
+    return !(e && e[0] == '0');
+  }();
+  return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 && c.OW <= 32 &&
+         128 % c.OW == 0 && (c.OH * c.OW) % 128 == 0;
+}
+
 int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64_t B, cudaStream_t s) {
   const Conv& c = m->convs[ci];
   const int64_t M = B * c.OH * c.OW;
@@ -487,6 +500,7 @@ int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64
     call.ta = nhwc(B, c.H, c.W, c.cin);
     call.ga = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
     call.ldb = call.K;
+    call.halo = halo_ok(c);
   }
   int st = conv_gemm(call, s);
   if (st) return st;
@@ -551,6 +565,7 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
     call.M = B * c.H * c.W;
     call.K = (int64_t)c.k * c.k * c.cout;
     call.ga = ConvGeom{c.k, c.k, c.cout / 64, 1, c.k / 2, c.H, c.W, c.cout};
+    call.halo = halo_ok(c);
     return conv_gemm(call, s);
   }
   // stride 2: one GEMM per output parity class (a, b).  dX(2i+a, 2j+b) gathers
@@ -837,6 +852,7 @@ extern "C" int dbs_dev_conv2d_fwd(const void* d_x, int32_t N, int32_t H, int32_t
   call.epi = DBS_EPI_BF16;
   call.d = d_y;
   call.ldd = Cout;
+  call.halo = halo_ok(c);
   return conv_gemm(call, as_stream(stream));
 }
 

@@ -32,7 +32,7 @@ Disturbance (DisturbanceEvent, cluster.py:25-56), realised on the device:
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -239,7 +239,11 @@ class SimulatedTrainer:
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
-            skip_update: bool = False, timed_from: Optional[int] = None) -> RunResult:
+            skip_update: bool = False, timed_from: Optional[int] = None,
+            epoch_hook: Optional[Callable[[int], None]] = None) -> RunResult:
+        """Train n_epochs under `config`.  epoch_hook(epoch), when given, runs at the
+        start of every epoch inside the timed region (e.g. a host->device upload of
+        that epoch's data, for end-to-end measurements)."""
         torch = self.torch
         n, D = self.n, self.D
         self.rng = DeviceRng(seed, self.dev)
@@ -256,6 +260,8 @@ class SimulatedTrainer:
                 t_start = torch.cuda.Event(enable_timing=True)
                 t_start.record()
             timing = timed_from is not None and epoch >= timed_from
+            if epoch_hook is not None:
+                epoch_hook(epoch)
             launches0 = _lib.lib().dbs_launch_count()
             captured = 0
             plan, smoothed = cluster.next_plan(config, epoch, n, D, stats[-1] if stats else None, smoothed)

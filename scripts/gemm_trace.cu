@@ -6,15 +6,25 @@
 #include "dbs_b200.h"
 extern "C" int dbs_gemm_trace_copy(unsigned long long* host, int n);
 int main(int argc, char** argv) {
-  long M = argc > 1 ? atol(argv[1]) : 131072, N = argc > 2 ? atol(argv[2]) : 64, K = argc > 3 ? atol(argv[3]) : 64;
+  // gemm_trace M N K            plain GEMM
+  // gemm_trace conv N H C       3x3 stride-1 C->C conv forward on an N x H x H x C map
+  const bool conv = argc > 1 && argv[1][0] == 'c';
+  const int o = conv ? 1 : 0;
+  long M = argc > 1 + o ? atol(argv[1 + o]) : 131072, N = argc > 2 + o ? atol(argv[2 + o]) : 64, K = argc > 3 + o ? atol(argv[3 + o]) : 64;
   void *a, *b, *d;
-  cudaMalloc(&a, M * K * 2); cudaMalloc(&b, N * K * 2); cudaMalloc(&d, M * N * 2);
-  cudaMemset(a, 0x3c, M * K * 2); cudaMemset(b, 0x3c, N * K * 2);
+  size_t abytes = conv ? (size_t)M * N * N * K * 2 : M * K * 2, bbytes = conv ? (size_t)K * 9 * K * 2 : N * K * 2;
+  size_t dbytes = conv ? abytes : M * N * 2;
+  cudaMalloc(&a, abytes); cudaMalloc(&b, bbytes); cudaMalloc(&d, dbytes);
+  cudaMemset(a, 0x3c, abytes); cudaMemset(b, 0x3c, bbytes);
+  auto run = [&]() {
+    return conv ? dbs_dev_conv2d_fwd(a, (int)M, (int)N, (int)N, (int)K, b, (int)K, 3, 1, 1, d, nullptr)
+                : dbs_dev_gemm_bf16(a, 0, K, b, 0, K, d, N, M, N, K, DBS_EPI_BF16, nullptr, nullptr, nullptr);
+  };
   for (int i = 0; i < 5; i++)
-    if (dbs_dev_gemm_bf16(a, 0, K, b, 0, K, d, N, M, N, K, DBS_EPI_BF16, nullptr, nullptr, nullptr)) { printf("err %s\n", dbs_last_error()); return 1; }
+    if (run()) { printf("err %s\n", dbs_last_error()); return 1; }
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  dbs_dev_gemm_bf16(a, 0, K, b, 0, K, d, N, M, N, K, DBS_EPI_BF16, nullptr, nullptr, nullptr);
+  run();
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("M=%ld N=%ld K=%ld: %.1f us  err=%s\n", M, N, K, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
@@ -28,6 +38,9 @@ int main(int argc, char** argv) {
       printf("  tile %d: load %7lld  mma_acq %7lld  mma_commit %7lld  epi_acq %7lld  epi_rel %7lld  epi_done %7lld\n", j,
              (long long)(r[2 + j] - t0), (long long)(r[12 + j] - t0), (long long)(r[22 + j] - t0), (long long)(r[32 + j] - t0),
              (long long)(r[42 + j] - t0), (long long)(r[52 + j] - t0));
+    for (int j = 0; j < 8; j++)
+      printf("  mma tile %d: ready0 %lld ready1 %lld ready2 %lld\n", j, (long long)(r[96 + 3 * j] - t0),
+             (long long)(r[97 + 3 * j] - t0), (long long)(r[98 + 3 * j] - t0));
     for (int j = 0; j < 8; j++)
       printf("  epi tile %d: ldtm0 %lld chunk0 %lld ldtm1 %lld chunk1 %lld\n", j, (long long)(r[64 + 4 * j] - t0),
              (long long)(r[65 + 4 * j] - t0), (long long)(r[66 + 4 * j] - t0), (long long)(r[67 + 4 * j] - t0));
