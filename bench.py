@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "mlp"])
+    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "mlp"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -120,6 +120,9 @@ WL = {
                      desc="C3: ResNet-18 (CIFAR stem), synthetic CIFAR-10-shaped 50000x3x32x32 fp32 (bf16 tensor-core "
                           "operands), 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the B200, "
                           "B=512 (128/worker fixed), step = 1 epoch (97 iterations)"),
+    "resnet18_ma": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0, avg=4,
+                        desc="C4: C3 with periodic model averaging (local SGD on per-worker replicas, averaged every "
+                             "step=4 iterations), DBS vs fixed plan, step = 1 epoch"),
     "mlp": dict(D=60000, workers=3, per_worker=128, lr=0.05, mom=0.5, mult=2.0,
                 desc="C1: MLP 784-256-10, synthetic MNIST 60000x784, 3 simulated workers, B=384, step = 1 epoch"),
 }
@@ -140,13 +143,15 @@ def make_trainer(wl, rank, world=1):
     from paper_2007_11831_b200.trainer import DistributedTrainer, SimulatedTrainer
 
     w = WL[wl]
+    if world > 1 and w.get("avg"):
+        raise SystemExit("model averaging (resnet18_ma) runs on one GPU; the multi-GPU trainer is S-SGD")
     if world > 1:
         # one process per GPU: the same 4 SM-partition workers per GPU, the global
         # plan spans 4 x world workers, gradients meet in the fused NVLink kernel
         tr = DistributedTrainer(w["D"], workers_per_rank=w["workers"], model=wl, seed=0, partition=True,
                                 max_batch=3 * w["per_worker"])
         return tr, (None, None)
-    if wl == "resnet18":
+    if wl.startswith("resnet18"):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
         X, y = synthetic_cifar(w["D"], seed=rank)
@@ -169,8 +174,9 @@ def run_strategy(tr, wl, kind, args, world=1):
     cfg = cluster.StrategyConfig(kind, n_global * w["per_worker"])
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
+    extra = {"averaging_interval": w["avg"]} if w.get("avg") else {}
     res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=w["lr"], momentum=w["mom"],
-                 profiles=profiles(n_global, w["mult"]), record_loss=True, timed_from=args.warmup)
+                 profiles=profiles(n_global, w["mult"]), record_loss=True, timed_from=args.warmup, **extra)
     clocks = sampler.stop()
     timed = res.stats[args.warmup:]
     return {"samples_per_s": res.timed_samples / res.timed_seconds, "epoch_s": res.timed_seconds / len(timed),
@@ -231,7 +237,7 @@ def cpu_baseline(wl, X, y, threads=None):
 
     w = WL[wl]
     batches = [w["per_worker"]] * w["workers"]
-    if wl == "resnet18":
+    if wl.startswith("resnet18"):
         from paper_2007_11831_b200.resnet import init_params
 
         tens = init_params(seed=0)
@@ -269,9 +275,10 @@ def e2e_run(tr, wl, X, y, args):
         tr.y.copy_(yh, non_blocking=True)
 
     cfg = cluster.StrategyConfig("dbs", w["workers"] * w["per_worker"])
+    extra = {"averaging_interval": w["avg"]} if w.get("avg") else {}
     res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=w["lr"], momentum=w["mom"],
                  profiles=profiles(w["workers"], w["mult"]), record_loss=True, timed_from=args.warmup,
-                 epoch_hook=upload)
+                 epoch_hook=upload, **extra)
     timed = res.stats[args.warmup:]
     iters = [len(l) for l in res.losses[args.warmup:]]
     # read back per epoch: the [workers x iters] fp32 loss rows and the fp64 worker times
@@ -288,7 +295,7 @@ def reference_arm(args):
         return
     wl = args.workload
     w = WL[wl]
-    if wl == "resnet18":
+    if wl.startswith("resnet18"):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
         X, y = synthetic_cifar(w["workers"] * w["per_worker"], seed=0)
@@ -300,7 +307,7 @@ def reference_arm(args):
     base = vals[-1]
     out = {"impl": "reference", "metric": METRIC, "value": round(base["value"], 2), "unit": "samples/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-           "dtype": "f32" if wl == "resnet18" else "f64", "data": "synthetic",
+           "dtype": "f32" if wl.startswith("resnet18") else "f64", "data": "synthetic",
            "config": {"workload": w["desc"]}, "cpu_baseline": base,
            "e2e": {"value": round(base["value"], 2), "unit": "samples/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
@@ -348,7 +355,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": w["desc"],
                    "disturbance": (f"worker 0: a co-running spin kernel pins {1 - 1 / w['mult']:.0%} of its SM "
-                                   f"partition for every epoch (cost_multiplier {w['mult']})" if wl == "resnet18" else
+                                   f"partition for every epoch (cost_multiplier {w['mult']})" if wl.startswith("resnet18") else
                                    f"worker 0 on a {w['mult']}x slower device (proportional spin)"),
                    "l2": "inputs > L2: 614 MB dataset repacked into per-worker shards every epoch",
                    "lr": w["lr"], "momentum": w["mom"], "parallelism": f"{w['workers']} simulated DP workers/GPU"},

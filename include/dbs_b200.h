@@ -378,6 +378,20 @@ int dbs_run_iterations_comm(const dbs_worker_slot* workers, int32_t n, int64_t t
 /* fp32 weighted reduce out = sum_i w_i g_i (DBS_AGG_*), no step. */
 int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* batch_sizes, int64_t n, int32_t mode, int64_t P,
                           float* d_out, void* stream);
+/* Periodic model averaging (local SGD; BASELINE config 4, sync interval
+ * `step`): each worker trains its own replica d_params[i] / d_velocity[i] /
+ * d_params_bf16[i] with a local momentum-SGD step on its stream; after every
+ * sync_interval-th iteration of the epoch the replicas are replaced by their
+ * `mode`-weighted average (floor(T / sync_interval) rounds per epoch, as
+ * cluster.sync_rounds_for_epoch counts them, cluster.py:185-186).  Iteration
+ * indices are host-side (t0..t1 of the epoch). */
+int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                             float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
+                             uint16_t* const* d_params_bf16, void* agg_stream);
+/* x_bar = sum_i w_i x_i (w as in dbs_dev_aggregate_*), written to every replica
+ * and its bf16 copy (d_params_bf16 may be NULL). P % 4 == 0. */
+int dbs_dev_average_replicas_f32(float* const* d_params, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                                 uint16_t* const* d_params_bf16, void* stream);
 int dbs_mlp_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                            float lr, float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
                            int32_t skip_update, void* agg_stream);

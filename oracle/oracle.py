@@ -401,8 +401,19 @@ def epoch_layout(plan_source, epoch, n_workers, sample_count, plan_of=None):
 
 
 def run_parallel_sgd(problem, step_size, n_iterations, momentum, aggregation, seed, n_workers,
-                     plan_source, initial_point=None, record_loss=False):
-    """Restatement of sgdlab.run_parallel_sgd (sgdlab.py:343-396)."""
+                     plan_source, initial_point=None, record_loss=False, averaging_interval=None):
+    """Restatement of sgdlab.run_parallel_sgd (sgdlab.py:343-396).
+
+    averaging_interval=k switches the synchronous step to periodic model
+    averaging (the reference counts its rounds, cluster.py:185-186, but has no
+    numerics -- these are the declared semantics the GPU path implements):
+    every worker keeps its own x_i, v_i and takes a local sgd_step with its own
+    mean gradient; after iteration t of an epoch with (t + 1) % k == 0 the
+    replicas are replaced by their aggregation-weighted average.  The reported
+    x is the weighted average of the replicas."""
+    if averaging_interval is not None:
+        return _run_model_averaging(problem, step_size, n_iterations, momentum, aggregation, seed, n_workers,
+                                    plan_source, initial_point, record_loss, int(averaging_interval))
     if not (0.0 < step_size * problem.mu < 1.0):
         raise OracleError(10)
     rng = np.random.default_rng(seed)
@@ -448,6 +459,63 @@ def run_parallel_sgd(problem, step_size, n_iterations, momentum, aggregation, se
                 break
         epoch += 1
     return {"squared_distances": sq, "x": x, "losses": np.asarray(losses),
+            "final_loss": problem.objective_gap(x) if hasattr(problem, "objective_gap") else None}
+
+
+def _run_model_averaging(problem, step_size, n_iterations, momentum, aggregation, seed, n_workers, plan_source,
+                         initial_point, record_loss, interval):
+    if not (0.0 < step_size * problem.mu < 1.0):
+        raise OracleError(10)
+    if interval < 1:
+        raise OracleError(7)
+    rng = np.random.default_rng(seed)
+    x0 = np.ones(problem.dimension) if initial_point is None else np.asarray(initial_point, dtype=float).copy()
+    xs = [x0.copy() for _ in range(n_workers)]
+    vs = [np.zeros(problem.dimension) for _ in range(n_workers)]
+    sq = np.empty(n_iterations)
+    losses = []
+    done = 0
+    epoch = 0
+    mode = 1 if aggregation == "batch_weighted" else 0
+
+    def weights(batches):
+        if mode == 1:
+            w = np.asarray(batches, dtype=float)
+            return w / w.sum()
+        return np.full(len(batches), 1.0 / len(batches))
+
+    batches = None
+    while done < n_iterations:
+        batches, spans = epoch_layout(plan_source, epoch, n_workers, problem.sample_count)
+        perms = [start + rng.permutation(end - start) for start, end in spans]
+        iters = min((end - start) // b for (start, end), b in zip(spans, batches))
+        if iters == 0:
+            raise OracleError(7)
+        w = weights(batches)
+        for t in range(iters):
+            lsum = 0.0
+            for i, (perm, b) in enumerate(zip(perms, batches)):
+                idx = perm[t * b:(t + 1) * b]
+                if record_loss and hasattr(problem, "loss_and_grad"):
+                    l, g = problem.loss_and_grad(xs[i], idx)
+                    lsum += l * b
+                else:
+                    g = problem.per_sample_gradients(xs[i], idx).mean(axis=0)
+                vs[i] = momentum * vs[i] + g
+                xs[i] = xs[i] - step_size * vs[i]
+            if record_loss:
+                losses.append(lsum / sum(batches))
+            if (t + 1) % interval == 0:
+                xbar = w @ np.stack(xs)
+                xs = [xbar.copy() for _ in range(n_workers)]
+            diff = (w @ np.stack(xs)) - problem.optimum
+            sq[done] = float(diff @ diff)
+            done += 1
+            if done == n_iterations:
+                break
+        epoch += 1
+    x = weights(batches) @ np.stack(xs)
+    return {"squared_distances": sq, "x": x, "replicas": xs, "losses": np.asarray(losses),
             "final_loss": problem.objective_gap(x) if hasattr(problem, "objective_gap") else None}
 
 

@@ -384,6 +384,100 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
   return DBS_OK;
 }
 
+// Periodic model averaging (local SGD): worker i trains its own replica
+// (d_params[i], d_velocity[i], d_params_bf16[i]) with a local momentum-SGD step
+// on its own stream every iteration; after every sync_interval-th iteration of
+// the epoch (t + 1 multiple of sync_interval) the replicas are averaged with the
+// batch weights of `mode` -- floor(T / sync_interval) rounds per epoch
+// (cluster.sync_rounds_for_epoch, cluster.py:185-186).  Between rounds no
+// worker waits for another.
+extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                        float lr, float mom, int32_t sync_interval, float* const* d_params,
+                                        float* const* d_velocity, uint16_t* const* d_params_bf16, void* agg_stream) {
+  DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0 && sync_interval >= 1 && d_params && d_velocity && d_params_bf16,
+              DBS_ERR_ARGUMENT, "run_iterations_local: bad arguments");
+  for (int i = 0; i < n; i++)
+    DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18),
+                DBS_ERR_ARGUMENT, "run_iterations_local: worker %d has a bad model", i);
+  cudaEvent_t* ev;
+  int st = events(n + 1, &ev);
+  if (st) return st;
+  cudaStream_t agg = as_stream(agg_stream);
+  int64_t batches[64];
+  for (int i = 0; i < n; i++) batches[i] = w[i].batch;
+  const int64_t P = (w[0].model_kind == DBS_MODEL_MLP) ? static_cast<const dbs_mlp*>(w[0].model)->P
+                                                       : resnet_param_count(static_cast<const dbs_resnet*>(w[0].model));
+  DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
+  for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(as_stream(w[i].stream), ev[n], 0));
+  for (int64_t t = t0; t < t1; t++) {
+    const bool sync = ((t + 1) % sync_interval) == 0;
+    for (int i = 0; i < n; i++) {
+      cudaStream_t s = as_stream(w[i].stream);
+      st = ctx_push(w[i].ctx);
+      if (st) return st;
+      st = [&]() -> int {
+        if (w[i].stamps) {
+          st = stamp(w[i].stamps, 0, s);
+          if (st) return st;
+        }
+        if (w[i].spin_ns > 0 && w[i].spin_ctas > 0) {
+          st = dbs_dev_spin_for(w[i].spin_ctas, w[i].spin_ns, s);
+          if (st) return st;
+        }
+        const int64_t b = w[i].batch;
+        if (w[i].model_kind == DBS_MODEL_MLP) {
+          dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
+          const uint16_t* x = static_cast<const uint16_t*>(w[i].x_shard) + t * b * m->in;
+          st = mlp_fwd_bwd(m, d_params_bf16[i], d_params[i], x, w[i].y_shard + t * b, b, w[i].grad,
+                           w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
+        } else {
+          dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
+          const float* x = static_cast<const float*>(w[i].x_shard) + t * b * 3072;
+          st = resnet_fwd_bwd(m, d_params_bf16[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,
+                              w[i].loss ? w[i].loss + t : nullptr, s);
+        }
+        if (st) return st;
+        if (w[i].stamps) {
+          st = stamp(w[i].stamps, 1, s);
+          if (st) return st;
+          if (w[i].slow_scale > 0.f && w[i].slow_ctas > 0) {
+            st = spin_scaled(w[i].stamps, 0, 1, w[i].slow_scale, w[i].slow_ctas, s);
+            if (st) return st;
+            st = stamp(w[i].stamps, 1, s);
+            if (st) return st;
+          }
+          st = dbs_dev_accumulate_time(w[i].stamps, 0, 1, w[i].seconds, w[i].worker_index, s);
+          if (st) return st;
+        }
+        // the worker's own momentum-SGD step on its replica
+        const float* g = w[i].grad;
+        const int64_t one = 1;
+        st = dbs_dev_aggregate_sgd_f32(&g, &one, 1, DBS_AGG_UNIFORM, P, lr, mom, d_params[i], d_velocity[i],
+                                       d_params_bf16[i], s);
+        if (st) return st;
+        if (sync) DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
+        return DBS_OK;
+      }();
+      const int st_pop = ctx_pop(w[i].ctx);
+      if (st) return st;
+      if (st_pop) return st_pop;
+    }
+    if (sync) {
+      for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
+      st = dbs_dev_average_replicas_f32(d_params, batches, n, mode, P, d_params_bf16, agg_stream);
+      if (st) return st;
+      DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
+      for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(as_stream(w[i].stream), ev[n], 0));
+    }
+  }
+  // the epoch ends with every worker joined into the aggregation stream
+  for (int i = 0; i < n; i++) {
+    DBS_CUDA_TRY(cudaEventRecord(ev[i], as_stream(w[i].stream)));
+    DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
+  }
+  return DBS_OK;
+}
+
 extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                       float lr, float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
                                       int32_t skip_update, void* agg_stream) {

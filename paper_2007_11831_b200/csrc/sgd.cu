@@ -132,6 +132,32 @@ __global__ void __launch_bounds__(256) aggregate_f32_kernel(AggArgs a, int64_t P
   }
 }
 
+// model averaging: x_bar = sum_i w_i x_i (the same weights as the gradient
+// aggregation), written back to every replica (fp32 + its bf16 operand copy)
+struct ReplicaArgs {
+  float4* x[kMaxWorkers];
+  uint2* xb[kMaxWorkers];
+};
+
+__global__ void __launch_bounds__(256) average_replicas_f32_kernel(AggArgs a, ReplicaArgs r, int64_t P4) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x) {
+    const float w0 = (a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[0] : 1.0f / (float)a.n;
+    float4 g = r.x[0][p];
+    g.x *= w0; g.y *= w0; g.z *= w0; g.w *= w0;
+    for (int i = 1; i < a.n; i++) {
+      const float wi = (a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[i] : 1.0f / (float)a.n;
+      const float4 h = r.x[i][p];
+      g.x = fmaf(wi, h.x, g.x); g.y = fmaf(wi, h.y, g.y);
+      g.z = fmaf(wi, h.z, g.z); g.w = fmaf(wi, h.w, g.w);
+    }
+    const uint2 gb = make_uint2(bf16_bits(g.x) | (bf16_bits(g.y) << 16), bf16_bits(g.z) | (bf16_bits(g.w) << 16));
+    for (int i = 0; i < a.n; i++) {
+      r.x[i][p] = g;
+      if (r.xb[i]) r.xb[i][p] = gb;
+    }
+  }
+}
+
 int grid_for(int64_t P, int threads) {
   int64_t blocks = (P + threads - 1) / threads;
   int64_t cap = (int64_t)num_sms() * 8;
@@ -199,6 +225,24 @@ extern "C" int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t*
   DBS_REQUIRE(P % 4 == 0, DBS_ERR_ARGUMENT, "fp32 aggregate: P must be a multiple of 4");
   if (P <= 0) return DBS_OK;
   aggregate_f32_kernel<<<grid_for(P / 4, 256), 256, 0, as_stream(stream)>>>(a, P / 4, (float4*)d_out);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_average_replicas_f32(float* const* d_params, const int64_t* b, int64_t n, int32_t mode,
+                                            int64_t P, uint16_t* const* d_params_bf16, void* stream) {
+  AggArgs a;
+  int st = make_args(a, (const void* const*)d_params, b, n, mode);
+  if (st) return st;
+  DBS_REQUIRE(P % 4 == 0, DBS_ERR_ARGUMENT, "average_replicas: P must be a multiple of 4");
+  ReplicaArgs r;
+  for (int64_t i = 0; i < n; i++) {
+    DBS_REQUIRE(((uintptr_t)d_params[i] % 16) == 0, DBS_ERR_ARGUMENT, "replica buffers must be 16-byte aligned");
+    r.x[i] = reinterpret_cast<float4*>(d_params[i]);
+    r.xb[i] = d_params_bf16 ? reinterpret_cast<uint2*>(d_params_bf16[i]) : nullptr;
+  }
+  if (P <= 0) return DBS_OK;
+  average_replicas_f32_kernel<<<grid_for(P / 4, 256), 256, 0, as_stream(stream)>>>(a, r, P / 4);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }

@@ -31,6 +31,7 @@ Disturbance (DisturbanceEvent, cluster.py:25-56), realised on the device:
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -38,6 +39,7 @@ import numpy as np
 
 from . import _lib, cluster
 from .cluster import EpochStats, StrategyConfig, WorkerProfile
+from .errors import ConfigurationError
 from .sgdlab import DeviceRng
 
 _MODE = {"uniform_average": 0, "batch_weighted": 1}
@@ -191,6 +193,37 @@ class SimulatedTrainer:
                                            d_iter.data_ptr() if d_iter is not None else None)
         _lib.check(st, "run_iterations")
 
+    def _replicas_begin(self, mode: int):
+        """Per-worker model replicas for local SGD, copied from the shared model;
+        the averaging kernel is loaded here (never lazily behind a spin kernel)."""
+        torch = self.torch
+        m = self.model
+        self._rep_p = [m.params.clone() for _ in range(self.n)]
+        self._rep_v = [m.velocity.clone() for _ in range(self.n)]
+        self._rep_pb = [m.params_bf16.clone() for _ in range(self.n)]
+        arr = lambda ts: (ctypes.c_void_p * self.n)(*[t.data_ptr() for t in ts])
+        self._rep_ptrs = (arr(self._rep_p), arr(self._rep_v), arr(self._rep_pb))
+        self._rep_mode = mode
+        self._average_replicas(mode)
+        torch.cuda.synchronize()
+
+    def _average_replicas(self, mode: int, batches=None):
+        b = np.asarray(batches if batches is not None else [1] * self.n, dtype=np.int64)
+        st = _lib.lib().dbs_dev_average_replicas_f32(self._rep_ptrs[0], b.ctypes.data_as(_lib.P_i64), self.n, int(mode),
+                                                     self.model.P, self._rep_ptrs[2], int(self.agg.cuda_stream))
+        _lib.check(st, "average_replicas")
+
+    def _replicas_end(self, final_average: bool, batches):
+        """Hand the (averaged) replica back to the shared model."""
+        torch = self.torch
+        if final_average:
+            self._average_replicas(self._rep_mode, batches)
+        torch.cuda.current_stream().wait_stream(self.agg)
+        self.model.params.copy_(self._rep_p[0])
+        self.model.velocity.copy_(self._rep_v[0])
+        self.model.params_bf16.copy_(self._rep_pb[0])
+        torch.cuda.synchronize()
+
     def _prime(self, slots, mode: int):
         """One throw-away iteration on scratch parameters before the first spin
         kernel or graph capture: every kernel of an iteration gets loaded (a lazily
@@ -240,11 +273,30 @@ class SimulatedTrainer:
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
             skip_update: bool = False, timed_from: Optional[int] = None,
-            epoch_hook: Optional[Callable[[int], None]] = None) -> RunResult:
+            epoch_hook: Optional[Callable[[int], None]] = None,
+            averaging_interval: Optional[int] = None) -> RunResult:
         """Train n_epochs under `config`.  epoch_hook(epoch), when given, runs at the
         start of every epoch inside the timed region (e.g. a host->device upload of
-        that epoch's data, for end-to-end measurements)."""
+        that epoch's data, for end-to-end measurements).
+
+        Synchronisation: S-SGD (aggregated gradient, one shared model) for
+        "fixed_ssgd" / "dbs"; periodic model averaging (local SGD on per-worker
+        replicas, averaged every `sync_interval` iterations) for "model_averaging",
+        and a single average at the end of the run for "one_shot"
+        (cluster.sync_rounds_for_epoch, cluster.py:173-189).  averaging_interval=k
+        applies model averaging every k iterations on top of any plan kind -- with
+        "dbs" that is the DBS model-averaging variant (BASELINE config 4)."""
         torch = self.torch
+        local_interval = averaging_interval
+        if local_interval is None and config.kind == "model_averaging":
+            local_interval = config.sync_interval
+        if local_interval is None and config.kind == "one_shot":
+            local_interval = 1 << 30
+        if local_interval is not None and local_interval < 1:
+            raise ConfigurationError("averaging_interval must be >= 1")
+        local = local_interval is not None and not skip_update
+        if local:
+            self._replicas_begin(mode=_MODE[aggregation])
         n, D = self.n, self.D
         self.rng = DeviceRng(seed, self.dev)
         stats: list = []
@@ -338,7 +390,7 @@ class SimulatedTrainer:
                 self._prime(slots, mode)
             graph = None
             per_replay = 0
-            if self.graphs and iters > 0:
+            if self.graphs and iters > 0 and not local:
                 key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
                        bool(record_loss))
                 graph, per_replay, captured = self._graph(key, slots, mode, lr, momentum, skip_update)
@@ -359,6 +411,11 @@ class SimulatedTrainer:
                     with torch.cuda.stream(self.agg):
                         for _ in range(iters):
                             graph.replay()
+                elif local:
+                    st = _lib.lib().dbs_run_iterations_local(slots, self.n, 0, iters, mode, float(lr), float(momentum),
+                                                             int(local_interval), self._rep_ptrs[0], self._rep_ptrs[1],
+                                                             self._rep_ptrs[2], int(self.agg.cuda_stream))
+                    _lib.check(st, "run_iterations_local")
                 else:
                     self._run_iters(slots, 0, iters, mode, lr, momentum, self.model.params, self.model.velocity,
                                     self.model.params_bf16, skip_update)
@@ -393,6 +450,9 @@ class SimulatedTrainer:
             t_end.record()
             torch.cuda.synchronize()
             timed = t_start.elapsed_time(t_end) / 1e3
+        if local:
+            self._replicas_end(final_average=(config.kind == "one_shot"),
+                               batches=list(plans[-1].int_batches) if plans else None)
         return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
                          wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
                          timed_launches=timed_launches)

@@ -99,3 +99,35 @@ def test_dbs_plans_feed_identical_batches(dev):
     ref = O.run_parallel_sgd(prob, 0.05, n_it, 0.5, "batch_weighted", 5, 3, plans,
                              initial_point=p0.astype(np.float64), record_loss=True)
     np.testing.assert_allclose(res.losses, ref["losses"], rtol=2e-2)
+
+
+@pytest.mark.parametrize("kind,interval", [("model_averaging", None), ("dbs", 4), ("one_shot", None)])
+def test_model_averaging_matches_oracle(dev, kind, interval):
+    """Local SGD on per-worker replicas with periodic averaging (BASELINE config
+    4 semantics; the reference only counts the rounds) against the oracle."""
+    from paper_2007_11831_b200 import cluster, mlp
+    from paper_2007_11831_b200.trainer import SimulatedTrainer
+
+    X, y = mlp.synthetic_mnist(6000, seed=0)
+    tr = SimulatedTrainer(X, y, n_workers=3, seed=0, partition=False)
+    p0 = tr.model.host_params().copy()
+    cfg = cluster.StrategyConfig(kind, 384, sync_interval=4 if kind == "model_averaging" else 1)
+    prof = None
+    if kind == "dbs":
+        prof = [cluster.WorkerProfile(0, 1.0, disturbances=(cluster.DisturbanceEvent(0, extra_epoch_seconds=0.02),)),
+                cluster.WorkerProfile(1, 1.0), cluster.WorkerProfile(2, 1.0)]
+    res = tr.run(cfg, n_epochs=3, lr=0.05, momentum=0.5, seed=0, max_iters=40, profiles=prof,
+                 averaging_interval=interval)
+    plans = [{"int_batches": list(p.int_batches), "cum": [0] + list(np.cumsum(p.int_batches))} for p in res.plans]
+    prob = O.MlpProblem(X, y, emulate_bf16=True)
+    k = 4 if kind != "one_shot" else 1 << 30
+    ref = O.run_parallel_sgd(prob, 0.05, 40, 0.5, "batch_weighted", 0, 3, plans,
+                             initial_point=p0.astype(np.float64), record_loss=True, averaging_interval=k)
+    assert len(res.losses) == 40
+    np.testing.assert_allclose(res.losses, ref["losses"], rtol=2e-2)
+    if kind == "one_shot":  # one average at the very end of the run
+        w = np.asarray(plans[-1]["int_batches"], dtype=float)
+        want = (w / w.sum()) @ np.stack(ref["replicas"])
+    else:  # the trainer hands worker 0's replica back to the shared model
+        want = ref["replicas"][0]
+    assert _rel(tr.model.host_params().astype(np.float64), want) < 1e-2

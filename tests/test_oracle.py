@@ -188,3 +188,34 @@ def test_mlp_adapter_gradient_is_batch_mean():
         e[k] = eps
         fd = (p.loss_and_grad(x + e, np.arange(64))[0] - p.loss_and_grad(x - e, np.arange(64))[0]) / (2 * eps)
         assert abs(fd - g_all[k]) < 1e-6
+
+
+def test_model_averaging_every_iteration_without_momentum_is_ssgd():
+    """Declared model-averaging semantics, pinned by a size-independent identity:
+    averaging after every step with momentum 0 is exactly synchronous SGD."""
+    X, y = O.synthetic_mnist(600, 20, 5, seed=3)
+    p = O.MlpProblem(X, y, hidden=16, classes=5)
+    x0 = O.mlp_init(20, 16, 5).astype(np.float64)
+    plans = [{"int_batches": [30, 50, 40], "cum": [0, 30, 80, 120]}] * 4
+    for agg in ("batch_weighted", "uniform_average"):
+        ref = O.run_parallel_sgd(p, 0.05, 12, 0.0, agg, 0, 3, plans, initial_point=x0, record_loss=True)
+        avg = O.run_parallel_sgd(p, 0.05, 12, 0.0, agg, 0, 3, plans, initial_point=x0, record_loss=True,
+                                 averaging_interval=1)
+        np.testing.assert_allclose(avg["x"], ref["x"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(avg["losses"], ref["losses"], rtol=1e-12)
+
+
+def test_model_averaging_rounds_and_replicas():
+    """k > 1: replicas diverge between rounds and coincide right after one
+    (floor(T / k) rounds per epoch, cluster.sync_rounds_for_epoch)."""
+    X, y = O.synthetic_mnist(600, 20, 5, seed=4)
+    p = O.MlpProblem(X, y, hidden=16, classes=5)
+    x0 = O.mlp_init(20, 16, 5).astype(np.float64)
+    plans = [{"int_batches": [30, 50, 40], "cum": [0, 30, 80, 120]}] * 4
+    # 5 iterations per epoch (spans 150 / 250 / 200): a round after the 4th
+    at_round = O.run_parallel_sgd(p, 0.05, 4, 0.5, "batch_weighted", 0, 3, plans, initial_point=x0,
+                                  averaging_interval=4)
+    assert all(np.array_equal(r, at_round["replicas"][0]) for r in at_round["replicas"])
+    between = O.run_parallel_sgd(p, 0.05, 6, 0.5, "batch_weighted", 0, 3, plans, initial_point=x0,
+                                 averaging_interval=4)
+    assert not np.array_equal(between["replicas"][0], between["replicas"][1])
