@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--report", default=None,
+                    help="directory for the reference-format run reports (epoch CSV per strategy + run JSON)")
     ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "mlp"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -336,6 +338,17 @@ def main():
     # its samples count every worker of every rank)
     res = {k: run_strategy(tr, wl, k, args, world) for k in ("fixed_ssgd", "dbs")}
     dbs, fixed = res["dbs"], res["fixed_ssgd"]
+    if args.report and rank == 0:
+        from pathlib import Path
+
+        from paper_2007_11831_b200 import report as rpt
+
+        out = Path(args.report)
+        out.mkdir(parents=True, exist_ok=True)
+        reps = [rpt.RunReport.from_stats(f"bench_{wl}_n{world}", k, 0, res[k]["stats"]) for k in ("fixed_ssgd", "dbs")]
+        for r in reps:
+            rpt.write_epoch_csv(r, out / f"{r.scenario_name}_{r.strategy}.csv")
+        rpt.write_run_json(reps, [], out / f"bench_{wl}_n{world}.json")
     roof = kernel_roofline(peaks)
     e2e = None if (args.no_e2e or world > 1) else e2e_run(tr, wl, X, y, args)
     cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl, X, y)

@@ -301,6 +301,42 @@ def gen_sgd_trajectories():
     return recs
 
 
+def gen_reports():
+    """The reference's report formats (report.py) for a simulated scenario: the
+    scenario definition, the DBS run's long CSV, the run JSON of every strategy
+    and the savings table against fixed S-SGD."""
+    from dbsim import report
+
+    scen = builtin_scenarios()["robustness"]
+    profs = scen.profiles()
+    reports = []
+    for strat in scen.strategies:
+        stats = cluster.run_training(profs, strat, scen.dataset_size, scen.n_epochs)
+        reports.append(report.RunReport.from_stats(scen.name, strat.kind, 0, stats))
+    csv_path = HERE / "report_robustness_dbs.csv"
+    report.write_epoch_csv(next(r for r in reports if r.strategy == "dbs"), csv_path)
+    json_path = HERE / "report_robustness.json"
+    report.write_run_json(reports, [], json_path)
+    table = report.compare_strategies(reports, "fixed_ssgd")
+    definition = {
+        "name": scen.name, "dataset_size": scen.dataset_size, "n_epochs": scen.n_epochs,
+        "profiles": [{"worker_id": p.worker_id, "base_cost": hx(p.base_cost),
+                      "per_iteration_overhead": hx(p.per_iteration_overhead),
+                      "disturbances": [{"start_epoch": d.start_epoch, "end_epoch": d.end_epoch,
+                                        "extra_epoch_seconds": None if d.extra_epoch_seconds is None
+                                        else hx(d.extra_epoch_seconds),
+                                        "cost_multiplier": None if d.cost_multiplier is None
+                                        else hx(d.cost_multiplier)} for d in p.disturbances]}
+                     for p in profs],
+        "strategies": [{"kind": s.kind, "total_budget": s.total_budget, "sync_interval": s.sync_interval,
+                        "sync_cost_per_round": hx(s.sync_cost_per_round),
+                        "sync_cost_per_worker": hx(s.sync_cost_per_worker),
+                        "perf_smoothing": hx(s.perf_smoothing)} for s in scen.strategies],
+        "savings": [[k, hx(t), hx(v)] for k, t, v in table],
+    }
+    return definition
+
+
 def main():
     rng = random.Random(20072011831)
     data = {
@@ -315,6 +351,7 @@ def main():
     (HERE / "plan_streams.json").write_text(json.dumps(gen_plan_streams(), separators=(",", ":")))
     (HERE / "permutation.json").write_text(json.dumps(gen_permutations(), indent=1))
     (HERE / "sgd_trajectories.json").write_text(json.dumps(gen_sgd_trajectories(), separators=(",", ":")))
+    (HERE / "report_scenario.json").write_text(json.dumps(gen_reports(), indent=1))
     for p in sorted(HERE.glob("*.json")):
         print(p.name, p.stat().st_size)
 
