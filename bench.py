@@ -282,7 +282,7 @@ def e2e_run(tr, wl, X, y, args):
                  profiles=profiles(w["workers"], w["mult"]), record_loss=True, timed_from=args.warmup,
                  epoch_hook=upload, **extra)
     timed = res.stats[args.warmup:]
-    iters = [len(l) for l in res.losses[args.warmup:]]
+    iters = [cluster.iterations_for_plan(s.plan) for s in timed]
     # read back per epoch: the [workers x iters] fp32 loss rows and the fp64 worker times
     d2h = [4 * tr.n * it + tr.seconds.numel() * tr.seconds.element_size() for it in iters]
     return {"value": round(res.timed_samples / res.timed_seconds, 1), "unit": "samples/s",
