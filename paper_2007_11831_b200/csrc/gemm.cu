@@ -34,6 +34,8 @@
 // batch size that changes every epoch needs no recompilation and no padding.
 #include <cuda.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "common.cuh"
@@ -453,9 +455,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int kb_begin;
     const int num_k = decode(t, m0, n0, kb_begin);
     int a_n = 0, a_oh = 0, a_ow = 0;
-    if (p.a_mode == 2) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
+    if (p.a_mode == 2 || p.a_mode == 4) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
     int b_r = 0, b_s = 0, b_c0 = 0;
-    if (p.b_mode == 2) {
+    if (p.b_mode == 2 || p.b_mode == 4) {
       const int rs = (int)(n0 / p.gb.Cin);
       b_c0 = (int)(n0 - (int64_t)rs * p.gb.Cin);
       b_r = rs / p.gb.S;
@@ -475,6 +477,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (p.a_mode == 1) {
         tma_load_2d(a, &tmA, &full[s], (int32_t)m0, k0);
         tma_load_2d(a + 8192, &tmA, &full[s], (int32_t)m0 + 64, k0);
+      } else if (p.a_mode == 4) {
+        // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
+        // the window corner, shifted by the tap; the tensor map's bounding box
+        // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int h0, w0, oh, ow;
+        if (p.taps.n > 0) {
+          h0 = a_oh - 1;
+          w0 = a_ow - 1;
+          oh = p.taps.dh[rs] + 1;
+          ow = p.taps.dw[rs] + 1;
+        } else {
+          oh = rs / g.S;
+          ow = rs - oh * g.S;
+          h0 = a_oh * g.stride - g.pad;
+          w0 = a_ow * g.stride - g.pad;
+        }
+        tma_load_im2col_4d(a, &tmA, &full[s], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
       } else {
         const ConvGeom& g = p.ga;
         const int cb = kb % g.cblocks;
@@ -505,6 +527,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
 #pragma unroll
         for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
+      } else if (p.b_mode == 4) {
+        const ConvGeom& g = p.gb;
+        int bn_, boh, bow;
+        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_im2col_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride - g.pad,
+                             boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
       } else {
         const ConvGeom& g = p.gb;
         int bn_, boh, bow;
@@ -792,6 +822,69 @@ int make_tmap_nhwc(CUtensorMap* tm, const void* base, const ConvTensor& t, int b
   return DBS_OK;
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
+// im2col view of a 4-D NHWC bf16 tensor: each load is `pixels` output pixels x
+// 64 channels.  The bounding box of window corners is [lower, extent - 1 + upper]
+// on H and W, walked with the conv stride, so the output grid is
+// (extent + upper - lower - 1) / stride + 1 -- any feature-map size, a tile may
+// cross rows and images (fprop / dgrad: lower = -pad, upper = pad - (k - 1)).
+int make_tmap_im2col(CUtensorMap* tm, const void* base, const ConvTensor& t, int lower, int upper, int pixels,
+                     int stride) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeIm2col unavailable");
+  DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 64 == 0, DBS_ERR_ARGUMENT,
+              "im2col TMA: 16-byte aligned base and C %% 64 == 0 required");
+  DBS_REQUIRE(pixels >= 1 && pixels <= 256 && lower >= -128 && upper <= 127, DBS_ERR_ARGUMENT,
+              "im2col TMA: %d pixels, corners [%d, %d] out of range", pixels, lower, upper);
+  cuuint64_t dims[4] = {(cuuint64_t)t.C, (cuuint64_t)t.W, (cuuint64_t)t.H, (cuuint64_t)t.N};
+  cuuint64_t strides[3] = {(cuuint64_t)t.C * 2, (cuuint64_t)t.W * t.C * 2, (cuuint64_t)t.H * t.W * t.C * 2};
+  int lo[2] = {lower, lower}, hi[2] = {upper, upper};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lo, hi, 64,
+                  (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
+  // drivers up to 13.1 mis-set one descriptor bit for im2col maps of tensors
+  // under 128 KB (the same correction CUTLASS applies)
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (uint64_t)t.N * t.H * t.W * t.C * 2 < 131072ull)
+    reinterpret_cast<uint64_t*>(tm)[1] &= ~(1ull << 21);
+  return DBS_OK;
+}
+
+// the 4-D box path covers a tile of `rows` pixels only when it aligns with whole rows / images
+bool pixel_box_fits(int OH, int OW, int rows) {
+  const int hw = OH * OW;
+  if (hw >= rows) return hw % rows == 0 && (rows % OW == 0 || OW % rows == 0);
+  return rows % hw == 0;
+}
+
+bool force_im2col() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_CONV_IM2COL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // pixels of one box: `rows` consecutive output pixels in NHWC order -> (bw, bh, bn)
 int pixel_box(int OH, int OW, int rows, int& bw, int& bh, int& bn) {
   const int hw = OH * OW;
@@ -994,7 +1087,14 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   }
   // ---- A ----
   p.a_mode = c.a_mode;
-  if (c.a_mode == 2) {
+  if (c.a_mode == 2 && (force_im2col() || !pixel_box_fits(c.ga.OH, c.ga.OW, kBM))) {
+    const bool taps = c.taps.n > 0;
+    st = make_tmap_im2col(&ta, c.a, c.ta, taps ? -1 : -c.ga.pad, taps ? -1 : c.ga.pad - (c.ga.R - 1), kBM,
+                          c.ga.stride);
+    if (st) return st;
+    p.a_mode = 4;
+    p.ga = c.ga;
+  } else if (c.a_mode == 2) {
     int bw, bh, bnn;
     st = pixel_box(c.ga.OH, c.ga.OW, kBM, bw, bh, bnn);
     if (st) return st;
@@ -1008,7 +1108,14 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   }
   // ---- B ----
   p.b_mode = c.b_mode;
-  if (c.b_mode == 2) {
+  if (c.b_mode == 2 && (force_im2col() || !pixel_box_fits(c.gb.OH, c.gb.OW, kBK))) {
+    st = make_tmap_im2col(&tb, c.b, c.tb, -c.gb.pad, c.gb.pad - (c.gb.R - 1), kBK, c.gb.stride);
+    if (st) return st;
+    p.b_mode = 4;
+    p.gb = c.gb;
+    DBS_REQUIRE(c.gb.Cin % bn == 0 || bn % c.gb.Cin == 0, DBS_ERR_ARGUMENT, "wgrad: tile must not straddle (r,s)");
+    DBS_REQUIRE(bn <= c.gb.Cin, DBS_ERR_ARGUMENT, "wgrad: BN %d > Cin %d", bn, c.gb.Cin);
+  } else if (c.b_mode == 2) {
     int bw, bh, bnn;
     st = pixel_box(c.gb.OH, c.gb.OW, kBK, bw, bh, bnn);
     if (st) return st;

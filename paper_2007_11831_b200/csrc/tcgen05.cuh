@@ -69,6 +69,21 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* desc, uint64_
       : "memory");
 }
 
+// im2col-mode load of a 4-D NHWC tensor: `pixelsPerColumn` consecutive output
+// pixels (walking W, then H, then N inside the tensor map's bounding box, so a
+// tile may cross rows and images) x `channelsPerPixel` channels, starting at
+// the window corner (c0, w, h, n) shifted by the filter tap (off_w, off_h);
+// pixels outside the tensor are zero-filled.
+__device__ __forceinline__ void tma_load_im2col_4d(void* dst, const void* desc, uint64_t* bar, int32_t c0, int32_t w,
+                                                   int32_t h, int32_t n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(w), "r"(h), "r"(n), "h"(off_w),
+      "h"(off_h)
+      : "memory");
+}
+
 // ---- TMEM -----------------------------------------------------------------
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
