@@ -306,8 +306,16 @@ int dbs_resnet_param_count(const dbs_resnet* m, int64_t* P);
 int dbs_resnet_param_table(const dbs_resnet* m, int64_t* off, int64_t* len, int32_t* kind, int32_t capacity,
                            int32_t* count);
 int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, const float* d_params,
-                                const float* d_x, const int32_t* d_labels, int64_t batch, const int64_t* d_iter,
+                                const void* d_x, const int32_t* d_labels, int64_t batch, const int64_t* d_iter,
                                 float* d_grad, float* d_loss, void* stream);
+/* ResNet-50 (config 5; torchvision layout, stride on the 3x3 conv, 25,557,032
+ * weights at 1000 classes): depth = 50, image = input side (224; any multiple of
+ * 32 in [64, 512]), classes 2..8192.  Input rows are uint8 [B][3][image][image]
+ * (pixel (u - 128) / 64), the stem weight is stored [64][160] (147 used), the
+ * FC weight [classes][2048].  depth = 18 / image = 32 is dbs_resnet_create. */
+int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_batch, int32_t classes, dbs_resnet** out);
+/* depth, input side, bytes per input row, padded stem K (any pointer may be NULL) */
+int dbs_resnet_info(const dbs_resnet* m, int32_t* depth, int32_t* image, int64_t* row_bytes, int32_t* stem_k);
 
 /* Implicit-GEMM convolutions (NHWC bf16, weights [Cout][k][k][Cin] bf16) on the
  * tcgen05 GEMM with 4-D TMA operand loads: y = conv(x, w); dx = dgrad(dy, w)

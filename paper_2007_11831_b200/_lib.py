@@ -127,6 +127,8 @@ SIGNATURES = {
     "dbs_dev_average_replicas_f32": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, ctypes.POINTER(c_vp),
                                              c_vp]),
     "dbs_resnet_create": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_resnet_create_ex": (c_i32, [c_i32, c_i32, c_i64, c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_resnet_info": (c_i32, [c_vp, P_i32, P_i32, P_i64, P_i32]),
     "dbs_resnet_destroy": (c_i32, [c_vp]),
     "dbs_resnet_param_count": (c_i32, [c_vp, P_i64]),
     "dbs_resnet_param_table": (c_i32, [c_vp, P_i64, P_i64, P_i32, c_i32, P_i32]),

@@ -239,9 +239,10 @@ extern "C" int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, i
                                        int64_t worker, void* stream);
 
 namespace dbs {
-int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const float* x_base, const int32_t* y_base,
+int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const void* x_base, const int32_t* y_base,
                    const int64_t* d_iter, int64_t B, float* grad, float* loss, cudaStream_t s);
 int resnet_param_count(const dbs_resnet* m);
+int64_t resnet_row_bytes(const dbs_resnet* m);
 int iter_increment(int64_t* d_iter, cudaStream_t s);
 }  // namespace dbs
 
@@ -327,11 +328,11 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
                          w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
       } else {
         dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
-        const float* x = static_cast<const float*>(w[i].x_shard);
+        const uint8_t* x = static_cast<const uint8_t*>(w[i].x_shard);
         const int32_t* y = w[i].y_shard;
         float* loss = w[i].loss;
         if (!d_iter) {  // host-indexed iteration
-          x += t * b * 3072;
+          x += t * b * resnet_row_bytes(m);
           y += t * b;
           loss = loss ? loss + t : nullptr;
         }
@@ -432,7 +433,7 @@ extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int
                            w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
         } else {
           dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
-          const float* x = static_cast<const float*>(w[i].x_shard) + t * b * 3072;
+          const uint8_t* x = static_cast<const uint8_t*>(w[i].x_shard) + t * b * resnet_row_bytes(m);
           st = resnet_fwd_bwd(m, d_params_bf16[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,
                               w[i].loss ? w[i].loss + t : nullptr, s);
         }

@@ -1,7 +1,10 @@
-// resnet.cu -- ResNet-18 (CIFAR stem: 3x3 conv, no max-pool) forward/backward
-// of one worker's variable batch, on the tcgen05 implicit-GEMM convolution.
+// resnet.cu -- ResNet-18 (CIFAR stem: 3x3 conv, no max-pool; configs 3-4) and
+// ResNet-50 (ImageNet stem: 7x7/2 conv + 3x3/2 max-pool, bottleneck blocks
+// [3, 4, 6, 3] with the stride on the 3x3 conv as in torchvision; config 5)
+// forward/backward of one worker's variable batch, on the tcgen05
+// implicit-GEMM convolution.
 //
-// This is the named model of configs 3-4 (BASELINE.json): the per-worker
+// These are the named models of BASELINE.json's configs: the per-worker
 // gradient of sgdlab.minibatch_gradient (sgdlab.py:200-205) for a network the
 // reference only models by its cost (cluster.py:132-145).
 //
@@ -29,7 +32,9 @@ namespace dbs {
 namespace {
 
 constexpr float kBnEps = 1e-5f;
-constexpr int kStemK = 32;  // 27 = 3x3x3 padded to 32
+constexpr int kStemK = 32;     // ResNet-18 stem: 27 = 3x3x3 padded to 32
+constexpr int kStem7K = 160;   // ResNet-50 stem: 147 = 7x7x3 padded to 160 (K blocks past 160 are TMA zero fill)
+constexpr int kMaxC = 2048;    // widest BatchNorm (ResNet-50 layer 4)
 
 __device__ __forceinline__ uint16_t f2bf(float f) {
   uint32_t u = __float_as_uint(f);
@@ -45,7 +50,7 @@ struct Conv {
 };
 
 struct Block {
-  int c1, c2, ds;  // indices into convs (ds = -1 when identity shortcut)
+  int c1, c2, c3, ds;  // indices into convs (c3 = -1: basic block; ds = -1: identity shortcut)
 };
 
 // ----------------------------- kernels ------------------------------------
@@ -317,6 +322,238 @@ __global__ void head_wgrad_kernel(const float* __restrict__ feat, const float* _
 
 __global__ void iter_inc_kernel(int64_t* it) { *it += 1; }
 
+// ---------------------------- ResNet-50 kernels -----------------------------
+
+// 7x7 / stride-2 / pad-3 stem im2col: x uint8 [B][3][S][S] (CHW per sample;
+// pixel value (u - 128) / 64, exact in bf16) -> A bf16 [B*OS*OS][160],
+// K = (r, s, c) with c fastest, columns 147..159 zero.
+__global__ void im2col_stem7_kernel(const uint8_t* __restrict__ x_base, const int64_t* __restrict__ iter, int64_t B,
+                                    int S, uint16_t* __restrict__ out) {
+  const int64_t t = iter ? *iter : 0;
+  const int64_t plane = (int64_t)S * S;
+  const uint8_t* x = x_base + t * B * 3 * plane;
+  const int OS = S / 2;
+  const int64_t total = B * OS * OS;
+  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < total;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = pix / ((int64_t)OS * OS);
+    const int rem = (int)(pix - n * OS * OS);
+    const int oh = rem / OS, ow = rem - (rem / OS) * OS;
+    const uint8_t* xs = x + n * 3 * plane;
+    uint4* o = reinterpret_cast<uint4*>(out + pix * kStem7K);
+    uint32_t acc[4] = {0, 0, 0, 0};
+    int k = 0;
+    for (int r = 0; r < 7; r++) {
+      const int hh = 2 * oh + r - 3;
+      for (int s = 0; s < 7; s++) {
+        const int ww = 2 * ow + s - 3;
+        const bool in = (hh >= 0 && hh < S && ww >= 0 && ww < S);
+#pragma unroll
+        for (int c = 0; c < 3; c++, k++) {
+          const float v = in ? ((float)xs[c * plane + (int64_t)hh * S + ww] - 128.0f) * 0.015625f : 0.0f;
+          acc[(k & 7) >> 1] |= (uint32_t)f2bf(v) << ((k & 1) * 16);
+          if ((k & 7) == 7) {
+            o[k >> 3] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+            acc[0] = acc[1] = acc[2] = acc[3] = 0;
+          }
+        }
+      }
+    }
+    // k == 147: flush the partial chunk, then zero chunks up to 160
+    o[k >> 3] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+    for (int q = (k >> 3) + 1; q < kStem7K / 8; q++) o[q] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+// 3x3 / stride-2 / pad-1 max-pool, NHWC bf16, 8 channels per thread; idx keeps
+// the first maximal tap (row-major scan, as torch's max_pool2d) for backward
+__global__ void maxpool_fwd_kernel(const uint16_t* __restrict__ in, int64_t B, int H, int W, int C, int OH, int OW,
+                                   uint16_t* __restrict__ out, uint8_t* __restrict__ idx) {
+  const int cv = C / 8;
+  const int64_t total = B * OH * OW * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    const int64_t pix = i / cv;
+    const int ow = (int)(pix % OW);
+    const int oh = (int)((pix / OW) % OH);
+    const int64_t n = pix / ((int64_t)OW * OH);
+    float best[8];
+    uint8_t arg[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      best[k] = -INFINITY;
+      arg[k] = 0;
+    }
+    for (int r = 0; r < 3; r++) {
+      const int h = 2 * oh + r - 1;
+      if (h < 0 || h >= H) continue;
+      for (int s = 0; s < 3; s++) {
+        const int w = 2 * ow + s - 1;
+        if (w < 0 || w >= W) continue;
+        const uint4 q = reinterpret_cast<const uint4*>(in + ((n * H + h) * W + w) * C)[c8];
+        const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const float v = bf2f((uint16_t)(wv[k >> 1] >> ((k & 1) * 16)));
+          if (v > best[k]) {
+            best[k] = v;
+            arg[k] = (uint8_t)(r * 3 + s);
+          }
+        }
+      }
+    }
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; k++) o[k >> 1] |= (uint32_t)f2bf(best[k]) << ((k & 1) * 16);
+    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    uint2 a;
+    a.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | ((uint32_t)arg[3] << 24);
+    a.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | ((uint32_t)arg[7] << 24);
+    reinterpret_cast<uint2*>(idx)[i] = a;
+  }
+}
+
+// max-pool backward in gather form (no atomics): input pixel (h, w) collects
+// the gradient of every window (<= 2 x 2) whose recorded maximum it is
+__global__ void maxpool_bwd_kernel(const uint16_t* __restrict__ gout, const uint8_t* __restrict__ idx, int64_t B,
+                                   int H, int W, int C, int OH, int OW, uint16_t* __restrict__ gin) {
+  const int cv = C / 8;
+  const int64_t total = B * H * W * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    const int64_t pix = i / cv;
+    const int w = (int)(pix % W);
+    const int h = (int)((pix / W) % H);
+    const int64_t n = pix / ((int64_t)W * H);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc[k] = 0.f;
+    for (int oh = (h > 0 ? h : 1) / 2; oh <= (h + 1) / 2 && oh < OH; oh++) {
+      const int r = h - (2 * oh - 1);
+      if (r < 0 || r > 2) continue;
+      for (int ow = (w > 0 ? w : 1) / 2; ow <= (w + 1) / 2 && ow < OW; ow++) {
+        const int s = w - (2 * ow - 1);
+        if (s < 0 || s > 2) continue;
+        const int64_t o = ((n * OH + oh) * OW + ow) * cv + c8;
+        const uint2 a = reinterpret_cast<const uint2*>(idx)[o];
+        const uint4 q = reinterpret_cast<const uint4*>(gout)[o];
+        const uint32_t gv[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t av[2] = {a.x, a.y};
+        const uint32_t tap = (uint32_t)(r * 3 + s);
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+          if (((av[k >> 2] >> ((k & 3) * 8)) & 0xFFu) == tap) acc[k] += bf2f((uint16_t)(gv[k >> 1] >> ((k & 1) * 16)));
+      }
+    }
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; k++) o[k >> 1] |= (uint32_t)f2bf(acc[k]) << ((k & 1) * 16);
+    reinterpret_cast<uint4*>(gin)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// global average pool: x bf16 [B][HW][C] -> feat bf16 [B][C] (the FC GEMM operand)
+__global__ void avgpool_kernel(const uint16_t* __restrict__ x, int64_t B, int HW, int C, uint16_t* __restrict__ feat) {
+  const int cv = C / 8;
+  const int64_t total = B * cv;
+  const float inv = 1.0f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / cv;
+    const int c8 = (int)(i - n * cv);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc[k] = 0.f;
+    for (int p = 0; p < HW; p++) {
+      const uint4 q = reinterpret_cast<const uint4*>(x + (n * HW + p) * C)[c8];
+      const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 8; k++) acc[k] += bf2f((uint16_t)(wv[k >> 1] >> ((k & 1) * 16)));
+    }
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; k++) o[k >> 1] |= (uint32_t)f2bf(acc[k] * inv) << ((k & 1) * 16);
+    reinterpret_cast<uint4*>(feat)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  float r = sh[0];
+  for (int w = 1; w < nw; w++) r = is_max ? fmaxf(r, sh[w]) : r + sh[w];
+  return r;
+}
+
+// softmax cross-entropy, one CTA per sample: logits fp32 [B][ld] -> per-sample
+// loss, dlogits / B in fp32 (bias gradient) and bf16 (GEMM operand, padding
+// columns zeroed)
+__global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, int ld,
+                                                 const int32_t* __restrict__ y_base, const int64_t* __restrict__ iter,
+                                                 int64_t B, int classes, float* __restrict__ dlog_f,
+                                                 uint16_t* __restrict__ dlog_b, float* __restrict__ loss_per) {
+  __shared__ float sh[32];
+  const int64_t n = blockIdx.x;
+  const int64_t t = iter ? *iter : 0;
+  const int32_t label = y_base[t * B + n];
+  const float* z = logits + n * ld;
+  float mx = -INFINITY;
+  for (int k = threadIdx.x; k < classes; k += blockDim.x) mx = fmaxf(mx, z[k]);
+  mx = block_reduce(mx, sh, true);
+  float se = 0.f;
+  for (int k = threadIdx.x; k < classes; k += blockDim.x) se += __expf(z[k] - mx);
+  se = block_reduce(se, sh, false);
+  const float inv = 1.0f / se, invB = 1.0f / (float)B;
+  for (int k = threadIdx.x; k < ld; k += blockDim.x) {
+    float g = 0.f;
+    if (k < classes) g = (__expf(z[k] - mx) * inv - (k == label ? 1.f : 0.f)) * invB;
+    dlog_f[n * ld + k] = g;
+    dlog_b[n * ld + k] = f2bf(g);
+  }
+  if (threadIdx.x == 0) loss_per[n] = (mx + __logf(se)) - z[label];
+}
+
+// FC bias gradient (column sums of dlogits) and the batch-mean loss
+__global__ void head_bias_kernel(const float* __restrict__ dlog_f, int ld, const float* __restrict__ loss_per,
+                                 int64_t B, int classes, float* __restrict__ db, float* __restrict__ loss_out,
+                                 const int64_t* __restrict__ iter) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < classes) {
+    float s = 0.f;
+    for (int64_t n = 0; n < B; n++) s += dlog_f[n * ld + k];
+    db[k] = s;
+  }
+  if (k == 0 && loss_out) {
+    float s = 0.f;
+    for (int64_t n = 0; n < B; n++) s += loss_per[n];
+    loss_out[iter ? *iter : 0] = s / (float)B;
+  }
+}
+
+// gradient of the average pool: dOut[n][p][c] = dfeat[n][c] / HW (bf16)
+__global__ void head_bcast_kernel(const float* __restrict__ dfeat, int64_t B, int HW, int C,
+                                  uint16_t* __restrict__ dout) {
+  const int cv = C / 8;
+  const int64_t total = B * HW * cv;
+  const float inv = 1.0f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    const int64_t n = i / ((int64_t)cv * HW);
+    const float4 a = reinterpret_cast<const float4*>(dfeat + n * C + c8 * 8)[0];
+    const float4 b = reinterpret_cast<const float4*>(dfeat + n * C + c8 * 8)[1];
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; k++) o[k >> 1] |= (uint32_t)f2bf(v[k] * inv) << ((k & 1) * 16);
+    reinterpret_cast<uint4*>(dout)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   int64_t cap = (int64_t)num_sms() * 8;
@@ -331,6 +568,22 @@ using namespace dbs;
 struct dbs_resnet {
   int64_t max_b = 0;
   int classes = 10;
+  int arch = 18;                           // 18 (CIFAR stem) or 50 (ImageNet stem)
+  int image = 32;                          // input side (32 for ResNet-18; 224 for config 5)
+  int64_t row_bytes = 3072 * 4;            // one input sample in the repacked shard
+  int stem_k = kStemK;                     // padded K of the stem's explicit im2col
+  int feat_c = 512, feat_hw = 16;          // last feature map: channels, pixels
+  int cpad = 16;                           // logits / dlogits row pitch (ResNet-50 head)
+  std::vector<char> need_a;                // per conv: post-BN(+ReLU) output is stored
+  // ResNet-50 extras
+  uint16_t* mp_out = nullptr;              // max-pool output [B][S/4][S/4][64]
+  uint8_t* mp_idx = nullptr;               // its arg-max taps
+  uint16_t* feat_b = nullptr;              // pooled features bf16 [B][2048]
+  float* logits = nullptr;                 // [B][cpad]
+  float* dlog_f = nullptr;                 // [B][cpad]
+  uint16_t* dlog_b = nullptr;              // [B][cpad]
+  float* dfeat = nullptr;                  // [B][2048]
+  uint16_t* g4 = nullptr;
   std::vector<Conv> convs;
   std::vector<Block> blocks;
   int stem = 0;
@@ -396,6 +649,7 @@ void build_layers(dbs_resnet* m) {
       const int cout = widths[L];
       const int stride = (L > 0 && bI == 0) ? 2 : 1;
       Block b{};
+      b.c3 = -1;
       b.c1 = add_conv(cin, cout, 3, stride, 1, H, H);
       const int OH = m->convs[b.c1].OH;
       b.c2 = add_conv(cout, cout, 3, 1, 1, OH, OH);
@@ -408,6 +662,66 @@ void build_layers(dbs_resnet* m) {
   m->fc_w = add_param((int64_t)m->classes * 512, 3);
   m->fc_b = add_param(m->classes, 4);
   m->P = (off + 31) & ~int64_t(31);
+  m->need_a.assign(m->convs.size(), 0);
+  m->need_a[m->stem] = 1;
+  for (auto& b : m->blocks) m->need_a[b.c1] = 1;
+}
+
+// ResNet-50 (torchvision layout, v1.5: stride on the 3x3 conv), S x S input
+void build_layers50(dbs_resnet* m) {
+  int64_t off = 0;
+  auto add_param = [&](int64_t len, int kind) {
+    const int64_t o = off;
+    m->t_off.push_back(o);
+    m->t_len.push_back(len);
+    m->t_kind.push_back(kind);
+    off += pad8(len);
+    return o;
+  };
+  auto add_conv = [&](int cin, int cout, int k, int stride, int pad, int H) {
+    Conv c{};
+    c.cin = cin;
+    c.cout = cout;
+    c.k = k;
+    c.stride = stride;
+    c.pad = pad;
+    c.H = c.W = H;
+    c.OH = c.OW = (H + 2 * pad - k) / stride + 1;
+    c.w_len = (cin == 3) ? (int64_t)cout * kStem7K : (int64_t)cout * k * k * cin;
+    c.w_off = add_param(c.w_len, 0);
+    c.g_off = add_param(cout, 1);
+    c.b_off = add_param(cout, 2);
+    m->convs.push_back(c);
+    return (int)m->convs.size() - 1;
+  };
+  const int S = m->image;
+  m->stem = add_conv(3, 64, 7, 2, 3, S);
+  int H = S / 4, cin = 64;  // after the stem (S/2) and the max-pool (S/4)
+  const int widths[4] = {64, 128, 256, 512};
+  const int depth[4] = {3, 4, 6, 3};
+  for (int L = 0; L < 4; L++) {
+    for (int bI = 0; bI < depth[L]; bI++) {
+      const int w = widths[L], cout = 4 * w;
+      const int stride = (L > 0 && bI == 0) ? 2 : 1;
+      Block b{};
+      b.c1 = add_conv(cin, w, 1, 1, 0, H);
+      b.c2 = add_conv(w, w, 3, stride, 1, H);
+      const int OH = m->convs[b.c2].OH;
+      b.c3 = add_conv(w, cout, 1, 1, 0, OH);
+      b.ds = (stride != 1 || cin != cout) ? add_conv(cin, cout, 1, stride, 0, H) : -1;
+      m->blocks.push_back(b);
+      cin = cout;
+      H = OH;
+    }
+  }
+  m->feat_c = cin;
+  m->feat_hw = H * H;
+  m->fc_w = add_param((int64_t)m->classes * cin, 3);
+  m->fc_b = add_param(m->classes, 4);
+  m->P = (off + 31) & ~int64_t(31);
+  m->need_a.assign(m->convs.size(), 0);
+  m->need_a[m->stem] = 1;
+  for (auto& b : m->blocks) m->need_a[b.c1] = m->need_a[b.c2] = 1;
 }
 
 int alloc_all(dbs_resnet* m) {
@@ -416,13 +730,17 @@ int alloc_all(dbs_resnet* m) {
   auto A = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, bytes);
   };
-  A((void**)&m->stem_cols, (size_t)B * 1024 * kStemK * 2);
+  {
+    const Conv& st = m->convs[m->stem];
+    A((void**)&m->stem_cols, (size_t)B * st.OH * st.OW * m->stem_k * 2);
+  }
   int64_t max_act = 0;
-  for (auto& c : m->convs) {
+  for (size_t ci = 0; ci < m->convs.size(); ci++) {
+    const Conv& c = m->convs[ci];
     const int64_t n = B * c.OH * c.OW * c.cout;
-    uint16_t *y, *a;
+    uint16_t *y, *a = nullptr;
     A((void**)&y, n * 2);
-    A((void**)&a, n * 2);
+    if (m->need_a[ci]) A((void**)&a, n * 2);
     m->y.push_back(y);
     m->a.push_back(a);
     float *mu, *is;
@@ -435,19 +753,33 @@ int alloc_all(dbs_resnet* m) {
     if (nin > max_act) max_act = nin;
   }
   for (size_t i = 0; i < m->blocks.size(); i++) {
-    const Conv& c = m->convs[m->blocks[i].c2];
+    const Block& bk = m->blocks[i];
+    const Conv& c = m->convs[bk.c3 >= 0 ? bk.c3 : bk.c2];  // the block's last conv shapes its output
     uint16_t* o;
     A((void**)&o, (size_t)B * c.OH * c.OW * c.cout * 2);
     m->blk_out.push_back(o);
   }
-  A((void**)&m->sum_part, 512 * sizeof(double));
-  A((void**)&m->sq_part, 512 * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(m->sum_part, 0, 512 * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(m->sq_part, 0, 512 * sizeof(double));
+  A((void**)&m->sum_part, kMaxC * sizeof(double));
+  A((void**)&m->sq_part, kMaxC * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(m->sum_part, 0, kMaxC * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(m->sq_part, 0, kMaxC * sizeof(double));
   A((void**)&m->g0, max_act * 2);
   A((void**)&m->g1, max_act * 2);
   A((void**)&m->g2, max_act * 2);
   A((void**)&m->g3, max_act * 2);
+  if (m->arch == 50) {
+    const Conv& st = m->convs[m->stem];
+    const int P = st.OH / 2;
+    const int64_t mp = B * P * P * 64;
+    A((void**)&m->g4, max_act * 2);
+    A((void**)&m->mp_out, mp * 2);
+    A((void**)&m->mp_idx, mp);
+    A((void**)&m->feat_b, (size_t)B * m->feat_c * 2);
+    A((void**)&m->logits, (size_t)B * m->cpad * 4);
+    A((void**)&m->dlog_f, (size_t)B * m->cpad * 4);
+    A((void**)&m->dlog_b, (size_t)B * m->cpad * 2);
+    A((void**)&m->dfeat, (size_t)B * m->feat_c * 4);
+  }
   A((void**)&m->feat, (size_t)B * 512 * 4);
   A((void**)&m->dlog, (size_t)B * 16 * 4);
   A((void**)&m->loss_per, (size_t)B * 4);
@@ -487,12 +819,18 @@ int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64
   call.sq_part = m->sq_part;
   call.b = wb + c.w_off;
   call.b_mode = 0;
-  if (c.cin == 3) {  // stem: explicit im2col columns [M][32]
-    call.K = kStemK;
+  if (c.cin == 3) {  // stem: explicit im2col columns [M][stem_k]
+    call.K = m->stem_k;
     call.a_mode = 0;
     call.a = m->stem_cols;
-    call.lda = kStemK;
-    call.ldb = kStemK;
+    call.lda = m->stem_k;
+    call.ldb = m->stem_k;
+  } else if (c.k == 1 && c.stride == 1) {  // 1x1: a plain GEMM over the [pixels][Cin] view
+    call.K = c.cin;
+    call.a_mode = 0;
+    call.a = x;
+    call.lda = c.cin;
+    call.ldb = c.cin;
   } else {
     call.K = (int64_t)c.k * c.k * c.cin;
     call.a_mode = 2;
@@ -560,6 +898,17 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
   call.epi = accumulate ? DBS_EPI_BF16_ACCUM : DBS_EPI_BF16;
   call.d = dx;
   call.ldd = c.cin;
+  if (c.k == 1 && c.stride == 1) {
+    // 1x1: dX [pixels][Cin] = dY [pixels][Cout] x W [Cout][Cin] (W read MN-major)
+    call.M = B * c.H * c.W;
+    call.K = c.cout;
+    call.a_mode = 0;
+    call.lda = c.cout;
+    call.b_mode = 1;
+    call.ldb = c.cin;
+    call.tb = ConvTensor{};
+    return conv_gemm(call, s);
+  }
   if (c.stride == 1) {
     // stride 1: the flipped filter over dY, same padding
     call.M = B * c.H * c.W;
@@ -627,14 +976,24 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
   call.epi = DBS_EPI_F32_ATOMIC;
   call.d = dw;
   int bn;
-  if (c.cin == 3) {  // stem: columns [pixels][32]
-    call.N = kStemK;
+  if (c.cin == 3) {  // stem: columns [pixels][stem_k]
+    const int sk = (int)(c.w_len / c.cout);
+    call.N = sk;
     call.K = pixels;
     call.b_mode = 1;
     call.b = x;
-    call.ldb = kStemK;
-    call.ldd = kStemK;
+    call.ldb = sk;
+    call.ldd = sk;
     bn = 64;
+  } else if (c.k == 1 && c.stride == 1) {  // 1x1: dW = dY^T X over the [pixels][Cin] view
+    call.N = c.cin;
+    call.K = pixels;
+    call.b_mode = 1;
+    call.b = x;
+    call.ldb = c.cin;
+    call.ldd = c.cin;
+    bn = c.cin >= 256 ? 256 : c.cin;
+    call.bn_override = bn;
   } else {
     call.N = (int64_t)c.k * c.k * c.cin;
     call.K = pixels;
@@ -666,11 +1025,111 @@ int conv_wgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* x, int
 
 namespace dbs {
 
-int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const float* x_base, const int32_t* y_base,
+int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const uint8_t* x_base,
+                     const int32_t* y_base, const int64_t* d_iter, int64_t B, float* grad, float* loss,
+                     cudaStream_t s) {
+  int st;
+  DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
+  // ---------------- stem: 7x7/2 conv (explicit im2col) + BN + ReLU + 3x3/2 max-pool ----------------
+  const Conv& sc = m->convs[m->stem];
+  im2col_stem7_kernel<<<grid_for(B * sc.OH * sc.OW, 128), 128, 0, s>>>(x_base, d_iter, B, m->image, m->stem_cols);
+  DBS_LAUNCH_CHECK();
+  if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
+  if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
+  const int PH = sc.OH / 2;
+  maxpool_fwd_kernel<<<grid_for(B * PH * PH * 8, 256), 256, 0, s>>>(m->a[m->stem], B, sc.OH, sc.OW, 64, PH, PH,
+                                                                     m->mp_out, m->mp_idx);
+  DBS_LAUNCH_CHECK();
+  // ---------------- bottleneck blocks ----------------
+  const uint16_t* x = m->mp_out;
+  std::vector<const uint16_t*> blk_in(m->blocks.size());
+  for (size_t i = 0; i < m->blocks.size(); i++) {
+    const Block& b = m->blocks[i];
+    blk_in[i] = x;
+    if ((st = conv_fwd(m, b.c1, x, wb, B, s))) return st;
+    if ((st = bn_apply(m, b.c1, pf, nullptr, -1, 1, B, m->a[b.c1], s))) return st;
+    if ((st = conv_fwd(m, b.c2, m->a[b.c1], wb, B, s))) return st;
+    if ((st = bn_apply(m, b.c2, pf, nullptr, -1, 1, B, m->a[b.c2], s))) return st;
+    if ((st = conv_fwd(m, b.c3, m->a[b.c2], wb, B, s))) return st;
+    if (b.ds >= 0 && (st = conv_fwd(m, b.ds, x, wb, B, s))) return st;
+    if ((st = bn_apply(m, b.c3, pf, b.ds >= 0 ? nullptr : x, b.ds, 1, B, m->blk_out[i], s))) return st;
+    x = m->blk_out[i];
+  }
+  // ---------------- head: average pool, FC (tcgen05 GEMMs), softmax cross-entropy ----------------
+  const int C = m->feat_c, HW = m->feat_hw, K = m->classes, ld = m->cpad;
+  avgpool_kernel<<<grid_for(B * (C / 8), 256), 256, 0, s>>>(x, B, HW, C, m->feat_b);
+  DBS_LAUNCH_CHECK();
+  const uint16_t* wfc = wb + m->fc_w;
+  // logits [B][K] = feat [B][C] . Wfc [K][C]^T + b
+  if ((st = gemm_bf16(m->feat_b, 0, C, wfc, 0, C, m->logits, ld, B, K, C, DBS_EPI_BIAS_F32, pf + m->fc_b, nullptr, s,
+                      nullptr)))
+    return st;
+  ce_kernel<<<(unsigned)B, 256, 0, s>>>(m->logits, ld, y_base, d_iter, B, K, m->dlog_f, m->dlog_b, m->loss_per);
+  DBS_LAUNCH_CHECK();
+  head_bias_kernel<<<(K + 255) / 256, 256, 0, s>>>(m->dlog_f, ld, m->loss_per, B, K, grad + m->fc_b,
+                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr);
+  DBS_LAUNCH_CHECK();
+  // dWfc [K][C] = dlog^T . feat  (both MN-major over the batch)
+  if ((st = gemm_bf16(m->dlog_b, 1, ld, m->feat_b, 1, C, grad + m->fc_w, C, K, C, B, DBS_EPI_F32, nullptr, nullptr, s,
+                      nullptr)))
+    return st;
+  // dfeat [B][C] = dlog [B][K] . Wfc [K][C]  (Wfc MN-major)
+  if ((st = gemm_bf16(m->dlog_b, 0, ld, wfc, 1, C, m->dfeat, C, B, C, K, DBS_EPI_F32, nullptr, nullptr, s, nullptr)))
+    return st;
+  uint16_t* gcur = m->g0;
+  head_bcast_kernel<<<grid_for(B * HW * (C / 8), 256), 256, 0, s>>>(m->dfeat, B, HW, C, gcur);
+  DBS_LAUNCH_CHECK();
+  // ---------------- backward through the blocks ----------------
+  // buffers: gx = gradient of the block input, t0 = BN outputs' gradients,
+  // t1 = conv input gradients / masked shortcut gradient, t2 = shortcut BN's
+  uint16_t* gx = m->g1;
+  uint16_t* t0 = m->g2;
+  uint16_t* t1 = m->g3;
+  uint16_t* t2 = m->g4;
+  for (int i = (int)m->blocks.size() - 1; i >= 0; i--) {
+    const Block& b = m->blocks[i];
+    // BN3 with the block's output ReLU mask; the masked gradient is the
+    // identity shortcut's gradient (gx) or the projection's input (t1)
+    if ((st = bn_bwd(m, b.c3, pf, grad, gcur, m->blk_out[i], B, t0, b.ds >= 0 ? t1 : gx, s))) return st;
+    if (b.ds >= 0) {
+      if ((st = bn_bwd(m, b.ds, pf, grad, t1, nullptr, B, t2, nullptr, s))) return st;
+      if ((st = conv_wgrad(m, b.ds, t2, blk_in[i], B, grad, s))) return st;
+    }
+    if ((st = conv_wgrad(m, b.c3, t0, m->a[b.c2], B, grad, s))) return st;
+    if ((st = conv_dgrad(m, b.c3, t0, wb, B, t1, 0, s))) return st;
+    if ((st = bn_bwd(m, b.c2, pf, grad, t1, m->a[b.c2], B, t0, nullptr, s))) return st;
+    if ((st = conv_wgrad(m, b.c2, t0, m->a[b.c1], B, grad, s))) return st;
+    if ((st = conv_dgrad(m, b.c2, t0, wb, B, t1, 0, s))) return st;
+    if ((st = bn_bwd(m, b.c1, pf, grad, t1, m->a[b.c1], B, t0, nullptr, s))) return st;
+    if ((st = conv_wgrad(m, b.c1, t0, blk_in[i], B, grad, s))) return st;
+    if (b.ds >= 0) {
+      // the 1x1 stride-1 conv1 covers every input pixel; the projection's
+      // (stride-2: even pixels only) input gradient accumulates onto it
+      if ((st = conv_dgrad(m, b.c1, t0, wb, B, gx, 0, s))) return st;
+      if ((st = conv_dgrad(m, b.ds, t2, wb, B, gx, 1, s))) return st;
+    } else {
+      if ((st = conv_dgrad(m, b.c1, t0, wb, B, gx, 1, s))) return st;
+    }
+    uint16_t* old = gcur;
+    gcur = gx;
+    gx = old;
+  }
+  // ---------------- stem backward: max-pool, BN + ReLU mask, weight gradient ----------------
+  maxpool_bwd_kernel<<<grid_for(B * sc.OH * sc.OW * 8, 256), 256, 0, s>>>(gcur, m->mp_idx, B, sc.OH, sc.OW, 64, PH,
+                                                                           PH, t1);
+  DBS_LAUNCH_CHECK();
+  if ((st = bn_bwd(m, m->stem, pf, grad, t1, m->a[m->stem], B, t0, nullptr, s))) return st;
+  return conv_wgrad(m, m->stem, t0, nullptr, B, grad, s);
+}
+
+int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const void* x_any, const int32_t* y_base,
                    const int64_t* d_iter, int64_t B, float* grad, float* loss, cudaStream_t s) {
-  DBS_REQUIRE(m && wb && pf && x_base && y_base && grad, DBS_ERR_ARGUMENT, "resnet: null argument");
+  DBS_REQUIRE(m && wb && pf && x_any && y_base && grad, DBS_ERR_ARGUMENT, "resnet: null argument");
   DBS_REQUIRE(B >= 1 && B <= m->max_b, DBS_ERR_ARGUMENT, "resnet: batch %lld outside [1, %lld]", (long long)B,
               (long long)m->max_b);
+  if (m->arch == 50)
+    return resnet50_fwd_bwd(m, wb, pf, static_cast<const uint8_t*>(x_any), y_base, d_iter, B, grad, loss, s);
+  const float* x_base = static_cast<const float*>(x_any);
   int st;
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
   // ---------------- forward ----------------
@@ -745,6 +1204,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const flo
 }
 
 int resnet_param_count(const dbs_resnet* m) { return (int)m->P; }
+int64_t resnet_row_bytes(const dbs_resnet* m) { return m->row_bytes; }
 
 int iter_increment(int64_t* d_iter, cudaStream_t s) {
   iter_inc_kernel<<<1, 1, 0, s>>>(d_iter);
@@ -754,19 +1214,48 @@ int iter_increment(int64_t* d_iter, cudaStream_t s) {
 
 }  // namespace dbs
 
-extern "C" int dbs_resnet_create(int64_t max_batch, int32_t classes, dbs_resnet** out) {
-  DBS_REQUIRE(out && max_batch > 0 && classes >= 2 && classes <= 16, DBS_ERR_ARGUMENT,
-              "resnet_create: need max_batch > 0 and 2 <= classes <= 16");
+extern "C" int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_batch, int32_t classes,
+                                    dbs_resnet** out) {
+  DBS_REQUIRE(out && max_batch > 0, DBS_ERR_ARGUMENT, "resnet_create: need max_batch > 0");
+  DBS_REQUIRE((depth == 18 && image == 32 && classes >= 2 && classes <= 16) ||
+                  (depth == 50 && image >= 64 && image % 32 == 0 && image <= 512 && classes >= 2 && classes <= 8192),
+              DBS_ERR_ARGUMENT,
+              "resnet_create: depth 18 needs a 32x32 image and 2..16 classes; depth 50 a multiple-of-32 image side "
+              "in [64, 512] and 2..8192 classes (got depth %d, image %d, classes %d)",
+              depth, image, classes);
   dbs_resnet* m = new dbs_resnet();
   m->max_b = max_batch;
   m->classes = classes;
-  build_layers(m);
+  m->arch = depth;
+  m->image = image;
+  if (depth == 50) {
+    m->row_bytes = (int64_t)3 * image * image;  // uint8 pixels
+    m->stem_k = kStem7K;
+    m->cpad = (classes + 7) & ~7;
+    build_layers50(m);
+  } else {
+    build_layers(m);
+  }
   int st = alloc_all(m);
   if (st) {
     dbs_resnet_destroy(m);
     return st;
   }
   *out = m;
+  return DBS_OK;
+}
+
+extern "C" int dbs_resnet_create(int64_t max_batch, int32_t classes, dbs_resnet** out) {
+  return dbs_resnet_create_ex(18, 32, max_batch, classes, out);
+}
+
+extern "C" int dbs_resnet_info(const dbs_resnet* m, int32_t* depth, int32_t* image, int64_t* row_bytes,
+                               int32_t* stem_k) {
+  DBS_REQUIRE(m, DBS_ERR_ARGUMENT, "resnet_info: null");
+  if (depth) *depth = m->arch;
+  if (image) *image = m->image;
+  if (row_bytes) *row_bytes = m->row_bytes;
+  if (stem_k) *stem_k = m->stem_k;
   return DBS_OK;
 }
 
@@ -788,6 +1277,14 @@ extern "C" int dbs_resnet_destroy(dbs_resnet* m) {
   cudaFree(m->dlog);
   cudaFree(m->loss_per);
   cudaFree(m->loss_scratch);
+  cudaFree(m->g4);
+  cudaFree(m->mp_out);
+  cudaFree(m->mp_idx);
+  cudaFree(m->feat_b);
+  cudaFree(m->logits);
+  cudaFree(m->dlog_f);
+  cudaFree(m->dlog_b);
+  cudaFree(m->dfeat);
   delete m;
   return DBS_OK;
 }
@@ -813,7 +1310,7 @@ extern "C" int dbs_resnet_param_table(const dbs_resnet* m, int64_t* off, int64_t
 }
 
 extern "C" int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, const float* d_params,
-                                           const float* d_x, const int32_t* d_labels, int64_t batch,
+                                           const void* d_x, const int32_t* d_labels, int64_t batch,
                                            const int64_t* d_iter, float* d_grad, float* d_loss, void* stream) {
   return resnet_fwd_bwd(m, d_params_bf16, d_params, d_x, d_labels, d_iter, batch, d_grad, d_loss, as_stream(stream));
 }

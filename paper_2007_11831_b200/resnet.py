@@ -1,4 +1,5 @@
-"""ResNet-18 (CIFAR variant) -- the named model of configs 3/4 -- on tcgen05.
+"""ResNet-18 (CIFAR variant; configs 3/4) and ResNet-50 (ImageNet stem,
+torchvision v1.5 bottlenecks; config 5) on tcgen05.
 
 Host side of csrc/resnet.cu: the flat parameter layout (queried from the
 library's parameter table, torchvision order), host initialisation
@@ -7,7 +8,8 @@ uniform for the classifier), conversion to / from PyTorch OIHW tensors for the
 parity tests, and per-worker activation scratch.
 
 Data: synthetic CIFAR-shaped samples, fp32 [D][3][32][32] rows, labels 0..9
-(SURVEY.md 8d, C3/C4 inputs).
+(SURVEY.md 8d, C3/C4 inputs); synthetic ImageNet-shaped samples, uint8
+[D][3][224][224] rows (pixel value (u - 128) / 64), labels 0..999 (C5).
 """
 
 from __future__ import annotations
@@ -20,7 +22,6 @@ import numpy as np
 from . import _lib
 
 KIND_CONV, KIND_BN_G, KIND_BN_B, KIND_FC_W, KIND_FC_B = 0, 1, 2, 3, 4
-STEM_K = 32
 
 
 class ResnetLayout:
@@ -28,45 +29,63 @@ class ResnetLayout:
 
     _cache = {}
 
-    def __init__(self, classes: int = 10):
-        key = classes
+    def __init__(self, classes: int = 10, depth: int = 18, image: int = 32):
+        key = (classes, depth, image)
         if key not in ResnetLayout._cache:
             h = ctypes.c_void_p()
-            _lib.check(_lib.lib().dbs_resnet_create(1, classes, ctypes.byref(h)), "resnet_create")
+            _lib.check(_lib.lib().dbs_resnet_create_ex(depth, image, 1, classes, ctypes.byref(h)), "resnet_create")
             try:
                 P = ctypes.c_int64()
                 _lib.check(_lib.lib().dbs_resnet_param_count(h, ctypes.byref(P)), "resnet_param_count")
-                cap = 256
+                cap = 512
                 off = (ctypes.c_int64 * cap)()
                 ln = (ctypes.c_int64 * cap)()
                 kd = (ctypes.c_int32 * cap)()
                 cnt = ctypes.c_int32()
                 _lib.check(_lib.lib().dbs_resnet_param_table(h, off, ln, kd, cap, ctypes.byref(cnt)), "param_table")
-                ResnetLayout._cache[key] = (P.value, [(off[i], ln[i], kd[i]) for i in range(cnt.value)])
+                rb, sk = ctypes.c_int64(), ctypes.c_int32()
+                _lib.check(_lib.lib().dbs_resnet_info(h, None, None, ctypes.byref(rb), ctypes.byref(sk)), "info")
+                ResnetLayout._cache[key] = (P.value, [(off[i], ln[i], kd[i]) for i in range(cnt.value)], rb.value,
+                                            sk.value)
             finally:
                 _lib.lib().dbs_resnet_destroy(h)
-        self.P, self.table = ResnetLayout._cache[key]
-        self.classes = classes
+        self.P, self.table, self.row_bytes, self.stem_k = ResnetLayout._cache[key]
+        self.classes, self.depth, self.image = classes, depth, image
         self.shapes = self._shapes()
 
     def _shapes(self):
         """PyTorch (OIHW) shape of each table entry, in torchvision order."""
         shapes = []
-        convs = [(3, 64, 3)]
-        cin = 64
-        for L, w in enumerate((64, 128, 256, 512)):
-            for b in range(2):
-                stride = 2 if (L > 0 and b == 0) else 1
-                convs.append((cin, w, 3))
-                convs.append((w, w, 3))
-                if stride != 1 or cin != w:
-                    convs.append((cin, w, 1))
-                cin = w
+        if self.depth == 18:
+            convs = [(3, 64, 3)]
+            cin = 64
+            for L, w in enumerate((64, 128, 256, 512)):
+                for b in range(2):
+                    stride = 2 if (L > 0 and b == 0) else 1
+                    convs.append((cin, w, 3))
+                    convs.append((w, w, 3))
+                    if stride != 1 or cin != w:
+                        convs.append((cin, w, 1))
+                    cin = w
+        else:
+            convs = [(3, 64, 7)]
+            cin = 64
+            for L, (w, n) in enumerate(zip((64, 128, 256, 512), (3, 4, 6, 3))):
+                for b in range(n):
+                    stride = 2 if (L > 0 and b == 0) else 1
+                    convs += [(cin, w, 1), (w, w, 3), (w, 4 * w, 1)]
+                    if stride != 1 or cin != 4 * w:
+                        convs.append((cin, 4 * w, 1))
+                    cin = 4 * w
         for ci, co, k in convs:
             shapes += [(co, ci, k, k), (co,), (co,)]
-        shapes += [(self.classes, 512), (self.classes,)]
+        shapes += [(self.classes, cin), (self.classes,)]
         assert len(shapes) == len(self.table), (len(shapes), len(self.table))
         return shapes
+
+    @property
+    def feat_dim(self) -> int:
+        return self.shapes[-2][1]
 
     @property
     def n_weights(self) -> int:
@@ -79,9 +98,10 @@ class ResnetLayout:
             a = np.asarray(t, dtype=np.float32).reshape(shp)
             if kind == KIND_CONV:
                 w = a.transpose(0, 2, 3, 1)  # OIHW -> OHWI (c fastest)
-                if shp[1] == 3:  # stem: [64][27] padded to [64][32]
-                    w2 = np.zeros((shp[0], STEM_K), dtype=np.float32)
-                    w2[:, :27] = w.reshape(shp[0], 27)
+                if shp[1] == 3:  # stem: [64][k*k*3] padded to [64][stem_k]
+                    kk = shp[2] * shp[3] * 3
+                    w2 = np.zeros((shp[0], self.stem_k), dtype=np.float32)
+                    w2[:, :kk] = w.reshape(shp[0], kk)
                     w = w2
                 flat[off:off + ln] = w.reshape(-1)
             else:
@@ -96,17 +116,17 @@ class ResnetLayout:
             v = flat[off:off + ln]
             if kind == KIND_CONV:
                 if shp[1] == 3:
-                    v = v.reshape(shp[0], STEM_K)[:, :27]
+                    v = v.reshape(shp[0], self.stem_k)[:, :shp[2] * shp[3] * 3]
                 out.append(v.reshape(shp[0], shp[2], shp[3], shp[1]).transpose(0, 3, 1, 2).copy())
             else:
                 out.append(v.reshape(shp).copy())
         return out
 
 
-def init_params(classes: int = 10, seed: int = 0) -> list:
+def init_params(classes: int = 10, seed: int = 0, depth: int = 18, image: int = 32) -> list:
     """Host initialisation in torchvision order (kaiming fan-out / BN 1, 0 / FC uniform)."""
     rng = np.random.default_rng(seed)
-    L = ResnetLayout(classes)
+    L = ResnetLayout(classes, depth, image)
     out = []
     for shp, (_, _, kind) in zip(L.shapes, L.table):
         if kind == KIND_CONV:
@@ -117,9 +137,25 @@ def init_params(classes: int = 10, seed: int = 0) -> list:
         elif kind == KIND_BN_B:
             out.append(np.zeros(shp, dtype=np.float32))
         else:
-            bound = 1.0 / math.sqrt(512)
+            bound = 1.0 / math.sqrt(L.feat_dim)
             out.append(rng.uniform(-bound, bound, shp).astype(np.float32))
     return out
+
+
+def synthetic_imagenet(n_samples=20000, image=224, classes=1000, seed=0, device=None):
+    """C5 inputs: uint8 [D][3][image][image] uniform pixels, labels integers(0, classes).
+    device=None: numpy arrays on the host; else torch tensors generated on that device."""
+    if device is None:
+        rng = np.random.default_rng(seed)
+        X = rng.integers(0, 256, size=(n_samples, 3, image, image), dtype=np.uint8)
+        y = rng.integers(0, classes, size=n_samples).astype(np.int32)
+        return X, y
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    X = torch.randint(0, 256, (n_samples, 3, image, image), generator=g, device=device, dtype=torch.uint8)
+    y = torch.randint(0, classes, (n_samples,), generator=g, device=device, dtype=torch.int32)
+    return X, y
 
 
 def synthetic_cifar(n_samples=50000, classes=10, seed=0):
@@ -133,13 +169,13 @@ def synthetic_cifar(n_samples=50000, classes=10, seed=0):
 class ResnetModel:
     """Device parameters (fp32 master, bf16 shadow, momentum) of one replica."""
 
-    def __init__(self, classes=10, seed=0, device=None, params=None):
+    def __init__(self, classes=10, seed=0, device=None, params=None, depth=18, image=32):
         import torch
 
         _lib.require_device()
-        self.layout = L = ResnetLayout(classes)
+        self.layout = L = ResnetLayout(classes, depth, image)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
-        tensors = init_params(classes, seed) if params is None else params
+        tensors = init_params(classes, seed, depth, image) if params is None else params
         self.params = torch.as_tensor(L.pack(tensors), device=self.device)
         self.params_bf16 = self.params.to(torch.bfloat16)
         self.velocity = torch.zeros_like(self.params)
@@ -155,9 +191,10 @@ class ResnetModel:
 class ResnetScratch:
     """Per-worker activation scratch (dbs_resnet) sized for the largest batch."""
 
-    def __init__(self, max_batch: int, classes: int = 10):
+    def __init__(self, max_batch: int, classes: int = 10, depth: int = 18, image: int = 32):
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().dbs_resnet_create(int(max_batch), classes, ctypes.byref(h)), "resnet_create")
+        _lib.check(_lib.lib().dbs_resnet_create_ex(depth, image, int(max_batch), classes, ctypes.byref(h)),
+                   "resnet_create")
         self.handle = h
         self.max_batch = int(max_batch)
 

@@ -112,8 +112,9 @@ class RunResult:
 class SimulatedTrainer:
     """W simulated workers of synchronous S-SGD on one GPU.
 
-    model = "mlp" (config 1: X fp32 [D][784]) or "resnet18" (configs 3/4:
-    X fp32 [D][3][32][32]).
+    model = "mlp" (config 1: X fp32 [D][784]), "resnet18" (configs 3/4:
+    X fp32 [D][3][32][32]) or "resnet50" (config 5: X uint8 [D][3][S][S],
+    S = 224 for ImageNet-shaped data).
     """
 
     def __init__(self, X, y, n_workers: int, model: str = "mlp", hidden: int = 256, classes: int = 10,
@@ -126,12 +127,18 @@ class SimulatedTrainer:
         self.dev = torch.device("cuda", torch.cuda.current_device())
         X = X if isinstance(X, torch.Tensor) else torch.as_tensor(X)
         y = y if isinstance(y, torch.Tensor) else torch.as_tensor(y)
-        self.X = X.to(self.dev, torch.float32).contiguous()
+        if model not in ("mlp", "resnet18", "resnet50"):
+            raise ConfigurationError(f"unknown model {model!r}")
+        x_dtype = torch.uint8 if model == "resnet50" else torch.float32
+        self.X = X.to(self.dev, x_dtype).contiguous()
         self.y = y.to(self.dev, torch.int32).contiguous()
         self.D = int(self.X.shape[0])
         self.row_elems = int(np.prod(self.X.shape[1:]))
+        self.row_bytes = self.row_elems * self.X.element_size()
         self.n = n_workers
+        self.classes = classes
         self.kind = MODEL_MLP if model == "mlp" else MODEL_RESNET18
+        self.depth, self.image = (50, int(self.X.shape[-1])) if model == "resnet50" else (18, 32)
         if self.kind == MODEL_MLP:
             from .mlp import MlpModel
 
@@ -139,8 +146,10 @@ class SimulatedTrainer:
         else:
             from .resnet import ResnetModel
 
-            assert tuple(self.X.shape[1:]) == (3, 32, 32), "resnet18 expects CIFAR-shaped [D][3][32][32] rows"
-            self.model = ResnetModel(classes, seed, self.dev, params=params)
+            S = self.image
+            if tuple(self.X.shape[1:]) != (3, S, S) or (model == "resnet18" and S != 32):
+                raise ConfigurationError(f"{model} expects [D][3][{S}][{S}] rows, got {tuple(self.X.shape)}")
+            self.model = ResnetModel(classes, seed, self.dev, params=params, depth=self.depth, image=S)
         self.workers = make_workers(n_workers, partition)
         partitioned = any(w.ctx for w in self.workers)
         # iteration graphs for ResNet (one context); partitioned workers launch eagerly
@@ -162,7 +171,7 @@ class SimulatedTrainer:
         self.agg = torch.cuda.Stream()
         self.rng = None
         # fixed-address shards (graph replays need stable pointers)
-        shard_dtype = torch.bfloat16 if self.kind == MODEL_MLP else torch.float32
+        shard_dtype = torch.bfloat16 if self.kind == MODEL_MLP else x_dtype
         self.shard_x = [torch.empty((self.D, self.row_elems), dtype=shard_dtype, device=self.dev) for _ in
                         range(n_workers)]
         self.shard_y = [torch.empty(self.D, dtype=torch.int32, device=self.dev) for _ in range(n_workers)]
@@ -182,7 +191,7 @@ class SimulatedTrainer:
             else:
                 from .resnet import ResnetScratch
 
-                cur = ResnetScratch(cap)
+                cur = ResnetScratch(cap, self.classes, self.depth, self.image)
             self.scratch[w] = cur
             self._graph_cache.clear()  # scratch pointers changed
         return cur
@@ -338,7 +347,7 @@ class SimulatedTrainer:
                                                                      self.row_elems, xs.data_ptr(), s_main)
                     else:
                         st = _lib.lib().dbs_dev_gather_rows(self.X.data_ptr(), idx.data_ptr(), rows,
-                                                            self.row_elems * 4, xs.data_ptr(), s_main)
+                                                            self.row_bytes, xs.data_ptr(), s_main)
                     _lib.check(st, "gather")
                     _lib.check(_lib.lib().dbs_dev_gather_i32(self.y.data_ptr(), idx.data_ptr(), rows, ys.data_ptr(),
                                                               s_main), "gather labels")
@@ -500,7 +509,8 @@ class DistributedTrainer(SimulatedTrainer):
     """
 
     def __init__(self, D_per_rank: int, workers_per_rank: int = 1, model: str = "resnet18", classes: int = 10,
-                 seed: int = 0, partition: Optional[bool] = None, max_batch: Optional[int] = None, group=None):
+                 seed: int = 0, partition: Optional[bool] = None, max_batch: Optional[int] = None, group=None,
+                 image: int = 224):
         import torch
         import torch.distributed as dist
 
@@ -513,6 +523,8 @@ class DistributedTrainer(SimulatedTrainer):
         g = torch.Generator(device=dev).manual_seed(seed + 1234)
         if model == "resnet18":
             X = torch.randn((D, 3, 32, 32), generator=g, device=dev)
+        elif model == "resnet50":
+            X = torch.randint(0, 256, (D, 3, image, image), generator=g, device=dev, dtype=torch.uint8)
         else:
             X = torch.randn((D, 784), generator=g, device=dev)
         y = torch.randint(0, classes, (D,), generator=g, device=dev, dtype=torch.int32)
@@ -576,7 +588,7 @@ class DistributedTrainer(SimulatedTrainer):
                                                                      self.row_elems, xs.data_ptr(), s_main)
                     else:
                         st = _lib.lib().dbs_dev_gather_rows(self.X.data_ptr(), idx.data_ptr(), rows,
-                                                            self.row_elems * 4, xs.data_ptr(), s_main)
+                                                            self.row_bytes, xs.data_ptr(), s_main)
                     _lib.check(st, "gather")
                     _lib.check(_lib.lib().dbs_dev_gather_i32(self.y.data_ptr(), idx.data_ptr(), rows, ys.data_ptr(),
                                                               s_main), "gather labels")
