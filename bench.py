@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--report", default=None,
                     help="directory for the reference-format run reports (epoch CSV per strategy + run JSON)")
-    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "mlp"])
+    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "resnet50", "mlp"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -125,14 +125,34 @@ WL = {
     "resnet18_ma": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0, avg=4,
                         desc="C4: C3 with periodic model averaging (local SGD on per-worker replicas, averaged every "
                              "step=4 iterations), DBS vs fixed plan, step = 1 epoch"),
+    "resnet50": dict(D=12800, workers=4, per_worker=64, lr=0.05, mom=0.9, mult=None, image=224, classes=1000,
+                     max_batch=160, cpu_per_worker=16,
+                     desc="C5: ResNet-50 (torchvision v1.5) on synthetic ImageNet-shaped 12800x3x224x224 uint8, 1000 "
+                          "classes, 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the B200, "
+                          "B=256 (64/worker fixed), step = 1 epoch (50 iterations)"),
     "mlp": dict(D=60000, workers=3, per_worker=128, lr=0.05, mom=0.5, mult=2.0,
                 desc="C1: MLP 784-256-10, synthetic MNIST 60000x784, 3 simulated workers, B=384, step = 1 epoch"),
 }
 
 
+def varying_multipliers(n_epochs=64, seed=2007):
+    """Per-epoch SM fractions f ~ U(0.25, 0.6) stolen from workers 0 and 1
+    (cost multiplier 1 / (1 - f)): persistent disturbed workers whose intensity
+    changes every epoch."""
+    rng = np.random.default_rng(seed)
+    f = rng.uniform(0.25, 0.6, size=(2, n_epochs))
+    return 1.0 / (1.0 - f)
+
+
 def profiles(n, mult):
     from paper_2007_11831_b200 import cluster
 
+    if mult is None:
+        m = varying_multipliers()
+        prof = [cluster.WorkerProfile(w, 1.0, disturbances=tuple(
+            cluster.DisturbanceEvent(e, e + 1, cost_multiplier=float(m[w, e])) for e in range(m.shape[1])))
+            for w in range(2)]
+        return prof + [cluster.WorkerProfile(i, 1.0) for i in range(2, n)]
     # a persistent slow worker (SURVEY.md A.6: rotating disturbances defeat the
     # one-epoch-lag estimator; persistent ones are what DBS absorbs)
     prof = [cluster.WorkerProfile(0, 1.0, disturbances=(cluster.DisturbanceEvent(0, cost_multiplier=mult),))]
@@ -151,8 +171,16 @@ def make_trainer(wl, rank, world=1):
         # one process per GPU: the same 4 SM-partition workers per GPU, the global
         # plan spans 4 x world workers, gradients meet in the fused NVLink kernel
         tr = DistributedTrainer(w["D"], workers_per_rank=w["workers"], model=wl, seed=0, partition=True,
-                                max_batch=3 * w["per_worker"])
+                                max_batch=w.get("max_batch", 3 * w["per_worker"]), classes=w.get("classes", 10),
+                                image=w.get("image", 224))
         return tr, (None, None)
+    if wl == "resnet50":
+        from paper_2007_11831_b200.resnet import synthetic_imagenet
+
+        X, y = synthetic_imagenet(w["D"], w["image"], w["classes"], seed=rank, device=torch.device("cuda"))
+        tr = SimulatedTrainer(X, y, n_workers=w["workers"], model="resnet50", classes=w["classes"], seed=0,
+                              partition=True, max_batch=w["max_batch"])
+        return tr, (X.cpu().numpy(), y.cpu().numpy())
     if wl.startswith("resnet18"):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
@@ -186,23 +214,35 @@ def run_strategy(tr, wl, kind, args, world=1):
             "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
-def kernel_roofline(peaks):
-    """Dominant kernel: the tcgen05 implicit-GEMM 3x3 convolution of the 64-channel
-    stage (the most frequent conv shape; 64->64 at 32x32, b=128 per worker:
-    M = 131072 pixels, N = 64, K = 576).  200 launches captured in a CUDA graph,
-    timed with CUDA events on the capturing stream."""
+ROOFLINE_CONV = {
+    # workload -> (N, H, Cin, Cout, k, stride, description): the dominant conv shape
+    "resnet18": (128, 32, 64, 64, 3, 1, "gemm_bf16_kernel<64> implicit-GEMM conv3x3 64->64 @32x32, b=128 "
+                                        "(M=131072, N=64, K=576)"),
+    "resnet50": (64, 14, 256, 256, 3, 1, "gemm_bf16_kernel<256> implicit-GEMM (im2col TMA) conv3x3 256->256 @14x14, "
+                                         "b=64 (M=12544, N=256, K=2304; layer 3 carries the most FLOPs)"),
+}
+
+
+def kernel_roofline(peaks, wl="resnet18"):
+    """Dominant kernel: the tcgen05 implicit-GEMM convolution of the workload's
+    most expensive conv shape (ResNet-18: the 64-channel 3x3 stage, 64->64 at
+    32x32, b=128 per worker; ResNet-50: the layer-3 3x3, 256->256 at 14x14, b=64).
+    200 launches captured in a CUDA graph, timed with CUDA events on the
+    capturing stream."""
     import torch
 
     from paper_2007_11831_b200 import _lib
 
-    N, H, C = 128, 32, 64
+    N, H, C, Co, k, stride, desc = ROOFLINE_CONV.get(wl, ROOFLINE_CONV["resnet18"])
+    pad = k // 2
+    OH = (H + 2 * pad - k) // stride + 1
     x = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
-    w = (torch.randn(C, 3, 3, C, device="cuda") / 24).to(torch.bfloat16)
-    y = torch.empty(N, H, H, C, dtype=torch.bfloat16, device="cuda")
+    w = (torch.randn(Co, k, k, C, device="cuda") / (k * k * C) ** 0.5).to(torch.bfloat16)
+    y = torch.empty(N, OH, OH, Co, dtype=torch.bfloat16, device="cuda")
     L = _lib.lib()
 
     def launch(s):
-        st = L.dbs_dev_conv2d_fwd(x.data_ptr(), N, H, H, C, w.data_ptr(), C, 3, 1, 1, y.data_ptr(), s)
+        st = L.dbs_dev_conv2d_fwd(x.data_ptr(), N, H, H, C, w.data_ptr(), Co, k, stride, pad, y.data_ptr(), s)
         assert st == 0, _lib.last_error()
 
     for _ in range(10):
@@ -222,14 +262,24 @@ def kernel_roofline(peaks):
         e1.record(cs)
     torch.cuda.synchronize()
     dur = e0.elapsed_time(e1) / 1e3 / 200
-    flops = 2.0 * N * H * H * C * 9 * C
+    flops = 2.0 * N * OH * OH * Co * k * k * C
     achieved = flops / dur / 1e12
     peak = peaks["bf16_tflops"]
-    return {"bound": "tensor", "kernel": "gemm_bf16_kernel<64> implicit-GEMM conv3x3 64->64 @32x32, b=128 "
-                                         "(M=131072, N=64, K=576)",
+    return {"bound": "tensor", "kernel": desc,
             "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "traffic": None, "avg_launch_us": round(dur * 1e6, 2), "algorithmic_flops_per_launch": flops,
             "peak_source": peaks["source"]}
+
+
+def disturbance_desc(wl):
+    w = WL[wl]
+    if w["mult"] is None:
+        return ("workers 0 and 1: co-running spin kernels pin a fraction f ~ U(0.25, 0.6) of their SM partitions, "
+                "redrawn every epoch (seeded; cost_multiplier 1/(1-f))")
+    if wl.startswith("resnet"):
+        return (f"worker 0: a co-running spin kernel pins {1 - 1 / w['mult']:.0%} of its SM partition for every "
+                f"epoch (cost_multiplier {w['mult']})")
+    return f"worker 0 on a {w['mult']}x slower device (proportional spin)"
 
 
 def cpu_baseline(wl, X, y, threads=None):
@@ -238,13 +288,15 @@ def cpu_baseline(wl, X, y, threads=None):
     from oracle import oracle as O
 
     w = WL[wl]
-    batches = [w["per_worker"]] * w["workers"]
-    if wl.startswith("resnet18"):
+    batches = [w.get("cpu_per_worker", w["per_worker"])] * w["workers"]
+    if wl.startswith("resnet"):
         from paper_2007_11831_b200.resnet import init_params
 
-        tens = init_params(seed=0)
-        sec = O.cpu_resnet_iteration_seconds(tens, X[:sum(batches)], y[:sum(batches)], batches, threads=threads)
-        sample = (f"1 iteration x {w['workers']} workers x {w['per_worker']} samples, ResNet-18 fwd+bwd on "
+        depth = 50 if wl == "resnet50" else 18
+        tens = (init_params(w["classes"], 0, depth=50, image=w["image"]) if depth == 50 else init_params(seed=0))
+        sec = O.cpu_resnet_iteration_seconds(tens, X[:sum(batches)], y[:sum(batches)], batches, threads=threads,
+                                             depth=depth)
+        sample = (f"1 iteration x {w['workers']} workers x {batches[0]} samples, ResNet-{depth} fwd+bwd on "
                   "PyTorch-CPU inside the restated run_parallel_sgd loop (fp32)")
     else:
         prob = O.MlpProblem(X, y)
@@ -301,6 +353,10 @@ def reference_arm(args):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
         X, y = synthetic_cifar(w["workers"] * w["per_worker"], seed=0)
+    elif wl == "resnet50":
+        from paper_2007_11831_b200.resnet import synthetic_imagenet
+
+        X, y = synthetic_imagenet(w["workers"] * w["cpu_per_worker"], w["image"], w["classes"], seed=0)
     else:
         from paper_2007_11831_b200.mlp import synthetic_mnist
 
@@ -309,7 +365,7 @@ def reference_arm(args):
     base = vals[-1]
     out = {"impl": "reference", "metric": METRIC, "value": round(base["value"], 2), "unit": "samples/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-           "dtype": "f32" if wl.startswith("resnet18") else "f64", "data": "synthetic",
+           "dtype": "f32" if wl.startswith("resnet") else "f64", "data": "synthetic",
            "config": {"workload": w["desc"]}, "cpu_baseline": base,
            "e2e": {"value": round(base["value"], 2), "unit": "samples/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
@@ -349,7 +405,7 @@ def main():
         for r in reps:
             rpt.write_epoch_csv(r, out / f"{r.scenario_name}_{r.strategy}.csv")
         rpt.write_run_json(reps, [], out / f"bench_{wl}_n{world}.json")
-    roof = kernel_roofline(peaks)
+    roof = kernel_roofline(peaks, wl)
     e2e = None if (args.no_e2e or world > 1) else e2e_run(tr, wl, X, y, args)
     cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl, X, y)
     gaps = [np.mean(s.per_worker_wait) / max(s.per_worker_gpu) for s in fixed["stats"]]
@@ -367,10 +423,9 @@ def main():
         "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": w["desc"],
-                   "disturbance": (f"worker 0: a co-running spin kernel pins {1 - 1 / w['mult']:.0%} of its SM "
-                                   f"partition for every epoch (cost_multiplier {w['mult']})" if wl.startswith("resnet18") else
-                                   f"worker 0 on a {w['mult']}x slower device (proportional spin)"),
-                   "l2": "inputs > L2: 614 MB dataset repacked into per-worker shards every epoch",
+                   "disturbance": disturbance_desc(wl),
+                   "l2": (f"inputs > L2: {tr.X.numel() * tr.X.element_size() / 1e6:.0f} MB dataset repacked into "
+                          "per-worker shards every epoch"),
                    "lr": w["lr"], "momentum": w["mom"], "parallelism": f"{w['workers']} simulated DP workers/GPU"},
         "fixed": {"samples_per_s": round(fixed["samples_per_s"], 1), "ms_per_epoch": round(fixed["epoch_s"] * 1e3, 3)},
         "dbs_vs_fixed_speedup": round(dbs["samples_per_s"] / fixed["samples_per_s"], 4),

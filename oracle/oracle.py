@@ -556,8 +556,43 @@ def torch_cpu_resnet18(tensors):
     return forward, params
 
 
-def cpu_resnet_iteration_seconds(tensors, X, y, batches, lr=0.05, momentum=0.9, threads=None):
-    """One synchronous iteration (sgdlab.py:380-391) with CPU ResNet-18 workers:
+def torch_cpu_resnet50(tensors):
+    """Functional ResNet-50 (torchvision v1.5 topology) on the CPU; uint8 input
+    rows are mapped to (u - 128) / 64 as on the device."""
+    import torch
+    import torch.nn.functional as F
+
+    params = [torch.as_tensor(np.asarray(t), dtype=torch.float32).requires_grad_(True) for t in tensors]
+
+    def forward(x):
+        it = iter(params)
+        if x.dtype == torch.uint8:
+            x = (x.float() - 128.0) / 64.0
+
+        def conv_bn(h, stride, pad, relu=True):
+            w, g, b = next(it), next(it), next(it)
+            y = F.batch_norm(F.conv2d(h, w, stride=stride, padding=pad), None, None, g, b, training=True, eps=1e-5)
+            return F.relu(y) if relu else y
+
+        h = F.max_pool2d(conv_bn(x, 2, 3), 3, 2, 1)
+        cin = 64
+        for L, (wdt, n) in enumerate(zip((64, 128, 256, 512), (3, 4, 6, 3))):
+            for blk in range(n):
+                stride = 2 if (L > 0 and blk == 0) else 1
+                a = conv_bn(h, 1, 0)
+                a = conv_bn(a, stride, 1)
+                a = conv_bn(a, 1, 0, relu=False)
+                sc = conv_bn(h, stride, 0, relu=False) if (stride != 1 or cin != 4 * wdt) else h
+                h = F.relu(a + sc)
+                cin = 4 * wdt
+        wf, bf = next(it), next(it)
+        return h.mean(dim=(2, 3)) @ wf.t() + bf
+
+    return forward, params
+
+
+def cpu_resnet_iteration_seconds(tensors, X, y, batches, lr=0.05, momentum=0.9, threads=None, depth=18):
+    """One synchronous iteration (sgdlab.py:380-391) with CPU ResNet-18/50 workers:
     per-worker batch-mean gradient, batch-weighted aggregation, heavy-ball step."""
     import time
 
@@ -566,7 +601,7 @@ def cpu_resnet_iteration_seconds(tensors, X, y, batches, lr=0.05, momentum=0.9, 
 
     if threads:
         torch.set_num_threads(threads)
-    forward, params = torch_cpu_resnet18(tensors)
+    forward, params = (torch_cpu_resnet50 if depth == 50 else torch_cpu_resnet18)(tensors)
     vel = [torch.zeros_like(p) for p in params]
     t0 = time.perf_counter()
     grads = []
