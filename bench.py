@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--report", default=None,
                     help="directory for the reference-format run reports (epoch CSV per strategy + run JSON)")
-    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "resnet50", "mlp"])
+    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "resnet50", "mlp", "allreduce"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -265,10 +265,91 @@ def kernel_roofline(peaks, wl="resnet18"):
     flops = 2.0 * N * OH * OH * Co * k * k * C
     achieved = flops / dur / 1e12
     peak = peaks["bf16_tflops"]
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic_r1.json"
+    if tf.exists():
+        rec = json.loads(tf.read_text()).get(wl if wl in ROOFLINE_CONV else "resnet18")
+        if rec:
+            traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
     return {"bound": "tensor", "kernel": desc,
             "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-            "traffic": None, "avg_launch_us": round(dur * 1e6, 2), "algorithmic_flops_per_launch": flops,
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu, profiles/ncu_traffic_r1.json)",
+            "algorithmic_bytes_per_launch": 2.0 * (N * H * H * C + N * OH * OH * Co + Co * k * k * C),
+            "avg_launch_us": round(dur * 1e6, 2), "algorithmic_flops_per_launch": flops,
             "peak_source": peaks["source"]}
+
+
+def _graph_time(launch, reps=20):
+    """Mean device time of `launch(stream)` over `reps` launches captured in a CUDA
+    graph (CUDA events on the capturing stream)."""
+    import torch
+
+    from paper_2007_11831_b200 import _lib
+
+    for _ in range(3):
+        launch(_lib.stream_handle())
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cs):
+        for _ in range(reps):
+            launch(int(cs.cuda_stream))
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cs):
+        e0.record(cs)
+        g.replay()
+        e1.record(cs)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def aux_rooflines(tr, peaks):
+    """HBM rooflines of the two other hot-path kernels, on the workload's own
+    buffers: the repartition gather (gather.cu; 2 * row_bytes + 8 B per row:
+    every dataset row to a shard in a random order) and the fused batch-weighted
+    aggregate + momentum SGD of the simulated workers (sgd.cu; (4n + 4 * 4 + 2) B
+    per parameter: n gradients, x and v read, x, v and the bf16 shadow written)."""
+    import ctypes
+
+    import torch
+
+    from paper_2007_11831_b200 import _lib
+
+    L = _lib.lib()
+    out = {}
+    D, rb = tr.D, tr.row_bytes
+    perm = torch.randperm(D, device=tr.dev)
+    dst = tr.shard_x[0]
+
+    def gather(st):
+        assert L.dbs_dev_gather_rows(tr.X.data_ptr(), perm.data_ptr(), D, rb, dst.data_ptr(), st) == 0, _lib.last_error()
+
+    t = _graph_time(gather, 10)
+    byt = 2.0 * D * rb + 8.0 * D
+    out["repartition_gather"] = {"bound": "hbm", "achieved": round(byt / t / 1e9, 1), "peak": peaks["hbm_gbs"],
+                                 "unit": "GB/s", "frac": round(byt / t / 1e9 / peaks["hbm_gbs"], 4),
+                                 "bytes_per_launch": byt, "avg_launch_us": round(t * 1e6, 2),
+                                 "launch": f"{D} rows x {rb} B, random permutation"}
+    n, P = tr.n, tr.model.P
+    ptrs = (ctypes.c_void_p * n)(*[g.data_ptr() for g in tr.grads])
+    b = np.asarray([37 + 36 * (i % 2) for i in range(n)], dtype=np.int64)
+    x = tr.model.params.clone()
+    v = torch.zeros_like(x)
+    xb = tr.model.params_bf16.clone()
+
+    def agg(st):
+        assert L.dbs_dev_aggregate_sgd_f32(ptrs, b.ctypes.data_as(_lib.P_i64), n, 1, P, 0.0, 0.9, x.data_ptr(),
+                                           v.data_ptr(), xb.data_ptr(), st) == 0, _lib.last_error()
+
+    t = _graph_time(agg, 20)
+    byt = (4.0 * n + 16.0 + 2.0) * P
+    out["aggregate_sgd"] = {"bound": "hbm", "achieved": round(byt / t / 1e9, 1), "peak": peaks["hbm_gbs"],
+                            "unit": "GB/s", "frac": round(byt / t / 1e9 / peaks["hbm_gbs"], 4),
+                            "bytes_per_launch": byt, "avg_launch_us": round(t * 1e6, 2),
+                            "launch": f"{n} worker gradients x {P} fp32 parameters"}
+    return out
 
 
 def disturbance_desc(wl):
@@ -343,11 +424,43 @@ def e2e_run(tr, wl, X, y, args):
             "note": "DBS epochs with the dataset re-uploaded from pinned host memory each epoch (H2D in the timed region)"}
 
 
+def reference_arm_allreduce(args, world):
+    """Reference arm of C2: aggregate_gradients(batch_weighted) + sgd_step
+    (sgdlab.py:208-238) restated in C (oracle/dbs_oracle.c, fp64 like the
+    reference), W rank gradients of a bounded 16 MiB-equivalent size."""
+    from oracle import oracle as O
+
+    n = max(world, 1)
+    P = 16 * (1 << 20) // 4
+    rng = np.random.default_rng(0)
+    grads = [rng.standard_normal(P) for _ in range(n)]
+    x, v = rng.standard_normal(P), np.zeros(P)
+    b = [C2_BATCHES[r % len(C2_BATCHES)] for r in range(n)]
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        g = O.aggregate(grads, b, 1)
+        x, v = O.sgd_step(x, g, v, 0.05, 0.9)
+        ts.append(time.perf_counter() - t0)
+    t = min(ts)
+    val = round(22.0 * P / t / 1e9, 3)
+    out = {"impl": "reference", "metric": "batch-weighted aggregate + momentum SGD, GB/s (22 B per parameter)",
+           "value": val, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"C2 reference: {n} rank gradients x 16 MiB-equivalent on the host"},
+           "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "port",
+                            "sample": f"aggregate_gradients + sgd_step over {n} x {P} fp64 (C restatement)"},
+           "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
 def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     wl = args.workload
+    if wl == "allreduce":
+        return reference_arm_allreduce(args, world)
     w = WL[wl]
     if wl.startswith("resnet18"):
         from paper_2007_11831_b200.resnet import synthetic_cifar
@@ -372,8 +485,103 @@ def reference_arm(args):
     print(json.dumps(out), flush=True)
 
 
+C2_BATCHES = [37, 37, 73, 73, 73, 73, 73, 73]  # a DBS plan of 8 ranks, sum 512
+C2_SIZES_MIB = [1, 4, 16, 64, 256, 1024]
+
+
+def run_allreduce(args):
+    """C2: the fused batch-weighted all-reduce + momentum SGD (comm.cu) swept over
+    1 MiB .. 1 GiB of fp32 gradient per rank with unequal batch weights.  One
+    launch per step; CUDA events on the launching stream, max over ranks.
+    Bytes per rank and direction over NVLink: 4P(W-1)/W of gradient shards
+    pulled + 6P(W-1)/W of updated parameters (fp32 + bf16 shadow) pushed, i.e.
+    10P(W-1)/W; busbw is NCCL's all-reduce convention 2(W-1)/W * 4P / t.  At
+    W = 1 there is no exchange: the kernel is the HBM-bound local update
+    (22 B per parameter: read g, x, v; write x, v and the bf16 shadow)."""
+    import torch
+
+    from paper_2007_11831_b200.comm import Communicator, max_over_ranks
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local if world > 1 else 0)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29517", rank=0, world_size=1)
+    peaks = load_peaks()
+    b = [C2_BATCHES[r % len(C2_BATCHES)] for r in range(world)]
+    rows = []
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    for mib in C2_SIZES_MIB:
+        P = mib * (1 << 20) // 4
+        comm = Communicator.create(P, group) if world > 1 else Communicator.local(1, P)[0]
+        g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        comm.grad.copy_(torch.randn(comm.P, generator=g, device="cuda"))
+        comm.params.copy_(torch.randn(comm.P, generator=g, device="cuda"))
+        s = torch.cuda.current_stream()
+        for _ in range(args.warmup):
+            comm.allreduce_sgd(b, 0.05, 0.9, stream=s)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(args.steps):
+            comm.allreduce_sgd(b, 0.05, 0.9, stream=s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / args.steps
+        if world > 1:
+            t = max_over_ranks(t)
+        Pp = comm.P
+        row = {"MiB": mib, "us": round(t * 1e6, 2)}
+        if world > 1:
+            nv = 10.0 * Pp * (world - 1) / world
+            row.update({"busbw_GBps": round(2.0 * (world - 1) / world * 4 * Pp / t / 1e9, 1),
+                        "nvlink_GBps_per_dir": round(nv / t / 1e9, 1),
+                        "nvlink_frac_of_770": round(nv / t / 1e9 / 770.0, 3)})
+        else:
+            row.update({"hbm_GBps": round(22.0 * Pp / t / 1e9, 1),
+                        "hbm_frac": round(22.0 * Pp / t / 1e9 / peaks["hbm_gbs"], 3)})
+        rows.append(row)
+        comm.close()
+        del comm
+        torch.cuda.empty_cache()
+    clocks = sampler.stop()
+    top = rows[-1]
+    out = {
+        "metric": "batch-weighted all-reduce + momentum SGD (fused NVLink kernel), bus bandwidth at 1 GiB"
+                  if world > 1 else "batch-weighted aggregate + momentum SGD (W=1: local update), HBM GB/s at 1 GiB",
+        "value": top["busbw_GBps"] if world > 1 else top["hbm_GBps"], "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(top["us"] / 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: fused batch-weighted all-reduce + SGD sweep 1 MiB-1 GiB fp32 per rank, "
+                               f"batch weights {b}, lr 0.05, momentum 0.9",
+                   "l2": "1 GiB gradient + parameters per rank exceed L2"},
+        "sweep": rows,
+        "roofline": ({"bound": "nvlink", "achieved": top["nvlink_GBps_per_dir"], "peak": 770.0, "unit": "GB/s",
+                      "frac": top["nvlink_frac_of_770"], "traffic": None,
+                      "peak_source": "B200_PROFILING.md measured peer copy per direction"} if world > 1 else
+                     {"bound": "hbm", "achieved": top["hbm_GBps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                      "frac": top["hbm_frac"], "traffic": None, "peak_source": peaks["source"]}),
+        "e2e": None, "cpu_baseline": None, "clocks": clocks,
+        "gpu_launches": (args.warmup + args.steps) * len(C2_SIZES_MIB),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.workload == "allreduce" and args.impl != "reference":
+        return run_allreduce(args)
     if args.impl == "reference":
         return reference_arm(args)
     rank, world, local = dist_env()
@@ -406,6 +614,7 @@ def main():
             rpt.write_epoch_csv(r, out / f"{r.scenario_name}_{r.strategy}.csv")
         rpt.write_run_json(reps, [], out / f"bench_{wl}_n{world}.json")
     roof = kernel_roofline(peaks, wl)
+    aux = aux_rooflines(tr, peaks) if world == 1 else None
     e2e = None if (args.no_e2e or world > 1) else e2e_run(tr, wl, X, y, args)
     cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl, X, y)
     gaps = [np.mean(s.per_worker_wait) / max(s.per_worker_gpu) for s in fixed["stats"]]
@@ -434,6 +643,7 @@ def main():
         "per_worker_gpu_s_last_epoch": {"fixed": [round(v, 4) for v in fixed["stats"][-1].per_worker_gpu],
                                         "dbs": [round(v, 4) for v in dbs["stats"][-1].per_worker_gpu]},
         "roofline": roof,
+        "kernel_rooflines": aux,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": dbs["clocks"],

@@ -83,6 +83,13 @@ struct GemmParams {
   OutMap omap;          // strided output rows (on = 0: row-major)
 };
 
+// two floats -> packed bf16x2 (lo in bits 0..15), one round-to-nearest-even
+// conversion instruction (F2FP) instead of integer rounding per element
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 __device__ __forceinline__ uint16_t f2bf(float f) {
   uint32_t u = __float_as_uint(f);
   return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
@@ -218,10 +225,10 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
 #pragma unroll
     for (int j = 0; j < 32; j += 8) {
       uint4 q;
-      q.x = f2bf(x[j + 0]) | ((uint32_t)f2bf(x[j + 1]) << 16);
-      q.y = f2bf(x[j + 2]) | ((uint32_t)f2bf(x[j + 3]) << 16);
-      q.z = f2bf(x[j + 4]) | ((uint32_t)f2bf(x[j + 5]) << 16);
-      q.w = f2bf(x[j + 6]) | ((uint32_t)f2bf(x[j + 7]) << 16);
+      q.x = pack_bf16x2(x[j + 0], x[j + 1]);
+      q.y = pack_bf16x2(x[j + 2], x[j + 3]);
+      q.z = pack_bf16x2(x[j + 4], x[j + 5]);
+      q.w = pack_bf16x2(x[j + 6], x[j + 7]);
       *reinterpret_cast<uint4*>(d + j) = q;
     }
   }
@@ -715,19 +722,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           // memory: 32 stores + 32 loads instead of 160 shuffles) -> tile sums
           // over the 4 epilogue warps -> one fp64 atomic per column and tile
           __shared__ float red_s[4][32], red_q[4][32];
+          // one transpose: lane j reads column j and forms both sums
 #pragma unroll
           for (int k = 0; k < 32; k++) tr[lane * 33 + k] = v[k];
           __syncwarp();
-          float s = 0.f;
+          float s = 0.f, sq = 0.f;
 #pragma unroll
-          for (int r2 = 0; r2 < 32; r2++) s += tr[r2 * 33 + lane];
-          __syncwarp();
-#pragma unroll
-          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = v[k] * v[k];
-          __syncwarp();
-          float sq = 0.f;
-#pragma unroll
-          for (int r2 = 0; r2 < 32; r2++) sq += tr[r2 * 33 + lane];
+          for (int r2 = 0; r2 < 32; r2++) {
+            const float e = tr[r2 * 33 + lane];
+            s += e;
+            sq = fmaf(e, e, sq);
+          }
           __syncwarp();
           red_s[q][lane] = s;
           red_q[q][lane] = sq;
