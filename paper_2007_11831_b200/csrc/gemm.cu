@@ -81,6 +81,9 @@ struct GemmParams {
   int splits;           // split-K slices (atomic epilogue when > 1)
   ConvTaps taps;        // explicit conv taps of A (n = 0: R x S window)
   OutMap omap;          // strided output rows (on = 0: row-major)
+  int halo_rows;        // halo variant: image rows per TMA box
+  int halo_tpi;         // halo variant: tiles per image (ceil(OH (OW + 1) / 128))
+  int64_t halo_tiles;   // halo variant: images x tiles per image
 };
 
 // two floats -> packed bf16x2 (lo in bits 0..15), one round-to-nearest-even
@@ -112,21 +115,22 @@ struct Cfg {
 
 // Halo variant (3x3 stride-1 conv with 64 input channels, 64 output columns):
 // the 9 filter taps stay resident in shared memory for the CTA's lifetime and
-// each output tile of TR = 128 / W whole rows streams only three column-shifted
-// copies of its (TR + 2)-row input halo -- 3 x 24 KB instead of 9 x (16 + 8) KB
-// per tile, so the L2 -> SM traffic drops ~3x; tap (r, s) is the copy for s
-// viewed from row r * W (a 1 KB-aligned start in the 128-byte swizzle).
-// Each copy is ONE 2-D TMA box over the [pixels][64] view of the activation
-// (measured: a 2-D box costs the TMA unit ~300 cycles, a 4-D box ~560, nearly
-// independent of size -- scripts/tma_bench.cu); the rows that view gets wrong
-// (the column wrap-around of the shifted copies, the zero-padding rows above /
-// below the image) are zeroed in shared memory by a fix-up warp before the
-// MMA warp may read the slot.
+// each output tile streams its input halo ONCE, as one 4-D TMA box of
+// `halo_rows` image rows x (W + 1) pixels starting at column -1: the extra
+// column is TMA zero fill and serves as the left padding of every row and the
+// right padding of the row before it.  Output tiles enumerate the same padded
+// positions P = h (W + 1) + w of one image (128 per tile, crossing rows;
+// w = W is a junk position the epilogue drops, 1 / (W + 1) of the MMA work),
+// so tap (r, s) is the slot viewed from row (P0 mod (W + 1)) + r (W + 1) + s:
+// a 128-byte-row shift of a swizzled tile is a plain descriptor start-address
+// offset (the swizzle phase follows the absolute address bits -- verified by
+// scripts/shift_test.cu).  Per tile ~(128 + 3 (W + 1)) x 128 B of L2 -> SMEM
+// traffic instead of 9 x (16 + 8) KB for the plain implicit GEMM.
 struct HaloCfg {
-  static constexpr uint32_t kSlotBytes = 24 * 1024;  // (TR + 2) * W rows of 128 B, W <= 32
+  static constexpr uint32_t kSlotBytes = 44 * 1024;  // halo_rows x (W + 1) pixel rows of 128 B
   static constexpr uint32_t kTapBytes = 64 * 128;    // one 64 x 64 bf16 filter tap
   static constexpr uint32_t kBResBytes = 9 * kTapBytes;
-  static constexpr int kStages = 5;
+  static constexpr int kStages = 3;
   static constexpr uint32_t kAccCols = 64;
   static constexpr uint32_t kTmemCols = 128;
   static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) GEMM_TRACE(0);
   const int64_t m_tiles = (p.M + kBM - 1) / kBM;
   const int64_t n_tiles = (p.N + BN - 1) / BN;
-  const int64_t num_tiles = m_tiles * n_tiles * p.splits;
+  const int64_t num_tiles = kHalo ? p.halo_tiles : m_tiles * n_tiles * p.splits;
   const int num_k_total = (int)((p.K + kBK - 1) / kBK);
   const int a_mn = (p.a_mode == 1) ? 1 : 0;
   const int b_mn = (p.b_mode >= 1) ? 1 : 0;
@@ -443,18 +447,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     const ConvGeom& g = p.ga;
-    const uint32_t halo_bytes = (uint32_t)(kBM + 2 * g.OW) * 128u;
-    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    const int W1 = g.OW + 1;
+    const uint32_t halo_bytes = (uint32_t)(p.halo_rows * W1) * 128u;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, it++) {
       if (pt < 10) GEMM_TRACE(2 + pt);
       pt++;
-      // first halo pixel: one row above the tile, shifted by sx - 1 columns
-      const int32_t row0 = (int32_t)(t * kBM) - g.OW - 1;
-      for (int sx = 0; sx < 3; sx++, it++) {
-        const int s = (int)(it % kStages);
-        mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[s], halo_bytes);
-        tma_load_2d(sA + s * kSlotA, &tmA, &full[s], 0, row0 + sx);
-      }
+      const int img = (int)(t / p.halo_tpi);
+      const int P0 = (int)(t - (int64_t)img * p.halo_tpi) * kBM;
+      const int s = (int)(it % kStages);
+      mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], halo_bytes);
+      // rows from one above the tile's first row, columns from -1 (zero fill)
+      tma_load_4d(sA + s * kSlotA, &tmA, &full[s], 0, -1, P0 / W1 - 1, img);
     }
    } else {
    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -566,33 +570,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       // descriptors by arithmetic on the 16-byte address field (no per-MMA
       // re-encoding: the MMA thread's issue rate, not the tensor pipe, was the limit)
-      const uint32_t row16 = (uint32_t)p.ga.OW * 8u;  // one input row of the halo, in 16 B units
+      const int W1 = p.ga.OW + 1;
       const uint64_t a_desc0 = make_sdesc(smem_u32(sA), 16, 1024);
       const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 1024) : make_sdesc(smem_u32(sB), 16, 1024);
       const uint32_t b_kstep = b_mn ? 128u : 2u;
-      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, it++) {
         const int b = (int)(j & 1);
         mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         GEMM_TRACE(12 + j);
         const uint32_t d_tmem = tmem_base + b * kAccCols;
-        for (int sx = 0; sx < 3; sx++, it++) {
-          const int s = (int)(it % kStages);
-          mbar_wait(&ready[s], (it / kStages) & 1);
-          if (j < 8) GEMM_TRACE(96 + 3 * j + sx);
-          tc_fence_after();
-          const uint64_t a_slot = a_desc0 + (uint64_t)((s * kSlotA) >> 4);
+        const int s = (int)(it % kStages);
+        mbar_wait(&full[s], (it / kStages) & 1);
+        if (j < 8) GEMM_TRACE(96 + 3 * j);
+        tc_fence_after();
+        const int img = (int)(t / p.halo_tpi);
+        const int off = ((int)(t - (int64_t)img * p.halo_tpi) * kBM) % W1;
+        const uint64_t a_slot = a_desc0 + (uint64_t)((s * kSlotA) >> 4);
 #pragma unroll
-          for (int r = 0; r < 3; r++) {
-            const uint64_t a_r = a_slot + (uint64_t)(r * row16);
-            const uint64_t b_r = b_desc0 + (uint64_t)((r * 3 + sx) * (H::kTapBytes >> 4));
+        for (int r = 0; r < 3; r++) {
+#pragma unroll
+          for (int sx = 0; sx < 3; sx++) {
+            const uint64_t a_t = a_slot + (uint64_t)((off + r * W1 + sx) * 8);  // 128-byte rows
+            const uint64_t b_t = b_desc0 + (uint64_t)((r * 3 + sx) * (H::kTapBytes >> 4));
 #pragma unroll
             for (int k = 0; k < kBK / 16; k++)
-              mma_bf16_ss(d_tmem, a_r + (uint64_t)(k * 2), b_r + (uint64_t)(k * b_kstep), idesc,
-                          (sx | r | k) != 0 ? 1u : 0u);
+              mma_bf16_ss(d_tmem, a_t + (uint64_t)(k * 2), b_t + (uint64_t)(k * b_kstep), idesc,
+                          (r | sx | k) != 0 ? 1u : 0u);
           }
-          mma_commit(&empty[s]);
         }
+        mma_commit(&empty[s]);
         mma_commit(&acc_full[b]);
         GEMM_TRACE(22 + j);
         j++;
@@ -631,53 +638,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 6) {
-    // ---------------- halo fix-up (halo variant only) ----------------
-    if constexpr (kHalo) {
-      const ConvGeom& g = p.ga;
-      const int W = g.OW, TR = kBM / g.OW, HW = g.OH * g.OW;
-      uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int h0 = (int)((t * kBM) % HW) / W;
-        const bool top = (h0 == 0), bottom = (h0 + TR == g.OH);
-        for (int sx = 0; sx < 3; sx++, it++) {
-          const int s = (int)(it % kStages);
-          mbar_wait(&full[s], (it / kStages) & 1);
-          uint8_t* slot = sA + s * kSlotA;
-          // row j = hh * W + w of the copy is padding when hh is the row above /
-          // below the image, or when the shifted column w + sx - 1 leaves [0, W);
-          // each lane zeroes 16-byte chunks (a row is 8 chunks, swizzle-agnostic)
-          const uint4 z = make_uint4(0, 0, 0, 0);
-          if (sx != 1) {
-            const int w = (sx == 0) ? 0 : W - 1;
-            for (int k = lane; k < (TR + 2) * 8; k += 32)
-              *reinterpret_cast<uint4*>(slot + ((k >> 3) * W + w) * 128 + (k & 7) * 16) = z;
-          }
-          if (top)
-            for (int k = lane; k < W * 8; k += 32) *reinterpret_cast<uint4*>(slot + k * 16) = z;
-          if (bottom)
-            for (int k = lane; k < W * 8; k += 32) *reinterpret_cast<uint4*>(slot + (TR + 1) * W * 128 + k * 16) = z;
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ready[s]);
-        }
-      }
-    }
+    // (idle: the padded halo needs no shared-memory fix-up)
   } else {
   // ---------------- epilogue (warps 2..5) ----------------
   const int q = warp & 3;  // the TMEM lane quadrant this warp may access
   float* tr = sEpi + (warp - 2) * (32 * 33);
   uint32_t tj = 0;
   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-    int64_t m0, n0;
+    int64_t m0 = 0, n0 = 0;
     int kb_begin;
-    if (decode(t, m0, n0, kb_begin) == 0) continue;
+    if (!kHalo && decode(t, m0, n0, kb_begin) == 0) continue;
     const int b = (int)(tj & 1);
     mbar_wait(&acc_full[b], (tj >> 1) & 1);
     if (warp == 2 && lane == 0) GEMM_TRACE(32 + tj);
     tc_fence_after();
-    const int64_t row = m0 + q * 32 + lane;
+    int64_t row = m0 + q * 32 + lane;
     int64_t orow = row;  // the output row this thread writes
-    if (p.omap.on && row < p.M) {
+    bool valid = row < p.M;
+    if (kHalo) {
+      // padded position P = h (W + 1) + w of image img; w = W is junk
+      const int W1 = p.ga.OW + 1;
+      const int img = (int)(t / p.halo_tpi);
+      const int P = (int)(t - (int64_t)img * p.halo_tpi) * kBM + q * 32 + lane;
+      const int h = P / W1, w = P - (P / W1) * W1;
+      valid = (w < p.ga.OW) && (h < p.ga.OH);
+      orow = ((int64_t)img * p.ga.OH + h) * p.ga.OW + w;
+      row = orow;
+    } else if (p.omap.on && row < p.M) {
       const int64_t hw = (int64_t)p.omap.OH * p.omap.OW;
       const int64_t img = row / hw;
       const int rem = (int)(row - img * hw);
@@ -705,11 +692,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32], vo[32];
 #pragma unroll
         for (int k = 0; k < 32; k++) {
-          v[k] = (row < p.M) ? __uint_as_float(r[k]) : 0.0f;
+          v[k] = valid ? __uint_as_float(r[k]) : 0.0f;
           vo[k] = 0.0f;
         }
         const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
-        if (row < p.M) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
+        if (valid) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
         if (warp == 2 && lane == 0 && tj < 8) GEMM_TRACE(64 + 4 * tj + 2 * c + 1);
         if (p.colsum_part != nullptr) {
           const int64_t g = (m0 >> 5) + q;
@@ -947,7 +934,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   GemmParams q = p;
   q.splits = splits;
   // persistent: one CTA per SM of the current (possibly green) context
-  const int64_t tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
+  const int64_t tiles = kHalo ? p.halo_tiles : ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
   const int64_t sms = current_sm_count();
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   gemm_bf16_kernel<BN, kHalo><<<grid, kThreads, kSmem, s>>>(ta, tb, q);
@@ -974,6 +961,12 @@ int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, 
 }
 
 }  // namespace
+
+bool halo_fits(int OH, int OW) {
+  const int W1 = OW + 1;
+  const int rows = (OW + kBM - 1) / W1 + 3;
+  return OH >= 1 && W1 <= 256 && rows <= 256 && (uint32_t)(rows * W1) * 128u <= HaloCfg::kSlotBytes;
+}
 
 int preload_gemm() {
   // force-load every instantiation (lazy module loading must never happen while
@@ -1064,10 +1057,14 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     const ConvGeom& g = c.ga;
     DBS_REQUIRE(c.a_mode == 2 && (c.b_mode == 0 || c.b_mode == 3) && g.R == 3 && g.S == 3 && g.stride == 1 &&
                     g.pad == 1 && g.cblocks == 1 && c.N == 64 && c.K == 576 && c.taps.n == 0 && !c.omap.on &&
-                    g.OW <= 32 && kBM % g.OW == 0 && (g.OH * g.OW) % kBM == 0 && c.ta.H == g.OH && c.ta.W == g.OW,
+                    halo_fits(g.OH, g.OW) && c.ta.H == g.OH && c.ta.W == g.OW,
                 DBS_ERR_ARGUMENT, "conv halo variant: unsupported geometry");
-    // 2-D [pixels][64] view of the NHWC activation, boxes of (TR + 2) * W pixel rows
-    st = make_tmap(&ta, c.a, 64, (uint64_t)c.ta.N * c.ta.H * c.ta.W, 64, 64, (uint32_t)(kBM + 2 * g.OW));
+    // one 4-D box per tile: halo_rows image rows x (W + 1) pixels from column -1
+    const int W1 = g.OW + 1;
+    p.halo_rows = (g.OW + kBM - 1) / W1 + 3;
+    p.halo_tpi = (g.OH * W1 + kBM - 1) / kBM;
+    p.halo_tiles = (int64_t)c.ta.N * p.halo_tpi;
+    st = make_tmap_nhwc(&ta, c.a, c.ta, W1, p.halo_rows, 1, 1);
     if (st) return st;
     if (c.b_mode == 0) {
       st = make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, 64);

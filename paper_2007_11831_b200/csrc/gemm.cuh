@@ -68,6 +68,8 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
               float* colsum_part);
 int conv_gemm(const ConvCall& c, cudaStream_t s);
 int preload_gemm();
+// the halo variant's one-box-per-tile input halo fits its shared-memory slot
+bool halo_fits(int OH, int OW);
 // SMs of the current (possibly green) context -- what a launch issued now can use
 int current_sm_count();
 

@@ -103,48 +103,78 @@ __global__ void bn_stats_kernel(double* __restrict__ sum_acc, double* __restrict
   invstd[c] = (float)(1.0 / sqrt(var + (double)kBnEps));
 }
 
-// out = act( gamma*(y-mean)*invstd + beta  [+ res | + BN_ds(yd)] ), 8 channels / thread
-__global__ void bn_apply_kernel(const uint16_t* __restrict__ y, const float* __restrict__ mean,
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void unpack8(const uint4 q, float (&v)[8]) {
+  v[0] = __uint_as_float(q.x << 16); v[1] = __uint_as_float(q.x & 0xFFFF0000u);
+  v[2] = __uint_as_float(q.y << 16); v[3] = __uint_as_float(q.y & 0xFFFF0000u);
+  v[4] = __uint_as_float(q.z << 16); v[5] = __uint_as_float(q.z & 0xFFFF0000u);
+  v[6] = __uint_as_float(q.w << 16); v[7] = __uint_as_float(q.w & 0xFFFF0000u);
+}
+__device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
+  return make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                    pack_bf16x2(v[6], v[7]));
+}
+// 8 consecutive per-channel coefficients from a shared-memory table
+__device__ __forceinline__ void coef8(const float* t, int c0, float (&k)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(t + c0), b = *reinterpret_cast<const float4*>(t + c0 + 4);
+  k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+}
+
+// out = act( a*y + b  [+ res | + a_d*yd + b_d] ), a = gamma*invstd, b = beta - mean*a:
+// the per-channel affine maps are formed once per CTA in shared memory; 8
+// channels (one 16-byte vector) per thread and trip
+__global__ void __launch_bounds__(256) bn_apply_kernel(const uint16_t* __restrict__ y, const float* __restrict__ mean,
                                 const float* __restrict__ invstd, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, const uint16_t* __restrict__ res,
                                 const uint16_t* __restrict__ yd, const float* __restrict__ mean_d,
                                 const float* __restrict__ invstd_d, const float* __restrict__ gamma_d,
                                 const float* __restrict__ beta_d, int relu, int C, int64_t M,
                                 uint16_t* __restrict__ out) {
+  extern __shared__ float tab[];  // [C] a, [C] b, ([C] a_d, [C] b_d)
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float a = gamma[c] * invstd[c];
+    tab[c] = a;
+    tab[C + c] = beta[c] - mean[c] * a;
+    if (yd) {
+      const float ad = gamma_d[c] * invstd_d[c];
+      tab[2 * C + c] = ad;
+      tab[3 * C + c] = beta_d[c] - mean_d[c] * ad;
+    }
+  }
+  __syncthreads();
   const int cv = C / 8;
   const int64_t total = M * cv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;  // C is a power of two (64..512)
-    const uint4 q = reinterpret_cast<const uint4*>(y)[i];
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-    uint32_t rw[4] = {0, 0, 0, 0}, dw[4] = {0, 0, 0, 0};
+    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;  // C is a power of two (64..2048)
+    float v[8], ka[8], kb[8];
+    unpack8(reinterpret_cast<const uint4*>(y)[i], v);
+    coef8(tab, c0, ka);
+    coef8(tab + C, c0, kb);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = fmaf(ka[k], v[k], kb[k]);
     if (res) {
-      const uint4 r = reinterpret_cast<const uint4*>(res)[i];
-      rw[0] = r.x; rw[1] = r.y; rw[2] = r.z; rw[3] = r.w;
+      float r[8];
+      unpack8(reinterpret_cast<const uint4*>(res)[i], r);
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] += r[k];
     }
     if (yd) {
-      const uint4 r = reinterpret_cast<const uint4*>(yd)[i];
-      dw[0] = r.x; dw[1] = r.y; dw[2] = r.z; dw[3] = r.w;
-    }
-    uint32_t o[4];
+      float r[8];
+      unpack8(reinterpret_cast<const uint4*>(yd)[i], r);
+      coef8(tab + 2 * C, c0, ka);
+      coef8(tab + 3 * C, c0, kb);
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int c = c0 + k;
-      const float v = bf2f((uint16_t)(w[k >> 1] >> ((k & 1) * 16)));
-      float z = fmaf(gamma[c] * invstd[c], v - mean[c], beta[c]);
-      if (res) z += bf2f((uint16_t)(rw[k >> 1] >> ((k & 1) * 16)));
-      if (yd) {
-        const float vd = bf2f((uint16_t)(dw[k >> 1] >> ((k & 1) * 16)));
-        z += fmaf(gamma_d[c] * invstd_d[c], vd - mean_d[c], beta_d[c]);
-      }
-      if (relu) z = fmaxf(z, 0.0f);
-      const uint32_t h = f2bf(z);
-      if (k & 1)
-        o[k >> 1] |= h << 16;
-      else
-        o[k >> 1] = h;
+      for (int k = 0; k < 8; k++) v[k] += fmaf(ka[k], r[k], kb[k]);
     }
-    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    if (relu) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] = fmaxf(v[k], 0.0f);
+    }
+    reinterpret_cast<uint4*>(out)[i] = pack8(v);
   }
 }
 
@@ -172,22 +202,36 @@ __global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __re
     is[k] = invstd[c0 + k];
   }
   if (lane_r < rows_per_pass) {
-    for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + lane_r; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
-      const int64_t i = r * cv + lane_c;
-      const uint4 qg = reinterpret_cast<const uint4*>(gin)[i];
-      const uint4 qy = reinterpret_cast<const uint4*>(y)[i];
-      uint4 qm = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-      if (mask) qm = reinterpret_cast<const uint4*>(mask)[i];
-      const uint32_t gw[4] = {qg.x, qg.y, qg.z, qg.w}, yw[4] = {qy.x, qy.y, qy.z, qy.w},
-                     mw[4] = {qm.x, qm.y, qm.z, qm.w};
+    // two rows per trip, all loads issued before the arithmetic
+    const int64_t step = (int64_t)gridDim.x * rows_per_pass;
+    for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + lane_r; r < M; r += 2 * step) {
+      const bool two = (r + step < M);
+      const int64_t i0 = r * cv + lane_c, i1 = (r + step) * cv + lane_c;
+      const uint4 qg0 = reinterpret_cast<const uint4*>(gin)[i0];
+      const uint4 qy0 = reinterpret_cast<const uint4*>(y)[i0];
+      const uint4 zero = make_uint4(0, 0, 0, 0), ones = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+      const uint4 qm0 = mask ? reinterpret_cast<const uint4*>(mask)[i0] : ones;
+      const uint4 qg1 = two ? reinterpret_cast<const uint4*>(gin)[i1] : zero;
+      const uint4 qy1 = two ? reinterpret_cast<const uint4*>(y)[i1] : zero;
+      const uint4 qm1 = (two && mask) ? reinterpret_cast<const uint4*>(mask)[i1] : ones;
+      float g[8], yv[8], mv[8];
+      unpack8(qg0, g);
+      unpack8(qy0, yv);
+      unpack8(qm0, mv);
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        const int sh = (k & 1) * 16;
-        float g = bf2f((uint16_t)(gw[k >> 1] >> sh));
-        if (mask && !(bf2f((uint16_t)(mw[k >> 1] >> sh)) > 0.0f)) g = 0.0f;
-        const float yh = (bf2f((uint16_t)(yw[k >> 1] >> sh)) - mu[k]) * is[k];
-        sb[k] += g;
-        sg[k] = fmaf(g, yh, sg[k]);
+        const float gg = mv[k] > 0.0f ? g[k] : 0.0f;
+        sb[k] += gg;
+        sg[k] = fmaf(gg, (yv[k] - mu[k]) * is[k], sg[k]);
+      }
+      unpack8(qg1, g);
+      unpack8(qy1, yv);
+      unpack8(qm1, mv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const float gg = mv[k] > 0.0f ? g[k] : 0.0f;
+        sb[k] += gg;
+        sg[k] = fmaf(gg, (yv[k] - mu[k]) * is[k], sg[k]);
       }
     }
   }
@@ -212,37 +256,46 @@ __global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __re
   }
 }
 
-// BN backward, pass 2: dy = gamma*invstd*(g - dbeta/M - yhat*dgamma/M), bf16;
-// optionally also stores g (the masked incoming gradient, for the shortcut).
-__global__ void bn_bwd_apply_kernel(const uint16_t* __restrict__ gin, const uint16_t* __restrict__ mask,
+// BN backward, pass 2: dy = gamma*invstd*(g - dbeta/M - yhat*dgamma/M) = k1 g + k2 y + k3
+// (k1 = gamma*invstd, k2 = -k1*invstd*dgamma/M, k3 = k1*(mean*invstd*dgamma - dbeta)/M,
+// formed once per CTA in shared memory), bf16; optionally also stores g (the masked
+// incoming gradient, for the shortcut).
+__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const uint16_t* __restrict__ gin, const uint16_t* __restrict__ mask,
                                     const uint16_t* __restrict__ y, const float* __restrict__ mean,
                                     const float* __restrict__ invstd, const float* __restrict__ gamma,
                                     const float* __restrict__ dgamma, const float* __restrict__ dbeta, int C,
                                     int64_t M, uint16_t* __restrict__ dy, uint16_t* __restrict__ g_out) {
+  extern __shared__ float tab[];  // [C] k1, [C] k2, [C] k3
+  const float invM = 1.0f / (float)M;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float is = invstd[c];
+    const float k1 = gamma[c] * is;
+    tab[c] = k1;
+    tab[C + c] = -k1 * is * dgamma[c] * invM;
+    tab[2 * C + c] = k1 * (mean[c] * is * dgamma[c] - dbeta[c]) * invM;
+  }
+  __syncthreads();
   const int cv = C / 8;
   const int64_t total = M * cv;
-  const float invM = 1.0f / (float)M;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;  // C is a power of two (64..512)
-    const uint4 qg = reinterpret_cast<const uint4*>(gin)[i];
-    const uint4 qy = reinterpret_cast<const uint4*>(y)[i];
-    uint4 qm = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    if (mask) qm = reinterpret_cast<const uint4*>(mask)[i];
-    const uint32_t gw[4] = {qg.x, qg.y, qg.z, qg.w}, yw[4] = {qy.x, qy.y, qy.z, qy.w},
-                   mw[4] = {qm.x, qm.y, qm.z, qm.w};
-    uint32_t o[4] = {0, 0, 0, 0}, go[4] = {0, 0, 0, 0};
+    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;  // C is a power of two (64..2048)
+    float g[8], yv[8], k1[8], k2[8], k3[8];
+    unpack8(reinterpret_cast<const uint4*>(gin)[i], g);
+    unpack8(reinterpret_cast<const uint4*>(y)[i], yv);
+    if (mask) {
+      float mv[8];
+      unpack8(reinterpret_cast<const uint4*>(mask)[i], mv);
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int c = c0 + k, sh = (k & 1) * 16;
-      float g = bf2f((uint16_t)(gw[k >> 1] >> sh));
-      if (mask && !(bf2f((uint16_t)(mw[k >> 1] >> sh)) > 0.0f)) g = 0.0f;
-      const float yh = (bf2f((uint16_t)(yw[k >> 1] >> sh)) - mean[c]) * invstd[c];
-      const float d = gamma[c] * invstd[c] * (g - dbeta[c] * invM - yh * dgamma[c] * invM);
-      o[k >> 1] |= (uint32_t)f2bf(d) << sh;
-      go[k >> 1] |= (uint32_t)f2bf(g) << sh;
+      for (int k = 0; k < 8; k++) g[k] = mv[k] > 0.0f ? g[k] : 0.0f;
     }
-    reinterpret_cast<uint4*>(dy)[i] = make_uint4(o[0], o[1], o[2], o[3]);
-    if (g_out) reinterpret_cast<uint4*>(g_out)[i] = make_uint4(go[0], go[1], go[2], go[3]);
+    coef8(tab, c0, k1);
+    coef8(tab + C, c0, k2);
+    coef8(tab + 2 * C, c0, k3);
+    float d[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) d[k] = fmaf(k1[k], g[k], fmaf(k2[k], yv[k], k3[k]));
+    reinterpret_cast<uint4*>(dy)[i] = pack8(d);
+    if (g_out) reinterpret_cast<uint4*>(g_out)[i] = pack8(g);
   }
 }
 
@@ -794,16 +847,15 @@ int alloc_all(dbs_resnet* m) {
 ConvTensor nhwc(int64_t N, int H, int W, int C) { return ConvTensor{(int)N, H, W, C}; }
 
 // forward conv -> y (bf16) + BN statistics -> mean/invstd
-// 3x3 / stride 1 / 64 -> 64 channels on whole-row tiles: the GEMM's halo
-// variant (resident filter, 3 shifted input halos per tile; gemm.cu HaloCfg).
+// 3x3 / stride 1 / 64 -> 64 channels: the GEMM's halo variant (resident filter, one
+// zero-padded input halo box per tile; gemm.cu HaloCfg).
 // DBS_CONV_HALO=0 turns it off (A/B measurements).
 bool halo_ok(const Conv& c) {
   static const bool enabled = [] {
     const char* e = getenv("DBS_CONV_HALO");
     return !(e && e[0] == '0');
   }();
-  return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 && c.OW <= 32 &&
-         128 % c.OW == 0 && (c.OH * c.OW) % 128 == 0;
+  return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 && halo_fits(c.OH, c.OW);
 }
 
 int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64_t B, cudaStream_t s) {
@@ -854,7 +906,7 @@ int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds
   const int64_t M = B * c.OH * c.OW;
   const int64_t total = M * (c.cout / 8);
   const Conv* d = ds >= 0 ? &m->convs[ds] : nullptr;
-  bn_apply_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+  bn_apply_kernel<<<grid_for(total, 256), 256, (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s>>>(
       m->y[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res, d ? m->y[ds] : nullptr,
       d ? m->mean[ds] : nullptr, d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
       d ? pf + d->b_off : nullptr, relu, c.cout, M, out);
@@ -869,14 +921,14 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
   const int64_t M = B * c.OH * c.OW;
   const int cv = c.cout / 8;
   const int rows_per_pass = 256 / cv;
-  int blocks = (int)((M + rows_per_pass * 16 - 1) / (rows_per_pass * 16));
-  if (blocks > num_sms() * 4) blocks = num_sms() * 4;
+  int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   if (blocks < 1) blocks = 1;
   bn_bwd_reduce_kernel<8><<<blocks, 256, 0, s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci], c.cout, M,
                                                   grad + c.g_off, grad + c.b_off);
   DBS_LAUNCH_CHECK();
   const int64_t total = M * cv;
-  bn_bwd_apply_kernel<<<grid_for(total, 256), 256, 0, s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
+  bn_bwd_apply_kernel<<<grid_for(total, 256), 256, (size_t)3 * c.cout * sizeof(float), s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
                                                             pf + c.g_off, grad + c.g_off, grad + c.b_off, c.cout, M,
                                                             dy, g_out);
   DBS_LAUNCH_CHECK();

@@ -1,5 +1,6 @@
 """Dev probe: kernel-time breakdown (torch.profiler/CUPTI) of ResNet-18 worker iterations."""
 import sys, collections, torch
+sys.path.insert(0, ".")
 from torch.profiler import profile, ProfilerActivity
 from paper_2007_11831_b200 import resnet, cluster
 from paper_2007_11831_b200.trainer import SimulatedTrainer
