@@ -479,7 +479,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kb = kb_begin + i;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], C::kABytes + C::kBBytes);
+      if (it < 12) GEMM_TRACE(100 + it);
+      // MN-major A: the upper 64 rows of the tile are skipped when they lie past
+      // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
+      // accumulator rows the epilogue masks
+      const bool a_hi = (p.a_mode != 1) || (m0 + 64 < p.M);
+      mbar_arrive_expect_tx(&full[s], (a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes);
       const int32_t k0 = kb * kBK;
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(a, &tmA, &full[s], k0, (int32_t)m0);
       } else if (p.a_mode == 1) {
         tma_load_2d(a, &tmA, &full[s], (int32_t)m0, k0);
-        tma_load_2d(a + 8192, &tmA, &full[s], (int32_t)m0 + 64, k0);
+        if (a_hi) tma_load_2d(a + 8192, &tmA, &full[s], (int32_t)m0 + 64, k0);
       } else if (p.a_mode == 4) {
         // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
         // the window corner, shifted by the tap; the tensor map's bounding box
@@ -621,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < num_k; i++, it++) {
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
+        if (it < 12) GEMM_TRACE(112 + it);
         tc_fence_after();
         const uint64_t a_s = a_desc0 + (uint64_t)((s * C::kABytes) >> 4);
         const uint64_t b_s = b_desc0 + (uint64_t)((s * C::kBBytes) >> 4);
@@ -696,7 +702,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           vo[k] = 0.0f;
         }
         const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
-        if (valid) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
+        // plain bf16 output (conv forward / input gradient): staged through
+        // shared memory so each store instruction writes 8 rows x 64 contiguous
+        // bytes instead of 32 scattered 16-byte pieces
+        const bool staged = (p.epi == DBS_EPI_BF16) && (cnt == 32) && (p.colsum_part == nullptr) &&
+                            (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
+        if (valid && !staged) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
+        if (staged) {
+          uint32_t* st = reinterpret_cast<uint32_t*>(tr);  // 32 rows x 20 words (16 + 4 pad) of this warp
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            *reinterpret_cast<uint4*>(st + lane * 20 + 4 * j) =
+                make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                           pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          __syncwarp();
+          uint16_t* dbase = reinterpret_cast<uint16_t*>(p.d) + n_base + (lane & 3) * 8;
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            const int rr = 8 * i + (lane >> 2);
+            const int64_t orow_r = __shfl_sync(0xffffffffu, orow, rr);
+            const int valid_r = __shfl_sync(0xffffffffu, (int)valid, rr);
+            if (valid_r)
+              *reinterpret_cast<uint4*>(dbase + orow_r * p.ldd) =
+                  *reinterpret_cast<const uint4*>(st + rr * 20 + (lane & 3) * 4);
+          }
+          __syncwarp();
+        }
         if (warp == 2 && lane == 0 && tj < 8) GEMM_TRACE(64 + 4 * tj + 2 * c + 1);
         if (p.colsum_part != nullptr) {
           const int64_t g = (m0 >> 5) + q;

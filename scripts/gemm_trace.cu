@@ -41,6 +41,9 @@ int main(int argc, char** argv) {
     for (int j = 0; j < 8; j++)
       printf("  mma tile %d: ready0 %lld ready1 %lld ready2 %lld\n", j, (long long)(r[96 + 3 * j] - t0),
              (long long)(r[97 + 3 * j] - t0), (long long)(r[98 + 3 * j] - t0));
+    printf("  k-block: producer-issue / mma-full:");
+    for (int j = 0; j < 12; j++) printf(" %lld/%lld", (long long)(r[100 + j] - t0), (long long)(r[112 + j] - t0));
+    printf("\n");
     for (int j = 0; j < 8; j++)
       printf("  epi tile %d: ldtm0 %lld chunk0 %lld ldtm1 %lld chunk1 %lld\n", j, (long long)(r[64 + 4 * j] - t0),
              (long long)(r[65 + 4 * j] - t0), (long long)(r[66 + 4 * j] - t0), (long long)(r[67 + 4 * j] - t0));

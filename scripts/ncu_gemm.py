@@ -1,5 +1,6 @@
 """ncu target: one plain tcgen05 GEMM launch (after warm-up) of shape M N K (bf16 out)."""
 import sys, torch
+sys.path.insert(0, ".")
 from paper_2007_11831_b200 import _lib
 M, N, K = (int(v) for v in sys.argv[1:4])
 L = _lib.lib()

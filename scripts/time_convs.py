@@ -21,6 +21,8 @@ SETS = {
     "r50": [(64, 56, 64, 64, 3, 1), (64, 56, 64, 256, 1, 1), (64, 56, 256, 64, 1, 1), (64, 28, 128, 128, 3, 1),
             (64, 14, 256, 256, 3, 1), (64, 14, 1024, 256, 1, 1), (64, 7, 512, 512, 3, 1), (64, 7, 512, 2048, 1, 1),
             (64, 56, 128, 128, 3, 2)],
+    "l2": [(128, 4, 512, 512, 3, 1), (256, 4, 512, 512, 3, 1), (512, 4, 512, 512, 3, 1),
+           (32, 14, 256, 256, 3, 1), (64, 14, 256, 256, 3, 1), (96, 14, 256, 256, 3, 1)],
 }
 which = sys.argv[1:] or ["r18"]
 for (N, H, C, K, k, s) in [sh for w in which if w in SETS for sh in SETS[w]]:
