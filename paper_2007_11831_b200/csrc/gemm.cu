@@ -81,6 +81,7 @@ struct GemmParams {
   int splits;           // split-K slices (atomic epilogue when > 1)
   ConvTaps taps;        // explicit conv taps of A (n = 0: R x S window)
   OutMap omap;          // strided output rows (on = 0: row-major)
+  int pair_a, pair_b;   // one TMA box covers two consecutive k-blocks (ring slots s, s+1) of A / B
   int halo_rows;        // halo variant: image rows per TMA box
   int halo_tpi;         // halo variant: tiles per image (ceil(OH (OW + 1) / 128))
   int64_t halo_tiles;   // halo variant: images x tiles per image
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       b_s = rs - b_r * p.gb.S;
     }
     if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
+    if ((p.pair_a | p.pair_b) == 0) {
     for (int i = 0; i < num_k; i++, it++) {
       const int kb = kb_begin + i;
       const int s = (int)(it % kStages);
@@ -560,6 +562,138 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
                       boh * g.stride + b_r - g.pad, bn_);
       }
+    }
+    } else {
+    // paired k-blocks (host guarantees an even k-block count per tile)
+    for (int i = 0; i < num_k;) {
+      constexpr int npair = 2;
+      const int s0 = (int)(it % kStages);
+      for (int u = 0; u < npair; u++)
+        mbar_wait(&empty[s0 + u], (((it + u) / kStages) & 1) ^ 1);
+      if (it < 12) GEMM_TRACE(100 + it);
+      // MN-major A: the upper 64 rows of the tile are skipped when they lie past
+      // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
+      // accumulator rows the epilogue masks
+      const bool a_hi = (p.a_mode != 1) || (m0 + 64 < p.M);
+      // a pair's bytes all complete on full[s0]; full[s0 + 1] gets a plain
+      // arrival (the MMA reaches slot s0 + 1 only after full[s0] completed)
+      mbar_arrive_expect_tx(&full[s0], npair * ((a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes));
+      mbar_arrive(&full[s0 + 1]);
+      for (int u = 0; u < npair; u++) {
+      const int s = s0 + u;
+      const int kb = kb_begin + i + u;
+      const int32_t k0 = kb * kBK;
+      uint8_t* a = sA + s * C::kABytes;
+      uint8_t* b = sB + s * C::kBBytes;
+      if (p.pair_a) {
+        if (u == 0) {
+          if (p.a_mode == 0) {
+            tma_load_3d(a, &tmA, &full[s0], 0, (int32_t)m0, kb);
+          } else {
+            const ConvGeom& g = p.ga;
+            const int cb = kb % g.cblocks;
+            const int rs = kb / g.cblocks;
+            int ah, aw;
+            if (p.taps.n > 0) {
+              ah = a_oh + p.taps.dh[rs];
+              aw = a_ow + p.taps.dw[rs];
+            } else {
+              const int r = rs / g.S, sx = rs - r * g.S;
+              ah = a_oh * g.stride + r - g.pad;
+              aw = a_ow * g.stride + sx - g.pad;
+            }
+            tma_load_5d(a, &tmA, &full[s0], 0, aw, ah, a_n, cb);
+          }
+        }
+      } else if (p.a_mode == 0) {
+        tma_load_2d(a, &tmA, &full[s0], k0, (int32_t)m0);
+      } else if (p.a_mode == 1) {
+        tma_load_2d(a, &tmA, &full[s0], (int32_t)m0, k0);
+        if (a_hi) tma_load_2d(a + 8192, &tmA, &full[s0], (int32_t)m0 + 64, k0);
+      } else if (p.a_mode == 4) {
+        // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
+        // the window corner, shifted by the tap; the tensor map's bounding box
+        // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int h0, w0, oh, ow;
+        if (p.taps.n > 0) {
+          h0 = a_oh - 1;
+          w0 = a_ow - 1;
+          oh = p.taps.dh[rs] + 1;
+          ow = p.taps.dw[rs] + 1;
+        } else {
+          oh = rs / g.S;
+          ow = rs - oh * g.S;
+          h0 = a_oh * g.stride - g.pad;
+          w0 = a_ow * g.stride - g.pad;
+        }
+        tma_load_im2col_4d(a, &tmA, &full[s0], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+      } else {
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int ah, aw;
+        if (p.taps.n > 0) {
+          ah = a_oh + p.taps.dh[rs];
+          aw = a_ow + p.taps.dw[rs];
+        } else {
+          const int r = rs / g.S, sx = rs - r * g.S;
+          ah = a_oh * g.stride + r - g.pad;
+          aw = a_ow * g.stride + sx - g.pad;
+        }
+        tma_load_4d(a, &tmA, &full[s0], cb * 64, aw, ah, a_n);
+      }
+      if (p.pair_b) {
+        if (u == 0) {
+          if (p.b_mode == 0) {
+            tma_load_3d(b, &tmB, &full[s0], 0, (int32_t)n0, kb);
+          } else {  // mode 3, BN = 64: the two k-blocks are consecutive 64-row k ranges
+            const ConvGeom& g = p.ga;
+            const int cb = kb % g.cblocks;
+            const int rs = kb / g.cblocks;
+            const int r = rs / g.S, sx = rs - r * g.S;
+            const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+            tma_load_3d(b, &tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
+          }
+        }
+      } else if (p.b_mode == 0) {
+        tma_load_2d(b, &tmB, &full[s0], k0, (int32_t)n0);
+      } else if (p.b_mode == 1) {
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, &tmB, &full[s0], (int32_t)n0 + 64 * j, k0);
+      } else if (p.b_mode == 3) {
+        // input gradient: the filter W[k][r][s][c] read in place as the flipped,
+        // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        const int r = rs / g.S, sx = rs - r * g.S;
+        const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
+      } else if (p.b_mode == 4) {
+        const ConvGeom& g = p.gb;
+        int bn_, boh, bow;
+        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_im2col_4d(b + j * 8192, &tmB, &full[s0], b_c0 + 64 * j, bow * g.stride - g.pad,
+                             boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
+      } else {
+        const ConvGeom& g = p.gb;
+        int bn_, boh, bow;
+        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_4d(b + j * 8192, &tmB, &full[s0], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
+                      boh * g.stride + b_r - g.pad, bn_);
+      }
+      }
+      it += npair;
+      i += npair;
+    }
     }
    }
    }
@@ -894,6 +1028,51 @@ int make_tmap_im2col(CUtensorMap* tm, const void* base, const ConvTensor& t, int
   return DBS_OK;
 }
 
+// K-major [rows][ld] matrix viewed as {64 k, rows, K / 64 k-blocks}: one box of
+// {64, box_rows, 2} fills two consecutive ring slots (K % 128 == 0 required)
+int make_tmap_kpair(CUtensorMap* tm, const void* base, uint64_t K, uint64_t rows, uint64_t ld_elems,
+                    uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  DBS_REQUIRE(((uintptr_t)base & 15) == 0 && (ld_elems * 2) % 16 == 0 && K % 128 == 0, DBS_ERR_ARGUMENT,
+              "paired k-block view: aligned base, ld %% 8 == 0 and K %% 128 == 0 required");
+  cuuint64_t dims[3] = {64, rows, K / 64};
+  cuuint64_t strides[2] = {ld_elems * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (k-pair) failed (%d)", (int)r);
+  return DBS_OK;
+}
+
+// NHWC activation viewed as {64 c, W, H, N, C / 64 channel blocks}: one box of
+// {64, bw, bh, bn, 2} fills two consecutive ring slots (two channel blocks of one tap)
+int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride) {
+  EncodeTiledFn fn = encode_fn();
+  DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 128 == 0, DBS_ERR_ARGUMENT,
+              "conv pair TMA: aligned base and C %% 128 == 0 required");
+  cuuint64_t dims[5] = {64, (cuuint64_t)t.W, (cuuint64_t)t.H, (cuuint64_t)t.N, (cuuint64_t)t.C / 64};
+  cuuint64_t strides[4] = {(cuuint64_t)t.C * 2, (cuuint64_t)t.W * t.C * 2, (cuuint64_t)t.H * t.W * t.C * 2, 128};
+  cuuint32_t box[5] = {64, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn, 2};
+  cuuint32_t es[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (5d pair) failed (%d)", (int)r);
+  return DBS_OK;
+}
+
+bool kpair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_KPAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // the 4-D box path covers a tile of `rows` pixels only when it aligns with whole rows / images
 bool pixel_box_fits(int OH, int OW, int rows) {
   const int hw = OH * OW;
@@ -1024,14 +1203,21 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
   CUtensorMap ta, tb;
   int st;
   // A: K-major [M][lda] -> box {64 K, 128 M};  MN-major [K][lda] -> box {64 M, 64 K}
+  // K-major operands with K % 128 == 0: one box per two k-blocks (fewer TMA operations)
+  const bool kp = kpair_enabled() && (K % 128 == 0) && (lda * 2) % 16 == 0 && (ldb * 2) % 16 == 0;
+  const bool pa = kp && !a_mn, pb = kp && !b_mn;
   st = a_mn ? make_tmap(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 64, 64)
+       : pa ? make_tmap_kpair(&ta, a, (uint64_t)K, (uint64_t)M, (uint64_t)lda, 128)
             : make_tmap(&ta, a, (uint64_t)K, (uint64_t)M, (uint64_t)lda, 64, 128);
   if (st) return st;
   // B: K-major [N][ldb] -> box {64 K, BN};  MN-major [K][ldb] -> box {64 N, 64 K}
   st = b_mn ? make_tmap(&tb, b, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 64, 64)
+       : pb ? make_tmap_kpair(&tb, b, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)bn)
             : make_tmap(&tb, b, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, 64, (uint32_t)bn);
   if (st) return st;
   GemmParams p{};
+  p.pair_a = pa;
+  p.pair_b = pb;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1084,6 +1270,8 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     }
     bn = pick;
   }
+  // paired k-block loads need an even k-block count in every tile: no split-K
+  const bool pairing = kpair_enabled() && (c.splits <= 1) && ((c.K + kBK - 1) / kBK) % 2 == 0;
   // ---- halo variant: 3x3 / stride 1 / 64 -> 64 channels, whole-row tiles of one image ----
   if (c.halo) {
     const ConvGeom& g = c.ga;
@@ -1132,12 +1320,22 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     int bw, bh, bnn;
     st = pixel_box(c.ga.OH, c.ga.OW, kBM, bw, bh, bnn);
     if (st) return st;
-    st = make_tmap_nhwc(&ta, c.a, c.ta, bw, bh, bnn, c.ga.stride);
+    if (pairing && c.ga.cblocks % 2 == 0) {
+      st = make_tmap_nhwc_pair(&ta, c.a, c.ta, bw, bh, bnn, c.ga.stride);
+      p.pair_a = 1;
+    } else {
+      st = make_tmap_nhwc(&ta, c.a, c.ta, bw, bh, bnn, c.ga.stride);
+    }
     if (st) return st;
     p.ga = c.ga;
   } else {
-    st = c.a_mode ? make_tmap(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 64, 64)
-                  : make_tmap(&ta, c.a, (uint64_t)c.K, (uint64_t)c.M, (uint64_t)c.lda, 64, 128);
+    if (c.a_mode == 0 && pairing && c.K % 128 == 0 && (c.lda * 2) % 16 == 0) {
+      st = make_tmap_kpair(&ta, c.a, (uint64_t)c.K, (uint64_t)c.M, (uint64_t)c.lda, 128);
+      p.pair_a = 1;
+    } else {
+      st = c.a_mode ? make_tmap(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 64, 64)
+                    : make_tmap(&ta, c.a, (uint64_t)c.K, (uint64_t)c.M, (uint64_t)c.lda, 64, 128);
+    }
     if (st) return st;
   }
   // ---- B ----
@@ -1164,18 +1362,26 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     DBS_REQUIRE(c.tb.C % 64 == 0 && c.tb.N % 64 == 0 && ((uintptr_t)c.b & 15) == 0, DBS_ERR_ARGUMENT,
                 "dgrad filter view: Cin, Cout multiples of 64 required");
+    // BN = 64: two consecutive 64-row k blocks of one tap are one box of 128 k rows
+    const bool pb = pairing && bn == 64 && c.ga.cblocks % 2 == 0;
     cuuint64_t dims[3] = {(cuuint64_t)c.tb.C, (cuuint64_t)c.tb.W, (cuuint64_t)c.tb.N};
     cuuint64_t strides[2] = {(cuuint64_t)c.tb.C * 2, (cuuint64_t)c.tb.W * c.tb.C * 2};
-    cuuint32_t box[3] = {64, 1, 64};
+    cuuint32_t box[3] = {64, 1, pb ? 128u : 64u};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.b), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (3d filter) failed (%d)", (int)r);
     DBS_REQUIRE(c.a_mode == 2, DBS_ERR_ARGUMENT, "flipped-filter B needs a conv-mode A");
+    p.pair_b = pb;
   } else {
-    st = c.b_mode ? make_tmap(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, 64, 64)
-                  : make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, (uint32_t)bn);
+    if (c.b_mode == 0 && pairing && c.K % 128 == 0 && (c.ldb * 2) % 16 == 0) {
+      st = make_tmap_kpair(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, (uint32_t)bn);
+      p.pair_b = 1;
+    } else {
+      st = c.b_mode ? make_tmap(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, 64, 64)
+                    : make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, (uint32_t)bn);
+    }
     if (st) return st;
   }
   const int num_k = (int)((c.K + kBK - 1) / kBK);
