@@ -814,62 +814,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem_base + b * kAccCols + ((uint32_t)(q * 32) << 16);
     const bool stats = (p.sum_part != nullptr);
     if (BN >= 32) {
+      // software-pipelined TMEM reads: chunk c + 1 is loaded while chunk c is
+      // stored (the registers are free once chunk c is packed / copied)
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(lane_addr, r);
+      tmem_ld_wait();
 #pragma unroll 1
       for (int c = 0; c < BN / 32; c++) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(lane_addr + c * 32, r);
-        tmem_ld_wait();
-        if (warp == 2 && lane == 0 && tj < 8) GEMM_TRACE(64 + 4 * tj + 2 * c);
-        if (c == BN / 32 - 1) {
-          // accumulator fully in registers: hand it back to the MMA warp
+        const int64_t n_base = n0 + c * 32;
+        const bool last = (c == BN / 32 - 1) || (n_base + 32 >= p.N);  // warp-uniform
+        if (last) {
+          // accumulator fully read: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[b]);
           if (warp == 2 && lane == 0) GEMM_TRACE(42 + tj);
         }
-        const int64_t n_base = n0 + c * 32;
-        if (n_base >= p.N) continue;  // warp-uniform
-        float v[32], vo[32];
-#pragma unroll
-        for (int k = 0; k < 32; k++) {
-          v[k] = valid ? __uint_as_float(r[k]) : 0.0f;
-          vo[k] = 0.0f;
-        }
+        const bool prefetch = !last;
         const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
-        // plain bf16 output (conv forward / input gradient): staged through
-        // shared memory so each store instruction writes 8 rows x 64 contiguous
-        // bytes instead of 32 scattered 16-byte pieces
+        // plain bf16 output (conv forward / input gradient): packed straight from
+        // the TMEM registers and staged through shared memory so each store
+        // instruction writes 8 rows x 64 contiguous bytes (the epilogue warps are
+        // alone on their schedulers: instruction count is the epilogue's cost)
         const bool staged = (p.epi == DBS_EPI_BF16) && (cnt == 32) && (p.colsum_part == nullptr) &&
                             (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
-        if (valid && !staged) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
-        if (staged) {
-          uint32_t* st = reinterpret_cast<uint32_t*>(tr);  // 32 rows x 20 words (16 + 4 pad) of this warp
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 4; j++)
-            *reinterpret_cast<uint4*>(st + lane * 20 + 4 * j) =
-                make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                           pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-          __syncwarp();
-          uint16_t* dbase = reinterpret_cast<uint16_t*>(p.d) + n_base + (lane & 3) * 8;
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const int rr = 8 * i + (lane >> 2);
-            const int64_t orow_r = __shfl_sync(0xffffffffu, orow, rr);
-            const int valid_r = __shfl_sync(0xffffffffu, (int)valid, rr);
-            if (valid_r)
-              *reinterpret_cast<uint4*>(dbase + orow_r * p.ldd) =
-                  *reinterpret_cast<const uint4*>(st + rr * 20 + (lane & 3) * 4);
-          }
-          __syncwarp();
-        }
-        if (warp == 2 && lane == 0 && tj < 8) GEMM_TRACE(64 + 4 * tj + 2 * c + 1);
-        if (p.colsum_part != nullptr) {
-          const int64_t g = (m0 >> 5) + q;
-          const bool group_live = (m0 + q * 32 < p.M);
-          const float s = warp_colsum(vo, lane);
-          if (lane < cnt && group_live) p.colsum_part[g * p.N + n_base + lane] = s;
-        }
         if (stats) {
           // BN batch statistics: warp column sums (a 32x33 transpose in shared
           // memory: 32 stores + 32 loads instead of 160 shuffles) -> tile sums
@@ -877,7 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __shared__ float red_s[4][32], red_q[4][32];
           // one transpose: lane j reads column j and forms both sums
 #pragma unroll
-          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = v[k];
+          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = valid ? __uint_as_float(r[k]) : 0.0f;
           __syncwarp();
           float s = 0.f, sq = 0.f;
 #pragma unroll
@@ -898,6 +866,58 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           epilogue_bar();
         }
+        if (staged) {
+          uint32_t* st = reinterpret_cast<uint32_t*>(tr);  // 32 rows x 20 words (16 + 4 pad) of this warp
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            *reinterpret_cast<uint4*>(st + lane * 20 + 4 * j) = make_uint4(
+                pack_bf16x2(__uint_as_float(r[8 * j]), __uint_as_float(r[8 * j + 1])),
+                pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
+                pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
+                pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
+          if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+          __syncwarp();
+          uint16_t* dbase = reinterpret_cast<uint16_t*>(p.d) + n_base + (lane & 3) * 8;
+          if (!kHalo && !p.omap.on) {
+            // identity row map: the storing lane forms its row itself
+            const int64_t row_w = m0 + q * 32;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              const int rr = 8 * i + (lane >> 2);
+              const uint4 val = *reinterpret_cast<const uint4*>(st + rr * 20 + (lane & 3) * 4);
+              if (row_w + rr < p.M) *reinterpret_cast<uint4*>(dbase + (row_w + rr) * p.ldd) = val;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              const int rr = 8 * i + (lane >> 2);
+              const int64_t orow_r = __shfl_sync(0xffffffffu, orow, rr);
+              const int valid_r = __shfl_sync(0xffffffffu, (int)valid, rr);
+              if (valid_r)
+                *reinterpret_cast<uint4*>(dbase + orow_r * p.ldd) =
+                    *reinterpret_cast<const uint4*>(st + rr * 20 + (lane & 3) * 4);
+            }
+          }
+          __syncwarp();
+        } else {
+          float v[32], vo[32];
+#pragma unroll
+          for (int k = 0; k < 32; k++) {
+            v[k] = valid ? __uint_as_float(r[k]) : 0.0f;
+            vo[k] = 0.0f;
+          }
+          if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+          if (valid) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
+          if (p.colsum_part != nullptr) {
+            const int64_t g = (m0 >> 5) + q;
+            const bool group_live = (m0 + q * 32 < p.M);
+            const float s = warp_colsum(vo, lane);
+            if (lane < cnt && group_live) p.colsum_part[g * p.N + n_base + lane] = s;
+          }
+        }
+        if (prefetch) tmem_ld_wait();
+        if (last) break;
       }
     } else {
       uint32_t r[16];
@@ -1144,6 +1164,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   }
   GemmParams q = p;
   q.splits = splits;
+
   // persistent: one CTA per SM of the current (possibly green) context
   const int64_t tiles = kHalo ? p.halo_tiles : ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
   const int64_t sms = current_sm_count();
