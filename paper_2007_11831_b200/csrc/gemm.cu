@@ -589,6 +589,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (u == 0) {
           if (p.a_mode == 0) {
             tma_load_3d(a, &tmA, &full[s0], 0, (int32_t)m0, kb);
+          } else if (p.a_mode == 1) {  // <= 64 rows: 128 k rows fill both halves of slot s0
+            tma_load_2d(a, &tmA, &full[s0], (int32_t)m0, k0);
           } else {
             const ConvGeom& g = p.ga;
             const int cb = kb % g.cblocks;
@@ -649,6 +651,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (u == 0) {
           if (p.b_mode == 0) {
             tma_load_3d(b, &tmB, &full[s0], 0, (int32_t)n0, kb);
+          } else if (p.b_mode == 2 || p.b_mode == 4) {  // BN = 64: 128 output pixels in one box
+            const ConvGeom& g = p.gb;
+            int bn_, boh, bow;
+            pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+            if (p.b_mode == 4)
+              tma_load_im2col_4d(b, &tmB, &full[s0], b_c0, bow * g.stride - g.pad, boh * g.stride - g.pad, bn_,
+                                 (uint16_t)b_s, (uint16_t)b_r);
+            else
+              tma_load_4d(b, &tmB, &full[s0], b_c0, bow * g.stride + b_s - g.pad, boh * g.stride + b_r - g.pad, bn_);
           } else {  // mode 3, BN = 64: the two k-blocks are consecutive 64-row k ranges
             const ConvGeom& g = p.ga;
             const int cb = kb % g.cblocks;
@@ -762,7 +773,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], (it / kStages) & 1);
         if (it < 12) GEMM_TRACE(112 + it);
         tc_fence_after();
-        const uint64_t a_s = a_desc0 + (uint64_t)((s * C::kABytes) >> 4);
+        // (pair_a == 2: an MN-major A of <= 64 rows whose paired box put k-block
+        // kb + 1 in the unused upper half of slot s - 1)
+        const uint32_t a_off = p.pair_a == 2 ? (uint32_t)((s & ~1) * C::kABytes + (s & 1) * 8192)
+                                             : (uint32_t)(s * C::kABytes);
+        const uint64_t a_s = a_desc0 + (uint64_t)(a_off >> 4);
         const uint64_t b_s = b_desc0 + (uint64_t)((s * C::kBBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < kBK / 16; k++)
@@ -1293,6 +1308,11 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   }
   // paired k-block loads need an even k-block count in every tile: no split-K
   const bool pairing = kpair_enabled() && (c.splits <= 1) && ((c.K + kBK - 1) / kBK) % 2 == 0;
+  // weight gradient of a <= 64-output-channel conv (dY^T MN-major A, im2col(X) B,
+  // 64-wide N tile): 128 pixels per box for both operands; split-K slices are
+  // rounded to an even number of k-blocks
+  const bool wpair = kpair_enabled() && c.a_mode == 1 && c.M <= 64 && c.b_mode == 2 && bn == 64 &&
+                     ((c.K + kBK - 1) / kBK) % 2 == 0;
   // ---- halo variant: 3x3 / stride 1 / 64 -> 64 channels, whole-row tiles of one image ----
   if (c.halo) {
     const ConvGeom& g = c.ga;
@@ -1354,27 +1374,31 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
       st = make_tmap_kpair(&ta, c.a, (uint64_t)c.K, (uint64_t)c.M, (uint64_t)c.lda, 128);
       p.pair_a = 1;
     } else {
-      st = c.a_mode ? make_tmap(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 64, 64)
+      st = c.a_mode ? make_tmap(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 64, wpair ? 128 : 64)
                     : make_tmap(&ta, c.a, (uint64_t)c.K, (uint64_t)c.M, (uint64_t)c.lda, 64, 128);
+      if (wpair) p.pair_a = 2;
     }
     if (st) return st;
   }
   // ---- B ----
   p.b_mode = c.b_mode;
-  if (c.b_mode == 2 && (force_im2col() || !pixel_box_fits(c.gb.OH, c.gb.OW, kBK))) {
-    st = make_tmap_im2col(&tb, c.b, c.tb, -c.gb.pad, c.gb.pad - (c.gb.R - 1), kBK, c.gb.stride);
+  const int kpix = wpair ? 2 * kBK : kBK;  // pixels per weight-gradient B box
+  if (c.b_mode == 2 && (force_im2col() || !pixel_box_fits(c.gb.OH, c.gb.OW, kpix))) {
+    st = make_tmap_im2col(&tb, c.b, c.tb, -c.gb.pad, c.gb.pad - (c.gb.R - 1), kpix, c.gb.stride);
     if (st) return st;
     p.b_mode = 4;
+    p.pair_b = wpair;
     p.gb = c.gb;
     DBS_REQUIRE(c.gb.Cin % bn == 0 || bn % c.gb.Cin == 0, DBS_ERR_ARGUMENT, "wgrad: tile must not straddle (r,s)");
     DBS_REQUIRE(bn <= c.gb.Cin, DBS_ERR_ARGUMENT, "wgrad: BN %d > Cin %d", bn, c.gb.Cin);
   } else if (c.b_mode == 2) {
     int bw, bh, bnn;
-    st = pixel_box(c.gb.OH, c.gb.OW, kBK, bw, bh, bnn);
+    st = pixel_box(c.gb.OH, c.gb.OW, kpix, bw, bh, bnn);
     if (st) return st;
     st = make_tmap_nhwc(&tb, c.b, c.tb, bw, bh, bnn, c.gb.stride);
     if (st) return st;
     p.gb = c.gb;
+    p.pair_b = wpair;
     DBS_REQUIRE(c.gb.Cin % bn == 0 || bn % c.gb.Cin == 0, DBS_ERR_ARGUMENT, "wgrad: tile must not straddle (r,s)");
     DBS_REQUIRE(bn <= c.gb.Cin, DBS_ERR_ARGUMENT, "wgrad: BN %d > Cin %d", bn, c.gb.Cin);
   } else if (c.b_mode == 3) {
@@ -1409,6 +1433,7 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   int splits = c.splits > 0 ? c.splits : 1;
   if (splits > num_k) splits = num_k;
   p.kb_per_split = (num_k + splits - 1) / splits;
+  if (p.pair_a | p.pair_b) p.kb_per_split += p.kb_per_split & 1;  // even k-block count per slice
   splits = (num_k + p.kb_per_split - 1) / p.kb_per_split;
   DBS_REQUIRE(splits == 1 || c.epi == DBS_EPI_F32_ATOMIC, DBS_ERR_ARGUMENT, "split-K needs the atomic epilogue");
   return dispatch(ta, tb, p, bn, splits, s);
