@@ -202,52 +202,63 @@ __global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __re
     is[k] = invstd[c0 + k];
   }
   if (lane_r < rows_per_pass) {
-    // two rows per trip, all loads issued before the arithmetic
+    // four rows per trip, all twelve 16-byte loads issued before the arithmetic
     const int64_t step = (int64_t)gridDim.x * rows_per_pass;
-    for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + lane_r; r < M; r += 2 * step) {
-      const bool two = (r + step < M);
-      const int64_t i0 = r * cv + lane_c, i1 = (r + step) * cv + lane_c;
-      const uint4 qg0 = reinterpret_cast<const uint4*>(gin)[i0];
-      const uint4 qy0 = reinterpret_cast<const uint4*>(y)[i0];
-      const uint4 zero = make_uint4(0, 0, 0, 0), ones = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-      const uint4 qm0 = mask ? reinterpret_cast<const uint4*>(mask)[i0] : ones;
-      const uint4 qg1 = two ? reinterpret_cast<const uint4*>(gin)[i1] : zero;
-      const uint4 qy1 = two ? reinterpret_cast<const uint4*>(y)[i1] : zero;
-      const uint4 qm1 = (two && mask) ? reinterpret_cast<const uint4*>(mask)[i1] : ones;
-      float g[8], yv[8], mv[8];
-      unpack8(qg0, g);
-      unpack8(qy0, yv);
-      unpack8(qm0, mv);
+    const uint4 zero = make_uint4(0, 0, 0, 0), ones = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + lane_r; r < M; r += 4 * step) {
+      uint4 qg[4], qy[4], qm[4];
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const float gg = mv[k] > 0.0f ? g[k] : 0.0f;
-        sb[k] += gg;
-        sg[k] = fmaf(gg, (yv[k] - mu[k]) * is[k], sg[k]);
+      for (int u = 0; u < 4; u++) {
+        const int64_t rr = r + u * step;
+        const bool ok = rr < M;
+        const int64_t i = rr * cv + lane_c;
+        qg[u] = ok ? reinterpret_cast<const uint4*>(gin)[i] : zero;
+        qy[u] = ok ? reinterpret_cast<const uint4*>(y)[i] : zero;
+        qm[u] = (ok && mask) ? reinterpret_cast<const uint4*>(mask)[i] : ones;
       }
-      unpack8(qg1, g);
-      unpack8(qy1, yv);
-      unpack8(qm1, mv);
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const float gg = mv[k] > 0.0f ? g[k] : 0.0f;
-        sb[k] += gg;
-        sg[k] = fmaf(gg, (yv[k] - mu[k]) * is[k], sg[k]);
+      for (int u = 0; u < 4; u++) {
+        float g[8], yv[8], mv[8];
+        unpack8(qg[u], g);
+        unpack8(qy[u], yv);
+        unpack8(qm[u], mv);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const float gg = mv[k] > 0.0f ? g[k] : 0.0f;
+          sb[k] += gg;
+          sg[k] = fmaf(gg, (yv[k] - mu[k]) * is[k], sg[k]);
+        }
       }
     }
   }
-  // block reduction over lane_r for each channel: [rows_per_pass][C] partials in
-  // shared memory (no shared-memory atomics), then one global atomic per channel
-  if (lane_r < rows_per_pass) {
+  // reduction over lane_r: first inside the warp (lanes lane_c, lane_c + cv, ...
+  // hold the same channels), then across the warps in shared memory, then one
+  // global atomic per channel and block
+  if (cv < 32) {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      red_g[lane_r * C + c0 + k] = sg[k];
-      red_b[lane_r * C + c0 + k] = sb[k];
+      for (int o = cv; o < 32; o <<= 1) {
+        sg[k] += __shfl_xor_sync(0xffffffffu, sg[k], o);
+        sb[k] += __shfl_xor_sync(0xffffffffu, sb[k], o);
+      }
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const bool writer = (cv < 32) ? (lane < cv) : (lane_r < rows_per_pass);
+  const int slot = (cv < 32) ? warp : lane_r;  // partial index
+  const int nslot = (cv < 32) ? nw : rows_per_pass;
+  if (writer) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      red_g[slot * C + c0 + k] = sg[k];
+      red_b[slot * C + c0 + k] = sb[k];
     }
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < C; idx += blockDim.x) {
     float a = 0.f, b = 0.f;
-    for (int r = 0; r < rows_per_pass; r++) {
+    for (int r = 0; r < nslot; r++) {
       a += red_g[r * C + idx];
       b += red_b[r * C + idx];
     }
@@ -921,7 +932,7 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
   const int64_t M = B * c.OH * c.OW;
   const int cv = c.cout / 8;
   const int rows_per_pass = 256 / cv;
-  int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread
+  int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread (one trip)
   if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   if (blocks < 1) blocks = 1;
   bn_bwd_reduce_kernel<8><<<blocks, 256, 0, s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci], c.cout, M,
