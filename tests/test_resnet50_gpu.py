@@ -30,6 +30,10 @@ SHAPES_R50 = [  # N, H, Cin, Cout, k, stride
     (4, 7, 512, 512, 3, 1),
     (3, 7, 2048, 512, 1, 1),
     (5, 14, 128, 64, 3, 1),
+    (3, 16, 64, 64, 3, 1),   # halo variant at other widths (tiles cross rows, per-image tails)
+    (2, 28, 64, 64, 3, 1),
+    (7, 8, 64, 64, 3, 1),
+    (3, 16, 128, 64, 3, 1),  # paired 128-pixel weight-gradient boxes (box mode), 4 tiles per image
 ]
 
 
