@@ -9,7 +9,7 @@
 
 using namespace dbs::sm100;
 
-template <int N>
+template <int N, int M = 128>
 __global__ void __launch_bounds__(128, 1) mma_kernel(int reps, int variant, unsigned long long* out) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int reps, int variant, unsi
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
     const uint32_t a_base = smem_u32(sm), b_base = smem_u32(sm + 128 * 128);
-    const uint32_t idesc = make_idesc_bf16(128, N, 0, 0);
+    const uint32_t idesc = make_idesc_bf16(M, N, 0, 0);
     const long long t0 = clock64();
     for (int i = 0; i < reps; i++) {
 #pragma unroll
@@ -58,15 +58,15 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int reps, int variant, unsi
   if (warp == 0) tmem_dealloc<(N < 32 ? 32 : N)>(tmem);
 }
 
-template <int N>
+template <int N, int M = 128>
 void run(int grid, int variant) {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 1024);
   const int smem = (128 + N) * 128 + 1024;
-  cudaFuncSetAttribute(mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_kernel<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int reps = 2000;
-  mma_kernel<N><<<grid, 128, smem>>>(reps, variant, d);
-  mma_kernel<N><<<grid, 128, smem>>>(reps, variant, d);
+  mma_kernel<N, M><<<grid, 128, smem>>>(reps, variant, d);
+  mma_kernel<N, M><<<grid, 128, smem>>>(reps, variant, d);
   cudaDeviceSynchronize();
   unsigned long long h[1024];
   cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
@@ -74,16 +74,17 @@ void run(int grid, int variant) {
   for (int i = 0; i < grid; i++) avg += (double)h[i];
   avg /= grid;
   const double per = avg / (reps * 4);
-  printf("variant %d  M=128 N=%3d K=16 SS: %6.1f clk/MMA  %7.0f MAC/clk/SM  (%.0f%% of 4096)  err=%s\n", variant, N, per,
-         128.0 * N * 16 / per, 100.0 * 128.0 * N * 16 / per / 4096, cudaGetErrorString(cudaGetLastError()));
+  printf("variant %d  M=%d N=%3d K=16 SS: %6.1f clk/MMA  %7.0f MAC/clk/SM  (%.0f%% of 4096)  err=%s\n", variant, M, N, per,
+         (double)M * N * 16 / per, 100.0 * M * N * 16 / per / 4096, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
 int main(int argc, char** argv) {
   const int grid = argc > 1 ? atoi(argv[1]) : 148;
-  for (int v = 0; v < 3; v++) {
-    run<64>(grid, v);
-    run<128>(grid, v);
-  }
+  run<64>(grid, 0);
+  run<128>(grid, 0);
+  run<256>(grid, 0);
+  run<256, 64>(grid, 0);
+  run<128, 64>(grid, 0);
   return 0;
 }
