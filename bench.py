@@ -60,6 +60,30 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def bench_device(local, world):
+    """One process per GPU.  DBS_BENCH_SHARE_GPU=1 (testing the multi-rank path on a
+    one-GPU box only) maps every rank onto the visible devices round-robin."""
+    import torch
+
+    if world <= 1:
+        return 0
+    if os.environ.get("DBS_BENCH_SHARE_GPU") == "1":
+        return local % torch.cuda.device_count()
+    return local
+
+
+def init_group():
+    """Host-side process group (IPC handles, worker times, max over ranks): NCCL
+    over NVLink; gloo when ranks share a GPU (NCCL refuses duplicate devices)."""
+    import torch
+    import torch.distributed as dist
+
+    if os.environ.get("DBS_BENCH_SHARE_GPU") == "1":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -503,12 +527,12 @@ def run_allreduce(args):
     from paper_2007_11831_b200.comm import Communicator, max_over_ranks
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local if world > 1 else 0)
+    torch.cuda.set_device(bench_device(local, world))
     group = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_group()
     else:
         import torch.distributed as dist
 
@@ -587,11 +611,11 @@ def main():
     rank, world, local = dist_env()
     import torch
 
-    torch.cuda.set_device(local if world > 1 else 0)
+    torch.cuda.set_device(bench_device(local, world))
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_group()
     peaks = load_peaks()
     wl = args.workload
     w = WL[wl]
