@@ -416,15 +416,18 @@ def cpu_baseline(wl, X, y, threads=None):
             "kind": "port", "sample": sample}
 
 
-def e2e_run(tr, wl, X, y, args):
+def e2e_run(tr, wl, X, y, args, world=1):
     """Public API end to end: the same DBS run (same disturbance, plan carried across
     epochs) with the dataset uploaded from pinned host memory at the start of every
-    epoch and the per-iteration losses / worker times read back every epoch."""
+    epoch and the per-iteration losses / worker times read back every epoch.  Under
+    torchrun every rank uploads its own dataset copy; the time is the max over ranks."""
     import torch
 
     from paper_2007_11831_b200 import cluster
 
     w = WL[wl]
+    if X is None:  # the distributed trainer generated its data on the device
+        X, y = tr.X.cpu().numpy(), tr.y.cpu().numpy()
     Xh = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()
     yh = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
     h2d_per_epoch = Xh.numel() * Xh.element_size() + yh.numel() * yh.element_size()
@@ -433,10 +436,10 @@ def e2e_run(tr, wl, X, y, args):
         tr.X.copy_(Xh.view(tr.X.shape), non_blocking=True)
         tr.y.copy_(yh, non_blocking=True)
 
-    cfg = cluster.StrategyConfig("dbs", w["workers"] * w["per_worker"])
+    cfg = cluster.StrategyConfig("dbs", w["workers"] * world * w["per_worker"])
     extra = {"averaging_interval": w["avg"]} if w.get("avg") else {}
     res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=w["lr"], momentum=w["mom"],
-                 profiles=profiles(w["workers"], w["mult"]), record_loss=True, timed_from=args.warmup,
+                 profiles=profiles(w["workers"] * world, w["mult"]), record_loss=True, timed_from=args.warmup,
                  epoch_hook=upload, **extra)
     timed = res.stats[args.warmup:]
     iters = [cluster.iterations_for_plan(s.plan) for s in timed]
@@ -639,7 +642,7 @@ def main():
         rpt.write_run_json(reps, [], out / f"bench_{wl}_n{world}.json")
     roof = kernel_roofline(peaks, wl)
     aux = aux_rooflines(tr, peaks) if world == 1 else None
-    e2e = None if (args.no_e2e or world > 1) else e2e_run(tr, wl, X, y, args)
+    e2e = None if args.no_e2e else e2e_run(tr, wl, X, y, args, world)
     cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl, X, y)
     gaps = [np.mean(s.per_worker_wait) / max(s.per_worker_gpu) for s in fixed["stats"]]
     out = {

@@ -544,7 +544,8 @@ class DistributedTrainer(SimulatedTrainer):
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
-            skip_update: bool = False, timed_from: Optional[int] = None) -> RunResult:
+            skip_update: bool = False, timed_from: Optional[int] = None,
+            epoch_hook: Optional[Callable[[int], None]] = None) -> RunResult:
         import torch
 
         from .comm import max_over_ranks
@@ -565,6 +566,8 @@ class DistributedTrainer(SimulatedTrainer):
                 torch.distributed.barrier(self.group)
                 t_start = torch.cuda.Event(enable_timing=True)
                 t_start.record()
+            if epoch_hook is not None:
+                epoch_hook(epoch)
             launches0 = _lib.lib().dbs_launch_count()
             plan, smoothed = distributed_plan(config, epoch, W, D, stats[-1] if stats else None, smoothed)
             plans.append(plan)
