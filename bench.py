@@ -150,7 +150,7 @@ WL = {
                         desc="C4: C3 with periodic model averaging (local SGD on per-worker replicas, averaged every "
                              "step=4 iterations), DBS vs fixed plan, step = 1 epoch"),
     "resnet50": dict(D=12800, workers=4, per_worker=64, lr=0.05, mom=0.9, mult=None, image=224, classes=1000,
-                     max_batch=160, cpu_per_worker=16,
+                     max_batch=160, cpu_per_worker=16, smoothing=0.7,
                      desc="C5: ResNet-50 (torchvision v1.5) on synthetic ImageNet-shaped 12800x3x224x224 uint8, 1000 "
                           "classes, 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the B200, "
                           "B=256 (64/worker fixed), step = 1 epoch (50 iterations)"),
@@ -225,7 +225,9 @@ def run_strategy(tr, wl, kind, args, world=1):
 
     w = WL[wl]
     n_global = w["workers"] * world
-    cfg = cluster.StrategyConfig(kind, n_global * w["per_worker"])
+    # the reference's perf-smoothing EMA (cluster.py:263-266) for a disturbance
+    # redrawn every epoch: the plan follows the mean speed, not last epoch's draw
+    cfg = cluster.StrategyConfig(kind, n_global * w["per_worker"], perf_smoothing=w.get("smoothing", 0.0))
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     extra = {"averaging_interval": w["avg"]} if w.get("avg") else {}
@@ -380,7 +382,8 @@ def disturbance_desc(wl):
     w = WL[wl]
     if w["mult"] is None:
         return ("workers 0 and 1: co-running spin kernels pin a fraction f ~ U(0.25, 0.6) of their SM partitions, "
-                "redrawn every epoch (seeded; cost_multiplier 1/(1-f))")
+                "redrawn every epoch (seeded; cost_multiplier 1/(1-f)); DBS plans with the reference's "
+                f"perf-smoothing EMA a = {w.get('smoothing', 0.0)}")
     if wl.startswith("resnet"):
         return (f"worker 0: a co-running spin kernel pins {1 - 1 / w['mult']:.0%} of its SM partition for every "
                 f"epoch (cost_multiplier {w['mult']})")
@@ -436,7 +439,7 @@ def e2e_run(tr, wl, X, y, args, world=1):
         tr.X.copy_(Xh.view(tr.X.shape), non_blocking=True)
         tr.y.copy_(yh, non_blocking=True)
 
-    cfg = cluster.StrategyConfig("dbs", w["workers"] * world * w["per_worker"])
+    cfg = cluster.StrategyConfig("dbs", w["workers"] * world * w["per_worker"], perf_smoothing=w.get("smoothing", 0.0))
     extra = {"averaging_interval": w["avg"]} if w.get("avg") else {}
     res = tr.run(cfg, n_epochs=args.warmup + args.steps, lr=w["lr"], momentum=w["mom"],
                  profiles=profiles(w["workers"] * world, w["mult"]), record_loss=True, timed_from=args.warmup,
