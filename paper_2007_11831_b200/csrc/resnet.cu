@@ -390,42 +390,53 @@ __global__ void iter_inc_kernel(int64_t* it) { *it += 1; }
 
 // 7x7 / stride-2 / pad-3 stem im2col: x uint8 [B][3][S][S] (CHW per sample;
 // pixel value (u - 128) / 64, exact in bf16) -> A bf16 [B*OS*OS][160],
-// K = (r, s, c) with c fastest, columns 147..159 zero.
-__global__ void im2col_stem7_kernel(const uint8_t* __restrict__ x_base, const int64_t* __restrict__ iter, int64_t B,
-                                    int S, uint16_t* __restrict__ out) {
+// K = (r, s, c) with c fastest, columns 147..159 zero.  One CTA per output
+// row: the 7 input rows it needs (x 3 channels, zero-padded to S + 6 columns)
+// are staged once in shared memory as floats, a K -> offset table replaces the
+// per-element index arithmetic, and consecutive threads write consecutive
+// 16-byte chunks of the output rows.
+__global__ void __launch_bounds__(256) im2col_stem7_kernel(const uint8_t* __restrict__ x_base,
+                                                           const int64_t* __restrict__ iter, int64_t B, int S,
+                                                           uint16_t* __restrict__ out) {
+  extern __shared__ float tile[];  // [3][7][S + 6]
+  __shared__ int koff[kStem7K];
+  constexpr int kChunks = kStem7K / 8;  // 20
+  const int SP = S + 6, OS = S / 2;
   const int64_t t = iter ? *iter : 0;
   const int64_t plane = (int64_t)S * S;
-  const uint8_t* x = x_base + t * B * 3 * plane;
-  const int OS = S / 2;
-  const int64_t total = B * OS * OS;
-  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < total;
-       pix += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t n = pix / ((int64_t)OS * OS);
-    const int rem = (int)(pix - n * OS * OS);
-    const int oh = rem / OS, ow = rem - (rem / OS) * OS;
-    const uint8_t* xs = x + n * 3 * plane;
-    uint4* o = reinterpret_cast<uint4*>(out + pix * kStem7K);
-    uint32_t acc[4] = {0, 0, 0, 0};
-    int k = 0;
-    for (int r = 0; r < 7; r++) {
-      const int hh = 2 * oh + r - 3;
-      for (int s = 0; s < 7; s++) {
-        const int ww = 2 * ow + s - 3;
-        const bool in = (hh >= 0 && hh < S && ww >= 0 && ww < S);
-#pragma unroll
-        for (int c = 0; c < 3; c++, k++) {
-          const float v = in ? ((float)xs[c * plane + (int64_t)hh * S + ww] - 128.0f) * 0.015625f : 0.0f;
-          acc[(k & 7) >> 1] |= (uint32_t)f2bf(v) << ((k & 1) * 16);
-          if ((k & 7) == 7) {
-            o[k >> 3] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
-            acc[0] = acc[1] = acc[2] = acc[3] = 0;
-          }
-        }
-      }
+  const int64_t n = blockIdx.x / OS;
+  const int oh = (int)(blockIdx.x - n * OS);
+  const uint8_t* xs = x_base + (t * B + n) * 3 * plane;
+  for (int k = threadIdx.x; k < kStem7K; k += blockDim.x) {
+    int o = -1;
+    if (k < 147) {
+      const int rs = k / 3, c = k - rs * 3;
+      const int r = rs / 7, sx = rs - r * 7;
+      o = (c * 7 + r) * SP + sx;
     }
-    // k == 147: flush the partial chunk, then zero chunks up to 160
-    o[k >> 3] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
-    for (int q = (k >> 3) + 1; q < kStem7K / 8; q++) o[q] = make_uint4(0, 0, 0, 0);
+    koff[k] = o;
+  }
+  for (int e = threadIdx.x; e < 3 * 7 * SP; e += blockDim.x) {
+    const int c = e / (7 * SP), rem = e - c * 7 * SP;
+    const int r = rem / SP, col = rem - r * SP;
+    const int hh = 2 * oh + r - 3, ww = col - 3;
+    float v = 0.0f;
+    if (hh >= 0 && hh < S && ww >= 0 && ww < S) v = ((float)xs[c * plane + (int64_t)hh * S + ww] - 128.0f) * 0.015625f;
+    tile[e] = v;
+  }
+  __syncthreads();
+  uint4* o4 = reinterpret_cast<uint4*>(out) + (int64_t)blockIdx.x * OS * kChunks;
+  for (int i = threadIdx.x; i < OS * kChunks; i += blockDim.x) {
+    const int px = i / kChunks, ch = i - (i / kChunks) * kChunks;
+    const float* base = tile + 2 * px;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int o = koff[ch * 8 + e];
+      v[e] = o >= 0 ? base[o] : 0.0f;
+    }
+    o4[i] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                       pack_bf16x2(v[6], v[7]));
   }
 }
 
@@ -1095,7 +1106,8 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
   // ---------------- stem: 7x7/2 conv (explicit im2col) + BN + ReLU + 3x3/2 max-pool ----------------
   const Conv& sc = m->convs[m->stem];
-  im2col_stem7_kernel<<<grid_for(B * sc.OH * sc.OW, 128), 128, 0, s>>>(x_base, d_iter, B, m->image, m->stem_cols);
+  im2col_stem7_kernel<<<(unsigned)(B * sc.OH), 256, (size_t)3 * 7 * (m->image + 6) * sizeof(float), s>>>(
+      x_base, d_iter, B, m->image, m->stem_cols);
   DBS_LAUNCH_CHECK();
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;

@@ -15,6 +15,19 @@ def summarize(prof, title):
     print(f"== {title}: total kernel time {tot/1e3:.2f} ms")
     for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
         print(f"{t/1e3:9.3f} ms {c:6d}x  {k}")
+if mode == "single50":
+    B = 64
+    m = resnet.ResnetModel(1000, seed=0, depth=50, image=224); sc = resnet.ResnetScratch(B, 1000, depth=50, image=224)
+    X, y = resnet.synthetic_imagenet(B, 224, 1000, seed=0)
+    x = torch.as_tensor(X, device="cuda"); yl = torch.as_tensor(y, device="cuda")
+    g = torch.zeros(m.P, device="cuda"); loss = torch.zeros(1, device="cuda")
+    for _ in range(3): resnet.forward_backward(m, sc, x, yl, g, loss)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(2): resnet.forward_backward(m, sc, x, yl, g, loss)
+        torch.cuda.synchronize()
+    summarize(prof, "ResNet-50 single worker B=64 x2")
+    sys.exit(0)
 if mode == "single":
     B = 128
     m = resnet.ResnetModel(seed=0); sc = resnet.ResnetScratch(B)
