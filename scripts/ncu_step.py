@@ -1,5 +1,6 @@
 """ncu target: warm-up + ONE ResNet-18 worker forward/backward (b=128), or the 64->64 conv alone."""
 import sys, torch
+sys.path.insert(0, ".")
 from paper_2007_11831_b200 import resnet, _lib
 what = sys.argv[1] if len(sys.argv) > 1 else "step"
 if what == "conv":
