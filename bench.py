@@ -240,6 +240,11 @@ def run_strategy(tr, wl, kind, args, world=1):
             "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
+# measured tcgen05.mma (SS, bf16, M=128, K=16) throughput by N tile, as a share of the
+# tensor peak (scripts/mma_bench.cu -> profiles/mma_rate_r1.txt): a single-CTA MMA takes
+# >= ~95 cycles whatever N is, so only N = 256 reaches the peak
+MMA_SHAPE_CEILING = {64: 0.34, 128: 0.67, 256: 1.0}
+
 ROOFLINE_CONV = {
     # workload -> (N, H, Cin, Cout, k, stride, description): the dominant conv shape
     "resnet18": (128, 32, 64, 64, 3, 1, "gemm_bf16_kernel<64> implicit-GEMM conv3x3 64->64 @32x32, b=128 "
@@ -297,8 +302,11 @@ def kernel_roofline(peaks, wl="resnet18"):
         rec = json.loads(tf.read_text()).get(wl if wl in ROOFLINE_CONV else "resnet18")
         if rec:
             traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
+    n_tile = 64 if Co <= 64 else (128 if Co <= 128 else 256)
+    ceiling = MMA_SHAPE_CEILING[n_tile]
     return {"bound": "tensor", "kernel": desc,
             "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+            "mma_shape_ceiling_frac": ceiling, "frac_of_shape_ceiling": round(achieved / peak / ceiling, 4),
             "traffic": traffic, "traffic_unit": "bytes per launch (ncu, profiles/ncu_traffic_r1.json)",
             "algorithmic_bytes_per_launch": 2.0 * (N * H * H * C + N * OH * OH * Co + Co * k * k * C),
             "avg_launch_us": round(dur * 1e6, 2), "algorithmic_flops_per_launch": flops,
