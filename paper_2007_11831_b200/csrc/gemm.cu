@@ -49,7 +49,7 @@ using namespace sm100;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
-constexpr int kThreads = 224;  // producer warp, MMA warp, 4 epilogue warps, halo fix-up warp
+constexpr int kThreads = 192;  // producer warp, MMA warp, 4 epilogue warps
 
 // Development-only timeline probe (-DDBS_GEMM_TRACE, scripts/gemm_trace.cu):
 // per-CTA clock64 stamps of the producer / MMA / epilogue hand-offs.
@@ -385,8 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + kStages;  // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2;    // [2] epilogue -> MMA
   uint64_t* bres_full = acc_empty + 2;   // resident filter landed (halo)
-  uint64_t* ready = bres_full + 1;       // [kStages] halo slot fixed up (halo)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + kStages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GEMM_TRACE(0);
@@ -420,7 +419,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
     }
     mbar_init(bres_full, 1);
-    for (int s = 0; s < kStages; s++) mbar_init(&ready[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -792,8 +790,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     }
     __syncwarp();
-  } else if (warp == 6) {
-    // (idle: the padded halo needs no shared-memory fix-up)
   } else {
   // ---------------- epilogue (warps 2..5) ----------------
   const int q = warp & 3;  // the TMEM lane quadrant this warp may access
