@@ -355,7 +355,7 @@ def aux_rooflines(tr, peaks):
     out = {}
     D, rb = tr.D, tr.row_bytes
     perm = torch.randperm(D, device=tr.dev)
-    dst = tr.shard_x[0]
+    dst = torch.empty_like(tr.X)  # the dataset's own row format (MLP shards hold bf16 rows)
 
     def gather(st):
         assert L.dbs_dev_gather_rows(tr.X.data_ptr(), perm.data_ptr(), D, rb, dst.data_ptr(), st) == 0, _lib.last_error()
