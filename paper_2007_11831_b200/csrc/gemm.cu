@@ -956,6 +956,223 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Halo conv on a CTA pair (forward, 3x3 / stride 1 / 64 -> 64): one
+// tcgen05.mma.cta_group::2 (M = 256) covers the same 128-position tile of two
+// images, one per CTA.  A single-CTA 128x64x16 MMA is capped at ~34% of the
+// tensor peak by its ~95-cycle issue cost; the pair instruction (45 cycles for
+// 256x64x16) reaches ~70% (profiles/mma_rate_r1.txt).  Pairing images (not
+// neighbouring tiles) keeps both CTAs' halo slots at the same row shift, which
+// the shared A descriptor needs.  Each CTA loads its own image's halo and half
+// of the filter (output channels 32 r .. 32 r + 31, the N split of a pair MMA);
+// the loads complete on the leader's barriers (mapa), the leader issues every
+// MMA and multicasts its commits to both CTAs, and both epilogues drain their
+// own 128 accumulator rows and arrive on the leader's acc_empty.
+// ---------------------------------------------------------------------------
+struct Halo2Cfg {
+  static constexpr uint32_t kSlotBytes = 44 * 1024;
+  static constexpr uint32_t kTapBytes = 32 * 128;  // this CTA's 32 output channels of one tap
+  static constexpr uint32_t kBResBytes = 9 * kTapBytes;
+  static constexpr int kStages = 3;
+  static constexpr uint32_t kAccCols = 64;
+  static constexpr uint32_t kTmemCols = 128;
+  static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kSlotBytes + kBResBytes + kEpiBytes + 256;
+  static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    halo_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  using H = Halo2Cfg;
+  constexpr int kStages = H::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * H::kSlotBytes;
+  float* sEpi = reinterpret_cast<float*>(sB + H::kBResBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + H::kEpiBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bres_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GEMM_TRACE(0);
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = (crank == 0);
+  const ConvGeom& g = p.ga;
+  const int W1 = g.OW + 1;
+  const int64_t num_pairs = p.halo_tiles;
+  const int64_t pair0 = blockIdx.x >> 1, pair_step = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // 4 epilogue warps x 2 CTAs (the leader's copy is used)
+    }
+    mbar_init(bres_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<H::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / TMA completion
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_TRACE(1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs; completions on the leader) ----------------
+      const uint32_t bres_cl = map_to_rank(smem_u32(bres_full), 0);
+      if (leader) mbar_arrive_expect_tx(bres_full, 2 * H::kBResBytes);
+      for (int tap = 0; tap < 9; tap++) tma_load_2d_cl(sB + tap * H::kTapBytes, &tmB, bres_cl, tap * 64, 32 * (int)crank);
+      const uint32_t halo_bytes = (uint32_t)(p.halo_rows * W1) * 128u;
+      uint32_t it = 0;
+      for (int64_t q = pair0; q < num_pairs; q += pair_step, it++) {
+        const int img = (int)(q / p.halo_tpi) * 2 + (int)crank;
+        const int P0 = (int)(q - (q / p.halo_tpi) * p.halo_tpi) * kBM;
+        const int s = (int)(it % kStages);
+        mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+        if (it < 10) GEMM_TRACE(2 + it);
+        if (leader) mbar_arrive_expect_tx(&full[s], 2 * halo_bytes);
+        tma_load_4d_cl(sA + s * H::kSlotBytes, &tmA, map_to_rank(smem_u32(&full[s]), 0), 0, -1, P0 / W1 - 1, img);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader only) ----------------
+      const uint32_t idesc = make_idesc_bf16(256, 64, 0, 0);
+      const uint64_t a_desc0 = make_sdesc(smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = make_sdesc(smem_u32(sB), 16, 1024);
+      mbar_wait(bres_full, 0);
+      tc_fence_after();
+      uint32_t it = 0, j = 0;
+      for (int64_t q = pair0; q < num_pairs; q += pair_step, it++, j++) {
+        const int b = (int)(j & 1);
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (j < 10) GEMM_TRACE(12 + j);
+        const int s = (int)(it % kStages);
+        mbar_wait(&full[s], (it / kStages) & 1);
+        tc_fence_after();
+        if (j < 8) GEMM_TRACE(96 + 3 * j);
+        const int off = ((int)(q - (q / p.halo_tpi) * p.halo_tpi) * kBM) % W1;
+        const uint64_t a_slot = a_desc0 + (uint64_t)((s * H::kSlotBytes) >> 4);
+        const uint32_t d_tmem = tmem_base + b * H::kAccCols;
+#pragma unroll
+        for (int r = 0; r < 3; r++) {
+#pragma unroll
+          for (int sx = 0; sx < 3; sx++) {
+            const uint64_t a_t = a_slot + (uint64_t)((off + r * W1 + sx) * 8);
+            const uint64_t b_t = b_desc0 + (uint64_t)((r * 3 + sx) * (H::kTapBytes >> 4));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; k++)
+              mma_bf16_ss_pair(d_tmem, a_t + (uint64_t)(k * 2), b_t + (uint64_t)(k * 2), idesc,
+                               (r | sx | k) != 0 ? 1u : 0u);
+          }
+        }
+        mma_commit_pair(&empty[s], (uint16_t)3);
+        mma_commit_pair(&acc_full[b], (uint16_t)3);
+        if (j < 10) GEMM_TRACE(22 + j);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 2..5 of both CTAs: their own 128 rows) ----------------
+    const int qd = warp & 3;
+    float* tr = sEpi + (warp - 2) * (32 * 33);
+    const uint32_t acc_empty_cl0 = map_to_rank(smem_u32(&acc_empty[0]), 0);
+    const uint32_t acc_empty_cl1 = map_to_rank(smem_u32(&acc_empty[1]), 0);
+    const bool stats = (p.sum_part != nullptr);
+    const int n_img = (int)(p.M / ((int64_t)g.OH * g.OW));
+    uint32_t tj = 0;
+    for (int64_t q = pair0; q < num_pairs; q += pair_step, tj++) {
+      const int b = (int)(tj & 1);
+      mbar_wait(&acc_full[b], (tj >> 1) & 1);
+      tc_fence_after();
+      if (warp == 2 && lane == 0 && tj < 10) GEMM_TRACE(32 + tj);
+      const int img = (int)(q / p.halo_tpi) * 2 + (int)crank;
+      const int P = (int)(q - (q / p.halo_tpi) * p.halo_tpi) * kBM + qd * 32 + lane;
+      const int h = P / W1, w = P - (P / W1) * W1;
+      const bool valid = (w < g.OW) && (h < g.OH) && (img < n_img);
+      const int64_t orow = ((int64_t)img * g.OH + h) * g.OW + w;
+      const uint32_t lane_addr = tmem_base + b * H::kAccCols + ((uint32_t)(qd * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < 2; c++) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(lane_addr + c * 32, r);
+        tmem_ld_wait();
+        if (c == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(b ? acc_empty_cl1 : acc_empty_cl0);
+          if (warp == 2 && lane == 0 && tj < 10) GEMM_TRACE(42 + tj);
+        }
+        const int n_base = c * 32;
+        if (stats) {
+          __shared__ float red_s2[4][32], red_q2[4][32];
+#pragma unroll
+          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = valid ? __uint_as_float(r[k]) : 0.0f;
+          __syncwarp();
+          float s1 = 0.f, sq = 0.f;
+#pragma unroll
+          for (int r2 = 0; r2 < 32; r2++) {
+            const float e = tr[r2 * 33 + lane];
+            s1 += e;
+            sq = fmaf(e, e, sq);
+          }
+          __syncwarp();
+          red_s2[qd][lane] = s1;
+          red_q2[qd][lane] = sq;
+          epilogue_bar();
+          if (warp == 2) {
+            const double ts = (double)red_s2[0][lane] + red_s2[1][lane] + red_s2[2][lane] + red_s2[3][lane];
+            const double tq = (double)red_q2[0][lane] + red_q2[1][lane] + red_q2[2][lane] + red_q2[3][lane];
+            atomicAdd(p.sum_part + n_base + lane, ts);
+            atomicAdd(p.sq_part + n_base + lane, tq);
+          }
+          epilogue_bar();
+        }
+        // bf16 tile staged through shared memory, 8 rows x 64 contiguous bytes per store
+        uint32_t* st = reinterpret_cast<uint32_t*>(tr);
+        __syncwarp();
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++)
+          *reinterpret_cast<uint4*>(st + lane * 20 + 4 * jj) = make_uint4(
+              pack_bf16x2(__uint_as_float(r[8 * jj]), __uint_as_float(r[8 * jj + 1])),
+              pack_bf16x2(__uint_as_float(r[8 * jj + 2]), __uint_as_float(r[8 * jj + 3])),
+              pack_bf16x2(__uint_as_float(r[8 * jj + 4]), __uint_as_float(r[8 * jj + 5])),
+              pack_bf16x2(__uint_as_float(r[8 * jj + 6]), __uint_as_float(r[8 * jj + 7])));
+        __syncwarp();
+        uint16_t* dbase = reinterpret_cast<uint16_t*>(p.d) + n_base + (lane & 3) * 8;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int rr = 8 * i + (lane >> 2);
+          const int64_t orow_r = __shfl_sync(0xffffffffu, orow, rr);
+          const int valid_r = __shfl_sync(0xffffffffu, (int)valid, rr);
+          if (valid_r)
+            *reinterpret_cast<uint4*>(dbase + orow_r * p.ldd) =
+                *reinterpret_cast<const uint4*>(st + rr * 20 + (lane & 3) * 4);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (threadIdx.x == 64) GEMM_TRACE(52);
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while its peer may still signal it
+  if (threadIdx.x == 0) GEMM_TRACE(63);
+  if (warp == 1) tmem_dealloc_pair<H::kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
 // host: tensor-map encoding through the driver entry point (no -lcuda needed)
 // ---------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1185,6 +1402,50 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   return DBS_OK;
 }
 
+// Experimental, off by default (DBS_HALO_PAIR=1 enables it): correct (same parity
+// tests), but measured no faster than the single-CTA halo kernel -- with streamed,
+// row-shifted operands the pair instruction takes ~86 cycles, so per-SM MMA time
+// per tile is unchanged (profiles/ncu_conv_r1_summary.md) -- and a cluster launch
+// inside a worker's SM partition competes with the co-running disturbance kernel.
+bool halo_pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_HALO_PAIR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// the CTA-pair halo kernel: clusters of 2, persistent over image-pair tiles
+int launch_halo_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t s) {
+  constexpr size_t kSmem = Halo2Cfg::kSmem;
+  static thread_local void* seen[16] = {nullptr};
+  static thread_local int nseen = 0;
+  void* ctx = current_ctx();
+  bool known = false;
+  for (int i = 0; i < nseen; i++) known |= (seen[i] == ctx);
+  if (!known) {
+    DBS_CUDA_TRY(cudaFuncSetAttribute(halo_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    if (nseen < 16) seen[nseen++] = ctx;
+  }
+  const int64_t clusters_max = current_sm_count() / 2;
+  const int64_t clusters = p.halo_tiles < clusters_max ? p.halo_tiles : clusters_max;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * (clusters > 0 ? clusters : 1)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DBS_CUDA_TRY(cudaLaunchKernelEx(&cfg, halo_pair_kernel, ta, tb, p));
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
 int pick_bn(int64_t N, int b_mode) {
   if (N <= 16 && b_mode == 0) return 16;
   if (N <= 64) return 64;
@@ -1219,6 +1480,7 @@ int preload_gemm() {
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<256>::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(halo_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Halo2Cfg::kSmem));
   return DBS_OK;
 }
 
@@ -1323,6 +1585,18 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     p.halo_tiles = (int64_t)c.ta.N * p.halo_tpi;
     st = make_tmap_nhwc(&ta, c.a, c.ta, W1, p.halo_rows, 1, 1);
     if (st) return st;
+    if (c.b_mode == 0 && halo_pair_enabled() && current_sm_count() >= 2 &&
+        (uint32_t)(p.halo_rows * W1) * 128u <= Halo2Cfg::kSlotBytes) {
+      // CTA pair: image 2k + rank, both CTAs at the same tile; half the filter rows each
+      st = make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, 32);
+      if (st) return st;
+      p.halo_tiles = ((int64_t)(c.ta.N + 1) / 2) * p.halo_tpi;
+      p.a_mode = 2;
+      p.b_mode = 0;
+      p.ga = g;
+      p.kb_per_split = 9;
+      return launch_halo_pair(ta, tb, p, s);
+    }
     if (c.b_mode == 0) {
       st = make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, 64);
       if (st) return st;

@@ -1,5 +1,6 @@
 // Dev probe: tcgen05.mma (kind::f16, SS operands, cta_group::1) issue rate per SM
-// for M = 128 and N = 64 / 128 / 256, with operands resident in shared memory.
+// for M = 128 and N = 64 / 128 / 256, with operands resident in shared memory;
+// variant 0: one fixed A tile, 1: A start shifted by one 128-byte row, 2: A cycling over 8 aligned tiles.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2007_11831_b200/csrc \
 //        scripts/mma_bench.cu -o scripts/_bin/mma_bench
 #include <cuda_runtime.h>
@@ -16,7 +17,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int reps, int variant, unsi
   __shared__ uint64_t done, side[8];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < (128 + N) * 64 * 2 / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < (192 + N) * 64 * 2 / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     mbar_init(&done, 1);
@@ -30,22 +31,16 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int reps, int variant, unsi
   tc_fence_after();
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
-    const uint32_t a_base = smem_u32(sm), b_base = smem_u32(sm + 128 * 128);
+    const uint32_t a_base = smem_u32(sm), b_base = smem_u32(sm + 192 * 128);
     const uint32_t idesc = make_idesc_bf16(M, N, 0, 0);
     const long long t0 = clock64();
     for (int i = 0; i < reps; i++) {
 #pragma unroll
       for (int k = 0; k < 4; k++) {
-        const uint64_t ad = make_sdesc(a_base + k * 32, 16, 1024);
+        const uint32_t a_off = variant == 1 ? 128u : (variant == 2 ? (uint32_t)((i & 7) * 1024) : 0u);
+        const uint64_t ad = make_sdesc(a_base + a_off + k * 32, 16, 1024);
         const uint64_t bd = make_sdesc(b_base + k * 32, 16, 1024);
         mma_bf16_ss(tmem, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
-      }
-      if (variant >= 1 && (i % 3) == 2) mma_commit(&side[(i / 3) & 7]);  // a commit per 12 MMAs
-      if (variant >= 2 && (i % 3) == 2 && i >= 24) {
-        // wait for the commit 8 groups back (the ring depth) + fence, as the GEMM does
-        const int g = i / 3 - 8;
-        mbar_wait(&side[g & 7], (g >> 3) & 1);
-        tc_fence_after();
       }
     }
     mma_commit(&done);
@@ -62,7 +57,7 @@ template <int N, int M = 128>
 void run(int grid, int variant) {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 1024);
-  const int smem = (128 + N) * 128 + 1024;
+  const int smem = (192 + N) * 128 + 1024;
   cudaFuncSetAttribute(mma_kernel<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int reps = 2000;
   mma_kernel<N, M><<<grid, 128, smem>>>(reps, variant, d);
@@ -81,10 +76,10 @@ void run(int grid, int variant) {
 
 int main(int argc, char** argv) {
   const int grid = argc > 1 ? atoi(argv[1]) : 148;
-  run<64>(grid, 0);
-  run<128>(grid, 0);
-  run<256>(grid, 0);
-  run<256, 64>(grid, 0);
-  run<128, 64>(grid, 0);
+  for (int v = 0; v < 3; v++) {
+    run<64>(grid, v);
+    run<128>(grid, v);
+    run<256>(grid, v);
+  }
   return 0;
 }

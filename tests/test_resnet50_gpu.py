@@ -200,3 +200,14 @@ def test_resnet50_trainer_first_iteration(dev, graphs):
         resnet.forward_backward(ref, sc, x, yl, grad, loss)
         torch.cuda.synchronize()
         assert float(tr.loss_buf[w, 0]) == pytest.approx(float(loss), rel=1e-3, abs=1e-4)
+
+
+def test_conv_halo_cta_pair_path(dev):
+    """The experimental CTA-pair halo kernel (DBS_HALO_PAIR=1, read once per process:
+    run in a child) on the 64->64 conv shapes and the ResNet-50 network test."""
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBS_HALO_PAIR="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        str(root / "tests" / "test_resnet50_gpu.py"), "-k", "im2col_shapes or forward_backward"],
+                       env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
