@@ -34,7 +34,6 @@ namespace {
 constexpr float kBnEps = 1e-5f;
 constexpr int kStemK = 32;     // ResNet-18 stem: 27 = 3x3x3 padded to 32
 constexpr int kStem7K = 160;   // ResNet-50 stem: 147 = 7x7x3 padded to 160 (K blocks past 160 are TMA zero fill)
-constexpr int kMaxC = 2048;    // widest BatchNorm (ResNet-50 layer 4)
 
 __device__ __forceinline__ uint16_t f2bf(float f) {
   uint32_t u = __float_as_uint(f);
@@ -87,22 +86,6 @@ __global__ void im2col_stem_kernel(const float* __restrict__ x_base, const int64
   }
 }
 
-// BN batch statistics: the conv epilogue's fp64 column sums -> mean,
-// 1/sqrt(var+eps); the accumulators are re-zeroed for the next convolution.
-__global__ void bn_stats_kernel(double* __restrict__ sum_acc, double* __restrict__ sq_acc, int C, int64_t M,
-                                float* __restrict__ mean, float* __restrict__ invstd) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const double s = sum_acc[c], q = sq_acc[c];
-  sum_acc[c] = 0.0;
-  sq_acc[c] = 0.0;
-  const double mu = s / (double)M;
-  double var = q / (double)M - mu * mu;
-  if (var < 0.0) var = 0.0;
-  mean[c] = (float)mu;
-  invstd[c] = (float)(1.0 / sqrt(var + (double)kBnEps));
-}
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -127,22 +110,44 @@ __device__ __forceinline__ void coef8(const float* t, int c0, float (&k)[8]) {
 // out = act( a*y + b  [+ res | + a_d*yd + b_d] ), a = gamma*invstd, b = beta - mean*a:
 // the per-channel affine maps are formed once per CTA in shared memory; 8
 // channels (one 16-byte vector) per thread and trip
-__global__ void __launch_bounds__(256) bn_apply_kernel(const uint16_t* __restrict__ y, const float* __restrict__ mean,
-                                const float* __restrict__ invstd, const float* __restrict__ gamma,
+__device__ __forceinline__ void bn_finalise(const double* acc, int C, int c, int64_t M, float& mean, float& invstd) {
+  const double mu = acc[c] / (double)M;
+  double var = acc[C + c] / (double)M - mu * mu;
+  if (var < 0.0) var = 0.0;
+  mean = (float)mu;
+  invstd = (float)(1.0 / sqrt(var + (double)kBnEps));
+}
+
+__global__ void __launch_bounds__(256) bn_apply_kernel(const uint16_t* __restrict__ y, const double* __restrict__ acc,
+                                float* __restrict__ mean, float* __restrict__ invstd, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, const uint16_t* __restrict__ res,
-                                const uint16_t* __restrict__ yd, const float* __restrict__ mean_d,
-                                const float* __restrict__ invstd_d, const float* __restrict__ gamma_d,
-                                const float* __restrict__ beta_d, int relu, int C, int64_t M,
-                                uint16_t* __restrict__ out) {
+                                const uint16_t* __restrict__ yd, const double* __restrict__ acc_d,
+                                float* __restrict__ mean_d, float* __restrict__ invstd_d,
+                                const float* __restrict__ gamma_d, const float* __restrict__ beta_d, int relu, int C,
+                                int64_t M, uint16_t* __restrict__ out) {
+  // the conv epilogue's fp64 column sums -> mean, 1/sqrt(var + eps) (every CTA
+  // forms them for its table; CTA 0 also publishes them for the backward pass)
   extern __shared__ float tab[];  // [C] a, [C] b, ([C] a_d, [C] b_d)
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const float a = gamma[c] * invstd[c];
+    float mu, is;
+    bn_finalise(acc, C, c, M, mu, is);
+    const float a = gamma[c] * is;
     tab[c] = a;
-    tab[C + c] = beta[c] - mean[c] * a;
+    tab[C + c] = beta[c] - mu * a;
+    if (blockIdx.x == 0) {
+      mean[c] = mu;
+      invstd[c] = is;
+    }
     if (yd) {
-      const float ad = gamma_d[c] * invstd_d[c];
+      float mud, isd;
+      bn_finalise(acc_d, C, c, M, mud, isd);
+      const float ad = gamma_d[c] * isd;
       tab[2 * C + c] = ad;
-      tab[3 * C + c] = beta_d[c] - mean_d[c] * ad;
+      tab[3 * C + c] = beta_d[c] - mud * ad;
+      if (blockIdx.x == 0) {
+        mean_d[c] = mud;
+        invstd_d[c] = isd;
+      }
     }
   }
   __syncthreads();
@@ -671,8 +676,9 @@ struct dbs_resnet {
   std::vector<uint16_t*> y, a;             // per conv: pre-BN output, post-BN(+ReLU) output
   std::vector<uint16_t*> blk_out;          // per block output (post residual ReLU)
   std::vector<float*> mean, invstd;        // per conv
-  double* sum_part = nullptr;              // [512] fp64 BN sum accumulators (kept zeroed)
-  double* sq_part = nullptr;               // [512] sum of squares
+  double* stats_acc = nullptr;             // per conv: [cout] fp64 sums + [cout] sums of squares (BN statistics)
+  std::vector<int64_t> stats_off;          // offset of each conv's accumulators in stats_acc
+  int64_t stats_len = 0;
   uint16_t* g0 = nullptr;                  // gradient ping-pong buffers (largest activation)
   uint16_t* g1 = nullptr;
   uint16_t* g2 = nullptr;
@@ -834,10 +840,13 @@ int alloc_all(dbs_resnet* m) {
     A((void**)&o, (size_t)B * c.OH * c.OW * c.cout * 2);
     m->blk_out.push_back(o);
   }
-  A((void**)&m->sum_part, kMaxC * sizeof(double));
-  A((void**)&m->sq_part, kMaxC * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(m->sum_part, 0, kMaxC * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(m->sq_part, 0, kMaxC * sizeof(double));
+  m->stats_off.clear();
+  m->stats_len = 0;
+  for (auto& c : m->convs) {
+    m->stats_off.push_back(m->stats_len);
+    m->stats_len += 2 * (int64_t)c.cout;
+  }
+  A((void**)&m->stats_acc, (size_t)m->stats_len * sizeof(double));
   A((void**)&m->g0, max_act * 2);
   A((void**)&m->g1, max_act * 2);
   A((void**)&m->g2, max_act * 2);
@@ -889,8 +898,8 @@ int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64
   call.epi = DBS_EPI_BF16;
   call.d = m->y[ci];
   call.ldd = c.cout;
-  call.sum_part = m->sum_part;
-  call.sq_part = m->sq_part;
+  call.sum_part = m->stats_acc + m->stats_off[ci];
+  call.sq_part = m->stats_acc + m->stats_off[ci] + c.cout;
   call.b = wb + c.w_off;
   call.b_mode = 0;
   if (c.cin == 3) {  // stem: explicit im2col columns [M][stem_k]
@@ -916,10 +925,7 @@ int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64
   }
   int st = conv_gemm(call, s);
   if (st) return st;
-  bn_stats_kernel<<<(c.cout + 127) / 128, 128, 0, s>>>(m->sum_part, m->sq_part, c.cout, M, m->mean[ci],
-                                                        m->invstd[ci]);
-  DBS_LAUNCH_CHECK();
-  return DBS_OK;
+  return DBS_OK;  // batch statistics are finalised by the BN apply kernel (bn_apply_kernel)
 }
 
 int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds, int relu, int64_t B,
@@ -929,8 +935,9 @@ int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds
   const int64_t total = M * (c.cout / 8);
   const Conv* d = ds >= 0 ? &m->convs[ds] : nullptr;
   bn_apply_kernel<<<grid_for(total, 256), 256, (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s>>>(
-      m->y[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res, d ? m->y[ds] : nullptr,
-      d ? m->mean[ds] : nullptr, d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
+      m->y[ci], m->stats_acc + m->stats_off[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res,
+      d ? m->y[ds] : nullptr, d ? m->stats_acc + m->stats_off[ds] : nullptr, d ? m->mean[ds] : nullptr,
+      d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
       d ? pf + d->b_off : nullptr, relu, c.cout, M, out);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
@@ -1104,6 +1111,7 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
                      cudaStream_t s) {
   int st;
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
+  DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- stem: 7x7/2 conv (explicit im2col) + BN + ReLU + 3x3/2 max-pool ----------------
   const Conv& sc = m->convs[m->stem];
   im2col_stem7_kernel<<<(unsigned)(B * sc.OH), 256, (size_t)3 * 7 * (m->image + 6) * sizeof(float), s>>>(
@@ -1207,6 +1215,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
   const float* x_base = static_cast<const float*>(x_any);
   int st;
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
+  DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- forward ----------------
   im2col_stem_kernel<<<grid_for(B * 1024, 256), 256, 0, s>>>(x_base, d_iter, B, m->stem_cols);
   DBS_LAUNCH_CHECK();
@@ -1342,8 +1351,7 @@ extern "C" int dbs_resnet_destroy(dbs_resnet* m) {
   for (auto p : m->blk_out) cudaFree(p);
   for (auto p : m->mean) cudaFree(p);
   for (auto p : m->invstd) cudaFree(p);
-  cudaFree(m->sum_part);
-  cudaFree(m->sq_part);
+  cudaFree(m->stats_acc);
   cudaFree(m->g0);
   cudaFree(m->g1);
   cudaFree(m->g2);
