@@ -26,6 +26,32 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // every kernel launch of the library goes through this check, which also counts it
 void count_launch();
+
+// Programmatic dependent launch: the kernel may start (prologue: barriers, TMEM,
+// shared-memory tables) while its predecessor on the stream drains; it calls
+// pdl_wait() before touching memory the predecessor produces or consumes
+// (griddepcontrol.wait returns once the predecessor grid has completed and its
+// writes are visible -- a no-op for a launch without the attribute).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+// let the next PDL launch on the stream begin its prologue, then wait for ours
+__device__ __forceinline__ void pdl_trigger_and_wait() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 #define DBS_LAUNCH_CHECK()     \
   do {                         \
     ::dbs::count_launch();     \

@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above overlapped the previous kernel's tail; operands and outputs only from here
+  pdl_trigger_and_wait();
   if (threadIdx.x == 0) GEMM_TRACE(1);
 
   if (warp == 0) {
@@ -1397,7 +1399,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   const int64_t tiles = kHalo ? p.halo_tiles : ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
   const int64_t sms = current_sm_count();
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  gemm_bf16_kernel<BN, kHalo><<<grid, kThreads, kSmem, s>>>(ta, tb, q);
+  DBS_CUDA_TRY(launch_pdl(gemm_bf16_kernel<BN, kHalo>, dim3(grid), dim3(kThreads), kSmem, s, ta, tb, q));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }

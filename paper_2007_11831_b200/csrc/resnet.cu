@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const uint16_t* __restric
                                 float* __restrict__ mean_d, float* __restrict__ invstd_d,
                                 const float* __restrict__ gamma_d, const float* __restrict__ beta_d, int relu, int C,
                                 int64_t M, uint16_t* __restrict__ out) {
+  pdl_trigger_and_wait();
   // the conv epilogue's fp64 column sums -> mean, 1/sqrt(var + eps) (every CTA
   // forms them for its table; CTA 0 also publishes them for the backward pass)
   extern __shared__ float tab[];  // [C] a, [C] b, ([C] a_d, [C] b_d)
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __re
                                                             const float* __restrict__ mean,
                                                             const float* __restrict__ invstd, int C, int64_t M,
                                                             float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  pdl_trigger_and_wait();
   // each thread owns 8 channels (c0 = 8 * (tid % cv)) over rows tid / cv, +rows_per_pass
   __shared__ float red_g[2048], red_b[2048];
   const int cv = C / 8;
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const uint16_t* __res
                                     const float* __restrict__ invstd, const float* __restrict__ gamma,
                                     const float* __restrict__ dgamma, const float* __restrict__ dbeta, int C,
                                     int64_t M, uint16_t* __restrict__ dy, uint16_t* __restrict__ g_out) {
+  pdl_trigger_and_wait();
   extern __shared__ float tab[];  // [C] k1, [C] k2, [C] k3
   const float invM = 1.0f / (float)M;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -934,11 +937,12 @@ int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds
   const int64_t M = B * c.OH * c.OW;
   const int64_t total = M * (c.cout / 8);
   const Conv* d = ds >= 0 ? &m->convs[ds] : nullptr;
-  bn_apply_kernel<<<grid_for(total, 256), 256, (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s>>>(
+  DBS_CUDA_TRY(launch_pdl(
+      bn_apply_kernel, dim3(grid_for(total, 256)), dim3(256), (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s,
       m->y[ci], m->stats_acc + m->stats_off[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res,
       d ? m->y[ds] : nullptr, d ? m->stats_acc + m->stats_off[ds] : nullptr, d ? m->mean[ds] : nullptr,
       d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
-      d ? pf + d->b_off : nullptr, relu, c.cout, M, out);
+      d ? pf + d->b_off : nullptr, relu, c.cout, M, out));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -953,13 +957,13 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
   int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread (one trip)
   if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   if (blocks < 1) blocks = 1;
-  bn_bwd_reduce_kernel<8><<<blocks, 256, 0, s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci], c.cout, M,
-                                                  grad + c.g_off, grad + c.b_off);
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_kernel<8>, dim3(blocks), dim3(256), 0, s, gin, mask, m->y[ci], m->mean[ci],
+                          m->invstd[ci], c.cout, M, grad + c.g_off, grad + c.b_off));
   DBS_LAUNCH_CHECK();
   const int64_t total = M * cv;
-  bn_bwd_apply_kernel<<<grid_for(total, 256), 256, (size_t)3 * c.cout * sizeof(float), s>>>(gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
-                                                            pf + c.g_off, grad + c.g_off, grad + c.b_off, c.cout, M,
-                                                            dy, g_out);
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_kernel, dim3(grid_for(total, 256)), dim3(256),
+                          (size_t)3 * c.cout * sizeof(float), s, gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
+                          pf + c.g_off, grad + c.g_off, grad + c.b_off, c.cout, M, dy, g_out));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
