@@ -58,6 +58,7 @@ struct Block {
 // t*B .. ) -> A bf16 [B*1024][32], K = (r, s, c) with c fastest, zero padded.
 __global__ void im2col_stem_kernel(const float* __restrict__ x_base, const int64_t* __restrict__ iter, int64_t B,
                                    uint16_t* __restrict__ out) {
+  pdl_trigger_and_wait();
   const int64_t t = iter ? *iter : 0;
   const float* x = x_base + t * B * 3072;
   const int64_t total = B * 1024;
@@ -326,6 +327,7 @@ __global__ void __launch_bounds__(256) head_kernel(const uint16_t* __restrict__ 
                                                    const int64_t* __restrict__ iter, int64_t B, int classes,
                                                    float* __restrict__ feat, float* __restrict__ dlog,
                                                    float* __restrict__ loss_per, uint16_t* __restrict__ dout) {
+  pdl_trigger_and_wait();
   __shared__ float f[512];
   __shared__ float logit[16];
   const int64_t n = blockIdx.x;
@@ -373,6 +375,7 @@ __global__ void __launch_bounds__(256) head_kernel(const uint16_t* __restrict__ 
 __global__ void head_wgrad_kernel(const float* __restrict__ feat, const float* __restrict__ dlog,
                                   const float* __restrict__ loss_per, int64_t B, int classes, float* __restrict__ dW,
                                   float* __restrict__ db, float* __restrict__ loss_out, const int64_t* __restrict__ iter) {
+  pdl_trigger_and_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx < classes * 512) {
     const int k = idx / 512, c = idx % 512;
@@ -406,6 +409,7 @@ __global__ void iter_inc_kernel(int64_t* it) { *it += 1; }
 __global__ void __launch_bounds__(256) im2col_stem7_kernel(const uint8_t* __restrict__ x_base,
                                                            const int64_t* __restrict__ iter, int64_t B, int S,
                                                            uint16_t* __restrict__ out) {
+  pdl_trigger_and_wait();
   extern __shared__ float tile[];  // [3][7][S + 6]
   __shared__ int koff[kStem7K];
   constexpr int kChunks = kStem7K / 8;  // 20
@@ -452,6 +456,7 @@ __global__ void __launch_bounds__(256) im2col_stem7_kernel(const uint8_t* __rest
 // the first maximal tap (row-major scan, as torch's max_pool2d) for backward
 __global__ void maxpool_fwd_kernel(const uint16_t* __restrict__ in, int64_t B, int H, int W, int C, int OH, int OW,
                                    uint16_t* __restrict__ out, uint8_t* __restrict__ idx) {
+  pdl_trigger_and_wait();
   const int cv = C / 8;
   const int64_t total = B * OH * OW * cv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -500,6 +505,7 @@ __global__ void maxpool_fwd_kernel(const uint16_t* __restrict__ in, int64_t B, i
 // the gradient of every window (<= 2 x 2) whose recorded maximum it is
 __global__ void maxpool_bwd_kernel(const uint16_t* __restrict__ gout, const uint8_t* __restrict__ idx, int64_t B,
                                    int H, int W, int C, int OH, int OW, uint16_t* __restrict__ gin) {
+  pdl_trigger_and_wait();
   const int cv = C / 8;
   const int64_t total = B * H * W * cv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -537,6 +543,7 @@ __global__ void maxpool_bwd_kernel(const uint16_t* __restrict__ gout, const uint
 
 // global average pool: x bf16 [B][HW][C] -> feat bf16 [B][C] (the FC GEMM operand)
 __global__ void avgpool_kernel(const uint16_t* __restrict__ x, int64_t B, int HW, int C, uint16_t* __restrict__ feat) {
+  pdl_trigger_and_wait();
   const int cv = C / 8;
   const int64_t total = B * cv;
   const float inv = 1.0f / (float)HW;
@@ -580,6 +587,7 @@ __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logit
                                                  const int32_t* __restrict__ y_base, const int64_t* __restrict__ iter,
                                                  int64_t B, int classes, float* __restrict__ dlog_f,
                                                  uint16_t* __restrict__ dlog_b, float* __restrict__ loss_per) {
+  pdl_trigger_and_wait();
   __shared__ float sh[32];
   const int64_t n = blockIdx.x;
   const int64_t t = iter ? *iter : 0;
@@ -605,6 +613,7 @@ __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logit
 __global__ void head_bias_kernel(const float* __restrict__ dlog_f, int ld, const float* __restrict__ loss_per,
                                  int64_t B, int classes, float* __restrict__ db, float* __restrict__ loss_out,
                                  const int64_t* __restrict__ iter) {
+  pdl_trigger_and_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < classes) {
     float s = 0.f;
@@ -621,6 +630,7 @@ __global__ void head_bias_kernel(const float* __restrict__ dlog_f, int ld, const
 // gradient of the average pool: dOut[n][p][c] = dfeat[n][c] / HW (bf16)
 __global__ void head_bcast_kernel(const float* __restrict__ dfeat, int64_t B, int HW, int C,
                                   uint16_t* __restrict__ dout) {
+  pdl_trigger_and_wait();
   const int cv = C / 8;
   const int64_t total = B * HW * cv;
   const float inv = 1.0f / (float)HW;
@@ -1118,14 +1128,14 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- stem: 7x7/2 conv (explicit im2col) + BN + ReLU + 3x3/2 max-pool ----------------
   const Conv& sc = m->convs[m->stem];
-  im2col_stem7_kernel<<<(unsigned)(B * sc.OH), 256, (size_t)3 * 7 * (m->image + 6) * sizeof(float), s>>>(
-      x_base, d_iter, B, m->image, m->stem_cols);
+  DBS_CUDA_TRY(launch_pdl(im2col_stem7_kernel, dim3((unsigned)(B * sc.OH)), dim3(256), (size_t)3 * 7 * (m->image + 6) * sizeof(float), s, 
+      x_base, d_iter, B, m->image, m->stem_cols));
   DBS_LAUNCH_CHECK();
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
   const int PH = sc.OH / 2;
-  maxpool_fwd_kernel<<<grid_for(B * PH * PH * 8, 256), 256, 0, s>>>(m->a[m->stem], B, sc.OH, sc.OW, 64, PH, PH,
-                                                                     m->mp_out, m->mp_idx);
+  DBS_CUDA_TRY(launch_pdl(maxpool_fwd_kernel, dim3(grid_for(B * PH * PH * 8, 256)), dim3(256), 0, s, m->a[m->stem], B, sc.OH, sc.OW, 64, PH, PH,
+                                                                     m->mp_out, m->mp_idx));
   DBS_LAUNCH_CHECK();
   // ---------------- bottleneck blocks ----------------
   const uint16_t* x = m->mp_out;
@@ -1144,17 +1154,17 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   }
   // ---------------- head: average pool, FC (tcgen05 GEMMs), softmax cross-entropy ----------------
   const int C = m->feat_c, HW = m->feat_hw, K = m->classes, ld = m->cpad;
-  avgpool_kernel<<<grid_for(B * (C / 8), 256), 256, 0, s>>>(x, B, HW, C, m->feat_b);
+  DBS_CUDA_TRY(launch_pdl(avgpool_kernel, dim3(grid_for(B * (C / 8), 256)), dim3(256), 0, s, x, B, HW, C, m->feat_b));
   DBS_LAUNCH_CHECK();
   const uint16_t* wfc = wb + m->fc_w;
   // logits [B][K] = feat [B][C] . Wfc [K][C]^T + b
   if ((st = gemm_bf16(m->feat_b, 0, C, wfc, 0, C, m->logits, ld, B, K, C, DBS_EPI_BIAS_F32, pf + m->fc_b, nullptr, s,
                       nullptr)))
     return st;
-  ce_kernel<<<(unsigned)B, 256, 0, s>>>(m->logits, ld, y_base, d_iter, B, K, m->dlog_f, m->dlog_b, m->loss_per);
+  DBS_CUDA_TRY(launch_pdl(ce_kernel, dim3((unsigned)B), dim3(256), 0, s, m->logits, ld, y_base, d_iter, B, K, m->dlog_f, m->dlog_b, m->loss_per));
   DBS_LAUNCH_CHECK();
-  head_bias_kernel<<<(K + 255) / 256, 256, 0, s>>>(m->dlog_f, ld, m->loss_per, B, K, grad + m->fc_b,
-                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr);
+  DBS_CUDA_TRY(launch_pdl(head_bias_kernel, dim3((K + 255) / 256), dim3(256), 0, s, m->dlog_f, ld, m->loss_per, B, K, grad + m->fc_b,
+                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr));
   DBS_LAUNCH_CHECK();
   // dWfc [K][C] = dlog^T . feat  (both MN-major over the batch)
   if ((st = gemm_bf16(m->dlog_b, 1, ld, m->feat_b, 1, C, grad + m->fc_w, C, K, C, B, DBS_EPI_F32, nullptr, nullptr, s,
@@ -1164,7 +1174,7 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   if ((st = gemm_bf16(m->dlog_b, 0, ld, wfc, 1, C, m->dfeat, C, B, C, K, DBS_EPI_F32, nullptr, nullptr, s, nullptr)))
     return st;
   uint16_t* gcur = m->g0;
-  head_bcast_kernel<<<grid_for(B * HW * (C / 8), 256), 256, 0, s>>>(m->dfeat, B, HW, C, gcur);
+  DBS_CUDA_TRY(launch_pdl(head_bcast_kernel, dim3(grid_for(B * HW * (C / 8), 256)), dim3(256), 0, s, m->dfeat, B, HW, C, gcur));
   DBS_LAUNCH_CHECK();
   // ---------------- backward through the blocks ----------------
   // buffers: gx = gradient of the block input, t0 = BN outputs' gradients,
@@ -1202,8 +1212,8 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
     gx = old;
   }
   // ---------------- stem backward: max-pool, BN + ReLU mask, weight gradient ----------------
-  maxpool_bwd_kernel<<<grid_for(B * sc.OH * sc.OW * 8, 256), 256, 0, s>>>(gcur, m->mp_idx, B, sc.OH, sc.OW, 64, PH,
-                                                                           PH, t1);
+  DBS_CUDA_TRY(launch_pdl(maxpool_bwd_kernel, dim3(grid_for(B * sc.OH * sc.OW * 8, 256)), dim3(256), 0, s, gcur, m->mp_idx, B, sc.OH, sc.OW, 64, PH,
+                                                                           PH, t1));
   DBS_LAUNCH_CHECK();
   if ((st = bn_bwd(m, m->stem, pf, grad, t1, m->a[m->stem], B, t0, nullptr, s))) return st;
   return conv_wgrad(m, m->stem, t0, nullptr, B, grad, s);
@@ -1221,7 +1231,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
   DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- forward ----------------
-  im2col_stem_kernel<<<grid_for(B * 1024, 256), 256, 0, s>>>(x_base, d_iter, B, m->stem_cols);
+  DBS_CUDA_TRY(launch_pdl(im2col_stem_kernel, dim3(grid_for(B * 1024, 256)), dim3(256), 0, s, x_base, d_iter, B, m->stem_cols));
   DBS_LAUNCH_CHECK();
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
@@ -1241,12 +1251,12 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
   }
   // ---------------- head ----------------
   uint16_t* gcur = m->g0;  // gradient w.r.t. the current block output
-  head_kernel<<<(unsigned)B, 256, 0, s>>>(x, pf + m->fc_w, pf + m->fc_b, y_base, d_iter, B, m->classes, m->feat,
-                                          m->dlog, m->loss_per, gcur);
+  DBS_CUDA_TRY(launch_pdl(head_kernel, dim3((unsigned)B), dim3(256), 0, s, x, pf + m->fc_w, pf + m->fc_b, y_base, d_iter, B, m->classes, m->feat,
+                                          m->dlog, m->loss_per, gcur));
   DBS_LAUNCH_CHECK();
-  head_wgrad_kernel<<<(m->classes * 512 + 255) / 256, 256, 0, s>>>(m->feat, m->dlog, m->loss_per, B, m->classes,
+  DBS_CUDA_TRY(launch_pdl(head_wgrad_kernel, dim3((m->classes * 512 + 255) / 256), dim3(256), 0, s, m->feat, m->dlog, m->loss_per, B, m->classes,
                                                                     grad + m->fc_w, grad + m->fc_b,
-                                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr);
+                                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr));
   DBS_LAUNCH_CHECK();
   // ---------------- backward through the blocks ----------------
   uint16_t* bufs[3] = {m->g1, m->g2, m->g3};
