@@ -242,8 +242,8 @@ def run_strategy(tr, wl, kind, args, world=1):
 
 # measured tcgen05.mma (SS, bf16, M=128, K=16) throughput by N tile, as a share of the
 # tensor peak (scripts/mma_bench.cu -> profiles/mma_rate_r1.txt): a single-CTA MMA takes
-# >= ~95 cycles whatever N is, so only N = 256 reaches the peak
-MMA_SHAPE_CEILING = {64: 0.34, 128: 0.67, 256: 1.0}
+# >= ~83 cycles whatever N is (aligned operands), so only N = 256 reaches the peak
+MMA_SHAPE_CEILING = {64: 0.38, 128: 0.77, 256: 1.0}
 
 ROOFLINE_CONV = {
     # workload -> (N, H, Cin, Cout, k, stride, description): the dominant conv shape
