@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--epochs", type=int, default=41)
     ap.add_argument("--out", default=str(ROOT / "profiles" / "robustness_r1"))
     ap.add_argument("--dataset", type=int, default=50000)
+    ap.add_argument("--starts", default="10,21,31", help="epochs at which workers 0, 1, 2 get a background job")
     args = ap.parse_args()
 
     import torch
@@ -40,7 +41,7 @@ def main():
     torch.cuda.set_device(0)
     X, y = synthetic_cifar(args.dataset, seed=0)
     tr = SimulatedTrainer(X, y, n_workers=4, model="resnet18", seed=0, partition=True, max_batch=384)
-    starts = {0: 10, 1: 21, 2: 31}
+    starts = {w: int(e) for w, e in enumerate(args.starts.split(","))}
     profiles = [cluster.WorkerProfile(w, 1.0, disturbances=((cluster.DisturbanceEvent(starts[w], cost_multiplier=2.0),)
                                                              if w in starts else ()))
                 for w in range(4)]

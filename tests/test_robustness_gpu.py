@@ -1,0 +1,31 @@
+"""Short hardware replay of the reference's robustness scenario
+(scripts/replay_robustness.py): background jobs join three workers at epochs
+2, 3, 4; DBS must re-plan exactly one epoch after each one (the previous-epoch
+estimator of allocation.plan_next_epoch) and, re-planned, beat fixed batching; the epoch
+CSVs use the reference report schema."""
+
+from __future__ import annotations
+
+import csv
+import json
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def test_robustness_replay_short(dev, tmp_path):
+    r = subprocess.run([sys.executable, str(ROOT / "scripts" / "replay_robustness.py"), "--epochs", "7",
+                        "--dataset", "12000", "--starts", "2,3,4", "--out", str(tmp_path)],
+                       capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    summary = json.loads((tmp_path / "summary.json").read_text())
+    assert summary["rebalance_epochs_after_start"] == {"0": 1, "1": 1, "2": 1}
+    # once re-planned after the last job (epoch 4 -> plan at 5), DBS epochs beat fixed ones
+    assert summary["dbs"]["epoch_wall_s"][6] < summary["fixed_ssgd"]["epoch_wall_s"][6]
+    rows = list(csv.DictReader(open(tmp_path / "robustness_b200_dbs.csv")))
+    assert len(rows) == 7 * 4 and {"epoch", "worker_id", "t_gpu", "t_w"} <= set(rows[0])
