@@ -16,11 +16,13 @@ Prints ONE JSON line on rank 0.  Definitions ("Measurement"):
     cpu_baseline (the reference loop with a CPU model on the host cores),
     clocks sampled in-process with NVML during the timed region.
 Workload at N=1 (config 3, BASELINE.json): ResNet-18 on synthetic CIFAR-shaped
-data, 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the
-B200, B=512 (128/worker fixed); worker 0 shares its partition with a co-running
-spin kernel that pins half of its SMs (cost_multiplier 2, the paper's SM
-disturbance).  Under torchrun each rank runs the same 4-worker
-simulation on its own GPU (weak scaling, no data-path collective across GPUs).
+data, 3 simulated workers = 3 disjoint 48-SM partitions (green contexts; 144 of the
+148 SMs -- partitions come in multiples of 8 SMs) of the B200, B=510 (170/worker
+fixed); worker 0 shares its partition with a co-running spin kernel that pins
+half of its SMs (cost_multiplier 2, the paper's SM disturbance).  Under torchrun
+every rank hosts the same workers on its own GPU, the global plan spans all
+ranks' workers, and the gradients meet every iteration in the fused NVLink
+all-reduce + SGD kernel (comm.cu); the epoch time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -50,7 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--report", default=None,
                     help="directory for the reference-format run reports (epoch CSV per strategy + run JSON)")
-    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_ma", "resnet50", "mlp", "allreduce"])
+    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_4w", "resnet18_ma", "resnet50", "mlp", "allreduce"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -142,11 +144,14 @@ class ClockSampler:
 # workloads
 # ---------------------------------------------------------------------------
 WL = {
-    "resnet18": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0,
+    "resnet18": dict(D=50000, workers=3, per_worker=170, lr=0.05, mom=0.9, mult=2.0,
                      desc="C3: ResNet-18 (CIFAR stem), synthetic CIFAR-10-shaped 50000x3x32x32 fp32 (bf16 tensor-core "
-                          "operands), 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the B200, "
-                          "B=512 (128/worker fixed), step = 1 epoch (97 iterations)"),
-    "resnet18_ma": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0, avg=4,
+                          "operands), 3 simulated workers = 3 disjoint 48-SM partitions (green contexts, 144 of the "
+                          "148 SMs) of the B200, B=510 (170/worker fixed), step = 1 epoch (98 iterations)"),
+    "resnet18_4w": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0,
+                        desc="C3 variant: ResNet-18 CIFAR, 4 simulated workers = 4 disjoint 32-SM partitions (128 of "
+                             "148 SMs; partitions come in multiples of 8 SMs), B=512"),
+    "resnet18_ma": dict(D=50000, workers=3, per_worker=170, lr=0.05, mom=0.9, mult=2.0, avg=4,
                         desc="C4: C3 with periodic model averaging (local SGD on per-worker replicas, averaged every "
                              "step=4 iterations), DBS vs fixed plan, step = 1 epoch"),
     "resnet50": dict(D=12800, workers=4, per_worker=64, lr=0.05, mom=0.9, mult=None, image=224, classes=1000,
