@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--report", default=None,
                     help="directory for the reference-format run reports (epoch CSV per strategy + run JSON)")
-    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_4w", "resnet18_ma", "resnet50", "mlp", "allreduce"])
+    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_4w", "resnet18_ma", "resnet50", "resnet50_3w", "mlp", "allreduce"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -154,6 +154,9 @@ WL = {
     "resnet18_ma": dict(D=50000, workers=3, per_worker=170, lr=0.05, mom=0.9, mult=2.0, avg=4,
                         desc="C4: C3 with periodic model averaging (local SGD on per-worker replicas, averaged every "
                              "step=4 iterations), DBS vs fixed plan, step = 1 epoch"),
+    "resnet50_3w": dict(D=12800, workers=3, per_worker=85, lr=0.05, mom=0.9, mult=None, image=224, classes=1000,
+                        max_batch=200, cpu_per_worker=16, smoothing=0.7,
+                        desc="C5 variant: ResNet-50 224, 3 simulated workers = 3 disjoint 48-SM partitions, B=255"),
     "resnet50": dict(D=12800, workers=4, per_worker=64, lr=0.05, mom=0.9, mult=None, image=224, classes=1000,
                      max_batch=160, cpu_per_worker=16, smoothing=0.7,
                      desc="C5: ResNet-50 (torchvision v1.5) on synthetic ImageNet-shaped 12800x3x224x224 uint8, 1000 "
@@ -203,7 +206,7 @@ def make_trainer(wl, rank, world=1):
                                 max_batch=w.get("max_batch", 3 * w["per_worker"]), classes=w.get("classes", 10),
                                 image=w.get("image", 224))
         return tr, (None, None)
-    if wl == "resnet50":
+    if wl.startswith("resnet50"):
         from paper_2007_11831_b200.resnet import synthetic_imagenet
 
         X, y = synthetic_imagenet(w["D"], w["image"], w["classes"], seed=rank, device=torch.device("cuda"))
@@ -269,7 +272,7 @@ def kernel_roofline(peaks, wl="resnet18"):
 
     from paper_2007_11831_b200 import _lib
 
-    N, H, C, Co, k, stride, desc = ROOFLINE_CONV.get(wl, ROOFLINE_CONV["resnet18"])
+    N, H, C, Co, k, stride, desc = ROOFLINE_CONV["resnet50" if wl.startswith("resnet50") else "resnet18"]
     pad = k // 2
     OH = (H + 2 * pad - k) // stride + 1
     x = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
@@ -304,7 +307,7 @@ def kernel_roofline(peaks, wl="resnet18"):
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic_r1.json"
     if tf.exists():
-        rec = json.loads(tf.read_text()).get(wl if wl in ROOFLINE_CONV else "resnet18")
+        rec = json.loads(tf.read_text()).get("resnet50" if wl.startswith("resnet50") else "resnet18")
         if rec:
             traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
     n_tile = 64 if Co <= 64 else (128 if Co <= 128 else 256)
@@ -413,7 +416,7 @@ def cpu_baseline(wl, X, y, threads=None):
     if wl.startswith("resnet"):
         from paper_2007_11831_b200.resnet import init_params
 
-        depth = 50 if wl == "resnet50" else 18
+        depth = 50 if wl.startswith("resnet50") else 18
         tens = (init_params(w["classes"], 0, depth=50, image=w["image"]) if depth == 50 else init_params(seed=0))
         sec = O.cpu_resnet_iteration_seconds(tens, X[:sum(batches)], y[:sum(batches)], batches, threads=threads,
                                              depth=depth)
@@ -531,7 +534,7 @@ def reference_arm(args):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
         X, y = synthetic_cifar(w["workers"] * w["per_worker"], seed=0)
-    elif wl == "resnet50":
+    elif wl.startswith("resnet50"):
         from paper_2007_11831_b200.resnet import synthetic_imagenet
 
         X, y = synthetic_imagenet(w["workers"] * w["cpu_per_worker"], w["image"], w["classes"], seed=0)
