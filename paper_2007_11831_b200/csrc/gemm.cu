@@ -82,6 +82,11 @@ struct GemmParams {
   ConvTaps taps;        // explicit conv taps of A (n = 0: R x S window)
   OutMap omap;          // strided output rows (on = 0: row-major)
   int pair_a, pair_b;   // one TMA box covers two consecutive k-blocks (ring slots s, s+1) of A / B
+  int nclass;           // > 0: merged output-parity classes (stride-2 input gradient), class c owns
+  int64_t cls_start[5]; //   tiles [cls_start[c], cls_start[c + 1]) with its own taps / output map
+  int cls_kb[4];        //   and k-block count
+  ConvTaps cls_taps[4];
+  OutMap cls_omap[4];
   int halo_rows;        // halo variant: image rows per TMA box
   int halo_tpi;         // halo variant: tiles per image (ceil(OH (OW + 1) / 128))
   int64_t halo_tiles;   // halo variant: images x tiles per image
@@ -391,13 +396,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) GEMM_TRACE(0);
   const int64_t m_tiles = (p.M + kBM - 1) / kBM;
   const int64_t n_tiles = (p.N + BN - 1) / BN;
-  const int64_t num_tiles = kHalo ? p.halo_tiles : m_tiles * n_tiles * p.splits;
+  const int64_t num_tiles = kHalo ? p.halo_tiles : (p.nclass > 0 ? p.cls_start[p.nclass] : m_tiles * n_tiles * p.splits);
   const int num_k_total = (int)((p.K + kBK - 1) / kBK);
   const int a_mn = (p.a_mode == 1) ? 1 : 0;
   const int b_mn = (p.b_mode >= 1) ? 1 : 0;
   // tile t -> (m tile fastest, then n tile, then split-K slice): the tiles
   // resident at one time share their B block (and neighbouring A windows) in L2
-  auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& kb_begin) -> int {
+  // tile t -> (m0, n0, first k-block, class); returns the tile's k-block count
+  auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& kb_begin, int& cls) -> int {
+    cls = -1;
+    if (p.nclass > 0) {  // merged classes: one N tile, no split-K
+      int c = 0;
+      while (c + 1 < p.nclass && t >= p.cls_start[c + 1]) c++;
+      cls = c;
+      m0 = (t - p.cls_start[c]) * kBM;
+      n0 = 0;
+      kb_begin = 0;
+      return p.cls_kb[c];
+    }
     const int64_t rest = t / m_tiles;
     m0 = (t - rest * m_tiles) * kBM;
     const int64_t split = rest / n_tiles;
@@ -464,8 +480,9 @@ __global__ void __launch_bounds__(kThreads, 1)
    } else {
    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     int64_t m0, n0;
-    int kb_begin;
-    const int num_k = decode(t, m0, n0, kb_begin);
+    int kb_begin, cls;
+    const int num_k = decode(t, m0, n0, kb_begin, cls);
+    const ConvTaps& tp = cls >= 0 ? p.cls_taps[cls] : p.taps;
     int a_n = 0, a_oh = 0, a_ow = 0;
     if (p.a_mode == 2 || p.a_mode == 4) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
     int b_r = 0, b_s = 0, b_c0 = 0;
@@ -503,11 +520,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         int h0, w0, oh, ow;
-        if (p.taps.n > 0) {
+        if (tp.n > 0) {
           h0 = a_oh - 1;
           w0 = a_ow - 1;
-          oh = p.taps.dh[rs] + 1;
-          ow = p.taps.dw[rs] + 1;
+          oh = tp.dh[rs] + 1;
+          ow = tp.dw[rs] + 1;
         } else {
           oh = rs / g.S;
           ow = rs - oh * g.S;
@@ -520,9 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         int ah, aw;
-        if (p.taps.n > 0) {
-          ah = a_oh + p.taps.dh[rs];
-          aw = a_ow + p.taps.dw[rs];
+        if (tp.n > 0) {
+          ah = a_oh + tp.dh[rs];
+          aw = a_ow + tp.dw[rs];
         } else {
           const int r = rs / g.S, sx = rs - r * g.S;
           ah = a_oh * g.stride + r - g.pad;
@@ -542,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         const int r = rs / g.S, sx = rs - r * g.S;
-        const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+        const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
 #pragma unroll
         for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
       } else if (p.b_mode == 4) {
@@ -596,9 +613,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int cb = kb % g.cblocks;
             const int rs = kb / g.cblocks;
             int ah, aw;
-            if (p.taps.n > 0) {
-              ah = a_oh + p.taps.dh[rs];
-              aw = a_ow + p.taps.dw[rs];
+            if (tp.n > 0) {
+              ah = a_oh + tp.dh[rs];
+              aw = a_ow + tp.dw[rs];
             } else {
               const int r = rs / g.S, sx = rs - r * g.S;
               ah = a_oh * g.stride + r - g.pad;
@@ -620,11 +637,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         int h0, w0, oh, ow;
-        if (p.taps.n > 0) {
+        if (tp.n > 0) {
           h0 = a_oh - 1;
           w0 = a_ow - 1;
-          oh = p.taps.dh[rs] + 1;
-          ow = p.taps.dw[rs] + 1;
+          oh = tp.dh[rs] + 1;
+          ow = tp.dw[rs] + 1;
         } else {
           oh = rs / g.S;
           ow = rs - oh * g.S;
@@ -637,9 +654,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         int ah, aw;
-        if (p.taps.n > 0) {
-          ah = a_oh + p.taps.dh[rs];
-          aw = a_ow + p.taps.dw[rs];
+        if (tp.n > 0) {
+          ah = a_oh + tp.dh[rs];
+          aw = a_ow + tp.dw[rs];
         } else {
           const int r = rs / g.S, sx = rs - r * g.S;
           ah = a_oh * g.stride + r - g.pad;
@@ -665,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int cb = kb % g.cblocks;
             const int rs = kb / g.cblocks;
             const int r = rs / g.S, sx = rs - r * g.S;
-            const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+            const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
             tma_load_3d(b, &tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
           }
         }
@@ -681,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = kb % g.cblocks;
         const int rs = kb / g.cblocks;
         const int r = rs / g.S, sx = rs - r * g.S;
-        const int rs_flip = p.taps.n > 0 ? (int)p.taps.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+        const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
 #pragma unroll
         for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
       } else if (p.b_mode == 4) {
@@ -760,8 +777,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t a_kstep = a_mn ? 128u : 2u, b_kstep = b_mn ? 128u : 2u;  // one UMMA_K step, 16 B units
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int64_t m0, n0;
-      int kb_begin;
-      const int num_k = decode(t, m0, n0, kb_begin);
+      int kb_begin, cls;
+      const int num_k = decode(t, m0, n0, kb_begin, cls);
       if (num_k == 0) continue;
       const int b = (int)(j & 1);
       mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
@@ -799,8 +816,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t tj = 0;
   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     int64_t m0 = 0, n0 = 0;
-    int kb_begin;
-    if (!kHalo && decode(t, m0, n0, kb_begin) == 0) continue;
+    int kb_begin, cls = -1;
+    if (!kHalo && decode(t, m0, n0, kb_begin, cls) == 0) continue;
+    const OutMap& om = cls >= 0 ? p.cls_omap[cls] : p.omap;
     const int b = (int)(tj & 1);
     mbar_wait(&acc_full[b], (tj >> 1) & 1);
     if (warp == 2 && lane == 0) GEMM_TRACE(32 + tj);
@@ -817,12 +835,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       valid = (w < p.ga.OW) && (h < p.ga.OH);
       orow = ((int64_t)img * p.ga.OH + h) * p.ga.OW + w;
       row = orow;
-    } else if (p.omap.on && row < p.M) {
-      const int64_t hw = (int64_t)p.omap.OH * p.omap.OW;
+    } else if (om.on && row < p.M) {
+      const int64_t hw = (int64_t)om.OH * om.OW;
       const int64_t img = row / hw;
       const int rem = (int)(row - img * hw);
-      const int i = rem / p.omap.OW, jj = rem - i * p.omap.OW;
-      orow = (img * p.omap.H + 2 * i + p.omap.a) * p.omap.W + 2 * jj + p.omap.b;
+      const int i = rem / om.OW, jj = rem - i * om.OW;
+      orow = (img * om.H + 2 * i + om.a) * om.W + 2 * jj + om.b;
     }
     const uint32_t lane_addr = tmem_base + b * kAccCols + ((uint32_t)(q * 32) << 16);
     const bool stats = (p.sum_part != nullptr);
@@ -892,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
           __syncwarp();
           uint16_t* dbase = reinterpret_cast<uint16_t*>(p.d) + n_base + (lane & 3) * 8;
-          if (!kHalo && !p.omap.on) {
+          if (!kHalo && !om.on) {
             // identity row map: the storing lane forms its row itself
             const int64_t row_w = m0 + q * 32;
 #pragma unroll
@@ -1396,7 +1414,8 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   q.splits = splits;
 
   // persistent: one CTA per SM of the current (possibly green) context
-  const int64_t tiles = kHalo ? p.halo_tiles : ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits;
+  const int64_t tiles = kHalo ? p.halo_tiles
+                      : (p.nclass > 0 ? p.cls_start[p.nclass] : ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits);
   const int64_t sms = current_sm_count();
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
   DBS_CUDA_TRY(launch_pdl(gemm_bf16_kernel<BN, kHalo>, dim3(grid), dim3(kThreads), kSmem, s, ta, tb, q));
@@ -1546,6 +1565,18 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   p.sq_part = c.sq_part;
   p.taps = c.taps;
   p.omap = c.omap;
+  p.nclass = c.nclass;
+  if (c.nclass > 0) {
+    DBS_REQUIRE(c.nclass <= 4 && c.splits <= 1 && c.a_mode == 2, DBS_ERR_ARGUMENT, "merged classes: bad call");
+    const int64_t mt = (c.M + kBM - 1) / kBM;
+    p.cls_start[0] = 0;
+    for (int k = 0; k < c.nclass; k++) {
+      p.cls_taps[k] = c.cls_taps[k];
+      p.cls_omap[k] = c.cls_omap[k];
+      p.cls_kb[k] = c.cls_taps[k].n * c.ga.cblocks;
+      p.cls_start[k + 1] = p.cls_start[k] + mt;
+    }
+  }
   p.colsum_part = nullptr;
   int st;
   int bn = (c.bn_override > 0) ? c.bn_override : pick_bn(c.N, c.b_mode);
@@ -1567,7 +1598,8 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     bn = pick;
   }
   // paired k-block loads need an even k-block count in every tile: no split-K
-  const bool pairing = kpair_enabled() && (c.splits <= 1) && ((c.K + kBK - 1) / kBK) % 2 == 0;
+  bool pairing = kpair_enabled() && (c.splits <= 1) && ((c.K + kBK - 1) / kBK) % 2 == 0;
+  for (int k = 0; k < c.nclass; k++) pairing = pairing && (c.cls_taps[k].n * c.ga.cblocks) % 2 == 0;
   // weight gradient of a <= 64-output-channel conv (dY^T MN-major A, im2col(X) B,
   // 64-wide N tile): 128 pixels per box for both operands; split-K slices are
   // rounded to an even number of k-blocks

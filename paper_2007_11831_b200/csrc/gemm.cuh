@@ -61,6 +61,11 @@ struct ConvCall {
   ConvTaps taps;
   OutMap omap;
   int halo;                  // 3x3 stride-1 64->64 conv: resident filter + halo rows (gemm.cu HaloCfg)
+  // merged stride-2 input gradient: nclass output-parity classes in ONE launch, each
+  // a full M-row GEMM with its own tap list / output map (taps, omap unused then)
+  int nclass;
+  ConvTaps cls_taps[4];
+  OutMap cls_omap[4];
 };
 
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,

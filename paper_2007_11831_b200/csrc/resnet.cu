@@ -978,6 +978,14 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
   return DBS_OK;
 }
 
+bool merge_parity_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_MERGE_PARITY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // dX (+)= dgrad of conv c from dy; accumulate selects the bf16 accumulate epilogue.
 int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t B, uint16_t* dx, int accumulate,
                   cudaStream_t s) {
@@ -1030,6 +1038,36 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
     }
   if (empty_class && !accumulate)
     DBS_CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(uint16_t) * (size_t)(B * c.H * c.W * c.cin), s));
+  if (c.cin <= 256 && merge_parity_enabled()) {
+    // all non-empty parity classes in ONE launch (one N tile: the 64..256-wide N tile
+    // covers Cin), each class a full GEMM over the OH x OW grid with its own taps
+    ConvCall mc = call;
+    mc.M = B * c.OH * c.OW;
+    mc.nclass = 0;
+    int kmax = 0;
+    for (int a = 0; a < 2; a++)
+      for (int b = 0; b < 2; b++) {
+        ConvTaps t{};
+        for (int r = 0; r < c.k; r++)
+          for (int q = 0; q < c.k; q++) {
+            if (((a + pad - r) & 1) != 0 || ((b + pad - q) & 1) != 0) continue;
+            t.dh[t.n] = (int8_t)((a + pad - r) / 2);
+            t.dw[t.n] = (int8_t)((b + pad - q) / 2);
+            t.rs[t.n] = (uint8_t)(r * c.k + q);
+            t.n++;
+          }
+        if (t.n == 0) continue;
+        mc.cls_taps[mc.nclass] = t;
+        mc.cls_omap[mc.nclass] = OutMap{1, c.H, c.W, a, b, c.OH, c.OW};
+        mc.nclass++;
+        if (t.n > kmax) kmax = t.n;
+      }
+    mc.K = (int64_t)kmax * c.cout;
+    mc.ga = ConvGeom{1, kmax, c.cout / 64, 1, 0, c.OH, c.OW, c.cout};
+    mc.taps = mc.cls_taps[0];
+    mc.bn_override = c.cin <= 64 ? 64 : (c.cin <= 128 ? 128 : 256);
+    return conv_gemm(mc, s);
+  }
   for (int a = 0; a < 2; a++)
     for (int b = 0; b < 2; b++) {
       ConvTaps t{};
