@@ -197,12 +197,11 @@ def make_trainer(wl, rank, world=1):
     from paper_2007_11831_b200.trainer import DistributedTrainer, SimulatedTrainer
 
     w = WL[wl]
-    if world > 1 and w.get("avg"):
-        raise SystemExit("model averaging (resnet18_ma) runs on one GPU; the multi-GPU trainer is S-SGD")
     if world > 1:
         # one process per GPU: the same 4 SM-partition workers per GPU, the global
         # plan spans 4 x world workers, gradients meet in the fused NVLink kernel
-        tr = DistributedTrainer(w["D"], workers_per_rank=w["workers"], model=wl, seed=0, partition=True,
+        model = "resnet50" if wl.startswith("resnet50") else ("resnet18" if wl.startswith("resnet18") else "mlp")
+        tr = DistributedTrainer(w["D"], workers_per_rank=w["workers"], model=model, seed=0, partition=True,
                                 max_batch=w.get("max_batch", 3 * w["per_worker"]), classes=w.get("classes", 10),
                                 image=w.get("image", 224))
         return tr, (None, None)

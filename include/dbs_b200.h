@@ -396,6 +396,14 @@ int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* batch_size
 int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                              float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
                              uint16_t* const* d_params_bf16, void* agg_stream);
+/* The same across GPUs (one process per GPU): after the local average of every
+ * sync round, d_params[0] -- which must be the communicator's parameter block --
+ * is averaged across ranks with rank weights = rank_batches[r] (the ranks' batch
+ * sums) by the fused NVLink kernel and copied back into the other replicas. */
+int dbs_run_iterations_local_comm(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                  float lr, float momentum, int32_t sync_interval, float* const* d_params,
+                                  float* const* d_velocity, uint16_t* const* d_params_bf16, dbs_comm* comm,
+                                  const int64_t* rank_batches, void* agg_stream);
 /* x_bar = sum_i w_i x_i (w as in dbs_dev_aggregate_*), written to every replica
  * and its bf16 copy (d_params_bf16 may be NULL). P % 4 == 0. */
 int dbs_dev_average_replicas_f32(float* const* d_params, const int64_t* b, int64_t n, int32_t mode, int64_t P,

@@ -126,6 +126,9 @@ SIGNATURES = {
                                          ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_vp]),
     "dbs_dev_average_replicas_f32": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, ctypes.POINTER(c_vp),
                                              c_vp]),
+    "dbs_run_iterations_local_comm": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt,
+                                              c_i32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                              c_vp, P_i64, c_vp]),
     "dbs_resnet_create": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_vp)]),
     "dbs_resnet_create_ex": (c_i32, [c_i32, c_i32, c_i64, c_i32, ctypes.POINTER(c_vp)]),
     "dbs_resnet_info": (c_i32, [c_vp, P_i32, P_i32, P_i64, P_i32]),

@@ -392,9 +392,37 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
 // batch weights of `mode` -- floor(T / sync_interval) rounds per epoch
 // (cluster.sync_rounds_for_epoch, cluster.py:185-186).  Between rounds no
 // worker waits for another.
+static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                                float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
+                                uint16_t* const* d_params_bf16, void* agg_stream, dbs_comm* comm,
+                                const int64_t* rank_batches);
+
 extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                         float lr, float mom, int32_t sync_interval, float* const* d_params,
                                         float* const* d_velocity, uint16_t* const* d_params_bf16, void* agg_stream) {
+  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_bf16,
+                              agg_stream, nullptr, nullptr);
+}
+
+// Model averaging across GPUs: every sync round first averages this rank's
+// replicas (weighted by the local batches), then averages replica 0 -- which
+// must be the communicator's symmetric parameter block -- across the ranks with
+// the fused NVLink kernel (rank weights = the ranks' batch sums, so the result is
+// the global batch-weighted average), and copies it back into the other replicas.
+extern "C" int dbs_run_iterations_local_comm(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1,
+                                             int32_t mode, float lr, float mom, int32_t sync_interval,
+                                             float* const* d_params, float* const* d_velocity,
+                                             uint16_t* const* d_params_bf16, dbs_comm* comm,
+                                             const int64_t* rank_batches, void* agg_stream) {
+  DBS_REQUIRE(comm && rank_batches, DBS_ERR_ARGUMENT, "run_iterations_local_comm: null communicator / batches");
+  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_bf16,
+                              agg_stream, comm, rank_batches);
+}
+
+static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
+                                float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
+                                uint16_t* const* d_params_bf16, void* agg_stream, dbs_comm* comm,
+                                const int64_t* rank_batches) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0 && sync_interval >= 1 && d_params && d_velocity && d_params_bf16,
               DBS_ERR_ARGUMENT, "run_iterations_local: bad arguments");
   for (int i = 0; i < n; i++)
@@ -467,6 +495,15 @@ extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int
       for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
       st = dbs_dev_average_replicas_f32(d_params, batches, n, mode, P, d_params_bf16, agg_stream);
       if (st) return st;
+      if (comm) {
+        st = dbs_comm_average_params(comm, rank_batches, mode, agg_stream);
+        if (st) return st;
+        for (int i = 1; i < n; i++) {
+          DBS_CUDA_TRY(cudaMemcpyAsync(d_params[i], d_params[0], sizeof(float) * P, cudaMemcpyDeviceToDevice, agg));
+          DBS_CUDA_TRY(cudaMemcpyAsync(d_params_bf16[i], d_params_bf16[0], sizeof(uint16_t) * P,
+                                       cudaMemcpyDeviceToDevice, agg));
+        }
+      }
       DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
       for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(as_stream(w[i].stream), ev[n], 0));
     }

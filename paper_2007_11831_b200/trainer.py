@@ -545,10 +545,34 @@ class DistributedTrainer(SimulatedTrainer):
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
             skip_update: bool = False, timed_from: Optional[int] = None,
-            epoch_hook: Optional[Callable[[int], None]] = None) -> RunResult:
+            epoch_hook: Optional[Callable[[int], None]] = None,
+            averaging_interval: Optional[int] = None) -> RunResult:
+        """S-SGD across GPUs (fused NVLink all-reduce + SGD every iteration), or --
+        for "model_averaging" / "one_shot" / averaging_interval=k -- local SGD on
+        per-worker replicas with a global batch-weighted parameter average every k
+        iterations (local average, then the NVLink average across ranks)."""
+        import ctypes
+
         import torch
 
         from .comm import max_over_ranks
+
+        local_interval = averaging_interval
+        if local_interval is None and config.kind == "model_averaging":
+            local_interval = config.sync_interval
+        if local_interval is None and config.kind == "one_shot":
+            local_interval = 1 << 30
+        if local_interval is not None and local_interval < 1:
+            raise ConfigurationError("averaging_interval must be >= 1")
+        local = local_interval is not None and not skip_update
+        if local:
+            # replica 0 IS the symmetric parameter block the cross-rank average runs on
+            Pm = self.model.P
+            self._rep_p = [self.comm.params] + [self.comm.params.clone() for _ in range(self.n - 1)]
+            self._rep_pb = [self.comm.params_bf16] + [self.comm.params_bf16.clone() for _ in range(self.n - 1)]
+            self._rep_v = [torch.zeros(Pm, dtype=torch.float32, device=self.dev) for _ in range(self.n)]
+            arr = lambda ts: (ctypes.c_void_p * self.n)(*[t.data_ptr() for t in ts])
+            rep_ptrs = (arr(self._rep_p), arr(self._rep_v), arr(self._rep_pb))
 
         n_loc, W, R = self.n, self.n * self.world, self.rank
         D = self.D
@@ -637,7 +661,13 @@ class DistributedTrainer(SimulatedTrainer):
                 wk.stream.wait_stream(cur)
             start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             start.record(self.agg)
-            if iters > 0:
+            if iters > 0 and local:
+                st = _lib.lib().dbs_run_iterations_local_comm(
+                    slots, n_loc, 0, iters, mode, float(lr), float(momentum), int(local_interval), rep_ptrs[0],
+                    rep_ptrs[1], rep_ptrs[2], self.comm.h, rank_batches.ctypes.data_as(_lib.P_i64),
+                    int(self.agg.cuda_stream))
+                _lib.check(st, "run_iterations_local_comm")
+            elif iters > 0:
                 st = _lib.lib().dbs_run_iterations_comm(slots, n_loc, 0, iters, mode, float(lr), float(momentum),
                                                         self.comm.h, rank_batches.ctypes.data_as(_lib.P_i64),
                                                         self.comm.velocity.data_ptr(), int(self.agg.cuda_stream), None)
@@ -671,6 +701,16 @@ class DistributedTrainer(SimulatedTrainer):
             t_end.record()
             torch.cuda.synchronize()
             timed = max_over_ranks(t_start.elapsed_time(t_end) / 1e3, self.group)
+        if local and config.kind == "one_shot" and plans:
+            # the single averaging round of one-shot averaging (cluster.py:187-188)
+            last = list(plans[-1].int_batches)
+            b_loc = np.asarray(last[R * n_loc:(R + 1) * n_loc], dtype=np.int64)
+            _lib.check(_lib.lib().dbs_dev_average_replicas_f32(rep_ptrs[0], b_loc.ctypes.data_as(_lib.P_i64), n_loc,
+                                                               mode, self.model.P, rep_ptrs[2],
+                                                               int(self.agg.cuda_stream)), "average_replicas")
+            rb = np.asarray([sum(last[r * n_loc:(r + 1) * n_loc]) for r in range(self.world)], dtype=np.int64)
+            self.comm.average_params(rb, mode=mode, stream=self.agg)
+            torch.cuda.synchronize()
         return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
                          wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
                          timed_launches=timed_launches)
@@ -695,6 +735,13 @@ class DistributedTrainer(SimulatedTrainer):
                                                         self.model.P, self.comm.grad.data_ptr(),
                                                         _lib.stream_handle()), "aggregate_f32")
         self.comm.allreduce_sgd(rank_batches, 0.0, 0.0, mode=mode)
+        # the model-averaging round's kernels too (identical parameters on every rank: no change)
+        self.comm.average_params(rank_batches, mode=mode)
+        ptr1 = (ctypes.c_void_p * 1)(self.comm.params.data_ptr())
+        ptrb = (ctypes.c_void_p * 1)(self.comm.params_bf16.data_ptr())
+        one = np.ones(1, dtype=np.int64)
+        _lib.check(_lib.lib().dbs_dev_average_replicas_f32(ptr1, one.ctypes.data_as(_lib.P_i64), 1, mode, self.model.P,
+                                                           ptrb, _lib.stream_handle()), "average_replicas")
         torch.cuda.synchronize()
         self.comm.velocity.zero_()
         torch.distributed.barrier(self.group)

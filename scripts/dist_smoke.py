@@ -11,7 +11,9 @@ model = sys.argv[1] if len(sys.argv) > 1 else "mlp"
 tr = DistributedTrainer(2000 if model == "mlp" else 1024, workers_per_rank=1, model=model, seed=0, partition=False,
                         max_batch=256)
 t = time.time()
-r = tr.run(cluster.StrategyConfig("dbs", 128 * world), n_epochs=2, max_iters=6, record_loss=True)
+avg = int(sys.argv[2]) if len(sys.argv) > 2 else None  # model averaging every `avg` iterations
+r = tr.run(cluster.StrategyConfig("dbs", 128 * world), n_epochs=2, max_iters=6, record_loss=True,
+           averaging_interval=avg)
 torch.cuda.synchronize()
 p = tr.comm.params[:1024].double().sum().item()
 ps = [None] * world

@@ -18,10 +18,17 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def test_two_process_distributed_trainer(dev):
+@pytest.mark.parametrize("extra", [[], ["2"]], ids=["ssgd", "model_averaging_k2"])
+def test_two_process_distributed_trainer(dev, extra):
+    """S-SGD through the fused all-reduce + SGD kernel, and model averaging every 2
+    iterations (local replica average, then the NVLink parameter average across
+    ranks): both must leave identical parameters on the two ranks (6 iterations end
+    on a sync round)."""
     env = dict(os.environ, PYTHONPATH=str(ROOT))
+    port = "29531" if not extra else "29533"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", str(ROOT / "scripts" / "dist_smoke.py"), "mlp"]
+           "--master-addr", "127.0.0.1", "--master-port", port, str(ROOT / "scripts" / "dist_smoke.py"), "mlp",
+           *extra]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=str(ROOT))
     out = p.stdout + p.stderr
     assert p.returncode == 0, out[-3000:]
