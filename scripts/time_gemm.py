@@ -5,6 +5,10 @@ sys.path.insert(0, ".")
 from paper_2007_11831_b200 import _lib  # noqa: E402
 L = _lib.lib()
 shapes = [(200704, 256, 64), (200704, 64, 256), (16384, 256, 2304), (50176, 256, 1024), (12544, 1024, 256)]
+if len(sys.argv) > 1 and sys.argv[1] == "transposed":
+    # normal (M = pixels, N = Cout) vs transposed (M = Cout, N = pixels) orientation
+    shapes = [(50176, 128, 1152), (128, 50176, 1152), (50176, 64, 576), (64, 50176, 576), (32768, 128, 1152),
+              (128, 32768, 1152)]
 for M, N, K in shapes:
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
