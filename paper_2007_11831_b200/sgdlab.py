@@ -287,6 +287,15 @@ def sgd_step(x, gradient, config: SgdConfig, velocity):
 PlanSource = Union[Sequence[int], Sequence[PartitionPlan]]
 
 
+def theorem1_bound(j: int, gamma: float, mu: float, initial_sq_dist: float, sigma_sq: float) -> float:
+    """Geometric contraction bound (1 - gamma mu)^j d0 + gamma sigma^2 / mu (sgdlab.py:241-249)."""
+    if not (0.0 < gamma * mu < 1.0):
+        raise InvalidStepSizeError(f"gamma*mu must be in (0, 1), got {gamma * mu}")
+    if sigma_sq < 0.0 or initial_sq_dist < 0.0:
+        raise ConfigurationError("distances and noise must be non-negative")
+    return (1.0 - gamma * mu) ** j * initial_sq_dist + gamma * sigma_sq / mu
+
+
 def _epoch_layout(plan_source: PlanSource, epoch: int, n_workers: int,
                   sample_count: int) -> tuple[list[int], list[tuple[int, int]]]:
     """Per-epoch batches and spans (sgdlab.py:320-340); spans from the device controller."""

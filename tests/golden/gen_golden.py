@@ -301,6 +301,18 @@ def gen_sgd_trajectories():
     return recs
 
 
+def gen_equivalence():
+    """checks.check_dbs_equivalence (checks.py:185-244) at a small size."""
+    from dbsim import checks
+
+    quad = sgdlab.ConvexProblem.quadratic(dimension=8, mu=1.0, sample_noise_scale=0.5, sample_count=4096, seed=0)
+    res = checks.check_dbs_equivalence(quad, n_workers=4, total_budget=64, n_seeds=6, n_iterations=200, seed=2)
+    return {"args": {"n_workers": 4, "total_budget": 64, "n_seeds": 6, "n_iterations": 200, "seed": 2},
+            "final_gap_fixed": hx(res.final_gap_fixed), "final_gap_dynamic": hx(res.final_gap_dynamic),
+            "relative_gap_diff": hx(res.relative_gap_diff), "max_trajectory_z": hx(res.max_trajectory_z),
+            "passed": bool(res.passed)}
+
+
 def gen_reports():
     """The reference's report formats (report.py) for a simulated scenario: the
     scenario definition, the DBS run's long CSV, the run JSON of every strategy
@@ -352,6 +364,7 @@ def main():
     (HERE / "permutation.json").write_text(json.dumps(gen_permutations(), indent=1))
     (HERE / "sgd_trajectories.json").write_text(json.dumps(gen_sgd_trajectories(), separators=(",", ":")))
     (HERE / "report_scenario.json").write_text(json.dumps(gen_reports(), indent=1))
+    (HERE / "equivalence.json").write_text(json.dumps(gen_equivalence(), indent=1))
     for p in sorted(HERE.glob("*.json")):
         print(p.name, p.stat().st_size)
 

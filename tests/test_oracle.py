@@ -219,3 +219,17 @@ def test_model_averaging_rounds_and_replicas():
     between = O.run_parallel_sgd(p, 0.05, 6, 0.5, "batch_weighted", 0, 3, plans, initial_point=x0,
                                  averaging_interval=4)
     assert not np.array_equal(between["replicas"][0], between["replicas"][1])
+
+
+def test_theorem1_bound_formula():
+    """sgdlab.theorem1_bound (host formula, sgdlab.py:241-249) and its domain errors."""
+    import pytest as _pt
+
+    from paper_2007_11831_b200 import errors, sgdlab
+
+    assert sgdlab.theorem1_bound(0, 0.1, 1.0, 2.0, 0.5) == 2.0 + 0.1 * 0.5
+    assert sgdlab.theorem1_bound(3, 0.1, 1.0, 2.0, 0.0) == (0.9 ** 3) * 2.0
+    with _pt.raises(errors.InvalidStepSizeError):
+        sgdlab.theorem1_bound(1, 2.0, 1.0, 1.0, 1.0)
+    with _pt.raises(errors.ConfigurationError):
+        sgdlab.theorem1_bound(1, 0.1, 1.0, -1.0, 1.0)
