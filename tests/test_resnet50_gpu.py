@@ -222,3 +222,34 @@ def test_conv_separate_parity_classes_path(dev):
                         str(root / "tests" / "test_resnet50_gpu.py"), "-k", "conv_fwd_dgrad_wgrad or im2col_shapes"],
                        env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_resnet50_tiny_variable_batches(dev, B):
+    """DBS can hand a worker any batch size >= 1: ResNet-50 at b = 1 and 3 (tiles
+    mostly masked, BN over one image's pixels) stays within the bf16 noise floor."""
+    import torch
+
+    from paper_2007_11831_b200 import resnet
+
+    image, classes = 64, 16
+    params = tame_residual_branches(resnet.init_params(classes, 1, depth=50, image=image), 0.1)
+    model = resnet.ResnetModel(classes, depth=50, image=image, params=params)
+    sc = resnet.ResnetScratch(8, classes, depth=50, image=image)
+    X, y = resnet.synthetic_imagenet(B, image=image, classes=classes, seed=11)
+    x = torch.as_tensor(X, device=dev)
+    yl = torch.as_tensor(y, device=dev)
+    grad = torch.zeros(model.P, device=dev)
+    loss = torch.zeros(1, device=dev)
+    resnet.forward_backward(model, sc, x, yl, grad, loss)
+    torch.cuda.synchronize()
+    xr = (x.float() - 128.0) / 64.0
+    build, params_t = torch_resnet50(torch, model.host_tensors())
+    ref = torch.nn.functional.cross_entropy(build(xr), yl.long())
+    ref.backward()
+    assert float(loss) == pytest.approx(float(ref), rel=2e-2)
+    got = model.layout.unpack(grad.cpu().numpy())
+    fc = params_t[-2].grad.detach().cpu().numpy().astype(np.float64)
+    rel = np.linalg.norm(got[-2] - fc) / (np.linalg.norm(fc) + 1e-30)
+    assert rel < 0.05, rel
+    assert np.isfinite(grad.cpu().numpy()).all()

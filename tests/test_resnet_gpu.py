@@ -181,3 +181,29 @@ def test_param_layout_roundtrip(dev):
     back = L.unpack(L.pack(t))
     for a, b in zip(t, back):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("B", [1, 5])
+def test_resnet18_tiny_variable_batches(dev, B):
+    """ResNet-18 at b = 1 and 5 (partial M tiles everywhere) vs fp32 torch."""
+    import torch
+
+    from paper_2007_11831_b200 import resnet
+
+    model = resnet.ResnetModel(seed=4)
+    sc = resnet.ResnetScratch(8)
+    X, y = resnet.synthetic_cifar(B, seed=9)
+    x = torch.as_tensor(X, device=dev)
+    yl = torch.as_tensor(y, device=dev)
+    grad = torch.zeros(model.P, device=dev)
+    loss = torch.zeros(1, device=dev)
+    resnet.forward_backward(model, sc, x, yl, grad, loss)
+    torch.cuda.synchronize()
+    build, params = torch_resnet18(torch, model.host_tensors())
+    ref = torch.nn.functional.cross_entropy(build(x.to(torch.bfloat16).float()), yl.long())
+    ref.backward()
+    assert float(loss) == pytest.approx(float(ref), rel=3e-2)
+    got = model.layout.unpack(grad.cpu().numpy())
+    fc = params[-2].grad.detach().cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(got[-2] - fc) / (np.linalg.norm(fc) + 1e-30) < 0.05
+    assert np.isfinite(grad.cpu().numpy()).all()
