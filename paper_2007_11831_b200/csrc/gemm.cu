@@ -90,6 +90,7 @@ struct GemmParams {
   int halo_rows;        // halo variant: image rows per TMA box
   int halo_tpi;         // halo variant: tiles per image (ceil(OH (OW + 1) / 128))
   int64_t halo_tiles;   // halo variant: images x tiles per image
+  int d_trans;          // F32 atomic epilogue: D stored transposed (d[n * ldd + m])
 };
 
 // two floats -> packed bf16x2 (lo in bits 0..15), one round-to-nearest-even
@@ -152,6 +153,29 @@ __device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int
   ow = rem - oh * g.OW;
 }
 
+// (image, row, column) of a K-side pixel index advanced one 64-pixel k-block at a
+// time: the producer thread's per-k-block 64-bit divisions were on its critical path
+struct PixelCursor {
+  int n, oh, ow, dr, dc;
+  __device__ __forceinline__ void init(const ConvGeom& g, int64_t pix) {
+    pixel_coords(g, pix, n, oh, ow);
+    dr = kBK / g.OW;
+    dc = kBK - dr * g.OW;
+  }
+  __device__ __forceinline__ void advance(const ConvGeom& g) {
+    ow += dc;
+    oh += dr;
+    if (ow >= g.OW) {
+      ow -= g.OW;
+      oh++;
+    }
+    while (oh >= g.OH) {
+      oh -= g.OH;
+      n++;
+    }
+  }
+};
+
 __device__ __forceinline__ void ld_bf16x32(const uint16_t* src, float (&x)[32]) {
 #pragma unroll
   for (int j = 0; j < 32; j += 8) {
@@ -184,7 +208,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
   const bool f32_out = (epi == DBS_EPI_F32 || epi == DBS_EPI_F32_ACCUM || epi == DBS_EPI_BIAS_F32 ||
                         epi == DBS_EPI_F32_ATOMIC);
   const int align_elems = f32_out ? 4 : 8;
-  const bool fast = (cnt == 32) && (p.ldd % align_elems == 0) &&
+  const bool fast = (cnt == 32) && !p.d_trans && (p.ldd % align_elems == 0) &&
                     ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0) && (p.aux == nullptr || ((reinterpret_cast<uintptr_t>(p.aux) & 15) == 0)) &&
                     (p.bias == nullptr || ((reinterpret_cast<uintptr_t>(p.bias) & 15) == 0));
   if (!fast) {
@@ -272,7 +296,14 @@ __device__ void epilogue_chunk_generic(const GemmParams& p, int64_t row, int64_t
         for (int j = 0; j < 32; j++)
           if (j < cnt && n_base + j < N) d[j] += o[j];
       } else if (p.epi == DBS_EPI_F32_ATOMIC) {
-        if (vec) {
+        if (p.d_trans) {
+          // transposed weight gradient: column j of this row is d[(n_base + j) * ldd + row];
+          // consecutive lanes hold consecutive rows, so each reduction is warp-coalesced
+          float* dt = reinterpret_cast<float*>(p.d) + n_base * p.ldd + row;
+#pragma unroll
+          for (int j = 0; j < 32; j++)
+            if (j < cnt && n_base + j < N) atomicAdd(dt + j * p.ldd, o[j]);
+        } else if (vec) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             atomicAdd(reinterpret_cast<float4*>(d + j), make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]));
@@ -398,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t n_tiles = (p.N + BN - 1) / BN;
   const int64_t num_tiles = kHalo ? p.halo_tiles : (p.nclass > 0 ? p.cls_start[p.nclass] : m_tiles * n_tiles * p.splits);
   const int num_k_total = (int)((p.K + kBK - 1) / kBK);
-  const int a_mn = (p.a_mode == 1) ? 1 : 0;
+  const int a_mn = (p.a_mode == 1 || p.a_mode >= 5) ? 1 : 0;
   const int b_mn = (p.b_mode >= 1) ? 1 : 0;
   // tile t -> (m tile fastest, then n tile, then split-K slice): the tiles
   // resident at one time share their B block (and neighbouring A windows) in L2
@@ -492,6 +523,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       b_r = rs / p.gb.S;
       b_s = rs - b_r * p.gb.S;
     }
+    // transposed weight gradient: the tile's two 64-row halves are fixed (tap, channel block)s
+    int at_r[2] = {0, 0}, at_s[2] = {0, 0}, at_c[2] = {0, 0};
+    if (p.a_mode >= 5) {
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const int mj = (int)m0 + 64 * j;
+        const int rs = mj / p.ga.Cin;
+        at_c[j] = mj - rs * p.ga.Cin;
+        at_r[j] = rs / p.ga.S;
+        at_s[j] = rs - at_r[j] * p.ga.S;
+      }
+    }
+    const ConvGeom& gk = p.a_mode >= 5 ? p.ga : p.gb;  // geometry of a pixel-indexed K
+    PixelCursor pc{};
+    const bool k_pix = p.a_mode >= 5 || p.b_mode == 2 || p.b_mode == 4;
+    if (k_pix) pc.init(gk, (int64_t)kb_begin * kBK);
     if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
     if ((p.pair_a | p.pair_b) == 0) {
     for (int i = 0; i < num_k; i++, it++) {
@@ -502,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // MN-major A: the upper 64 rows of the tile are skipped when they lie past
       // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
       // accumulator rows the epilogue masks
-      const bool a_hi = (p.a_mode != 1) || (m0 + 64 < p.M);
+      const bool a_hi = (p.a_mode != 1 && p.a_mode < 5) || (m0 + 64 < p.M);
       mbar_arrive_expect_tx(&full[s], (a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes);
       const int32_t k0 = kb * kBK;
       uint8_t* a = sA + s * C::kABytes;
@@ -512,6 +559,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (p.a_mode == 1) {
         tma_load_2d(a, &tmA, &full[s], (int32_t)m0, k0);
         if (a_hi) tma_load_2d(a + 8192, &tmA, &full[s], (int32_t)m0 + 64, k0);
+      } else if (p.a_mode >= 5) {
+        // weight gradient, transposed: A[k = pixel][m = (r, s, c)] is the conv
+        // input window of 64 output pixels at tap (r, s), channels c .. c + 63 --
+        // one MN-major 64 x 64 box per 64-row half of the tile (mode 6: im2col TMA)
+        const ConvGeom& g = p.ga;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          if (j == 1 && !a_hi) break;
+          if (p.a_mode == 6)
+            tma_load_im2col_4d(a + j * 8192, &tmA, &full[s], at_c[j], pc.ow * g.stride - g.pad,
+                               pc.oh * g.stride - g.pad, pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
+          else
+            tma_load_4d(a + j * 8192, &tmA, &full[s], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
+                        pc.oh * g.stride + at_r[j] - g.pad, pc.n);
+        }
       } else if (p.a_mode == 4) {
         // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
         // the window corner, shifted by the tap; the tensor map's bounding box
@@ -564,21 +626,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
       } else if (p.b_mode == 4) {
         const ConvGeom& g = p.gb;
-        int bn_, boh, bow;
-        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
           tma_load_im2col_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride - g.pad,
                              boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
       } else {
         const ConvGeom& g = p.gb;
-        int bn_, boh, bow;
-        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
           tma_load_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
                       boh * g.stride + b_r - g.pad, bn_);
       }
+      if (k_pix) pc.advance(gk);
     }
     } else {
     // paired k-blocks (host guarantees an even k-block count per tile)
@@ -591,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // MN-major A: the upper 64 rows of the tile are skipped when they lie past
       // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
       // accumulator rows the epilogue masks
-      const bool a_hi = (p.a_mode != 1) || (m0 + 64 < p.M);
+      const bool a_hi = (p.a_mode != 1 && p.a_mode < 5) || (m0 + 64 < p.M);
       // a pair's bytes all complete on full[s0]; full[s0 + 1] gets a plain
       // arrival (the MMA reaches slot s0 + 1 only after full[s0] completed)
       mbar_arrive_expect_tx(&full[s0], npair * ((a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes));
@@ -604,7 +665,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t* b = sB + s * C::kBBytes;
       if (p.pair_a) {
         if (u == 0) {
-          if (p.a_mode == 0) {
+          if (p.a_mode >= 5) {
+            // transposed weight gradient: one 128-pixel box per 64-row half fills
+            // slot s0 + j with that half's k-blocks kb and kb + 1 (descriptor LBO 16 KB)
+            const ConvGeom& g = p.ga;
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+              if (j == 1 && !a_hi) break;
+              uint8_t* aj = sA + (s0 + j) * C::kABytes;
+              if (p.a_mode == 6)
+                tma_load_im2col_4d(aj, &tmA, &full[s0], at_c[j], pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+                                   pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
+              else
+                tma_load_4d(aj, &tmA, &full[s0], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
+                            pc.oh * g.stride + at_r[j] - g.pad, pc.n);
+            }
+          } else if (p.a_mode == 0) {
             tma_load_3d(a, &tmA, &full[s0], 0, (int32_t)m0, kb);
           } else if (p.a_mode == 1) {  // <= 64 rows: 128 k rows fill both halves of slot s0
             tma_load_2d(a, &tmA, &full[s0], (int32_t)m0, k0);
@@ -668,10 +744,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (u == 0) {
           if (p.b_mode == 0) {
             tma_load_3d(b, &tmB, &full[s0], 0, (int32_t)n0, kb);
+          } else if (p.b_mode == 1) {  // BN = 64, MN-major: 128 k rows fill the B parts of slots s0, s0 + 1
+            tma_load_2d(b, &tmB, &full[s0], (int32_t)n0, k0);
           } else if (p.b_mode == 2 || p.b_mode == 4) {  // BN = 64: 128 output pixels in one box
             const ConvGeom& g = p.gb;
-            int bn_, boh, bow;
-            pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+            const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
             if (p.b_mode == 4)
               tma_load_im2col_4d(b, &tmB, &full[s0], b_c0, bow * g.stride - g.pad, boh * g.stride - g.pad, bn_,
                                  (uint16_t)b_s, (uint16_t)b_r);
@@ -703,21 +780,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
       } else if (p.b_mode == 4) {
         const ConvGeom& g = p.gb;
-        int bn_, boh, bow;
-        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
           tma_load_im2col_4d(b + j * 8192, &tmB, &full[s0], b_c0 + 64 * j, bow * g.stride - g.pad,
                              boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
       } else {
         const ConvGeom& g = p.gb;
-        int bn_, boh, bow;
-        pixel_coords(g, (int64_t)k0, bn_, boh, bow);
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
           tma_load_4d(b + j * 8192, &tmB, &full[s0], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
                       boh * g.stride + b_r - g.pad, bn_);
       }
+      if (k_pix) pc.advance(gk);
       }
       it += npair;
       i += npair;
@@ -772,7 +848,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         j++;
       }
     } else {
-    const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), 8192, 1024) : make_sdesc(smem_u32(sA), 16, 1024);
+    const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), p.pair_a == 3 ? 16384 : 8192, 1024)
+                                  : make_sdesc(smem_u32(sA), 16, 1024);
     const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 1024) : make_sdesc(smem_u32(sB), 16, 1024);
     const uint32_t a_kstep = a_mn ? 128u : 2u, b_kstep = b_mn ? 128u : 2u;  // one UMMA_K step, 16 B units
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -792,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         // (pair_a == 2: an MN-major A of <= 64 rows whose paired box put k-block
         // kb + 1 in the unused upper half of slot s - 1)
-        const uint32_t a_off = p.pair_a == 2 ? (uint32_t)((s & ~1) * C::kABytes + (s & 1) * 8192)
+        const uint32_t a_off = p.pair_a >= 2 ? (uint32_t)((s & ~1) * C::kABytes + (s & 1) * 8192)
                                              : (uint32_t)(s * C::kABytes);
         const uint64_t a_s = a_desc0 + (uint64_t)(a_off >> 4);
         const uint64_t b_s = b_desc0 + (uint64_t)((s * C::kBBytes) >> 4);
@@ -929,6 +1006,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<uint4*>(dbase + orow_r * p.ldd) =
                     *reinterpret_cast<const uint4*>(st + rr * 20 + (lane & 3) * 4);
             }
+          }
+          __syncwarp();
+        } else if (p.d_trans) {
+          // transposed weight gradient: a 32x33 shared-memory transpose so that each
+          // reduction is a float4 over 4 consecutive rows of one column (8 per chunk
+          // instead of 32 scalar ones; the split-K slices all hit the same lines)
+#pragma unroll
+          for (int k = 0; k < 32; k++) tr[lane * 33 + k] = valid ? __uint_as_float(r[k]) : 0.0f;
+          if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+          __syncwarp();
+          const int rq = 4 * (lane & 7);
+          const int64_t mrow = m0 + q * 32 + rq;
+          float* dt = reinterpret_cast<float*>(p.d) + mrow;
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int col = 4 * u + (lane >> 3);
+            const float4 v4 = make_float4(tr[rq * 33 + col], tr[(rq + 1) * 33 + col], tr[(rq + 2) * 33 + col],
+                                          tr[(rq + 3) * 33 + col]);
+            if (col < cnt && mrow < p.M) atomicAdd(reinterpret_cast<float4*>(dt + (n_base + col) * p.ldd), v4);
           }
           __syncwarp();
         } else {
@@ -1654,7 +1750,32 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
   }
   // ---- A ----
   p.a_mode = c.a_mode;
-  if (c.a_mode == 2 && (force_im2col() || !pixel_box_fits(c.ga.OH, c.ga.OW, kBM))) {
+  p.d_trans = c.d_trans;
+  DBS_REQUIRE(!c.d_trans || (c.epi == DBS_EPI_F32_ATOMIC && c.M % 4 == 0 && c.ldd % 4 == 0 &&
+                             ((uintptr_t)c.d & 15) == 0),
+              DBS_ERR_ARGUMENT, "transposed D: atomic epilogue, M and ldd multiples of 4, 16-byte aligned D");
+  if (c.a_mode == 5) {
+    // transposed weight gradient: 64-pixel windows of the conv input per 64 rows of M
+    DBS_REQUIRE(c.ga.Cin % 64 == 0 && c.M == (int64_t)c.ga.R * c.ga.S * c.ga.Cin && c.b_mode == 1 && c.d_trans,
+                DBS_ERR_ARGUMENT, "transposed wgrad: bad call");
+    // paired: 128-pixel boxes for both operands (an even k-block count per split)
+    const bool tpair = kpair_enabled() && ((c.K + kBK - 1) / kBK) % 2 == 0;
+    const int kpx = tpair ? 2 * kBK : kBK;
+    if (force_im2col() || !pixel_box_fits(c.ga.OH, c.ga.OW, kpx)) {
+      st = make_tmap_im2col(&ta, c.a, c.ta, -c.ga.pad, c.ga.pad - (c.ga.R - 1), kpx, c.ga.stride);
+      p.a_mode = 6;
+    } else {
+      int bw, bh, bnn;
+      st = pixel_box(c.ga.OH, c.ga.OW, kpx, bw, bh, bnn);
+      if (st) return st;
+      st = make_tmap_nhwc(&ta, c.a, c.ta, bw, bh, bnn, c.ga.stride);
+    }
+    if (st) return st;
+    p.ga = c.ga;
+    p.pair_a = tpair ? 3 : 0;
+    p.pair_b = tpair ? 1 : 0;
+    pairing = false;
+  } else if (c.a_mode == 2 && (force_im2col() || !pixel_box_fits(c.ga.OH, c.ga.OW, kBM))) {
     const bool taps = c.taps.n > 0;
     st = make_tmap_im2col(&ta, c.a, c.ta, taps ? -1 : -c.ga.pad, taps ? -1 : c.ga.pad - (c.ga.R - 1), kBM,
                           c.ga.stride);
@@ -1728,7 +1849,7 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
       st = make_tmap_kpair(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, (uint32_t)bn);
       p.pair_b = 1;
     } else {
-      st = c.b_mode ? make_tmap(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, 64, 64)
+      st = c.b_mode ? make_tmap(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, 64, p.pair_b ? 128 : 64)
                     : make_tmap(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, 64, (uint32_t)bn);
     }
     if (st) return st;

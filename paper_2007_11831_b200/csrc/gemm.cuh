@@ -40,7 +40,8 @@ struct OutMap {
 
 struct ConvCall {
   int64_t M, N, K;
-  int a_mode, b_mode;        // 0 K-major 2-D, 1 MN-major 2-D, 2 conv 4-D
+  int a_mode, b_mode;        // 0 K-major 2-D, 1 MN-major 2-D, 2 conv 4-D;
+                             // A 5: the conv input as an MN-major A [k = pixel][m = (r, s, c)] (weight gradient)
   const void* a;
   int64_t lda;
   ConvTensor ta;
@@ -66,6 +67,7 @@ struct ConvCall {
   int nclass;
   ConvTaps cls_taps[4];
   OutMap cls_omap[4];
+  int d_trans;               // F32 atomic epilogue writes D transposed: d[n * ldd + m]
 };
 
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,

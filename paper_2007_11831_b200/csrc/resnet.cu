@@ -1098,10 +1098,52 @@ int conv_dgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* wb, in
   return conv_dgrad_ex(c, dy, wb + c.w_off, B, dx, accumulate, s);
 }
 
+bool wgrad_trans_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_WGRAD_T");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // dW of conv c (fp32 atomics into dw) from dy and the conv input x (stem: im2col columns)
 int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t B, float* dw, cudaStream_t s) {
   const int64_t pixels = B * c.OH * c.OW;
   ConvCall call{};
+  if (c.cout == 64 && c.cin % 64 == 0 && (c.k == 1 ? c.stride == 1 : true) && ((uintptr_t)dw & 15) == 0 &&
+      wgrad_trans_enabled()) {
+    // 64 output channels: dW^T = X^T dY puts the (r, s, c) reduction rows on the
+    // 128-row MMA M side (all rows live) instead of the 64 output channels (half
+    // of every M = 128 instruction wasted); the epilogue stores D transposed
+    call.M = (int64_t)c.k * c.k * c.cin;
+    call.N = c.cout;
+    call.K = pixels;
+    call.b_mode = 1;  // dY [pixels][Cout], MN-major
+    call.b = dy;
+    call.ldb = c.cout;
+    if (c.k == 1) {
+      call.a_mode = 1;  // X [pixels][Cin], MN-major
+      call.a = x;
+      call.lda = c.cin;
+    } else {
+      call.a_mode = 5;
+      call.a = x;
+      call.ta = nhwc(B, c.H, c.W, c.cin);
+      call.ga = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
+    }
+    call.epi = DBS_EPI_F32_ATOMIC;
+    call.d = dw;
+    call.ldd = call.M;
+    call.d_trans = 1;
+    call.bn_override = 64;
+    const int64_t tiles = (call.M + 127) / 128;
+    int64_t splits = current_sm_count() / tiles;
+    const int64_t kblocks = (call.K + 63) / 64;
+    if (splits > kblocks) splits = kblocks;
+    if (splits < 1) splits = 1;
+    call.splits = (int)splits;
+    return conv_gemm(call, s);
+  }
   call.a_mode = 1;  // dY^T: dY stored [pixels][Cout]
   call.a = dy;
   call.lda = c.cout;
@@ -1128,6 +1170,8 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
     bn = c.cin >= 256 ? 256 : c.cin;
     call.bn_override = bn;
   } else {
+    // N = (r, s, c): the tile must divide Cin so it never straddles two taps
+    // (a 192-channel input takes 64-wide tiles, not the 256-wide kernel)
     call.N = (int64_t)c.k * c.k * c.cin;
     call.K = pixels;
     call.b_mode = 2;
@@ -1135,7 +1179,7 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
     call.tb = nhwc(B, c.H, c.W, c.cin);
     call.gb = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
     call.ldd = call.N;
-    bn = c.cin >= 256 ? 256 : c.cin;
+    bn = c.cin % 256 == 0 ? 256 : (c.cin % 128 == 0 ? 128 : 64);
     call.bn_override = bn;
   }
   // split the long pixel reduction so the persistent GEMM's one round of

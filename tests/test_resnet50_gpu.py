@@ -34,6 +34,9 @@ SHAPES_R50 = [  # N, H, Cin, Cout, k, stride
     (2, 28, 64, 64, 3, 1),
     (7, 8, 64, 64, 3, 1),
     (3, 16, 128, 64, 3, 1),  # paired 128-pixel weight-gradient boxes (box mode), 4 tiles per image
+    (2, 56, 256, 64, 1, 1),  # 1x1 -> 64 channels: transposed weight gradient (X^T dY)
+    (3, 16, 64, 64, 1, 1),
+    (2, 20, 192, 64, 3, 1),  # transposed weight gradient with a half-empty last M tile (576 + 1152 rows)
 ]
 
 
@@ -209,6 +212,17 @@ def test_conv_halo_cta_pair_path(dev):
     env = dict(os.environ, DBS_HALO_PAIR="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                         str(root / "tests" / "test_resnet50_gpu.py"), "-k", "im2col_shapes or forward_backward"],
+                       env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_conv_untransposed_wgrad_path(dev):
+    """The 64-output-channel weight gradient in the dY^T X orientation
+    (DBS_WGRAD_T=0) on every conv shape."""
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBS_WGRAD_T="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", str(root / "tests" / "test_resnet_gpu.py"),
+                        str(root / "tests" / "test_resnet50_gpu.py"), "-k", "conv_fwd_dgrad_wgrad or im2col_shapes"],
                        env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
