@@ -91,6 +91,7 @@ struct GemmParams {
   int halo_tpi;         // halo variant: tiles per image (ceil(OH (OW + 1) / 128))
   int64_t halo_tiles;   // halo variant: images x tiles per image
   int d_trans;          // F32 atomic epilogue: D stored transposed (d[n * ldd + m])
+  int b_wide;           // flipped-filter B (mode 3): one 4-D box per k-block covers all BN / 64 channel blocks
 };
 
 // two floats -> packed bf16x2 (lo in bits 0..15), one round-to-nearest-even
@@ -399,6 +400,377 @@ __device__ __forceinline__ float warp_colsum(float (&x)[32], int lane) {
   return mine;
 }
 
+// tile t -> (m tile fastest, then n tile, then split-K slice): the tiles
+// resident at one time share their B block (and neighbouring A windows) in L2;
+// returns the tile's k-block count (merged parity classes: class c's own count)
+template <int BN>
+__device__ __forceinline__ int tile_decode(const GemmParams& p, int64_t t, int64_t m_tiles, int64_t n_tiles,
+                                           int num_k_total, int64_t& m0, int64_t& n0, int& kb_begin, int& cls) {
+  cls = -1;
+  if (p.nclass > 0) {  // merged classes: one N tile, no split-K
+    int c = 0;
+    while (c + 1 < p.nclass && t >= p.cls_start[c + 1]) c++;
+    cls = c;
+    m0 = (t - p.cls_start[c]) * kBM;
+    n0 = 0;
+    kb_begin = 0;
+    return p.cls_kb[c];
+  }
+  const int64_t rest = t / m_tiles;
+  m0 = (t - rest * m_tiles) * kBM;
+  const int64_t split = rest / n_tiles;
+  n0 = (rest - split * n_tiles) * BN;
+  kb_begin = (int)split * p.kb_per_split;
+  const int kb_end = min(kb_begin + p.kb_per_split, num_k_total);
+  return kb_end > kb_begin ? kb_end - kb_begin : 0;
+}
+
+// The non-halo TMA producer, specialised per operand-mode pair (AM / BMD < 0:
+// runtime modes).  The single producer thread is the latency-critical path of
+// the conv kernels: a compact loop with the other modes' branches compiled out
+// keeps it short (and its code local), instead of one loop over every mode.
+template <int BN, int AM, int BMD>
+__device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* tmA, const CUtensorMap* tmB, uint8_t* sA,
+                                        uint8_t* sB, uint64_t* full, uint64_t* empty, int64_t num_tiles, int64_t m_tiles,
+                                        int64_t n_tiles, int num_k_total) {
+  using C = Cfg<BN>;
+  constexpr int kStages = C::kStages;
+  const int am = AM >= 0 ? AM : p.a_mode;
+  const int bm = BMD >= 0 ? BMD : p.b_mode;
+  uint32_t it = 0;  // ring position, continuous across tiles
+  uint32_t pt = 0;
+  (void)pt;
+   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    int64_t m0, n0;
+    int kb_begin, cls;
+    const int num_k = tile_decode<BN>(p, t, m_tiles, n_tiles, num_k_total, m0, n0, kb_begin, cls);
+    const ConvTaps& tp = cls >= 0 ? p.cls_taps[cls] : p.taps;
+    int a_n = 0, a_oh = 0, a_ow = 0;
+    if (am == 2 || am == 4) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
+    int b_r = 0, b_s = 0, b_c0 = 0;
+    if (bm == 2 || bm == 4) {
+      const int rs = (int)(n0 / p.gb.Cin);
+      b_c0 = (int)(n0 - (int64_t)rs * p.gb.Cin);
+      b_r = rs / p.gb.S;
+      b_s = rs - b_r * p.gb.S;
+    }
+    // transposed weight gradient: the tile's two 64-row halves are fixed (tap, channel block)s
+    int at_r[2] = {0, 0}, at_s[2] = {0, 0}, at_c[2] = {0, 0};
+    if (am >= 5) {
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const int mj = (int)m0 + 64 * j;
+        const int rs = mj / p.ga.Cin;
+        at_c[j] = mj - rs * p.ga.Cin;
+        at_r[j] = rs / p.ga.S;
+        at_s[j] = rs - at_r[j] * p.ga.S;
+      }
+    }
+    const ConvGeom& gk = am >= 5 ? p.ga : p.gb;  // geometry of a pixel-indexed K
+    PixelCursor pc{};
+    const bool k_pix = am >= 5 || bm == 2 || bm == 4;
+    if (k_pix) pc.init(gk, (int64_t)kb_begin * kBK);
+    if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
+    if ((p.pair_a | p.pair_b) == 0) {
+    for (int i = 0; i < num_k; i++, it++) {
+      const int kb = kb_begin + i;
+      const int s = (int)(it % kStages);
+      mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+      if (it < 12) GEMM_TRACE(100 + it);
+      // MN-major A: the upper 64 rows of the tile are skipped when they lie past
+      // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
+      // accumulator rows the epilogue masks
+      const bool a_hi = (am != 1 && am < 5) || (m0 + 64 < p.M);
+      mbar_arrive_expect_tx(&full[s], (a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes);
+      const int32_t k0 = kb * kBK;
+      uint8_t* a = sA + s * C::kABytes;
+      uint8_t* b = sB + s * C::kBBytes;
+      if (am == 0) {
+        tma_load_2d(a, tmA, &full[s], k0, (int32_t)m0);
+      } else if (am == 1) {
+        tma_load_2d(a, tmA, &full[s], (int32_t)m0, k0);
+        if (a_hi) tma_load_2d(a + 8192, tmA, &full[s], (int32_t)m0 + 64, k0);
+      } else if (am >= 5) {
+        // weight gradient, transposed: A[k = pixel][m = (r, s, c)] is the conv
+        // input window of 64 output pixels at tap (r, s), channels c .. c + 63 --
+        // one MN-major 64 x 64 box per 64-row half of the tile (mode 6: im2col TMA)
+        const ConvGeom& g = p.ga;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          if (j == 1 && !a_hi) break;
+          if (am == 6)
+            tma_load_im2col_4d(a + j * 8192, tmA, &full[s], at_c[j], pc.ow * g.stride - g.pad,
+                               pc.oh * g.stride - g.pad, pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
+          else
+            tma_load_4d(a + j * 8192, tmA, &full[s], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
+                        pc.oh * g.stride + at_r[j] - g.pad, pc.n);
+        }
+        pc.advance(g);  // (only in the pixel-K branches: the producer thread is latency-critical)
+      } else if (am == 4) {
+        // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
+        // the window corner, shifted by the tap; the tensor map's bounding box
+        // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int h0, w0, oh, ow;
+        if (tp.n > 0) {
+          h0 = a_oh - 1;
+          w0 = a_ow - 1;
+          oh = tp.dh[rs] + 1;
+          ow = tp.dw[rs] + 1;
+        } else {
+          oh = rs / g.S;
+          ow = rs - oh * g.S;
+          h0 = a_oh * g.stride - g.pad;
+          w0 = a_ow * g.stride - g.pad;
+        }
+        tma_load_im2col_4d(a, tmA, &full[s], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+      } else {
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int ah, aw;
+        if (tp.n > 0) {
+          ah = a_oh + tp.dh[rs];
+          aw = a_ow + tp.dw[rs];
+        } else {
+          const int r = rs / g.S, sx = rs - r * g.S;
+          ah = a_oh * g.stride + r - g.pad;
+          aw = a_ow * g.stride + sx - g.pad;
+        }
+        tma_load_4d(a, tmA, &full[s], cb * 64, aw, ah, a_n);
+      }
+      if (bm == 0) {
+        tma_load_2d(b, tmB, &full[s], k0, (int32_t)n0);
+      } else if (bm == 1) {
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, tmB, &full[s], (int32_t)n0 + 64 * j, k0);
+      } else if (bm == 3) {
+        // input gradient: the filter W[k][r][s][c] read in place as the flipped,
+        // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        const int r = rs / g.S, sx = rs - r * g.S;
+        const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+        if (p.b_wide) {
+          tma_load_4d(b, tmB, &full[s], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
+        }
+      } else if (bm == 4) {
+        const ConvGeom& g = p.gb;
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_im2col_4d(b + j * 8192, tmB, &full[s], b_c0 + 64 * j, bow * g.stride - g.pad,
+                             boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
+        pc.advance(g);
+      } else {
+        const ConvGeom& g = p.gb;
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_4d(b + j * 8192, tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
+                      boh * g.stride + b_r - g.pad, bn_);
+        pc.advance(g);
+      }
+    }
+    } else {
+    // paired k-blocks (host guarantees an even k-block count per tile)
+    for (int i = 0; i < num_k;) {
+      constexpr int npair = 2;
+      const int s0 = (int)(it % kStages);
+      for (int u = 0; u < npair; u++)
+        mbar_wait(&empty[s0 + u], (((it + u) / kStages) & 1) ^ 1);
+      if (it < 12) GEMM_TRACE(100 + it);
+      // MN-major A: the upper 64 rows of the tile are skipped when they lie past
+      // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
+      // accumulator rows the epilogue masks
+      const bool a_hi = (am != 1 && am < 5) || (m0 + 64 < p.M);
+      // a pair's bytes all complete on full[s0]; full[s0 + 1] gets a plain
+      // arrival (the MMA reaches slot s0 + 1 only after full[s0] completed)
+      mbar_arrive_expect_tx(&full[s0], npair * ((a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes));
+      mbar_arrive(&full[s0 + 1]);
+      for (int u = 0; u < npair; u++) {
+      const int s = s0 + u;
+      const int kb = kb_begin + i + u;
+      const int32_t k0 = kb * kBK;
+      uint8_t* a = sA + s * C::kABytes;
+      uint8_t* b = sB + s * C::kBBytes;
+      if (p.pair_a) {
+        if (u == 0) {
+          if (am >= 5) {
+            // transposed weight gradient: one 128-pixel box per 64-row half fills
+            // slot s0 + j with that half's k-blocks kb and kb + 1 (descriptor LBO 16 KB)
+            const ConvGeom& g = p.ga;
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+              if (j == 1 && !a_hi) break;
+              uint8_t* aj = sA + (s0 + j) * C::kABytes;
+              if (am == 6)
+                tma_load_im2col_4d(aj, tmA, &full[s0], at_c[j], pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+                                   pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
+              else
+                tma_load_4d(aj, tmA, &full[s0], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
+                            pc.oh * g.stride + at_r[j] - g.pad, pc.n);
+            }
+            pc.advance(g);
+            pc.advance(g);
+          } else if (am == 0) {
+            tma_load_3d(a, tmA, &full[s0], 0, (int32_t)m0, kb);
+          } else if (am == 1) {  // <= 64 rows: 128 k rows fill both halves of slot s0
+            tma_load_2d(a, tmA, &full[s0], (int32_t)m0, k0);
+          } else {
+            const ConvGeom& g = p.ga;
+            const int cb = kb % g.cblocks;
+            const int rs = kb / g.cblocks;
+            int ah, aw;
+            if (tp.n > 0) {
+              ah = a_oh + tp.dh[rs];
+              aw = a_ow + tp.dw[rs];
+            } else {
+              const int r = rs / g.S, sx = rs - r * g.S;
+              ah = a_oh * g.stride + r - g.pad;
+              aw = a_ow * g.stride + sx - g.pad;
+            }
+            tma_load_5d(a, tmA, &full[s0], 0, aw, ah, a_n, cb);
+          }
+        }
+      } else if (am == 0) {
+        tma_load_2d(a, tmA, &full[s0], k0, (int32_t)m0);
+      } else if (am == 1) {
+        tma_load_2d(a, tmA, &full[s0], (int32_t)m0, k0);
+        if (a_hi) tma_load_2d(a + 8192, tmA, &full[s0], (int32_t)m0 + 64, k0);
+      } else if (am == 4) {
+        // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
+        // the window corner, shifted by the tap; the tensor map's bounding box
+        // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int h0, w0, oh, ow;
+        if (tp.n > 0) {
+          h0 = a_oh - 1;
+          w0 = a_ow - 1;
+          oh = tp.dh[rs] + 1;
+          ow = tp.dw[rs] + 1;
+        } else {
+          oh = rs / g.S;
+          ow = rs - oh * g.S;
+          h0 = a_oh * g.stride - g.pad;
+          w0 = a_ow * g.stride - g.pad;
+        }
+        tma_load_im2col_4d(a, tmA, &full[s0], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+      } else {
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        int ah, aw;
+        if (tp.n > 0) {
+          ah = a_oh + tp.dh[rs];
+          aw = a_ow + tp.dw[rs];
+        } else {
+          const int r = rs / g.S, sx = rs - r * g.S;
+          ah = a_oh * g.stride + r - g.pad;
+          aw = a_ow * g.stride + sx - g.pad;
+        }
+        tma_load_4d(a, tmA, &full[s0], cb * 64, aw, ah, a_n);
+      }
+      if (p.pair_b) {
+        if (u == 0) {
+          if (bm == 0) {
+            tma_load_3d(b, tmB, &full[s0], 0, (int32_t)n0, kb);
+          } else if (bm == 1) {  // BN = 64, MN-major: 128 k rows fill the B parts of slots s0, s0 + 1
+            tma_load_2d(b, tmB, &full[s0], (int32_t)n0, k0);
+          } else if (bm == 2 || bm == 4) {  // BN = 64: 128 output pixels in one box
+            const ConvGeom& g = p.gb;
+            const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
+            if (bm == 4)
+              tma_load_im2col_4d(b, tmB, &full[s0], b_c0, bow * g.stride - g.pad, boh * g.stride - g.pad, bn_,
+                                 (uint16_t)b_s, (uint16_t)b_r);
+            else
+              tma_load_4d(b, tmB, &full[s0], b_c0, bow * g.stride + b_s - g.pad, boh * g.stride + b_r - g.pad, bn_);
+            pc.advance(g);
+            pc.advance(g);
+          } else {  // mode 3, BN = 64: the two k-blocks are consecutive 64-row k ranges
+            const ConvGeom& g = p.ga;
+            const int cb = kb % g.cblocks;
+            const int rs = kb / g.cblocks;
+            const int r = rs / g.S, sx = rs - r * g.S;
+            const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+            tma_load_3d(b, tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
+          }
+        }
+      } else if (bm == 0) {
+        tma_load_2d(b, tmB, &full[s0], k0, (int32_t)n0);
+      } else if (bm == 1) {
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, tmB, &full[s0], (int32_t)n0 + 64 * j, k0);
+      } else if (bm == 3) {
+        // input gradient: the filter W[k][r][s][c] read in place as the flipped,
+        // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
+        const ConvGeom& g = p.ga;
+        const int cb = kb % g.cblocks;
+        const int rs = kb / g.cblocks;
+        const int r = rs / g.S, sx = rs - r * g.S;
+        const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
+        if (p.b_wide) {
+          tma_load_4d(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
+        }
+      } else if (bm == 4) {
+        const ConvGeom& g = p.gb;
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_im2col_4d(b + j * 8192, tmB, &full[s0], b_c0 + 64 * j, bow * g.stride - g.pad,
+                             boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
+        pc.advance(g);
+      } else {
+        const ConvGeom& g = p.gb;
+        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
+#pragma unroll
+        for (int j = 0; j < BN / 64; j++)
+          tma_load_4d(b + j * 8192, tmB, &full[s0], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
+                      boh * g.stride + b_r - g.pad, bn_);
+        pc.advance(g);
+      }
+      }
+      it += npair;
+      i += npair;
+    }
+    }
+   }
+}
+
+template <int BN>
+__device__ __forceinline__ void produce_dispatch(const GemmParams& p, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                                 uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
+                                                 int64_t num_tiles, int64_t m_tiles, int64_t n_tiles, int num_k_total) {
+#define DBS_PRODUCE(A, B) produce<BN, A, B>(p, tmA, tmB, sA, sB, full, empty, num_tiles, m_tiles, n_tiles, num_k_total)
+  if constexpr (BN == 16) {
+    DBS_PRODUCE(-1, -1);
+  } else {
+    switch (p.a_mode * 8 + p.b_mode) {
+      case 2 * 8 + 0: DBS_PRODUCE(2, 0); break;  // conv forward, 4-D box A
+      case 4 * 8 + 0: DBS_PRODUCE(4, 0); break;  // conv forward, im2col A
+      case 2 * 8 + 3: DBS_PRODUCE(2, 3); break;  // input gradient (flipped filter B)
+      case 4 * 8 + 3: DBS_PRODUCE(4, 3); break;
+      case 1 * 8 + 2: DBS_PRODUCE(1, 2); break;  // weight gradient dY^T im2col(X)
+      case 1 * 8 + 4: DBS_PRODUCE(1, 4); break;
+      case 5 * 8 + 1: DBS_PRODUCE(5, 1); break;  // transposed weight gradient X^T dY
+      case 6 * 8 + 1: DBS_PRODUCE(6, 1); break;
+      default: DBS_PRODUCE(-1, -1); break;       // plain GEMMs (modes 0 / 1)
+    }
+  }
+#undef DBS_PRODUCE
+}
+
 template <int BN, bool kHalo>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
@@ -435,24 +807,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // resident at one time share their B block (and neighbouring A windows) in L2
   // tile t -> (m0, n0, first k-block, class); returns the tile's k-block count
   auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& kb_begin, int& cls) -> int {
-    cls = -1;
-    if (p.nclass > 0) {  // merged classes: one N tile, no split-K
-      int c = 0;
-      while (c + 1 < p.nclass && t >= p.cls_start[c + 1]) c++;
-      cls = c;
-      m0 = (t - p.cls_start[c]) * kBM;
-      n0 = 0;
-      kb_begin = 0;
-      return p.cls_kb[c];
-    }
-    const int64_t rest = t / m_tiles;
-    m0 = (t - rest * m_tiles) * kBM;
-    const int64_t split = rest / n_tiles;
-    n0 = (rest - split * n_tiles) * BN;
-    kb_begin = (int)split * p.kb_per_split;
-    const int kb_end = min(kb_begin + p.kb_per_split, num_k_total);
-    return kb_end > kb_begin ? kb_end - kb_begin : 0;
+    return tile_decode<BN>(p, t, m_tiles, n_tiles, num_k_total, m0, n0, kb_begin, cls);
   };
+
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -509,297 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_4d(sA + s * kSlotA, &tmA, &full[s], 0, -1, P0 / W1 - 1, img);
     }
    } else {
-   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-    int64_t m0, n0;
-    int kb_begin, cls;
-    const int num_k = decode(t, m0, n0, kb_begin, cls);
-    const ConvTaps& tp = cls >= 0 ? p.cls_taps[cls] : p.taps;
-    int a_n = 0, a_oh = 0, a_ow = 0;
-    if (p.a_mode == 2 || p.a_mode == 4) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
-    int b_r = 0, b_s = 0, b_c0 = 0;
-    if (p.b_mode == 2 || p.b_mode == 4) {
-      const int rs = (int)(n0 / p.gb.Cin);
-      b_c0 = (int)(n0 - (int64_t)rs * p.gb.Cin);
-      b_r = rs / p.gb.S;
-      b_s = rs - b_r * p.gb.S;
-    }
-    // transposed weight gradient: the tile's two 64-row halves are fixed (tap, channel block)s
-    int at_r[2] = {0, 0}, at_s[2] = {0, 0}, at_c[2] = {0, 0};
-    if (p.a_mode >= 5) {
-#pragma unroll
-      for (int j = 0; j < 2; j++) {
-        const int mj = (int)m0 + 64 * j;
-        const int rs = mj / p.ga.Cin;
-        at_c[j] = mj - rs * p.ga.Cin;
-        at_r[j] = rs / p.ga.S;
-        at_s[j] = rs - at_r[j] * p.ga.S;
-      }
-    }
-    const ConvGeom& gk = p.a_mode >= 5 ? p.ga : p.gb;  // geometry of a pixel-indexed K
-    PixelCursor pc{};
-    const bool k_pix = p.a_mode >= 5 || p.b_mode == 2 || p.b_mode == 4;
-    if (k_pix) pc.init(gk, (int64_t)kb_begin * kBK);
-    if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
-    if ((p.pair_a | p.pair_b) == 0) {
-    for (int i = 0; i < num_k; i++, it++) {
-      const int kb = kb_begin + i;
-      const int s = (int)(it % kStages);
-      mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-      if (it < 12) GEMM_TRACE(100 + it);
-      // MN-major A: the upper 64 rows of the tile are skipped when they lie past
-      // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
-      // accumulator rows the epilogue masks
-      const bool a_hi = (p.a_mode != 1 && p.a_mode < 5) || (m0 + 64 < p.M);
-      mbar_arrive_expect_tx(&full[s], (a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes);
-      const int32_t k0 = kb * kBK;
-      uint8_t* a = sA + s * C::kABytes;
-      uint8_t* b = sB + s * C::kBBytes;
-      if (p.a_mode == 0) {
-        tma_load_2d(a, &tmA, &full[s], k0, (int32_t)m0);
-      } else if (p.a_mode == 1) {
-        tma_load_2d(a, &tmA, &full[s], (int32_t)m0, k0);
-        if (a_hi) tma_load_2d(a + 8192, &tmA, &full[s], (int32_t)m0 + 64, k0);
-      } else if (p.a_mode >= 5) {
-        // weight gradient, transposed: A[k = pixel][m = (r, s, c)] is the conv
-        // input window of 64 output pixels at tap (r, s), channels c .. c + 63 --
-        // one MN-major 64 x 64 box per 64-row half of the tile (mode 6: im2col TMA)
-        const ConvGeom& g = p.ga;
-#pragma unroll
-        for (int j = 0; j < 2; j++) {
-          if (j == 1 && !a_hi) break;
-          if (p.a_mode == 6)
-            tma_load_im2col_4d(a + j * 8192, &tmA, &full[s], at_c[j], pc.ow * g.stride - g.pad,
-                               pc.oh * g.stride - g.pad, pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
-          else
-            tma_load_4d(a + j * 8192, &tmA, &full[s], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
-                        pc.oh * g.stride + at_r[j] - g.pad, pc.n);
-        }
-      } else if (p.a_mode == 4) {
-        // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
-        // the window corner, shifted by the tap; the tensor map's bounding box
-        // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
-        const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        int h0, w0, oh, ow;
-        if (tp.n > 0) {
-          h0 = a_oh - 1;
-          w0 = a_ow - 1;
-          oh = tp.dh[rs] + 1;
-          ow = tp.dw[rs] + 1;
-        } else {
-          oh = rs / g.S;
-          ow = rs - oh * g.S;
-          h0 = a_oh * g.stride - g.pad;
-          w0 = a_ow * g.stride - g.pad;
-        }
-        tma_load_im2col_4d(a, &tmA, &full[s], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
-      } else {
-        const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        int ah, aw;
-        if (tp.n > 0) {
-          ah = a_oh + tp.dh[rs];
-          aw = a_ow + tp.dw[rs];
-        } else {
-          const int r = rs / g.S, sx = rs - r * g.S;
-          ah = a_oh * g.stride + r - g.pad;
-          aw = a_ow * g.stride + sx - g.pad;
-        }
-        tma_load_4d(a, &tmA, &full[s], cb * 64, aw, ah, a_n);
-      }
-      if (p.b_mode == 0) {
-        tma_load_2d(b, &tmB, &full[s], k0, (int32_t)n0);
-      } else if (p.b_mode == 1) {
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, k0);
-      } else if (p.b_mode == 3) {
-        // input gradient: the filter W[k][r][s][c] read in place as the flipped,
-        // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
-        const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        const int r = rs / g.S, sx = rs - r * g.S;
-        const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
-      } else if (p.b_mode == 4) {
-        const ConvGeom& g = p.gb;
-        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++)
-          tma_load_im2col_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride - g.pad,
-                             boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
-      } else {
-        const ConvGeom& g = p.gb;
-        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++)
-          tma_load_4d(b + j * 8192, &tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
-                      boh * g.stride + b_r - g.pad, bn_);
-      }
-      if (k_pix) pc.advance(gk);
-    }
-    } else {
-    // paired k-blocks (host guarantees an even k-block count per tile)
-    for (int i = 0; i < num_k;) {
-      constexpr int npair = 2;
-      const int s0 = (int)(it % kStages);
-      for (int u = 0; u < npair; u++)
-        mbar_wait(&empty[s0 + u], (((it + u) / kStages) & 1) ^ 1);
-      if (it < 12) GEMM_TRACE(100 + it);
-      // MN-major A: the upper 64 rows of the tile are skipped when they lie past
-      // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
-      // accumulator rows the epilogue masks
-      const bool a_hi = (p.a_mode != 1 && p.a_mode < 5) || (m0 + 64 < p.M);
-      // a pair's bytes all complete on full[s0]; full[s0 + 1] gets a plain
-      // arrival (the MMA reaches slot s0 + 1 only after full[s0] completed)
-      mbar_arrive_expect_tx(&full[s0], npair * ((a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes));
-      mbar_arrive(&full[s0 + 1]);
-      for (int u = 0; u < npair; u++) {
-      const int s = s0 + u;
-      const int kb = kb_begin + i + u;
-      const int32_t k0 = kb * kBK;
-      uint8_t* a = sA + s * C::kABytes;
-      uint8_t* b = sB + s * C::kBBytes;
-      if (p.pair_a) {
-        if (u == 0) {
-          if (p.a_mode >= 5) {
-            // transposed weight gradient: one 128-pixel box per 64-row half fills
-            // slot s0 + j with that half's k-blocks kb and kb + 1 (descriptor LBO 16 KB)
-            const ConvGeom& g = p.ga;
-#pragma unroll
-            for (int j = 0; j < 2; j++) {
-              if (j == 1 && !a_hi) break;
-              uint8_t* aj = sA + (s0 + j) * C::kABytes;
-              if (p.a_mode == 6)
-                tma_load_im2col_4d(aj, &tmA, &full[s0], at_c[j], pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
-                                   pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
-              else
-                tma_load_4d(aj, &tmA, &full[s0], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
-                            pc.oh * g.stride + at_r[j] - g.pad, pc.n);
-            }
-          } else if (p.a_mode == 0) {
-            tma_load_3d(a, &tmA, &full[s0], 0, (int32_t)m0, kb);
-          } else if (p.a_mode == 1) {  // <= 64 rows: 128 k rows fill both halves of slot s0
-            tma_load_2d(a, &tmA, &full[s0], (int32_t)m0, k0);
-          } else {
-            const ConvGeom& g = p.ga;
-            const int cb = kb % g.cblocks;
-            const int rs = kb / g.cblocks;
-            int ah, aw;
-            if (tp.n > 0) {
-              ah = a_oh + tp.dh[rs];
-              aw = a_ow + tp.dw[rs];
-            } else {
-              const int r = rs / g.S, sx = rs - r * g.S;
-              ah = a_oh * g.stride + r - g.pad;
-              aw = a_ow * g.stride + sx - g.pad;
-            }
-            tma_load_5d(a, &tmA, &full[s0], 0, aw, ah, a_n, cb);
-          }
-        }
-      } else if (p.a_mode == 0) {
-        tma_load_2d(a, &tmA, &full[s0], k0, (int32_t)m0);
-      } else if (p.a_mode == 1) {
-        tma_load_2d(a, &tmA, &full[s0], (int32_t)m0, k0);
-        if (a_hi) tma_load_2d(a + 8192, &tmA, &full[s0], (int32_t)m0 + 64, k0);
-      } else if (p.a_mode == 4) {
-        // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
-        // the window corner, shifted by the tap; the tensor map's bounding box
-        // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
-        const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        int h0, w0, oh, ow;
-        if (tp.n > 0) {
-          h0 = a_oh - 1;
-          w0 = a_ow - 1;
-          oh = tp.dh[rs] + 1;
-          ow = tp.dw[rs] + 1;
-        } else {
-          oh = rs / g.S;
-          ow = rs - oh * g.S;
-          h0 = a_oh * g.stride - g.pad;
-          w0 = a_ow * g.stride - g.pad;
-        }
-        tma_load_im2col_4d(a, &tmA, &full[s0], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
-      } else {
-        const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        int ah, aw;
-        if (tp.n > 0) {
-          ah = a_oh + tp.dh[rs];
-          aw = a_ow + tp.dw[rs];
-        } else {
-          const int r = rs / g.S, sx = rs - r * g.S;
-          ah = a_oh * g.stride + r - g.pad;
-          aw = a_ow * g.stride + sx - g.pad;
-        }
-        tma_load_4d(a, &tmA, &full[s0], cb * 64, aw, ah, a_n);
-      }
-      if (p.pair_b) {
-        if (u == 0) {
-          if (p.b_mode == 0) {
-            tma_load_3d(b, &tmB, &full[s0], 0, (int32_t)n0, kb);
-          } else if (p.b_mode == 1) {  // BN = 64, MN-major: 128 k rows fill the B parts of slots s0, s0 + 1
-            tma_load_2d(b, &tmB, &full[s0], (int32_t)n0, k0);
-          } else if (p.b_mode == 2 || p.b_mode == 4) {  // BN = 64: 128 output pixels in one box
-            const ConvGeom& g = p.gb;
-            const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
-            if (p.b_mode == 4)
-              tma_load_im2col_4d(b, &tmB, &full[s0], b_c0, bow * g.stride - g.pad, boh * g.stride - g.pad, bn_,
-                                 (uint16_t)b_s, (uint16_t)b_r);
-            else
-              tma_load_4d(b, &tmB, &full[s0], b_c0, bow * g.stride + b_s - g.pad, boh * g.stride + b_r - g.pad, bn_);
-          } else {  // mode 3, BN = 64: the two k-blocks are consecutive 64-row k ranges
-            const ConvGeom& g = p.ga;
-            const int cb = kb % g.cblocks;
-            const int rs = kb / g.cblocks;
-            const int r = rs / g.S, sx = rs - r * g.S;
-            const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
-            tma_load_3d(b, &tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
-          }
-        }
-      } else if (p.b_mode == 0) {
-        tma_load_2d(b, &tmB, &full[s0], k0, (int32_t)n0);
-      } else if (p.b_mode == 1) {
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, &tmB, &full[s0], (int32_t)n0 + 64 * j, k0);
-      } else if (p.b_mode == 3) {
-        // input gradient: the filter W[k][r][s][c] read in place as the flipped,
-        // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
-        const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        const int r = rs / g.S, sx = rs - r * g.S;
-        const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, &tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
-      } else if (p.b_mode == 4) {
-        const ConvGeom& g = p.gb;
-        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++)
-          tma_load_im2col_4d(b + j * 8192, &tmB, &full[s0], b_c0 + 64 * j, bow * g.stride - g.pad,
-                             boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
-      } else {
-        const ConvGeom& g = p.gb;
-        const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
-#pragma unroll
-        for (int j = 0; j < BN / 64; j++)
-          tma_load_4d(b + j * 8192, &tmB, &full[s0], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
-                      boh * g.stride + b_r - g.pad, bn_);
-      }
-      if (k_pix) pc.advance(gk);
-      }
-      it += npair;
-      i += npair;
-    }
-    }
-   }
+   produce_dispatch<BN>(p, &tmA, &tmB, sA, sB, full, empty, num_tiles, m_tiles, n_tiles, num_k_total);
    }
     }
     __syncwarp();
@@ -1583,6 +1650,14 @@ int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, 
 
 }  // namespace
 
+bool wide_filter_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_WIDE_FILTER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool halo_fits(int OH, int OW) {
   const int W1 = OW + 1;
   const int rows = (OW + kBM - 1) / W1 + 3;
@@ -1834,13 +1909,29 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
                 "dgrad filter view: Cin, Cout multiples of 64 required");
     // BN = 64: two consecutive 64-row k blocks of one tap are one box of 128 k rows
     const bool pb = pairing && bn == 64 && c.ga.cblocks % 2 == 0;
-    cuuint64_t dims[3] = {(cuuint64_t)c.tb.C, (cuuint64_t)c.tb.W, (cuuint64_t)c.tb.N};
-    cuuint64_t strides[2] = {(cuuint64_t)c.tb.C * 2, (cuuint64_t)c.tb.W * c.tb.C * 2};
-    cuuint32_t box[3] = {64, 1, pb ? 128u : 64u};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.b), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // BN >= 128: the view {64 c, Cout k, Cin / 64 c-blocks, R*S} takes all BN / 64
+    // channel blocks of one k-block in ONE box, landing as consecutive 64 k x 64 c
+    // MN-major chunks (one TMA operation instead of BN / 64)
+    const bool wide = bn >= 128 && wide_filter_enabled();
+    CUresult r;
+    if (wide) {
+      cuuint64_t dims[4] = {64, (cuuint64_t)c.tb.N, (cuuint64_t)c.tb.C / 64, (cuuint64_t)c.tb.W};
+      cuuint64_t strides[3] = {(cuuint64_t)c.tb.W * c.tb.C * 2, 128, (cuuint64_t)c.tb.C * 2};
+      cuuint32_t box[4] = {64, 64, (cuuint32_t)(bn / 64), 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(c.b), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      p.b_wide = 1;
+    } else {
+      cuuint64_t dims[3] = {(cuuint64_t)c.tb.C, (cuuint64_t)c.tb.W, (cuuint64_t)c.tb.N};
+      cuuint64_t strides[2] = {(cuuint64_t)c.tb.C * 2, (cuuint64_t)c.tb.W * c.tb.C * 2};
+      cuuint32_t box[3] = {64, 1, pb ? 128u : 64u};
+      cuuint32_t es[3] = {1, 1, 1};
+      r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.b), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (3d filter) failed (%d)", (int)r);
     DBS_REQUIRE(c.a_mode == 2, DBS_ERR_ARGUMENT, "flipped-filter B needs a conv-mode A");
     p.pair_b = pb;
