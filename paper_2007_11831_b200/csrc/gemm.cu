@@ -37,6 +37,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -955,6 +956,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
   // ---------------- epilogue (warps 2..5) ----------------
+  // two compiled copies: plain bf16 output with every chunk staged (conv forward /
+  // input gradient -- the hot case, compact code) and everything else
+  __shared__ float red_s[4][32], red_q[4][32];  // per-warp BN-statistics partials (both copies)
+  auto epilogue_loop = [&](auto kst) {
+  constexpr bool kSt = decltype(kst)::value;
   const int q = warp & 3;  // the TMEM lane quadrant this warp may access
   float* tr = sEpi + (warp - 2) * (32 * 33);
   uint32_t tj = 0;
@@ -1011,13 +1017,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the TMEM registers and staged through shared memory so each store
         // instruction writes 8 rows x 64 contiguous bytes (the epilogue warps are
         // alone on their schedulers: instruction count is the epilogue's cost)
-        const bool staged = (p.epi == DBS_EPI_BF16) && (cnt == 32) && (p.colsum_part == nullptr) &&
-                            (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
+        // (kSt: the host-checked all-chunks-staged case, compiled without the other paths)
+        constexpr bool staged = kSt;
+        (void)cnt;
         if (stats) {
           // BN batch statistics: warp column sums (a 32x33 transpose in shared
           // memory: 32 stores + 32 loads instead of 160 shuffles) -> tile sums
           // over the 4 epilogue warps -> one fp64 atomic per column and tile
-          __shared__ float red_s[4][32], red_q[4][32];
           // one transpose: lane j reads column j and forms both sums
 #pragma unroll
           for (int k = 0; k < 32; k++) tr[lane * 33 + k] = valid ? __uint_as_float(r[k]) : 0.0f;
@@ -1131,6 +1137,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2 && lane == 0) GEMM_TRACE(52 + tj);
     tj++;
   }
+  };
+  const bool all_staged = BN >= 32 && p.epi == DBS_EPI_BF16 && p.colsum_part == nullptr && !p.d_trans &&
+                          p.N % 32 == 0 && p.ldd % 8 == 0 && ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
+  if (all_staged)
+    epilogue_loop(std::true_type{});
+  else
+    epilogue_loop(std::false_type{});
   }
   tc_fence_before();
   __syncthreads();
