@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/dbs_b200.h"
@@ -32,6 +33,15 @@ void count_launch();
 // pdl_wait() before touching memory the predecessor produces or consumes
 // (griddepcontrol.wait returns once the predecessor grid has completed and its
 // writes are visible -- a no-op for a launch without the attribute).
+// DBS_PDL=0: plain stream-ordered launches (profiling: per-kernel times without the
+// early-launched waiting that programmatic dependent launch folds into them)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -44,7 +54,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 // let the next PDL launch on the stream begin its prologue, then wait for ours
