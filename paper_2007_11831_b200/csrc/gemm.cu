@@ -702,7 +702,10 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
             const int rs = kb / g.cblocks;
             const int r = rs / g.S, sx = rs - r * g.S;
             const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
-            tma_load_3d(b, tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
+            if (p.b_wide)  // BN >= 128: all channel blocks x 128 k rows in one 4-D box (pair_b 3)
+              tma_load_4d(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
+            else
+              tma_load_3d(b, tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
           }
         }
       } else if (bm == 0) {
@@ -918,7 +921,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
     const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), p.pair_a == 3 ? 16384 : 8192, 1024)
                                   : make_sdesc(smem_u32(sA), 16, 1024);
-    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 1024) : make_sdesc(smem_u32(sB), 16, 1024);
+    // (pair_b == 3: a paired wide flipped-filter box put the 64-channel blocks 16 KB
+    // apart, k-block kb + 1 8 KB after kb)
+    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), p.pair_b == 3 ? 16384 : 8192, 1024)
+                                  : make_sdesc(smem_u32(sB), 16, 1024);
     const uint32_t a_kstep = a_mn ? 128u : 2u, b_kstep = b_mn ? 128u : 2u;  // one UMMA_K step, 16 B units
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int64_t m0, n0;
@@ -940,7 +946,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t a_off = p.pair_a >= 2 ? (uint32_t)((s & ~1) * C::kABytes + (s & 1) * 8192)
                                              : (uint32_t)(s * C::kABytes);
         const uint64_t a_s = a_desc0 + (uint64_t)(a_off >> 4);
-        const uint64_t b_s = b_desc0 + (uint64_t)((s * C::kBBytes) >> 4);
+        const uint32_t b_off = p.pair_b == 3 ? (uint32_t)((s & ~1) * C::kBBytes + (s & 1) * 8192)
+                                             : (uint32_t)(s * C::kBBytes);
+        const uint64_t b_s = b_desc0 + (uint64_t)(b_off >> 4);
 #pragma unroll
         for (int k = 0; k < kBK / 16; k++)
           mma_bf16_ss(d_tmem, a_s + (uint64_t)(k * a_kstep), b_s + (uint64_t)(k * b_kstep), idesc,
@@ -1926,11 +1934,13 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     // channel blocks of one k-block in ONE box, landing as consecutive 64 k x 64 c
     // MN-major chunks (one TMA operation instead of BN / 64)
     const bool wide = bn >= 128 && wide_filter_enabled();
+    // ... and with paired k-blocks, 128 k rows per box (channel blocks 16 KB apart)
+    const bool wpb = wide && pairing && c.ga.cblocks % 2 == 0;
     CUresult r;
     if (wide) {
       cuuint64_t dims[4] = {64, (cuuint64_t)c.tb.N, (cuuint64_t)c.tb.C / 64, (cuuint64_t)c.tb.W};
       cuuint64_t strides[3] = {(cuuint64_t)c.tb.W * c.tb.C * 2, 128, (cuuint64_t)c.tb.C * 2};
-      cuuint32_t box[4] = {64, 64, (cuuint32_t)(bn / 64), 1};
+      cuuint32_t box[4] = {64, wpb ? 128u : 64u, (cuuint32_t)(bn / 64), 1};
       cuuint32_t es[4] = {1, 1, 1, 1};
       r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(c.b), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1947,7 +1957,7 @@ int conv_gemm(const ConvCall& c, cudaStream_t s) {
     }
     DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (3d filter) failed (%d)", (int)r);
     DBS_REQUIRE(c.a_mode == 2, DBS_ERR_ARGUMENT, "flipped-filter B needs a conv-mode A");
-    p.pair_b = pb;
+    p.pair_b = wpb ? 3 : pb;
   } else {
     if (c.b_mode == 0 && pairing && c.K % 128 == 0 && (c.ldb * 2) % 16 == 0) {
       st = make_tmap_kpair(&tb, c.b, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldb, (uint32_t)bn);
