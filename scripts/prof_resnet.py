@@ -40,6 +40,16 @@ if mode == "single":
         for _ in range(2): resnet.forward_backward(m, sc, x, yl, g, loss)
         torch.cuda.synchronize()
     summarize(prof, "single worker B=128 x2")
+elif mode == "part":
+    # the bench layout: 3 workers on disjoint 48-SM partitions, 170 samples each
+    X, y = resnet.synthetic_cifar(8000, seed=0)
+    tr = SimulatedTrainer(X, y, n_workers=3, model="resnet18", partition=True, graphs=False, max_batch=210)
+    tr.run(cluster.StrategyConfig("fixed_ssgd", 510), n_epochs=1, max_iters=2)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        r = tr.run(cluster.StrategyConfig("fixed_ssgd", 510), n_epochs=1, max_iters=4)
+        torch.cuda.synchronize()
+    summarize(prof, "trainer 3 workers x 48 SMs, 4 iterations")
 else:
     X, y = resnet.synthetic_cifar(8000, seed=0)
     tr = SimulatedTrainer(X, y, n_workers=4, model="resnet18", partition=False, graphs=False, max_batch=512)
