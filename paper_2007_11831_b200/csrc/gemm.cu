@@ -148,11 +148,13 @@ struct HaloCfg {
 };
 
 __device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int& n, int& oh, int& ow) {
-  const int64_t hw = (int64_t)g.OH * g.OW;
-  n = (int)(pix / hw);
-  const int rem = (int)(pix - (int64_t)n * hw);
-  oh = rem / g.OW;
-  ow = rem - oh * g.OW;
+  // 32-bit arithmetic: conv GEMM rows / pixel-K extents are < 2^31 (checked by conv_gemm)
+  const uint32_t hw = (uint32_t)(g.OH * g.OW), p32 = (uint32_t)pix;
+  const uint32_t nn = p32 / hw;
+  const uint32_t rem = p32 - nn * hw;
+  n = (int)nn;
+  oh = (int)(rem / (uint32_t)g.OW);
+  ow = (int)rem - oh * g.OW;
 }
 
 // (image, row, column) of a K-side pixel index advanced one 64-pixel k-block at a
@@ -417,10 +419,13 @@ __device__ __forceinline__ int tile_decode(const GemmParams& p, int64_t t, int64
     kb_begin = 0;
     return p.cls_kb[c];
   }
-  const int64_t rest = t / m_tiles;
-  m0 = (t - rest * m_tiles) * kBM;
-  const int64_t split = rest / n_tiles;
-  n0 = (rest - split * n_tiles) * BN;
+  // 32-bit divisions (tile counts are far below 2^31; a 64-bit division is a ~100-instruction
+  // subroutine on every role's per-tile path)
+  const uint32_t tt = (uint32_t)t, mt = (uint32_t)m_tiles, nt = (uint32_t)n_tiles;
+  const uint32_t rest = tt / mt;
+  m0 = (int64_t)(tt - rest * mt) * kBM;
+  const uint32_t split = rest / nt;
+  n0 = (int64_t)(rest - split * nt) * BN;
   kb_begin = (int)split * p.kb_per_split;
   const int kb_end = min(kb_begin + p.kb_per_split, num_k_total);
   return kb_end > kb_begin ? kb_end - kb_begin : 0;
@@ -1701,6 +1706,7 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
               int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
               float* colsum_part) {
   DBS_REQUIRE(M > 0 && N > 0 && K > 0 && a && b && d, DBS_ERR_ARGUMENT, "gemm: bad shape/pointers");
+  DBS_REQUIRE((M / 128 + 1) * (N / 16 + 1) < (int64_t(1) << 31), DBS_ERR_ARGUMENT, "gemm: too many tiles");
   DBS_REQUIRE(epi >= DBS_EPI_F32 && epi <= DBS_EPI_BF16_ACCUM, DBS_ERR_ARGUMENT, "gemm: bad epilogue %d", epi);
   DBS_REQUIRE(!((epi == DBS_EPI_BIAS_RELU_BF16 || epi == DBS_EPI_BIAS_F32) && !bias), DBS_ERR_ARGUMENT,
               "gemm: epilogue needs bias");
@@ -1743,6 +1749,8 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
 // Implicit-GEMM convolution family (see gemm.cuh).
 int conv_gemm(const ConvCall& c, cudaStream_t s) {
   DBS_REQUIRE(c.d && c.M > 0 && c.N > 0 && c.K > 0, DBS_ERR_ARGUMENT, "conv_gemm: bad call");
+  DBS_REQUIRE(c.M < (int64_t(1) << 31) && c.K < (int64_t(1) << 31), DBS_ERR_ARGUMENT,
+              "conv_gemm: M and K must stay below 2^31 (32-bit tile / pixel arithmetic)");
   CUtensorMap ta, tb;
   GemmParams p{};
   p.M = c.M;
