@@ -180,6 +180,26 @@ struct PixelCursor {
   }
 };
 
+struct TapCursor {
+  int cb, rs, r, sx;
+  __device__ __forceinline__ void init(const ConvGeom& g, int kb) {
+    cb = kb % g.cblocks;
+    rs = kb / g.cblocks;
+    r = rs / g.S;
+    sx = rs - r * g.S;
+  }
+  __device__ __forceinline__ void advance(const ConvGeom& g) {
+    if (++cb == g.cblocks) {
+      cb = 0;
+      ++rs;
+      if (++sx == g.S) {
+        sx = 0;
+        ++r;
+      }
+    }
+  }
+};
+
 __device__ __forceinline__ void ld_bf16x32(const uint16_t* src, float (&x)[32]) {
 #pragma unroll
   for (int j = 0; j < 32; j += 8) {
@@ -476,6 +496,11 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
     PixelCursor pc{};
     const bool k_pix = am >= 5 || bm == 2 || bm == 4;
     if (k_pix) pc.init(gk, (int64_t)kb_begin * kBK);
+    // (tap, channel block) of the current k-block, advanced incrementally (no per-k-block division)
+    constexpr bool kTapK = (AM == 2 || AM == 4 || BMD == 3);
+    const bool tap_k = kTapK || (AM < 0 && (am == 2 || am == 4 || bm == 3));
+    TapCursor tc{};
+    if (tap_k) tc.init(p.ga, kb_begin);
     if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
     if ((p.pair_a | p.pair_b) == 0) {
     for (int i = 0; i < num_k; i++, it++) {
@@ -517,8 +542,8 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         // the window corner, shifted by the tap; the tensor map's bounding box
         // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
         const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
+        const int cb = tc.cb;
+        const int rs = tc.rs;
         int h0, w0, oh, ow;
         if (tp.n > 0) {
           h0 = a_oh - 1;
@@ -526,22 +551,22 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
           oh = tp.dh[rs] + 1;
           ow = tp.dw[rs] + 1;
         } else {
-          oh = rs / g.S;
-          ow = rs - oh * g.S;
+          oh = tc.r;
+          ow = tc.sx;
           h0 = a_oh * g.stride - g.pad;
           w0 = a_ow * g.stride - g.pad;
         }
         tma_load_im2col_4d(a, tmA, &full[s], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
       } else {
         const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
+        const int cb = tc.cb;
+        const int rs = tc.rs;
         int ah, aw;
         if (tp.n > 0) {
           ah = a_oh + tp.dh[rs];
           aw = a_ow + tp.dw[rs];
         } else {
-          const int r = rs / g.S, sx = rs - r * g.S;
+          const int r = tc.r, sx = tc.sx;
           ah = a_oh * g.stride + r - g.pad;
           aw = a_ow * g.stride + sx - g.pad;
         }
@@ -556,9 +581,9 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         // input gradient: the filter W[k][r][s][c] read in place as the flipped,
         // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
         const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        const int r = rs / g.S, sx = rs - r * g.S;
+        const int cb = tc.cb;
+        const int rs = tc.rs;
+        const int r = tc.r, sx = tc.sx;
         const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
         if (p.b_wide) {
           tma_load_4d(b, tmB, &full[s], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
@@ -583,6 +608,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
                       boh * g.stride + b_r - g.pad, bn_);
         pc.advance(g);
       }
+      if (tap_k) tc.advance(p.ga);
     }
     } else {
     // paired k-blocks (host guarantees an even k-block count per tile)
@@ -631,14 +657,14 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
             tma_load_2d(a, tmA, &full[s0], (int32_t)m0, k0);
           } else {
             const ConvGeom& g = p.ga;
-            const int cb = kb % g.cblocks;
-            const int rs = kb / g.cblocks;
+            const int cb = tc.cb;
+            const int rs = tc.rs;
             int ah, aw;
             if (tp.n > 0) {
               ah = a_oh + tp.dh[rs];
               aw = a_ow + tp.dw[rs];
             } else {
-              const int r = rs / g.S, sx = rs - r * g.S;
+              const int r = tc.r, sx = tc.sx;
               ah = a_oh * g.stride + r - g.pad;
               aw = a_ow * g.stride + sx - g.pad;
             }
@@ -655,8 +681,8 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         // the window corner, shifted by the tap; the tensor map's bounding box
         // starts at -pad (-1 for an explicit tap list, whose offsets are +1)
         const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
+        const int cb = tc.cb;
+        const int rs = tc.rs;
         int h0, w0, oh, ow;
         if (tp.n > 0) {
           h0 = a_oh - 1;
@@ -664,22 +690,22 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
           oh = tp.dh[rs] + 1;
           ow = tp.dw[rs] + 1;
         } else {
-          oh = rs / g.S;
-          ow = rs - oh * g.S;
+          oh = tc.r;
+          ow = tc.sx;
           h0 = a_oh * g.stride - g.pad;
           w0 = a_ow * g.stride - g.pad;
         }
         tma_load_im2col_4d(a, tmA, &full[s0], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
       } else {
         const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
+        const int cb = tc.cb;
+        const int rs = tc.rs;
         int ah, aw;
         if (tp.n > 0) {
           ah = a_oh + tp.dh[rs];
           aw = a_ow + tp.dw[rs];
         } else {
-          const int r = rs / g.S, sx = rs - r * g.S;
+          const int r = tc.r, sx = tc.sx;
           ah = a_oh * g.stride + r - g.pad;
           aw = a_ow * g.stride + sx - g.pad;
         }
@@ -703,9 +729,9 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
             pc.advance(g);
           } else {  // mode 3, BN = 64: the two k-blocks are consecutive 64-row k ranges
             const ConvGeom& g = p.ga;
-            const int cb = kb % g.cblocks;
-            const int rs = kb / g.cblocks;
-            const int r = rs / g.S, sx = rs - r * g.S;
+            const int cb = tc.cb;
+            const int rs = tc.rs;
+            const int r = tc.r, sx = tc.sx;
             const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
             if (p.b_wide)  // BN >= 128: all channel blocks x 128 k rows in one 4-D box (pair_b 3)
               tma_load_4d(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
@@ -722,9 +748,9 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         // input gradient: the filter W[k][r][s][c] read in place as the flipped,
         // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
         const ConvGeom& g = p.ga;
-        const int cb = kb % g.cblocks;
-        const int rs = kb / g.cblocks;
-        const int r = rs / g.S, sx = rs - r * g.S;
+        const int cb = tc.cb;
+        const int rs = tc.rs;
+        const int r = tc.r, sx = tc.sx;
         const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
         if (p.b_wide) {
           tma_load_4d(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
@@ -749,6 +775,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
                       boh * g.stride + b_r - g.pad, bn_);
         pc.advance(g);
       }
+      if (tap_k) tc.advance(p.ga);
       }
       it += npair;
       i += npair;
@@ -866,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, it++) {
       if (pt < 10) GEMM_TRACE(2 + pt);
       pt++;
-      const int img = (int)(t / p.halo_tpi);
+      const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
       const int P0 = (int)(t - (int64_t)img * p.halo_tpi) * kBM;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
@@ -903,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], (it / kStages) & 1);
         if (j < 8) GEMM_TRACE(96 + 3 * j);
         tc_fence_after();
-        const int img = (int)(t / p.halo_tpi);
+        const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
         const int off = ((int)(t - (int64_t)img * p.halo_tpi) * kBM) % W1;
         const uint64_t a_slot = a_desc0 + (uint64_t)((s * kSlotA) >> 4);
 #pragma unroll
@@ -992,16 +1019,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kHalo) {
       // padded position P = h (W + 1) + w of image img; w = W is junk
       const int W1 = p.ga.OW + 1;
-      const int img = (int)(t / p.halo_tpi);
+      const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
       const int P = (int)(t - (int64_t)img * p.halo_tpi) * kBM + q * 32 + lane;
       const int h = P / W1, w = P - (P / W1) * W1;
       valid = (w < p.ga.OW) && (h < p.ga.OH);
       orow = ((int64_t)img * p.ga.OH + h) * p.ga.OW + w;
       row = orow;
     } else if (om.on && row < p.M) {
-      const int64_t hw = (int64_t)om.OH * om.OW;
-      const int64_t img = row / hw;
-      const int rem = (int)(row - img * hw);
+      const uint32_t hw = (uint32_t)(om.OH * om.OW), r32 = (uint32_t)row;
+      const int64_t img = r32 / hw;
+      const int rem = (int)(r32 - (uint32_t)img * hw);
       const int i = rem / om.OW, jj = rem - i * om.OW;
       orow = (img * om.H + 2 * i + om.a) * om.W + 2 * jj + om.b;
     }
