@@ -227,6 +227,18 @@ def test_conv_untransposed_wgrad_path(dev):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+def test_conv_narrow_filter_boxes_and_no_pdl(dev):
+    """The input gradient with one flipped-filter box per 64 channels
+    (DBS_WIDE_FILTER=0) and every launch without programmatic dependent launch
+    (DBS_PDL=0), on every conv shape."""
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBS_WIDE_FILTER="0", DBS_PDL="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", str(root / "tests" / "test_resnet_gpu.py"),
+                        str(root / "tests" / "test_resnet50_gpu.py"), "-k", "conv_fwd_dgrad_wgrad or im2col_shapes"],
+                       env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_conv_separate_parity_classes_path(dev):
     """The stride-2 input gradient with one launch per parity class
     (DBS_MERGE_PARITY=0, the fallback for Cin > 256) on every conv shape."""
