@@ -839,9 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_k_total = (int)((p.K + kBK - 1) / kBK);
   const int a_mn = (p.a_mode == 1 || p.a_mode >= 5) ? 1 : 0;
   const int b_mn = (p.b_mode >= 1) ? 1 : 0;
-  // tile t -> (m tile fastest, then n tile, then split-K slice): the tiles
-  // resident at one time share their B block (and neighbouring A windows) in L2
-  // tile t -> (m0, n0, first k-block, class); returns the tile's k-block count
+  // tile t -> (m0, n0, first k-block, class); returns the tile's k-block count (tile_decode)
   auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& kb_begin, int& cls) -> int {
     return tile_decode<BN>(p, t, m_tiles, n_tiles, num_k_total, m0, n0, kb_begin, cls);
   };
