@@ -649,7 +649,7 @@ __global__ void head_bcast_kernel(const float* __restrict__ dfeat, int64_t B, in
 
 int grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
-  int64_t cap = (int64_t)num_sms() * 8;
+  int64_t cap = (int64_t)current_sm_count() * 8;
   return (int)(b < 1 ? 1 : (b < cap ? b : cap));
 }
 
@@ -965,7 +965,7 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
   const int cv = c.cout / 8;
   const int rows_per_pass = 256 / cv;
   int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread (one trip)
-  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  if (blocks > current_sm_count() * 8) blocks = current_sm_count() * 8;
   if (blocks < 1) blocks = 1;
   DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_kernel<8>, dim3(blocks), dim3(256), 0, s, gin, mask, m->y[ci], m->mean[ci],
                           m->invstd[ci], c.cout, M, grad + c.g_off, grad + c.b_off));
