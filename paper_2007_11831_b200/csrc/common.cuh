@@ -91,5 +91,7 @@ int pinned_get(size_t bytes, void** out);
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
 
 int num_sms();
+// SMs of the current (possibly green) context -- what a launch issued now can use (partition.cu)
+int current_sm_count();
 
 }  // namespace dbs

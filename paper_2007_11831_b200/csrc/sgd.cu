@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) average_replicas_f32_kernel(AggArgs a, Re
 
 int grid_for(int64_t P, int threads) {
   int64_t blocks = (P + threads - 1) / threads;
-  int64_t cap = (int64_t)num_sms() * 8;
+  int64_t cap = (int64_t)current_sm_count() * 8;
   return (int)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
 }
 
