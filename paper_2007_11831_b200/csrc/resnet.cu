@@ -653,6 +653,30 @@ int grid_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : (b < cap ? b : cap));
 }
 
+// CTAs of `kernel` one SM holds at once (registers / shared memory), cached per kernel
+template <typename K>
+int resident_per_sm(K kernel, int threads, size_t smem) {
+  static int cached = 0;  // one instantiation per kernel type; the BN kernels below are distinct types
+  static size_t cached_smem = ~size_t(0);
+  if (cached == 0 || cached_smem != smem) {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, smem) != cudaSuccess || v < 1) v = 1;
+    cached = v;
+    cached_smem = smem;
+  }
+  return cached;
+}
+
+// grid-stride kernels: at most ONE wave of resident CTAs on the SMs this launch can use
+// (the BN kernels hold 3-6 CTAs per SM, not 8: a fixed 8-per-SM grid left a partial
+// second / third wave)
+template <typename K>
+int grid_one_wave(K kernel, int64_t n, int threads, size_t smem) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)current_sm_count() * resident_per_sm(kernel, threads, smem);
+  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
 }  // namespace
 }  // namespace dbs
 
@@ -948,7 +972,8 @@ int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds
   const int64_t total = M * (c.cout / 8);
   const Conv* d = ds >= 0 ? &m->convs[ds] : nullptr;
   DBS_CUDA_TRY(launch_pdl(
-      bn_apply_kernel, dim3(grid_for(total, 256)), dim3(256), (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s,
+      bn_apply_kernel, dim3(grid_one_wave(bn_apply_kernel, total, 256, (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float))),
+      dim3(256), (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s,
       m->y[ci], m->stats_acc + m->stats_off[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res,
       d ? m->y[ds] : nullptr, d ? m->stats_acc + m->stats_off[ds] : nullptr, d ? m->mean[ds] : nullptr,
       d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
@@ -965,13 +990,14 @@ int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* 
   const int cv = c.cout / 8;
   const int rows_per_pass = 256 / cv;
   int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread (one trip)
-  if (blocks > current_sm_count() * 8) blocks = current_sm_count() * 8;
+  const int cap = current_sm_count() * resident_per_sm(bn_bwd_reduce_kernel<8>, 256, 0);
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_kernel<8>, dim3(blocks), dim3(256), 0, s, gin, mask, m->y[ci], m->mean[ci],
                           m->invstd[ci], c.cout, M, grad + c.g_off, grad + c.b_off));
   DBS_LAUNCH_CHECK();
   const int64_t total = M * cv;
-  DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_kernel, dim3(grid_for(total, 256)), dim3(256),
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_kernel, dim3(grid_one_wave(bn_bwd_apply_kernel, total, 256, (size_t)3 * c.cout * sizeof(float))), dim3(256),
                           (size_t)3 * c.cout * sizeof(float), s, gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
                           pf + c.g_off, grad + c.g_off, grad + c.b_off, c.cout, M, dy, g_out));
   DBS_LAUNCH_CHECK();
