@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const uint16_t* __restric
 // BN backward, pass 1: dbeta[c] += sum g, dgamma[c] += sum g*yhat,
 // g = gin * [mask > 0] (mask = saved post-ReLU output, nullable)
 template <int C8>
-__global__ void __launch_bounds__(256) bn_bwd_reduce_kernel(const uint16_t* __restrict__ gin,
+__global__ void __launch_bounds__(256, 4) bn_bwd_reduce_kernel(const uint16_t* __restrict__ gin,
                                                             const uint16_t* __restrict__ mask,
                                                             const uint16_t* __restrict__ y,
                                                             const float* __restrict__ mean,
