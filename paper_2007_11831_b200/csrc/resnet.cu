@@ -647,12 +647,6 @@ __global__ void head_bcast_kernel(const float* __restrict__ dfeat, int64_t B, in
   }
 }
 
-int grid_for(int64_t n, int threads) {
-  int64_t b = (n + threads - 1) / threads;
-  int64_t cap = (int64_t)current_sm_count() * 8;
-  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
-}
-
 // CTAs of `kernel` one SM holds at once (registers / shared memory), cached per kernel
 template <typename K>
 int resident_per_sm(K kernel, int threads, size_t smem) {
@@ -1242,7 +1236,7 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
   const int PH = sc.OH / 2;
-  DBS_CUDA_TRY(launch_pdl(maxpool_fwd_kernel, dim3(grid_for(B * PH * PH * 8, 256)), dim3(256), 0, s, m->a[m->stem], B, sc.OH, sc.OW, 64, PH, PH,
+  DBS_CUDA_TRY(launch_pdl(maxpool_fwd_kernel, dim3(grid_one_wave(maxpool_fwd_kernel, B * PH * PH * 8, 256, 0)), dim3(256), 0, s, m->a[m->stem], B, sc.OH, sc.OW, 64, PH, PH,
                                                                      m->mp_out, m->mp_idx));
   DBS_LAUNCH_CHECK();
   // ---------------- bottleneck blocks ----------------
@@ -1262,7 +1256,7 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   }
   // ---------------- head: average pool, FC (tcgen05 GEMMs), softmax cross-entropy ----------------
   const int C = m->feat_c, HW = m->feat_hw, K = m->classes, ld = m->cpad;
-  DBS_CUDA_TRY(launch_pdl(avgpool_kernel, dim3(grid_for(B * (C / 8), 256)), dim3(256), 0, s, x, B, HW, C, m->feat_b));
+  DBS_CUDA_TRY(launch_pdl(avgpool_kernel, dim3(grid_one_wave(avgpool_kernel, B * (C / 8), 256, 0)), dim3(256), 0, s, x, B, HW, C, m->feat_b));
   DBS_LAUNCH_CHECK();
   const uint16_t* wfc = wb + m->fc_w;
   // logits [B][K] = feat [B][C] . Wfc [K][C]^T + b
@@ -1282,7 +1276,7 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   if ((st = gemm_bf16(m->dlog_b, 0, ld, wfc, 1, C, m->dfeat, C, B, C, K, DBS_EPI_F32, nullptr, nullptr, s, nullptr)))
     return st;
   uint16_t* gcur = m->g0;
-  DBS_CUDA_TRY(launch_pdl(head_bcast_kernel, dim3(grid_for(B * HW * (C / 8), 256)), dim3(256), 0, s, m->dfeat, B, HW, C, gcur));
+  DBS_CUDA_TRY(launch_pdl(head_bcast_kernel, dim3(grid_one_wave(head_bcast_kernel, B * HW * (C / 8), 256, 0)), dim3(256), 0, s, m->dfeat, B, HW, C, gcur));
   DBS_LAUNCH_CHECK();
   // ---------------- backward through the blocks ----------------
   // buffers: gx = gradient of the block input, t0 = BN outputs' gradients,
@@ -1320,7 +1314,7 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
     gx = old;
   }
   // ---------------- stem backward: max-pool, BN + ReLU mask, weight gradient ----------------
-  DBS_CUDA_TRY(launch_pdl(maxpool_bwd_kernel, dim3(grid_for(B * sc.OH * sc.OW * 8, 256)), dim3(256), 0, s, gcur, m->mp_idx, B, sc.OH, sc.OW, 64, PH,
+  DBS_CUDA_TRY(launch_pdl(maxpool_bwd_kernel, dim3(grid_one_wave(maxpool_bwd_kernel, B * sc.OH * sc.OW * 8, 256, 0)), dim3(256), 0, s, gcur, m->mp_idx, B, sc.OH, sc.OW, 64, PH,
                                                                            PH, t1));
   DBS_LAUNCH_CHECK();
   if ((st = bn_bwd(m, m->stem, pf, grad, t1, m->a[m->stem], B, t0, nullptr, s))) return st;
@@ -1339,7 +1333,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
   DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- forward ----------------
-  DBS_CUDA_TRY(launch_pdl(im2col_stem_kernel, dim3(grid_for(B * 1024, 256)), dim3(256), 0, s, x_base, d_iter, B, m->stem_cols));
+  DBS_CUDA_TRY(launch_pdl(im2col_stem_kernel, dim3(grid_one_wave(im2col_stem_kernel, B * 1024, 256, 0)), dim3(256), 0, s, x_base, d_iter, B, m->stem_cols));
   DBS_LAUNCH_CHECK();
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
