@@ -271,11 +271,34 @@ enum {
   DBS_EPI_BF16 = 4,          /* D bf16 = acc                                    */
   DBS_EPI_RELU_GRAD_BF16 = 5,/* D bf16 = acc * (aux bf16 [M][ldd] > 0)          */
   DBS_EPI_F32_ATOMIC = 6,    /* D fp32 += acc with atomics (split-K reduction)  */
-  DBS_EPI_BF16_ACCUM = 7     /* D bf16 = D + acc (gradient accumulation)        */
+  DBS_EPI_BF16_ACCUM = 7,    /* D bf16 = D + acc (gradient accumulation)        */
+  /* S32 outputs (fp32-class operand format, see dbs_dev_gemm_tf32x3) */
+  DBS_EPI_S32 = 8,           /* D s32 = acc                                     */
+  DBS_EPI_BIAS_RELU_S32 = 9, /* D s32 = relu(acc + bias[n])                     */
+  DBS_EPI_RELU_GRAD_S32 = 10 /* D s32 = acc * (aux s32 [M][ldd] > 0)            */
 };
 int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, const void* d_b,
                       int32_t b_major, int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N,
                       int64_t K, int32_t epilogue, const float* d_bias, void* d_aux, void* stream);
+
+/* fp32-class tensor-core GEMM ("3xTF32"): the same D[M,N] (+)= A[M,K] * B[N,K]^T
+ * with fp32-accurate operands in the S32 split format and three kind::tf32
+ * MMA passes per K block (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM).
+ * S32 format of a logical row-major [rows][ld] fp32 matrix (ld % 32 == 0):
+ * every 32-element block of a row is stored as 32 fp32 "hi" values followed by
+ * 32 fp32 "lo" values, hi = rn_tf32(x), lo = rn_tf32(x - hi), so hi + lo = x to
+ * within ~2^-23 |x| and each part is exact in tf32 (row pitch 2*ld floats).
+ * lda/ldb/ldd are LOGICAL leading dimensions (elements); S32 epilogues write D
+ * in S32, F32 epilogues plain fp32.  Operand/epilogue rules as dbs_dev_gemm_bf16. */
+int dbs_dev_gemm_tf32x3(const void* d_a, int32_t a_major, int64_t lda, const void* d_b,
+                        int32_t b_major, int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N,
+                        int64_t K, int32_t epilogue, const float* d_bias, void* d_aux, void* stream);
+/* fp32 [rows][ld_in] (cols valid) -> S32 [rows][ld_out] (ld_out % 32 == 0, columns
+ * past cols zero) and back (s32 -> fp32: x = hi + lo). */
+int dbs_dev_split_s32(const float* d_x, int64_t rows, int64_t cols, int64_t ld_in, float* d_s32,
+                      int64_t ld_out, void* stream);
+int dbs_dev_join_s32(const float* d_s32, int64_t rows, int64_t cols, int64_t ld_in, float* d_x,
+                     int64_t ld_out, void* stream);
 
 /* 2-layer MLP (784 -> H -> C, ReLU, softmax cross-entropy): one variable-batch
  * forward + backward of a worker's batch.  Params live in one flat fp32

@@ -111,6 +111,10 @@ SIGNATURES = {
     "dbs_dev_sq_dist": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "dbs_dev_gemm_bf16": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_i32, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i32,
                                   c_vp, c_vp, c_vp]),
+    "dbs_dev_gemm_tf32x3": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_i32, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i32,
+                                    c_vp, c_vp, c_vp]),
+    "dbs_dev_split_s32": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "dbs_dev_join_s32": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "dbs_mlp_create": (c_i32, [c_i64, c_i64, c_i64, c_i64, ctypes.POINTER(c_vp)]),
     "dbs_mlp_destroy": (c_i32, [c_vp]),
     "dbs_mlp_param_count": (c_i32, [c_vp, P_i64]),

@@ -108,6 +108,30 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
 }
 __device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
 
+// S32 (fp32-class operand format, include/dbs_b200.h dbs_dev_gemm_tf32x3): each
+// 32-element block of a row is 32 tf32 "hi" values then 32 tf32 "lo" values
+__device__ __forceinline__ float tf32_rn(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
+}
+// 32 consecutive logical values -> one S32 block (256 contiguous bytes at `blk`)
+__device__ __forceinline__ void store_s32x32(float* blk, const float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 4) {
+    float h[4], l[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      h[u] = tf32_rn(x[j + u]);
+      l[u] = tf32_rn(x[j + u] - h[u]);
+    }
+    *reinterpret_cast<float4*>(blk + j) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(blk + 32 + j) = make_float4(l[0], l[1], l[2], l[3]);
+  }
+}
+__device__ __forceinline__ bool is_s32_epi(int epi) {
+  return epi == DBS_EPI_S32 || epi == DBS_EPI_BIAS_RELU_S32 || epi == DBS_EPI_RELU_GRAD_S32;
+}
+
 template <int BN>
 struct Cfg {
   static constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
@@ -120,6 +144,28 @@ struct Cfg {
   static constexpr int kStages = kRing > 8 ? 8 : kRing;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiBytes + 256;
   static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+// S32 tiles (3xTF32): a ring slot holds one 32-wide logical K block of A and B,
+// each operand's hi half then its lo half (both loaded once, by one paired box);
+// the MMA issuer forms hi*hi, hi*lo and lo*hi from the same slot
+template <int BN>
+struct CfgTf {
+  static constexpr uint32_t kABytes = 2 * kBM * 128;  // 32 KB: [hi | lo] x 128 rows x 128 B
+  static constexpr uint32_t kBBytes = 2 * BN * 128;
+  static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;
+  // per tile buffer (kMains) main accumulators (hi*hi, round-robin over logical
+  // k-blocks) + 1 correction accumulator (hi*lo + lo*hi): double-buffered 256 TMEM
+  // columns (BN <= 64: 3 / 7 mains), or one buffer of 512 for BN = 128 (3 mains; no
+  // epilogue / MMA overlap, but a 3x-MMA S32 tile spends far longer in the MMA)
+  static constexpr int kNumBuf = kAccCols >= 128 ? 1 : 2;
+  static constexpr uint32_t kBufCols = 512 / kNumBuf;
+  static constexpr int kMains = (int)(kBufCols / kAccCols) - 1;
+  static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;
+  static constexpr int kRing = (int)((212u * 1024u - kEpiBytes) / (kABytes + kBBytes));
+  static constexpr int kStages = kRing > 8 ? 8 : kRing;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiBytes + 256;
+  static_assert(kMains >= 1 && kSmem + 1024 <= 227 * 1024, "S32 tile budget");
 };
 
 // Halo variant (3x3 stride-1 conv with 64 input channels, 64 output columns):
@@ -161,10 +207,10 @@ __device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int
 // time: the producer thread's per-k-block 64-bit divisions were on its critical path
 struct PixelCursor {
   int n, oh, ow, dr, dc;
-  __device__ __forceinline__ void init(const ConvGeom& g, int64_t pix) {
+  __device__ __forceinline__ void init(const ConvGeom& g, int64_t pix, int step = kBK) {
     pixel_coords(g, pix, n, oh, ow);
-    dr = kBK / g.OW;
-    dc = kBK - dr * g.OW;
+    dr = step / g.OW;
+    dc = step - dr * g.OW;
   }
   __device__ __forceinline__ void advance(const ConvGeom& g) {
     ow += dc;
@@ -225,12 +271,31 @@ __device__ void epilogue_chunk_generic(const GemmParams& p, int64_t row, int64_t
 // One thread's 32 consecutive outputs of one row.  Full, aligned chunks take a
 // branch-free vector path per epilogue kind (the common case: every conv / MLP
 // hidden layer); ragged or unaligned chunks fall back to the per-element path.
-template <int BN>
+template <int BN, bool kTf = false>
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row, int64_t n_base, float (&v)[32],
                                                int cnt, float (&vo)[32]) {
   const int epi = p.epi;
   const bool f32_out = (epi == DBS_EPI_F32 || epi == DBS_EPI_F32_ACCUM || epi == DBS_EPI_BIAS_F32 ||
                         epi == DBS_EPI_F32_ATOMIC);
+  if (kTf && is_s32_epi(epi)) {  // (compiled into the S32 kernels only)
+    // S32 output: row pitch 2 * ldd floats, the chunk is one 32-element block
+    float x[32];
+    const int64_t N = p.N;
+#pragma unroll
+    for (int j = 0; j < 32; j++) x[j] = (j < cnt && n_base + j < N) ? v[j] : 0.0f;
+    if (epi == DBS_EPI_BIAS_RELU_S32) {
+#pragma unroll
+      for (int j = 0; j < 32; j++) x[j] = (j < cnt && n_base + j < N) ? fmaxf(x[j] + p.bias[n_base + j], 0.0f) : 0.0f;
+    } else if (epi == DBS_EPI_RELU_GRAD_S32) {
+      const float* ah = reinterpret_cast<const float*>(p.aux) + row * 2 * p.ldd + 2 * n_base;
+#pragma unroll
+      for (int j = 0; j < 32; j++) x[j] = ah[j] > 0.0f ? x[j] : 0.0f;
+    }
+    store_s32x32(reinterpret_cast<float*>(p.d) + row * 2 * p.ldd + 2 * n_base, x);
+#pragma unroll
+    for (int j = 0; j < 32; j++) vo[j] = x[j];
+    return;
+  }
   const int align_elems = f32_out ? 4 : 8;
   const bool fast = (cnt == 32) && !p.d_trans && (p.ldd % align_elems == 0) &&
                     ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0) && (p.aux == nullptr || ((reinterpret_cast<uintptr_t>(p.aux) & 15) == 0)) &&
@@ -784,6 +849,111 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
    }
 }
 
+// TMA producer for S32 operands (3xTF32).  One ring slot = one 32-wide logical K
+// block: A as [hi | lo] and B as [hi | lo], each half in the canonical layout of a
+// 128-byte k-block (K-major: rows x 128 B; MN-major: 32-column groups of 32 K rows
+// x 128 B, each group followed by its lo group -- the SWIZZLE_128B_BASE32B layout).
+// The tensor maps view S32 bytes as bf16 units (4 per logical element) with a
+// hi/lo dimension of stride 128 B, so ONE box fetches both halves (except im2col
+// maps: two boxes).  The MMA issuer then runs (A hi, B hi), (A hi, B lo), (A lo, B hi).
+template <int BN>
+__device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                           uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
+                                           int64_t num_tiles, int64_t m_tiles, int64_t n_tiles, int num_k_total) {
+  using C = CfgTf<BN>;
+  constexpr int kStages = C::kStages;
+  const int am = p.a_mode, bm = p.b_mode;
+  uint32_t it = 0;
+  for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    int64_t m0, n0;
+    int kb_begin, cls;
+    const int num_k = tile_decode<BN>(p, t, m_tiles, n_tiles, num_k_total, m0, n0, kb_begin, cls);
+    const ConvTaps& tp = cls >= 0 ? p.cls_taps[cls] : p.taps;
+    int a_n = 0, a_oh = 0, a_ow = 0;
+    if (am == 2 || am == 4) pixel_coords(p.ga, m0, a_n, a_oh, a_ow);
+    int b_r = 0, b_s = 0, b_c0 = 0;
+    if (bm == 2 || bm == 4) {
+      const int rs = (int)(n0 / p.gb.Cin);
+      b_c0 = (int)(n0 - (int64_t)rs * p.gb.Cin);
+      b_r = rs / p.gb.S;
+      b_s = rs - b_r * p.gb.S;
+    }
+    const bool k_pix = (bm == 2 || bm == 4);
+    PixelCursor pc{};
+    if (k_pix) pc.init(p.gb, (int64_t)kb_begin * 32, 32);
+    const bool tap_k = (am == 2 || am == 4 || bm == 3);
+    TapCursor tc{};
+    if (tap_k) tc.init(p.ga, kb_begin);
+    for (int i = 0; i < num_k; i++, it++) {
+      const int L = kb_begin + i;
+      const int s = (int)(it % kStages);
+      mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], C::kABytes + C::kBBytes);
+      uint8_t* a = sA + s * C::kABytes;
+      uint8_t* b = sB + s * C::kBBytes;
+      if (am == 0) {
+        tma_load_3d(a, tmA, &full[s], 0, (int32_t)m0, 2 * L);  // {64, 128 rows, hi/lo}
+      } else if (am == 1) {
+        tma_load_4d(a, tmA, &full[s], 0, L * 32, 0, (int32_t)(m0 / 32));  // {64, 32 k, hi/lo, 4 groups}
+      } else if (am == 4) {
+        const ConvGeom& g = p.ga;
+        int h0, w0, oh, ow;
+        if (tp.n > 0) {
+          h0 = a_oh - 1;
+          w0 = a_ow - 1;
+          oh = tp.dh[tc.rs] + 1;
+          ow = tp.dw[tc.rs] + 1;
+        } else {
+          oh = tc.r;
+          ow = tc.sx;
+          h0 = a_oh * g.stride - g.pad;
+          w0 = a_ow * g.stride - g.pad;
+        }
+        tma_load_im2col_4d(a, tmA, &full[s], tc.cb * 128, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+        tma_load_im2col_4d(a + kBM * 128, tmA, &full[s], tc.cb * 128 + 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+      } else {
+        const ConvGeom& g = p.ga;
+        int ah, aw;
+        if (tp.n > 0) {
+          ah = a_oh + tp.dh[tc.rs];
+          aw = a_ow + tp.dw[tc.rs];
+        } else {
+          ah = a_oh * g.stride + tc.r - g.pad;
+          aw = a_ow * g.stride + tc.sx - g.pad;
+        }
+        tma_load_5d(a, tmA, &full[s], 0, aw, ah, a_n, 2 * tc.cb);  // {64, pixels..., hi/lo}
+      }
+      if (bm == 0) {
+        tma_load_3d(b, tmB, &full[s], 0, (int32_t)n0, 2 * L);
+      } else if (bm == 1) {
+        tma_load_4d(b, tmB, &full[s], 0, L * 32, 0, (int32_t)(n0 / 32));
+      } else if (bm == 3) {
+        const ConvGeom& g = p.ga;
+        const int rs_flip = tp.n > 0 ? (int)tp.rs[tc.rs] : (g.R - 1 - tc.r) * g.S + (g.S - 1 - tc.sx);
+        tma_load_5d(b, tmB, &full[s], 0, tc.cb * 32, 0, (int32_t)(n0 / 32), rs_flip);  // {64, 32 k, hi/lo, groups, rs}
+      } else if (bm == 4) {
+        const ConvGeom& g = p.gb;
+#pragma unroll
+        for (int j = 0; j < BN / 32; j++) {
+          const int cu = (b_c0 / 32 + j) * 128;
+          tma_load_im2col_4d(b + j * 8192, tmB, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+                             pc.n, (uint16_t)b_s, (uint16_t)b_r);
+          tma_load_im2col_4d(b + j * 8192 + 4096, tmB, &full[s], cu + 64, pc.ow * g.stride - g.pad,
+                             pc.oh * g.stride - g.pad, pc.n, (uint16_t)b_s, (uint16_t)b_r);
+        }
+      } else {
+        const ConvGeom& g = p.gb;
+#pragma unroll
+        for (int j = 0; j < BN / 32; j++)
+          tma_load_5d(b + j * 8192, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad, pc.oh * g.stride + b_r - g.pad,
+                      pc.n, 2 * (b_c0 / 32 + j));
+      }
+      if (tap_k) tc.advance(p.ga);
+      if (k_pix) pc.advance(p.gb);
+    }
+  }
+}
+
 template <int BN>
 __device__ __forceinline__ void produce_dispatch(const GemmParams& p, const CUtensorMap* tmA, const CUtensorMap* tmB,
                                                  uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
@@ -807,17 +977,29 @@ __device__ __forceinline__ void produce_dispatch(const GemmParams& p, const CUte
 #undef DBS_PRODUCE
 }
 
-template <int BN, bool kHalo>
+// kTf: S32 operands, kind::tf32, three virtual k-blocks per 32-wide logical K block (produce_tf)
+template <int BN, bool kHalo, bool kTf = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   using C = Cfg<BN>;
   using H = HaloCfg;
   static_assert(!kHalo || BN == 64, "halo variant: 64 output columns");
-  constexpr int kStages = kHalo ? H::kStages : C::kStages;
+  static_assert(!(kHalo && kTf), "no halo variant for S32 operands");
+  using CT = CfgTf<BN < 128 ? BN : 128>;
+  constexpr int kStages = kHalo ? H::kStages : (kTf ? CT::kStages : C::kStages);
   constexpr uint32_t kAccCols = kHalo ? H::kAccCols : C::kAccCols;
-  constexpr uint32_t kTmemCols = kHalo ? H::kTmemCols : C::kTmemCols;
-  constexpr uint32_t kSlotA = kHalo ? H::kSlotBytes : C::kABytes;
-  constexpr uint32_t kSlotB = kHalo ? 0u : C::kBBytes;
+  // S32: each tile buffer holds CT::kMains main accumulators (hi*hi, round-robin over
+  // the logical k-blocks) and one correction accumulator (hi*lo + lo*hi, 2^-11 smaller),
+  // summed in fp32 (round to nearest) by the epilogue.  The tensor core's in-TMEM
+  // accumulation truncates: every accumulator step costs up to one ulp of the running
+  // sum, so fewer steps per accumulator = fewer truncations (gemm accuracy test).
+  static_assert(!kTf || BN <= 128, "S32 tiles: BN <= 128");
+  constexpr int kMains = kTf ? CT::kMains : 1;
+  constexpr uint32_t kBufCols = kTf ? CT::kBufCols : kAccCols;
+  constexpr int kNumBuf = kTf ? CT::kNumBuf : 2;  // accumulator buffers (tile j uses j % kNumBuf)
+  constexpr uint32_t kTmemCols = kHalo ? H::kTmemCols : (kTf ? 512u : C::kTmemCols);
+  constexpr uint32_t kSlotA = kHalo ? H::kSlotBytes : (kTf ? CT::kABytes : C::kABytes);
+  constexpr uint32_t kSlotB = kHalo ? 0u : (kTf ? CT::kBBytes : C::kBBytes);
   constexpr uint32_t kBRes = kHalo ? H::kBResBytes : 0u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -836,7 +1018,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t m_tiles = (p.M + kBM - 1) / kBM;
   const int64_t n_tiles = (p.N + BN - 1) / BN;
   const int64_t num_tiles = kHalo ? p.halo_tiles : (p.nclass > 0 ? p.cls_start[p.nclass] : m_tiles * n_tiles * p.splits);
-  const int num_k_total = (int)((p.K + kBK - 1) / kBK);
+  const int num_k_total = kTf ? (int)((p.K + 31) / 32) : (int)((p.K + kBK - 1) / kBK);
   const int a_mn = (p.a_mode == 1 || p.a_mode >= 5) ? 1 : 0;
   const int b_mn = (p.b_mode >= 1) ? 1 : 0;
   // tile t -> (m0, n0, first k-block, class); returns the tile's k-block count (tile_decode)
@@ -899,6 +1081,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // rows from one above the tile's first row, columns from -1 (zero fill)
       tma_load_4d(sA + s * kSlotA, &tmA, &full[s], 0, -1, P0 / W1 - 1, img);
     }
+   } else if constexpr (kTf) {
+   produce_tf<BN>(p, &tmA, &tmB, sA, sB, full, empty, num_tiles, m_tiles, n_tiles, num_k_total);
    } else {
    produce_dispatch<BN>(p, &tmA, &tmB, sA, sB, full, empty, num_tiles, m_tiles, n_tiles, num_k_total);
    }
@@ -907,7 +1091,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = make_idesc_bf16(kBM, BN, a_mn, b_mn);
+    const uint32_t idesc = kTf ? make_idesc_tf32(kBM, BN, a_mn, b_mn) : make_idesc_bf16(kBM, BN, a_mn, b_mn);
     uint32_t it = 0, j = 0;
     if constexpr (kHalo) {
       mbar_wait(bres_full, 0);
@@ -948,6 +1132,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         GEMM_TRACE(22 + j);
         j++;
       }
+    } else {
+    if constexpr (kTf) {
+    // ---- S32 slots: [A hi | A lo], [B hi | B lo] of one logical k-block ----
+    // MN-major halves: 32-column groups of 32 K rows (4 KB), hi and lo of a group
+    // adjacent (group stride LBO = 8 KB), SWIZZLE_128B_BASE32B (4-row K groups 512 B apart)
+    const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), 8192, 512, 1) : make_sdesc(smem_u32(sA), 16, 1024);
+    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 512, 1) : make_sdesc(smem_u32(sB), 16, 1024);
+    const uint32_t a_lo = a_mn ? 4096u >> 4 : (uint32_t)(kBM * 128) >> 4;  // lo half offset, 16-byte units
+    const uint32_t b_lo = b_mn ? 4096u >> 4 : (uint32_t)(BN * 128) >> 4;
+    const uint32_t a_kstep = a_mn ? 64u : 2u, b_kstep = b_mn ? 64u : 2u;  // UMMA_K = 8: 8 K rows / 32 B
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int64_t m0, n0;
+      int kb_begin, cls;
+      const int num_k = decode(t, m0, n0, kb_begin, cls);
+      if (num_k == 0) continue;
+      const int b = kNumBuf == 1 ? 0 : (int)(j & 1);
+      mbar_wait(&acc_empty[b], (kNumBuf == 1 ? (j & 1) : ((j >> 1) & 1)) ^ 1);
+      tc_fence_after();
+      const uint32_t d_buf = tmem_base + b * kBufCols;
+      const uint32_t d_corr = d_buf + kMains * kAccCols;
+      for (int i = 0; i < num_k; i++, it++) {
+        const int s = (int)(it % kStages);
+        mbar_wait(&full[s], (it / kStages) & 1);
+        tc_fence_after();
+        const int mi = i % kMains;
+        const uint32_t d_main = d_buf + mi * kAccCols;
+        const uint64_t a_hi = a_desc0 + (uint64_t)((s * kSlotA) >> 4), b_hi = b_desc0 + (uint64_t)((s * kSlotB) >> 4);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc, (i < kMains && k == 0) ? 0u : 1u);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32_ss(d_corr, a_hi + k * a_kstep, b_hi + b_lo + k * b_kstep, idesc, (i == 0 && k == 0) ? 0u : 1u);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32_ss(d_corr, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
+        mma_commit(&empty[s]);
+      }
+      // (a short tile, num_k < kMains, leaves the higher mains unwritten: the epilogue skips them)
+      mma_commit(&acc_full[b]);
+      j++;
+    }
     } else {
     const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), p.pair_a == 3 ? 16384 : 8192, 1024)
                                   : make_sdesc(smem_u32(sA), 16, 1024);
@@ -991,6 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     }
     }
+    }
     __syncwarp();
   } else {
   // ---------------- epilogue (warps 2..5) ----------------
@@ -1005,10 +1232,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     int64_t m0 = 0, n0 = 0;
     int kb_begin, cls = -1;
-    if (!kHalo && decode(t, m0, n0, kb_begin, cls) == 0) continue;
+    const int tile_k = kHalo ? 1 : decode(t, m0, n0, kb_begin, cls);
+    if (tile_k == 0) continue;
+    const int nmain = tile_k < kMains ? tile_k : kMains;  // S32: main accumulators this tile wrote
+    (void)nmain;
     const OutMap& om = cls >= 0 ? p.cls_omap[cls] : p.omap;
-    const int b = (int)(tj & 1);
-    mbar_wait(&acc_full[b], (tj >> 1) & 1);
+    const int b = kNumBuf == 1 ? 0 : (int)(tj & 1);
+    mbar_wait(&acc_full[b], kNumBuf == 1 ? (tj & 1) : ((tj >> 1) & 1));
     if (warp == 2 && lane == 0) GEMM_TRACE(32 + tj);
     tc_fence_after();
     int64_t row = m0 + q * 32 + lane;
@@ -1030,14 +1260,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i = rem / om.OW, jj = rem - i * om.OW;
       orow = (img * om.H + 2 * i + om.a) * om.W + 2 * jj + om.b;
     }
-    const uint32_t lane_addr = tmem_base + b * kAccCols + ((uint32_t)(q * 32) << 16);
+    const uint32_t lane_addr = tmem_base + b * kBufCols + ((uint32_t)(q * 32) << 16);
     const bool stats = (p.sum_part != nullptr);
+    // S32: fold the other main accumulators and the correction accumulator of chunk c
+    // into r (fp32 adds, round to nearest; the corrections last)
+    auto add_corr = [&](int c, uint32_t (&r)[32]) {
+      if constexpr (kTf) {
+        uint32_t r2[32];
+        for (int m = 1; m <= kMains; m++) {
+          if (m < kMains && m >= nmain) continue;
+          tmem_ld_32x32b_x32(lane_addr + m * kAccCols + c * 32, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 32; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+        }
+      }
+    };
     if (BN >= 32) {
       // software-pipelined TMEM reads: chunk c + 1 is loaded while chunk c is
       // stored (the registers are free once chunk c is packed / copied)
       uint32_t r[32];
       tmem_ld_32x32b_x32(lane_addr, r);
       tmem_ld_wait();
+      add_corr(0, r);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; c++) {
         const int64_t n_base = n0 + c * 32;
@@ -1146,7 +1391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             vo[k] = 0.0f;
           }
           if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
-          if (valid) epilogue_chunk<BN>(p, orow, n_base, v, cnt, vo);
+          if (valid) epilogue_chunk<BN, kTf>(p, orow, n_base, v, cnt, vo);
           if (p.colsum_part != nullptr) {
             const int64_t g = (m0 >> 5) + q;
             const bool group_live = (m0 + q * 32 < p.M);
@@ -1154,13 +1399,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane < cnt && group_live) p.colsum_part[g * p.N + n_base + lane] = s;
           }
         }
-        if (prefetch) tmem_ld_wait();
+        if (prefetch) {
+          tmem_ld_wait();
+          add_corr(c + 1, r);
+        }
         if (last) break;
       }
     } else {
       uint32_t r[16];
       tmem_ld_32x32b_x16(lane_addr, r);
       tmem_ld_wait();
+      if constexpr (kTf) {
+        uint32_t r2[16];
+        for (int m = 1; m <= kMains; m++) {
+          if (m < kMains && m >= nmain) continue;
+          tmem_ld_32x32b_x16(lane_addr + m * kAccCols, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
@@ -1169,7 +1427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 16; k++) v[k] = __uint_as_float(r[k]);
         const int cnt = (int)((p.N - n0) < 16 ? (p.N - n0) : 16);
-        epilogue_chunk<BN>(p, orow, n0, v, cnt, vo);
+        epilogue_chunk<BN, kTf>(p, orow, n0, v, cnt, vo);
       }
     }
     if (warp == 2 && lane == 0) GEMM_TRACE(52 + tj);
@@ -1428,7 +1686,7 @@ EncodeTiledFn encode_fn() {
 
 // 2-D bf16 tensor [rows][ld] (inner dim `inner` elements), box {box0, box1}
 int make_tmap(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t rows, uint64_t ld_elems, uint32_t box0,
-              uint32_t box1) {
+              uint32_t box1, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && (ld_elems * 2) % 16 == 0, DBS_ERR_ARGUMENT,
@@ -1438,14 +1696,15 @@ int make_tmap(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t rows, 
   cuuint32_t box[2] = {box0, box1};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DBS_OK;
 }
 
 // 4-D NHWC bf16 tensor [N][H][W][C]: box {64 c, bw*stride, bh*stride, bn}, traversal stride on W/H
-int make_tmap_nhwc(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride) {
+int make_tmap_nhwc(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride,
+                   CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 64 == 0, DBS_ERR_ARGUMENT,
@@ -1456,7 +1715,7 @@ int make_tmap_nhwc(CUtensorMap* tm, const void* base, const ConvTensor& t, int b
   cuuint32_t box[4] = {64, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (4d) failed (%d)", (int)r);
   return DBS_OK;
@@ -1486,7 +1745,7 @@ EncodeIm2colFn encode_im2col_fn() {
 // (extent + upper - lower - 1) / stride + 1 -- any feature-map size, a tile may
 // cross rows and images (fprop / dgrad: lower = -pad, upper = pad - (k - 1)).
 int make_tmap_im2col(CUtensorMap* tm, const void* base, const ConvTensor& t, int lower, int upper, int pixels,
-                     int stride) {
+                     int stride, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeIm2colFn fn = encode_im2col_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeIm2col unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 64 == 0, DBS_ERR_ARGUMENT,
@@ -1498,7 +1757,7 @@ int make_tmap_im2col(CUtensorMap* tm, const void* base, const ConvTensor& t, int
   int lo[2] = {lower, lower}, hi[2] = {upper, upper};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lo, hi, 64,
-                  (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
   // drivers up to 13.1 mis-set one descriptor bit for im2col maps of tensors
@@ -1531,7 +1790,8 @@ int make_tmap_kpair(CUtensorMap* tm, const void* base, uint64_t K, uint64_t rows
 
 // NHWC activation viewed as {64 c, W, H, N, C / 64 channel blocks}: one box of
 // {64, bw, bh, bn, 2} fills two consecutive ring slots (two channel blocks of one tap)
-int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride) {
+int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride,
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 128 == 0, DBS_ERR_ARGUMENT,
@@ -1541,9 +1801,28 @@ int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, 
   cuuint32_t box[5] = {64, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn, 2};
   cuuint32_t es[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (5d pair) failed (%d)", (int)r);
+  return DBS_OK;
+}
+
+// MN-major S32 matrix [K rows][ld] (logical ld, row pitch 8 ld bytes) viewed as
+// {64 units, K rows, hi/lo, 32-column groups}: one box {64, 32, 2, groups} lands as
+// per group [hi 32 rows x 128 B | lo 32 rows x 128 B] (SWIZZLE_128B_ATOM_32B)
+int make_tmap_s32_mn(CUtensorMap* tm, const void* base, uint64_t mn, uint64_t krows, uint64_t ld, uint32_t groups) {
+  EncodeTiledFn fn = encode_fn();
+  DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  DBS_REQUIRE(((uintptr_t)base & 15) == 0 && ld % 32 == 0 && groups >= 1 && groups <= 8, DBS_ERR_ARGUMENT,
+              "S32 MN-major view: aligned base, ld %% 32 == 0");
+  cuuint64_t dims[4] = {64, krows, 2, (mn + 31) / 32};
+  cuuint64_t strides[3] = {ld * 8, 128, 256};
+  cuuint32_t box[4] = {64, 32, 2, groups};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (S32 MN) failed (%d)", (int)r);
   return DBS_OK;
 }
 
@@ -1611,16 +1890,16 @@ void* current_ctx() {
   return c;
 }
 
-template <int BN, bool kHalo = false>
+template <int BN, bool kHalo = false, bool kTf = false>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits, cudaStream_t s) {
-  constexpr size_t kSmem = kHalo ? HaloCfg::kSmem : Cfg<BN>::kSmem;
+  constexpr size_t kSmem = kHalo ? HaloCfg::kSmem : (kTf ? CfgTf<(BN < 128 ? BN : 128)>::kSmem : Cfg<BN>::kSmem);
   static thread_local void* seen[16] = {nullptr};
   static thread_local int nseen = 0;
   void* ctx = current_ctx();
   bool known = false;
   for (int i = 0; i < nseen; i++) known |= (seen[i] == ctx);
   if (!known) {
-    DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN, kHalo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<BN, kHalo, kTf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmem));
     if (nseen < 16) seen[nseen++] = ctx;
   }
@@ -1632,7 +1911,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
                       : (p.nclass > 0 ? p.cls_start[p.nclass] : ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * splits);
   const int64_t sms = current_sm_count();
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  DBS_CUDA_TRY(launch_pdl(gemm_bf16_kernel<BN, kHalo>, dim3(grid), dim3(kThreads), kSmem, s, ta, tb, q));
+  DBS_CUDA_TRY(launch_pdl(gemm_bf16_kernel<BN, kHalo, kTf>, dim3(grid), dim3(kThreads), kSmem, s, ta, tb, q));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -1689,7 +1968,14 @@ int pick_bn(int64_t N, int b_mode) {
 }
 
 int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int bn, int splits, cudaStream_t s,
-             bool halo = false) {
+             bool halo = false, bool tf = false) {
+  if (tf) {
+    switch (bn) {
+      case 16: return launch<16, false, true>(ta, tb, p, splits, s);
+      case 64: return launch<64, false, true>(ta, tb, p, splits, s);
+      default: return launch<128, false, true>(ta, tb, p, splits, s);
+    }
+  }
   if (halo) return launch<64, true>(ta, tb, p, 1, s);
   switch (bn) {
     case 16: return launch<16>(ta, tb, p, splits, s);
@@ -1724,6 +2010,9 @@ int preload_gemm() {
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<256>::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(halo_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Halo2Cfg::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<16, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgTf<16>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgTf<64>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<128, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgTf<128>::kSmem));
   return DBS_OK;
 }
 
@@ -1771,8 +2060,185 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
   return dispatch(ta, tb, p, bn, 1, s);
 }
 
+bool is_s32_epi_host(int epi) {
+  return epi == DBS_EPI_S32 || epi == DBS_EPI_BIAS_RELU_S32 || epi == DBS_EPI_RELU_GRAD_S32;
+}
+
+// S32 operands: the tensor maps view the S32 bytes as bf16 units (4 per logical
+// element); K-major rows {4 K32 units} (K32 = K rounded up to 32), MN-major rows
+// {4 MN32 units}, 32-row boxes
+int64_t ceil32(int64_t x) { return (x + 31) & ~int64_t(31); }
+// MN-major tf32 operands: the SWIZZLE_128B_BASE32B smem layout (tcgen05.cuh make_sdesc)
+constexpr CUtensorMapSwizzle kMnSwz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+
+int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
+            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s) {
+  DBS_REQUIRE(M > 0 && N > 0 && K > 0 && a && b && d, DBS_ERR_ARGUMENT, "gemm_tf: bad shape/pointers");
+  DBS_REQUIRE((M / 128 + 1) * (N / 16 + 1) < (int64_t(1) << 31), DBS_ERR_ARGUMENT, "gemm_tf: too many tiles");
+  DBS_REQUIRE(epi == DBS_EPI_F32 || epi == DBS_EPI_F32_ACCUM || epi == DBS_EPI_BIAS_F32 || epi == DBS_EPI_F32_ATOMIC ||
+                  is_s32_epi_host(epi),
+              DBS_ERR_ARGUMENT, "gemm_tf: epilogue %d has no S32 / fp32 form", epi);
+  DBS_REQUIRE(!((epi == DBS_EPI_BIAS_RELU_S32 || epi == DBS_EPI_BIAS_F32) && !bias), DBS_ERR_ARGUMENT,
+              "gemm_tf: epilogue needs bias");
+  DBS_REQUIRE(!(epi == DBS_EPI_RELU_GRAD_S32 && !aux), DBS_ERR_ARGUMENT, "gemm_tf: epilogue needs aux");
+  DBS_REQUIRE(lda % 32 == 0 && ldb % 32 == 0 && (!is_s32_epi_host(epi) || ldd % 32 == 0), DBS_ERR_ARGUMENT,
+              "gemm_tf: S32 leading dimensions must be multiples of 32");
+  DBS_REQUIRE(lda >= (a_mn ? M : K) && ldb >= (b_mn ? N : K), DBS_ERR_ARGUMENT, "gemm_tf: leading dimension too small");
+  const int bn = pick_bn(N, b_mn) > 128 ? 128 : pick_bn(N, b_mn);
+  CUtensorMap ta, tb;
+  int st = a_mn ? make_tmap_s32_mn(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 4)
+                : make_tmap_kpair(&ta, a, (uint64_t)(4 * ceil32(K)), (uint64_t)M, (uint64_t)(4 * lda), 128);
+  if (st) return st;
+  st = b_mn ? make_tmap_s32_mn(&tb, b, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, (uint32_t)(bn / 32))
+            : make_tmap_kpair(&tb, b, (uint64_t)(4 * ceil32(K)), (uint64_t)N, (uint64_t)(4 * ldb), (uint32_t)bn);
+  if (st) return st;
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.a_mode = a_mn;
+  p.b_mode = b_mn;
+  p.epi = epi;
+  p.d = d;
+  p.ldd = ldd;
+  p.bias = bias;
+  p.aux = reinterpret_cast<const uint16_t*>(aux);
+  p.kb_per_split = (int)((K + 31) / 32);
+  return dispatch(ta, tb, p, bn, 1, s, false, true);
+}
+
+// Implicit-GEMM convolution family with S32 operands (ConvCall.tf; see gemm.cuh):
+// A conv operands (mode 2) are NHWC S32 viewed as {4 C units, W, H, N}; the
+// flipped filter (B mode 3) is [Cout][R*S][Cin] S32 viewed as {4 Cin, R*S, Cout};
+// the weight gradient's im2col B (mode 2) takes 32-pixel boxes.
+int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
+  DBS_REQUIRE(c.d && c.M > 0 && c.N > 0 && c.K > 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: bad call");
+  DBS_REQUIRE(c.M < (int64_t(1) << 31) && c.K < (int64_t(1) << 31), DBS_ERR_ARGUMENT,
+              "conv_gemm_tf: M and K must stay below 2^31");
+  DBS_REQUIRE(c.a_mode <= 2 && c.b_mode <= 3 && !c.d_trans && !(c.b_mode == 3 && c.a_mode != 2) &&
+                  !(c.b_mode == 2 && c.a_mode != 1),
+              DBS_ERR_ARGUMENT, "conv_gemm_tf: unsupported operand modes (%d, %d)", c.a_mode, c.b_mode);
+  CUtensorMap ta, tb;
+  GemmParams p{};
+  p.M = c.M;
+  p.N = c.N;
+  p.K = c.K;
+  p.epi = c.epi;
+  p.d = c.d;
+  p.ldd = c.ldd;
+  p.bias = c.bias;
+  p.aux = c.aux;
+  p.sum_part = c.sum_part;
+  p.sq_part = c.sq_part;
+  p.taps = c.taps;
+  p.omap = c.omap;
+  p.nclass = c.nclass;
+  p.ga = c.ga;
+  p.gb = c.gb;
+  if (c.a_mode == 2) DBS_REQUIRE(c.ga.cblocks * 32 == c.ta.C, DBS_ERR_ARGUMENT, "conv_gemm_tf: cblocks counts 32 channels");
+  if (c.nclass > 0) {
+    DBS_REQUIRE(c.nclass <= 4 && c.splits <= 1 && c.a_mode == 2, DBS_ERR_ARGUMENT, "merged classes: bad call");
+    const int64_t mt = (c.M + kBM - 1) / kBM;
+    p.cls_start[0] = 0;
+    for (int k = 0; k < c.nclass; k++) {
+      p.cls_taps[k] = c.cls_taps[k];
+      p.cls_omap[k] = c.cls_omap[k];
+      p.cls_kb[k] = c.cls_taps[k].n * c.ga.cblocks;
+      p.cls_start[k + 1] = p.cls_start[k] + mt;
+    }
+  }
+  int bn = (c.bn_override > 0) ? c.bn_override : pick_bn(c.N, c.b_mode);
+  if (bn > 128) bn = 128;  // two accumulators per S32 tile (gemm_bf16_kernel<BN, false, true>)
+  if (c.bn_override <= 0 && c.b_mode != 2 && bn >= 64) {
+    const int64_t sms = current_sm_count();
+    const int64_t mt = (c.M + kBM - 1) / kBM;
+    int64_t best = -1;
+    int pick = bn;
+    for (int cand = bn; cand >= 64; cand /= 2) {
+      const int64_t tiles = mt * ((c.N + cand - 1) / cand);
+      const int64_t cost = ((tiles + sms - 1) / sms) * (int64_t)(kBM * kBK * 2 + cand * kBK * 2);
+      if (best < 0 || cost < best) {
+        best = cost;
+        pick = cand;
+      }
+    }
+    bn = pick;
+  }
+  int st;
+  // ---- A ----
+  p.a_mode = c.a_mode;
+  if (c.a_mode == 2) {
+    const ConvTensor t4{c.ta.N, c.ta.H, c.ta.W, 4 * c.ta.C};
+    const bool taps = c.taps.n > 0 || c.nclass > 0;
+    if (force_im2col() || !pixel_box_fits(c.ga.OH, c.ga.OW, kBM)) {
+      st = make_tmap_im2col(&ta, c.a, t4, taps ? -1 : -c.ga.pad, taps ? -1 : c.ga.pad - (c.ga.R - 1), kBM,
+                            c.ga.stride);
+      p.a_mode = 4;
+    } else {
+      int bw, bh, bnn;
+      st = pixel_box(c.ga.OH, c.ga.OW, kBM, bw, bh, bnn);
+      if (st) return st;
+      st = make_tmap_nhwc_pair(&ta, c.a, t4, bw, bh, bnn, c.ga.stride);  // {64, pixels, hi/lo}
+    }
+  } else if (c.a_mode == 1) {
+    DBS_REQUIRE(c.lda % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: lda %% 32");
+    st = make_tmap_s32_mn(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 4);
+  } else {
+    DBS_REQUIRE(c.lda % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: lda %% 32");
+    st = make_tmap_kpair(&ta, c.a, (uint64_t)(4 * ceil32(c.K)), (uint64_t)c.M, (uint64_t)(4 * c.lda), 128);
+  }
+  if (st) return st;
+  // ---- B ----
+  p.b_mode = c.b_mode;
+  if (c.b_mode == 2) {
+    const ConvTensor t4{c.tb.N, c.tb.H, c.tb.W, 4 * c.tb.C};
+    DBS_REQUIRE(c.gb.Cin % bn == 0 && bn <= c.gb.Cin, DBS_ERR_ARGUMENT, "wgrad: tile must not straddle (r,s)");
+    if (force_im2col() || !pixel_box_fits(c.gb.OH, c.gb.OW, 32)) {
+      st = make_tmap_im2col(&tb, c.b, t4, -c.gb.pad, c.gb.pad - (c.gb.R - 1), 32, c.gb.stride, kMnSwz);
+      p.b_mode = 4;
+    } else {
+      int bw, bh, bnn;
+      st = pixel_box(c.gb.OH, c.gb.OW, 32, bw, bh, bnn);
+      if (st) return st;
+      st = make_tmap_nhwc_pair(&tb, c.b, t4, bw, bh, bnn, c.gb.stride, kMnSwz);  // {64, 32 pixels, hi/lo}
+    }
+  } else if (c.b_mode == 3) {
+    // filter [Cout][R*S][Cin] S32 read as the flipped, transposed filter: the MN-major
+    // view {64 units, Cout k (K rows), hi/lo, Cin / 32 groups, R*S}, box {64, 32 k, 2, BN / 32, 1}
+    EncodeTiledFn fn = encode_fn();
+    DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    DBS_REQUIRE(c.tb.C % 32 == 0 && c.tb.N % 32 == 0 && ((uintptr_t)c.b & 15) == 0 && bn % 32 == 0, DBS_ERR_ARGUMENT,
+                "dgrad filter view: Cin, Cout multiples of 32 required");
+    const uint64_t cin = (uint64_t)c.tb.C, rs = (uint64_t)c.tb.W;
+    cuuint64_t dims[5] = {64, (cuuint64_t)c.tb.N, 2, (cuuint64_t)(cin / 32), (cuuint64_t)rs};
+    cuuint64_t strides[4] = {(cuuint64_t)(rs * cin * 8), 128, 256, (cuuint64_t)(cin * 8)};
+    cuuint32_t box[5] = {64, 32, 2, (cuuint32_t)(bn / 32), 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(c.b), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, kMnSwz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (3d S32 filter) failed (%d)", (int)r);
+    st = DBS_OK;
+  } else if (c.b_mode == 1) {
+    DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
+    st = make_tmap_s32_mn(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, (uint32_t)(bn / 32));
+  } else {
+    DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
+    st = make_tmap_kpair(&tb, c.b, (uint64_t)(4 * ceil32(c.K)), (uint64_t)c.N, (uint64_t)(4 * c.ldb), (uint32_t)bn);
+  }
+  if (st) return st;
+  const int num_l = (int)((c.K + 31) / 32);  // logical (32-wide) k-blocks
+  int splits = c.splits > 0 ? c.splits : 1;
+  if (splits > num_l) splits = num_l;
+  p.kb_per_split = (num_l + splits - 1) / splits;
+  splits = (num_l + p.kb_per_split - 1) / p.kb_per_split;
+  DBS_REQUIRE(splits == 1 || c.epi == DBS_EPI_F32_ATOMIC, DBS_ERR_ARGUMENT, "split-K needs the atomic epilogue");
+  return dispatch(ta, tb, p, bn, splits, s, false, true);
+}
+
 // Implicit-GEMM convolution family (see gemm.cuh).
 int conv_gemm(const ConvCall& c, cudaStream_t s) {
+  if (c.tf) return conv_gemm_tf(c, s);
   DBS_REQUIRE(c.d && c.M > 0 && c.N > 0 && c.K > 0, DBS_ERR_ARGUMENT, "conv_gemm: bad call");
   DBS_REQUIRE(c.M < (int64_t(1) << 31) && c.K < (int64_t(1) << 31), DBS_ERR_ARGUMENT,
               "conv_gemm: M and K must stay below 2^31 (32-bit tile / pixel arithmetic)");
@@ -2024,4 +2490,11 @@ extern "C" int dbs_dev_gemm_bf16(const void* d_a, int32_t a_major, int64_t lda, 
                                  int32_t epilogue, const float* d_bias, void* d_aux, void* stream) {
   return dbs::gemm_bf16(d_a, a_major, lda, d_b, b_major, ldb, d_d, ldd, M, N, K, epilogue, d_bias, d_aux,
                         dbs::as_stream(stream), nullptr);
+}
+
+extern "C" int dbs_dev_gemm_tf32x3(const void* d_a, int32_t a_major, int64_t lda, const void* d_b, int32_t b_major,
+                                   int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N, int64_t K,
+                                   int32_t epilogue, const float* d_bias, void* d_aux, void* stream) {
+  return dbs::gemm_tf(d_a, a_major, lda, d_b, b_major, ldb, d_d, ldd, M, N, K, epilogue, d_bias, d_aux,
+                      dbs::as_stream(stream));
 }

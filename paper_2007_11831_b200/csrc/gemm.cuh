@@ -68,12 +68,19 @@ struct ConvCall {
   ConvTaps cls_taps[4];
   OutMap cls_omap[4];
   int d_trans;               // F32 atomic epilogue writes D transposed: d[n * ldd + m]
+  // S32 operands (3xTF32, fp32-class): tensors / channel counts / ld are logical,
+  // the operands are in the S32 format of dbs_dev_gemm_tf32x3; ConvGeom.cblocks
+  // counts 32-channel blocks.  No halo / pairing / transposed-wgrad variants.
+  int tf;
 };
 
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
               int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
               float* colsum_part);
 int conv_gemm(const ConvCall& c, cudaStream_t s);
+// plain GEMM with S32 operands (lda / ldb / ldd logical, multiples of 32)
+int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
+            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s);
 int preload_gemm();
 // the halo variant's one-box-per-tile input halo fits its shared-memory slot
 bool halo_fits(int OH, int OW);
