@@ -168,6 +168,10 @@ int dbs_dev_gather_rows(const void* d_src, const int64_t* d_idx, int64_t rows,
 /* Same, converting fp32 rows of `cols` elements to bf16 (model input staging). */
 int dbs_dev_gather_rows_f32_bf16(const float* d_src, const int64_t* d_idx, int64_t rows,
                                  int64_t cols, void* d_dst_bf16, void* stream);
+/* fp32 rows -> S32 rows of ld_out (% 32) logical columns (the fp32-class MLP input
+ * format; columns past cols zero). */
+int dbs_dev_gather_rows_f32_s32(const float* d_src, const int64_t* d_idx, int64_t rows, int64_t cols,
+                                float* d_dst, int64_t ld_out, void* stream);
 /* Same for int32 labels. */
 int dbs_dev_gather_i32(const int32_t* d_src, const int64_t* d_idx, int64_t rows,
                        int32_t* d_dst, void* stream);
@@ -197,6 +201,20 @@ int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* batch_
                               int32_t mode, int64_t P, float step, float momentum, float* d_x,
                               float* d_v, uint16_t* d_x_bf16, void* stream);
 
+/* Operand precision of a model's tensor-core path:
+ *   DBS_PREC_BF16 -- bf16 GEMM operands, parameter shadow bf16 [P];
+ *   DBS_PREC_F32  -- fp32-class 3xTF32 GEMMs on S32 operands (dbs_dev_gemm_tf32x3),
+ *                    parameter shadow = the flat param vector in S32 format
+ *                    (2P floats: element i's hi at 2 (i & ~31) + (i & 31), lo 32 later;
+ *                    every tensor starts at a multiple of 32, P % 32 == 0). */
+enum { DBS_PREC_BF16 = 0, DBS_PREC_F32 = 1 };
+/* aggregate + step writing the operand shadow in shadow_prec's format */
+int dbs_dev_aggregate_sgd_f32_ex(const float* const* d_grads, const int64_t* batch_sizes, int64_t n,
+                                 int32_t mode, int64_t P, float step, float momentum, float* d_x,
+                                 float* d_v, void* d_shadow, int32_t shadow_prec, void* stream);
+/* shadow <- the operand copy of fp32 params x[P] (DBS_PREC_* format) */
+int dbs_dev_refresh_shadow(const float* d_x, int64_t P, void* d_shadow, int32_t prec, void* stream);
+
 /* Multi-GPU: one process per GPU.  A communicator holds the peer-mapped
  * (CUDA IPC over NVLink/NVSwitch) symmetric buffers:
  *   grad[P] fp32, param[P] fp32, param_bf16[P], signal words.
@@ -208,7 +226,13 @@ int dbs_comm_handle_size(void);
 int dbs_comm_alloc(int32_t rank, int32_t world, int64_t P, dbs_comm** out, void* handle_out);
 int dbs_comm_open(dbs_comm* comm, const void* all_handles /* world * handle_size */);
 int dbs_comm_buffers(dbs_comm* comm, float** d_grad, float** d_param, uint16_t** d_param_bf16);
-/* padded parameter count (multiple of 4 * world) and the per-rank shard length */
+/* Parameter operand shadow of the communicator: DBS_PREC_BF16 (default) = its bf16
+ * block, pushed to every peer with the fp32 parameters; DBS_PREC_F32 = a local S32
+ * buffer of 2 P floats (P = the padded count), refreshed by the iteration driver
+ * after each update (the fused kernel then pushes fp32 only). */
+int dbs_comm_set_shadow(dbs_comm* comm, void* d_shadow, int32_t prec);
+int dbs_comm_shadow(const dbs_comm* comm, void** d_shadow, int32_t* prec);
+/* padded parameter count (multiple of 32 * world) and the per-rank shard length */
 int dbs_comm_info(const dbs_comm* comm, int64_t* padded_P, int64_t* shard);
 /* unmap the IPC-opened peer blocks (before dbs_comm_destroy) */
 int dbs_comm_close_peers(dbs_comm* comm);
@@ -308,10 +332,17 @@ int dbs_dev_join_s32(const float* d_s32, int64_t rows, int64_t cols, int64_t ld_
 typedef struct dbs_mlp dbs_mlp;
 int dbs_mlp_create(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch,
                    dbs_mlp** out);
+/* precision DBS_PREC_*: DBS_PREC_F32 runs the 5 GEMMs as 3xTF32 on S32 operands;
+ * its layout pads W1's rows to in_ld = in rounded up to 32 and starts every block
+ * on a 32-element boundary, and its input rows are S32 [batch][in_ld]. */
+int dbs_mlp_create_ex(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch, int32_t precision,
+                      dbs_mlp** out);
+int dbs_mlp_info(const dbs_mlp* m, int32_t* precision, int64_t* in_ld);
 int dbs_mlp_destroy(dbs_mlp* m);
 int dbs_mlp_param_count(const dbs_mlp* m, int64_t* out);
-int dbs_mlp_forward_backward(dbs_mlp* m, const uint16_t* d_params_bf16, const float* d_params,
-                             const uint16_t* d_x_bf16, const int32_t* d_labels, int64_t batch,
+/* d_params_shadow / d_x: bf16 (DBS_PREC_BF16) or S32 (DBS_PREC_F32) */
+int dbs_mlp_forward_backward(dbs_mlp* m, const void* d_params_shadow, const float* d_params,
+                             const void* d_x, const int32_t* d_labels, int64_t batch,
                              float* d_grad, float* d_loss, void* stream);
 
 /* ResNet-18, CIFAR variant (3x3 stem, no max-pool; 11,173,962 weights): one
@@ -328,7 +359,8 @@ int dbs_resnet_param_count(const dbs_resnet* m, int64_t* P);
  * [64][32], 27 used), 1 BN gamma, 2 BN beta, 3 FC weight [C][512], 4 FC bias */
 int dbs_resnet_param_table(const dbs_resnet* m, int64_t* off, int64_t* len, int32_t* kind, int32_t capacity,
                            int32_t* count);
-int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, const float* d_params,
+/* d_params_shadow: the operand copy of d_params in the model's precision (bf16 [P] or S32 [2P floats]) */
+int dbs_resnet_forward_backward(dbs_resnet* m, const void* d_params_shadow, const float* d_params,
                                 const void* d_x, const int32_t* d_labels, int64_t batch, const int64_t* d_iter,
                                 float* d_grad, float* d_loss, void* stream);
 /* ResNet-50 (config 5; torchvision layout, stride on the 3x3 conv, 25,557,032
@@ -337,6 +369,15 @@ int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, co
  * (pixel (u - 128) / 64), the stem weight is stored [64][160] (147 used), the
  * FC weight [classes][2048].  depth = 18 / image = 32 is dbs_resnet_create. */
 int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_batch, int32_t classes, dbs_resnet** out);
+/* The same with an operand precision (DBS_PREC_*).  DBS_PREC_F32: every conv / FC
+ * GEMM is 3xTF32 on S32 operands, conv outputs and input gradients are stored
+ * fp32, GEMM operands S32; BatchNorm running statistics (torch semantics,
+ * momentum 0.1, unbiased variance) are tracked per worker. */
+int dbs_resnet_create_ex2(int32_t depth, int32_t image, int64_t max_batch, int32_t classes, int32_t precision,
+                          dbs_resnet** out);
+int dbs_resnet_precision(const dbs_resnet* m, int32_t* precision);
+/* device pointer to conv `conv`'s running statistics: [cout] mean, [cout] variance */
+int dbs_resnet_running_stats(const dbs_resnet* m, int32_t conv, float** d_stats, int32_t* channels);
 /* depth, input side, bytes per input row, padded stem K (any pointer may be NULL) */
 int dbs_resnet_info(const dbs_resnet* m, int32_t* depth, int32_t* image, int64_t* row_bytes, int32_t* stem_k);
 
@@ -352,6 +393,14 @@ int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int32_t W, int3
                          void* stream);
 int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin,
                          int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw, void* stream);
+/* fp32-class forms: S32 operands (NHWC activations, [Cout][k][k][Cin] weights,
+ * channels multiples of 32), fp32 outputs (y, dx; dw accumulated atomically) */
+int dbs_dev_conv2d_fwd_s32(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
+                           int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_y, void* stream);
+int dbs_dev_conv2d_dgrad_s32(const void* d_dy, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
+                             int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dx, void* stream);
+int dbs_dev_conv2d_wgrad_s32(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                             int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw, void* stream);
 
 /* One worker of a synchronous iteration (simulated worker on a shared GPU or
  * one rank's local worker).  Device pointers unless noted. */
@@ -394,9 +443,11 @@ int dbs_dev_spin_until_ctx(int32_t num_ctas, const volatile int32_t* d_stop, voi
  * momentum-SGD update (mode DBS_AGG_*) on agg_stream, ordered with events;
  * skip_update = 1 measures compute only.  With d_iter != NULL (ResNet only) the
  * kernels read the iteration index from *d_iter and the update increments it,
- * so every iteration is the same launch sequence (CUDA-graph capturable). */
+ * so every iteration is the same launch sequence (CUDA-graph capturable).
+ * d_params_shadow is the operand copy in the workers' model precision (bf16 [P]
+ * or S32 [2P floats]); all workers must share one precision. */
 int dbs_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
-                       float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                       float momentum, float* d_params, float* d_velocity, void* d_params_shadow,
                        int32_t skip_update, void* agg_stream, int64_t* d_iter);
 /* Multi-GPU form (one process per GPU): the rank's n local workers, then a local
  * weighted reduce into the communicator's gradient block and the fused NVLink
@@ -418,21 +469,24 @@ int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* batch_size
  * indices are host-side (t0..t1 of the epoch). */
 int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                              float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
-                             uint16_t* const* d_params_bf16, void* agg_stream);
+                             void* const* d_params_shadow, void* agg_stream);
 /* The same across GPUs (one process per GPU): after the local average of every
  * sync round, d_params[0] -- which must be the communicator's parameter block --
  * is averaged across ranks with rank weights = rank_batches[r] (the ranks' batch
  * sums) by the fused NVLink kernel and copied back into the other replicas. */
 int dbs_run_iterations_local_comm(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                   float lr, float momentum, int32_t sync_interval, float* const* d_params,
-                                  float* const* d_velocity, uint16_t* const* d_params_bf16, dbs_comm* comm,
+                                  float* const* d_velocity, void* const* d_params_shadow, dbs_comm* comm,
                                   const int64_t* rank_batches, void* agg_stream);
 /* x_bar = sum_i w_i x_i (w as in dbs_dev_aggregate_*), written to every replica
  * and its bf16 copy (d_params_bf16 may be NULL). P % 4 == 0. */
 int dbs_dev_average_replicas_f32(float* const* d_params, const int64_t* b, int64_t n, int32_t mode, int64_t P,
                                  uint16_t* const* d_params_bf16, void* stream);
+/* the same with the shadows in shadow_prec's format (d_shadows may be NULL) */
+int dbs_dev_average_replicas_f32_ex(float* const* d_params, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                                    void* const* d_shadows, int32_t shadow_prec, void* stream);
 int dbs_mlp_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
-                           float lr, float momentum, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                           float lr, float momentum, float* d_params, float* d_velocity, void* d_params_shadow,
                            int32_t skip_update, void* agg_stream);
 
 /* ------------------------------------------------------------------------ */

@@ -87,6 +87,7 @@ SIGNATURES = {
     "dbs_dev_permute_spans": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "dbs_dev_gather_rows": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "dbs_dev_gather_rows_f32_bf16": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "dbs_dev_gather_rows_f32_s32": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "dbs_dev_gather_i32": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "dbs_dev_aggregate_f64": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, c_vp, c_vp]),
     "dbs_dev_sgd_step_f64": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
@@ -94,6 +95,11 @@ SIGNATURES = {
                                           c_vp, c_vp]),
     "dbs_dev_aggregate_sgd_f32": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, c_flt, c_flt, c_vp,
                                           c_vp, c_vp, c_vp]),
+    "dbs_dev_aggregate_sgd_f32_ex": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, c_flt, c_flt, c_vp,
+                                             c_vp, c_vp, c_i32, c_vp]),
+    "dbs_dev_refresh_shadow": (c_i32, [c_vp, c_i64, c_vp, c_i32, c_vp]),
+    "dbs_comm_set_shadow": (c_i32, [c_vp, c_vp, c_i32]),
+    "dbs_comm_shadow": (c_i32, [c_vp, ctypes.POINTER(c_vp), P_i32]),
     "dbs_comm_handle_size": (c_i32, []),
     "dbs_comm_alloc": (c_i32, [c_i32, c_i32, c_i64, ctypes.POINTER(c_vp), c_vp]),
     "dbs_comm_open": (c_i32, [c_vp, c_vp]),
@@ -116,6 +122,8 @@ SIGNATURES = {
     "dbs_dev_split_s32": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "dbs_dev_join_s32": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "dbs_mlp_create": (c_i32, [c_i64, c_i64, c_i64, c_i64, ctypes.POINTER(c_vp)]),
+    "dbs_mlp_create_ex": (c_i32, [c_i64, c_i64, c_i64, c_i64, c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_mlp_info": (c_i32, [c_vp, P_i32, P_i64]),
     "dbs_mlp_destroy": (c_i32, [c_vp]),
     "dbs_mlp_param_count": (c_i32, [c_vp, P_i64]),
     "dbs_mlp_forward_backward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
@@ -135,6 +143,9 @@ SIGNATURES = {
                                               c_vp, P_i64, c_vp]),
     "dbs_resnet_create": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_vp)]),
     "dbs_resnet_create_ex": (c_i32, [c_i32, c_i32, c_i64, c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_resnet_create_ex2": (c_i32, [c_i32, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_resnet_precision": (c_i32, [c_vp, P_i32]),
+    "dbs_resnet_running_stats": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_vp), P_i32]),
     "dbs_resnet_info": (c_i32, [c_vp, P_i32, P_i32, P_i64, P_i32]),
     "dbs_resnet_destroy": (c_i32, [c_vp]),
     "dbs_resnet_param_count": (c_i32, [c_vp, P_i64]),
@@ -144,6 +155,13 @@ SIGNATURES = {
     "dbs_dev_conv2d_dgrad": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp,
                                      c_vp]),
     "dbs_dev_conv2d_wgrad": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "dbs_dev_conv2d_fwd_s32": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "dbs_dev_conv2d_dgrad_s32": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp,
+                                         c_vp]),
+    "dbs_dev_conv2d_wgrad_s32": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
+                                         c_vp]),
+    "dbs_dev_average_replicas_f32_ex": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64,
+                                                ctypes.POINTER(c_vp), c_i32, c_vp]),
     "dbs_dev_spin_until": (c_i32, [c_i32, c_vp, c_vp]),
     "dbs_dev_spin_until_ctx": (c_i32, [c_i32, c_vp, c_vp, c_vp]),
     "dbs_partition_create": (c_i32, [c_i32, c_i32, ctypes.POINTER(c_vp), P_i32]),
@@ -207,6 +225,38 @@ def require_device():
 
 def ptr(t) -> int:
     return int(t.data_ptr())
+
+
+PREC_BF16, PREC_F32 = 0, 1
+PRECISIONS = {"bf16": PREC_BF16, "f32": PREC_F32}
+
+
+def precision_code(precision) -> int:
+    """'f32' (3xTF32 tensor-core GEMMs on S32 operands, the fp32 class) or 'bf16'."""
+    if isinstance(precision, int) and precision in (PREC_BF16, PREC_F32):
+        return precision
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be 'f32' or 'bf16', got {precision!r}")
+    return PRECISIONS[precision]
+
+
+def new_shadow(params, precision):
+    """Operand copy of flat fp32 params on the device: bf16 [P] or S32 [2P] floats."""
+    import torch
+
+    code = precision_code(precision)
+    if code == PREC_BF16:
+        return params.to(torch.bfloat16)
+    out = torch.empty(2 * params.numel(), dtype=torch.float32, device=params.device)
+    refresh_shadow(params, out, code)
+    return out
+
+
+def refresh_shadow(params, shadow, precision, stream=None):
+    code = precision_code(precision)
+    st = lib().dbs_dev_refresh_shadow(params.data_ptr(), int(params.numel()), shadow.data_ptr(), code,
+                                      stream_handle(stream))
+    check(st, "refresh_shadow")
 
 
 def env_flag(name: str) -> bool:

@@ -83,6 +83,14 @@ class Communicator:
         _lib.check(_lib.lib().dbs_comm_create_local(world, int(P), arr), "comm_create_local")
         return [cls(ctypes.c_void_p(arr[r]), r, world, dev, ipc=False) for r in range(world)]
 
+    def set_shadow(self, shadow, precision):
+        """Register the parameter operand copy: precision "bf16" = the block's bf16
+        region (pushed to every peer), "f32" = a local S32 tensor of 2 P floats that
+        the iteration driver refreshes after each update."""
+        code = _lib.precision_code(precision)
+        st = _lib.lib().dbs_comm_set_shadow(self.h, shadow.data_ptr() if shadow is not None else None, code)
+        _lib.check(st, "comm_set_shadow")
+
     # -- data path -------------------------------------------------------------
     def allreduce_sgd(self, batch_sizes, lr: float, momentum: float, mode: int = 1, stream=None):
         b = np.ascontiguousarray(np.asarray([int(x) for x in batch_sizes], dtype=np.int64))

@@ -58,6 +58,11 @@ struct dbs_comm {
   uint32_t gen = 0;      // barrier generation (identical sequence on every rank)
   PeerTable table{};
   int grid = 0;
+  // operand shadow of the parameters: DBS_PREC_BF16 = the block's bf16 region,
+  // pushed to every peer by the fused kernel; DBS_PREC_F32 = a registered local S32
+  // buffer (dbs_comm_set_shadow) that the caller refreshes after the update
+  int shadow_prec = DBS_PREC_BF16;
+  void* shadow = nullptr;
 };
 
 namespace dbs {
@@ -79,15 +84,18 @@ __device__ __forceinline__ long long gtimer() {
 }
 
 // Wait until every rank's flag reached `gen`.  A peer that never arrives (dead
-// rank, mismatched call sequence) must not wedge the GPU: after 20 s the wait
-// gives up and raises the error word (signal[48]) that the host checks.
+// rank, mismatched call sequence) must not wedge the GPU, and the update must not
+// silently reduce an incomplete gradient: after 20 s the wait records the error
+// word (signal[48], for post-mortems) and traps, so the launch fails with a CUDA
+// error that the next synchronising call on the host reports.
 __device__ __forceinline__ void wait_flags(const uint32_t* base, int world, uint32_t gen, uint32_t* err) {
   const long long t0 = gtimer();
   for (int j = 0; j < world; j++) {
     while ((int32_t)(ld_acquire_sys(base + j) - gen) < 0) {
       if (gtimer() - t0 > 20000000000LL) {
         atomicExch(err, 1u);
-        return;
+        __threadfence_system();
+        __trap();
       }
     }
   }
@@ -99,7 +107,8 @@ __device__ __forceinline__ uint32_t bf16_bits(float f) {
 }
 
 // mode 0: gradient all-reduce + SGD;  mode 1: parameter averaging
-template <int MODE>
+// BF16: also push the bf16 operand shadow (an S32-shadow communicator refreshes its own)
+template <int MODE, bool BF16>
 __global__ void __launch_bounds__(kThreads) fused_kernel(PeerTable T, int rank, int world, int64_t shard4,
                                                          float lr, float mom, float4* __restrict__ vel,
                                                          uint32_t gen) {
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(PeerTable T, int rank, 
       if (j >= world) break;
       const int jj = (rank + j) % world;  // stagger the peers to spread NVLink traffic
       reinterpret_cast<float4*>(T.param[jj])[p4] = x;
-      reinterpret_cast<uint2*>(T.param_bf16[jj])[p4] = xb;
+      if (BF16) reinterpret_cast<uint2*>(T.param_bf16[jj])[p4] = xb;
     }
   }
   // ---- phase 2: all shards written everywhere --------------------------------
@@ -198,11 +207,19 @@ int launch_fused(dbs_comm* c, const int64_t* batch_sizes, int32_t mode, int kind
     c->table.w[j] = (float)(mode == DBS_AGG_BATCH_WEIGHTED ? (double)batch_sizes[j] / tot : 1.0 / c->world);
   c->gen += 1;
   const int64_t shard4 = c->shard / 4;
-  if (kind == 0)
-    fused_kernel<0><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, lr, mom,
-                                                  reinterpret_cast<float4*>(vel), c->gen);
+  const bool bf = c->shadow_prec == DBS_PREC_BF16;
+  if (kind == 0 && bf)
+    fused_kernel<0, true><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, lr, mom,
+                                                        reinterpret_cast<float4*>(vel), c->gen);
+  else if (kind == 0)
+    fused_kernel<0, false><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, lr, mom,
+                                                         reinterpret_cast<float4*>(vel), c->gen);
+  else if (bf)
+    fused_kernel<1, true><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, 0.f, 0.f, nullptr,
+                                                        c->gen);
   else
-    fused_kernel<1><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, 0.f, 0.f, nullptr, c->gen);
+    fused_kernel<1, false><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, 0.f, 0.f, nullptr,
+                                                         c->gen);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -220,7 +237,7 @@ static int comm_new(int32_t rank, int32_t world, int64_t P, dbs_comm** out) {
   dbs_comm* c = new dbs_comm();
   c->rank = rank;
   c->world = world;
-  const int64_t q = 4 * (int64_t)world;
+  const int64_t q = 32 * (int64_t)world;  // shards of whole float4s and 32-element S32 blocks
   c->P = (P + q - 1) / q * q;
   c->shard = c->P / world;
   size_t op, ob, os;
@@ -297,6 +314,21 @@ extern "C" int dbs_comm_buffers(dbs_comm* c, float** d_grad, float** d_param, ui
   if (d_grad) *d_grad = c->table.grad[c->rank];
   if (d_param) *d_param = c->table.param[c->rank];
   if (d_param_bf16) *d_param_bf16 = c->table.param_bf16[c->rank];
+  return DBS_OK;
+}
+
+extern "C" int dbs_comm_set_shadow(dbs_comm* c, void* d_shadow, int32_t prec) {
+  DBS_REQUIRE(c && (prec == DBS_PREC_BF16 || (prec == DBS_PREC_F32 && d_shadow && c->P % 32 == 0)), DBS_ERR_ARGUMENT,
+              "comm_set_shadow: bf16, or an S32 buffer of 2 P floats (padded P %% 32 == 0)");
+  c->shadow_prec = prec;
+  c->shadow = prec == DBS_PREC_F32 ? d_shadow : nullptr;
+  return DBS_OK;
+}
+
+extern "C" int dbs_comm_shadow(const dbs_comm* c, void** d_shadow, int32_t* prec) {
+  DBS_REQUIRE(c, DBS_ERR_ARGUMENT, "comm_shadow: null comm");
+  if (d_shadow) *d_shadow = c->shadow_prec == DBS_PREC_F32 ? c->shadow : (void*)c->table.param_bf16[c->rank];
+  if (prec) *prec = c->shadow_prec;
   return DBS_OK;
 }
 

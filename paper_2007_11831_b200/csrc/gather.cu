@@ -77,6 +77,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
+__device__ __forceinline__ float rn_tf32(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
+}
+
+// fp32 rows of `cols` (cols % 4 == 0) -> S32 rows of ld_out (ld_out % 32 == 0, pad columns
+// zero): the fp32-class operand format (s32.cu), written once per epoch with the repack
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    gather_f32_s32_kernel(const float4* __restrict__ src, const int64_t* __restrict__ idx, int64_t rows,
+                          int64_t vec_per_row, int64_t ld_out, float* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  const int64_t q_out = ld_out / 4;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float4* s = src + __ldg(&idx[r]) * vec_per_row;
+    float* d = dst + r * 2 * ld_out;
+    for (int64_t c = lane; c < q_out; c += 32) {
+      const float4 v = c < vec_per_row ? __ldcs(s + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 h = make_float4(rn_tf32(v.x), rn_tf32(v.y), rn_tf32(v.z), rn_tf32(v.w));
+      const int64_t e = 4 * c;
+      float* o = d + 2 * (e & ~int64_t(31)) + (e & 31);
+      __stcs(reinterpret_cast<float4*>(o), h);
+      __stcs(reinterpret_cast<float4*>(o + 32),
+             make_float4(rn_tf32(v.x - h.x), rn_tf32(v.y - h.y), rn_tf32(v.z - h.z), rn_tf32(v.w - h.w)));
+    }
+  }
+}
+
 __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ idx,
                                   int64_t rows, int32_t* __restrict__ dst) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
@@ -125,6 +154,18 @@ extern "C" int dbs_dev_gather_rows_f32_bf16(const float* d_src, const int64_t* d
   if (rows == 0 || cols == 0) return DBS_OK;
   gather_f32_bf16_kernel<<<grid_for_rows(rows), kWarpsPerBlock * 32, 0, as_stream(stream)>>>(
       (const float4*)d_src, d_idx, rows, cols / 4, (uint2*)d_dst);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_gather_rows_f32_s32(const float* d_src, const int64_t* d_idx, int64_t rows, int64_t cols,
+                                           float* d_dst, int64_t ld_out, void* stream) {
+  DBS_REQUIRE(rows >= 0 && cols % 4 == 0 && ld_out >= cols && ld_out % 32 == 0 && ((uintptr_t)d_src % 16 == 0) &&
+                  ((uintptr_t)d_dst % 16 == 0),
+              DBS_ERR_ARGUMENT, "dbs_dev_gather_rows_f32_s32: cols %% 4, ld_out %% 32 >= cols, aligned buffers");
+  if (rows == 0 || cols == 0) return DBS_OK;
+  gather_f32_s32_kernel<<<grid_for_rows(rows), kWarpsPerBlock * 32, 0, as_stream(stream)>>>(
+      (const float4*)d_src, d_idx, rows, cols / 4, ld_out, d_dst);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }

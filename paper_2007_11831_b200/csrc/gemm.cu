@@ -2072,7 +2072,8 @@ int64_t ceil32(int64_t x) { return (x + 31) & ~int64_t(31); }
 constexpr CUtensorMapSwizzle kMnSwz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
 
 int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
-            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s) {
+            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
+            float* colsum_part) {
   DBS_REQUIRE(M > 0 && N > 0 && K > 0 && a && b && d, DBS_ERR_ARGUMENT, "gemm_tf: bad shape/pointers");
   DBS_REQUIRE((M / 128 + 1) * (N / 16 + 1) < (int64_t(1) << 31), DBS_ERR_ARGUMENT, "gemm_tf: too many tiles");
   DBS_REQUIRE(epi == DBS_EPI_F32 || epi == DBS_EPI_F32_ACCUM || epi == DBS_EPI_BIAS_F32 || epi == DBS_EPI_F32_ATOMIC ||
@@ -2085,6 +2086,7 @@ int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64
               "gemm_tf: S32 leading dimensions must be multiples of 32");
   DBS_REQUIRE(lda >= (a_mn ? M : K) && ldb >= (b_mn ? N : K), DBS_ERR_ARGUMENT, "gemm_tf: leading dimension too small");
   const int bn = pick_bn(N, b_mn) > 128 ? 128 : pick_bn(N, b_mn);
+  DBS_REQUIRE(!(colsum_part && bn < 32), DBS_ERR_ARGUMENT, "gemm_tf: column sums need N > 16");
   CUtensorMap ta, tb;
   int st = a_mn ? make_tmap_s32_mn(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 4)
                 : make_tmap_kpair(&ta, a, (uint64_t)(4 * ceil32(K)), (uint64_t)M, (uint64_t)(4 * lda), 128);
@@ -2103,6 +2105,7 @@ int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64
   p.ldd = ldd;
   p.bias = bias;
   p.aux = reinterpret_cast<const uint16_t*>(aux);
+  p.colsum_part = colsum_part;
   p.kb_per_split = (int)((K + 31) / 32);
   return dispatch(ta, tb, p, bn, 1, s, false, true);
 }
@@ -2496,5 +2499,5 @@ extern "C" int dbs_dev_gemm_tf32x3(const void* d_a, int32_t a_major, int64_t lda
                                    int64_t ldb, void* d_d, int64_t ldd, int64_t M, int64_t N, int64_t K,
                                    int32_t epilogue, const float* d_bias, void* d_aux, void* stream) {
   return dbs::gemm_tf(d_a, a_major, lda, d_b, b_major, ldb, d_d, ldd, M, N, K, epilogue, d_bias, d_aux,
-                      dbs::as_stream(stream));
+                      dbs::as_stream(stream), nullptr);
 }

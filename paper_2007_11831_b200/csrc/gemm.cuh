@@ -80,7 +80,8 @@ int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int
 int conv_gemm(const ConvCall& c, cudaStream_t s);
 // plain GEMM with S32 operands (lda / ldb / ldd logical, multiples of 32)
 int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
-            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s);
+            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
+            float* colsum_part = nullptr);
 int preload_gemm();
 // the halo variant's one-box-per-tile input halo fits its shared-memory slot
 bool halo_fits(int OH, int OW);

@@ -25,6 +25,9 @@ namespace dbs {
 int gemm_bf16(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
               int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
               float* colsum_part);
+int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64_t ldb, void* d, int64_t ldd,
+            int64_t M, int64_t N, int64_t K, int epi, const float* bias, const void* aux, cudaStream_t s,
+            float* colsum_part = nullptr);
 int stamp(int64_t* d_stamps, int64_t slot, cudaStream_t s);
 int spin_scaled(const int64_t* d_stamps, int64_t b, int64_t e, float scale, int ctas, cudaStream_t s);
 int ctx_push(void* ctx);
@@ -33,11 +36,13 @@ int ctx_pop(void* ctx);
 
 struct dbs_mlp {
   int64_t in, hid, cls, max_b;
+  int prec = DBS_PREC_BF16;     // DBS_PREC_F32: S32 operands, 3xTF32 GEMMs
+  int64_t in_ld;                // W1 row length / input row length (f32: in rounded up to 32)
   int64_t off_w1, off_b1, off_w2, off_b2, P;
-  uint16_t* act = nullptr;      // [max_b][hid]
+  void* act = nullptr;          // [max_b][hid] bf16 | S32
   float* logits = nullptr;      // [max_b][16]
-  uint16_t* dz = nullptr;       // [max_b][16]
-  uint16_t* dh = nullptr;       // [max_b][hid]
+  void* dz = nullptr;           // [max_b][16] bf16 | [max_b][32] S32
+  void* dh = nullptr;           // [max_b][hid] bf16 | S32
   float* colsum = nullptr;      // [ceil(max_b/32)][hid]
 };
 
@@ -104,6 +109,63 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict
   }
 }
 
+// fp32-class form: dZ written in S32 ([b][32], zero past cls -- the K padding of
+// the dH GEMM and the M tail of the dW2 GEMM)
+__device__ __forceinline__ float rn_tf32(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
+}
+__global__ void __launch_bounds__(256) softmax_ce_s32_kernel(const float* __restrict__ z, const int32_t* __restrict__ y,
+                                                             int64_t b, int cls, float* __restrict__ dz,
+                                                             float* __restrict__ db2, float* __restrict__ loss) {
+  __shared__ float red[8][17];
+  float acc[16];
+  float lsum = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 16; c++) acc[c] = 0.0f;
+  const float inv_b = 1.0f / (float)b;
+  for (int64_t r = threadIdx.x; r < b; r += blockDim.x) {
+    const float* zr = z + r * kLdZ;
+    float mx = -INFINITY;
+    for (int c = 0; c < cls; c++) mx = fmaxf(mx, zr[c]);
+    float se = 0.0f;
+    float e[16];
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      e[c] = (c < cls) ? expf(zr[c] - mx) : 0.0f;
+      se += e[c];
+    }
+    const int yr = y[r];
+    lsum += (mx + logf(se)) - zr[yr];
+    const float inv = 1.0f / se;
+    float* d = dz + r * 64;
+#pragma unroll
+    for (int c = 0; c < 32; c++) {
+      const float g = (c < cls) ? (e[c & 15] * inv - (c == yr ? 1.0f : 0.0f)) * inv_b : 0.0f;
+      if (c < 16) acc[c] += g;
+      const float h = rn_tf32(g);
+      d[c] = h;
+      d[32 + c] = rn_tf32(g - h);
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    float s = acc[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp][c] = s;
+  }
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if (lane == 0) red[warp][16] = lsum;
+  __syncthreads();
+  if (threadIdx.x < 17) {
+    float s = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w][threadIdx.x];
+    if (threadIdx.x < cls) db2[threadIdx.x] = s;
+    if (threadIdx.x == 16) *loss = s * inv_b;
+  }
+}
+
 // db1[n] = sum_g part[g][n] over g < groups (fixed order => deterministic)
 __global__ void colsum_reduce_kernel(const float* __restrict__ part, int64_t groups, int64_t n,
                                      float* __restrict__ out) {
@@ -116,11 +178,45 @@ __global__ void colsum_reduce_kernel(const float* __restrict__ part, int64_t gro
 
 }  // namespace
 
-int mlp_fwd_bwd(dbs_mlp* m, const uint16_t* pb, const float* pf, const uint16_t* x, const int32_t* y, int64_t b,
+// fp32-class forward/backward: the same 5 GEMMs on S32 operands (3xTF32).  x is the
+// S32 input [b][in_ld], the shadow the flat S32 parameter vector (W1 [H][in_ld])
+int mlp_fwd_bwd_f32(dbs_mlp* m, const float* sh, const float* pf, const float* x, const int32_t* y, int64_t b,
+                    float* grad, float* loss, cudaStream_t s) {
+  int st;
+  const int64_t I = m->in_ld, H = m->hid, C = m->cls;
+  const float* w1 = sh + 2 * m->off_w1;
+  const float* w2 = sh + 2 * m->off_w2;
+  st = gemm_tf(x, 0, I, w1, 0, I, m->act, H, b, H, I, DBS_EPI_BIAS_RELU_S32, pf + m->off_b1, nullptr, s, nullptr);
+  if (st) return st;
+  st = gemm_tf(m->act, 0, H, w2, 0, H, m->logits, kLdZ, b, C, H, DBS_EPI_BIAS_F32, pf + m->off_b2, nullptr, s, nullptr);
+  if (st) return st;
+  softmax_ce_s32_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, static_cast<float*>(m->dz), grad + m->off_b2, loss);
+  DBS_LAUNCH_CHECK();
+  // dW2 [C][H] = dZ^T H  (dZ S32 [b][32] MN-major, M = C)
+  st = gemm_tf(m->dz, 1, 32, m->act, 1, H, grad + m->off_w2, H, C, H, b, DBS_EPI_F32, nullptr, nullptr, s, nullptr);
+  if (st) return st;
+  // dH = (dZ W2) * [H > 0]: K = C (padded to 32 with dZ's zero columns), W2 [C][H] read MN-major
+  st = gemm_tf(m->dz, 0, 32, w2, 1, H, m->dh, H, b, H, C, DBS_EPI_RELU_GRAD_S32, nullptr, m->act, s, m->colsum);
+  if (st) return st;
+  {
+    int grid = (int)((H + 255) / 256);
+    colsum_reduce_kernel<<<grid, 256, 0, s>>>(m->colsum, (b + 31) / 32, H, grad + m->off_b1);
+    DBS_LAUNCH_CHECK();
+  }
+  // dW1 [H][in_ld] = dH^T X  (columns past `in` are 0: X's zero padding)
+  return gemm_tf(m->dh, 1, H, x, 1, I, grad + m->off_w1, I, H, I, b, DBS_EPI_F32, nullptr, nullptr, s, nullptr);
+}
+
+int mlp_fwd_bwd(dbs_mlp* m, const void* shadow, const float* pf, const void* x_any, const int32_t* y, int64_t b,
                 float* grad, float* loss, cudaStream_t s) {
-  DBS_REQUIRE(m && pb && pf && x && y && grad && loss, DBS_ERR_ARGUMENT, "mlp: null argument");
+  DBS_REQUIRE(m && shadow && pf && x_any && y && grad && loss, DBS_ERR_ARGUMENT, "mlp: null argument");
   DBS_REQUIRE(b >= 1 && b <= m->max_b, DBS_ERR_ARGUMENT, "mlp: batch %lld outside [1, %lld]", (long long)b,
               (long long)m->max_b);
+  if (m->prec == DBS_PREC_F32)
+    return mlp_fwd_bwd_f32(m, static_cast<const float*>(shadow), pf, static_cast<const float*>(x_any), y, b, grad, loss,
+                           s);
+  const uint16_t* pb = static_cast<const uint16_t*>(shadow);
+  const uint16_t* x = static_cast<const uint16_t*>(x_any);
   int st;
   const int64_t I = m->in, H = m->hid, C = m->cls;
   // 1. forward layer 1
@@ -132,7 +228,7 @@ int mlp_fwd_bwd(dbs_mlp* m, const uint16_t* pb, const float* pf, const uint16_t*
                  nullptr, s, nullptr);
   if (st) return st;
   // 3. softmax cross-entropy + db2
-  softmax_ce_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, m->dz, grad + m->off_b2, loss);
+  softmax_ce_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, static_cast<uint16_t*>(m->dz), grad + m->off_b2, loss);
   DBS_LAUNCH_CHECK();
   // 4. dW2 = dZ^T H
   st = gemm_bf16(m->dz, 1, kLdZ, m->act, 1, H, grad + m->off_w2, H, C, H, b, DBS_EPI_F32, nullptr, nullptr, s,
@@ -157,26 +253,36 @@ int mlp_fwd_bwd(dbs_mlp* m, const uint16_t* pb, const float* pf, const uint16_t*
 
 using namespace dbs;
 
-extern "C" int dbs_mlp_create(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch, dbs_mlp** out) {
+extern "C" int dbs_mlp_create_ex(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch, int32_t precision,
+                                 dbs_mlp** out) {
   DBS_REQUIRE(out && in_dim > 0 && hidden > 16 && classes >= 2 && classes <= 16 && max_batch > 0, DBS_ERR_ARGUMENT,
               "mlp_create: need in>0, hidden>16, 2<=classes<=16");
-  DBS_REQUIRE(in_dim % 8 == 0 && hidden % 8 == 0, DBS_ERR_ARGUMENT, "mlp_create: in/hidden must be multiples of 8");
+  DBS_REQUIRE(precision == DBS_PREC_BF16 || precision == DBS_PREC_F32, DBS_ERR_ARGUMENT, "mlp_create: precision %d",
+              precision);
+  DBS_REQUIRE(in_dim % 8 == 0 && hidden % (precision == DBS_PREC_F32 ? 32 : 8) == 0, DBS_ERR_ARGUMENT,
+              "mlp_create: in must be a multiple of 8, hidden of 8 (bf16) / 32 (f32)");
   dbs_mlp* m = new dbs_mlp();
   m->in = in_dim;
   m->hid = hidden;
   m->cls = classes;
   m->max_b = max_batch;
+  m->prec = precision;
+  const bool f32 = precision == DBS_PREC_F32;
+  // f32: every block starts on a 32-element boundary (the flat S32 shadow), W1 rows padded to 32
+  auto padp = [&](int64_t x) { return f32 ? (x + 31) & ~int64_t(31) : pad8(x); };
+  m->in_ld = f32 ? (in_dim + 31) & ~int64_t(31) : in_dim;
   m->off_w1 = 0;
-  m->off_b1 = pad8(hidden * in_dim);
-  m->off_w2 = m->off_b1 + pad8(hidden);
-  m->off_b2 = m->off_w2 + pad8(classes * hidden);
-  m->P = m->off_b2 + pad8(classes);
+  m->off_b1 = padp(hidden * m->in_ld);
+  m->off_w2 = m->off_b1 + padp(hidden);
+  m->off_b2 = m->off_w2 + padp(classes * hidden);
+  m->P = m->off_b2 + padp(classes);
   const int64_t groups = (max_batch + 31) / 32 + 4;
+  const size_t es = f32 ? 8 : 2;  // bytes per stored operand element (S32 hi + lo | bf16)
   cudaError_t e = cudaSuccess;
-  e = e ? e : cudaMalloc(&m->act, sizeof(uint16_t) * max_batch * hidden);
+  e = e ? e : cudaMalloc(&m->act, es * max_batch * hidden);
   e = e ? e : cudaMalloc(&m->logits, sizeof(float) * max_batch * kLdZ);
-  e = e ? e : cudaMalloc(&m->dz, sizeof(uint16_t) * max_batch * kLdZ);
-  e = e ? e : cudaMalloc(&m->dh, sizeof(uint16_t) * max_batch * hidden);
+  e = e ? e : cudaMalloc(&m->dz, f32 ? es * max_batch * 32 : es * max_batch * kLdZ);
+  e = e ? e : cudaMalloc(&m->dh, es * max_batch * hidden);
   e = e ? e : cudaMalloc(&m->colsum, sizeof(float) * groups * hidden);
   if (e != cudaSuccess) {
     set_error("mlp_create: %s", cudaGetErrorString(e));
@@ -184,6 +290,17 @@ extern "C" int dbs_mlp_create(int64_t in_dim, int64_t hidden, int64_t classes, i
     return DBS_ERR_CUDA;
   }
   *out = m;
+  return DBS_OK;
+}
+
+extern "C" int dbs_mlp_create(int64_t in_dim, int64_t hidden, int64_t classes, int64_t max_batch, dbs_mlp** out) {
+  return dbs_mlp_create_ex(in_dim, hidden, classes, max_batch, DBS_PREC_BF16, out);
+}
+
+extern "C" int dbs_mlp_info(const dbs_mlp* m, int32_t* precision, int64_t* in_ld) {
+  DBS_REQUIRE(m, DBS_ERR_ARGUMENT, "mlp_info: null");
+  if (precision) *precision = m->prec;
+  if (in_ld) *in_ld = m->in_ld;
   return DBS_OK;
 }
 
@@ -204,10 +321,10 @@ extern "C" int dbs_mlp_param_count(const dbs_mlp* m, int64_t* out) {
   return DBS_OK;
 }
 
-extern "C" int dbs_mlp_forward_backward(dbs_mlp* m, const uint16_t* d_params_bf16, const float* d_params,
-                                        const uint16_t* d_x_bf16, const int32_t* d_labels, int64_t batch,
+extern "C" int dbs_mlp_forward_backward(dbs_mlp* m, const void* d_params_shadow, const float* d_params,
+                                        const void* d_x, const int32_t* d_labels, int64_t batch,
                                         float* d_grad, float* d_loss, void* stream) {
-  return mlp_fwd_bwd(m, d_params_bf16, d_params, d_x_bf16, d_labels, batch, d_grad, d_loss, as_stream(stream));
+  return mlp_fwd_bwd(m, d_params_shadow, d_params, d_x, d_labels, batch, d_grad, d_loss, as_stream(stream));
 }
 
 // ---------------------------------------------------------------------------
@@ -231,18 +348,34 @@ int events(int n, cudaEvent_t** out) {
 }
 }  // namespace
 
-extern "C" int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode,
-                                         int64_t P, float step, float mom, float* d_x, float* d_v, uint16_t* d_x_bf16,
-                                         void* stream);
+extern "C" int dbs_dev_aggregate_sgd_f32_ex(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode,
+                                            int64_t P, float step, float mom, float* d_x, float* d_v, void* d_shadow,
+                                            int32_t shadow_prec, void* stream);
+extern "C" int dbs_dev_refresh_shadow(const float* d_x, int64_t P, void* d_shadow, int32_t prec, void* stream);
 extern "C" int dbs_dev_spin_for(int32_t num_ctas, int64_t ns, void* stream);
 extern "C" int dbs_dev_accumulate_time(const int64_t* d_stamps, int64_t begin, int64_t end, double* d_seconds,
                                        int64_t worker, void* stream);
 
 namespace dbs {
-int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const void* x_base, const int32_t* y_base,
+int resnet_fwd_bwd(dbs_resnet* m, const void* shadow, const float* pf, const void* x_base, const int32_t* y_base,
                    const int64_t* d_iter, int64_t B, float* grad, float* loss, cudaStream_t s);
 int resnet_param_count(const dbs_resnet* m);
 int64_t resnet_row_bytes(const dbs_resnet* m);
+int resnet_precision(const dbs_resnet* m);
+
+// operand precision (DBS_PREC_*) of a worker's model: the format of the parameter shadow
+int slot_precision(const dbs_worker_slot& w) {
+  return w.model_kind == DBS_MODEL_MLP ? static_cast<const dbs_mlp*>(w.model)->prec
+                                       : resnet_precision(static_cast<const dbs_resnet*>(w.model));
+}
+// bytes of one input row of the worker's shard
+int64_t slot_row_bytes(const dbs_worker_slot& w) {
+  if (w.model_kind == DBS_MODEL_MLP) {
+    const dbs_mlp* m = static_cast<const dbs_mlp*>(w.model);
+    return m->prec == DBS_PREC_F32 ? 8 * m->in_ld : 2 * m->in;
+  }
+  return resnet_row_bytes(static_cast<const dbs_resnet*>(w.model));
+}
 int iter_increment(int64_t* d_iter, cudaStream_t s);
 }  // namespace dbs
 
@@ -251,16 +384,17 @@ extern "C" int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t*
 extern "C" int dbs_comm_allreduce_sgd(dbs_comm* c, const int64_t* batch_sizes, int32_t mode, float step,
                                       float momentum, float* d_velocity_shard, void* stream);
 extern "C" int dbs_comm_buffers(dbs_comm* c, float** d_grad, float** d_param, uint16_t** d_param_bf16);
+extern "C" int dbs_comm_shadow(const dbs_comm* c, void** d_shadow, int32_t* prec);
 
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
-                               float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                               float mom, float* d_params, float* d_velocity, void* d_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
                                const int64_t* rank_batches);
 
 extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
-                                  float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                                  float mom, float* d_params, float* d_velocity, void* d_params_shadow,
                                   int32_t skip_update, void* agg_stream, int64_t* d_iter) {
-  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_bf16, skip_update,
+  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_shadow, skip_update,
                              agg_stream, d_iter, nullptr, nullptr);
 }
 
@@ -274,15 +408,20 @@ extern "C" int dbs_run_iterations_comm(const dbs_worker_slot* w, int32_t n, int6
                                        float* d_velocity_shard, void* agg_stream, int64_t* d_iter) {
   DBS_REQUIRE(comm && rank_batches && d_velocity_shard, DBS_ERR_ARGUMENT, "run_iterations_comm: null argument");
   float *g = nullptr, *p = nullptr;
-  uint16_t* pb = nullptr;
-  int st = dbs_comm_buffers(comm, &g, &p, &pb);
+  void* sh = nullptr;
+  int32_t prec = 0;
+  int st = dbs_comm_buffers(comm, &g, &p, nullptr);
   if (st) return st;
-  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, p, d_velocity_shard, pb, 0, agg_stream, d_iter, comm,
+  st = dbs_comm_shadow(comm, &sh, &prec);
+  if (st) return st;
+  DBS_REQUIRE(n >= 1 && prec == slot_precision(w[0]), DBS_ERR_ARGUMENT,
+              "run_iterations_comm: the communicator's shadow precision differs from the model's");
+  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, p, d_velocity_shard, sh, 0, agg_stream, d_iter, comm,
                              rank_batches);
 }
 
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
-                               float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                               float mom, float* d_params, float* d_velocity, void* d_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
                                const int64_t* rank_batches) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "run_iterations: bad arguments");
@@ -291,6 +430,9 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
                     !(d_iter && w[i].model_kind == DBS_MODEL_MLP),
                 DBS_ERR_ARGUMENT, "run_iterations: worker %d has a bad model (device iteration index is ResNet-only)",
                 i);
+  const int prec = slot_precision(w[0]);
+  for (int i = 1; i < n; i++)
+    DBS_REQUIRE(slot_precision(w[i]) == prec, DBS_ERR_ARGUMENT, "run_iterations: workers mix operand precisions");
   cudaEvent_t* ev;
   int st = events(n + 1, &ev);
   if (st) return st;
@@ -323,8 +465,8 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
       const int64_t b = w[i].batch;
       if (w[i].model_kind == DBS_MODEL_MLP) {
         dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
-        const uint16_t* x = static_cast<const uint16_t*>(w[i].x_shard) + t * b * m->in;
-        st = mlp_fwd_bwd(m, d_params_bf16, d_params, x, w[i].y_shard + t * b, b, w[i].grad,
+        const char* x = static_cast<const char*>(w[i].x_shard) + t * b * slot_row_bytes(w[i]);
+        st = mlp_fwd_bwd(m, d_shadow, d_params, x, w[i].y_shard + t * b, b, w[i].grad,
                          w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
       } else {
         dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
@@ -336,7 +478,7 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
           y += t * b;
           loss = loss ? loss + t : nullptr;
         }
-        st = resnet_fwd_bwd(m, d_params_bf16, d_params, x, y, d_iter, b, w[i].grad, loss, s);
+        st = resnet_fwd_bwd(m, d_shadow, d_params, x, y, d_iter, b, w[i].grad, loss, s);
       }
       if (st) return st;
       if (w[i].stamps) {
@@ -362,8 +504,8 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
     }
     for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
     if (!skip_update && comm == nullptr) {
-      st = dbs_dev_aggregate_sgd_f32(grads, batches, n, mode, P, lr, mom, d_params, d_velocity, d_params_bf16,
-                                     agg_stream);
+      st = dbs_dev_aggregate_sgd_f32_ex(grads, batches, n, mode, P, lr, mom, d_params, d_velocity, d_shadow, prec,
+                                        agg_stream);
       if (st) return st;
     } else if (!skip_update) {
       float* cg = nullptr;
@@ -375,6 +517,10 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
       }
       st = dbs_comm_allreduce_sgd(comm, rank_batches, mode, lr, mom, d_velocity, agg_stream);
       if (st) return st;
+      if (prec == DBS_PREC_F32) {  // the fp32 parameters arrived from every peer; S32 operand copy locally
+        st = dbs_dev_refresh_shadow(d_params, P, d_shadow, prec, agg_stream);
+        if (st) return st;
+      }
     }
     if (d_iter) {
       st = iter_increment(d_iter, agg);
@@ -394,13 +540,13 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
 // worker waits for another.
 static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                 float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
-                                uint16_t* const* d_params_bf16, void* agg_stream, dbs_comm* comm,
+                                void* const* d_shadows, void* agg_stream, dbs_comm* comm,
                                 const int64_t* rank_batches);
 
 extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                         float lr, float mom, int32_t sync_interval, float* const* d_params,
-                                        float* const* d_velocity, uint16_t* const* d_params_bf16, void* agg_stream) {
-  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_bf16,
+                                        float* const* d_velocity, void* const* d_params_shadow, void* agg_stream) {
+  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_shadow,
                               agg_stream, nullptr, nullptr);
 }
 
@@ -412,22 +558,25 @@ extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int
 extern "C" int dbs_run_iterations_local_comm(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1,
                                              int32_t mode, float lr, float mom, int32_t sync_interval,
                                              float* const* d_params, float* const* d_velocity,
-                                             uint16_t* const* d_params_bf16, dbs_comm* comm,
+                                             void* const* d_params_shadow, dbs_comm* comm,
                                              const int64_t* rank_batches, void* agg_stream) {
   DBS_REQUIRE(comm && rank_batches, DBS_ERR_ARGUMENT, "run_iterations_local_comm: null communicator / batches");
-  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_bf16,
+  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_shadow,
                               agg_stream, comm, rank_batches);
 }
 
 static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                 float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
-                                uint16_t* const* d_params_bf16, void* agg_stream, dbs_comm* comm,
+                                void* const* d_shadows, void* agg_stream, dbs_comm* comm,
                                 const int64_t* rank_batches) {
-  DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0 && sync_interval >= 1 && d_params && d_velocity && d_params_bf16,
+  DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0 && sync_interval >= 1 && d_params && d_velocity && d_shadows,
               DBS_ERR_ARGUMENT, "run_iterations_local: bad arguments");
   for (int i = 0; i < n; i++)
     DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18),
                 DBS_ERR_ARGUMENT, "run_iterations_local: worker %d has a bad model", i);
+  const int prec = slot_precision(w[0]);
+  for (int i = 1; i < n; i++)
+    DBS_REQUIRE(slot_precision(w[i]) == prec, DBS_ERR_ARGUMENT, "run_iterations_local: workers mix operand precisions");
   cudaEvent_t* ev;
   int st = events(n + 1, &ev);
   if (st) return st;
@@ -454,15 +603,14 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
           if (st) return st;
         }
         const int64_t b = w[i].batch;
+        const char* x = static_cast<const char*>(w[i].x_shard) + t * b * slot_row_bytes(w[i]);
         if (w[i].model_kind == DBS_MODEL_MLP) {
           dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
-          const uint16_t* x = static_cast<const uint16_t*>(w[i].x_shard) + t * b * m->in;
-          st = mlp_fwd_bwd(m, d_params_bf16[i], d_params[i], x, w[i].y_shard + t * b, b, w[i].grad,
+          st = mlp_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, b, w[i].grad,
                            w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
         } else {
           dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
-          const uint8_t* x = static_cast<const uint8_t*>(w[i].x_shard) + t * b * resnet_row_bytes(m);
-          st = resnet_fwd_bwd(m, d_params_bf16[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,
+          st = resnet_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,
                               w[i].loss ? w[i].loss + t : nullptr, s);
         }
         if (st) return st;
@@ -481,8 +629,8 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
         // the worker's own momentum-SGD step on its replica
         const float* g = w[i].grad;
         const int64_t one = 1;
-        st = dbs_dev_aggregate_sgd_f32(&g, &one, 1, DBS_AGG_UNIFORM, P, lr, mom, d_params[i], d_velocity[i],
-                                       d_params_bf16[i], s);
+        st = dbs_dev_aggregate_sgd_f32_ex(&g, &one, 1, DBS_AGG_UNIFORM, P, lr, mom, d_params[i], d_velocity[i],
+                                          d_shadows[i], prec, s);
         if (st) return st;
         if (sync) DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
         return DBS_OK;
@@ -493,15 +641,19 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
     }
     if (sync) {
       for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
-      st = dbs_dev_average_replicas_f32(d_params, batches, n, mode, P, d_params_bf16, agg_stream);
+      st = dbs_dev_average_replicas_f32_ex(d_params, batches, n, mode, P, d_shadows, prec, agg_stream);
       if (st) return st;
       if (comm) {
         st = dbs_comm_average_params(comm, rank_batches, mode, agg_stream);
         if (st) return st;
+        if (prec == DBS_PREC_F32) {
+          st = dbs_dev_refresh_shadow(d_params[0], P, d_shadows[0], prec, agg_stream);
+          if (st) return st;
+        }
+        const size_t sh_bytes = prec == DBS_PREC_F32 ? sizeof(float) * 2 * P : sizeof(uint16_t) * P;
         for (int i = 1; i < n; i++) {
           DBS_CUDA_TRY(cudaMemcpyAsync(d_params[i], d_params[0], sizeof(float) * P, cudaMemcpyDeviceToDevice, agg));
-          DBS_CUDA_TRY(cudaMemcpyAsync(d_params_bf16[i], d_params_bf16[0], sizeof(uint16_t) * P,
-                                       cudaMemcpyDeviceToDevice, agg));
+          DBS_CUDA_TRY(cudaMemcpyAsync(d_shadows[i], d_shadows[0], sh_bytes, cudaMemcpyDeviceToDevice, agg));
         }
       }
       DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
@@ -517,8 +669,8 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
 }
 
 extern "C" int dbs_mlp_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
-                                      float lr, float mom, float* d_params, float* d_velocity, uint16_t* d_params_bf16,
+                                      float lr, float mom, float* d_params, float* d_velocity, void* d_params_shadow,
                                       int32_t skip_update, void* agg_stream) {
-  return dbs_run_iterations(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_bf16, skip_update,
+  return dbs_run_iterations(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_shadow, skip_update,
                             agg_stream, nullptr);
 }

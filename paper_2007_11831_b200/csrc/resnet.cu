@@ -22,6 +22,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -647,18 +648,543 @@ __global__ void head_bcast_kernel(const float* __restrict__ dfeat, int64_t B, in
   }
 }
 
-// CTAs of `kernel` one SM holds at once (registers / shared memory), cached per kernel
+// ======================= fp32-class (DBS_PREC_F32) kernels =======================
+// Storage in this mode: conv outputs y, input gradients and the incoming BN-backward
+// gradients plain fp32; every GEMM operand (post-BN activations, block outputs,
+// BN-backward outputs dY, the stem's im2col columns, pooled features, dlogits) in
+// the S32 format of the 3xTF32 GEMM (s32.cu): flat element e of a tensor whose
+// rows are multiples of 32 sits at 2 (e & ~31) + (e & 31) (hi), +32 (lo).
+__device__ __forceinline__ float rn_tf32(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
+}
+__device__ __forceinline__ int64_t s32_off(int64_t e) { return 2 * (e & ~int64_t(31)) + (e & 31); }
+// elements 8 i .. 8 i + 7
+__device__ __forceinline__ void ld8_f32(const float* p, int64_t i, float (&v)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[2 * i], b = reinterpret_cast<const float4*>(p)[2 * i + 1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8_f32(float* p, int64_t i, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[2 * i] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[2 * i + 1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void ld8_s32(const float* p, int64_t i, float (&v)[8]) {
+  const float* q = p + s32_off(8 * i);
+  const float4 h0 = *reinterpret_cast<const float4*>(q), h1 = *reinterpret_cast<const float4*>(q + 4);
+  const float4 l0 = *reinterpret_cast<const float4*>(q + 32), l1 = *reinterpret_cast<const float4*>(q + 36);
+  v[0] = h0.x + l0.x; v[1] = h0.y + l0.y; v[2] = h0.z + l0.z; v[3] = h0.w + l0.w;
+  v[4] = h1.x + l1.x; v[5] = h1.y + l1.y; v[6] = h1.z + l1.z; v[7] = h1.w + l1.w;
+}
+__device__ __forceinline__ void st8_s32(float* p, int64_t i, const float (&v)[8]) {
+  float* q = p + s32_off(8 * i);
+  float h[8], l[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    h[k] = rn_tf32(v[k]);
+    l[k] = rn_tf32(v[k] - h[k]);
+  }
+  *reinterpret_cast<float4*>(q) = make_float4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<float4*>(q + 4) = make_float4(h[4], h[5], h[6], h[7]);
+  *reinterpret_cast<float4*>(q + 32) = make_float4(l[0], l[1], l[2], l[3]);
+  *reinterpret_cast<float4*>(q + 36) = make_float4(l[4], l[5], l[6], l[7]);
+}
+__device__ __forceinline__ void st1_s32(float* p, int64_t e, float v) {
+  const float h = rn_tf32(v);
+  p[s32_off(e)] = h;
+  p[s32_off(e) + 32] = rn_tf32(v - h);
+}
+
+// ResNet-18 stem im2col, S32 columns [B*1024][32] (K = (r, s, c), 27 used)
+__global__ void im2col_stem_f32_kernel(const float* __restrict__ x_base, const int64_t* __restrict__ iter, int64_t B,
+                                       float* __restrict__ out) {
+  pdl_trigger_and_wait();
+  const int64_t t = iter ? *iter : 0;
+  const float* x = x_base + t * B * 3072;
+  const int64_t total = B * 1024;
+  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < total;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = pix >> 10;
+    const int h = (int)((pix >> 5) & 31), w = (int)(pix & 31);
+    const float* xs = x + n * 3072;
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) v[k] = 0.0f;
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+      for (int s = 0; s < 3; s++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const int hh = h + r - 1, ww = w + s - 1;
+          v[(r * 3 + s) * 3 + c] = (hh >= 0 && hh < 32 && ww >= 0 && ww < 32) ? xs[c * 1024 + hh * 32 + ww] : 0.0f;
+        }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      float u[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) u[k] = v[8 * q + k];
+      st8_s32(out, pix * 4 + q, u);
+    }
+  }
+}
+
+// ResNet-50 stem im2col (7x7 / 2 / 3), S32 columns [B*OS*OS][160]
+__global__ void __launch_bounds__(256) im2col_stem7_f32_kernel(const uint8_t* __restrict__ x_base,
+                                                               const int64_t* __restrict__ iter, int64_t B, int S,
+                                                               float* __restrict__ out) {
+  pdl_trigger_and_wait();
+  extern __shared__ float tile[];  // [3][7][S + 6]
+  __shared__ int koff[kStem7K];
+  constexpr int kChunks = kStem7K / 8;
+  const int SP = S + 6, OS = S / 2;
+  const int64_t t = iter ? *iter : 0;
+  const int64_t plane = (int64_t)S * S;
+  const int64_t n = blockIdx.x / OS;
+  const int oh = (int)(blockIdx.x - n * OS);
+  const uint8_t* xs = x_base + (t * B + n) * 3 * plane;
+  for (int k = threadIdx.x; k < kStem7K; k += blockDim.x) {
+    int o = -1;
+    if (k < 147) {
+      const int rs = k / 3, c = k - rs * 3;
+      const int r = rs / 7, sx = rs - r * 7;
+      o = (c * 7 + r) * SP + sx;
+    }
+    koff[k] = o;
+  }
+  for (int e = threadIdx.x; e < 3 * 7 * SP; e += blockDim.x) {
+    const int c = e / (7 * SP), rem = e - c * 7 * SP;
+    const int r = rem / SP, col = rem - r * SP;
+    const int hh = 2 * oh + r - 3, ww = col - 3;
+    float v = 0.0f;
+    if (hh >= 0 && hh < S && ww >= 0 && ww < S) v = ((float)xs[c * plane + (int64_t)hh * S + ww] - 128.0f) * 0.015625f;
+    tile[e] = v;
+  }
+  __syncthreads();
+  const int64_t row0 = (int64_t)blockIdx.x * OS;
+  for (int i = threadIdx.x; i < OS * kChunks; i += blockDim.x) {
+    const int px = i / kChunks, ch = i - (i / kChunks) * kChunks;
+    const float* base = tile + 2 * px;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int o = koff[ch * 8 + e];
+      v[e] = o >= 0 ? base[o] : 0.0f;
+    }
+    st8_s32(out, (row0 + px) * kChunks + ch, v);
+  }
+}
+
+// out (S32) = act(a*y + b [+ res (S32) | + a_d*yd + b_d]), y / yd fp32; also the
+// running statistics (momentum `rm`, unbiased variance, as torch's BatchNorm2d)
+__global__ void __launch_bounds__(256) bn_apply_f32_kernel(
+    const float* __restrict__ y, const double* __restrict__ acc, float* __restrict__ mean, float* __restrict__ invstd,
+    const float* __restrict__ gamma, const float* __restrict__ beta, const float* __restrict__ res,
+    const float* __restrict__ yd, const double* __restrict__ acc_d, float* __restrict__ mean_d,
+    float* __restrict__ invstd_d, const float* __restrict__ gamma_d, const float* __restrict__ beta_d, int relu, int C,
+    int64_t M, float* __restrict__ out, float* __restrict__ run, float* __restrict__ run_d, float rm) {
+  pdl_trigger_and_wait();
+  extern __shared__ float tab[];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float mu, is;
+    bn_finalise(acc, C, c, M, mu, is);
+    const float a = gamma[c] * is;
+    tab[c] = a;
+    tab[C + c] = beta[c] - mu * a;
+    if (blockIdx.x == 0) {
+      mean[c] = mu;
+      invstd[c] = is;
+      if (run) {
+        const double mud = acc[c] / (double)M, var = fmax(acc[C + c] / (double)M - mud * mud, 0.0);
+        run[c] = (1.0f - rm) * run[c] + rm * mu;
+        run[C + c] = (1.0f - rm) * run[C + c] + rm * (float)(var * (double)M / (double)(M > 1 ? M - 1 : 1));
+      }
+    }
+    if (yd) {
+      float mud, isd;
+      bn_finalise(acc_d, C, c, M, mud, isd);
+      const float ad = gamma_d[c] * isd;
+      tab[2 * C + c] = ad;
+      tab[3 * C + c] = beta_d[c] - mud * ad;
+      if (blockIdx.x == 0) {
+        mean_d[c] = mud;
+        invstd_d[c] = isd;
+        if (run_d) {
+          const double m2 = acc_d[c] / (double)M, var = fmax(acc_d[C + c] / (double)M - m2 * m2, 0.0);
+          run_d[c] = (1.0f - rm) * run_d[c] + rm * mud;
+          run_d[C + c] = (1.0f - rm) * run_d[C + c] + rm * (float)(var * (double)M / (double)(M > 1 ? M - 1 : 1));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int cv = C / 8;
+  const int64_t total = M * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;
+    float v[8], ka[8], kb[8];
+    ld8_f32(y, i, v);
+    coef8(tab, c0, ka);
+    coef8(tab + C, c0, kb);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = fmaf(ka[k], v[k], kb[k]);
+    if (res) {
+      float r[8];
+      ld8_s32(res, i, r);
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] += r[k];
+    }
+    if (yd) {
+      float r[8];
+      ld8_f32(yd, i, r);
+      coef8(tab + 2 * C, c0, ka);
+      coef8(tab + 3 * C, c0, kb);
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] += fmaf(ka[k], r[k], kb[k]);
+    }
+    if (relu) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] = fmaxf(v[k], 0.0f);
+    }
+    st8_s32(out, i, v);
+  }
+}
+
+// BN backward pass 1 (fp32 gradient / y, S32 ReLU mask): dbeta += sum g, dgamma += sum g yhat
+__global__ void __launch_bounds__(256) bn_bwd_reduce_f32_kernel(const float* __restrict__ gin,
+                                                                const float* __restrict__ mask,
+                                                                const float* __restrict__ y,
+                                                                const float* __restrict__ mean,
+                                                                const float* __restrict__ invstd, int C, int64_t M,
+                                                                float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  pdl_trigger_and_wait();
+  __shared__ float red_g[2048], red_b[2048];
+  const int cv = C / 8;
+  const int rows_per_pass = blockDim.x / cv;
+  const int lane_c = threadIdx.x % cv, lane_r = threadIdx.x / cv;
+  float sg[8], sb[8], mu[8], is[8];
+  const int c0 = lane_c * 8;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    sg[k] = 0.f;
+    sb[k] = 0.f;
+    mu[k] = mean[c0 + k];
+    is[k] = invstd[c0 + k];
+  }
+  if (lane_r < rows_per_pass) {
+    const int64_t step = (int64_t)gridDim.x * rows_per_pass;
+    for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + lane_r; r < M; r += step) {
+      const int64_t i = r * cv + lane_c;
+      float g[8], yv[8], mv[8];
+      ld8_f32(gin, i, g);
+      ld8_f32(y, i, yv);
+      if (mask) ld8_s32(mask, i, mv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const float gg = (!mask || mv[k] > 0.0f) ? g[k] : 0.0f;
+        sb[k] += gg;
+        sg[k] = fmaf(gg, (yv[k] - mu[k]) * is[k], sg[k]);
+      }
+    }
+  }
+  if (cv < 32) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      for (int o = cv; o < 32; o <<= 1) {
+        sg[k] += __shfl_xor_sync(0xffffffffu, sg[k], o);
+        sb[k] += __shfl_xor_sync(0xffffffffu, sb[k], o);
+      }
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const bool writer = (cv < 32) ? (lane < cv) : (lane_r < rows_per_pass);
+  const int slot = (cv < 32) ? warp : lane_r;
+  const int nslot = (cv < 32) ? nw : rows_per_pass;
+  if (writer) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      red_g[slot * C + c0 + k] = sg[k];
+      red_b[slot * C + c0 + k] = sb[k];
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < C; idx += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int r = 0; r < nslot; r++) {
+      a += red_g[r * C + idx];
+      b += red_b[r * C + idx];
+    }
+    atomicAdd(&dgamma[idx], a);
+    atomicAdd(&dbeta[idx], b);
+  }
+}
+
+// BN backward pass 2: dy (S32) = k1 g + k2 y + k3; g_out (fp32) = the masked gradient
+__global__ void __launch_bounds__(256) bn_bwd_apply_f32_kernel(const float* __restrict__ gin,
+                                                               const float* __restrict__ mask,
+                                                               const float* __restrict__ y, const float* __restrict__ mean,
+                                                               const float* __restrict__ invstd,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ dgamma,
+                                                               const float* __restrict__ dbeta, int C, int64_t M,
+                                                               float* __restrict__ dy, float* __restrict__ g_out) {
+  pdl_trigger_and_wait();
+  extern __shared__ float tab[];
+  const float invM = 1.0f / (float)M;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float is = invstd[c];
+    const float k1 = gamma[c] * is;
+    tab[c] = k1;
+    tab[C + c] = -k1 * is * dgamma[c] * invM;
+    tab[2 * C + c] = k1 * (mean[c] * is * dgamma[c] - dbeta[c]) * invM;
+  }
+  __syncthreads();
+  const int cv = C / 8;
+  const int64_t total = M * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i & (int64_t)(cv - 1)) * 8;
+    float g[8], yv[8], k1[8], k2[8], k3[8];
+    ld8_f32(gin, i, g);
+    ld8_f32(y, i, yv);
+    if (mask) {
+      float mv[8];
+      ld8_s32(mask, i, mv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) g[k] = mv[k] > 0.0f ? g[k] : 0.0f;
+    }
+    coef8(tab, c0, k1);
+    coef8(tab + C, c0, k2);
+    coef8(tab + 2 * C, c0, k3);
+    float d[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) d[k] = fmaf(k1[k], g[k], fmaf(k2[k], yv[k], k3[k]));
+    st8_s32(dy, i, d);
+    if (g_out) st8_f32(g_out, i, g);
+  }
+}
+
+// ResNet-18 head (f32 storage): a4 S32 [B][16][512] -> feat, logits, loss, dlogits / B,
+// dOut (fp32) = (dlogits W) / 16
+__global__ void __launch_bounds__(256) head_f32_kernel(const float* __restrict__ a4, const float* __restrict__ Wfc,
+                                                       const float* __restrict__ bfc, const int32_t* __restrict__ y_base,
+                                                       const int64_t* __restrict__ iter, int64_t B, int classes,
+                                                       float* __restrict__ feat, float* __restrict__ dlog,
+                                                       float* __restrict__ loss_per, float* __restrict__ dout) {
+  pdl_trigger_and_wait();
+  __shared__ float f[512];
+  __shared__ float logit[16];
+  const int64_t n = blockIdx.x;
+  const int64_t t = iter ? *iter : 0;
+  const int32_t label = y_base[t * B + n];
+  for (int c = threadIdx.x; c < 512; c += blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < 16; p++) {
+      const int64_t o = s32_off((n * 16 + p) * 512 + c);
+      s += a4[o] + a4[o + 32];
+    }
+    f[c] = s * (1.0f / 16.0f);
+    feat[n * 512 + c] = f[c];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < classes; k += blockDim.x >> 5) {
+    float s = 0.f;
+    for (int c = lane; c < 512; c += 32) s = fmaf(f[c], Wfc[k * 512 + c], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) logit[k] = s + bfc[k];
+  }
+  __syncthreads();
+  __shared__ float dl[16];
+  if (threadIdx.x == 0) {
+    float mx = -INFINITY;
+    for (int k = 0; k < classes; k++) mx = fmaxf(mx, logit[k]);
+    float se = 0.f;
+    for (int k = 0; k < classes; k++) se += expf(logit[k] - mx);
+    loss_per[n] = (mx + logf(se)) - logit[label];
+    const float inv = 1.0f / se, invB = 1.0f / (float)B;
+    for (int k = 0; k < classes; k++) {
+      const float g = (expf(logit[k] - mx) * inv - (k == label ? 1.f : 0.f)) * invB;
+      dl[k] = g;
+      dlog[n * 16 + k] = g;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 512; c += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < classes; k++) s = fmaf(dl[k], Wfc[k * 512 + c], s);
+    const float h = s * (1.0f / 16.0f);
+    for (int p = 0; p < 16; p++) dout[(n * 16 + p) * 512 + c] = h;
+  }
+}
+
+// 3x3 / 2 / 1 max-pool on S32 (first maximal tap, row-major scan) and its backward (fp32)
+__global__ void maxpool_fwd_f32_kernel(const float* __restrict__ in, int64_t B, int H, int W, int C, int OH, int OW,
+                                       float* __restrict__ out, uint8_t* __restrict__ idx) {
+  pdl_trigger_and_wait();
+  const int cv = C / 8;
+  const int64_t total = B * OH * OW * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    const int64_t pix = i / cv;
+    const int ow = (int)(pix % OW);
+    const int oh = (int)((pix / OW) % OH);
+    const int64_t n = pix / ((int64_t)OW * OH);
+    float best[8];
+    uint8_t arg[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      best[k] = -INFINITY;
+      arg[k] = 0;
+    }
+    for (int r = 0; r < 3; r++) {
+      const int h = 2 * oh + r - 1;
+      if (h < 0 || h >= H) continue;
+      for (int s = 0; s < 3; s++) {
+        const int w = 2 * ow + s - 1;
+        if (w < 0 || w >= W) continue;
+        float v[8];
+        ld8_s32(in, ((n * H + h) * W + w) * cv + c8, v);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          if (v[k] > best[k]) {
+            best[k] = v[k];
+            arg[k] = (uint8_t)(r * 3 + s);
+          }
+        }
+      }
+    }
+    st8_s32(out, i, best);
+    uint2 a;
+    a.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | ((uint32_t)arg[3] << 24);
+    a.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | ((uint32_t)arg[7] << 24);
+    reinterpret_cast<uint2*>(idx)[i] = a;
+  }
+}
+
+__global__ void maxpool_bwd_f32_kernel(const float* __restrict__ gout, const uint8_t* __restrict__ idx, int64_t B,
+                                       int H, int W, int C, int OH, int OW, float* __restrict__ gin) {
+  pdl_trigger_and_wait();
+  const int cv = C / 8;
+  const int64_t total = B * H * W * cv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    const int64_t pix = i / cv;
+    const int w = (int)(pix % W);
+    const int h = (int)((pix / W) % H);
+    const int64_t n = pix / ((int64_t)W * H);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc[k] = 0.f;
+    for (int oh = (h > 0 ? h : 1) / 2; oh <= (h + 1) / 2 && oh < OH; oh++) {
+      const int r = h - (2 * oh - 1);
+      if (r < 0 || r > 2) continue;
+      for (int ow = (w > 0 ? w : 1) / 2; ow <= (w + 1) / 2 && ow < OW; ow++) {
+        const int s = w - (2 * ow - 1);
+        if (s < 0 || s > 2) continue;
+        const int64_t o = ((n * OH + oh) * OW + ow) * cv + c8;
+        const uint2 a = reinterpret_cast<const uint2*>(idx)[o];
+        float g[8];
+        ld8_f32(gout, o, g);
+        const uint32_t av[2] = {a.x, a.y};
+        const uint32_t tap = (uint32_t)(r * 3 + s);
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+          if (((av[k >> 2] >> ((k & 3) * 8)) & 0xFFu) == tap) acc[k] += g[k];
+      }
+    }
+    st8_f32(gin, i, acc);
+  }
+}
+
+// global average pool S32 [B][HW][C] -> S32 [B][C]
+__global__ void avgpool_f32_kernel(const float* __restrict__ x, int64_t B, int HW, int C, float* __restrict__ feat) {
+  pdl_trigger_and_wait();
+  const int cv = C / 8;
+  const int64_t total = B * cv;
+  const float inv = 1.0f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / cv;
+    const int c8 = (int)(i - n * cv);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc[k] = 0.f;
+    for (int p = 0; p < HW; p++) {
+      float v[8];
+      ld8_s32(x, (n * HW + p) * cv + c8, v);
+#pragma unroll
+      for (int k = 0; k < 8; k++) acc[k] += v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc[k] *= inv;
+    st8_s32(feat, i, acc);
+  }
+}
+
+// softmax cross-entropy (f32 storage): dlog_b S32 [B][ld32], pad columns zero
+__global__ void __launch_bounds__(256) ce_f32_kernel(const float* __restrict__ logits, int ld,
+                                                     const int32_t* __restrict__ y_base, const int64_t* __restrict__ iter,
+                                                     int64_t B, int classes, float* __restrict__ dlog_f,
+                                                     float* __restrict__ dlog_b, int ld32, float* __restrict__ loss_per) {
+  pdl_trigger_and_wait();
+  __shared__ float sh[32];
+  const int64_t n = blockIdx.x;
+  const int64_t t = iter ? *iter : 0;
+  const int32_t label = y_base[t * B + n];
+  const float* z = logits + n * ld;
+  float mx = -INFINITY;
+  for (int k = threadIdx.x; k < classes; k += blockDim.x) mx = fmaxf(mx, z[k]);
+  mx = block_reduce(mx, sh, true);
+  float se = 0.f;
+  for (int k = threadIdx.x; k < classes; k += blockDim.x) se += expf(z[k] - mx);
+  se = block_reduce(se, sh, false);
+  const float inv = 1.0f / se, invB = 1.0f / (float)B;
+  for (int k = threadIdx.x; k < ld32; k += blockDim.x) {
+    float g = 0.f;
+    if (k < classes) g = (expf(z[k] - mx) * inv - (k == label ? 1.f : 0.f)) * invB;
+    if (k < ld) dlog_f[n * ld + k] = g;
+    st1_s32(dlog_b, n * ld32 + k, g);
+  }
+  if (threadIdx.x == 0) loss_per[n] = (mx + logf(se)) - z[label];
+}
+
+// gradient of the average pool: dOut[n][p][c] = dfeat[n][c] / HW (fp32)
+__global__ void head_bcast_f32_kernel(const float* __restrict__ dfeat, int64_t B, int HW, int C,
+                                      float* __restrict__ dout) {
+  pdl_trigger_and_wait();
+  const int cv = C / 8;
+  const int64_t total = B * HW * cv;
+  const float inv = 1.0f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    const int64_t n = i / ((int64_t)cv * HW);
+    float v[8];
+    ld8_f32(dfeat + n * C, c8, v);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] *= inv;
+    st8_f32(dout, i, v);
+  }
+}
+
+// CTAs of `kernel` one SM holds at once (registers / shared memory), cached per
+// (kernel, block size, dynamic shared memory)
 template <typename K>
 int resident_per_sm(K kernel, int threads, size_t smem) {
-  static int cached = 0;  // one instantiation per kernel type; the BN kernels below are distinct types
-  static size_t cached_smem = ~size_t(0);
-  if (cached == 0 || cached_smem != smem) {
-    int v = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, smem) != cudaSuccess || v < 1) v = 1;
-    cached = v;
-    cached_smem = smem;
-  }
-  return cached;
+  struct Entry {
+    const void* fn;
+    int threads;
+    size_t smem;
+    int v;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  const void* fn = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const Entry& e : cache)
+    if (e.fn == fn && e.threads == threads && e.smem == smem) return e.v;
+  int v = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, smem) != cudaSuccess || v < 1) v = 1;
+  cache.push_back(Entry{fn, threads, smem, v});
+  return v;
 }
 
 // grid-stride kernels: at most ONE wave of resident CTAs on the SMs this launch can use
@@ -681,20 +1207,24 @@ struct dbs_resnet {
   int classes = 10;
   int arch = 18;                           // 18 (CIFAR stem) or 50 (ImageNet stem)
   int image = 32;                          // input side (32 for ResNet-18; 224 for config 5)
+  int prec = DBS_PREC_BF16;                // DBS_PREC_F32: 3xTF32 GEMMs on S32 operands, fp32 storage
   int64_t row_bytes = 3072 * 4;            // one input sample in the repacked shard
   int stem_k = kStemK;                     // padded K of the stem's explicit im2col
   int feat_c = 512, feat_hw = 16;          // last feature map: channels, pixels
   int cpad = 16;                           // logits / dlogits row pitch (ResNet-50 head)
+  int cpad32 = 32;                         // S32 dlogits row pitch (f32 mode)
   std::vector<char> need_a;                // per conv: post-BN(+ReLU) output is stored
+  // Buffers are typed by precision: "operand" tensors (a, blk_out, stem_cols, mp_out,
+  // feat_b, dlog_b, BN-backward outputs) bf16 or S32; y and input gradients bf16 or fp32.
   // ResNet-50 extras
-  uint16_t* mp_out = nullptr;              // max-pool output [B][S/4][S/4][64]
+  void* mp_out = nullptr;                  // max-pool output [B][S/4][S/4][64]
   uint8_t* mp_idx = nullptr;               // its arg-max taps
-  uint16_t* feat_b = nullptr;              // pooled features bf16 [B][2048]
+  void* feat_b = nullptr;                  // pooled features [B][2048]
   float* logits = nullptr;                 // [B][cpad]
   float* dlog_f = nullptr;                 // [B][cpad]
-  uint16_t* dlog_b = nullptr;              // [B][cpad]
+  void* dlog_b = nullptr;                  // [B][cpad] bf16 | [B][cpad32] S32
   float* dfeat = nullptr;                  // [B][2048]
-  uint16_t* g4 = nullptr;
+  void* g4 = nullptr;
   std::vector<Conv> convs;
   std::vector<Block> blocks;
   int stem = 0;
@@ -703,17 +1233,22 @@ struct dbs_resnet {
   std::vector<int64_t> t_off, t_len;
   std::vector<int32_t> t_kind;
   // activations
-  uint16_t* stem_cols = nullptr;           // [B*1024][32]
-  std::vector<uint16_t*> y, a;             // per conv: pre-BN output, post-BN(+ReLU) output
-  std::vector<uint16_t*> blk_out;          // per block output (post residual ReLU)
+  void* stem_cols = nullptr;               // [B*OH*OW][stem_k]
+  std::vector<void*> y, a;                 // per conv: pre-BN output, post-BN(+ReLU) output
+  std::vector<void*> blk_out;              // per block output (post residual ReLU)
   std::vector<float*> mean, invstd;        // per conv
   double* stats_acc = nullptr;             // per conv: [cout] fp64 sums + [cout] sums of squares (BN statistics)
   std::vector<int64_t> stats_off;          // offset of each conv's accumulators in stats_acc
   int64_t stats_len = 0;
-  uint16_t* g0 = nullptr;                  // gradient ping-pong buffers (largest activation)
-  uint16_t* g1 = nullptr;
-  uint16_t* g2 = nullptr;
-  uint16_t* g3 = nullptr;
+  // BN running statistics (f32 mode): per conv [cout] mean + [cout] unbiased variance,
+  // momentum bn_momentum (torch BatchNorm2d semantics), per worker
+  float* run_stats = nullptr;
+  std::vector<int64_t> run_off;
+  float bn_momentum = 0.1f;
+  void* g0 = nullptr;                      // gradient ping-pong buffers (largest activation)
+  void* g1 = nullptr;
+  void* g2 = nullptr;
+  void* g3 = nullptr;
   float* feat = nullptr;                   // [B][512]
   float* dlog = nullptr;                   // [B][16]
   float* loss_per = nullptr;               // [B]
@@ -722,7 +1257,9 @@ struct dbs_resnet {
 
 namespace {
 
-int64_t pad8(int64_t x) { return (x + 7) & ~int64_t(7); }
+// every parameter tensor starts on a 32-element boundary: the flat S32 operand
+// shadow of the fp32-class path is then the same layout (rows are multiples of 32)
+int64_t pad8(int64_t x) { return (x + 31) & ~int64_t(31); }
 
 void build_layers(dbs_resnet* m) {
   int64_t off = 0;
@@ -842,17 +1379,20 @@ int alloc_all(dbs_resnet* m) {
   auto A = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, bytes);
   };
+  const bool f32 = m->prec == DBS_PREC_F32;
+  const size_t es_op = f32 ? 8 : 2;  // operand tensors: S32 | bf16
+  const size_t es_y = f32 ? 4 : 2;   // conv outputs / input gradients: fp32 | bf16
   {
     const Conv& st = m->convs[m->stem];
-    A((void**)&m->stem_cols, (size_t)B * st.OH * st.OW * m->stem_k * 2);
+    A((void**)&m->stem_cols, (size_t)B * st.OH * st.OW * m->stem_k * es_op);
   }
   int64_t max_act = 0;
   for (size_t ci = 0; ci < m->convs.size(); ci++) {
     const Conv& c = m->convs[ci];
     const int64_t n = B * c.OH * c.OW * c.cout;
-    uint16_t *y, *a = nullptr;
-    A((void**)&y, n * 2);
-    if (m->need_a[ci]) A((void**)&a, n * 2);
+    void *y, *a = nullptr;
+    A((void**)&y, n * es_y);
+    if (m->need_a[ci]) A((void**)&a, n * es_op);
     m->y.push_back(y);
     m->a.push_back(a);
     float *mu, *is;
@@ -867,9 +1407,25 @@ int alloc_all(dbs_resnet* m) {
   for (size_t i = 0; i < m->blocks.size(); i++) {
     const Block& bk = m->blocks[i];
     const Conv& c = m->convs[bk.c3 >= 0 ? bk.c3 : bk.c2];  // the block's last conv shapes its output
-    uint16_t* o;
-    A((void**)&o, (size_t)B * c.OH * c.OW * c.cout * 2);
+    void* o;
+    A((void**)&o, (size_t)B * c.OH * c.OW * c.cout * es_op);
     m->blk_out.push_back(o);
+  }
+  m->run_off.clear();
+  int64_t run_len = 0;
+  for (auto& c : m->convs) {
+    m->run_off.push_back(run_len);
+    run_len += 2 * (int64_t)c.cout;
+  }
+  A((void**)&m->run_stats, (size_t)run_len * sizeof(float));
+  if (e == cudaSuccess) {
+    std::vector<float> init((size_t)run_len);
+    for (size_t ci = 0; ci < m->convs.size(); ci++)
+      for (int k = 0; k < m->convs[ci].cout; k++) {
+        init[m->run_off[ci] + k] = 0.0f;                      // running mean
+        init[m->run_off[ci] + m->convs[ci].cout + k] = 1.0f;  // running variance
+      }
+    e = cudaMemcpy(m->run_stats, init.data(), init.size() * sizeof(float), cudaMemcpyHostToDevice);
   }
   m->stats_off.clear();
   m->stats_len = 0;
@@ -878,21 +1434,22 @@ int alloc_all(dbs_resnet* m) {
     m->stats_len += 2 * (int64_t)c.cout;
   }
   A((void**)&m->stats_acc, (size_t)m->stats_len * sizeof(double));
-  A((void**)&m->g0, max_act * 2);
-  A((void**)&m->g1, max_act * 2);
-  A((void**)&m->g2, max_act * 2);
-  A((void**)&m->g3, max_act * 2);
+  // gradient buffers hold either kind (f32 mode: fp32 input gradients or S32 BN-backward outputs)
+  A((void**)&m->g0, max_act * es_op);
+  A((void**)&m->g1, max_act * es_op);
+  A((void**)&m->g2, max_act * es_op);
+  A((void**)&m->g3, max_act * es_op);
   if (m->arch == 50) {
     const Conv& st = m->convs[m->stem];
     const int P = st.OH / 2;
     const int64_t mp = B * P * P * 64;
-    A((void**)&m->g4, max_act * 2);
-    A((void**)&m->mp_out, mp * 2);
+    A((void**)&m->g4, max_act * es_op);
+    A((void**)&m->mp_out, mp * es_op);
     A((void**)&m->mp_idx, mp);
-    A((void**)&m->feat_b, (size_t)B * m->feat_c * 2);
+    A((void**)&m->feat_b, (size_t)B * m->feat_c * es_op);
     A((void**)&m->logits, (size_t)B * m->cpad * 4);
     A((void**)&m->dlog_f, (size_t)B * m->cpad * 4);
-    A((void**)&m->dlog_b, (size_t)B * m->cpad * 2);
+    A((void**)&m->dlog_b, f32 ? (size_t)B * m->cpad32 * 8 : (size_t)B * m->cpad * 2);
     A((void**)&m->dfeat, (size_t)B * m->feat_c * 4);
   }
   A((void**)&m->feat, (size_t)B * 512 * 4);
@@ -920,18 +1477,25 @@ bool halo_ok(const Conv& c) {
   return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 && halo_fits(c.OH, c.OW);
 }
 
-int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64_t B, cudaStream_t s) {
+// the operand copy of the parameter at flat offset `off` (bf16 or S32 shadow)
+const void* wptr(const dbs_resnet* m, const void* shadow, int64_t off) {
+  return static_cast<const char*>(shadow) + off * (m->prec == DBS_PREC_F32 ? 8 : 2);
+}
+
+int conv_fwd(dbs_resnet* m, int ci, const void* x, const void* shadow, int64_t B, cudaStream_t s) {
   const Conv& c = m->convs[ci];
+  const bool f32 = m->prec == DBS_PREC_F32;
   const int64_t M = B * c.OH * c.OW;
   ConvCall call{};
+  call.tf = f32;
   call.M = M;
   call.N = c.cout;
-  call.epi = DBS_EPI_BF16;
+  call.epi = f32 ? DBS_EPI_F32 : DBS_EPI_BF16;
   call.d = m->y[ci];
   call.ldd = c.cout;
   call.sum_part = m->stats_acc + m->stats_off[ci];
   call.sq_part = m->stats_acc + m->stats_off[ci] + c.cout;
-  call.b = wb + c.w_off;
+  call.b = wptr(m, shadow, c.w_off);
   call.b_mode = 0;
   if (c.cin == 3) {  // stem: explicit im2col columns [M][stem_k]
     call.K = m->stem_k;
@@ -950,50 +1514,84 @@ int conv_fwd(dbs_resnet* m, int ci, const uint16_t* x, const uint16_t* wb, int64
     call.a_mode = 2;
     call.a = x;
     call.ta = nhwc(B, c.H, c.W, c.cin);
-    call.ga = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
+    call.ga = ConvGeom{c.k, c.k, c.cin / (f32 ? 32 : 64), c.stride, c.pad, c.OH, c.OW, c.cin};
     call.ldb = call.K;
-    call.halo = halo_ok(c);
+    call.halo = !f32 && halo_ok(c);
   }
   int st = conv_gemm(call, s);
   if (st) return st;
   return DBS_OK;  // batch statistics are finalised by the BN apply kernel (bn_apply_kernel)
 }
 
-int bn_apply(dbs_resnet* m, int ci, const float* pf, const uint16_t* res, int ds, int relu, int64_t B,
-             uint16_t* out, cudaStream_t s) {
+int bn_apply(dbs_resnet* m, int ci, const float* pf, const void* res, int ds, int relu, int64_t B,
+             void* out, cudaStream_t s) {
   const Conv& c = m->convs[ci];
   const int64_t M = B * c.OH * c.OW;
   const int64_t total = M * (c.cout / 8);
   const Conv* d = ds >= 0 ? &m->convs[ds] : nullptr;
+  const size_t smem = (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float);
+  if (m->prec == DBS_PREC_F32) {
+    DBS_CUDA_TRY(launch_pdl(
+        bn_apply_f32_kernel, dim3(grid_one_wave(bn_apply_f32_kernel, total, 256, smem)), dim3(256), smem, s,
+        static_cast<const float*>(m->y[ci]), m->stats_acc + m->stats_off[ci], m->mean[ci], m->invstd[ci],
+        pf + c.g_off, pf + c.b_off, static_cast<const float*>(res), d ? static_cast<const float*>(m->y[ds]) : nullptr,
+        d ? m->stats_acc + m->stats_off[ds] : nullptr, d ? m->mean[ds] : nullptr, d ? m->invstd[ds] : nullptr,
+        d ? pf + d->g_off : nullptr, d ? pf + d->b_off : nullptr, relu, c.cout, M, static_cast<float*>(out),
+        m->run_stats + m->run_off[ci], d ? m->run_stats + m->run_off[ds] : nullptr, m->bn_momentum));
+    DBS_LAUNCH_CHECK();
+    return DBS_OK;
+  }
   DBS_CUDA_TRY(launch_pdl(
-      bn_apply_kernel, dim3(grid_one_wave(bn_apply_kernel, total, 256, (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float))),
-      dim3(256), (size_t)(ds >= 0 ? 4 : 2) * c.cout * sizeof(float), s,
-      m->y[ci], m->stats_acc + m->stats_off[ci], m->mean[ci], m->invstd[ci], pf + c.g_off, pf + c.b_off, res,
-      d ? m->y[ds] : nullptr, d ? m->stats_acc + m->stats_off[ds] : nullptr, d ? m->mean[ds] : nullptr,
-      d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
-      d ? pf + d->b_off : nullptr, relu, c.cout, M, out));
+      bn_apply_kernel, dim3(grid_one_wave(bn_apply_kernel, total, 256, smem)), dim3(256), smem, s,
+      static_cast<const uint16_t*>(m->y[ci]), m->stats_acc + m->stats_off[ci], m->mean[ci], m->invstd[ci],
+      pf + c.g_off, pf + c.b_off, static_cast<const uint16_t*>(res),
+      d ? static_cast<const uint16_t*>(m->y[ds]) : nullptr, d ? m->stats_acc + m->stats_off[ds] : nullptr,
+      d ? m->mean[ds] : nullptr, d ? m->invstd[ds] : nullptr, d ? pf + d->g_off : nullptr,
+      d ? pf + d->b_off : nullptr, relu, c.cout, M, static_cast<uint16_t*>(out)));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
 
 // BN backward for conv ci: gin (masked by `mask` > 0 when given) -> dy; gamma/beta grads into grad
-int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const uint16_t* gin, const uint16_t* mask, int64_t B,
-           uint16_t* dy, uint16_t* g_out, cudaStream_t s) {
+// (f32 mode: gin / g_out fp32, mask / dy S32)
+int bn_bwd(dbs_resnet* m, int ci, const float* pf, float* grad, const void* gin, const void* mask, int64_t B,
+           void* dy, void* g_out, cudaStream_t s) {
   const Conv& c = m->convs[ci];
   const int64_t M = B * c.OH * c.OW;
   const int cv = c.cout / 8;
   const int rows_per_pass = 256 / cv;
+  const int64_t total = M * cv;
+  const size_t smem = (size_t)3 * c.cout * sizeof(float);
+  if (m->prec == DBS_PREC_F32) {
+    int blocks = (int)((M + rows_per_pass - 1) / rows_per_pass);
+    const int cap = current_sm_count() * resident_per_sm(bn_bwd_reduce_f32_kernel, 256, 0);
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_f32_kernel, dim3(blocks), dim3(256), 0, s, static_cast<const float*>(gin),
+                            static_cast<const float*>(mask), static_cast<const float*>(m->y[ci]), m->mean[ci],
+                            m->invstd[ci], c.cout, M, grad + c.g_off, grad + c.b_off));
+    DBS_LAUNCH_CHECK();
+    DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_f32_kernel, dim3(grid_one_wave(bn_bwd_apply_f32_kernel, total, 256, smem)),
+                            dim3(256), smem, s, static_cast<const float*>(gin), static_cast<const float*>(mask),
+                            static_cast<const float*>(m->y[ci]), m->mean[ci], m->invstd[ci], pf + c.g_off,
+                            grad + c.g_off, grad + c.b_off, c.cout, M, static_cast<float*>(dy),
+                            static_cast<float*>(g_out)));
+    DBS_LAUNCH_CHECK();
+    return DBS_OK;
+  }
   int blocks = (int)((M + rows_per_pass * 4 - 1) / (rows_per_pass * 4));  // ~4 rows per thread (one trip)
   const int cap = current_sm_count() * resident_per_sm(bn_bwd_reduce_kernel<8>, 256, 0);
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_kernel<8>, dim3(blocks), dim3(256), 0, s, gin, mask, m->y[ci], m->mean[ci],
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_kernel<8>, dim3(blocks), dim3(256), 0, s, static_cast<const uint16_t*>(gin),
+                          static_cast<const uint16_t*>(mask), static_cast<const uint16_t*>(m->y[ci]), m->mean[ci],
                           m->invstd[ci], c.cout, M, grad + c.g_off, grad + c.b_off));
   DBS_LAUNCH_CHECK();
-  const int64_t total = M * cv;
-  DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_kernel, dim3(grid_one_wave(bn_bwd_apply_kernel, total, 256, (size_t)3 * c.cout * sizeof(float))), dim3(256),
-                          (size_t)3 * c.cout * sizeof(float), s, gin, mask, m->y[ci], m->mean[ci], m->invstd[ci],
-                          pf + c.g_off, grad + c.g_off, grad + c.b_off, c.cout, M, dy, g_out));
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_kernel, dim3(grid_one_wave(bn_bwd_apply_kernel, total, 256, smem)), dim3(256),
+                          smem, s, static_cast<const uint16_t*>(gin), static_cast<const uint16_t*>(mask),
+                          static_cast<const uint16_t*>(m->y[ci]), m->mean[ci], m->invstd[ci], pf + c.g_off,
+                          grad + c.g_off, grad + c.b_off, c.cout, M, static_cast<uint16_t*>(dy),
+                          static_cast<uint16_t*>(g_out)));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -1006,11 +1604,14 @@ bool merge_parity_enabled() {
   return on;
 }
 
-// dX (+)= dgrad of conv c from dy; accumulate selects the bf16 accumulate epilogue.
-int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t B, uint16_t* dx, int accumulate,
-                  cudaStream_t s) {
+// dX (+)= dgrad of conv c from dy; accumulate selects the accumulate epilogue.
+// tf: S32 dy / w, fp32 dx (F32 / F32_ACCUM); else bf16 throughout.
+int conv_dgrad_ex(const Conv& c, const void* dy, const void* w, int64_t B, void* dx, int accumulate,
+                  cudaStream_t s, bool tf = false) {
   // the GEMM reads the filter flipped and transposed in place (B mode 3)
+  const int cb = tf ? 32 : 64;  // channels per logical k-block
   ConvCall call{};
+  call.tf = tf;
   call.N = c.cin;
   call.a_mode = 2;
   call.a = dy;
@@ -1018,7 +1619,7 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
   call.b_mode = 3;
   call.b = w;
   call.tb = ConvTensor{c.cout, 1, c.k * c.k, c.cin};  // {N=Cout, -, W=R*S, C=Cin} filter view
-  call.epi = accumulate ? DBS_EPI_BF16_ACCUM : DBS_EPI_BF16;
+  call.epi = tf ? (accumulate ? DBS_EPI_F32_ACCUM : DBS_EPI_F32) : (accumulate ? DBS_EPI_BF16_ACCUM : DBS_EPI_BF16);
   call.d = dx;
   call.ldd = c.cin;
   if (c.k == 1 && c.stride == 1) {
@@ -1036,8 +1637,8 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
     // stride 1: the flipped filter over dY, same padding
     call.M = B * c.H * c.W;
     call.K = (int64_t)c.k * c.k * c.cout;
-    call.ga = ConvGeom{c.k, c.k, c.cout / 64, 1, c.k / 2, c.H, c.W, c.cout};
-    call.halo = halo_ok(c);
+    call.ga = ConvGeom{c.k, c.k, c.cout / cb, 1, c.k / 2, c.H, c.W, c.cout};
+    call.halo = !tf && halo_ok(c);
     return conv_gemm(call, s);
   }
   // stride 2: one GEMM per output parity class (a, b).  dX(2i+a, 2j+b) gathers
@@ -1057,10 +1658,10 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
       if (n == 0) empty_class = true;
     }
   if (empty_class && !accumulate)
-    DBS_CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(uint16_t) * (size_t)(B * c.H * c.W * c.cin), s));
-  if (c.cin <= 256 && merge_parity_enabled()) {
-    // all non-empty parity classes in ONE launch (one N tile: the 64..256-wide N tile
-    // covers Cin), each class a full GEMM over the OH x OW grid with its own taps
+    DBS_CUDA_TRY(cudaMemsetAsync(dx, 0, (tf ? sizeof(float) : sizeof(uint16_t)) * (size_t)(B * c.H * c.W * c.cin), s));
+  // all non-empty parity classes in ONE launch when one N tile covers Cin (bf16 tiles
+  // up to 256 wide, S32 tiles up to 128), each class a full GEMM over the OH x OW grid
+  if (c.cin <= (tf ? 128 : 256) && merge_parity_enabled()) {
     ConvCall mc = call;
     mc.M = B * c.OH * c.OW;
     mc.nclass = 0;
@@ -1083,7 +1684,7 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
         if (t.n > kmax) kmax = t.n;
       }
     mc.K = (int64_t)kmax * c.cout;
-    mc.ga = ConvGeom{1, kmax, c.cout / 64, 1, 0, c.OH, c.OW, c.cout};
+    mc.ga = ConvGeom{1, kmax, c.cout / cb, 1, 0, c.OH, c.OW, c.cout};
     mc.taps = mc.cls_taps[0];
     mc.bn_override = c.cin <= 64 ? 64 : (c.cin <= 128 ? 128 : 256);
     return conv_gemm(mc, s);
@@ -1103,7 +1704,7 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
       ConvCall cc = call;
       cc.M = B * c.OH * c.OW;
       cc.K = (int64_t)t.n * c.cout;
-      cc.ga = ConvGeom{1, t.n, c.cout / 64, 1, 0, c.OH, c.OW, c.cout};
+      cc.ga = ConvGeom{1, t.n, c.cout / cb, 1, 0, c.OH, c.OW, c.cout};
       cc.taps = t;
       cc.omap = OutMap{1, c.H, c.W, a, b, c.OH, c.OW};
       int st = conv_gemm(cc, s);
@@ -1112,10 +1713,10 @@ int conv_dgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* w, int64_t 
   return DBS_OK;
 }
 
-int conv_dgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* wb, int64_t B, uint16_t* dx, int accumulate,
+int conv_dgrad(dbs_resnet* m, int ci, const void* dy, const void* shadow, int64_t B, void* dx, int accumulate,
                cudaStream_t s) {
   const Conv& c = m->convs[ci];
-  return conv_dgrad_ex(c, dy, wb + c.w_off, B, dx, accumulate, s);
+  return conv_dgrad_ex(c, dy, wptr(m, shadow, c.w_off), B, dx, accumulate, s, m->prec == DBS_PREC_F32);
 }
 
 bool wgrad_trans_enabled() {
@@ -1127,10 +1728,14 @@ bool wgrad_trans_enabled() {
 }
 
 // dW of conv c (fp32 atomics into dw) from dy and the conv input x (stem: im2col columns)
-int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t B, float* dw, cudaStream_t s) {
+// tf: S32 dy / x; else bf16.  `stem_k` is the stem's padded K.
+int conv_wgrad_ex(const Conv& c, const void* dy, const void* x, int64_t B, float* dw, cudaStream_t s,
+                  bool tf = false, int stem_k = 0) {
   const int64_t pixels = B * c.OH * c.OW;
+  const int kb = tf ? 32 : 64;  // pixels per logical k-block
   ConvCall call{};
-  if (c.cout == 64 && c.cin % 64 == 0 && (c.k == 1 ? c.stride == 1 : true) && ((uintptr_t)dw & 15) == 0 &&
+  call.tf = tf;
+  if (!tf && c.cout == 64 && c.cin % 64 == 0 && (c.k == 1 ? c.stride == 1 : true) && ((uintptr_t)dw & 15) == 0 &&
       wgrad_trans_enabled()) {
     // 64 output channels: dW^T = X^T dY puts the (r, s, c) reduction rows on the
     // 128-row MMA M side (all rows live) instead of the 64 output channels (half
@@ -1172,13 +1777,12 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
   call.d = dw;
   int bn;
   if (c.cin == 3) {  // stem: columns [pixels][stem_k]
-    const int sk = (int)(c.w_len / c.cout);
-    call.N = sk;
+    call.N = stem_k;
     call.K = pixels;
     call.b_mode = 1;
     call.b = x;
-    call.ldb = sk;
-    call.ldd = sk;
+    call.ldb = stem_k;
+    call.ldd = stem_k;
     bn = 64;
   } else if (c.k == 1 && c.stride == 1) {  // 1x1: dW = dY^T X over the [pixels][Cin] view
     call.N = c.cin;
@@ -1188,6 +1792,7 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
     call.ldb = c.cin;
     call.ldd = c.cin;
     bn = c.cin >= 256 ? 256 : c.cin;
+    if (tf && bn > 128) bn = 128;
     call.bn_override = bn;
   } else {
     // N = (r, s, c): the tile must divide Cin so it never straddles two taps
@@ -1197,15 +1802,16 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
     call.b_mode = 2;
     call.b = x;
     call.tb = nhwc(B, c.H, c.W, c.cin);
-    call.gb = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
+    call.gb = ConvGeom{c.k, c.k, c.cin / kb, c.stride, c.pad, c.OH, c.OW, c.cin};
     call.ldd = call.N;
     bn = c.cin % 256 == 0 ? 256 : (c.cin % 128 == 0 ? 128 : 64);
+    if (tf && bn > 128) bn = 128;
     call.bn_override = bn;
   }
   // split the long pixel reduction so the persistent GEMM's one round of
   // tiles x splits just fits the SMs this launch can use
   const int64_t tiles = ((call.M + 127) / 128) * ((call.N + bn - 1) / bn);
-  const int64_t kblocks = (call.K + 63) / 64;
+  const int64_t kblocks = (call.K + kb - 1) / kb;
   int64_t splits = current_sm_count() / tiles;
   if (splits > kblocks) splits = kblocks;
   if (splits < 1) splits = 1;
@@ -1213,35 +1819,49 @@ int conv_wgrad_ex(const Conv& c, const uint16_t* dy, const uint16_t* x, int64_t 
   return conv_gemm(call, s);
 }
 
-int conv_wgrad(dbs_resnet* m, int ci, const uint16_t* dy, const uint16_t* x, int64_t B, float* grad, cudaStream_t s) {
+int conv_wgrad(dbs_resnet* m, int ci, const void* dy, const void* x, int64_t B, float* grad, cudaStream_t s) {
   const Conv& c = m->convs[ci];
-  return conv_wgrad_ex(c, dy, c.cin == 3 ? m->stem_cols : x, B, grad + c.w_off, s);
+  return conv_wgrad_ex(c, dy, c.cin == 3 ? m->stem_cols : x, B, grad + c.w_off, s, m->prec == DBS_PREC_F32,
+                       (int)(c.w_len / c.cout));
 }
 
 }  // namespace
 
 namespace dbs {
 
-int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const uint8_t* x_base,
+int resnet50_fwd_bwd(dbs_resnet* m, const void* wb, const float* pf, const uint8_t* x_base,
                      const int32_t* y_base, const int64_t* d_iter, int64_t B, float* grad, float* loss,
                      cudaStream_t s) {
   int st;
+  const bool f32 = m->prec == DBS_PREC_F32;
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
   DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- stem: 7x7/2 conv (explicit im2col) + BN + ReLU + 3x3/2 max-pool ----------------
   const Conv& sc = m->convs[m->stem];
-  DBS_CUDA_TRY(launch_pdl(im2col_stem7_kernel, dim3((unsigned)(B * sc.OH)), dim3(256), (size_t)3 * 7 * (m->image + 6) * sizeof(float), s, 
-      x_base, d_iter, B, m->image, m->stem_cols));
+  if (f32)
+    DBS_CUDA_TRY(launch_pdl(im2col_stem7_f32_kernel, dim3((unsigned)(B * sc.OH)), dim3(256),
+                            (size_t)3 * 7 * (m->image + 6) * sizeof(float), s, x_base, d_iter, B, m->image,
+                            static_cast<float*>(m->stem_cols)));
+  else
+    DBS_CUDA_TRY(launch_pdl(im2col_stem7_kernel, dim3((unsigned)(B * sc.OH)), dim3(256),
+                            (size_t)3 * 7 * (m->image + 6) * sizeof(float), s, x_base, d_iter, B, m->image,
+                            static_cast<uint16_t*>(m->stem_cols)));
   DBS_LAUNCH_CHECK();
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
   const int PH = sc.OH / 2;
-  DBS_CUDA_TRY(launch_pdl(maxpool_fwd_kernel, dim3(grid_one_wave(maxpool_fwd_kernel, B * PH * PH * 8, 256, 0)), dim3(256), 0, s, m->a[m->stem], B, sc.OH, sc.OW, 64, PH, PH,
-                                                                     m->mp_out, m->mp_idx));
+  if (f32)
+    DBS_CUDA_TRY(launch_pdl(maxpool_fwd_f32_kernel, dim3(grid_one_wave(maxpool_fwd_f32_kernel, B * PH * PH * 8, 256, 0)),
+                            dim3(256), 0, s, static_cast<const float*>(m->a[m->stem]), B, sc.OH, sc.OW, 64, PH, PH,
+                            static_cast<float*>(m->mp_out), m->mp_idx));
+  else
+    DBS_CUDA_TRY(launch_pdl(maxpool_fwd_kernel, dim3(grid_one_wave(maxpool_fwd_kernel, B * PH * PH * 8, 256, 0)),
+                            dim3(256), 0, s, static_cast<const uint16_t*>(m->a[m->stem]), B, sc.OH, sc.OW, 64, PH,
+                            PH, static_cast<uint16_t*>(m->mp_out), m->mp_idx));
   DBS_LAUNCH_CHECK();
   // ---------------- bottleneck blocks ----------------
-  const uint16_t* x = m->mp_out;
-  std::vector<const uint16_t*> blk_in(m->blocks.size());
+  const void* x = m->mp_out;
+  std::vector<const void*> blk_in(m->blocks.size());
   for (size_t i = 0; i < m->blocks.size(); i++) {
     const Block& b = m->blocks[i];
     blk_in[i] = x;
@@ -1256,35 +1876,62 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
   }
   // ---------------- head: average pool, FC (tcgen05 GEMMs), softmax cross-entropy ----------------
   const int C = m->feat_c, HW = m->feat_hw, K = m->classes, ld = m->cpad;
-  DBS_CUDA_TRY(launch_pdl(avgpool_kernel, dim3(grid_one_wave(avgpool_kernel, B * (C / 8), 256, 0)), dim3(256), 0, s, x, B, HW, C, m->feat_b));
+  const void* wfc = wptr(m, wb, m->fc_w);
+  if (f32) {
+    DBS_CUDA_TRY(launch_pdl(avgpool_f32_kernel, dim3(grid_one_wave(avgpool_f32_kernel, B * (C / 8), 256, 0)), dim3(256),
+                            0, s, static_cast<const float*>(x), B, HW, C, static_cast<float*>(m->feat_b)));
+    DBS_LAUNCH_CHECK();
+    if ((st = gemm_tf(m->feat_b, 0, C, wfc, 0, C, m->logits, ld, B, K, C, DBS_EPI_BIAS_F32, pf + m->fc_b, nullptr, s)))
+      return st;
+    DBS_CUDA_TRY(launch_pdl(ce_f32_kernel, dim3((unsigned)B), dim3(256), 0, s, m->logits, ld, y_base, d_iter, B, K,
+                            m->dlog_f, static_cast<float*>(m->dlog_b), m->cpad32, m->loss_per));
+    DBS_LAUNCH_CHECK();
+  } else {
+    DBS_CUDA_TRY(launch_pdl(avgpool_kernel, dim3(grid_one_wave(avgpool_kernel, B * (C / 8), 256, 0)), dim3(256), 0, s,
+                            static_cast<const uint16_t*>(x), B, HW, C, static_cast<uint16_t*>(m->feat_b)));
+    DBS_LAUNCH_CHECK();
+    // logits [B][K] = feat [B][C] . Wfc [K][C]^T + b
+    if ((st = gemm_bf16(m->feat_b, 0, C, wfc, 0, C, m->logits, ld, B, K, C, DBS_EPI_BIAS_F32, pf + m->fc_b, nullptr,
+                        s, nullptr)))
+      return st;
+    DBS_CUDA_TRY(launch_pdl(ce_kernel, dim3((unsigned)B), dim3(256), 0, s, m->logits, ld, y_base, d_iter, B, K,
+                            m->dlog_f, static_cast<uint16_t*>(m->dlog_b), m->loss_per));
+    DBS_LAUNCH_CHECK();
+  }
+  DBS_CUDA_TRY(launch_pdl(head_bias_kernel, dim3((K + 255) / 256), dim3(256), 0, s, m->dlog_f, ld, m->loss_per, B, K,
+                          grad + m->fc_b, loss ? loss : m->loss_scratch, loss ? d_iter : nullptr));
   DBS_LAUNCH_CHECK();
-  const uint16_t* wfc = wb + m->fc_w;
-  // logits [B][K] = feat [B][C] . Wfc [K][C]^T + b
-  if ((st = gemm_bf16(m->feat_b, 0, C, wfc, 0, C, m->logits, ld, B, K, C, DBS_EPI_BIAS_F32, pf + m->fc_b, nullptr, s,
-                      nullptr)))
-    return st;
-  DBS_CUDA_TRY(launch_pdl(ce_kernel, dim3((unsigned)B), dim3(256), 0, s, m->logits, ld, y_base, d_iter, B, K, m->dlog_f, m->dlog_b, m->loss_per));
-  DBS_LAUNCH_CHECK();
-  DBS_CUDA_TRY(launch_pdl(head_bias_kernel, dim3((K + 255) / 256), dim3(256), 0, s, m->dlog_f, ld, m->loss_per, B, K, grad + m->fc_b,
-                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr));
-  DBS_LAUNCH_CHECK();
-  // dWfc [K][C] = dlog^T . feat  (both MN-major over the batch)
-  if ((st = gemm_bf16(m->dlog_b, 1, ld, m->feat_b, 1, C, grad + m->fc_w, C, K, C, B, DBS_EPI_F32, nullptr, nullptr, s,
-                      nullptr)))
-    return st;
-  // dfeat [B][C] = dlog [B][K] . Wfc [K][C]  (Wfc MN-major)
-  if ((st = gemm_bf16(m->dlog_b, 0, ld, wfc, 1, C, m->dfeat, C, B, C, K, DBS_EPI_F32, nullptr, nullptr, s, nullptr)))
-    return st;
-  uint16_t* gcur = m->g0;
-  DBS_CUDA_TRY(launch_pdl(head_bcast_kernel, dim3(grid_one_wave(head_bcast_kernel, B * HW * (C / 8), 256, 0)), dim3(256), 0, s, m->dfeat, B, HW, C, gcur));
+  if (f32) {
+    // dWfc [K][C] = dlog^T . feat ; dfeat [B][C] = dlog [B][K] . Wfc [K][C]
+    if ((st = gemm_tf(m->dlog_b, 1, m->cpad32, m->feat_b, 1, C, grad + m->fc_w, C, K, C, B, DBS_EPI_F32, nullptr,
+                      nullptr, s)))
+      return st;
+    if ((st = gemm_tf(m->dlog_b, 0, m->cpad32, wfc, 1, C, m->dfeat, C, B, C, K, DBS_EPI_F32, nullptr, nullptr, s)))
+      return st;
+  } else {
+    // dWfc [K][C] = dlog^T . feat  (both MN-major over the batch)
+    if ((st = gemm_bf16(m->dlog_b, 1, ld, m->feat_b, 1, C, grad + m->fc_w, C, K, C, B, DBS_EPI_F32, nullptr, nullptr,
+                        s, nullptr)))
+      return st;
+    // dfeat [B][C] = dlog [B][K] . Wfc [K][C]  (Wfc MN-major)
+    if ((st = gemm_bf16(m->dlog_b, 0, ld, wfc, 1, C, m->dfeat, C, B, C, K, DBS_EPI_F32, nullptr, nullptr, s, nullptr)))
+      return st;
+  }
+  void* gcur = m->g0;
+  if (f32)
+    DBS_CUDA_TRY(launch_pdl(head_bcast_f32_kernel, dim3(grid_one_wave(head_bcast_f32_kernel, B * HW * (C / 8), 256, 0)),
+                            dim3(256), 0, s, m->dfeat, B, HW, C, static_cast<float*>(gcur)));
+  else
+    DBS_CUDA_TRY(launch_pdl(head_bcast_kernel, dim3(grid_one_wave(head_bcast_kernel, B * HW * (C / 8), 256, 0)),
+                            dim3(256), 0, s, m->dfeat, B, HW, C, static_cast<uint16_t*>(gcur)));
   DBS_LAUNCH_CHECK();
   // ---------------- backward through the blocks ----------------
   // buffers: gx = gradient of the block input, t0 = BN outputs' gradients,
   // t1 = conv input gradients / masked shortcut gradient, t2 = shortcut BN's
-  uint16_t* gx = m->g1;
-  uint16_t* t0 = m->g2;
-  uint16_t* t1 = m->g3;
-  uint16_t* t2 = m->g4;
+  void* gx = m->g1;
+  void* t0 = m->g2;
+  void* t1 = m->g3;
+  void* t2 = m->g4;
   for (int i = (int)m->blocks.size() - 1; i >= 0; i--) {
     const Block& b = m->blocks[i];
     // BN3 with the block's output ReLU mask; the masked gradient is the
@@ -1309,19 +1956,26 @@ int resnet50_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const u
     } else {
       if ((st = conv_dgrad(m, b.c1, t0, wb, B, gx, 1, s))) return st;
     }
-    uint16_t* old = gcur;
+    void* old = gcur;
     gcur = gx;
     gx = old;
   }
   // ---------------- stem backward: max-pool, BN + ReLU mask, weight gradient ----------------
-  DBS_CUDA_TRY(launch_pdl(maxpool_bwd_kernel, dim3(grid_one_wave(maxpool_bwd_kernel, B * sc.OH * sc.OW * 8, 256, 0)), dim3(256), 0, s, gcur, m->mp_idx, B, sc.OH, sc.OW, 64, PH,
-                                                                           PH, t1));
+  if (f32)
+    DBS_CUDA_TRY(launch_pdl(maxpool_bwd_f32_kernel,
+                            dim3(grid_one_wave(maxpool_bwd_f32_kernel, B * sc.OH * sc.OW * 8, 256, 0)), dim3(256), 0, s,
+                            static_cast<const float*>(gcur), m->mp_idx, B, sc.OH, sc.OW, 64, PH, PH,
+                            static_cast<float*>(t1)));
+  else
+    DBS_CUDA_TRY(launch_pdl(maxpool_bwd_kernel, dim3(grid_one_wave(maxpool_bwd_kernel, B * sc.OH * sc.OW * 8, 256, 0)),
+                            dim3(256), 0, s, static_cast<const uint16_t*>(gcur), m->mp_idx, B, sc.OH, sc.OW, 64, PH,
+                            PH, static_cast<uint16_t*>(t1)));
   DBS_LAUNCH_CHECK();
   if ((st = bn_bwd(m, m->stem, pf, grad, t1, m->a[m->stem], B, t0, nullptr, s))) return st;
   return conv_wgrad(m, m->stem, t0, nullptr, B, grad, s);
 }
 
-int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const void* x_any, const int32_t* y_base,
+int resnet_fwd_bwd(dbs_resnet* m, const void* wb, const float* pf, const void* x_any, const int32_t* y_base,
                    const int64_t* d_iter, int64_t B, float* grad, float* loss, cudaStream_t s) {
   DBS_REQUIRE(m && wb && pf && x_any && y_base && grad, DBS_ERR_ARGUMENT, "resnet: null argument");
   DBS_REQUIRE(B >= 1 && B <= m->max_b, DBS_ERR_ARGUMENT, "resnet: batch %lld outside [1, %lld]", (long long)B,
@@ -1329,16 +1983,22 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
   if (m->arch == 50)
     return resnet50_fwd_bwd(m, wb, pf, static_cast<const uint8_t*>(x_any), y_base, d_iter, B, grad, loss, s);
   const float* x_base = static_cast<const float*>(x_any);
+  const bool f32 = m->prec == DBS_PREC_F32;
   int st;
   DBS_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * m->P, s));
   DBS_CUDA_TRY(cudaMemsetAsync(m->stats_acc, 0, sizeof(double) * m->stats_len, s));
   // ---------------- forward ----------------
-  DBS_CUDA_TRY(launch_pdl(im2col_stem_kernel, dim3(grid_one_wave(im2col_stem_kernel, B * 1024, 256, 0)), dim3(256), 0, s, x_base, d_iter, B, m->stem_cols));
+  if (f32)
+    DBS_CUDA_TRY(launch_pdl(im2col_stem_f32_kernel, dim3(grid_one_wave(im2col_stem_f32_kernel, B * 1024, 256, 0)),
+                            dim3(256), 0, s, x_base, d_iter, B, static_cast<float*>(m->stem_cols)));
+  else
+    DBS_CUDA_TRY(launch_pdl(im2col_stem_kernel, dim3(grid_one_wave(im2col_stem_kernel, B * 1024, 256, 0)), dim3(256),
+                            0, s, x_base, d_iter, B, static_cast<uint16_t*>(m->stem_cols)));
   DBS_LAUNCH_CHECK();
   if ((st = conv_fwd(m, m->stem, nullptr, wb, B, s))) return st;
   if ((st = bn_apply(m, m->stem, pf, nullptr, -1, 1, B, m->a[m->stem], s))) return st;
-  const uint16_t* x = m->a[m->stem];
-  std::vector<const uint16_t*> blk_in(m->blocks.size());
+  const void* x = m->a[m->stem];
+  std::vector<const void*> blk_in(m->blocks.size());
   for (size_t i = 0; i < m->blocks.size(); i++) {
     const Block& b = m->blocks[i];
     blk_in[i] = x;
@@ -1352,26 +2012,32 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
     x = m->blk_out[i];
   }
   // ---------------- head ----------------
-  uint16_t* gcur = m->g0;  // gradient w.r.t. the current block output
-  DBS_CUDA_TRY(launch_pdl(head_kernel, dim3((unsigned)B), dim3(256), 0, s, x, pf + m->fc_w, pf + m->fc_b, y_base, d_iter, B, m->classes, m->feat,
-                                          m->dlog, m->loss_per, gcur));
+  void* gcur = m->g0;  // gradient w.r.t. the current block output
+  if (f32)
+    DBS_CUDA_TRY(launch_pdl(head_f32_kernel, dim3((unsigned)B), dim3(256), 0, s, static_cast<const float*>(x),
+                            pf + m->fc_w, pf + m->fc_b, y_base, d_iter, B, m->classes, m->feat, m->dlog, m->loss_per,
+                            static_cast<float*>(gcur)));
+  else
+    DBS_CUDA_TRY(launch_pdl(head_kernel, dim3((unsigned)B), dim3(256), 0, s, static_cast<const uint16_t*>(x),
+                            pf + m->fc_w, pf + m->fc_b, y_base, d_iter, B, m->classes, m->feat, m->dlog, m->loss_per,
+                            static_cast<uint16_t*>(gcur)));
   DBS_LAUNCH_CHECK();
-  DBS_CUDA_TRY(launch_pdl(head_wgrad_kernel, dim3((m->classes * 512 + 255) / 256), dim3(256), 0, s, m->feat, m->dlog, m->loss_per, B, m->classes,
-                                                                    grad + m->fc_w, grad + m->fc_b,
-                                                                    loss ? loss : m->loss_scratch, loss ? d_iter : nullptr));
+  DBS_CUDA_TRY(launch_pdl(head_wgrad_kernel, dim3((m->classes * 512 + 255) / 256), dim3(256), 0, s, m->feat, m->dlog,
+                          m->loss_per, B, m->classes, grad + m->fc_w, grad + m->fc_b, loss ? loss : m->loss_scratch,
+                          loss ? d_iter : nullptr));
   DBS_LAUNCH_CHECK();
   // ---------------- backward through the blocks ----------------
-  uint16_t* bufs[3] = {m->g1, m->g2, m->g3};
+  void* bufs[3] = {m->g1, m->g2, m->g3};
   for (int i = (int)m->blocks.size() - 1; i >= 0; i--) {
     const Block& b = m->blocks[i];
-    const uint16_t* out = m->blk_out[i];
+    const void* out = m->blk_out[i];
     // gradient w.r.t. the block input accumulates in gx (shortcut path first)
-    uint16_t* gx = bufs[0];
-    uint16_t* dy2 = bufs[1];
-    uint16_t* tmp = bufs[2];
+    void* gx = bufs[0];
+    void* dy2 = bufs[1];
+    void* tmp = bufs[2];
     // BN2 backward with the output ReLU mask; masked gradient g -> gx (identity) or tmp (ds)
     if ((st = bn_bwd(m, b.c2, pf, grad, gcur, out, B, dy2, b.ds >= 0 ? tmp : gx, s))) return st;
-    uint16_t* dyd = gcur;  // gcur is free once tmp holds the masked gradient
+    void* dyd = gcur;  // gcur is free once tmp holds the masked gradient
     if (b.ds >= 0) {
       // BN_ds backward on the same masked gradient and the 1x1 stride-2 conv's weight gradient
       if ((st = bn_bwd(m, b.ds, pf, grad, tmp, nullptr, B, dyd, nullptr, s))) return st;
@@ -1381,7 +2047,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
     if ((st = conv_wgrad(m, b.c2, dy2, m->a[b.c1], B, grad, s))) return st;
     if ((st = conv_dgrad(m, b.c2, dy2, wb, B, tmp, 0, s))) return st;
     // BN1 backward with the ReLU mask of a1 -> dy1 (dy2 buffer is free now)
-    uint16_t* dy1 = dy2;
+    void* dy1 = dy2;
     if ((st = bn_bwd(m, b.c1, pf, grad, tmp, m->a[b.c1], B, dy1, nullptr, s))) return st;
     if ((st = conv_wgrad(m, b.c1, dy1, blk_in[i], B, grad, s))) return st;
     if (b.ds >= 0) {
@@ -1393,7 +2059,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
       if ((st = conv_dgrad(m, b.c1, dy1, wb, B, gx, 1, s))) return st;  // accumulate onto the shortcut gradient
     }
     // rotate: gx becomes the next gcur
-    uint16_t* old = gcur;
+    void* old = gcur;
     gcur = gx;
     bufs[0] = old;
   }
@@ -1404,6 +2070,7 @@ int resnet_fwd_bwd(dbs_resnet* m, const uint16_t* wb, const float* pf, const voi
 }
 
 int resnet_param_count(const dbs_resnet* m) { return (int)m->P; }
+int resnet_precision(const dbs_resnet* m) { return m->prec; }
 int64_t resnet_row_bytes(const dbs_resnet* m) { return m->row_bytes; }
 
 int iter_increment(int64_t* d_iter, cudaStream_t s) {
@@ -1414,8 +2081,11 @@ int iter_increment(int64_t* d_iter, cudaStream_t s) {
 
 }  // namespace dbs
 
-extern "C" int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_batch, int32_t classes,
-                                    dbs_resnet** out) {
+extern "C" int dbs_resnet_create_ex2(int32_t depth, int32_t image, int64_t max_batch, int32_t classes,
+                                     int32_t precision, dbs_resnet** out) {
+  DBS_REQUIRE(out && max_batch > 0, DBS_ERR_ARGUMENT, "resnet_create: need max_batch > 0");
+  DBS_REQUIRE(precision == DBS_PREC_BF16 || precision == DBS_PREC_F32, DBS_ERR_ARGUMENT,
+              "resnet_create: precision %d", precision);
   DBS_REQUIRE(out && max_batch > 0, DBS_ERR_ARGUMENT, "resnet_create: need max_batch > 0");
   DBS_REQUIRE((depth == 18 && image == 32 && classes >= 2 && classes <= 16) ||
                   (depth == 50 && image >= 64 && image % 32 == 0 && image <= 512 && classes >= 2 && classes <= 8192),
@@ -1428,10 +2098,12 @@ extern "C" int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_ba
   m->classes = classes;
   m->arch = depth;
   m->image = image;
+  m->prec = precision;
   if (depth == 50) {
     m->row_bytes = (int64_t)3 * image * image;  // uint8 pixels
     m->stem_k = kStem7K;
     m->cpad = (classes + 7) & ~7;
+    m->cpad32 = (classes + 31) & ~31;
     build_layers50(m);
   } else {
     build_layers(m);
@@ -1445,8 +2117,28 @@ extern "C" int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_ba
   return DBS_OK;
 }
 
+extern "C" int dbs_resnet_create_ex(int32_t depth, int32_t image, int64_t max_batch, int32_t classes,
+                                    dbs_resnet** out) {
+  return dbs_resnet_create_ex2(depth, image, max_batch, classes, DBS_PREC_BF16, out);
+}
+
 extern "C" int dbs_resnet_create(int64_t max_batch, int32_t classes, dbs_resnet** out) {
-  return dbs_resnet_create_ex(18, 32, max_batch, classes, out);
+  return dbs_resnet_create_ex2(18, 32, max_batch, classes, DBS_PREC_BF16, out);
+}
+
+// BN running statistics of conv `conv` (f32 mode): [cout] mean then [cout] unbiased variance
+extern "C" int dbs_resnet_running_stats(const dbs_resnet* m, int32_t conv, float** d_stats, int32_t* channels) {
+  DBS_REQUIRE(m && conv >= 0 && conv < (int32_t)m->convs.size() && d_stats, DBS_ERR_ARGUMENT,
+              "resnet_running_stats: bad conv index");
+  *d_stats = m->run_stats + m->run_off[conv];
+  if (channels) *channels = m->convs[conv].cout;
+  return DBS_OK;
+}
+
+extern "C" int dbs_resnet_precision(const dbs_resnet* m, int32_t* precision) {
+  DBS_REQUIRE(m && precision, DBS_ERR_ARGUMENT, "resnet_precision: null");
+  *precision = m->prec;
+  return DBS_OK;
 }
 
 extern "C" int dbs_resnet_info(const dbs_resnet* m, int32_t* depth, int32_t* image, int64_t* row_bytes,
@@ -1484,6 +2176,7 @@ extern "C" int dbs_resnet_destroy(dbs_resnet* m) {
   cudaFree(m->dlog_f);
   cudaFree(m->dlog_b);
   cudaFree(m->dfeat);
+  cudaFree(m->run_stats);
   delete m;
   return DBS_OK;
 }
@@ -1508,10 +2201,10 @@ extern "C" int dbs_resnet_param_table(const dbs_resnet* m, int64_t* off, int64_t
   return DBS_OK;
 }
 
-extern "C" int dbs_resnet_forward_backward(dbs_resnet* m, const uint16_t* d_params_bf16, const float* d_params,
+extern "C" int dbs_resnet_forward_backward(dbs_resnet* m, const void* d_params_shadow, const float* d_params,
                                            const void* d_x, const int32_t* d_labels, int64_t batch,
                                            const int64_t* d_iter, float* d_grad, float* d_loss, void* stream) {
-  return resnet_fwd_bwd(m, d_params_bf16, d_params, d_x, d_labels, d_iter, batch, d_grad, d_loss, as_stream(stream));
+  return resnet_fwd_bwd(m, d_params_shadow, d_params, d_x, d_labels, d_iter, batch, d_grad, d_loss, as_stream(stream));
 }
 
 // ---- standalone convolution entry points (unit tests / other models) ----
@@ -1561,6 +2254,52 @@ extern "C" int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int3
   (void)d_scratch;  // no scratch since the stride-2 path runs per parity class
   return conv_dgrad_ex(c, static_cast<const uint16_t*>(d_dy), static_cast<const uint16_t*>(d_w), N,
                        static_cast<uint16_t*>(d_dx), 0, as_stream(stream));
+}
+
+// fp32-class (3xTF32) forms: S32 x / w / dy operands (rows of 32-multiples), fp32 outputs
+extern "C" int dbs_dev_conv2d_fwd_s32(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
+                                      int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_y, void* stream) {
+  DBS_REQUIRE(Cin % 32 == 0 && Cout % 32 == 0, DBS_ERR_ARGUMENT, "conv2d_fwd_s32: Cin, Cout multiples of 32");
+  const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
+  ConvCall call{};
+  call.tf = 1;
+  call.M = (int64_t)N * c.OH * c.OW;
+  call.N = Cout;
+  call.K = (int64_t)k * k * Cin;
+  call.b_mode = 0;
+  call.b = d_w;
+  call.ldb = call.K;
+  if (k == 1 && stride == 1) {
+    call.a_mode = 0;
+    call.a = d_x;
+    call.lda = Cin;
+  } else {
+    call.a_mode = 2;
+    call.a = d_x;
+    call.ta = nhwc(N, H, W, Cin);
+    call.ga = ConvGeom{k, k, Cin / 32, stride, pad, c.OH, c.OW, Cin};
+  }
+  call.epi = DBS_EPI_F32;
+  call.d = d_y;
+  call.ldd = Cout;
+  return conv_gemm(call, as_stream(stream));
+}
+
+extern "C" int dbs_dev_conv2d_dgrad_s32(const void* d_dy, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                                        const void* d_w, int32_t Cout, int32_t k, int32_t stride, int32_t pad,
+                                        float* d_dx, void* stream) {
+  DBS_REQUIRE(Cin % 32 == 0 && Cout % 32 == 0 && (stride == 1 || stride == 2) && pad == k / 2, DBS_ERR_ARGUMENT,
+              "conv2d_dgrad_s32: Cin, Cout %% 32, stride 1/2, same padding required");
+  const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
+  return conv_dgrad_ex(c, d_dy, d_w, N, d_dx, 0, as_stream(stream), true);
+}
+
+extern "C" int dbs_dev_conv2d_wgrad_s32(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W,
+                                        int32_t Cin, int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw,
+                                        void* stream) {
+  DBS_REQUIRE(Cin % 32 == 0 && Cout % 32 == 0, DBS_ERR_ARGUMENT, "conv2d_wgrad_s32: Cin, Cout %% 32 required");
+  const Conv c = make_conv(N, H, W, Cin, Cout, k, stride, pad);
+  return conv_wgrad_ex(c, d_dy, d_x, N, d_dw, as_stream(stream), true);
 }
 
 extern "C" int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin,

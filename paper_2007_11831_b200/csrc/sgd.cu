@@ -87,10 +87,33 @@ __device__ __forceinline__ uint32_t bf16_bits(float f) {
   return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
 }
 
+__device__ __forceinline__ float rn_tf32(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
+}
+
+// operand shadow of 4 consecutive parameters (index 4 p): bf16 [P], or the flat S32
+// format of the fp32-class GEMMs (s32.cu): element i's hi at 2 (i & ~31) + (i & 31), lo 32 later
+template <int PREC>
+__device__ __forceinline__ void store_shadow(void* sh, int64_t p, const float4 x) {
+  if (PREC == DBS_PREC_BF16) {
+    reinterpret_cast<uint2*>(sh)[p] =
+        make_uint2(bf16_bits(x.x) | (bf16_bits(x.y) << 16), bf16_bits(x.z) | (bf16_bits(x.w) << 16));
+  } else {
+    const int64_t i = 4 * p;
+    float* d = reinterpret_cast<float*>(sh) + 2 * (i & ~int64_t(31)) + (i & 31);
+    const float4 h = make_float4(rn_tf32(x.x), rn_tf32(x.y), rn_tf32(x.z), rn_tf32(x.w));
+    *reinterpret_cast<float4*>(d) = h;
+    *reinterpret_cast<float4*>(d + 32) =
+        make_float4(rn_tf32(x.x - h.x), rn_tf32(x.y - h.y), rn_tf32(x.z - h.z), rn_tf32(x.w - h.w));
+  }
+}
+
 // fp32 fused aggregate + step, 4 elements per thread (float4).
+template <int PREC>
 __global__ void __launch_bounds__(256) aggregate_sgd_f32_kernel(AggArgs a, int64_t P4, float step, float mom,
                                                                 float4* __restrict__ x, float4* __restrict__ v,
-                                                                uint2* __restrict__ xb) {
+                                                                void* __restrict__ xb) {
   // weights straight from the parameter bank (no local-memory array)
 #define W(i) ((a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[i] : 1.0f / (float)a.n)
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x) {
@@ -110,9 +133,17 @@ __global__ void __launch_bounds__(256) aggregate_sgd_f32_kernel(AggArgs a, int64
     xx.z = fmaf(-step, vv.z, xx.z); xx.w = fmaf(-step, vv.w, xx.w);
     v[p] = vv;
     x[p] = xx;
-    if (xb) xb[p] = make_uint2(bf16_bits(xx.x) | (bf16_bits(xx.y) << 16), bf16_bits(xx.z) | (bf16_bits(xx.w) << 16));
+    if (xb) store_shadow<PREC>(xb, p, xx);
   }
 #undef W
+}
+
+template <int PREC>
+__global__ void __launch_bounds__(256) refresh_shadow_kernel(const float4* __restrict__ x, int64_t P4,
+                                                             void* __restrict__ xb) {
+  pdl_trigger_and_wait();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x)
+    store_shadow<PREC>(xb, p, x[p]);
 }
 
 // fp32 weighted reduce without the step: out = sum_i w_i g_i (the local level of
@@ -136,9 +167,10 @@ __global__ void __launch_bounds__(256) aggregate_f32_kernel(AggArgs a, int64_t P
 // aggregation), written back to every replica (fp32 + its bf16 operand copy)
 struct ReplicaArgs {
   float4* x[kMaxWorkers];
-  uint2* xb[kMaxWorkers];
+  void* xb[kMaxWorkers];
 };
 
+template <int PREC>
 __global__ void __launch_bounds__(256) average_replicas_f32_kernel(AggArgs a, ReplicaArgs r, int64_t P4) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x) {
     const float w0 = (a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[0] : 1.0f / (float)a.n;
@@ -150,10 +182,9 @@ __global__ void __launch_bounds__(256) average_replicas_f32_kernel(AggArgs a, Re
       g.x = fmaf(wi, h.x, g.x); g.y = fmaf(wi, h.y, g.y);
       g.z = fmaf(wi, h.z, g.z); g.w = fmaf(wi, h.w, g.w);
     }
-    const uint2 gb = make_uint2(bf16_bits(g.x) | (bf16_bits(g.y) << 16), bf16_bits(g.z) | (bf16_bits(g.w) << 16));
     for (int i = 0; i < a.n; i++) {
       r.x[i][p] = g;
-      if (r.xb[i]) r.xb[i][p] = gb;
+      if (r.xb[i]) store_shadow<PREC>(r.xb[i], p, g);
     }
   }
 }
@@ -200,19 +231,45 @@ extern "C" int dbs_dev_aggregate_sgd_f64(const double* const* d_grads, const int
   return DBS_OK;
 }
 
-extern "C" int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* b, int64_t n,
-                                         int32_t mode, int64_t P, float step, float mom, float* d_x,
-                                         float* d_v, uint16_t* d_x_bf16, void* stream) {
+extern "C" int dbs_dev_aggregate_sgd_f32_ex(const float* const* d_grads, const int64_t* b, int64_t n,
+                                            int32_t mode, int64_t P, float step, float mom, float* d_x,
+                                            float* d_v, void* d_shadow, int32_t shadow_prec, void* stream) {
   AggArgs a;
   int st = make_args(a, (const void* const*)d_grads, b, n, mode);
   if (st) return st;
   DBS_REQUIRE(P % 4 == 0, DBS_ERR_ARGUMENT, "fp32 aggregate: P must be a multiple of 4 (pad the flat buffer)");
+  DBS_REQUIRE(shadow_prec == DBS_PREC_BF16 || (shadow_prec == DBS_PREC_F32 && P % 32 == 0), DBS_ERR_ARGUMENT,
+              "aggregate_sgd: shadow precision %d (S32 needs P %% 32 == 0)", shadow_prec);
   for (int64_t i = 0; i < n; i++)
     DBS_REQUIRE(((uintptr_t)d_grads[i] % 16) == 0, DBS_ERR_ARGUMENT, "gradient buffers must be 16-byte aligned");
   if (P <= 0) return DBS_OK;
   const int64_t P4 = P / 4;
-  aggregate_sgd_f32_kernel<<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
-      a, P4, step, mom, (float4*)d_x, (float4*)d_v, (uint2*)d_x_bf16);
+  if (shadow_prec == DBS_PREC_F32)
+    aggregate_sgd_f32_kernel<DBS_PREC_F32><<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
+        a, P4, step, mom, (float4*)d_x, (float4*)d_v, d_shadow);
+  else
+    aggregate_sgd_f32_kernel<DBS_PREC_BF16><<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
+        a, P4, step, mom, (float4*)d_x, (float4*)d_v, d_shadow);
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_aggregate_sgd_f32(const float* const* d_grads, const int64_t* b, int64_t n,
+                                         int32_t mode, int64_t P, float step, float mom, float* d_x,
+                                         float* d_v, uint16_t* d_x_bf16, void* stream) {
+  return dbs_dev_aggregate_sgd_f32_ex(d_grads, b, n, mode, P, step, mom, d_x, d_v, d_x_bf16, DBS_PREC_BF16, stream);
+}
+
+extern "C" int dbs_dev_refresh_shadow(const float* d_x, int64_t P, void* d_shadow, int32_t prec, void* stream) {
+  DBS_REQUIRE(d_x && d_shadow && P % 4 == 0 && (prec == DBS_PREC_BF16 || (prec == DBS_PREC_F32 && P % 32 == 0)),
+              DBS_ERR_ARGUMENT, "refresh_shadow: P %% 4 (bf16) / P %% 32 (S32) and a known precision");
+  if (P <= 0) return DBS_OK;
+  if (prec == DBS_PREC_F32)
+    DBS_CUDA_TRY(launch_pdl(refresh_shadow_kernel<DBS_PREC_F32>, dim3(grid_for(P / 4, 256)), dim3(256), 0,
+                            as_stream(stream), (const float4*)d_x, P / 4, d_shadow));
+  else
+    DBS_CUDA_TRY(launch_pdl(refresh_shadow_kernel<DBS_PREC_BF16>, dim3(grid_for(P / 4, 256)), dim3(256), 0,
+                            as_stream(stream), (const float4*)d_x, P / 4, d_shadow));
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -229,20 +286,31 @@ extern "C" int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t*
   return DBS_OK;
 }
 
-extern "C" int dbs_dev_average_replicas_f32(float* const* d_params, const int64_t* b, int64_t n, int32_t mode,
-                                            int64_t P, uint16_t* const* d_params_bf16, void* stream) {
+extern "C" int dbs_dev_average_replicas_f32_ex(float* const* d_params, const int64_t* b, int64_t n, int32_t mode,
+                                               int64_t P, void* const* d_shadows, int32_t shadow_prec, void* stream) {
   AggArgs a;
   int st = make_args(a, (const void* const*)d_params, b, n, mode);
   if (st) return st;
   DBS_REQUIRE(P % 4 == 0, DBS_ERR_ARGUMENT, "average_replicas: P must be a multiple of 4");
+  DBS_REQUIRE(shadow_prec == DBS_PREC_BF16 || (shadow_prec == DBS_PREC_F32 && P % 32 == 0), DBS_ERR_ARGUMENT,
+              "average_replicas: shadow precision %d (S32 needs P %% 32 == 0)", shadow_prec);
   ReplicaArgs r;
   for (int64_t i = 0; i < n; i++) {
     DBS_REQUIRE(((uintptr_t)d_params[i] % 16) == 0, DBS_ERR_ARGUMENT, "replica buffers must be 16-byte aligned");
     r.x[i] = reinterpret_cast<float4*>(d_params[i]);
-    r.xb[i] = d_params_bf16 ? reinterpret_cast<uint2*>(d_params_bf16[i]) : nullptr;
+    r.xb[i] = d_shadows ? d_shadows[i] : nullptr;
   }
   if (P <= 0) return DBS_OK;
-  average_replicas_f32_kernel<<<grid_for(P / 4, 256), 256, 0, as_stream(stream)>>>(a, r, P / 4);
+  if (shadow_prec == DBS_PREC_F32)
+    average_replicas_f32_kernel<DBS_PREC_F32><<<grid_for(P / 4, 256), 256, 0, as_stream(stream)>>>(a, r, P / 4);
+  else
+    average_replicas_f32_kernel<DBS_PREC_BF16><<<grid_for(P / 4, 256), 256, 0, as_stream(stream)>>>(a, r, P / 4);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
+}
+
+extern "C" int dbs_dev_average_replicas_f32(float* const* d_params, const int64_t* b, int64_t n, int32_t mode,
+                                            int64_t P, uint16_t* const* d_params_bf16, void* stream) {
+  return dbs_dev_average_replicas_f32_ex(d_params, b, n, mode, P, reinterpret_cast<void* const*>(d_params_bf16),
+                                         DBS_PREC_BF16, stream);
 }

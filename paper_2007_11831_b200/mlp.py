@@ -6,9 +6,12 @@ of minibatch_gradient sgdlab.py:200-205) -- but every step runs in
 libdbs_b200: the forward/backward is 5 tcgen05 GEMMs + 2 small kernels
 (csrc/mlp.cu), the update is the fused aggregate+SGD kernel.
 
-Parameter layout (flat, fp32 master + bf16 shadow for the GEMMs):
+Parameter layout (flat, fp32 master + an operand shadow for the GEMMs):
     [ W1 (H x IN) | b1 (H) | W2 (C x H) | b2 (C) ]
-each block padded to a multiple of 8 elements (16-byte TMA alignment).
+precision "f32" (default; the fp32 class of the reference's numpy fp64 loop):
+3xTF32 GEMMs on S32 operands, W1 rows padded to IN rounded up to 32, every
+block starting on a 32-element boundary (the flat S32 shadow, 2P floats);
+precision "bf16": bf16 operands, blocks padded to multiples of 8.
 """
 
 from __future__ import annotations
@@ -25,14 +28,22 @@ def _pad8(x: int) -> int:
     return (x + 7) & ~7
 
 
+def _pad32(x: int) -> int:
+    return (x + 31) & ~31
+
+
 class MlpLayout:
-    def __init__(self, in_dim: int = 784, hidden: int = 256, classes: int = 10):
+    def __init__(self, in_dim: int = 784, hidden: int = 256, classes: int = 10, precision="f32"):
         self.in_dim, self.hidden, self.classes = in_dim, hidden, classes
+        self.precision = _lib.precision_code(precision)
+        f32 = self.precision == _lib.PREC_F32
+        pad = _pad32 if f32 else _pad8
+        self.in_ld = _pad32(in_dim) if f32 else in_dim  # W1 row length (and S32 input row length)
         self.off_w1 = 0
-        self.off_b1 = _pad8(hidden * in_dim)
-        self.off_w2 = self.off_b1 + _pad8(hidden)
-        self.off_b2 = self.off_w2 + _pad8(classes * hidden)
-        self.P = self.off_b2 + _pad8(classes)
+        self.off_b1 = pad(hidden * self.in_ld)
+        self.off_w2 = self.off_b1 + pad(hidden)
+        self.off_b2 = self.off_w2 + pad(classes * hidden)
+        self.P = self.off_b2 + pad(classes)
         self.dimension = hidden * in_dim + hidden + classes * hidden + classes  # unpadded (reference view)
 
     def pad(self, flat):
@@ -40,8 +51,9 @@ class MlpLayout:
         flat = np.asarray(flat, dtype=np.float32).reshape(-1)
         H, I, C = self.hidden, self.in_dim, self.classes
         out = np.zeros(self.P, dtype=np.float32)
-        o = 0
-        for off, n in ((self.off_w1, H * I), (self.off_b1, H), (self.off_w2, C * H), (self.off_b2, C)):
+        out[self.off_w1:self.off_w1 + H * self.in_ld].reshape(H, self.in_ld)[:, :I] = flat[:H * I].reshape(H, I)
+        o = H * I
+        for off, n in ((self.off_b1, H), (self.off_w2, C * H), (self.off_b2, C)):
             out[off:off + n] = flat[o:o + n]
             o += n
         return out
@@ -49,7 +61,8 @@ class MlpLayout:
     def unpad(self, padded):
         padded = np.asarray(padded).reshape(-1)
         H, I, C = self.hidden, self.in_dim, self.classes
-        return np.concatenate([padded[self.off_w1:self.off_w1 + H * I], padded[self.off_b1:self.off_b1 + H],
+        w1 = padded[self.off_w1:self.off_w1 + H * self.in_ld].reshape(H, self.in_ld)[:, :I].reshape(-1)
+        return np.concatenate([w1, padded[self.off_b1:self.off_b1 + H],
                                padded[self.off_w2:self.off_w2 + C * H], padded[self.off_b2:self.off_b2 + C]])
 
 
@@ -74,25 +87,32 @@ def synthetic_mnist(n_samples=60000, in_dim=784, classes=10, seed=0):
 
 
 class MlpModel:
-    """Device parameters (fp32 master, bf16 shadow, momentum) of one replica."""
+    """Device parameters (fp32 master, operand shadow, momentum) of one replica.
+    ``params_op`` is the GEMM operand copy (S32 for "f32", bf16 for "bf16");
+    ``params_bf16`` names it for the bf16 precision."""
 
-    def __init__(self, in_dim=784, hidden=256, classes=10, seed=0, device=None, params=None):
+    def __init__(self, in_dim=784, hidden=256, classes=10, seed=0, device=None, params=None, precision="f32"):
         import torch
 
         _lib.require_device()
-        self.layout = L = MlpLayout(in_dim, hidden, classes)
+        self.layout = L = MlpLayout(in_dim, hidden, classes, precision)
+        self.precision = L.precision
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         flat = init_params(in_dim, hidden, classes, seed) if params is None else np.asarray(params, np.float32)
         self.params = torch.as_tensor(L.pad(flat), device=self.device)
-        self.params_bf16 = self.params.to(torch.bfloat16)
+        self.params_op = _lib.new_shadow(self.params, self.precision)
         self.velocity = torch.zeros_like(self.params)
+
+    @property
+    def params_bf16(self):
+        return self.params_op if self.precision == _lib.PREC_BF16 else None
 
     @property
     def P(self) -> int:
         return self.layout.P
 
     def refresh_shadow(self):
-        self.params_bf16.copy_(self.params.to(self.params_bf16.dtype))
+        _lib.refresh_shadow(self.params, self.params_op, self.precision)
 
     def host_params(self) -> np.ndarray:
         return self.layout.unpad(self.params.cpu().numpy())
@@ -103,8 +123,8 @@ class MlpScratch:
 
     def __init__(self, layout: MlpLayout, max_batch: int):
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().dbs_mlp_create(layout.in_dim, layout.hidden, layout.classes, int(max_batch),
-                                             ctypes.byref(h)), "mlp_create")
+        _lib.check(_lib.lib().dbs_mlp_create_ex(layout.in_dim, layout.hidden, layout.classes, int(max_batch),
+                                                layout.precision, ctypes.byref(h)), "mlp_create")
         self.handle = h
         self.max_batch = int(max_batch)
         p = ctypes.c_int64()
@@ -119,10 +139,24 @@ class MlpScratch:
             pass
 
 
-def forward_backward(model: MlpModel, scratch: MlpScratch, x_bf16, labels, grad, loss, stream=None):
-    """One worker's batch: flat fp32 gradient of the batch-mean CE loss."""
-    b = int(x_bf16.shape[0])
-    st = _lib.lib().dbs_mlp_forward_backward(scratch.handle, model.params_bf16.data_ptr(), model.params.data_ptr(),
-                                             x_bf16.data_ptr(), labels.data_ptr(), b, grad.data_ptr(), loss.data_ptr(),
+def operand_rows(layout: MlpLayout, x):
+    """Input rows fp32 [b][in] on the device -> the GEMM operand form (S32 [b][in_ld]
+    for "f32", bf16 for "bf16")."""
+    import torch
+
+    if layout.precision == _lib.PREC_BF16:
+        return x.to(torch.bfloat16).contiguous()
+    x = x.float().contiguous()
+    out = torch.empty((x.shape[0], 2 * layout.in_ld), dtype=torch.float32, device=x.device)
+    _lib.check(_lib.lib().dbs_dev_split_s32(x.data_ptr(), x.shape[0], layout.in_dim, layout.in_dim, out.data_ptr(),
+                                            layout.in_ld, _lib.stream_handle()), "split_s32")
+    return out
+
+
+def forward_backward(model: MlpModel, scratch: MlpScratch, x_op, labels, grad, loss, stream=None):
+    """One worker's batch (x_op from operand_rows): flat fp32 gradient of the batch-mean CE loss."""
+    b = int(x_op.shape[0])
+    st = _lib.lib().dbs_mlp_forward_backward(scratch.handle, model.params_op.data_ptr(), model.params.data_ptr(),
+                                             x_op.data_ptr(), labels.data_ptr(), b, grad.data_ptr(), loss.data_ptr(),
                                              _lib.stream_handle(stream))
     _lib.check(st, "mlp_forward_backward")

@@ -167,18 +167,28 @@ def synthetic_cifar(n_samples=50000, classes=10, seed=0):
 
 
 class ResnetModel:
-    """Device parameters (fp32 master, bf16 shadow, momentum) of one replica."""
+    """Device parameters (fp32 master, operand shadow, momentum) of one replica.
+    precision "f32" (default): 3xTF32 GEMMs, ``params_op`` = the S32 shadow (2P
+    floats); "bf16": bf16 operands, ``params_op`` = ``params_bf16``."""
 
-    def __init__(self, classes=10, seed=0, device=None, params=None, depth=18, image=32):
+    def __init__(self, classes=10, seed=0, device=None, params=None, depth=18, image=32, precision="f32"):
         import torch
 
         _lib.require_device()
         self.layout = L = ResnetLayout(classes, depth, image)
+        self.precision = _lib.precision_code(precision)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         tensors = init_params(classes, seed, depth, image) if params is None else params
         self.params = torch.as_tensor(L.pack(tensors), device=self.device)
-        self.params_bf16 = self.params.to(torch.bfloat16)
+        self.params_op = _lib.new_shadow(self.params, self.precision)
         self.velocity = torch.zeros_like(self.params)
+
+    @property
+    def params_bf16(self):
+        return self.params_op if self.precision == _lib.PREC_BF16 else None
+
+    def refresh_shadow(self):
+        _lib.refresh_shadow(self.params, self.params_op, self.precision)
 
     @property
     def P(self) -> int:
@@ -191,12 +201,25 @@ class ResnetModel:
 class ResnetScratch:
     """Per-worker activation scratch (dbs_resnet) sized for the largest batch."""
 
-    def __init__(self, max_batch: int, classes: int = 10, depth: int = 18, image: int = 32):
+    def __init__(self, max_batch: int, classes: int = 10, depth: int = 18, image: int = 32, precision="f32"):
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().dbs_resnet_create_ex(depth, image, int(max_batch), classes, ctypes.byref(h)),
-                   "resnet_create")
+        self.precision = _lib.precision_code(precision)
+        _lib.check(_lib.lib().dbs_resnet_create_ex2(depth, image, int(max_batch), classes, self.precision,
+                                                    ctypes.byref(h)), "resnet_create")
         self.handle = h
         self.max_batch = int(max_batch)
+
+    def running_stats(self, conv: int):
+        """(mean, variance) numpy arrays of conv `conv`'s BatchNorm running statistics (f32 mode)."""
+        import torch
+
+        ptr, ch = ctypes.c_void_p(), ctypes.c_int32()
+        _lib.check(_lib.lib().dbs_resnet_running_stats(self.handle, int(conv), ctypes.byref(ptr), ctypes.byref(ch)),
+                   "running_stats")
+        from .comm import _wrap
+
+        t = _wrap(ptr.value, 2 * ch.value, "<f4", torch.device("cuda", torch.cuda.current_device())).cpu().numpy()
+        return t[:ch.value].copy(), t[ch.value:].copy()
 
     def __del__(self):
         try:
@@ -209,8 +232,10 @@ class ResnetScratch:
 def forward_backward(model: ResnetModel, scratch: ResnetScratch, x, labels, grad, loss, stream=None, d_iter=None):
     """One worker's batch: flat fp32 gradient of the batch-mean cross-entropy."""
     b = int(labels.shape[0]) if d_iter is None else int(scratch.max_batch)
+    if model.precision != scratch.precision:
+        raise ValueError("model and scratch precisions differ")
     st = _lib.lib().dbs_resnet_forward_backward(
-        scratch.handle, model.params_bf16.data_ptr(), model.params.data_ptr(), x.data_ptr(), labels.data_ptr(), b,
+        scratch.handle, model.params_op.data_ptr(), model.params.data_ptr(), x.data_ptr(), labels.data_ptr(), b,
         d_iter.data_ptr() if d_iter is not None else None, grad.data_ptr(), loss.data_ptr() if loss is not None else None,
         _lib.stream_handle(stream))
     _lib.check(st, "resnet_forward_backward")

@@ -119,7 +119,7 @@ class SimulatedTrainer:
 
     def __init__(self, X, y, n_workers: int, model: str = "mlp", hidden: int = 256, classes: int = 10,
                  seed: int = 0, partition: bool = False, params=None, max_batch: Optional[int] = None,
-                 graphs: Optional[bool] = None, pin_sms: Optional[bool] = None):
+                 graphs: Optional[bool] = None, pin_sms: Optional[bool] = None, precision="f32"):
         import torch
 
         _lib.require_device()
@@ -138,18 +138,22 @@ class SimulatedTrainer:
         self.n = n_workers
         self.classes = classes
         self.kind = MODEL_MLP if model == "mlp" else MODEL_RESNET18
+        # tensor-core operand precision: "f32" = 3xTF32 on S32 operands (the fp32 class), or "bf16"
+        self.precision = _lib.precision_code(precision)
         self.depth, self.image = (50, int(self.X.shape[-1])) if model == "resnet50" else (18, 32)
         if self.kind == MODEL_MLP:
             from .mlp import MlpModel
 
-            self.model = MlpModel(self.row_elems, hidden, classes, seed, self.dev, params=params)
+            self.model = MlpModel(self.row_elems, hidden, classes, seed, self.dev, params=params,
+                                  precision=self.precision)
         else:
             from .resnet import ResnetModel
 
             S = self.image
             if tuple(self.X.shape[1:]) != (3, S, S) or (model == "resnet18" and S != 32):
                 raise ConfigurationError(f"{model} expects [D][3][{S}][{S}] rows, got {tuple(self.X.shape)}")
-            self.model = ResnetModel(classes, seed, self.dev, params=params, depth=self.depth, image=S)
+            self.model = ResnetModel(classes, seed, self.dev, params=params, depth=self.depth, image=S,
+                                     precision=self.precision)
         self.workers = make_workers(n_workers, partition)
         partitioned = any(w.ctx for w in self.workers)
         # iteration graphs for ResNet (one context); partitioned workers launch eagerly
@@ -170,10 +174,14 @@ class SimulatedTrainer:
         self.d_iter = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.agg = torch.cuda.Stream()
         self.rng = None
-        # fixed-address shards (graph replays need stable pointers)
-        shard_dtype = torch.bfloat16 if self.kind == MODEL_MLP else x_dtype
-        self.shard_x = [torch.empty((self.D, self.row_elems), dtype=shard_dtype, device=self.dev) for _ in
-                        range(n_workers)]
+        # fixed-address shards (graph replays need stable pointers); MLP rows are stored
+        # in the GEMM operand form (S32 [in_ld] for "f32", bf16 for "bf16")
+        if self.kind == MODEL_MLP and self.precision == _lib.PREC_F32:
+            shard_shape, shard_dtype = (self.D, 2 * self.model.layout.in_ld), torch.float32
+        else:
+            shard_shape = (self.D, self.row_elems)
+            shard_dtype = torch.bfloat16 if self.kind == MODEL_MLP else x_dtype
+        self.shard_x = [torch.empty(shard_shape, dtype=shard_dtype, device=self.dev) for _ in range(n_workers)]
         self.shard_y = [torch.empty(self.D, dtype=torch.int32, device=self.dev) for _ in range(n_workers)]
         self.loss_buf = torch.zeros((n_workers, self.D + 1), dtype=torch.float32, device=self.dev)
         self._graph_cache = {}
@@ -191,10 +199,18 @@ class SimulatedTrainer:
             else:
                 from .resnet import ResnetScratch
 
-                cur = ResnetScratch(cap, self.classes, self.depth, self.image)
+                cur = ResnetScratch(cap, self.classes, self.depth, self.image, self.precision)
             self.scratch[w] = cur
             self._graph_cache.clear()  # scratch pointers changed
         return cur
+
+    def _gather_mlp(self, idx, rows, xs, stream):
+        """Repack MLP rows into the worker's shard in the GEMM operand form."""
+        if self.precision == _lib.PREC_F32:
+            return _lib.lib().dbs_dev_gather_rows_f32_s32(self.X.data_ptr(), idx.data_ptr(), rows, self.row_elems,
+                                                          xs.data_ptr(), self.model.layout.in_ld, stream)
+        return _lib.lib().dbs_dev_gather_rows_f32_bf16(self.X.data_ptr(), idx.data_ptr(), rows, self.row_elems,
+                                                       xs.data_ptr(), stream)
 
     def _run_iters(self, slots, t0, t1, mode, lr, mom, params, vel, pb, skip, d_iter=None):
         st = _lib.lib().dbs_run_iterations(slots, self.n, t0, t1, mode, float(lr), float(mom), params.data_ptr(),
@@ -209,7 +225,7 @@ class SimulatedTrainer:
         m = self.model
         self._rep_p = [m.params.clone() for _ in range(self.n)]
         self._rep_v = [m.velocity.clone() for _ in range(self.n)]
-        self._rep_pb = [m.params_bf16.clone() for _ in range(self.n)]
+        self._rep_pb = [m.params_op.clone() for _ in range(self.n)]
         arr = lambda ts: (ctypes.c_void_p * self.n)(*[t.data_ptr() for t in ts])
         self._rep_ptrs = (arr(self._rep_p), arr(self._rep_v), arr(self._rep_pb))
         self._rep_mode = mode
@@ -218,8 +234,9 @@ class SimulatedTrainer:
 
     def _average_replicas(self, mode: int, batches=None):
         b = np.asarray(batches if batches is not None else [1] * self.n, dtype=np.int64)
-        st = _lib.lib().dbs_dev_average_replicas_f32(self._rep_ptrs[0], b.ctypes.data_as(_lib.P_i64), self.n, int(mode),
-                                                     self.model.P, self._rep_ptrs[2], int(self.agg.cuda_stream))
+        st = _lib.lib().dbs_dev_average_replicas_f32_ex(self._rep_ptrs[0], b.ctypes.data_as(_lib.P_i64), self.n,
+                                                        int(mode), self.model.P, self._rep_ptrs[2], self.precision,
+                                                        int(self.agg.cuda_stream))
         _lib.check(st, "average_replicas")
 
     def _replicas_end(self, final_average: bool, batches):
@@ -230,7 +247,7 @@ class SimulatedTrainer:
         torch.cuda.current_stream().wait_stream(self.agg)
         self.model.params.copy_(self._rep_p[0])
         self.model.velocity.copy_(self._rep_v[0])
-        self.model.params_bf16.copy_(self._rep_pb[0])
+        self.model.params_op.copy_(self._rep_pb[0])
         torch.cuda.synchronize()
 
     def _prime(self, slots, mode: int):
@@ -242,7 +259,7 @@ class SimulatedTrainer:
         torch = self.torch
         p = self.model.params.clone()
         v = torch.zeros_like(p)
-        pb = self.model.params_bf16.clone()
+        pb = self.model.params_op.clone()
         cur = torch.cuda.current_stream()
         self.agg.wait_stream(cur)
         for wk in self.workers:
@@ -272,7 +289,7 @@ class SimulatedTrainer:
         c0 = _lib.lib().dbs_launch_count()
         with torch.cuda.graph(g, stream=self.agg):
             self._run_iters(slots, 0, 1, mode, lr, mom, self.model.params, self.model.velocity,
-                            self.model.params_bf16, skip, self.d_iter)
+                            self.model.params_op, skip, self.d_iter)
         per = _lib.lib().dbs_launch_count() - c0
         self._graph_cache[key] = (g, per)
         return g, per, per
@@ -283,8 +300,10 @@ class SimulatedTrainer:
             seed: int = 0, record_loss: bool = True, max_iters: Optional[int] = None,
             skip_update: bool = False, timed_from: Optional[int] = None,
             epoch_hook: Optional[Callable[[int], None]] = None,
-            averaging_interval: Optional[int] = None) -> RunResult:
-        """Train n_epochs under `config`.  epoch_hook(epoch), when given, runs at the
+            averaging_interval: Optional[int] = None, plan_source=None) -> RunResult:
+        """Train n_epochs under `config`.  plan_source (a sequence of PartitionPlans),
+        when given, replaces the re-plan: epoch e runs plan_source[min(e, len - 1)],
+        the plan-list form of run_parallel_sgd's plan source (sgdlab.py:320-340).  epoch_hook(epoch), when given, runs at the
         start of every epoch inside the timed region (e.g. a host->device upload of
         that epoch's data, for end-to-end measurements).
 
@@ -325,7 +344,10 @@ class SimulatedTrainer:
                 epoch_hook(epoch)
             launches0 = _lib.lib().dbs_launch_count()
             captured = 0
-            plan, smoothed = cluster.next_plan(config, epoch, n, D, stats[-1] if stats else None, smoothed)
+            if plan_source is not None:
+                plan = plan_source[min(epoch, len(plan_source) - 1)]
+            else:
+                plan, smoothed = cluster.next_plan(config, epoch, n, D, stats[-1] if stats else None, smoothed)
             plans.append(plan)
             batches = list(plan.int_batches)
             spans = list(plan.sample_spans)
@@ -343,8 +365,7 @@ class SimulatedTrainer:
                 xs, ys = self.shard_x[w], self.shard_y[w]
                 if rows:
                     if self.kind == MODEL_MLP:
-                        st = _lib.lib().dbs_dev_gather_rows_f32_bf16(self.X.data_ptr(), idx.data_ptr(), rows,
-                                                                     self.row_elems, xs.data_ptr(), s_main)
+                        st = self._gather_mlp(idx, rows, xs, s_main)
                     else:
                         st = _lib.lib().dbs_dev_gather_rows(self.X.data_ptr(), idx.data_ptr(), rows,
                                                             self.row_bytes, xs.data_ptr(), s_main)
@@ -393,7 +414,9 @@ class SimulatedTrainer:
                             spin_key.append((w, "x", float(ev.cost_multiplier)))
                     elif ev.extra_epoch_seconds:
                         slots[w].spin_ns = int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
-                        slots[w].spin_ctas = wk.sm_count
+                        # in its own partition the spin occupies the worker's SMs; on a shared
+                        # GPU a 2-CTA timed spin delays only this worker's stream
+                        slots[w].spin_ctas = wk.sm_count if wk.ctx else 2
                         spin_key.append((w, slots[w].spin_ns))
             if iters > 0 and (spinning or self.graphs):
                 self._prime(slots, mode)
@@ -427,7 +450,7 @@ class SimulatedTrainer:
                     _lib.check(st, "run_iterations_local")
                 else:
                     self._run_iters(slots, 0, iters, mode, lr, momentum, self.model.params, self.model.velocity,
-                                    self.model.params_bf16, skip_update)
+                                    self.model.params_op, skip_update)
             end.record(self.agg)
             # stop the disturbance once the epoch's work is done (copy engine, no kernel)
             _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 1, int(self.agg.cuda_stream)), "set_flag")
@@ -510,7 +533,7 @@ class DistributedTrainer(SimulatedTrainer):
 
     def __init__(self, D_per_rank: int, workers_per_rank: int = 1, model: str = "resnet18", classes: int = 10,
                  seed: int = 0, partition: Optional[bool] = None, max_batch: Optional[int] = None, group=None,
-                 image: int = 224):
+                 image: int = 224, precision="f32"):
         import torch
         import torch.distributed as dist
 
@@ -530,16 +553,27 @@ class DistributedTrainer(SimulatedTrainer):
         y = torch.randint(0, classes, (D,), generator=g, device=dev, dtype=torch.int32)
         part = (workers_per_rank > 1) if partition is None else partition
         super().__init__(X, y, workers_per_rank, model=model, classes=classes, seed=seed, partition=part,
-                         max_batch=max_batch, graphs=False, pin_sms=True)
-        self.comm = Communicator.create(self.model.P, group)
-        self.comm.params.copy_(self.model.params)
-        self.comm.params_bf16.copy_(self.comm.params.to(torch.bfloat16))
+                         max_batch=max_batch, graphs=False, pin_sms=True, precision=precision)
+        P = self.model.P
+        self.comm = Communicator.create(P, group)
+        # the communicator pads P to a multiple of 32 * world: the model's P elements are its prefix
+        self.comm.params.zero_()
+        self.comm.params[:P].copy_(self.model.params)
+        if self.precision == _lib.PREC_F32:
+            # S32 operand copy kept locally, refreshed after every update (comm.cu pushes fp32 only)
+            self.comm_shadow = torch.zeros(2 * self.comm.P, dtype=torch.float32, device=self.dev)
+            _lib.refresh_shadow(self.comm.params, self.comm_shadow, self.precision)
+            self.comm.set_shadow(self.comm_shadow, self.precision)
+            shadow = self.comm_shadow[:2 * P]
+        else:
+            self.comm.params_bf16.copy_(self.comm.params.to(torch.bfloat16))
+            shadow = self.comm.params_bf16[:P]
         torch.cuda.synchronize()
         dist.barrier(group)
-        # the model's tensors now alias the symmetric blocks
-        self.model.params, self.model.params_bf16 = self.comm.params, self.comm.params_bf16
+        # the model's tensors now alias the symmetric blocks (their unpadded prefix)
+        self.model.params, self.model.params_op = self.comm.params[:P], shadow
         if workers_per_rank == 1:
-            self.grads = [self.comm.grad]
+            self.grads = [self.comm.grad[:P]]
 
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
@@ -569,7 +603,7 @@ class DistributedTrainer(SimulatedTrainer):
             # replica 0 IS the symmetric parameter block the cross-rank average runs on
             Pm = self.model.P
             self._rep_p = [self.comm.params] + [self.comm.params.clone() for _ in range(self.n - 1)]
-            self._rep_pb = [self.comm.params_bf16] + [self.comm.params_bf16.clone() for _ in range(self.n - 1)]
+            self._rep_pb = [self.model.params_op] + [self.model.params_op.clone() for _ in range(self.n - 1)]
             self._rep_v = [torch.zeros(Pm, dtype=torch.float32, device=self.dev) for _ in range(self.n)]
             arr = lambda ts: (ctypes.c_void_p * self.n)(*[t.data_ptr() for t in ts])
             rep_ptrs = (arr(self._rep_p), arr(self._rep_v), arr(self._rep_pb))
@@ -611,8 +645,7 @@ class DistributedTrainer(SimulatedTrainer):
                 xs, ys = self.shard_x[w], self.shard_y[w]
                 if rows:
                     if self.kind == MODEL_MLP:
-                        st = _lib.lib().dbs_dev_gather_rows_f32_bf16(self.X.data_ptr(), idx.data_ptr(), rows,
-                                                                     self.row_elems, xs.data_ptr(), s_main)
+                        st = self._gather_mlp(idx, rows, xs, s_main)
                     else:
                         st = _lib.lib().dbs_dev_gather_rows(self.X.data_ptr(), idx.data_ptr(), rows,
                                                             self.row_bytes, xs.data_ptr(), s_main)
@@ -705,11 +738,14 @@ class DistributedTrainer(SimulatedTrainer):
             # the single averaging round of one-shot averaging (cluster.py:187-188)
             last = list(plans[-1].int_batches)
             b_loc = np.asarray(last[R * n_loc:(R + 1) * n_loc], dtype=np.int64)
-            _lib.check(_lib.lib().dbs_dev_average_replicas_f32(rep_ptrs[0], b_loc.ctypes.data_as(_lib.P_i64), n_loc,
-                                                               mode, self.model.P, rep_ptrs[2],
-                                                               int(self.agg.cuda_stream)), "average_replicas")
+            _lib.check(_lib.lib().dbs_dev_average_replicas_f32_ex(rep_ptrs[0], b_loc.ctypes.data_as(_lib.P_i64),
+                                                                  n_loc, mode, self.model.P, rep_ptrs[2],
+                                                                  self.precision, int(self.agg.cuda_stream)),
+                       "average_replicas")
             rb = np.asarray([sum(last[r * n_loc:(r + 1) * n_loc]) for r in range(self.world)], dtype=np.int64)
             self.comm.average_params(rb, mode=mode, stream=self.agg)
+            if self.precision == _lib.PREC_F32:
+                _lib.refresh_shadow(self.model.params, self.model.params_op, self.precision, stream=self.agg)
             torch.cuda.synchronize()
         return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
                          wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
@@ -737,11 +773,14 @@ class DistributedTrainer(SimulatedTrainer):
         self.comm.allreduce_sgd(rank_batches, 0.0, 0.0, mode=mode)
         # the model-averaging round's kernels too (identical parameters on every rank: no change)
         self.comm.average_params(rank_batches, mode=mode)
-        ptr1 = (ctypes.c_void_p * 1)(self.comm.params.data_ptr())
-        ptrb = (ctypes.c_void_p * 1)(self.comm.params_bf16.data_ptr())
+        ptr1 = (ctypes.c_void_p * 1)(self.model.params.data_ptr())
+        ptrb = (ctypes.c_void_p * 1)(self.model.params_op.data_ptr())
         one = np.ones(1, dtype=np.int64)
-        _lib.check(_lib.lib().dbs_dev_average_replicas_f32(ptr1, one.ctypes.data_as(_lib.P_i64), 1, mode, self.model.P,
-                                                           ptrb, _lib.stream_handle()), "average_replicas")
+        _lib.check(_lib.lib().dbs_dev_average_replicas_f32_ex(ptr1, one.ctypes.data_as(_lib.P_i64), 1, mode,
+                                                              self.model.P, ptrb, self.precision, _lib.stream_handle()),
+                   "average_replicas")
+        if self.precision == _lib.PREC_F32:
+            _lib.refresh_shadow(self.model.params, self.model.params_op, self.precision)
         torch.cuda.synchronize()
         self.comm.velocity.zero_()
         torch.distributed.barrier(self.group)

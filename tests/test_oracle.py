@@ -233,3 +233,28 @@ def test_theorem1_bound_formula():
         sgdlab.theorem1_bound(1, 2.0, 1.0, 1.0, 1.0)
     with _pt.raises(errors.ConfigurationError):
         sgdlab.theorem1_bound(1, 0.1, 1.0, -1.0, 1.0)
+
+
+def test_oracle_mlp_loop_pinned_to_reference_golden():
+    """oracle.run_parallel_sgd + oracle.MlpProblem (fp64, no emulation) reproduce
+    the reference's own run_parallel_sgd on the config-1 MLP
+    (tests/golden/mlp_trajectories.json, gen_mlp_golden.py): squared distances and
+    per-iteration losses to 1e-12 relative (same fp64 operations, BLAS order aside)."""
+    from conftest import load_golden
+    from oracle import oracle as O
+
+    for case in load_golden("mlp_trajectories.json")["cases"]:
+        rng = np.random.default_rng(case["data_seed"])
+        X = rng.standard_normal((case["D"], 784), dtype=np.float32)
+        y = rng.integers(0, 10, size=case["D"]).astype(np.int32)
+        x0 = O.mlp_init(seed=case["init_seed"]).astype(np.float64)
+        plans = case.get("plans") or case["fixed_batches"]
+        ref = O.run_parallel_sgd(O.MlpProblem(X, y), case["step"], case["iters"], case["momentum"],
+                                 case["aggregation"], case["seed"], case["n_workers"], plans, initial_point=x0,
+                                 record_loss=True)
+        want_sq = np.array([float.fromhex(v) for v in case["sq_norm"]])
+        want_loss = np.array([float.fromhex(v) for v in case["losses"]])
+        np.testing.assert_allclose(ref["squared_distances"], want_sq, rtol=1e-12)
+        np.testing.assert_allclose(ref["losses"], want_loss, rtol=1e-12)
+        disp = np.array([float.fromhex(v) for v in case["sq_disp"]])
+        assert disp[-1] > 0 and np.all(np.diff(disp[:5]) > 0)

@@ -139,8 +139,8 @@ def test_resnet50_forward_backward_vs_torch(dev, image, classes, B):
     from paper_2007_11831_b200 import resnet
 
     params = tame_residual_branches(resnet.init_params(classes, 1, depth=50, image=image), 0.1)
-    model = resnet.ResnetModel(classes, depth=50, image=image, params=params)
-    sc = resnet.ResnetScratch(B + 3, classes, depth=50, image=image)
+    model = resnet.ResnetModel(classes, depth=50, image=image, params=params, precision="bf16")
+    sc = resnet.ResnetScratch(B + 3, classes, depth=50, image=image, precision="bf16")
     X, y = resnet.synthetic_imagenet(B, image=image, classes=classes, seed=3)
     x = torch.as_tensor(X, device=dev)
     yl = torch.as_tensor(y, device=dev)
@@ -169,8 +169,9 @@ def test_resnet50_forward_backward_vs_torch(dev, image, classes, B):
     assert not bad, bad
 
 
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
 @pytest.mark.parametrize("graphs", [False, True])
-def test_resnet50_trainer_first_iteration(dev, graphs):
+def test_resnet50_trainer_first_iteration(dev, graphs, prec):
     """The epoch driver on uint8 ImageNet-shaped rows: each worker's first-iteration
     loss equals a direct forward/backward of the samples the reference's sample
     assignment gives it (start + default_rng(seed).permutation(span), sgdlab.py:372-374)."""
@@ -183,17 +184,17 @@ def test_resnet50_trainer_first_iteration(dev, graphs):
     image, classes, D = 64, 16, 80
     X, y = resnet.synthetic_imagenet(D, image=image, classes=classes, seed=5)
     tr = SimulatedTrainer(X, y, n_workers=2, model="resnet50", classes=classes, seed=0, partition=False,
-                          max_batch=16, graphs=graphs)
+                          max_batch=16, graphs=graphs, precision=prec)
     p0 = tr.model.params.clone()
     res = tr.run(cluster.StrategyConfig("fixed_ssgd", 16), n_epochs=1, max_iters=2, lr=0.05, momentum=0.9)
     torch.cuda.synchronize()
     assert np.all(np.isfinite(res.losses)) and len(res.losses) == 2
     plan = res.plans[0]
     rng = np.random.default_rng(0)
-    ref = resnet.ResnetModel(classes, depth=50, image=image)
+    ref = resnet.ResnetModel(classes, depth=50, image=image, precision=prec)
     ref.params.copy_(p0)
-    ref.params_bf16.copy_(p0.to(torch.bfloat16))
-    sc = resnet.ResnetScratch(16, classes, depth=50, image=image)
+    ref.refresh_shadow()
+    sc = resnet.ResnetScratch(16, classes, depth=50, image=image, precision=prec)
     for w, ((s, e), b) in enumerate(zip(plan.sample_spans, plan.int_batches)):
         idx = s + rng.permutation(e - s)[:b]
         x = torch.as_tensor(X[idx], device=dev)
@@ -260,8 +261,8 @@ def test_resnet50_tiny_variable_batches(dev, B):
 
     image, classes = 64, 16
     params = tame_residual_branches(resnet.init_params(classes, 1, depth=50, image=image), 0.1)
-    model = resnet.ResnetModel(classes, depth=50, image=image, params=params)
-    sc = resnet.ResnetScratch(8, classes, depth=50, image=image)
+    model = resnet.ResnetModel(classes, depth=50, image=image, params=params, precision="bf16")
+    sc = resnet.ResnetScratch(8, classes, depth=50, image=image, precision="bf16")
     X, y = resnet.synthetic_imagenet(B, image=image, classes=classes, seed=11)
     x = torch.as_tensor(X, device=dev)
     yl = torch.as_tensor(y, device=dev)

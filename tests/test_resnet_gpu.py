@@ -129,8 +129,8 @@ def test_resnet_forward_backward_vs_torch(dev):
     from paper_2007_11831_b200 import resnet
 
     B = 32
-    model = resnet.ResnetModel(seed=1)
-    sc = resnet.ResnetScratch(64)
+    model = resnet.ResnetModel(seed=1, precision="bf16")
+    sc = resnet.ResnetScratch(64, precision="bf16")
     X, y = resnet.synthetic_cifar(B, seed=3)
     x = torch.as_tensor(X, device=dev)
     yl = torch.as_tensor(y, device=dev)
@@ -190,8 +190,8 @@ def test_resnet18_tiny_variable_batches(dev, B):
 
     from paper_2007_11831_b200 import resnet
 
-    model = resnet.ResnetModel(seed=4)
-    sc = resnet.ResnetScratch(8)
+    model = resnet.ResnetModel(seed=4, precision="bf16")
+    sc = resnet.ResnetScratch(8, precision="bf16")
     X, y = resnet.synthetic_cifar(B, seed=9)
     x = torch.as_tensor(X, device=dev)
     yl = torch.as_tensor(y, device=dev)
