@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--report", default=None,
                     help="directory for the reference-format run reports (epoch CSV per strategy + run JSON)")
     ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet18_4w", "resnet18_ma", "resnet50", "resnet50_3w", "mlp", "allreduce"])
+    ap.add_argument("--precision", default="f32", choices=["f32", "bf16"],
+                    help="tensor-core arithmetic of the models: f32 = 3xTF32 on S32 operands (fp32 class, the "
+                         "headline), bf16 = bf16 operands")
+    ap.add_argument("--no-bf16", action="store_true", help="skip the labelled bf16 variant of the headline workload")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -145,9 +149,9 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 WL = {
     "resnet18": dict(D=50000, workers=3, per_worker=170, lr=0.05, mom=0.9, mult=2.0,
-                     desc="C3: ResNet-18 (CIFAR stem), synthetic CIFAR-10-shaped 50000x3x32x32 fp32 (bf16 tensor-core "
-                          "operands), 3 simulated workers = 3 disjoint 48-SM partitions (green contexts, 144 of the "
-                          "148 SMs) of the B200, B=510 (170/worker fixed), step = 1 epoch (98 iterations)"),
+                     desc="C3: ResNet-18 (CIFAR stem), synthetic CIFAR-10-shaped 50000x3x32x32 fp32, 3 simulated "
+                          "workers = 3 disjoint 48-SM partitions (green contexts, 144 of the 148 SMs) of the B200, "
+                          "B=510 (170/worker fixed), step = 1 epoch (98 iterations)"),
     "resnet18_4w": dict(D=50000, workers=4, per_worker=128, lr=0.05, mom=0.9, mult=2.0,
                         desc="C3 variant: ResNet-18 CIFAR, 4 simulated workers = 4 disjoint 32-SM partitions (128 of "
                              "148 SMs; partitions come in multiples of 8 SMs), B=512"),
@@ -163,7 +167,8 @@ WL = {
                           "classes, 4 simulated workers = 4 disjoint 32-SM partitions (green contexts) of the B200, "
                           "B=256 (64/worker fixed), step = 1 epoch (50 iterations)"),
     "mlp": dict(D=60000, workers=3, per_worker=128, lr=0.05, mom=0.5, mult=2.0,
-                desc="C1: MLP 784-256-10, synthetic MNIST 60000x784, 3 simulated workers, B=384, step = 1 epoch"),
+                desc="C1: MLP 784-256-10, synthetic MNIST 60000x784, 3 simulated workers sharing the GPU, B=384 "
+                     "(128/worker fixed), step = 1 epoch (156 iterations)"),
 }
 
 
@@ -191,38 +196,72 @@ def profiles(n, mult):
     return prof + [cluster.WorkerProfile(i, 1.0) for i in range(1, n)]
 
 
-def make_trainer(wl, rank, world=1):
+PRECISION_DESC = {
+    "f32": "fp32 class: 3xTF32 tcgen05 GEMMs on S32 (hi/lo tf32 split) operands, fp32 accumulation, fp32 "
+           "parameters / BN / gradients",
+    "bf16": "bf16 tensor-core operands, fp32 accumulation, fp32 master parameters",
+}
+
+
+def workload_config(wl, precision):
+    """The config dict both arms print (same workload, same disturbance)."""
+    w = WL[wl]
+    cfg = {"workload": w["desc"], "disturbance": disturbance_desc(wl), "lr": w["lr"], "momentum": w["mom"],
+           "parallelism": f"{w['workers']} simulated DP workers/GPU", "arithmetic": PRECISION_DESC[precision]}
+    return cfg
+
+
+def make_trainer(wl, rank, world=1, precision="f32"):
     import torch
 
     from paper_2007_11831_b200.trainer import DistributedTrainer, SimulatedTrainer
 
     w = WL[wl]
     if world > 1:
-        # one process per GPU: the same 4 SM-partition workers per GPU, the global
-        # plan spans 4 x world workers, gradients meet in the fused NVLink kernel
+        # one process per GPU: the same SM-partition workers per GPU, the global
+        # plan spans workers x world workers, gradients meet in the fused NVLink kernel
         model = "resnet50" if wl.startswith("resnet50") else ("resnet18" if wl.startswith("resnet18") else "mlp")
         tr = DistributedTrainer(w["D"], workers_per_rank=w["workers"], model=model, seed=0, partition=True,
                                 max_batch=w.get("max_batch", 3 * w["per_worker"]), classes=w.get("classes", 10),
-                                image=w.get("image", 224))
+                                image=w.get("image", 224), precision=precision)
         return tr, (None, None)
     if wl.startswith("resnet50"):
         from paper_2007_11831_b200.resnet import synthetic_imagenet
 
         X, y = synthetic_imagenet(w["D"], w["image"], w["classes"], seed=rank, device=torch.device("cuda"))
         tr = SimulatedTrainer(X, y, n_workers=w["workers"], model="resnet50", classes=w["classes"], seed=0,
-                              partition=True, max_batch=w["max_batch"])
+                              partition=True, max_batch=w["max_batch"], precision=precision)
         return tr, (X.cpu().numpy(), y.cpu().numpy())
     if wl.startswith("resnet18"):
         from paper_2007_11831_b200.resnet import synthetic_cifar
 
         X, y = synthetic_cifar(w["D"], seed=rank)
         return SimulatedTrainer(X, y, n_workers=w["workers"], model="resnet18", seed=0, partition=True,
-                                max_batch=w["workers"] * w["per_worker"]), (X, y)
+                                max_batch=w["workers"] * w["per_worker"], precision=precision), (X, y)
     from paper_2007_11831_b200.mlp import synthetic_mnist
 
     X, y = synthetic_mnist(w["D"], seed=rank)
-    return SimulatedTrainer(X, y, n_workers=w["workers"], model="mlp", seed=0,
-                            max_batch=w["workers"] * w["per_worker"]), (X, y)
+    tr = SimulatedTrainer(X, y, n_workers=w["workers"], model="mlp", seed=0,
+                          max_batch=w["workers"] * w["per_worker"], precision=precision)
+    calibrate_slow_device(tr, w)
+    return tr, (X, y)
+
+
+def calibrate_slow_device(tr, w):
+    """C1's workers share the GPU: the slow device is a timed spin of (m - 1) x b x the
+    per-sample time, measured here on one undisturbed fixed-plan epoch (the median
+    worker's compute seconds / (T b)), so the disturbed worker is m x slower per
+    sample whatever batch DBS assigns it (the reference's law, cluster.py:123-145)."""
+    from paper_2007_11831_b200 import cluster
+
+    cfg = cluster.StrategyConfig("fixed_ssgd", w["workers"] * w["per_worker"])
+    res = tr.run(cfg, n_epochs=2, lr=0.0, momentum=0.0, record_loss=False)
+    st = res.stats[-1]
+    iters = cluster.iterations_for_plan(st.plan)
+    per = sorted(t / (iters * b) for t, b in zip(st.per_worker_gpu, st.plan.int_batches))
+    tr.slow_per_sample_ns = per[len(per) // 2] * 1e9
+    tr.model.velocity.zero_()
+    tr._graph_cache.clear()
 
 
 def run_strategy(tr, wl, kind, args, world=1):
@@ -247,76 +286,104 @@ def run_strategy(tr, wl, kind, args, world=1):
             "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
-# measured tcgen05.mma (SS, bf16, M=128, K=16) throughput by N tile, as a share of the
-# tensor peak (scripts/mma_bench.cu -> profiles/mma_rate_r1.txt): a single-CTA MMA takes
-# >= ~83 cycles whatever N is (aligned operands), so only N = 256 reaches the peak
-MMA_SHAPE_CEILING = {64: 0.38, 128: 0.77, 256: 1.0}
-
 ROOFLINE_CONV = {
-    # workload -> (N, H, Cin, Cout, k, stride, description): the dominant conv shape
-    "resnet18": (128, 32, 64, 64, 3, 1, "gemm_bf16_kernel<64> implicit-GEMM conv3x3 64->64 @32x32, b=128 "
-                                        "(M=131072, N=64, K=576)"),
-    "resnet50": (64, 14, 256, 256, 3, 1, "gemm_bf16_kernel<256> implicit-GEMM (im2col TMA) conv3x3 256->256 @14x14, "
-                                         "b=64 (M=12544, N=256, K=2304; layer 3 carries the most FLOPs)"),
+    # workload -> (H, Cin, Cout, k, stride, description): the dominant conv shape
+    "resnet18": (32, 64, 64, 3, 1, "3x3 64->64 @32x32"),
+    "resnet50": (14, 256, 256, 3, 1, "3x3 256->256 @14x14 (layer 3 carries the most FLOPs)"),
 }
 
 
-def kernel_roofline(peaks, wl="resnet18"):
-    """Dominant kernel: the tcgen05 implicit-GEMM convolution of the workload's
-    most expensive conv shape (ResNet-18: the 64-channel 3x3 stage, 64->64 at
-    32x32, b=128 per worker; ResNet-50: the layer-3 3x3, 256->256 at 14x14, b=64).
-    200 launches captured in a CUDA graph, timed with CUDA events on the
-    capturing stream."""
+def kernel_roofline(peaks, wl, precision, tr=None):
+    """Dominant kernel: the tcgen05 implicit-GEMM convolution of the workload's most
+    expensive conv shape, timed where the bench runs it -- inside worker 0's SM
+    partition (green context; its SM count sizes the persistent grid) at the
+    workload's per-worker batch -- with 100 launches on the partition's stream
+    between CUDA events.  Peak: the measured bf16 dense rate, divided by 6 for the
+    fp32-class kernel (kind::tf32 runs at half the bf16 rate and 3xTF32 issues
+    three MMAs per product), scaled by the partition's share of the SMs."""
+    import ctypes
+
     import torch
 
     from paper_2007_11831_b200 import _lib
 
-    N, H, C, Co, k, stride, desc = ROOFLINE_CONV["resnet50" if wl.startswith("resnet50") else "resnet18"]
+    w = WL[wl]
+    key = "resnet50" if wl.startswith("resnet50") else "resnet18"
+    H, C, Co, k, stride, desc = ROOFLINE_CONV[key]
+    N = w["per_worker"]
     pad = k // 2
     OH = (H + 2 * pad - k) // stride + 1
-    x = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
-    w = (torch.randn(Co, k, k, C, device="cuda") / (k * k * C) ** 0.5).to(torch.bfloat16)
-    y = torch.empty(N, OH, OH, Co, dtype=torch.bfloat16, device="cuda")
+    f32 = precision == "f32"
     L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(N * H * H, C, device="cuda", generator=g)
+    wt = torch.randn(Co, k * k * C, device="cuda", generator=g) / (k * k * C) ** 0.5
+    if f32:
+        def s32(t):
+            o = torch.empty(t.shape[0], 2 * t.shape[1], device="cuda")
+            assert L.dbs_dev_split_s32(t.data_ptr(), t.shape[0], t.shape[1], t.shape[1], o.data_ptr(), t.shape[1],
+                                       _lib.stream_handle()) == 0, _lib.last_error()
+            return o
 
-    def launch(s):
-        st = L.dbs_dev_conv2d_fwd(x.data_ptr(), N, H, H, C, w.data_ptr(), Co, k, stride, pad, y.data_ptr(), s)
-        assert st == 0, _lib.last_error()
+        xs, ws = s32(x), s32(wt)
+        y = torch.empty(N * OH * OH, Co, device="cuda")
+        fn = L.dbs_dev_conv2d_fwd_s32
+    else:
+        xs, ws = x.to(torch.bfloat16), wt.to(torch.bfloat16)
+        y = torch.empty(N * OH * OH, Co, dtype=torch.bfloat16, device="cuda")
+        fn = L.dbs_dev_conv2d_fwd
+    wk = tr.workers[0] if tr is not None and tr.workers and tr.workers[0].ctx else None
+    ctx = wk.ctx if wk else None
+    stream = wk.stream if wk else torch.cuda.Stream()
+    sms = wk.sm_count if wk else torch.cuda.get_device_properties(0).multi_processor_count
+    torch.cuda.synchronize()
+    if ctx:
+        _lib.check(L.dbs_partition_push(ctx), "partition_push")
+    try:
+        h = int(stream.cuda_stream)
 
-    for _ in range(10):
-        launch(_lib.stream_handle())
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    cs = torch.cuda.Stream()
-    with torch.cuda.graph(g, stream=cs):
-        for _ in range(200):
-            launch(int(cs.cuda_stream))
-    g.replay()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(cs):
-        e0.record(cs)
-        g.replay()
-        e1.record(cs)
-    torch.cuda.synchronize()
-    dur = e0.elapsed_time(e1) / 1e3 / 200
+        def launch():
+            st = fn(xs.data_ptr(), N, H, H, C, ws.data_ptr(), Co, k, stride, pad, y.data_ptr(), h)
+            assert st == 0, _lib.last_error()
+
+        for _ in range(10):
+            launch()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 100
+        e0.record(stream)
+        for _ in range(reps):
+            launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    finally:
+        if ctx:
+            _lib.check(L.dbs_partition_pop(ctx), "partition_pop")
+    dur = e0.elapsed_time(e1) / 1e3 / reps
     flops = 2.0 * N * OH * OH * Co * k * k * C
     achieved = flops / dur / 1e12
-    peak = peaks["bf16_tflops"]
+    share = sms / torch.cuda.get_device_properties(0).multi_processor_count
+    peak_full = peaks["bf16_tflops"] / (6.0 if f32 else 1.0)
+    peak = peak_full * share
     traffic = None
-    tf = ROOT / "profiles" / "ncu_traffic_r1.json"
+    tf = ROOT / "profiles" / "ncu_traffic_r2.json"
     if tf.exists():
-        rec = json.loads(tf.read_text()).get("resnet50" if wl.startswith("resnet50") else "resnet18")
+        rec = json.loads(tf.read_text()).get(f"{key}_{precision}")
         if rec:
             traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
-    n_tile = 64 if Co <= 64 else (128 if Co <= 128 else 256)
-    ceiling = MMA_SHAPE_CEILING[n_tile]
-    return {"bound": "tensor", "kernel": desc,
-            "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-            "mma_shape_ceiling_frac": ceiling, "frac_of_shape_ceiling": round(achieved / peak / ceiling, 4),
-            "traffic": traffic, "traffic_unit": "bytes per launch (ncu, profiles/ncu_traffic_r1.json)",
-            "algorithmic_bytes_per_launch": 2.0 * (N * H * H * C + N * OH * OH * Co + Co * k * k * C),
-            "avg_launch_us": round(dur * 1e6, 2), "algorithmic_flops_per_launch": flops,
+    kname = "gemm_bf16_kernel<64, false, true> (3xTF32)" if f32 else "gemm_bf16_kernel<64, true> (halo)"
+    return {"bound": "tensor", "kernel": f"{kname} implicit-GEMM conv {desc}, b={N} per worker, inside a "
+                                         f"{sms}-SM partition",
+            "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_unit": "bytes per launch (ncu --set full, profiles/ncu_traffic_r2.json)",
+            "algorithmic_flops_per_launch": flops,
+            "algorithmic_bytes_per_launch": (8.0 if f32 else 2.0) * (N * H * H * C + Co * k * k * C) +
+                                            (4.0 if f32 else 2.0) * N * OH * OH * Co,
+            "avg_launch_us": round(dur * 1e6, 2), "partition_sms": sms,
+            "peak_note": (f"measured bf16 {peaks['bf16_tflops']} TF/s / 6 (tf32 at half the bf16 rate, 3 MMAs per "
+                          f"fp32-class product) x {sms}/148 SMs" if f32 else
+                          f"measured bf16 {peaks['bf16_tflops']} TF/s x {sms}/148 SMs"),
+            "tensor_issue_frac": round(achieved * (6.0 if f32 else 1.0) / (peaks["bf16_tflops"] * share), 4),
             "peak_source": peaks["source"]}
 
 
@@ -350,8 +417,9 @@ def aux_rooflines(tr, peaks):
     """HBM rooflines of the two other hot-path kernels, on the workload's own
     buffers: the repartition gather (gather.cu; 2 * row_bytes + 8 B per row:
     every dataset row to a shard in a random order) and the fused batch-weighted
-    aggregate + momentum SGD of the simulated workers (sgd.cu; (4n + 4 * 4 + 2) B
-    per parameter: n gradients, x and v read, x, v and the bf16 shadow written)."""
+    aggregate + momentum SGD of the simulated workers (sgd.cu; (4n + 4 * 4 + s) B
+    per parameter: n gradients, x and v read, x, v and the operand shadow written,
+    s = 8 for the S32 shadow of the fp32 class, 2 for bf16)."""
     import ctypes
 
     import torch
@@ -378,14 +446,15 @@ def aux_rooflines(tr, peaks):
     b = np.asarray([37 + 36 * (i % 2) for i in range(n)], dtype=np.int64)
     x = tr.model.params.clone()
     v = torch.zeros_like(x)
-    xb = tr.model.params_bf16.clone()
+    xb = tr.model.params_op.clone()
+    sh_bytes = 8.0 if tr.precision == _lib.PREC_F32 else 2.0  # S32 / bf16 operand shadow written per parameter
 
     def agg(st):
-        assert L.dbs_dev_aggregate_sgd_f32(ptrs, b.ctypes.data_as(_lib.P_i64), n, 1, P, 0.0, 0.9, x.data_ptr(),
-                                           v.data_ptr(), xb.data_ptr(), st) == 0, _lib.last_error()
+        assert L.dbs_dev_aggregate_sgd_f32_ex(ptrs, b.ctypes.data_as(_lib.P_i64), n, 1, P, 0.0, 0.9, x.data_ptr(),
+                                              v.data_ptr(), xb.data_ptr(), tr.precision, st) == 0, _lib.last_error()
 
     t = _graph_time(agg, 20)
-    byt = (4.0 * n + 16.0 + 2.0) * P
+    byt = (4.0 * n + 16.0 + sh_bytes) * P
     out["aggregate_sgd"] = {"bound": "hbm", "achieved": round(byt / t / 1e9, 1), "peak": peaks["hbm_gbs"],
                             "unit": "GB/s", "frac": round(byt / t / 1e9 / peaks["hbm_gbs"], 4),
                             "bytes_per_launch": byt, "avg_launch_us": round(t * 1e6, 2),
@@ -405,33 +474,73 @@ def disturbance_desc(wl):
     return f"worker 0 on a {w['mult']}x slower device (proportional spin)"
 
 
-def cpu_baseline(wl, X, y, threads=None):
-    """The reference loop (sgdlab.py:380-391) with a CPU model on the host cores:
-    a bounded sample (one synchronous iteration of all workers)."""
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_iteration_seconds(wl, X, y, threads, k=3):
+    """Best of k timed samples of the reference loop (sgdlab.py:380-391) with a CPU
+    model on `threads` host threads (torch intra-op threads for the PyTorch-CPU
+    ResNet, BLAS threads via threadpoolctl for the numpy MLP).  Imports only the
+    oracle (test infrastructure) -- never the product package."""
+    from threadpoolctl import threadpool_limits
+
     from oracle import oracle as O
 
     w = WL[wl]
     batches = [w.get("cpu_per_worker", w["per_worker"])] * w["workers"]
-    if wl.startswith("resnet"):
-        from paper_2007_11831_b200.resnet import init_params
+    ts = []
+    with threadpool_limits(limits=threads):
+        if wl.startswith("resnet"):
+            import torch
 
-        depth = 50 if wl.startswith("resnet50") else 18
-        tens = (init_params(w["classes"], 0, depth=50, image=w["image"]) if depth == 50 else init_params(seed=0))
-        sec = O.cpu_resnet_iteration_seconds(tens, X[:sum(batches)], y[:sum(batches)], batches, threads=threads,
-                                             depth=depth)
-        sample = (f"1 iteration x {w['workers']} workers x {batches[0]} samples, ResNet-{depth} fwd+bwd on "
-                  "PyTorch-CPU inside the restated run_parallel_sgd loop (fp32)")
-    else:
-        prob = O.MlpProblem(X, y)
-        p0 = O.mlp_init().astype(np.float64)
-        t0 = time.perf_counter()
-        O.run_parallel_sgd(prob, w["lr"], 6, w["mom"], "batch_weighted", 0, w["workers"], batches, initial_point=p0)
-        sec = (time.perf_counter() - t0) / 6
-        sample = "6 iterations of the numpy float64 oracle (MLP Problem)"
-    import torch
+            torch.set_num_threads(threads)
+            depth = 50 if wl.startswith("resnet50") else 18
+            tens = O.resnet_init(w.get("classes", 10), 0, depth)
+            for _ in range(k):
+                ts.append(O.cpu_resnet_iteration_seconds(tens, X[:sum(batches)], y[:sum(batches)], batches,
+                                                         threads=threads, depth=depth))
+            sample = (f"best of {k}: 1 synchronous iteration x {w['workers']} workers x {batches[0]} samples, "
+                      f"ResNet-{depth} fwd+bwd on PyTorch-CPU (fp32) inside the restated run_parallel_sgd loop")
+        else:
+            prob = O.MlpProblem(X, y)
+            p0 = O.mlp_init().astype(np.float64)
+            for _ in range(k):
+                t0 = time.perf_counter()
+                O.run_parallel_sgd(prob, w["lr"], 4, w["mom"], "batch_weighted", 0, w["workers"], batches,
+                                   initial_point=p0)
+                ts.append((time.perf_counter() - t0) / 4)
+            sample = f"best of {k}: 4 iterations of the numpy float64 oracle loop (MLP Problem, 3 x 128 samples)"
+    return sum(batches) / min(ts), sample
 
-    return {"value": sum(batches) / sec, "unit": "samples/s", "cores": threads or torch.get_num_threads(),
-            "kind": "port", "sample": sample}
+
+def cpu_inputs(wl):
+    """The workload's inputs from the oracle's generators (identical to the package's)."""
+    from oracle import oracle as O
+
+    w = WL[wl]
+    if wl.startswith("resnet18"):
+        return O.synthetic_cifar(w["workers"] * w["per_worker"], seed=0)
+    if wl.startswith("resnet50"):
+        return O.synthetic_imagenet(w["workers"] * w["cpu_per_worker"], w["image"], w["classes"], seed=0)
+    return O.synthetic_mnist(w["D"], seed=0)
+
+
+def cpu_baseline(wl, threads=None):
+    """The reported CPU baseline (BASELINE.md CPU plan): all host cores, plus the
+    single-thread figure."""
+    cores = host_cores()
+    X, y = cpu_inputs(wl)
+    val, sample = cpu_iteration_seconds(wl, X, y, threads or cores)
+    one, _ = cpu_iteration_seconds(wl, X, y, 1, k=2)
+    return {"value": round(val, 2), "unit": "samples/s", "cores": threads or cores, "kind": "port",
+            "sample": sample, "single_thread": round(one, 2),
+            "env": {"OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+                    "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+                    "thread_limits": "threadpoolctl / torch.set_num_threads per measurement"}}
 
 
 def e2e_run(tr, wl, X, y, args, world=1):
@@ -522,33 +631,21 @@ def reference_arm_allreduce(args, world):
 
 
 def reference_arm(args):
+    """The reference's CPU implementation of the path on the host cores (the oracle
+    port of run_parallel_sgd with a CPU model), on the same workload / config as
+    our arm.  Imports only the oracle: no product code, no product .so."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     wl = args.workload
     if wl == "allreduce":
         return reference_arm_allreduce(args, world)
-    w = WL[wl]
-    if wl.startswith("resnet18"):
-        from paper_2007_11831_b200.resnet import synthetic_cifar
-
-        X, y = synthetic_cifar(w["workers"] * w["per_worker"], seed=0)
-    elif wl.startswith("resnet50"):
-        from paper_2007_11831_b200.resnet import synthetic_imagenet
-
-        X, y = synthetic_imagenet(w["workers"] * w["cpu_per_worker"], w["image"], w["classes"], seed=0)
-    else:
-        from paper_2007_11831_b200.mlp import synthetic_mnist
-
-        X, y = synthetic_mnist(w["D"], seed=0)
-    vals = [cpu_baseline(wl, X, y, threads=os.cpu_count()) for _ in range(max(1, min(args.steps, 2)))]
-    base = vals[-1]
-    out = {"impl": "reference", "metric": METRIC, "value": round(base["value"], 2), "unit": "samples/s",
+    base = cpu_baseline(wl)
+    out = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "samples/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
            "dtype": "f32" if wl.startswith("resnet") else "f64", "data": "synthetic",
-           "config": {"workload": w["desc"]}, "cpu_baseline": base,
-           "e2e": {"value": round(base["value"], 2), "unit": "samples/s", "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0}}
+           "config": workload_config(wl, args.precision), "cpu_baseline": base,
+           "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
@@ -662,7 +759,7 @@ def main():
     peaks = load_peaks()
     wl = args.workload
     w = WL[wl]
-    tr, (X, y) = make_trainer(wl, rank, world)
+    tr, (X, y) = make_trainer(wl, rank, world, args.precision)
     if world > 1:
         dist.barrier()
     # (multi-GPU: the trainer's timed seconds are already the max over ranks and
@@ -680,11 +777,32 @@ def main():
         for r in reps:
             rpt.write_epoch_csv(r, out / f"{r.scenario_name}_{r.strategy}.csv")
         rpt.write_run_json(reps, [], out / f"bench_{wl}_n{world}.json")
-    roof = kernel_roofline(peaks, wl)
+    roof = kernel_roofline(peaks, wl, args.precision, tr) if wl in ("resnet18", "resnet18_4w", "resnet18_ma", "resnet50",
+                                                                   "resnet50_3w") else None
     aux = aux_rooflines(tr, peaks) if world == 1 else None
     e2e = None if args.no_e2e else e2e_run(tr, wl, X, y, args, world)
-    cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl, X, y)
     gaps = [np.mean(s.per_worker_wait) / max(s.per_worker_gpu) for s in fixed["stats"]]
+    cfg = workload_config(wl, args.precision)
+    cfg["l2"] = (f"inputs > L2: {tr.X.numel() * tr.X.element_size() / 1e6:.0f} MB dataset repacked into per-worker "
+                 "shards every epoch")
+    if getattr(tr, "slow_per_sample_ns", None):
+        cfg["slow_device"] = (f"timed spin (m - 1) x b x {tr.slow_per_sample_ns:.0f} ns per iteration on the "
+                              "disturbed worker's stream (per-sample time calibrated on an undisturbed epoch)")
+    variant = None
+    if world == 1 and not args.no_bf16 and args.precision == "f32":
+        # the same workload with bf16 tensor-core operands: a labelled variant, not the headline
+        del tr
+        torch.cuda.empty_cache()
+        trb, _ = make_trainer(wl, rank, world, "bf16")
+        rb = {k: run_strategy(trb, wl, k, args, world) for k in ("fixed_ssgd", "dbs")}
+        variant = {"dtype": "bf16", "arithmetic": PRECISION_DESC["bf16"],
+                   "value": round(rb["dbs"]["samples_per_s"], 1),
+                   "fixed_samples_per_s": round(rb["fixed_ssgd"]["samples_per_s"], 1),
+                   "dbs_vs_fixed_speedup": round(rb["dbs"]["samples_per_s"] / rb["fixed_ssgd"]["samples_per_s"], 4),
+                   "ms_per_step": round(rb["dbs"]["epoch_s"] * 1e3, 3)}
+        del trb
+        torch.cuda.empty_cache()
+    cpu = None if (args.no_cpu or world > 1) else cpu_baseline(wl)
     out = {
         "metric": METRIC,
         "value": round(dbs["samples_per_s"], 1),
@@ -696,15 +814,12 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "bf16",
+        "dtype": args.precision,
         "data": "synthetic",
-        "config": {"workload": w["desc"],
-                   "disturbance": disturbance_desc(wl),
-                   "l2": (f"inputs > L2: {tr.X.numel() * tr.X.element_size() / 1e6:.0f} MB dataset repacked into "
-                          "per-worker shards every epoch"),
-                   "lr": w["lr"], "momentum": w["mom"], "parallelism": f"{w['workers']} simulated DP workers/GPU"},
+        "config": cfg,
         "fixed": {"samples_per_s": round(fixed["samples_per_s"], 1), "ms_per_epoch": round(fixed["epoch_s"] * 1e3, 3)},
         "dbs_vs_fixed_speedup": round(dbs["samples_per_s"] / fixed["samples_per_s"], 4),
+        "dbs_saving": round(1.0 - fixed["samples_per_s"] / dbs["samples_per_s"], 4),
         "utilisation_gap_fixed": round(float(np.mean(gaps)), 4),
         "final_plan": list(dbs["stats"][-1].plan.int_batches),
         "per_worker_gpu_s_last_epoch": {"fixed": [round(v, 4) for v in fixed["stats"][-1].per_worker_gpu],
@@ -713,6 +828,7 @@ def main():
         "kernel_rooflines": aux,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "bf16_variant": variant,
         "clocks": dbs["clocks"],
         "gpu_launches": int(dbs["launches"]),
     }

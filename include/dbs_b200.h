@@ -435,6 +435,9 @@ typedef struct {
 typedef struct dbs_partition dbs_partition;
 int dbs_partition_create(int32_t n_groups, int32_t sms_per_group, dbs_partition** out, int32_t* actual_sms);
 int dbs_partition_get(const dbs_partition* p, int32_t group, void** ctx, void** stream, void** side_stream);
+/* make a partition's context current on this thread / restore the previous one */
+int dbs_partition_push(void* ctx);
+int dbs_partition_pop(void* ctx);
 /* dbs_dev_spin_until launched inside a partition's context (ctx may be NULL). */
 int dbs_dev_spin_until_ctx(int32_t num_ctas, const volatile int32_t* d_stop, void* stream, void* ctx);
 

@@ -622,3 +622,73 @@ def cpu_resnet_iteration_seconds(tensors, X, y, batches, lr=0.05, momentum=0.9, 
             vel[k].mul_(momentum).add_(g)
             p.sub_(lr * vel[k])
     return time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+# Workload inputs for bench.py's CPU legs (the reference arm must not touch the
+# product package): the same numpy generators and torchvision-order
+# initialisation as paper_2007_11831_b200.{mlp,resnet} (same draws, same order)
+# ---------------------------------------------------------------------------
+
+def synthetic_mnist(n_samples=60000, in_dim=784, classes=10, seed=0):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n_samples, in_dim), dtype=np.float32)
+    y = rng.integers(0, classes, size=n_samples).astype(np.int32)
+    return X, y
+
+
+def synthetic_cifar(n_samples=50000, classes=10, seed=0):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n_samples, 3, 32, 32), dtype=np.float32)
+    y = rng.integers(0, classes, size=n_samples).astype(np.int32)
+    return X, y
+
+
+def synthetic_imagenet(n_samples=20000, image=224, classes=1000, seed=0):
+    rng = np.random.default_rng(seed)
+    X = rng.integers(0, 256, size=(n_samples, 3, image, image), dtype=np.uint8)
+    y = rng.integers(0, classes, size=n_samples).astype(np.int32)
+    return X, y
+
+
+def resnet_shapes(classes=10, depth=18):
+    """(kind, torch shape) of every parameter tensor in torchvision order
+    (kind 0 conv weight, 1 BN gamma, 2 BN beta, 3 FC weight, 4 FC bias)."""
+    if depth == 18:
+        convs, cin = [(3, 64, 3)], 64
+        for L, w in enumerate((64, 128, 256, 512)):
+            for b in range(2):
+                stride = 2 if (L > 0 and b == 0) else 1
+                convs += [(cin, w, 3), (w, w, 3)] + ([(cin, w, 1)] if (stride != 1 or cin != w) else [])
+                cin = w
+    else:
+        convs, cin = [(3, 64, 7)], 64
+        for L, (w, n) in enumerate(zip((64, 128, 256, 512), (3, 4, 6, 3))):
+            for b in range(n):
+                stride = 2 if (L > 0 and b == 0) else 1
+                convs += [(cin, w, 1), (w, w, 3), (w, 4 * w, 1)]
+                convs += [(cin, 4 * w, 1)] if (stride != 1 or cin != 4 * w) else []
+                cin = 4 * w
+    out = []
+    for ci, co, k in convs:
+        out += [(0, (co, ci, k, k)), (1, (co,)), (2, (co,))]
+    return out + [(3, (classes, cin)), (4, (classes,))]
+
+
+def resnet_init(classes=10, seed=0, depth=18):
+    """Kaiming-normal fan-out convolutions, BN (1, 0), uniform classifier."""
+    rng = np.random.default_rng(seed)
+    shapes = resnet_shapes(classes, depth)
+    feat = shapes[-2][1][1]
+    out = []
+    for kind, shp in shapes:
+        if kind == 0:
+            out.append(rng.normal(0.0, math.sqrt(2.0 / (shp[0] * shp[2] * shp[3])), shp).astype(np.float32))
+        elif kind == 1:
+            out.append(np.ones(shp, dtype=np.float32))
+        elif kind == 2:
+            out.append(np.zeros(shp, dtype=np.float32))
+        else:
+            bound = 1.0 / math.sqrt(feat)
+            out.append(rng.uniform(-bound, bound, shp).astype(np.float32))
+    return out

@@ -166,6 +166,8 @@ SIGNATURES = {
     "dbs_dev_spin_until_ctx": (c_i32, [c_i32, c_vp, c_vp, c_vp]),
     "dbs_partition_create": (c_i32, [c_i32, c_i32, ctypes.POINTER(c_vp), P_i32]),
     "dbs_partition_get": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    "dbs_partition_push": (c_i32, [c_vp]),
+    "dbs_partition_pop": (c_i32, [c_vp]),
     "dbs_dev_spin_for": (c_i32, [c_i32, c_i64, c_vp]),
     "dbs_dev_stamp": (c_i32, [c_vp, c_i64, c_vp]),
     "dbs_dev_set_flag": (c_i32, [c_vp, c_i32, c_vp]),

@@ -158,3 +158,9 @@ extern "C" int dbs_partition_get(const dbs_partition* p, int32_t group, void** c
   if (side_stream) *side_stream = p->side[group];
   return DBS_OK;
 }
+
+// Make a partition's context current on the calling thread (and restore the previous
+// one): host code that launches library kernels into that partition between the two
+// calls -- e.g. a per-kernel measurement inside a worker's SM set.
+extern "C" int dbs_partition_push(void* ctx) { return dbs::ctx_push(ctx); }
+extern "C" int dbs_partition_pop(void* ctx) { return dbs::ctx_pop(ctx); }

@@ -163,6 +163,9 @@ class SimulatedTrainer:
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
         self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
+        # shared-GPU slow devices: per-sample ns of the batch-proportional spin (None: a
+        # spin proportional to the worker's own measured forward/backward time)
+        self.slow_per_sample_ns: Optional[float] = None
         self.max_batch = max_batch
         self.scratch = {}
         P = self.model.P
@@ -406,6 +409,14 @@ class SimulatedTrainer:
                             ctas = max(0, min(ctas, wk.sm_count - 1))
                             if ctas:
                                 spinning.append((wk, ctas))
+                        elif self.slow_per_sample_ns:
+                            # a device m x slower per sample (the reference's timing law:
+                            # effective_cost x b per iteration, cluster.py:123-145): a timed
+                            # spin of (m - 1) x b x the calibrated per-sample time on the
+                            # worker's stream -- proportional to the batch DBS assigns it
+                            slots[w].spin_ns = int((ev.cost_multiplier - 1.0) * batches[w] * self.slow_per_sample_ns)
+                            slots[w].spin_ctas = 2
+                            spin_key.append((w, slots[w].spin_ns))
                         else:
                             # simulated workers share the GPU's SMs: the slow worker's
                             # device is emulated as m x its own forward/backward time

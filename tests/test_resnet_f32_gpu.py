@@ -243,3 +243,17 @@ def test_resnet18_f32_running_stats(dev):
     mean, var = sc.running_stats(0)
     np.testing.assert_allclose(mean, bn.running_mean.cpu().numpy(), rtol=1e-4, atol=1e-6)
     np.testing.assert_allclose(var, bn.running_var.cpu().numpy(), rtol=1e-4, atol=1e-6)
+
+
+def test_bench_cpu_inputs_match_package(dev):
+    """bench.py's reference arm builds its inputs from the oracle (no product import):
+    they must be the package's exact data / initialisation."""
+    from oracle import oracle as O
+    from paper_2007_11831_b200 import mlp, resnet
+
+    for depth, image, classes in ((18, 32, 10), (50, 224, 1000)):
+        a, b = O.resnet_init(classes, 3, depth), resnet.init_params(classes, 3, depth=depth, image=image)
+        assert len(a) == len(b) and all(np.array_equal(x, y) for x, y in zip(a, b))
+    for f, g, args in ((O.synthetic_cifar, resnet.synthetic_cifar, (10,)), (O.synthetic_mnist, mlp.synthetic_mnist, (10,)),
+                       (O.synthetic_imagenet, resnet.synthetic_imagenet, (3, 64, 10))):
+        assert all(np.array_equal(x, y) for x, y in zip(f(*args, seed=2), g(*args, seed=2)))
