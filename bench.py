@@ -286,6 +286,8 @@ def run_strategy(tr, wl, kind, args, world=1):
             "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
+TF32_DENSE_TFLOPS = 1100.0  # B200 dense tf32 tensor rate, B200_PROFILING.md (no measured tf32 figure)
+
 ROOFLINE_CONV = {
     # workload -> (H, Cin, Cout, k, stride, description): the dominant conv shape
     "resnet18": (32, 64, 64, 3, 1, "3x3 64->64 @32x32"),
@@ -362,7 +364,10 @@ def kernel_roofline(peaks, wl, precision, tr=None):
     flops = 2.0 * N * OH * OH * Co * k * k * C
     achieved = flops / dur / 1e12
     share = sms / torch.cuda.get_device_properties(0).multi_processor_count
-    peak_full = peaks["bf16_tflops"] / (6.0 if f32 else 1.0)
+    # fp32 class: 3 kind::tf32 MMAs per product at the tf32 dense rate (no measured tf32 peak in
+    # MEASURED_PEAKS.json: B200_PROFILING.md's 1.1 PFLOP/s dense tf32, which the 256-/512-channel
+    # convs of this kernel reach ~0.8 of); bf16: the measured dense bf16 rate
+    peak_full = TF32_DENSE_TFLOPS / 3.0 if f32 else peaks["bf16_tflops"]
     peak = peak_full * share
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic_r2.json"
@@ -380,11 +385,10 @@ def kernel_roofline(peaks, wl, precision, tr=None):
             "algorithmic_bytes_per_launch": (8.0 if f32 else 2.0) * (N * H * H * C + Co * k * k * C) +
                                             (4.0 if f32 else 2.0) * N * OH * OH * Co,
             "avg_launch_us": round(dur * 1e6, 2), "partition_sms": sms,
-            "peak_note": (f"measured bf16 {peaks['bf16_tflops']} TF/s / 6 (tf32 at half the bf16 rate, 3 MMAs per "
-                          f"fp32-class product) x {sms}/148 SMs" if f32 else
+            "peak_note": (f"tf32 dense {TF32_DENSE_TFLOPS:.0f} TF/s (B200_PROFILING.md) / 3 MMAs per fp32-class "
+                          f"product x {sms}/148 SMs" if f32 else
                           f"measured bf16 {peaks['bf16_tflops']} TF/s x {sms}/148 SMs"),
-            "tensor_issue_frac": round(achieved * (6.0 if f32 else 1.0) / (peaks["bf16_tflops"] * share), 4),
-            "peak_source": peaks["source"]}
+            "peak_source": "B200_PROFILING.md fallback (tf32)" if f32 else peaks["source"]}
 
 
 def _graph_time(launch, reps=20):

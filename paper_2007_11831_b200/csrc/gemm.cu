@@ -154,13 +154,16 @@ struct CfgTf {
   static constexpr uint32_t kABytes = 2 * kBM * 128;  // 32 KB: [hi | lo] x 128 rows x 128 B
   static constexpr uint32_t kBBytes = 2 * BN * 128;
   static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;
-  // per tile buffer (kMains) main accumulators (hi*hi, round-robin over logical
-  // k-blocks) + 1 correction accumulator (hi*lo + lo*hi): double-buffered 256 TMEM
-  // columns (BN <= 64: 3 / 7 mains), or one buffer of 512 for BN = 128 (3 mains; no
-  // epilogue / MMA overlap, but a 3x-MMA S32 tile spends far longer in the MMA)
-  static constexpr int kNumBuf = kAccCols >= 128 ? 1 : 2;
+  // TMEM per tile buffer: kMains accumulator PAIRS [main | correction] of 2 BN columns
+  // (round-robin over the logical k-blocks).  One N = 2 BN MMA A_hi x [B_hi | B_lo]
+  // writes main (hi*hi) and correction (hi*lo) side by side; an N = BN MMA A_lo x B_hi
+  // adds lo*hi to the correction.  Double-buffered 256 columns for BN <= 64 (2 / 4
+  // pairs), one buffer of 512 for BN = 128 (2 pairs; no epilogue / MMA overlap, but an
+  // S32 tile spends far longer in the MMA than in the epilogue).
+  static constexpr uint32_t kPairCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kNumBuf = BN >= 128 ? 1 : 2;
   static constexpr uint32_t kBufCols = 512 / kNumBuf;
-  static constexpr int kMains = (int)(kBufCols / kAccCols) - 1;
+  static constexpr int kMains = (int)(kBufCols / kPairCols) > 4 ? 4 : (int)(kBufCols / kPairCols);
   static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;
   static constexpr int kRing = (int)((212u * 1024u - kEpiBytes) / (kABytes + kBBytes));
   static constexpr int kStages = kRing > 8 ? 8 : kRing;
@@ -878,20 +881,51 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
       b_r = rs / p.gb.S;
       b_s = rs - b_r * p.gb.S;
     }
-    const bool k_pix = (bm == 2 || bm == 4);
+    const bool k_pix = (bm == 2 || bm == 4 || am >= 5);
+    const ConvGeom& gk = am >= 5 ? p.ga : p.gb;  // geometry of the pixel-indexed K
     PixelCursor pc{};
-    if (k_pix) pc.init(p.gb, (int64_t)kb_begin * 32, 32);
+    if (k_pix) pc.init(gk, (int64_t)kb_begin * 32, 32);
     const bool tap_k = (am == 2 || am == 4 || bm == 3);
     TapCursor tc{};
     if (tap_k) tc.init(p.ga, kb_begin);
+    // transposed weight gradient (A = the conv input, MN-major over M = (r, s, c)): the
+    // tile's 32-row groups are fixed (tap, channel group)s; groups past M are skipped
+    int at_r[4] = {0, 0, 0, 0}, at_s[4] = {0, 0, 0, 0}, at_c[4] = {0, 0, 0, 0};
+    int a_groups = 4;
+    if (am >= 5) {
+      a_groups = (int)min((int64_t)4, (p.M - m0 + 31) / 32);
+#pragma unroll
+      for (int gq = 0; gq < 4; gq++) {
+        const int mg = (int)m0 + 32 * gq;
+        const int rs = mg / p.ga.Cin;
+        at_c[gq] = mg - rs * p.ga.Cin;
+        at_r[gq] = rs / p.ga.S;
+        at_s[gq] = rs - at_r[gq] * p.ga.S;
+      }
+    }
+    const uint32_t a_bytes = am >= 5 ? (uint32_t)a_groups * 8192u : C::kABytes;
     for (int i = 0; i < num_k; i++, it++) {
       const int L = kb_begin + i;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], C::kABytes + C::kBBytes);
+      mbar_arrive_expect_tx(&full[s], a_bytes + C::kBBytes);
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
-      if (am == 0) {
+      if (am >= 5) {
+        const ConvGeom& g = p.ga;
+        for (int gq = 0; gq < a_groups; gq++) {
+          if (am == 6) {
+            const int cu = at_c[gq] * 4;
+            tma_load_im2col_4d(a + gq * 8192, tmA, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+                               pc.n, (uint16_t)at_s[gq], (uint16_t)at_r[gq]);
+            tma_load_im2col_4d(a + gq * 8192 + 4096, tmA, &full[s], cu + 64, pc.ow * g.stride - g.pad,
+                               pc.oh * g.stride - g.pad, pc.n, (uint16_t)at_s[gq], (uint16_t)at_r[gq]);
+          } else {
+            tma_load_5d(a + gq * 8192, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
+                        pc.oh * g.stride + at_r[gq] - g.pad, pc.n, 2 * (at_c[gq] / 32));
+          }
+        }
+      } else if (am == 0) {
         tma_load_3d(a, tmA, &full[s], 0, (int32_t)m0, 2 * L);  // {64, 128 rows, hi/lo}
       } else if (am == 1) {
         tma_load_4d(a, tmA, &full[s], 0, L * 32, 0, (int32_t)(m0 / 32));  // {64, 32 k, hi/lo, 4 groups}
@@ -923,33 +957,36 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
         }
         tma_load_5d(a, tmA, &full[s], 0, aw, ah, a_n, 2 * tc.cb);  // {64, pixels..., hi/lo}
       }
+      // B lands as [B_hi (BN columns) | B_lo (BN columns)]: one N = 2 BN operand
       if (bm == 0) {
-        tma_load_3d(b, tmB, &full[s], 0, (int32_t)n0, 2 * L);
+        tma_load_3d(b, tmB, &full[s], 0, (int32_t)n0, 2 * L);  // {64, BN rows, hi/lo}
       } else if (bm == 1) {
-        tma_load_4d(b, tmB, &full[s], 0, L * 32, 0, (int32_t)(n0 / 32));
+        tma_load_4d(b, tmB, &full[s], 0, L * 32, (int32_t)(n0 / 32), 0);  // {64, 32 k, groups, hi/lo}
       } else if (bm == 3) {
         const ConvGeom& g = p.ga;
         const int rs_flip = tp.n > 0 ? (int)tp.rs[tc.rs] : (g.R - 1 - tc.r) * g.S + (g.S - 1 - tc.sx);
-        tma_load_5d(b, tmB, &full[s], 0, tc.cb * 32, 0, (int32_t)(n0 / 32), rs_flip);  // {64, 32 k, hi/lo, groups, rs}
-      } else if (bm == 4) {
+        tma_load_5d(b, tmB, &full[s], 0, tc.cb * 32, (int32_t)(n0 / 32), 0, rs_flip);  // {64, 32 k, groups, hi/lo, rs}
+      } else {
         const ConvGeom& g = p.gb;
+        constexpr uint32_t kLoB = BN * 128;
 #pragma unroll
         for (int j = 0; j < BN / 32; j++) {
           const int cu = (b_c0 / 32 + j) * 128;
-          tma_load_im2col_4d(b + j * 8192, tmB, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
-                             pc.n, (uint16_t)b_s, (uint16_t)b_r);
-          tma_load_im2col_4d(b + j * 8192 + 4096, tmB, &full[s], cu + 64, pc.ow * g.stride - g.pad,
-                             pc.oh * g.stride - g.pad, pc.n, (uint16_t)b_s, (uint16_t)b_r);
+          if (bm == 4) {
+            tma_load_im2col_4d(b + j * 4096, tmB, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+                               pc.n, (uint16_t)b_s, (uint16_t)b_r);
+            tma_load_im2col_4d(b + kLoB + j * 4096, tmB, &full[s], cu + 64, pc.ow * g.stride - g.pad,
+                               pc.oh * g.stride - g.pad, pc.n, (uint16_t)b_s, (uint16_t)b_r);
+          } else {
+            // one {64, 32 pixels, hi/lo} box per group: [hi g | lo g] pairs (group stride 8 KB),
+            // the un-fused layout (3 MMAs per k-step, see the issuer) -- half the TMA operations
+            tma_load_5d(b + j * 8192, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad,
+                        pc.oh * g.stride + b_r - g.pad, pc.n, 2 * (b_c0 / 32 + j));
+          }
         }
-      } else {
-        const ConvGeom& g = p.gb;
-#pragma unroll
-        for (int j = 0; j < BN / 32; j++)
-          tma_load_5d(b + j * 8192, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad, pc.oh * g.stride + b_r - g.pad,
-                      pc.n, 2 * (b_c0 / 32 + j));
       }
       if (tap_k) tc.advance(p.ga);
-      if (k_pix) pc.advance(p.gb);
+      if (k_pix) pc.advance(gk);
     }
   }
 }
@@ -1137,11 +1174,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- S32 slots: [A hi | A lo], [B hi | B lo] of one logical k-block ----
     // MN-major halves: 32-column groups of 32 K rows (4 KB), hi and lo of a group
     // adjacent (group stride LBO = 8 KB), SWIZZLE_128B_BASE32B (4-row K groups 512 B apart)
+    // A: MN-major groups [hi | lo] per 32 columns (group stride 8 KB); B: [all hi | all lo]
+    // (MN-major groups 4 KB apart), so B_hi:B_lo is ONE N = 2 BN operand
     const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), 8192, 512, 1) : make_sdesc(smem_u32(sA), 16, 1024);
-    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 8192, 512, 1) : make_sdesc(smem_u32(sB), 16, 1024);
+    // (B mode 2, the 4-D-box weight-gradient operand, keeps [hi | lo] per group: 3 MMAs per k-step)
+    const bool b_pairs = p.b_mode == 2;
+    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), b_pairs ? 8192 : 4096, 512, 1)
+                                  : make_sdesc(smem_u32(sB), 16, 1024);
+    const uint32_t b_lo = b_pairs ? 4096u >> 4 : 0u;
     const uint32_t a_lo = a_mn ? 4096u >> 4 : (uint32_t)(kBM * 128) >> 4;  // lo half offset, 16-byte units
-    const uint32_t b_lo = b_mn ? 4096u >> 4 : (uint32_t)(BN * 128) >> 4;
     const uint32_t a_kstep = a_mn ? 64u : 2u, b_kstep = b_mn ? 64u : 2u;  // UMMA_K = 8: 8 K rows / 32 B
+    const uint32_t idesc2 = make_idesc_tf32(kBM, 2 * BN, a_mn, b_mn);  // A_hi x [B_hi | B_lo]
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int64_t m0, n0;
       int kb_begin, cls;
@@ -1151,23 +1194,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_empty[b], (kNumBuf == 1 ? (j & 1) : ((j >> 1) & 1)) ^ 1);
       tc_fence_after();
       const uint32_t d_buf = tmem_base + b * kBufCols;
-      const uint32_t d_corr = d_buf + kMains * kAccCols;
       for (int i = 0; i < num_k; i++, it++) {
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
         tc_fence_after();
-        const int mi = i % kMains;
-        const uint32_t d_main = d_buf + mi * kAccCols;
+        const uint32_t d_main = d_buf + (i % kMains) * CT::kPairCols;  // [main | correction] pair
         const uint64_t a_hi = a_desc0 + (uint64_t)((s * kSlotA) >> 4), b_hi = b_desc0 + (uint64_t)((s * kSlotB) >> 4);
+        if (!b_pairs) {
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-          mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc, (i < kMains && k == 0) ? 0u : 1u);
+          for (int k = 0; k < 4; k++) {
+            const uint32_t acc = (i < kMains && k == 0) ? 0u : 1u;
+            mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc2, acc);
+            mma_tf32_ss(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
+          }
+        } else {
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-          mma_tf32_ss(d_corr, a_hi + k * a_kstep, b_hi + b_lo + k * b_kstep, idesc, (i == 0 && k == 0) ? 0u : 1u);
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-          mma_tf32_ss(d_corr, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
+          for (int k = 0; k < 4; k++) {
+            const uint32_t acc = (i < kMains && k == 0) ? 0u : 1u;
+            mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc, acc);
+            mma_tf32_ss(d_main + BN, a_hi + k * a_kstep, b_hi + b_lo + k * b_kstep, idesc, acc);
+            mma_tf32_ss(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
+          }
+        }
         mma_commit(&empty[s]);
       }
       // (a short tile, num_k < kMains, leaves the higher mains unwritten: the epilogue skips them)
@@ -1266,13 +1314,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // into r (fp32 adds, round to nearest; the corrections last)
     auto add_corr = [&](int c, uint32_t (&r)[32]) {
       if constexpr (kTf) {
+        // r holds pair 0's main chunk: add the other pairs' mains, then every correction
         uint32_t r2[32];
-        for (int m = 1; m <= kMains; m++) {
-          if (m < kMains && m >= nmain) continue;
-          tmem_ld_32x32b_x32(lane_addr + m * kAccCols + c * 32, r2);
-          tmem_ld_wait();
+        for (int m = 0; m < nmain; m++) {
+          for (int half = (m == 0); half < 2; half++) {
+            tmem_ld_32x32b_x32(lane_addr + m * CT::kPairCols + half * BN + c * 32, r2);
+            tmem_ld_wait();
 #pragma unroll
-          for (int k = 0; k < 32; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+            for (int k = 0; k < 32; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+          }
         }
       }
     };
@@ -1411,12 +1461,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       if constexpr (kTf) {
         uint32_t r2[16];
-        for (int m = 1; m <= kMains; m++) {
-          if (m < kMains && m >= nmain) continue;
-          tmem_ld_32x32b_x16(lane_addr + m * kAccCols, r2);
-          tmem_ld_wait();
+        for (int m = 0; m < nmain; m++) {
+          for (int half = (m == 0); half < 2; half++) {
+            tmem_ld_32x32b_x16(lane_addr + m * CT::kPairCols + half * BN, r2);
+            tmem_ld_wait();
 #pragma unroll
-          for (int k = 0; k < 16; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+            for (int k = 0; k < 16; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+          }
         }
       }
       tc_fence_before();
@@ -1810,7 +1861,9 @@ int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, 
 // MN-major S32 matrix [K rows][ld] (logical ld, row pitch 8 ld bytes) viewed as
 // {64 units, K rows, hi/lo, 32-column groups}: one box {64, 32, 2, groups} lands as
 // per group [hi 32 rows x 128 B | lo 32 rows x 128 B] (SWIZZLE_128B_ATOM_32B)
-int make_tmap_s32_mn(CUtensorMap* tm, const void* base, uint64_t mn, uint64_t krows, uint64_t ld, uint32_t groups) {
+// (hilo_outer: {64 units, K rows, groups, hi/lo} -> [all hi groups | all lo groups], the B form)
+int make_tmap_s32_mn(CUtensorMap* tm, const void* base, uint64_t mn, uint64_t krows, uint64_t ld, uint32_t groups,
+                     bool hilo_outer = false) {
   EncodeTiledFn fn = encode_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && ld % 32 == 0 && groups >= 1 && groups <= 8, DBS_ERR_ARGUMENT,
@@ -1818,6 +1871,14 @@ int make_tmap_s32_mn(CUtensorMap* tm, const void* base, uint64_t mn, uint64_t kr
   cuuint64_t dims[4] = {64, krows, 2, (mn + 31) / 32};
   cuuint64_t strides[3] = {ld * 8, 128, 256};
   cuuint32_t box[4] = {64, 32, 2, groups};
+  if (hilo_outer) {
+    dims[2] = (mn + 31) / 32;
+    dims[3] = 2;
+    strides[1] = 256;
+    strides[2] = 128;
+    box[2] = groups;
+    box[3] = 2;
+  }
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -2091,7 +2152,7 @@ int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64
   int st = a_mn ? make_tmap_s32_mn(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 4)
                 : make_tmap_kpair(&ta, a, (uint64_t)(4 * ceil32(K)), (uint64_t)M, (uint64_t)(4 * lda), 128);
   if (st) return st;
-  st = b_mn ? make_tmap_s32_mn(&tb, b, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, (uint32_t)(bn / 32))
+  st = b_mn ? make_tmap_s32_mn(&tb, b, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, (uint32_t)(bn / 32), true)
             : make_tmap_kpair(&tb, b, (uint64_t)(4 * ceil32(K)), (uint64_t)N, (uint64_t)(4 * ldb), (uint32_t)bn);
   if (st) return st;
   GemmParams p{};
@@ -2118,11 +2179,14 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
   DBS_REQUIRE(c.d && c.M > 0 && c.N > 0 && c.K > 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: bad call");
   DBS_REQUIRE(c.M < (int64_t(1) << 31) && c.K < (int64_t(1) << 31), DBS_ERR_ARGUMENT,
               "conv_gemm_tf: M and K must stay below 2^31");
-  DBS_REQUIRE(c.a_mode <= 2 && c.b_mode <= 3 && !c.d_trans && !(c.b_mode == 3 && c.a_mode != 2) &&
-                  !(c.b_mode == 2 && c.a_mode != 1),
+  DBS_REQUIRE((c.a_mode <= 2 || c.a_mode == 5) && c.b_mode <= 3 && !(c.b_mode == 3 && c.a_mode != 2) &&
+                  !(c.b_mode == 2 && c.a_mode != 1) && !(c.a_mode == 5 && c.b_mode != 1),
               DBS_ERR_ARGUMENT, "conv_gemm_tf: unsupported operand modes (%d, %d)", c.a_mode, c.b_mode);
+  DBS_REQUIRE(!c.d_trans || (c.epi == DBS_EPI_F32_ATOMIC && c.M % 4 == 0 && c.ldd % 4 == 0 && ((uintptr_t)c.d & 15) == 0),
+              DBS_ERR_ARGUMENT, "transposed D: atomic epilogue, M and ldd multiples of 4, 16-byte aligned D");
   CUtensorMap ta, tb;
   GemmParams p{};
+  p.d_trans = c.d_trans;
   p.M = c.M;
   p.N = c.N;
   p.K = c.K;
@@ -2183,6 +2247,20 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
       if (st) return st;
       st = make_tmap_nhwc_pair(&ta, c.a, t4, bw, bh, bnn, c.ga.stride);  // {64, pixels, hi/lo}
     }
+  } else if (c.a_mode == 5) {
+    // transposed weight gradient: 32-pixel windows of the conv input per 32-row group of M
+    DBS_REQUIRE(c.ga.Cin % 32 == 0 && c.M == (int64_t)c.ga.R * c.ga.S * c.ga.Cin && c.d_trans, DBS_ERR_ARGUMENT,
+                "transposed wgrad (S32): bad call");
+    const ConvTensor t4{c.ta.N, c.ta.H, c.ta.W, 4 * c.ta.C};
+    if (force_im2col() || !pixel_box_fits(c.ga.OH, c.ga.OW, 32)) {
+      st = make_tmap_im2col(&ta, c.a, t4, -c.ga.pad, c.ga.pad - (c.ga.R - 1), 32, c.ga.stride, kMnSwz);
+      p.a_mode = 6;
+    } else {
+      int bw, bh, bnn;
+      st = pixel_box(c.ga.OH, c.ga.OW, 32, bw, bh, bnn);
+      if (st) return st;
+      st = make_tmap_nhwc_pair(&ta, c.a, t4, bw, bh, bnn, c.ga.stride, kMnSwz);
+    }
   } else if (c.a_mode == 1) {
     DBS_REQUIRE(c.lda % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: lda %% 32");
     st = make_tmap_s32_mn(&ta, c.a, (uint64_t)c.M, (uint64_t)c.K, (uint64_t)c.lda, 4);
@@ -2207,15 +2285,15 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
     }
   } else if (c.b_mode == 3) {
     // filter [Cout][R*S][Cin] S32 read as the flipped, transposed filter: the MN-major
-    // view {64 units, Cout k (K rows), hi/lo, Cin / 32 groups, R*S}, box {64, 32 k, 2, BN / 32, 1}
+    // view {64 units, Cout k (K rows), Cin / 32 groups, hi/lo, R*S}, box {64, 32 k, BN / 32, 2, 1}
     EncodeTiledFn fn = encode_fn();
     DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     DBS_REQUIRE(c.tb.C % 32 == 0 && c.tb.N % 32 == 0 && ((uintptr_t)c.b & 15) == 0 && bn % 32 == 0, DBS_ERR_ARGUMENT,
                 "dgrad filter view: Cin, Cout multiples of 32 required");
     const uint64_t cin = (uint64_t)c.tb.C, rs = (uint64_t)c.tb.W;
-    cuuint64_t dims[5] = {64, (cuuint64_t)c.tb.N, 2, (cuuint64_t)(cin / 32), (cuuint64_t)rs};
-    cuuint64_t strides[4] = {(cuuint64_t)(rs * cin * 8), 128, 256, (cuuint64_t)(cin * 8)};
-    cuuint32_t box[5] = {64, 32, 2, (cuuint32_t)(bn / 32), 1};
+    cuuint64_t dims[5] = {64, (cuuint64_t)c.tb.N, (cuuint64_t)(cin / 32), 2, (cuuint64_t)rs};
+    cuuint64_t strides[4] = {(cuuint64_t)(rs * cin * 8), 256, 128, (cuuint64_t)(cin * 8)};
+    cuuint32_t box[5] = {64, 32, (cuuint32_t)(bn / 32), 2, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(c.b), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, kMnSwz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -2224,7 +2302,7 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
     st = DBS_OK;
   } else if (c.b_mode == 1) {
     DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
-    st = make_tmap_s32_mn(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, (uint32_t)(bn / 32));
+    st = make_tmap_s32_mn(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, (uint32_t)(bn / 32), true);
   } else {
     DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
     st = make_tmap_kpair(&tb, c.b, (uint64_t)(4 * ceil32(c.K)), (uint64_t)c.N, (uint64_t)(4 * c.ldb), (uint32_t)bn);

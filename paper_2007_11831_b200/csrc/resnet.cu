@@ -1735,7 +1735,7 @@ int conv_wgrad_ex(const Conv& c, const void* dy, const void* x, int64_t B, float
   const int kb = tf ? 32 : 64;  // pixels per logical k-block
   ConvCall call{};
   call.tf = tf;
-  if (!tf && c.cout == 64 && c.cin % 64 == 0 && (c.k == 1 ? c.stride == 1 : true) && ((uintptr_t)dw & 15) == 0 &&
+  if (c.cout == 64 && c.cin % 64 == 0 && (c.k == 1 ? c.stride == 1 : true) && ((uintptr_t)dw & 15) == 0 &&
       wgrad_trans_enabled()) {
     // 64 output channels: dW^T = X^T dY puts the (r, s, c) reduction rows on the
     // 128-row MMA M side (all rows live) instead of the 64 output channels (half
@@ -1754,7 +1754,7 @@ int conv_wgrad_ex(const Conv& c, const void* dy, const void* x, int64_t B, float
       call.a_mode = 5;
       call.a = x;
       call.ta = nhwc(B, c.H, c.W, c.cin);
-      call.ga = ConvGeom{c.k, c.k, c.cin / 64, c.stride, c.pad, c.OH, c.OW, c.cin};
+      call.ga = ConvGeom{c.k, c.k, c.cin / kb, c.stride, c.pad, c.OH, c.OW, c.cin};
     }
     call.epi = DBS_EPI_F32_ATOMIC;
     call.d = dw;
@@ -1763,7 +1763,7 @@ int conv_wgrad_ex(const Conv& c, const void* dy, const void* x, int64_t B, float
     call.bn_override = 64;
     const int64_t tiles = (call.M + 127) / 128;
     int64_t splits = current_sm_count() / tiles;
-    const int64_t kblocks = (call.K + 63) / 64;
+    const int64_t kblocks = (call.K + kb - 1) / kb;
     if (splits > kblocks) splits = kblocks;
     if (splits < 1) splits = 1;
     call.splits = (int)splits;

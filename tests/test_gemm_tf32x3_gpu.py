@@ -4,9 +4,9 @@ fp64 PyTorch reference of the same op.
 S32 keeps every operand to ~2^-23 relative (hi = rn_tf32(x), lo = rn_tf32(x -
 hi)); the dropped lo*lo term is ~2^-24 per product; the tensor core truncates
 each accumulation step into TMEM (~2^-24 of the running sum), which the kernel
-spreads over 3 main accumulators plus a correction accumulator summed in fp32.
+spreads over 2 [main | correction] accumulator pairs summed in fp32.
 Stated tolerances: elementwise |err| <= 2e-6 * sum_k |a||b|; normwise relative
-error <= 1e-9 * K and >= 300x below a bf16-operand GEMM."""
+error <= 1.5e-9 * K and >= 300x below a bf16-operand GEMM."""
 
 from __future__ import annotations
 
@@ -116,10 +116,10 @@ def test_tf32x3_beats_bf16_and_tf32(dev):
                                                       [(0, 0), (1, 1)]):
         err, err_f32, err_bf16 = _accuracy_case(torch, dev, M, N, K, a_mn, b_mn)
         # stated bound: the tensor core truncates each in-TMEM accumulation step, and a
-        # main accumulator takes K / 8 / 3 steps (3 mains round-robin), so the normwise
-        # error grows ~linearly in K: <= 1e-9 K (measured 8.4e-7 at K = 1024, 3.7e-6 at
-        # 4608; cuBLAS fp32 2.7e-7..5.7e-7), and >= 300x below bf16 operands
-        if not (err < 1e-9 * K and err < err_bf16 / 300):
+        # main accumulator takes K / 8 / 2 steps (2 [main | correction] pairs round-robin),
+        # so the normwise error grows ~linearly in K: <= 1.5e-9 K (measured 1.2e-6 at
+        # K = 1024, 5.5e-6 at 4608; cuBLAS fp32 2.7e-7..5.7e-7), >= 300x below bf16 operands
+        if not (err < 1.5e-9 * K and err < err_bf16 / 300):
             bad.append((M, N, K, a_mn, b_mn, err, err_f32))
     assert not bad, bad
 
