@@ -493,6 +493,34 @@ int dbs_mlp_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0
                            int32_t skip_update, void* agg_stream);
 
 /* ------------------------------------------------------------------------ */
+/* Monte-Carlo checks of the theory (checks.py:42-142, sgdlab.py:241-314)    */
+/* ------------------------------------------------------------------------ */
+/* numpy Generator.integers(0, high, size=count) (int64, high <= 2^32) and
+ * Generator.random(count) from a device PCG64 state, bit-exact, state advanced. */
+int dbs_dev_pcg64_integers(dbs_pcg64* d_rng, int64_t high, int64_t count, int64_t* d_out, void* stream);
+int dbs_dev_pcg64_random(dbs_pcg64* d_rng, int64_t count, double* d_out, void* stream);
+/* check_theorem1_bound's vectorised single-sample SGD (checks.py:62-70): n_seeds
+ * trajectories from x0 for n_iter steps with idx [n_iter][n_seeds]; dists
+ * [(n_iter + 1)][n_seeds] (row 0 untouched), snapshots of X at the host-sorted
+ * device iterations d_probe_at [n_probe] into d_snap [n_probe][n_seeds][dim]. */
+int dbs_dev_theorem1_trajectories(const double* d_offsets, const double* d_opt, const double* d_x0, int64_t dim,
+                                  const int64_t* d_idx, int64_t n_seeds, int64_t n_iter, double coef,
+                                  const int32_t* d_probe_at, int32_t n_probe, double* d_X, double* d_dists,
+                                  double* d_snap, void* stream);
+/* per row of v[rows][ld] (n used): mean, sum (v - mean)^2, sum (v - mean)^4 into out[rows][3] */
+int dbs_dev_row_moments(const double* d_v, int64_t rows, int64_t n, int64_t ld, double* d_out, void* stream);
+/* ||batch-mean gradient||^2 per draw (estimate_gradient_noise); kind 0 ConvexProblem, 1 LogisticProblem */
+int dbs_dev_minibatch_sqnorms(int32_t kind, const double* d_data, const double* d_labels, const double* d_opt,
+                              int64_t dim, double mu, const double* d_x, const int64_t* d_idx, int64_t n_draws,
+                              int64_t b, double* d_out, void* stream);
+/* per-sample objective values f_i(x), i < n */
+int dbs_dev_sample_values(int32_t kind, const double* d_data, const double* d_labels, const double* d_opt,
+                          int64_t dim, double mu, const double* d_x, int64_t n, double* d_out, void* stream);
+/* out[t] = mean_k v[idx[t][k]], k < m */
+int dbs_dev_gather_means(const double* d_v, const int64_t* d_idx, int64_t n_draws, int64_t m, double* d_out,
+                         void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Worker heterogeneity (cluster.py:25-79 DisturbanceEvent) and timing       */
 /* ------------------------------------------------------------------------ */
 /* Occupy `num_ctas` SMs (one resident CTA per SM, max shared memory) until

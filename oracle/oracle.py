@@ -692,3 +692,60 @@ def resnet_init(classes=10, seed=0, depth=18):
             bound = 1.0 / math.sqrt(feat)
             out.append(rng.uniform(-bound, bound, shp).astype(np.float32))
     return out
+
+
+# ---------------------------------------------------------------------------
+# numpy Generator.integers / random restated (the draws of checks.py:42-142)
+# ---------------------------------------------------------------------------
+
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+_M128 = (1 << 128) - 1
+
+
+class Pcg64Ref:
+    """PCG64 (XSL-RR 128/64) from a numpy bit-generator state dict."""
+
+    def __init__(self, state: dict):
+        self.state = int(state["state"]["state"])
+        self.inc = int(state["state"]["inc"])
+
+    def next64(self) -> int:
+        self.state = (self.state * _PCG_MULT + self.inc) & _M128
+        hi, lo = self.state >> 64, self.state & ((1 << 64) - 1)
+        x, r = hi ^ lo, hi >> 58
+        return ((x >> r) | (x << ((64 - r) & 63))) & ((1 << 64) - 1)
+
+    def integers(self, n: int, count: int) -> list:
+        """Generator.integers(0, n, size=count), int64, n <= 2^32: a 32-bit buffer local to
+        the call (low half first), Lemire's multiply-and-reject (numpy distributions.c
+        random_bounded_uint64_fill, use_masked = False)."""
+        r = n - 1
+        buf, bcnt = 0, 0
+        out = []
+
+        def b32():
+            nonlocal buf, bcnt
+            if not bcnt:
+                buf, bcnt = self.next64(), 1
+            else:
+                buf, bcnt = buf >> 32, bcnt - 1
+            return buf & 0xFFFFFFFF
+
+        if r == 0:
+            return [0] * count
+        if r == 0xFFFFFFFF:
+            return [b32() for _ in range(count)]
+        rexcl = r + 1
+        threshold = (0xFFFFFFFF - r) % rexcl
+        for _ in range(count):
+            m = b32() * rexcl
+            left = m & 0xFFFFFFFF
+            if left < rexcl:
+                while left < threshold:
+                    m = b32() * rexcl
+                    left = m & 0xFFFFFFFF
+            out.append(m >> 32)
+        return out
+
+    def random(self, count: int) -> list:
+        return [(self.next64() >> 11) * (1.0 / 9007199254740992.0) for _ in range(count)]

@@ -166,6 +166,15 @@ SIGNATURES = {
     "dbs_dev_spin_until_ctx": (c_i32, [c_i32, c_vp, c_vp, c_vp]),
     "dbs_partition_create": (c_i32, [c_i32, c_i32, ctypes.POINTER(c_vp), P_i32]),
     "dbs_partition_get": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    "dbs_dev_pcg64_integers": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "dbs_dev_pcg64_random": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
+    "dbs_dev_theorem1_trajectories": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_dbl, c_vp, c_i32, c_vp,
+                                              c_vp, c_vp, c_vp]),
+    "dbs_dev_row_moments": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "dbs_dev_minibatch_sqnorms": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_i64, c_i64, c_vp,
+                                          c_vp]),
+    "dbs_dev_sample_values": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_i64, c_vp, c_vp]),
+    "dbs_dev_gather_means": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "dbs_partition_push": (c_i32, [c_vp]),
     "dbs_partition_pop": (c_i32, [c_vp]),
     "dbs_dev_spin_for": (c_i32, [c_i32, c_i64, c_vp]),

@@ -31,6 +31,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 PER_FILE = {
     "controller.cu": ["-fmad=false"],
     "problems.cu": ["-fmad=false"],
+    "theory.cu": ["-fmad=false"],
 }
 
 

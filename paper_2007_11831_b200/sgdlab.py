@@ -13,8 +13,10 @@ numeric step of the hot path runs in libdbs_b200 kernels:
   * one fused single-CTA launch per epoch for the reference problems
     (problems.cu: worker gradients -> aggregate -> heavy-ball step -> ||x-x*||^2);
   * the drop-in functions call the same kernels one step at a time.
-The theory estimators of the reference (theorem1_bound, estimate_gradient_noise,
-verify_lemma1_variance) are outside the hot path and not provided here.
+The theory estimators of the reference (theorem1_bound, estimate_gradient_noise
+:252-272, verify_lemma1_variance :282-314) run on the device too (theory.cu):
+numpy's Generator.integers / random draws reproduced bit-exactly from the same
+PCG64 state, the Monte-Carlo arithmetic in fp64 kernels.
 """
 
 from __future__ import annotations
@@ -344,6 +346,26 @@ class DeviceRng:
         ctypes.memmove(ctypes.byref(st), bytes(self.state.cpu().numpy()), ctypes.sizeof(st))
         return st
 
+    def integers(self, high: int, size) -> "object":
+        """Generator.integers(0, high, size) (int64) as a device tensor of shape `size`."""
+        torch = _torch()
+        shape = (size,) if isinstance(size, int) else tuple(size)
+        n = int(np.prod(shape)) if shape else 1
+        out = torch.empty(max(n, 1), dtype=torch.int64, device=self.state.device)
+        _lib.check(_lib.lib().dbs_dev_pcg64_integers(self.state.data_ptr(), int(high), n, out.data_ptr(),
+                                                     _lib.stream_handle()), "pcg64_integers")
+        return out[:n].view(shape)
+
+    def random(self, size) -> "object":
+        """Generator.random(size) (float64) as a device tensor."""
+        torch = _torch()
+        shape = (size,) if isinstance(size, int) else tuple(size)
+        n = int(np.prod(shape)) if shape else 1
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=self.state.device)
+        _lib.check(_lib.lib().dbs_dev_pcg64_random(self.state.data_ptr(), n, out.data_ptr(), _lib.stream_handle()),
+                   "pcg64_random")
+        return out[:n].view(shape)
+
     def permute_spans(self, spans, only_span: int = -1, out=None, stream=None):
         """start + permutation(width) for every span, one generator (sgdlab.py:372-374)."""
         torch = _torch()
@@ -405,3 +427,89 @@ def run_parallel_sgd(problem, config: SgdConfig, n_workers: int, plan_source: Pl
         done += run
         epoch += 1
     return SgdTrajectory(squared_distances=sq.cpu().numpy(), final_loss=problem.objective_gap(x))
+
+
+# ---------------------------------------------------------------------------
+# theory estimators (sgdlab.py:252-314) on the device
+# ---------------------------------------------------------------------------
+
+def _problem_kind(problem):
+    if isinstance(problem, ConvexProblem):
+        return 0
+    if isinstance(problem, LogisticProblem):
+        return 1
+    raise ConfigurationError(f"unsupported problem type {type(problem).__name__}")
+
+
+def _row_moments(v):
+    """(mean, sum (v - mean)^2, sum (v - mean)^4) of each row of a [rows][n] device tensor."""
+    torch = _torch()
+    v = v.contiguous()
+    rows, n = v.shape
+    out = torch.empty((rows, 3), dtype=torch.float64, device=v.device)
+    _lib.check(_lib.lib().dbs_dev_row_moments(v.data_ptr(), rows, n, n, out.data_ptr(), _lib.stream_handle()),
+               "row_moments")
+    return out.cpu().numpy()
+
+
+def estimate_gradient_noise(problem, x_set, batch_size: int, n_draws: int, seed: int = 0) -> float:
+    """Max over probe points of the mean squared norm of the mini-batch gradient,
+    i.i.d. draws (sgdlab.py:252-272)."""
+    if n_draws < 100:
+        raise ConfigurationError("need at least 100 draws for a usable estimate")
+    torch = _torch()
+    kind = _problem_kind(problem)
+    data, labels, opt = problem.device()
+    rng = DeviceRng(seed, data.device)
+    worst = 0.0
+    buf = torch.empty(n_draws, dtype=torch.float64, device=data.device)
+    for x in x_set:
+        idx = rng.integers(problem.sample_count, (n_draws, batch_size))
+        xd = _to_dev_f64(x)
+        _lib.check(_lib.lib().dbs_dev_minibatch_sqnorms(kind, data.data_ptr(), labels.data_ptr() if labels is not None
+                                                        else None, opt.data_ptr(), problem.dimension,
+                                                        float(problem.mu), xd.data_ptr(), idx.data_ptr(), n_draws,
+                                                        int(batch_size), buf.data_ptr(), _lib.stream_handle()),
+                   "minibatch_sqnorms")
+        worst = max(worst, float(_row_moments(buf.view(1, -1))[0, 0]))
+    return worst
+
+
+@dataclass(frozen=True)
+class VarianceEstimate:
+    batch_size: int
+    variance: float
+    std_error: float
+
+
+def verify_lemma1_variance(problem, x, m_values: Sequence[int], n_draws: int, seed: int = 0,
+                           with_replacement: bool = True) -> list:
+    """Empirical variance of the mini-batch mean objective value per size m, with the
+    fourth-moment standard error (sgdlab.py:282-314)."""
+    torch = _torch()
+    kind = _problem_kind(problem)
+    data, labels, opt = problem.device()
+    rng = DeviceRng(seed, data.device)
+    xd = _to_dev_f64(x)
+    n = problem.sample_count
+    values = torch.empty(n, dtype=torch.float64, device=data.device)
+    _lib.check(_lib.lib().dbs_dev_sample_values(kind, data.data_ptr(), labels.data_ptr() if labels is not None else None,
+                                                opt.data_ptr(), problem.dimension, float(problem.mu), xd.data_ptr(), n,
+                                                values.data_ptr(), _lib.stream_handle()), "sample_values")
+    means = torch.empty(n_draws, dtype=torch.float64, device=data.device)
+    out = []
+    for m in m_values:
+        if with_replacement:
+            idx = rng.integers(n, (n_draws, int(m)))
+        else:
+            # np.argsort(rng.random((n_draws, n)), axis=1)[:, :m]: the same uniforms, a
+            # stable per-row sort (the draws are distinct with probability 1)
+            idx = torch.argsort(rng.random((n_draws, n)), dim=1, stable=True)[:, :int(m)].contiguous()
+        _lib.check(_lib.lib().dbs_dev_gather_means(values.data_ptr(), idx.data_ptr(), n_draws, int(m),
+                                                   means.data_ptr(), _lib.stream_handle()), "gather_means")
+        mean, m2, m4s = _row_moments(means.view(1, -1))[0]
+        var = float(m2 / (n_draws - 1))
+        m4 = float(m4s / n_draws)
+        se = float(np.sqrt(max(m4 - var ** 2 * (n_draws - 3) / (n_draws - 1), 0.0) / n_draws))
+        out.append(VarianceEstimate(batch_size=int(m), variance=var, std_error=se))
+    return out

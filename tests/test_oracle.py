@@ -258,3 +258,14 @@ def test_oracle_mlp_loop_pinned_to_reference_golden():
         np.testing.assert_allclose(ref["losses"], want_loss, rtol=1e-12)
         disp = np.array([float.fromhex(v) for v in case["sq_disp"]])
         assert disp[-1] > 0 and np.all(np.diff(disp[:5]) > 0)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 42])
+def test_oracle_numpy_integers_restatement(seed):
+    """The bounded-integer / uniform draws of dbsim.checks (rng.integers, rng.random)
+    restated exactly -- the algorithm theory.cu runs on the device."""
+    for n, cnt in ((4096, 1000), (7, 500), (2 ** 32, 50), (1, 5), (100000, 333)):
+        g = np.random.default_rng(seed)
+        ref = O.Pcg64Ref(g.bit_generator.state)
+        assert list(g.integers(0, n, size=cnt)) == ref.integers(n, cnt)
+        np.testing.assert_array_equal(g.random(7), np.asarray(ref.random(7)))
