@@ -334,10 +334,11 @@ extern "C" int dbs_mlp_forward_backward(dbs_mlp* m, const void* d_params_shadow,
 // compute time is accumulated on the device from %globaltimer stamps.
 // ---------------------------------------------------------------------------
 namespace {
-std::vector<cudaEvent_t> g_events;
-std::mutex g_ev_mu;
+// One pool per host thread: two trainers driven from different threads never
+// record or wait on each other's events, and a grow cannot move another
+// caller's pointer.  (Events are never destroyed; a pool lives as long as its thread.)
+thread_local std::vector<cudaEvent_t> g_events;
 int events(int n, cudaEvent_t** out) {
-  std::lock_guard<std::mutex> lk(g_ev_mu);
   while ((int)g_events.size() < n) {
     cudaEvent_t e;
     DBS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
