@@ -196,6 +196,25 @@ struct HaloCfg {
   static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
 };
 
+// fp32-class halo variant (S32 operands, 3x3 stride-1 conv with 64 input and 64
+// output channels).  An S32 tile moves 4x the bytes of a bf16 one at half the MMA
+// rate, and the streamed implicit GEMM sat at the per-SM L2 -> shared-memory ingest
+// limit (~60 B/clk: 48 KB per 32-wide k-block against ~450 cycles of MMA; traced,
+// scripts/gemm_trace.cu).  A 64-channel S32 filter (295 KB) cannot stay resident, so
+// here the INPUT is the reused operand: per output tile and 32-channel block, one
+// zero-padded halo box ([hi plane | lo plane], halo_rows x (W + 1) pixel rows of
+// 128 B each) serves all 9 taps through row-shifted descriptors, and only the
+// filter k-blocks stream through the ring -- 22 KB instead of 48 KB per k-block.
+struct HaloTfCfg {
+  static constexpr uint32_t kASlotBytes = 60 * 1024;  // 2 x halo_rows x (W + 1) x 128 B (W <= 32)
+  static constexpr int kASlots = 2;                   // one per channel block in flight
+  static constexpr uint32_t kBBytes = 2 * 64 * 128;   // [B_hi | B_lo] of one tap x 32 channels
+  static constexpr int kStages = 5;
+  static constexpr uint32_t kEpiBytes = 4 * 32 * 33 * 4;
+  static constexpr size_t kSmem = 1024 + (size_t)kASlots * kASlotBytes + (size_t)kStages * kBBytes + kEpiBytes + 256;
+  static_assert(kSmem + 1024 <= 227 * 1024, "shared memory budget");
+};
+
 __device__ __forceinline__ void pixel_coords(const ConvGeom& g, int64_t pix, int& n, int& oh, int& ow) {
   // 32-bit arithmetic: conv GEMM rows / pixel-K extents are < 2^31 (checked by conv_gemm)
   const uint32_t hw = (uint32_t)(g.OH * g.OW), p32 = (uint32_t)pix;
@@ -908,6 +927,7 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
       const int L = kb_begin + i;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+      if (it < 12) GEMM_TRACE(100 + it);
       mbar_arrive_expect_tx(&full[s], a_bytes + C::kBBytes);
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
@@ -1021,9 +1041,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<BN>;
   using H = HaloCfg;
   static_assert(!kHalo || BN == 64, "halo variant: 64 output columns");
-  static_assert(!(kHalo && kTf), "no halo variant for S32 operands");
+  constexpr bool kHT = kHalo && kTf;  // fp32-class halo variant (HaloTfCfg)
+  using HT = HaloTfCfg;
   using CT = CfgTf<BN < 128 ? BN : 128>;
-  constexpr int kStages = kHalo ? H::kStages : (kTf ? CT::kStages : C::kStages);
+  constexpr int kStages = kHT ? HT::kStages : (kHalo ? H::kStages : (kTf ? CT::kStages : C::kStages));
   constexpr uint32_t kAccCols = kHalo ? H::kAccCols : C::kAccCols;
   // S32: each tile buffer holds CT::kMains main accumulators (hi*hi, round-robin over
   // the logical k-blocks) and one correction accumulator (hi*lo + lo*hi, 2^-11 smaller),
@@ -1035,20 +1056,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t kBufCols = kTf ? CT::kBufCols : kAccCols;
   constexpr int kNumBuf = kTf ? CT::kNumBuf : 2;  // accumulator buffers (tile j uses j % kNumBuf)
   constexpr uint32_t kTmemCols = kHalo ? H::kTmemCols : (kTf ? 512u : C::kTmemCols);
-  constexpr uint32_t kSlotA = kHalo ? H::kSlotBytes : (kTf ? CT::kABytes : C::kABytes);
-  constexpr uint32_t kSlotB = kHalo ? 0u : (kTf ? CT::kBBytes : C::kBBytes);
-  constexpr uint32_t kBRes = kHalo ? H::kBResBytes : 0u;
+  constexpr uint32_t kSlotA = kHT ? HT::kASlotBytes : (kHalo ? H::kSlotBytes : (kTf ? CT::kABytes : C::kABytes));
+  constexpr uint32_t kSlotB = kHT ? HT::kBBytes : (kHalo ? 0u : (kTf ? CT::kBBytes : C::kBBytes));
+  constexpr uint32_t kBRes = (kHalo && !kHT) ? H::kBResBytes : 0u;
+  constexpr int kASlots = kHT ? HT::kASlots : kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kSlotA;  // ring B slots, or the resident filter (halo)
+  uint8_t* sB = smem + kASlots * kSlotA;  // ring B slots, or the resident filter (halo)
   float* sEpi = reinterpret_cast<float*>(sB + kStages * kSlotB + kBRes);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + C::kEpiBytes);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;  // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2;    // [2] epilogue -> MMA
   uint64_t* bres_full = acc_empty + 2;   // resident filter landed (halo)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+  uint64_t* a_full = bres_full + 1;      // [2] halo slot landed (kHT)
+  uint64_t* a_empty = a_full + 2;        // [2] halo slot consumed by its 9 taps (kHT)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GEMM_TRACE(0);
@@ -1076,6 +1100,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
     }
     mbar_init(bres_full, 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&a_full[b], 1);
+      mbar_init(&a_empty[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -1093,7 +1121,37 @@ __global__ void __launch_bounds__(kThreads, 1)
    uint32_t it = 0;  // ring position, continuous across tiles
    uint32_t pt = 0;
    (void)pt;
-   if constexpr (kHalo) {
+   if constexpr (kHT) {
+    // per tile and 32-channel block: one [hi | lo] halo box, then the 9 taps' filter k-blocks
+    const ConvGeom& g = p.ga;
+    const int W1 = g.OW + 1;
+    const uint32_t a_bytes = 2u * (uint32_t)(p.halo_rows * W1) * 128u;
+    uint32_t ia = 0;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      if (pt < 10) GEMM_TRACE(2 + pt);
+      pt++;
+      const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
+      const int P0 = (int)(t - (int64_t)img * p.halo_tpi) * kBM;
+      for (int cb = 0; cb < g.cblocks; cb++, ia++) {
+        const int sa = (int)(ia & 1);
+        mbar_wait(&a_empty[sa], ((ia >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&a_full[sa], a_bytes);
+        tma_load_5d(sA + sa * kSlotA, &tmA, &a_full[sa], 0, -1, P0 / W1 - 1, img, 2 * cb);  // {64, W+1, rows, 1, hi/lo}
+        for (int tap = 0; tap < 9; tap++, it++) {
+          const int s = (int)(it % kStages);
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          if (it < 12) GEMM_TRACE(100 + it);
+          mbar_arrive_expect_tx(&full[s], kSlotB);
+          uint8_t* b = sB + s * kSlotB;
+          if (p.b_mode == 0) {
+            tma_load_3d(b, &tmB, &full[s], 0, 0, 2 * (tap * g.cblocks + cb));  // {64, 64 rows, hi/lo}
+          } else {  // flipped filter of the input gradient, MN-major {64, 32 k, groups, hi/lo, rs}
+            tma_load_5d(b, &tmB, &full[s], 0, cb * 32, 0, 0, 8 - tap);
+          }
+        }
+      }
+    }
+   } else if constexpr (kHalo) {
     // the 9 filter taps, once per CTA
     mbar_arrive_expect_tx(bres_full, H::kBResBytes);
     for (int tap = 0; tap < 9; tap++) {
@@ -1130,7 +1188,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = kTf ? make_idesc_tf32(kBM, BN, a_mn, b_mn) : make_idesc_bf16(kBM, BN, a_mn, b_mn);
     uint32_t it = 0, j = 0;
-    if constexpr (kHalo) {
+    if constexpr (kHT) {
+      const int W1 = p.ga.OW + 1;
+      const uint32_t a_lo = (uint32_t)(p.halo_rows * W1) * 8u;  // lo plane, 16-byte units
+      const uint64_t a_desc0 = make_sdesc(smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), 4096, 512, 1) : make_sdesc(smem_u32(sB), 16, 1024);
+      const uint32_t b_kstep = b_mn ? 64u : 2u;  // UMMA_K = 8: 8 K rows / 32 B
+      const uint32_t idesc1 = make_idesc_tf32(kBM, BN, 0, b_mn);
+      const uint32_t idesc2 = make_idesc_tf32(kBM, 2 * BN, 0, b_mn);  // A_hi x [B_hi | B_lo]
+      uint32_t ia = 0;
+      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int b = (int)(j & 1);
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        if (j < 10) GEMM_TRACE(12 + j);
+        tc_fence_after();
+        const uint32_t d_buf = tmem_base + b * kBufCols;
+        const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
+        const int off = ((int)(t - (int64_t)img * p.halo_tpi) * kBM) % W1;
+        int i = 0;  // logical k-block of the tile (main accumulator round robin)
+        for (int cb = 0; cb < p.ga.cblocks; cb++, ia++) {
+          const int sa = (int)(ia & 1);
+          mbar_wait(&a_full[sa], (ia >> 1) & 1);
+          tc_fence_after();
+          const uint64_t a_slot = a_desc0 + (uint64_t)((sa * kSlotA) >> 4);
+#pragma unroll 1
+          for (int tap = 0; tap < 9; tap++, it++, i++) {
+            const int s = (int)(it % kStages);
+            mbar_wait(&full[s], (it / kStages) & 1);
+            if (it < 12) GEMM_TRACE(112 + it);
+            tc_fence_after();
+            const int r = tap / 3, sx = tap - 3 * (tap / 3);
+            const uint64_t a_hi = a_slot + (uint64_t)((off + r * W1 + sx) * 8);  // 128-byte rows
+            const uint64_t b_hi = b_desc0 + (uint64_t)((s * kSlotB) >> 4);
+            const uint32_t d_main = d_buf + (i % kMains) * CT::kPairCols;  // [main | correction] pair
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const uint32_t acc = (i < kMains && k == 0) ? 0u : 1u;
+              mma_tf32_ss(d_main, a_hi + k * 2, b_hi + k * b_kstep, idesc2, acc);
+              mma_tf32_ss(d_main + BN, a_hi + a_lo + k * 2, b_hi + k * b_kstep, idesc1, 1u);
+            }
+            mma_commit(&empty[s]);
+            if (it < 12) GEMM_TRACE(64 + it);
+          }
+          mma_commit(&a_empty[sa]);
+        }
+        mma_commit(&acc_full[b]);
+        if (j < 10) GEMM_TRACE(22 + j);
+        j++;
+      }
+    } else if constexpr (kHalo) {
       mbar_wait(bres_full, 0);
       tc_fence_after();
       // descriptors by arithmetic on the 16-byte address field (no per-MMA
@@ -1192,11 +1298,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (num_k == 0) continue;
       const int b = kNumBuf == 1 ? 0 : (int)(j & 1);
       mbar_wait(&acc_empty[b], (kNumBuf == 1 ? (j & 1) : ((j >> 1) & 1)) ^ 1);
+      if (j < 10) GEMM_TRACE(12 + j);
       tc_fence_after();
       const uint32_t d_buf = tmem_base + b * kBufCols;
       for (int i = 0; i < num_k; i++, it++) {
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
+        if (it < 12) GEMM_TRACE(112 + it);
         tc_fence_after();
         const uint32_t d_main = d_buf + (i % kMains) * CT::kPairCols;  // [main | correction] pair
         const uint64_t a_hi = a_desc0 + (uint64_t)((s * kSlotA) >> 4), b_hi = b_desc0 + (uint64_t)((s * kSlotB) >> 4);
@@ -1220,6 +1328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // (a short tile, num_k < kMains, leaves the higher mains unwritten: the epilogue skips them)
       mma_commit(&acc_full[b]);
+      if (j < 10) GEMM_TRACE(22 + j);
       j++;
     }
     } else {
@@ -1280,14 +1389,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     int64_t m0 = 0, n0 = 0;
     int kb_begin, cls = -1;
-    const int tile_k = kHalo ? 1 : decode(t, m0, n0, kb_begin, cls);
+    const int tile_k = kHT ? 9 * p.ga.cblocks : (kHalo ? 1 : decode(t, m0, n0, kb_begin, cls));
     if (tile_k == 0) continue;
     const int nmain = tile_k < kMains ? tile_k : kMains;  // S32: main accumulators this tile wrote
     (void)nmain;
     const OutMap& om = cls >= 0 ? p.cls_omap[cls] : p.omap;
     const int b = kNumBuf == 1 ? 0 : (int)(tj & 1);
     mbar_wait(&acc_full[b], kNumBuf == 1 ? (tj & 1) : ((tj >> 1) & 1));
-    if (warp == 2 && lane == 0) GEMM_TRACE(32 + tj);
+    if (warp == 2 && lane == 0 && tj < 10) GEMM_TRACE(32 + tj);
     tc_fence_after();
     int64_t row = m0 + q * 32 + lane;
     int64_t orow = row;  // the output row this thread writes
@@ -1342,7 +1451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[b]);
-          if (warp == 2 && lane == 0) GEMM_TRACE(42 + tj);
+          if (warp == 2 && lane == 0 && tj < 10) GEMM_TRACE(42 + tj);
         }
         const bool prefetch = !last;
         const int cnt = (int)((p.N - n_base) < 32 ? (p.N - n_base) : 32);
@@ -1481,7 +1590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         epilogue_chunk<BN, kTf>(p, orow, n0, v, cnt, vo);
       }
     }
-    if (warp == 2 && lane == 0) GEMM_TRACE(52 + tj);
+    if (warp == 2 && lane == 0 && tj < 10) GEMM_TRACE(52 + tj);
     tj++;
   }
   };
@@ -1953,7 +2062,8 @@ void* current_ctx() {
 
 template <int BN, bool kHalo = false, bool kTf = false>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits, cudaStream_t s) {
-  constexpr size_t kSmem = kHalo ? HaloCfg::kSmem : (kTf ? CfgTf<(BN < 128 ? BN : 128)>::kSmem : Cfg<BN>::kSmem);
+  constexpr size_t kSmem = (kHalo && kTf) ? HaloTfCfg::kSmem
+                         : kHalo ? HaloCfg::kSmem : (kTf ? CfgTf<(BN < 128 ? BN : 128)>::kSmem : Cfg<BN>::kSmem);
   static thread_local void* seen[16] = {nullptr};
   static thread_local int nseen = 0;
   void* ctx = current_ctx();
@@ -2031,6 +2141,7 @@ int pick_bn(int64_t N, int b_mode) {
 int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int bn, int splits, cudaStream_t s,
              bool halo = false, bool tf = false) {
   if (tf) {
+    if (halo) return launch<64, true, true>(ta, tb, p, 1, s);
     switch (bn) {
       case 16: return launch<16, false, true>(ta, tb, p, splits, s);
       case 64: return launch<64, false, true>(ta, tb, p, splits, s);
@@ -2056,6 +2167,12 @@ bool wide_filter_enabled() {
   return on;
 }
 
+bool halo_tf_fits(int OH, int OW) {
+  const int W1 = OW + 1;
+  const int rows = (OW + kBM - 1) / W1 + 3;
+  return OH >= 1 && W1 <= 256 && rows <= 256 && 2u * (uint32_t)(rows * W1) * 128u <= HaloTfCfg::kASlotBytes;
+}
+
 bool halo_fits(int OH, int OW) {
   const int W1 = OW + 1;
   const int rows = (OW + kBM - 1) / W1 + 3;
@@ -2073,6 +2190,7 @@ int preload_gemm() {
   DBS_CUDA_TRY(cudaFuncSetAttribute(halo_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Halo2Cfg::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<16, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgTf<16>::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgTf<64>::kSmem));
+  DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<64, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloTfCfg::kSmem));
   DBS_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_kernel<128, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgTf<128>::kSmem));
   return DBS_OK;
 }
@@ -2232,6 +2350,44 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
     bn = pick;
   }
   int st;
+  if (c.halo) {
+    // ---- fp32-class halo variant: 3x3 / stride 1 / 64 -> 64 channels (HaloTfCfg) ----
+    const ConvGeom& g = c.ga;
+    DBS_REQUIRE(c.a_mode == 2 && (c.b_mode == 0 || c.b_mode == 3) && g.R == 3 && g.S == 3 && g.stride == 1 &&
+                    g.pad == 1 && g.cblocks == 2 && c.N == 64 && c.K == 576 && c.taps.n == 0 && !c.omap.on &&
+                    c.nclass == 0 && c.splits <= 1 && !c.d_trans && halo_tf_fits(g.OH, g.OW) && c.ta.H == g.OH &&
+                    c.ta.W == g.OW && c.ta.C == 64,
+                DBS_ERR_ARGUMENT, "conv halo variant (S32): unsupported geometry");
+    const int W1 = g.OW + 1;
+    p.halo_rows = (g.OW + kBM - 1) / W1 + 3;
+    p.halo_tpi = (g.OH * W1 + kBM - 1) / kBM;
+    p.halo_tiles = (int64_t)c.ta.N * p.halo_tpi;
+    const ConvTensor t4{c.ta.N, c.ta.H, c.ta.W, 4 * c.ta.C};
+    st = make_tmap_nhwc_pair(&ta, c.a, t4, W1, p.halo_rows, 1, 1);  // {64, W + 1, rows, 1, hi/lo}
+    if (st) return st;
+    if (c.b_mode == 0) {
+      DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
+      st = make_tmap_kpair(&tb, c.b, (uint64_t)(4 * ceil32(c.K)), (uint64_t)c.N, (uint64_t)(4 * c.ldb), 64u);
+    } else {
+      EncodeTiledFn fn = encode_fn();
+      DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+      const uint64_t cin = (uint64_t)c.tb.C, rs = (uint64_t)c.tb.W;
+      cuuint64_t dims[5] = {64, (cuuint64_t)c.tb.N, (cuuint64_t)(cin / 32), 2, (cuuint64_t)rs};
+      cuuint64_t strides[4] = {(cuuint64_t)(rs * cin * 8), 256, 128, (cuuint64_t)(cin * 8)};
+      cuuint32_t box[5] = {64, 32, 2, 2, 1};
+      cuuint32_t es[5] = {1, 1, 1, 1, 1};
+      CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(c.b), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, kMnSwz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      DBS_REQUIRE(r == CUDA_SUCCESS, DBS_ERR_CUDA, "cuTensorMapEncodeTiled (S32 halo filter) failed (%d)", (int)r);
+      st = DBS_OK;
+    }
+    if (st) return st;
+    p.a_mode = 2;
+    p.b_mode = c.b_mode;
+    p.kb_per_split = 18;
+    return dispatch(ta, tb, p, 64, 1, s, true, true);
+  }
   // ---- A ----
   p.a_mode = c.a_mode;
   if (c.a_mode == 2) {

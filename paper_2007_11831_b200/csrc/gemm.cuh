@@ -85,6 +85,7 @@ int gemm_tf(const void* a, int a_mn, int64_t lda, const void* b, int b_mn, int64
 int preload_gemm();
 // the halo variant's one-box-per-tile input halo fits its shared-memory slot
 bool halo_fits(int OH, int OW);
+bool halo_tf_fits(int OH, int OW);  // fp32-class halo variant (gemm.cu HaloTfCfg)
 // SMs of the current (possibly green) context -- what a launch issued now can use
 int current_sm_count();
 

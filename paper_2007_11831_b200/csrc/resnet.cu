@@ -1476,6 +1476,19 @@ bool halo_ok(const Conv& c) {
   }();
   return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 && halo_fits(c.OH, c.OW);
 }
+// the fp32-class (S32) halo variant (gemm.cu HaloTfCfg): same shape, W <= 32.
+// Off by default (DBS_HALO_TF=1 enables it): it moves 22 KB per k-block instead of
+// 48 KB, but the streamed kernel is not ingest-bound -- traced in-kernel, both spend
+// ~600 cycles issuing one k-block's 8 MMAs (+ ~220 waiting on the ring) -- so the
+// halo's 1/(W + 1) junk positions made it 10% slower.
+bool halo_tf_ok(const Conv& c) {
+  static const bool enabled = [] {
+    const char* e = getenv("DBS_HALO_TF");
+    return e && e[0] == '1';
+  }();
+  return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 &&
+         halo_tf_fits(c.OH, c.OW);
+}
 
 // the operand copy of the parameter at flat offset `off` (bf16 or S32 shadow)
 const void* wptr(const dbs_resnet* m, const void* shadow, int64_t off) {
@@ -1516,7 +1529,7 @@ int conv_fwd(dbs_resnet* m, int ci, const void* x, const void* shadow, int64_t B
     call.ta = nhwc(B, c.H, c.W, c.cin);
     call.ga = ConvGeom{c.k, c.k, c.cin / (f32 ? 32 : 64), c.stride, c.pad, c.OH, c.OW, c.cin};
     call.ldb = call.K;
-    call.halo = !f32 && halo_ok(c);
+    call.halo = f32 ? halo_tf_ok(c) : halo_ok(c);
   }
   int st = conv_gemm(call, s);
   if (st) return st;
@@ -1638,7 +1651,7 @@ int conv_dgrad_ex(const Conv& c, const void* dy, const void* w, int64_t B, void*
     call.M = B * c.H * c.W;
     call.K = (int64_t)c.k * c.k * c.cout;
     call.ga = ConvGeom{c.k, c.k, c.cout / cb, 1, c.k / 2, c.H, c.W, c.cout};
-    call.halo = !tf && halo_ok(c);
+    call.halo = tf ? halo_tf_ok(c) : halo_ok(c);
     return conv_gemm(call, s);
   }
   // stride 2: one GEMM per output parity class (a, b).  dX(2i+a, 2j+b) gathers
@@ -2278,6 +2291,7 @@ extern "C" int dbs_dev_conv2d_fwd_s32(const void* d_x, int32_t N, int32_t H, int
     call.a = d_x;
     call.ta = nhwc(N, H, W, Cin);
     call.ga = ConvGeom{k, k, Cin / 32, stride, pad, c.OH, c.OW, Cin};
+    call.halo = halo_tf_ok(c);
   }
   call.epi = DBS_EPI_F32;
   call.d = d_y;

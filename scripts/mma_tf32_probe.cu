@@ -165,7 +165,103 @@ void run(int fill, int shift, const uint8_t* g) {
   cudaFree(d);
 }
 
+
+// The 3xTF32 issue pattern of one 32-wide k-block (4 k-steps): A_hi x [B_hi | B_lo]
+// (N = 2 BN into [main | corr]) and A_lo x B_hi (N = BN) --
+//   pat 0: alternating, the second into corr (overlaps the first's columns)
+//   pat 1: grouped -- the 4 N = 2 BN MMAs, then the 4 N = BN ones (same accumulators)
+//   pat 2: alternating, the second into a separate accumulator (no overlap)
+template <int BN>
+__global__ void __launch_bounds__(128, 1) pattern(int reps, int pat, unsigned long long* out) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t done, ring[8];
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  const bool rnd = pat >= 10;
+  pat %= 10;
+  const bool rot = pat == 4;  // rotate the operands over 4 slots of 48 KB (a ring), no reuse between k-blocks
+  for (int i = threadIdx.x; i < (rot ? 4 * 49152 : kOpBytes) / 4; i += blockDim.x) {
+    // rnd: N(0,1)-like fp32 values (random mantissas, exponents around 1), else zeros
+    uint32_t h = (uint32_t)i * 2654435761u ^ 0x9e3779b9u;
+    h ^= h >> 15;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    const float v = rnd ? __uint_as_float(0x3f000000u | (h & 0x807FFFFFu)) : 0.0f;
+    reinterpret_cast<float*>(sm)[i] = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    for (int q = 0; q < 8; q++) mbar_init(&ring[q], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a_hi0 = smem_u32(sm), a_lo0 = a_hi0 + 16384, b0 = smem_u32(sm + 32768);
+    const uint32_t id2 = make_idesc_tf32(128, 2 * BN, 0, 0), id1 = make_idesc_tf32(128, BN, 0, 0);
+    const uint32_t corr = pat == 2 ? tmem + 2 * BN : tmem + BN;
+    const long long t0 = clock64();
+    for (int i = 0; i < reps; i++) {
+      const uint32_t rs = rot ? (uint32_t)(i & 3) * 49152u : 0u;
+      const uint32_t a_hi = a_hi0 + rs, a_lo = a_lo0 + rs, b = b0 + rs;
+      if (pat == 1) {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32_ss(tmem, make_sdesc(a_hi + k * 32, 16, 1024), make_sdesc(b + k * 32, 16, 1024), id2, (i | k) != 0);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32_ss(corr, make_sdesc(a_lo + k * 32, 16, 1024), make_sdesc(b + k * 32, 16, 1024), id1, 1u);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          mma_tf32_ss(tmem, make_sdesc(a_hi + k * 32, 16, 1024), make_sdesc(b + k * 32, 16, 1024), id2, (i | k) != 0);
+          mma_tf32_ss(corr, make_sdesc(a_lo + k * 32, 16, 1024), make_sdesc(b + k * 32, 16, 1024), id1, 1u);
+        }
+        // pat 3: a commit to a (never waited) mbarrier after every k-block, as the GEMM's ring does
+        if (pat == 3) mma_commit(&ring[i & 7]);
+      }
+    }
+    mma_commit(&done);
+    mbar_wait(&done, 0);
+    out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <int BN>
+void run_pattern(int pat) {
+  unsigned long long* d;
+  cudaMalloc(&d, 8 * 2048);
+  const int smem = 4 * 49152 + 2048;
+  cudaFuncSetAttribute(pattern<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int reps = 1000;
+  for (int w = 0; w < 2; w++) pattern<BN><<<148, 128, smem>>>(reps, pat, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, 8 * 148, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; i++) avg += (double)h[i];
+  avg /= 148;
+  const double per = avg / reps;  // one k-block = 4 k-steps x 2 MMAs
+  const double ideal = 3.0 * 128 * BN * 32 / 2048;
+  printf("3xTF32 BN=%3d pattern %2d (>= 10: random data): %6.1f clk per 32-wide k-block (ideal %5.1f, %3.0f%%)  %s\n", BN, pat, per, ideal,
+         100 * ideal / per, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
+  for (int pat : {0, 3, 4, 13, 14}) {
+    run_pattern<64>(pat);
+    run_pattern<128>(pat);
+  }
+
   uint8_t* g;
   cudaMalloc(&g, 16 << 20);
   cudaMemset(g, 1, 16 << 20);

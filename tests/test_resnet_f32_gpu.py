@@ -31,6 +31,12 @@ R18_SHAPES = [  # N, H, Cin, Cout, k, stride
     (16, 4, 512, 512, 3, 1),
     (3, 8, 256, 256, 3, 1),
 ]
+HALO_SHAPES = [  # the fp32-class halo variant (3x3 / 1, 64 -> 64, W <= 32): ragged image counts and widths
+    (1, 32, 64, 64, 3, 1),
+    (3, 16, 64, 64, 3, 1),
+    (2, 20, 64, 64, 3, 1),
+    (5, 7, 64, 64, 3, 1),
+]
 R50_SHAPES = [
     (2, 56, 64, 64, 3, 1),
     (2, 56, 64, 256, 1, 1),
@@ -61,7 +67,7 @@ def _rel(got, want):
     return float((got.double() - want.double()).norm() / (want.double().norm() + 1e-300))
 
 
-@pytest.mark.parametrize("N,H,Cin,Cout,k,stride", R18_SHAPES + R50_SHAPES)
+@pytest.mark.parametrize("N,H,Cin,Cout,k,stride", R18_SHAPES + HALO_SHAPES + R50_SHAPES)
 def test_conv_s32_fwd_dgrad_wgrad_vs_fp64(dev, N, H, Cin, Cout, k, stride):
     import torch
     import torch.nn.functional as F
@@ -257,3 +263,19 @@ def test_bench_cpu_inputs_match_package(dev):
     for f, g, args in ((O.synthetic_cifar, resnet.synthetic_cifar, (10,)), (O.synthetic_mnist, mlp.synthetic_mnist, (10,)),
                        (O.synthetic_imagenet, resnet.synthetic_imagenet, (3, 64, 10))):
         assert all(np.array_equal(x, y) for x, y in zip(f(*args, seed=2), g(*args, seed=2)))
+
+
+def test_conv_s32_halo_variant(dev):
+    """The experimental fp32-class halo kernel (DBS_HALO_TF=1, read once per process:
+    run in a child) on the 64->64 3x3 shapes, fwd and dgrad at the same 5e-6 bound."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBS_HALO_TF="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", str(Path(__file__).resolve()),
+                        "-k", "conv_s32_fwd_dgrad_wgrad and 64-64-3-1"],
+                       env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
