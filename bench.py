@@ -286,7 +286,40 @@ def run_strategy(tr, wl, kind, args, world=1):
             "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
-TF32_DENSE_TFLOPS = 1100.0  # B200 dense tf32 tensor rate, B200_PROFILING.md (no measured tf32 figure)
+TF32_DENSE_TFLOPS = 1100.0  # B200 dense tf32 tensor rate, B200_PROFILING.md (nominal, for context)
+
+
+def measure_tf32_peak(reps=10):
+    """Measured dense tf32 tensor rate of this GPU, the same recipe as the driver's bf16
+    burst figure in MEASURED_PEAKS.json: a cuBLAS 8192^3 fp32 matmul with TF32 math
+    (torch.backends.cuda.matmul.allow_tf32), best of `reps`, CUDA events.  Library code
+    used only as the roofline denominator, never on the measured path."""
+    import torch
+
+    n = 8192
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        c = torch.empty(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        torch.cuda.synchronize()
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None or t < best else best
+        del a, b, c
+        torch.cuda.empty_cache()
+        return 2.0 * n ** 3 / best / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 ROOFLINE_CONV = {
     # workload -> (H, Cin, Cout, k, stride, description): the dominant conv shape
@@ -367,7 +400,8 @@ def kernel_roofline(peaks, wl, precision, tr=None):
     # fp32 class: 3 kind::tf32 MMAs per product at the tf32 dense rate (no measured tf32 peak in
     # MEASURED_PEAKS.json: B200_PROFILING.md's 1.1 PFLOP/s dense tf32, which the 256-/512-channel
     # convs of this kernel reach ~0.8 of); bf16: the measured dense bf16 rate
-    peak_full = TF32_DENSE_TFLOPS / 3.0 if f32 else peaks["bf16_tflops"]
+    tf32 = measure_tf32_peak() if f32 else None
+    peak_full = tf32 / 3.0 if f32 else peaks["bf16_tflops"]
     peak = peak_full * share
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic_r2.json"
@@ -385,10 +419,12 @@ def kernel_roofline(peaks, wl, precision, tr=None):
             "algorithmic_bytes_per_launch": (8.0 if f32 else 2.0) * (N * H * H * C + Co * k * k * C) +
                                             (4.0 if f32 else 2.0) * N * OH * OH * Co,
             "avg_launch_us": round(dur * 1e6, 2), "partition_sms": sms,
-            "peak_note": (f"tf32 dense {TF32_DENSE_TFLOPS:.0f} TF/s (B200_PROFILING.md) / 3 MMAs per fp32-class "
-                          f"product x {sms}/148 SMs" if f32 else
+            "peak_note": (f"measured tf32 dense {tf32:.0f} TF/s (cuBLAS 8192^3, best of 10, this run) / 3 MMAs per "
+                          f"fp32-class product x {sms}/148 SMs" if f32 else
                           f"measured bf16 {peaks['bf16_tflops']} TF/s x {sms}/148 SMs"),
-            "peak_source": "B200_PROFILING.md fallback (tf32)" if f32 else peaks["source"]}
+            "peak_source": "measured (tf32, in bench.py)" if f32 else peaks["source"],
+            **({"frac_of_nominal": round(achieved / (TF32_DENSE_TFLOPS / 3.0 * share), 4),
+                "tf32_measured_tflops": round(tf32, 1)} if f32 else {})}
 
 
 def _graph_time(launch, reps=20):

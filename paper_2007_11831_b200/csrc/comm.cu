@@ -109,7 +109,7 @@ __device__ __forceinline__ uint32_t bf16_bits(float f) {
 // mode 0: gradient all-reduce + SGD;  mode 1: parameter averaging
 // BF16: also push the bf16 operand shadow (an S32-shadow communicator refreshes its own)
 template <int MODE, bool BF16>
-__global__ void __launch_bounds__(kThreads) fused_kernel(PeerTable T, int rank, int world, int64_t shard4,
+__global__ void __launch_bounds__(kThreads, 2) fused_kernel(PeerTable T, int rank, int world, int64_t shard4,
                                                          float lr, float mom, float4* __restrict__ vel,
                                                          uint32_t gen) {
   uint32_t* my_sig = T.signal[rank];
@@ -121,44 +121,67 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(PeerTable T, int rank, 
   }
   __syncthreads();
   // ---- phase 1: reduce my shard, update, push to every peer -----------------
+  // kUnroll float4s per thread and trip, every peer's loads issued before any use:
+  // up to 8 x kUnroll 16-byte NVLink reads in flight per thread (latency-bound otherwise)
+  constexpr int kUnroll = 2;
   const int64_t base4 = (int64_t)rank * shard4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < shard4; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p4 = base4 + i;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < shard4; i0 += stride * kUnroll) {
+    float4 acc[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 g[kMaxRanks][kUnroll];
 #pragma unroll
     for (int j = 0; j < kMaxRanks; j++) {
       if (j >= world) break;
-      const float4* src = reinterpret_cast<const float4*>(MODE == 0 ? T.grad[j] : T.param[j]) + p4;
-      const float4 g = __ldcv(src);  // peer memory over NVLink, bypass stale caches
+      const float4* src = reinterpret_cast<const float4*>(MODE == 0 ? T.grad[j] : T.param[j]) + base4;
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const int64_t i = i0 + u * stride;
+        g[j][u] = i < shard4 ? __ldcv(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);  // peer memory, no stale caches
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; j++) {
+      if (j >= world) break;
       const float w = T.w[j];
-      acc.x = fmaf(w, g.x, acc.x);
-      acc.y = fmaf(w, g.y, acc.y);
-      acc.z = fmaf(w, g.z, acc.z);
-      acc.w = fmaf(w, g.w, acc.w);
-    }
-    float4 x;
-    if (MODE == 0) {
-      float4 v = vel[i];
-      x = reinterpret_cast<const float4*>(T.param[rank])[p4];
-      v.x = fmaf(mom, v.x, acc.x);
-      v.y = fmaf(mom, v.y, acc.y);
-      v.z = fmaf(mom, v.z, acc.z);
-      v.w = fmaf(mom, v.w, acc.w);
-      x.x = fmaf(-lr, v.x, x.x);
-      x.y = fmaf(-lr, v.y, x.y);
-      x.z = fmaf(-lr, v.z, x.z);
-      x.w = fmaf(-lr, v.w, x.w);
-      vel[i] = v;
-    } else {
-      x = acc;
-    }
-    const uint2 xb = make_uint2(bf16_bits(x.x) | (bf16_bits(x.y) << 16), bf16_bits(x.z) | (bf16_bits(x.w) << 16));
 #pragma unroll
-    for (int j = 0; j < kMaxRanks; j++) {
-      if (j >= world) break;
-      const int jj = (rank + j) % world;  // stagger the peers to spread NVLink traffic
-      reinterpret_cast<float4*>(T.param[jj])[p4] = x;
-      if (BF16) reinterpret_cast<uint2*>(T.param_bf16[jj])[p4] = xb;
+      for (int u = 0; u < kUnroll; u++) {
+        acc[u].x = fmaf(w, g[j][u].x, acc[u].x);
+        acc[u].y = fmaf(w, g[j][u].y, acc[u].y);
+        acc[u].z = fmaf(w, g[j][u].z, acc[u].z);
+        acc[u].w = fmaf(w, g[j][u].w, acc[u].w);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++) {
+      const int64_t i = i0 + u * stride;
+      if (i >= shard4) break;
+      const int64_t p4 = base4 + i;
+      float4 x;
+      if (MODE == 0) {
+        float4 v = vel[i];
+        x = reinterpret_cast<const float4*>(T.param[rank])[p4];
+        v.x = fmaf(mom, v.x, acc[u].x);
+        v.y = fmaf(mom, v.y, acc[u].y);
+        v.z = fmaf(mom, v.z, acc[u].z);
+        v.w = fmaf(mom, v.w, acc[u].w);
+        x.x = fmaf(-lr, v.x, x.x);
+        x.y = fmaf(-lr, v.y, x.y);
+        x.z = fmaf(-lr, v.z, x.z);
+        x.w = fmaf(-lr, v.w, x.w);
+        vel[i] = v;
+      } else {
+        x = acc[u];
+      }
+      const uint2 xb = make_uint2(bf16_bits(x.x) | (bf16_bits(x.y) << 16), bf16_bits(x.z) | (bf16_bits(x.w) << 16));
+#pragma unroll
+      for (int j = 0; j < kMaxRanks; j++) {
+        if (j >= world) break;
+        const int jj = (rank + j) % world;  // stagger the peers to spread NVLink traffic
+        reinterpret_cast<float4*>(T.param[jj])[p4] = x;
+        if (BF16) reinterpret_cast<uint2*>(T.param_bf16[jj])[p4] = xb;
+      }
     }
   }
   // ---- phase 2: all shards written everywhere --------------------------------
@@ -242,8 +265,8 @@ static int comm_new(int32_t rank, int32_t world, int64_t P, dbs_comm** out) {
   c->shard = c->P / world;
   size_t op, ob, os;
   c->block_bytes = block_layout(c->P, &op, &ob, &os);
-  const int64_t want = (c->shard / 4 + kThreads - 1) / kThreads;
-  const int64_t cap = (int64_t)num_sms() * 2;
+  const int64_t want = (c->shard / 4 + 2 * kThreads - 1) / (2 * kThreads);  // 2 float4 per thread and trip
+  const int64_t cap = (int64_t)num_sms() * 2;  // 2 x 256 threads x 2 float4 x (W peers + x + v) in flight per SM
   c->grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   *out = c;
   return DBS_OK;

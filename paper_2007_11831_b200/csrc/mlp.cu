@@ -44,6 +44,7 @@ struct dbs_mlp {
   void* dz = nullptr;           // [max_b][16] bf16 | [max_b][32] S32
   void* dh = nullptr;           // [max_b][hid] bf16 | S32
   float* colsum = nullptr;      // [ceil(max_b/32)][hid]
+  void* xstage = nullptr;       // [max_b] input rows of the current iteration (device-indexed iterations)
 };
 
 namespace dbs {
@@ -60,9 +61,14 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
 
 // One CTA: mean cross-entropy over b rows, dZ = (softmax - onehot)/b (bf16),
 // db2 = sum_rows dZ (fp32, deterministic block reduction), loss.
-__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ z, const int32_t* __restrict__ y,
+__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ z, const int32_t* __restrict__ y_base,
                                                          int64_t b, int cls, uint16_t* __restrict__ dz,
-                                                         float* __restrict__ db2, float* __restrict__ loss) {
+                                                         float* __restrict__ db2, float* __restrict__ loss,
+                                                         const int64_t* __restrict__ d_iter, int loss_indexed) {
+  // device-indexed iteration (graph replays): rows t*b.. of the shard's labels, loss slot t
+  const int64_t t_it = d_iter ? *d_iter : 0;
+  const int32_t* __restrict__ y = y_base + t_it * b;
+  if (loss_indexed) loss += t_it;
   __shared__ float red[8][17];
   float acc[16];
   float lsum = 0.0f;
@@ -115,9 +121,14 @@ __device__ __forceinline__ float rn_tf32(float x) {
   const uint32_t u = __float_as_uint(x);
   return __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
 }
-__global__ void __launch_bounds__(256) softmax_ce_s32_kernel(const float* __restrict__ z, const int32_t* __restrict__ y,
+__global__ void __launch_bounds__(256) softmax_ce_s32_kernel(const float* __restrict__ z, const int32_t* __restrict__ y_base,
                                                              int64_t b, int cls, float* __restrict__ dz,
-                                                             float* __restrict__ db2, float* __restrict__ loss) {
+                                                             float* __restrict__ db2, float* __restrict__ loss,
+                                                         const int64_t* __restrict__ d_iter, int loss_indexed) {
+  // device-indexed iteration (graph replays): rows t*b.. of the shard's labels, loss slot t
+  const int64_t t_it = d_iter ? *d_iter : 0;
+  const int32_t* __restrict__ y = y_base + t_it * b;
+  if (loss_indexed) loss += t_it;
   __shared__ float red[8][17];
   float acc[16];
   float lsum = 0.0f;
@@ -166,6 +177,17 @@ __global__ void __launch_bounds__(256) softmax_ce_s32_kernel(const float* __rest
   }
 }
 
+// device-indexed iteration: rows [t b, (t + 1) b) of the worker's shard (t = *d_iter)
+// -> the fixed staging rows every GEMM of the iteration reads (graph replays keep
+// their TMA descriptors; 16-byte vectors, row bytes a multiple of 16)
+__global__ void __launch_bounds__(256) stage_rows_kernel(const uint4* __restrict__ shard, const int64_t* __restrict__ d_iter,
+                                                         int64_t b, int64_t row_vec, uint4* __restrict__ out) {
+  const int64_t n = b * row_vec;
+  const uint4* src = shard + (*d_iter) * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[i];
+}
+
 // db1[n] = sum_g part[g][n] over g < groups (fixed order => deterministic)
 __global__ void colsum_reduce_kernel(const float* __restrict__ part, int64_t groups, int64_t n,
                                      float* __restrict__ out) {
@@ -181,7 +203,7 @@ __global__ void colsum_reduce_kernel(const float* __restrict__ part, int64_t gro
 // fp32-class forward/backward: the same 5 GEMMs on S32 operands (3xTF32).  x is the
 // S32 input [b][in_ld], the shadow the flat S32 parameter vector (W1 [H][in_ld])
 int mlp_fwd_bwd_f32(dbs_mlp* m, const float* sh, const float* pf, const float* x, const int32_t* y, int64_t b,
-                    float* grad, float* loss, cudaStream_t s) {
+                    float* grad, float* loss, cudaStream_t s, const int64_t* d_iter, int loss_indexed) {
   int st;
   const int64_t I = m->in_ld, H = m->hid, C = m->cls;
   const float* w1 = sh + 2 * m->off_w1;
@@ -190,7 +212,8 @@ int mlp_fwd_bwd_f32(dbs_mlp* m, const float* sh, const float* pf, const float* x
   if (st) return st;
   st = gemm_tf(m->act, 0, H, w2, 0, H, m->logits, kLdZ, b, C, H, DBS_EPI_BIAS_F32, pf + m->off_b2, nullptr, s, nullptr);
   if (st) return st;
-  softmax_ce_s32_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, static_cast<float*>(m->dz), grad + m->off_b2, loss);
+  softmax_ce_s32_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, static_cast<float*>(m->dz), grad + m->off_b2, loss,
+                                          d_iter, loss_indexed);
   DBS_LAUNCH_CHECK();
   // dW2 [C][H] = dZ^T H  (dZ S32 [b][32] MN-major, M = C)
   st = gemm_tf(m->dz, 1, 32, m->act, 1, H, grad + m->off_w2, H, C, H, b, DBS_EPI_F32, nullptr, nullptr, s, nullptr);
@@ -207,14 +230,31 @@ int mlp_fwd_bwd_f32(dbs_mlp* m, const float* sh, const float* pf, const float* x
   return gemm_tf(m->dh, 1, H, x, 1, I, grad + m->off_w1, I, H, I, b, DBS_EPI_F32, nullptr, nullptr, s, nullptr);
 }
 
+// d_iter != nullptr: x_any / y are the worker's whole shard and the iteration index t
+// is read on the device (rows t b.. staged into m->xstage; labels and, with
+// loss_indexed, the loss slot t offset by the kernels) -- every launch argument is
+// then iteration-invariant, so one iteration can be captured in a CUDA graph.
 int mlp_fwd_bwd(dbs_mlp* m, const void* shadow, const float* pf, const void* x_any, const int32_t* y, int64_t b,
-                float* grad, float* loss, cudaStream_t s) {
+                float* grad, float* loss, cudaStream_t s, const int64_t* d_iter, int loss_indexed) {
   DBS_REQUIRE(m && shadow && pf && x_any && y && grad && loss, DBS_ERR_ARGUMENT, "mlp: null argument");
   DBS_REQUIRE(b >= 1 && b <= m->max_b, DBS_ERR_ARGUMENT, "mlp: batch %lld outside [1, %lld]", (long long)b,
               (long long)m->max_b);
+  if (d_iter) {
+    const int64_t row_bytes = m->prec == DBS_PREC_F32 ? 8 * m->in_ld : 2 * m->in;
+    DBS_REQUIRE(row_bytes % 16 == 0 && ((uintptr_t)x_any & 15) == 0, DBS_ERR_ARGUMENT,
+                "mlp: device-indexed rows need 16-byte rows");
+    const int64_t vec = row_bytes / 16;
+    const int64_t blocks = (b * vec + 255) / 256;
+    stage_rows_kernel<<<(unsigned)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(
+        static_cast<const uint4*>(x_any), d_iter, b, vec, static_cast<uint4*>(m->xstage));
+    DBS_LAUNCH_CHECK();
+    x_any = m->xstage;
+  } else {
+    loss_indexed = 0;
+  }
   if (m->prec == DBS_PREC_F32)
     return mlp_fwd_bwd_f32(m, static_cast<const float*>(shadow), pf, static_cast<const float*>(x_any), y, b, grad, loss,
-                           s);
+                           s, d_iter, loss_indexed);
   const uint16_t* pb = static_cast<const uint16_t*>(shadow);
   const uint16_t* x = static_cast<const uint16_t*>(x_any);
   int st;
@@ -228,7 +268,8 @@ int mlp_fwd_bwd(dbs_mlp* m, const void* shadow, const float* pf, const void* x_a
                  nullptr, s, nullptr);
   if (st) return st;
   // 3. softmax cross-entropy + db2
-  softmax_ce_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, static_cast<uint16_t*>(m->dz), grad + m->off_b2, loss);
+  softmax_ce_kernel<<<1, 256, 0, s>>>(m->logits, y, b, (int)C, static_cast<uint16_t*>(m->dz), grad + m->off_b2, loss,
+                                      d_iter, loss_indexed);
   DBS_LAUNCH_CHECK();
   // 4. dW2 = dZ^T H
   st = gemm_bf16(m->dz, 1, kLdZ, m->act, 1, H, grad + m->off_w2, H, C, H, b, DBS_EPI_F32, nullptr, nullptr, s,
@@ -284,6 +325,7 @@ extern "C" int dbs_mlp_create_ex(int64_t in_dim, int64_t hidden, int64_t classes
   e = e ? e : cudaMalloc(&m->dz, f32 ? es * max_batch * 32 : es * max_batch * kLdZ);
   e = e ? e : cudaMalloc(&m->dh, es * max_batch * hidden);
   e = e ? e : cudaMalloc(&m->colsum, sizeof(float) * groups * hidden);
+  e = e ? e : cudaMalloc(&m->xstage, (f32 ? 8 * m->in_ld : 2 * in_dim) * max_batch);
   if (e != cudaSuccess) {
     set_error("mlp_create: %s", cudaGetErrorString(e));
     dbs_mlp_destroy(m);
@@ -311,6 +353,7 @@ extern "C" int dbs_mlp_destroy(dbs_mlp* m) {
   cudaFree(m->dz);
   cudaFree(m->dh);
   cudaFree(m->colsum);
+  cudaFree(m->xstage);
   delete m;
   return DBS_OK;
 }
@@ -324,7 +367,7 @@ extern "C" int dbs_mlp_param_count(const dbs_mlp* m, int64_t* out) {
 extern "C" int dbs_mlp_forward_backward(dbs_mlp* m, const void* d_params_shadow, const float* d_params,
                                         const void* d_x, const int32_t* d_labels, int64_t batch,
                                         float* d_grad, float* d_loss, void* stream) {
-  return mlp_fwd_bwd(m, d_params_shadow, d_params, d_x, d_labels, batch, d_grad, d_loss, as_stream(stream));
+  return mlp_fwd_bwd(m, d_params_shadow, d_params, d_x, d_labels, batch, d_grad, d_loss, as_stream(stream), nullptr, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -427,10 +470,8 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
                                const int64_t* rank_batches) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "run_iterations: bad arguments");
   for (int i = 0; i < n; i++)
-    DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18) &&
-                    !(d_iter && w[i].model_kind == DBS_MODEL_MLP),
-                DBS_ERR_ARGUMENT, "run_iterations: worker %d has a bad model (device iteration index is ResNet-only)",
-                i);
+    DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18),
+                DBS_ERR_ARGUMENT, "run_iterations: worker %d has a bad model", i);
   const int prec = slot_precision(w[0]);
   for (int i = 1; i < n; i++)
     DBS_REQUIRE(slot_precision(w[i]) == prec, DBS_ERR_ARGUMENT, "run_iterations: workers mix operand precisions");
@@ -466,9 +507,14 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
       const int64_t b = w[i].batch;
       if (w[i].model_kind == DBS_MODEL_MLP) {
         dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
-        const char* x = static_cast<const char*>(w[i].x_shard) + t * b * slot_row_bytes(w[i]);
-        st = mlp_fwd_bwd(m, d_shadow, d_params, x, w[i].y_shard + t * b, b, w[i].grad,
-                         w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
+        if (d_iter) {  // device-indexed iteration (graph capture): the kernels offset by *d_iter
+          st = mlp_fwd_bwd(m, d_shadow, d_params, w[i].x_shard, w[i].y_shard, b, w[i].grad,
+                           w[i].loss ? w[i].loss : w[i].loss_scratch, s, d_iter, w[i].loss ? 1 : 0);
+        } else {
+          const char* x = static_cast<const char*>(w[i].x_shard) + t * b * slot_row_bytes(w[i]);
+          st = mlp_fwd_bwd(m, d_shadow, d_params, x, w[i].y_shard + t * b, b, w[i].grad,
+                           w[i].loss ? w[i].loss + t : w[i].loss_scratch, s, nullptr, 0);
+        }
       } else {
         dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
         const uint8_t* x = static_cast<const uint8_t*>(w[i].x_shard);
@@ -608,7 +654,7 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
         if (w[i].model_kind == DBS_MODEL_MLP) {
           dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
           st = mlp_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, b, w[i].grad,
-                           w[i].loss ? w[i].loss + t : w[i].loss_scratch, s);
+                           w[i].loss ? w[i].loss + t : w[i].loss_scratch, s, nullptr, 0);
         } else {
           dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
           st = resnet_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,

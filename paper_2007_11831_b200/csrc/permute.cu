@@ -67,11 +67,13 @@ __global__ void __launch_bounds__(32) draws_kernel(dbs_pcg64* rng, const int64_t
   int cur = 0;          // next unconsumed position of the window [0, 64)
   int last_pos = -1;    // last consumed position inside the current window
   bool drew = false;    // any fresh output consumed at all
+  uint32_t prev_hi31 = stale_u;  // upper half of the previous window's last output
   int64_t off = 0;
   int ok = 1;
   auto advance = [&]() {
     const uint64_t hi31 = __shfl_sync(0xffffffffu, (uint64_t)(st >> 64), 31);
     const uint64_t lo31 = __shfl_sync(0xffffffffu, (uint64_t)st, 31);
+    prev_hi31 = __shfl_sync(0xffffffffu, vhi, 31);
     S = ((u128)hi31 << 64) | lo31;
     st = A * S + C;
     o = xsl_rr(st);
@@ -80,6 +82,9 @@ __global__ void __launch_bounds__(32) draws_kernel(dbs_pcg64* rng, const int64_t
     cur = 0;
     last_pos = -1;
   };
+  // Per draw: two ballots and no shuffles on the serial chain -- the accepting
+  // position follows from the ballots alone (first accepting lane; its low half
+  // if that accepted, else its high half) and the accepting lane writes j itself.
   for (int64_t s = 0; s < n && ok; s++) {
     const int64_t start = spans[2 * s], L = spans[2 * s + 1] - start;
     if (L < 0 || L > 0x7fffffffLL) {
@@ -97,49 +102,45 @@ __global__ void __launch_bounds__(32) draws_kernel(dbs_pcg64* rng, const int64_t
           continue;
         }
       }
-      uint32_t j;
       for (;;) {
         const bool plo = (cur <= 2 * lane) && ((vlo & mask) <= mx);
         const bool phi = (cur <= 2 * lane + 1) && ((vhi & mask) <= mx);
         const unsigned any = __ballot_sync(0xffffffffu, plo || phi);
+        drew = true;
         if (any) {
+          const unsigned anylo = __ballot_sync(0xffffffffu, plo);
           const int l0 = __ffs(any) - 1;
-          const int pos_l = plo ? 2 * lane : 2 * lane + 1;
-          const int pos = __shfl_sync(0xffffffffu, pos_l, l0);
-          const uint32_t v = __shfl_sync(0xffffffffu, (pos & 1) ? vhi : vlo, l0);
-          stale_u = __shfl_sync(0xffffffffu, vhi, l0);
-          j = v & mask;
+          const int pos = ((anylo >> l0) & 1u) ? 2 * l0 : 2 * l0 + 1;
+          if (lane == l0) draws[off + i] = (int32_t)(((pos & 1) ? vhi : vlo) & mask);
           cur = pos + 1;
           last_pos = pos;
-          drew = true;
           break;
         }
-        // every remaining draw of the window was rejected (and consumed)
-        stale_u = __shfl_sync(0xffffffffu, vhi, 31);
-        drew = true;
-        advance();
+        advance();  // every remaining draw of the window was rejected (and consumed)
       }
-      if (lane == 0) draws[off + i] = (int32_t)j;
       if (cur >= 64) advance();
     }
     off += L;
   }
-  // Final generator state, numpy field for field.
+  // Final generator state, numpy field for field.  numpy keeps the upper half of the
+  // last 64-bit output drawn (consumed or not) in `uinteger`.
   const int l = last_pos >= 0 ? (last_pos >> 1) : 0;
   const uint64_t hi_l = __shfl_sync(0xffffffffu, (uint64_t)(st >> 64), l);
   const uint64_t lo_l = __shfl_sync(0xffffffffu, (uint64_t)st, l);
+  const uint32_t vhi_l = __shfl_sync(0xffffffffu, vhi, l);
   if (lane == 0) {
     if (last_pos >= 0) {
       rng->state_hi = hi_l;
       rng->state_lo = lo_l;
       rng->has_uint32 = ((last_pos & 1) == 0) ? 1u : 0u;
+      rng->uinteger = vhi_l;
     } else {
       // nothing consumed in the current window: state is the window base
       rng->state_hi = (uint64_t)(S >> 64);
       rng->state_lo = (uint64_t)S;
       rng->has_uint32 = drew ? 0u : has;
+      rng->uinteger = drew ? prev_hi31 : stale_u;
     }
-    rng->uinteger = stale_u;
     if (status) *status = ok ? 0 : (int32_t)DBS_ERR_ARGUMENT;
   }
 }

@@ -366,19 +366,30 @@ class DeviceRng:
                    "pcg64_random")
         return out[:n].view(shape)
 
-    def permute_spans(self, spans, only_span: int = -1, out=None, stream=None):
-        """start + permutation(width) for every span, one generator (sgdlab.py:372-374)."""
+    def permute_spans(self, spans, only_span: int = -1, out=None, stream=None, total=None):
+        """start + permutation(width) for every span, one generator (sgdlab.py:372-374).
+        `spans` may be a device int64 tensor [2n] (e.g. the device controller's output,
+        never copied to the host) when `total` (the sum of the widths) is given."""
         torch = _torch()
         dev = self.state.device
-        flat = torch.as_tensor(np.asarray(spans, dtype=np.int64).reshape(-1), device=dev)
-        widths = [e - s for s, e in spans]
-        total = int(sum(widths))
+        if isinstance(spans, torch.Tensor) and spans.is_cuda:
+            if total is None or only_span >= 0:
+                raise ValueError("device spans need total= and the whole-plan permutation")
+            flat = spans
+            n_spans = int(spans.numel()) // 2
+            widths = None
+            total = int(total)
+        else:
+            flat = torch.as_tensor(np.asarray(spans, dtype=np.int64).reshape(-1), device=dev)
+            n_spans = len(spans)
+            widths = [e - s for s, e in spans]
+            total = int(sum(widths))
         if self._draws is None or self._draws.numel() < max(total, 1):
             self._draws = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
         n_out = total if only_span < 0 else widths[only_span]
         if out is None:
             out = torch.empty(max(n_out, 1), dtype=torch.int64, device=dev)
-        st = _lib.lib().dbs_dev_permute_spans(self.state.data_ptr(), flat.data_ptr(), len(spans), total, only_span,
+        st = _lib.lib().dbs_dev_permute_spans(self.state.data_ptr(), flat.data_ptr(), n_spans, total, only_span,
                                               out.data_ptr(), self._draws.data_ptr(), _lib.stream_handle(stream))
         _lib.check(st, "permute_spans")
         return out[:n_out], flat

@@ -109,6 +109,75 @@ class RunResult:
     timed_launches: int = 0     # kernels of this library executed in that window
 
 
+class DevicePlanner:
+    """cluster.run_training's re-plan (cluster.py:253-271) on the device: the
+    measured per-worker seconds feed dbs_dev_replan where they were accumulated
+    (shares of the previous spans -> perf -> optional EMA -> times = s / p ->
+    plan_next_epoch, one single-CTA launch), and ONE pinned read-back per epoch
+    carries the new plan, the seconds and the status for the host bookkeeping
+    (EpochStats, launch sizes).  The epoch-0 / non-DBS even plan comes from the
+    same kernel (cluster.py:254-255, 223-231)."""
+
+    def __init__(self, torch, dev, n: int, config: StrategyConfig, D: int):
+        self.torch, self.n, self.D = torch, n, D
+        self.B = int(config.total_budget)
+        self.adaptive = 1 if config.kind == "dbs" else 0
+        self.smoothing = float(config.perf_smoothing) if self.adaptive else 0.0
+        # device pack: [b n | cum n+1 | spans 2n | iters 1 | seconds n (f64) | flags 2 x i32]
+        self.len = 5 * n + 3
+        self.pack = torch.zeros(self.len, dtype=torch.int64, device=dev)
+        self.host = torch.zeros(self.len, dtype=torch.int64, pin_memory=True)
+        o = 0
+        self.b = self.pack[o:o + n]; o += n
+        self.cum = self.pack[o:o + n + 1]; o += n + 1
+        self.spans_next = self.pack[o:o + 2 * n]; o += 2 * n
+        self.iters = self.pack[o:o + 1]; o += 1
+        self.secs = self.pack[o:o + n].view(torch.float64); o += n
+        self.flags = self.pack[o:o + 1].view(torch.int32)
+        self.spans = torch.zeros(2 * n, dtype=torch.int64, device=dev)  # the current epoch's spans (input)
+        self.smoothed = torch.zeros(n, dtype=torch.float64, device=dev)
+
+    def enqueue(self, epoch: int, seconds, stream: int, plan: bool = True) -> None:
+        """Plan `epoch` from `seconds` (the previous epoch's measured compute times,
+        device f64 [n]) and start the read-back; nothing waits here.  plan=False
+        (after the last epoch): only the seconds are read back."""
+        L = _lib.lib()
+        if not plan:
+            self.secs.copy_(seconds)
+            self.host.copy_(self.pack, non_blocking=True)
+            return
+        if epoch > 0:
+            self.spans.copy_(self.spans_next)
+        _lib.check(L.dbs_dev_replan(self.spans.data_ptr(), seconds.data_ptr(), self.n, self.B, self.D, int(epoch),
+                                    self.adaptive, self.smoothing, self.smoothed.data_ptr(), self.flags.data_ptr(),
+                                    self.b.data_ptr(), self.cum.data_ptr(), self.spans_next.data_ptr(),
+                                    self.iters.data_ptr(), stream), "dev_replan")
+        self.secs.copy_(seconds)
+        self.host.copy_(self.pack, non_blocking=True)
+
+    def seconds(self) -> tuple:
+        """The measured seconds carried by the last read-back (after a sync)."""
+        n = self.n
+        return tuple(float(x) for x in self.host.numpy()[4 * n + 2:5 * n + 2].view(np.float64))
+
+    def result(self, epoch: int):
+        """The plan of `epoch` from the read-back (after a sync); a controller error
+        raises the reference's exception class (errors.py:4-53)."""
+        from . import allocation
+        from .errors import from_status
+
+        h = self.host.numpy()
+        n = self.n
+        st = int(h[5 * n + 2:5 * n + 3].view(np.int32)[1])
+        if st != 0:
+            raise from_status(st, f"device re-plan of epoch {epoch} failed (dbs_status {st})")
+        return allocation.plan_from_arrays(h[:n], h[n:2 * n + 1], h[2 * n + 1:4 * n + 1], epoch)
+
+    def current_spans(self):
+        """Device spans of the plan of the epoch just read back."""
+        return self.spans_next
+
+
 class SimulatedTrainer:
     """W simulated workers of synchronous S-SGD on one GPU.
 
@@ -156,9 +225,10 @@ class SimulatedTrainer:
                                      precision=self.precision)
         self.workers = make_workers(n_workers, partition)
         partitioned = any(w.ctx for w in self.workers)
-        # iteration graphs for ResNet (one context); partitioned workers launch eagerly
-        # from their own contexts (a graph cannot span contexts)
-        default_graphs = self.kind == MODEL_RESNET18 and not partitioned
+        # iteration graphs (one context: every kernel reads the iteration index from
+        # device memory); partitioned workers launch eagerly from their own contexts
+        # (a graph cannot span contexts)
+        default_graphs = not partitioned
         self.graphs = default_graphs if graphs is None else bool(graphs and default_graphs)
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
@@ -263,14 +333,15 @@ class SimulatedTrainer:
         p = self.model.params.clone()
         v = torch.zeros_like(p)
         pb = self.model.params_op.clone()
+        # scratch first: the worker streams must see it initialised (they wait on `cur` below)
+        st_scratch = torch.zeros(2 * self.n, dtype=torch.int64, device=self.dev)
+        sec_scratch = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
+        it_scratch = torch.zeros(1, dtype=torch.int64, device=self.dev)
         cur = torch.cuda.current_stream()
         self.agg.wait_stream(cur)
         for wk in self.workers:
             wk.stream.wait_stream(cur)
         saved = [(slots[w].loss, slots[w].stamps, slots[w].seconds) for w in range(self.n)]
-        st_scratch = torch.zeros(2 * self.n, dtype=torch.int64, device=self.dev)
-        sec_scratch = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
-        it_scratch = torch.zeros(1, dtype=torch.int64, device=self.dev)
         for w in range(self.n):
             slots[w].loss = None
             slots[w].stamps = st_scratch[2 * w:].data_ptr()
@@ -330,6 +401,15 @@ class SimulatedTrainer:
             self._replicas_begin(mode=_MODE[aggregation])
         n, D = self.n, self.D
         self.rng = DeviceRng(seed, self.dev)
+        # device-resident re-plan (no host controller round trip) unless a plan list is given
+        planner = DevicePlanner(torch, self.dev, n, config, D) if plan_source is None else None
+        next_secs = None
+        if planner is not None:
+            self.seconds.zero_()
+            planner.enqueue(0, self.seconds, _lib.stream_handle())
+            torch.cuda.synchronize()
+        if record_loss and (getattr(self, "_loss_host", None) is None or self._loss_host.shape != self.loss_buf.shape):
+            self._loss_host = torch.zeros(self.loss_buf.shape, dtype=torch.float32, pin_memory=True)
         stats: list = []
         smoothed = None
         losses, plans = [], []
@@ -350,7 +430,7 @@ class SimulatedTrainer:
             if plan_source is not None:
                 plan = plan_source[min(epoch, len(plan_source) - 1)]
             else:
-                plan, smoothed = cluster.next_plan(config, epoch, n, D, stats[-1] if stats else None, smoothed)
+                plan = planner.result(epoch)
             plans.append(plan)
             batches = list(plan.int_batches)
             spans = list(plan.sample_spans)
@@ -358,7 +438,10 @@ class SimulatedTrainer:
             if max_iters is not None:
                 iters = min(iters, max_iters - done)
             # sample assignment (device) and the per-worker shard repack
-            perm, _ = self.rng.permute_spans(spans)
+            if planner is not None:
+                perm, _ = self.rng.permute_spans(planner.current_spans(), total=D)
+            else:
+                perm, _ = self.rng.permute_spans(spans)
             offs = np.cumsum([0] + [e - s for s, e in spans[:-1]])
             s_main = _lib.stream_handle()
             slots = (_lib.WorkerSlot * n)()
@@ -468,14 +551,24 @@ class SimulatedTrainer:
             for wk, _ in spinning:
                 self.agg.wait_stream(wk.spin_stream)
             cur.wait_stream(self.agg)
+            last = epoch == n_epochs - 1 or (max_iters is not None and done + iters >= max_iters)
+            if planner is not None:
+                # the next epoch's plan from this epoch's measured seconds, on the device;
+                # the read-back carries the seconds too (the only host round trip)
+                planner.enqueue(epoch + 1, self.seconds, _lib.stream_handle(), plan=not last)
+            if record_loss and iters > 0:
+                self._loss_host[:, :iters].copy_(self.loss_buf[:, :iters], non_blocking=True)
             torch.cuda.synchronize()
             ep_wall = start.elapsed_time(end) / 1e3
-            secs = tuple(float(x) for x in self.seconds.cpu().tolist())
+            if planner is not None:
+                secs = planner.seconds()
+            else:
+                secs = tuple(float(x) for x in self.seconds.cpu().tolist())
             slowest = max(secs) if secs else 0.0
             stats.append(EpochStats(epoch=epoch, per_worker_gpu=secs, per_worker_wait=tuple(slowest - s for s in secs),
                                     sync_time=max(0.0, ep_wall - slowest), epoch_wall_time=ep_wall, plan=plan))
             if record_loss and iters > 0:
-                lb = self.loss_buf[:, :iters].double().cpu().numpy()
+                lb = self._loss_host[:, :iters].double().numpy()
                 bw = np.asarray(batches, dtype=np.float64)[:, None]
                 losses.append((lb * bw).sum(axis=0) / bw.sum())
             samples += iters * sum(batches)
