@@ -37,6 +37,19 @@ __device__ __forceinline__ uint64_t xsl_rr(u128 s) {
   return (x >> r) | (x << ((64u - r) & 63u));
 }
 
+// 64-bit position mask from per-lane low-half / high-half ballots: bit 2l = lo of
+// lane l, bit 2l + 1 = hi of lane l (the window's draw order)
+__device__ __forceinline__ uint64_t spread(uint32_t x) {
+  uint64_t v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__device__ __forceinline__ uint64_t interleave(uint32_t lo, uint32_t hi) { return spread(lo) | (spread(hi) << 1); }
+
 __device__ __forceinline__ uint32_t smear(uint32_t m) {
   m |= m >> 1;
   m |= m >> 2;
@@ -101,6 +114,38 @@ __global__ void __launch_bounds__(32) draws_kernel(dbs_pcg64* rng, const int64_t
           if (lane == 0) draws[off + i] = (int32_t)v;
           continue;
         }
+      }
+      // Whole-window step.  While the draws i, i-1, .., i-63 share one mask m (and
+      // the span keeps >= 1 draw after them), a candidate v of the window is
+      // accepted by whichever draw examines it if (v & m) <= i - 63 and rejected by
+      // every one if (v & m) > i; only candidates in between ("ambiguous", 64 / m
+      // of them) depend on the exact draw index.  Those few are resolved in
+      // position order (the draw examining position p is i - #accepts before p),
+      // then every lane places its accepts by a popcount rank: draw i - r takes
+      // the r-th accepted position, and the window is consumed to its end.
+      if (i >= 65 && smear((uint32_t)(i - 63)) == mask) {
+        const uint32_t lo_ok = (uint32_t)(i - 63);
+        const bool vl = cur <= 2 * lane, vh = cur <= 2 * lane + 1;
+        const uint32_t ml = vlo & mask, mh = vhi & mask;
+        const uint64_t acc0 = interleave(__ballot_sync(0xffffffffu, vl && ml <= lo_ok),
+                                         __ballot_sync(0xffffffffu, vh && mh <= lo_ok));
+        uint64_t amb = interleave(__ballot_sync(0xffffffffu, vl && ml > lo_ok && ml <= mx),
+                                  __ballot_sync(0xffffffffu, vh && mh > lo_ok && mh <= mx));
+        uint64_t acc = acc0;
+        while (amb) {
+          const int p = __ffsll((long long)amb) - 1;
+          const uint32_t v = __shfl_sync(0xffffffffu, (p & 1) ? mh : ml, p >> 1);
+          const uint64_t i_at = (uint64_t)i - (uint64_t)__popcll(acc & ((1ull << p) - 1ull));
+          if ((uint64_t)v <= i_at) acc |= 1ull << p;
+          amb &= amb - 1ull;
+        }
+        const int p_lo = 2 * lane, p_hi = 2 * lane + 1;
+        if ((acc >> p_lo) & 1ull) draws[off + i - __popcll(acc & ((1ull << p_lo) - 1ull))] = (int32_t)ml;
+        if ((acc >> p_hi) & 1ull) draws[off + i - __popcll(acc & ((1ull << p_hi) - 1ull))] = (int32_t)mh;
+        drew = true;
+        advance();                 // the window is consumed to its end (trailing rejects included)
+        i -= __popcll(acc) - 1;    // the loop's i-- completes the step
+        continue;
       }
       for (;;) {
         const bool plo = (cur <= 2 * lane) && ((vlo & mask) <= mx);

@@ -233,9 +233,13 @@ class SimulatedTrainer:
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
         self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
-        # shared-GPU slow devices: per-sample ns of the batch-proportional spin (None: a
-        # spin proportional to the worker's own measured forward/backward time)
-        self.slow_per_sample_ns: Optional[float] = None
+        # shared-GPU emulated devices (C1): when set, every worker's iteration also runs a
+        # timed spin of m_w x b_w x device_per_sample_ns on its stream -- the reference's
+        # cost law effective_cost x samples (cluster.py:123-145) on top of the real
+        # (launch-latency-bound, nearly batch-independent) MLP compute, m_w the worker's
+        # active cost multiplier.  None: a disturbed worker's spin is proportional to
+        # its own measured forward/backward time.
+        self.device_per_sample_ns: Optional[float] = None
         self.max_batch = max_batch
         self.scratch = {}
         P = self.model.P
@@ -258,6 +262,7 @@ class SimulatedTrainer:
         self.shard_y = [torch.empty(self.D, dtype=torch.int32, device=self.dev) for _ in range(n_workers)]
         self.loss_buf = torch.zeros((n_workers, self.D + 1), dtype=torch.float32, device=self.dev)
         self._graph_cache = {}
+        self.graph_iters = 8  # iterations per captured graph
         self._primed = False
 
     # -- helpers --------------------------------------------------------------
@@ -352,20 +357,27 @@ class SimulatedTrainer:
         torch.cuda.synchronize()
         self._primed = True
 
-    def _graph(self, key, slots, mode, lr, mom, skip):
-        """(graph, kernels per replay, kernels recorded by a fresh capture now)."""
-        hit = self._graph_cache.get(key)
+    def _graph(self, key, k, slots, mode, lr, mom, skip):
+        """(graph of k iterations, kernels per replay, kernels recorded by a fresh
+        capture now).  Captured without a device-wide synchronisation (the queued
+        permutation / repack keeps running while the host records), thread-local
+        capture mode; every kernel reads the iteration index from d_iter, so one
+        graph of k iterations serves any k consecutive iterations of the plan."""
+        hit = self._graph_cache.get((key, k))
         if hit is not None:
             return hit[0], hit[1], 0
         torch = self.torch
         g = torch.cuda.CUDAGraph()
-        torch.cuda.synchronize()
         c0 = _lib.lib().dbs_launch_count()
-        with torch.cuda.graph(g, stream=self.agg):
-            self._run_iters(slots, 0, 1, mode, lr, mom, self.model.params, self.model.velocity,
-                            self.model.params_op, skip, self.d_iter)
+        with torch.cuda.stream(self.agg):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                self._run_iters(slots, 0, k, mode, lr, mom, self.model.params, self.model.velocity,
+                                self.model.params_op, skip, self.d_iter)
+            finally:
+                g.capture_end()
         per = _lib.lib().dbs_launch_count() - c0
-        self._graph_cache[key] = (g, per)
+        self._graph_cache[(key, k)] = (g, per)
         return g, per, per
 
     # -- the epoch loop -----------------------------------------------------------
@@ -479,6 +491,14 @@ class SimulatedTrainer:
             _lib.check(_lib.lib().dbs_dev_set_flag(self.stop.data_ptr(), 0, s_main), "set_flag")
             # disturbances of this epoch
             spinning, spin_key = [], []
+            emulate = bool(self.device_per_sample_ns) and not self.pin_sms
+            if emulate:
+                for w in range(n):
+                    prof = profiles[w] if profiles is not None else None
+                    m = cluster.effective_cost(prof, epoch) / prof.base_cost if prof is not None else 1.0
+                    slots[w].spin_ns = int(m * batches[w] * self.device_per_sample_ns)
+                    slots[w].spin_ctas = 2
+                    spin_key.append((w, slots[w].spin_ns))
             if profiles is not None:
                 for w, prof in enumerate(profiles):
                     ev = prof.active_disturbance(epoch)
@@ -492,14 +512,8 @@ class SimulatedTrainer:
                             ctas = max(0, min(ctas, wk.sm_count - 1))
                             if ctas:
                                 spinning.append((wk, ctas))
-                        elif self.slow_per_sample_ns:
-                            # a device m x slower per sample (the reference's timing law:
-                            # effective_cost x b per iteration, cluster.py:123-145): a timed
-                            # spin of (m - 1) x b x the calibrated per-sample time on the
-                            # worker's stream -- proportional to the batch DBS assigns it
-                            slots[w].spin_ns = int((ev.cost_multiplier - 1.0) * batches[w] * self.slow_per_sample_ns)
-                            slots[w].spin_ctas = 2
-                            spin_key.append((w, slots[w].spin_ns))
+                        elif emulate:
+                            pass  # folded into the emulated device's per-sample spin above
                         else:
                             # simulated workers share the GPU's SMs: the slow worker's
                             # device is emulated as m x its own forward/backward time
@@ -507,19 +521,30 @@ class SimulatedTrainer:
                             slots[w].slow_ctas = 8
                             spin_key.append((w, "x", float(ev.cost_multiplier)))
                     elif ev.extra_epoch_seconds:
-                        slots[w].spin_ns = int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
+                        slots[w].spin_ns = (slots[w].spin_ns if emulate else 0) + int(ev.extra_epoch_seconds * 1e9 /
+                                                                                       max(iters, 1))
                         # in its own partition the spin occupies the worker's SMs; on a shared
                         # GPU a 2-CTA timed spin delays only this worker's stream
                         slots[w].spin_ctas = wk.sm_count if wk.ctx else 2
                         spin_key.append((w, slots[w].spin_ns))
             if iters > 0 and (spinning or self.graphs):
                 self._prime(slots, mode)
-            graph = None
-            per_replay = 0
+            graph = graph_r = None
+            per_replay = per_r = 0
+            k_it = 1
             if self.graphs and iters > 0 and not local:
                 key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
                        bool(record_loss))
-                graph, per_replay, captured = self._graph(key, slots, mode, lr, momentum, skip_update)
+                # a plan seen before gets k-iteration graphs; a new one (DBS re-plans move
+                # batches by a sample or two from epoch to epoch) a one-iteration graph,
+                # whose capture hides under the queued permutation and repack
+                if (key, 1) in self._graph_cache:
+                    k_it = min(iters, self.graph_iters)
+                # graphs of k_it iterations (fewer dependent graph launches per epoch) + the remainder
+                graph, per_replay, captured = self._graph(key, k_it, slots, mode, lr, momentum, skip_update)
+                if iters % k_it:
+                    graph_r, per_r, cap_r = self._graph(key, iters % k_it, slots, mode, lr, momentum, skip_update)
+                    captured += cap_r
                 self.d_iter.zero_()
             cur = torch.cuda.current_stream()
             for wk, ctas in spinning:
@@ -535,8 +560,10 @@ class SimulatedTrainer:
             if iters > 0:
                 if graph is not None:
                     with torch.cuda.stream(self.agg):
-                        for _ in range(iters):
+                        for _ in range(iters // k_it):
                             graph.replay()
+                        if graph_r is not None:
+                            graph_r.replay()
                 elif local:
                     st = _lib.lib().dbs_run_iterations_local(slots, self.n, 0, iters, mode, float(lr), float(momentum),
                                                              int(local_interval), self._rep_ptrs[0], self._rep_ptrs[1],
@@ -577,7 +604,7 @@ class SimulatedTrainer:
             if timing:
                 timed_samples += iters * sum(batches)
                 timed_launches += (_lib.lib().dbs_launch_count() - launches0 - captured
-                                   + (per_replay * iters if graph is not None else 0))
+                                   + (per_replay * (iters // k_it) + per_r if graph is not None else 0))
             if max_iters is not None and done >= max_iters:
                 break
         timed = 0.0
