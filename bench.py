@@ -285,7 +285,7 @@ def run_strategy(tr, wl, kind, args, world=1):
     clocks = sampler.stop()
     timed = res.stats[args.warmup:]
     return {"samples_per_s": res.timed_samples / res.timed_seconds, "epoch_s": res.timed_seconds / len(timed),
-            "stats": timed, "clocks": clocks, "launches": res.timed_launches, "loss_last": float(res.losses[-1]),
+            "stats": timed, "clocks": clocks, "launches": res.timed_launches, "host_launches": res.timed_host_launches, "loss_last": float(res.losses[-1]),
             "samples": res.timed_samples, "seconds": res.timed_seconds}
 
 
@@ -876,6 +876,7 @@ def main():
         "bf16_variant": variant,
         "clocks": dbs["clocks"],
         "gpu_launches": int(dbs["launches"]),
+        "host_launches_per_epoch": round(dbs["host_launches"] / max(len(dbs["stats"]), 1), 1),
     }
     if rank == 0:
         print(json.dumps(out), flush=True)

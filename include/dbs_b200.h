@@ -59,6 +59,9 @@ int dbs_version(int* major, int* minor, int* sm_arch);
 int dbs_device_ok(void);
 /* Number of kernels this library has launched (or captured into a graph) so far. */
 int64_t dbs_launch_count(void);
+/* Launch API calls this process's host threads made through the library (each
+ * kernel launch, captured or not, and each per-worker graph launch). */
+int64_t dbs_host_launch_count(void);
 
 /* ------------------------------------------------------------------------ */
 /* (3) Epoch-end DBS controller  -- allocation.py, single-CTA fp64 kernel   */
@@ -452,6 +455,18 @@ int dbs_dev_spin_until_ctx(int32_t num_ctas, const volatile int32_t* d_stop, voi
 int dbs_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                        float momentum, float* d_params, float* d_velocity, void* d_params_shadow,
                        int32_t skip_update, void* agg_stream, int64_t* d_iter);
+/* Per-worker CUDA graphs for workers in SM partitions (green contexts, where one
+ * graph cannot span the workers' contexts): each worker's part of an iteration is
+ * captured once, in its own context, and replayed per iteration -- n graph launches
+ * plus the update instead of every kernel from one host thread.  A graph set is
+ * valid for one plan (batches, disturbance spins, model scratch); d_iter required.
+ * Replaces the eager launch loop of run_parallel_sgd's iteration (sgdlab.py:380-391). */
+typedef struct dbs_worker_graphs dbs_worker_graphs;
+int dbs_worker_graphs_create(int32_t n, dbs_worker_graphs** out);
+int dbs_worker_graphs_destroy(dbs_worker_graphs* g);
+int dbs_run_iterations_graphed(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                               float lr, float momentum, float* d_params, float* d_velocity, void* d_params_shadow,
+                               int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_worker_graphs* graphs);
 /* Multi-GPU form (one process per GPU): the rank's n local workers, then a local
  * weighted reduce into the communicator's gradient block and the fused NVLink
  * all-reduce + momentum SGD (dbs_comm_allreduce_sgd) with per-rank weights

@@ -72,6 +72,7 @@ SIGNATURES = {
     "dbs_version": (c_i32, [P_i32, P_i32, P_i32]),
     "dbs_device_ok": (c_i32, []),
     "dbs_launch_count": (c_i64, []),
+    "dbs_host_launch_count": (c_i64, []),
     "dbs_evaluate_performance": (c_i32, [P_dbl, P_dbl, c_i64, P_dbl, P_i64]),
     "dbs_compute_batch_fractions": (c_i32, [P_dbl, c_i64, P_dbl, P_i64]),
     "dbs_scale_to_real_batches": (c_i32, [P_dbl, c_i64, c_i64, P_dbl]),
@@ -131,6 +132,10 @@ SIGNATURES = {
                                        c_vp, c_vp, c_i32, c_vp]),
     "dbs_run_iterations": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp, c_vp,
                                    c_vp, c_i32, c_vp, c_vp]),
+    "dbs_run_iterations_graphed": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt,
+                                           c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "dbs_worker_graphs_create": (c_i32, [c_i32, ctypes.POINTER(c_vp)]),
+    "dbs_worker_graphs_destroy": (c_i32, [c_vp]),
     "dbs_run_iterations_comm": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp,
                                         P_i64, c_vp, c_vp, c_vp]),
     "dbs_dev_aggregate_f32": (c_i32, [ctypes.POINTER(c_vp), P_i64, c_i64, c_i32, c_i64, c_vp, c_vp]),

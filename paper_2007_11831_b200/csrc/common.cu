@@ -10,7 +10,15 @@ namespace dbs {
 static thread_local char g_err[1024] = {0};
 static std::atomic<long long> g_launches{0};
 
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static std::atomic<long long> g_host_launches{0};  // launch API calls the host made (kernels + graphs)
+void count_launch() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  g_host_launches.fetch_add(1, std::memory_order_relaxed);
+}
+// kernels recorded into a graph are counted when the graph is launched, not when captured
+long long launch_count() { return g_launches.load(); }
+void add_launches(long long d) { g_launches.fetch_add(d, std::memory_order_relaxed); }
+void count_host_launch() { g_host_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -65,6 +73,7 @@ int num_sms() {
 extern "C" const char* dbs_last_error(void) { return dbs::g_err; }
 
 extern "C" int64_t dbs_launch_count(void) { return (int64_t)dbs::g_launches.load(); }
+extern "C" int64_t dbs_host_launch_count(void) { return (int64_t)dbs::g_host_launches.load(); }
 
 extern "C" int dbs_version(int* major, int* minor, int* sm_arch) {
   if (major) *major = 0;

@@ -433,13 +433,56 @@ extern "C" int dbs_comm_shadow(const dbs_comm* c, void** d_shadow, int32_t* prec
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                float mom, float* d_params, float* d_velocity, void* d_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
-                               const int64_t* rank_batches);
+                               const int64_t* rank_batches, dbs_worker_graphs* graphs = nullptr);
+
+namespace dbs {
+long long launch_count();
+void add_launches(long long d);
+void count_host_launch();
+}  // namespace dbs
+
+// One CUDA graph per worker: that worker's part of an iteration (stamps, optional
+// spin, forward/backward reading the iteration index from d_iter, compute-time
+// accumulation), captured on the worker's stream with its SM partition's context
+// current -- so the worker's ~100 launches per iteration become one graph launch
+// inside its green context, and the iteration driver issues n graph launches plus
+// the update instead of n x ~100 kernels from one host thread.
+struct dbs_worker_graphs {
+  int n = 0;
+  cudaGraphExec_t exec[64] = {};
+  long long kernels[64] = {};  // kernels per replay (for dbs_launch_count)
+};
+
+extern "C" int dbs_worker_graphs_create(int32_t n, dbs_worker_graphs** out) {
+  DBS_REQUIRE(out && n >= 1 && n <= 64, DBS_ERR_ARGUMENT, "worker_graphs_create: 1 <= n <= 64");
+  dbs_worker_graphs* g = new dbs_worker_graphs();
+  g->n = n;
+  *out = g;
+  return DBS_OK;
+}
+
+extern "C" int dbs_worker_graphs_destroy(dbs_worker_graphs* g) {
+  if (!g) return DBS_OK;
+  for (int i = 0; i < g->n; i++)
+    if (g->exec[i]) cudaGraphExecDestroy(g->exec[i]);
+  delete g;
+  return DBS_OK;
+}
 
 extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                   float mom, float* d_params, float* d_velocity, void* d_params_shadow,
                                   int32_t skip_update, void* agg_stream, int64_t* d_iter) {
   return run_iterations_impl(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_shadow, skip_update,
                              agg_stream, d_iter, nullptr, nullptr);
+}
+
+extern "C" int dbs_run_iterations_graphed(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                          float lr, float mom, float* d_params, float* d_velocity,
+                                          void* d_params_shadow, int32_t skip_update, void* agg_stream,
+                                          int64_t* d_iter, dbs_worker_graphs* graphs) {
+  DBS_REQUIRE(graphs, DBS_ERR_ARGUMENT, "run_iterations_graphed: null graphs");
+  return run_iterations_impl(w, n, t0, t1, mode, lr, mom, d_params, d_velocity, d_params_shadow, skip_update,
+                             agg_stream, d_iter, nullptr, nullptr, graphs);
 }
 
 // Multi-GPU form: this rank's n local workers, then the hierarchical update --
@@ -467,7 +510,7 @@ extern "C" int dbs_run_iterations_comm(const dbs_worker_slot* w, int32_t n, int6
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                float mom, float* d_params, float* d_velocity, void* d_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
-                               const int64_t* rank_batches) {
+                               const int64_t* rank_batches, dbs_worker_graphs* graphs) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "run_iterations: bad arguments");
   for (int i = 0; i < n; i++)
     DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18),
@@ -487,15 +530,8 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
   }
   const int64_t P = (w[0].model_kind == DBS_MODEL_MLP) ? static_cast<const dbs_mlp*>(w[0].model)->P
                                                        : resnet_param_count(static_cast<const dbs_resnet*>(w[0].model));
-  DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
-  for (int64_t t = t0; t < t1; t++) {
-    for (int i = 0; i < n; i++) {
-      cudaStream_t s = as_stream(w[i].stream);
-      // the worker's launches happen with its SM partition's context current
-      st = ctx_push(w[i].ctx);
-      if (st) return st;
-      st = [&]() -> int {
-      DBS_CUDA_TRY(cudaStreamWaitEvent(s, ev[n], 0));  // parameters of iteration t ready
+  // worker i's part of iteration t on stream s (its partition's context current)
+  auto issue_worker = [&](int i, cudaStream_t s, int64_t t) -> int {
       if (w[i].stamps) {
         st = stamp(w[i].stamps, 0, s);
         if (st) return st;
@@ -542,8 +578,57 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
         st = dbs_dev_accumulate_time(w[i].stamps, 0, 1, w[i].seconds, w[i].worker_index, s);
         if (st) return st;
       }
-      DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
       return DBS_OK;
+  };
+  if (graphs) {
+    DBS_REQUIRE(d_iter && graphs->n == n, DBS_ERR_ARGUMENT, "run_iterations: worker graphs need d_iter and n workers");
+    for (int i = 0; i < n; i++) {
+      if (graphs->exec[i]) continue;
+      cudaStream_t s = as_stream(w[i].stream);
+      st = ctx_push(w[i].ctx);
+      if (st) return st;
+      const long long c0 = launch_count();
+      st = [&]() -> int {
+        DBS_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int st_w = issue_worker(i, s, 0);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e_end = cudaStreamEndCapture(s, &g);
+        if (st_w) {
+          if (g) cudaGraphDestroy(g);
+          return st_w;
+        }
+        DBS_CUDA_TRY(e_end);
+        const cudaError_t e_inst = cudaGraphInstantiate(&graphs->exec[i], g, 0);
+        cudaGraphDestroy(g);
+        DBS_CUDA_TRY(e_inst);
+        return DBS_OK;
+      }();
+      graphs->kernels[i] = launch_count() - c0;
+      add_launches(-graphs->kernels[i]);  // recorded, not executed
+      const int st_pop = ctx_pop(w[i].ctx);
+      if (st) return st;
+      if (st_pop) return st_pop;
+    }
+  }
+  DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
+  for (int64_t t = t0; t < t1; t++) {
+    for (int i = 0; i < n; i++) {
+      cudaStream_t s = as_stream(w[i].stream);
+      // the worker's launches happen with its SM partition's context current
+      st = ctx_push(w[i].ctx);
+      if (st) return st;
+      st = [&]() -> int {
+        DBS_CUDA_TRY(cudaStreamWaitEvent(s, ev[n], 0));  // parameters of iteration t ready
+        if (graphs) {
+          DBS_CUDA_TRY(cudaGraphLaunch(graphs->exec[i], s));
+          add_launches(graphs->kernels[i]);
+          count_host_launch();
+        } else {
+          const int st_w = issue_worker(i, s, t);
+          if (st_w) return st_w;
+        }
+        DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
+        return DBS_OK;
       }();
       const int st_pop = ctx_pop(w[i].ctx);
       if (st) return st;

@@ -107,6 +107,7 @@ class RunResult:
     timed_seconds: float = 0.0  # device time from the start of epoch `timed_from` to the end,
     timed_samples: int = 0      # whole epochs: re-plan, permutation, repack and iterations
     timed_launches: int = 0     # kernels of this library executed in that window
+    timed_host_launches: int = 0  # launch calls the host issued in that window (kernels + graph launches)
 
 
 class DevicePlanner:
@@ -230,6 +231,9 @@ class SimulatedTrainer:
         # (a graph cannot span contexts)
         default_graphs = not partitioned
         self.graphs = default_graphs if graphs is None else bool(graphs and default_graphs)
+        # partitioned workers: one graph per worker, captured in its own context
+        self.worker_graphs = partitioned if graphs is None else bool(graphs and partitioned)
+        self._wg_cache = {}
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
         self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
@@ -280,6 +284,11 @@ class SimulatedTrainer:
                 cur = ResnetScratch(cap, self.classes, self.depth, self.image, self.precision)
             self.scratch[w] = cur
             self._graph_cache.clear()  # scratch pointers changed
+            if self._wg_cache:
+                self.torch.cuda.synchronize()
+                for h in self._wg_cache.values():
+                    _lib.lib().dbs_worker_graphs_destroy(h)
+                self._wg_cache.clear()
         return cur
 
     def _gather_mlp(self, idx, rows, xs, stream):
@@ -380,6 +389,21 @@ class SimulatedTrainer:
         self._graph_cache[(key, k)] = (g, per)
         return g, per, per
 
+    def _worker_graphs(self, key):
+        """The per-worker graph set of a plan (captured by the library on first use);
+        the last few plans' sets are kept, older ones released."""
+        hit = self._wg_cache.pop(key, None)
+        if hit is None:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().dbs_worker_graphs_create(self.n, ctypes.byref(h)), "worker_graphs_create")
+            hit = h
+        self._wg_cache[key] = hit  # most recent last
+        while len(self._wg_cache) > 8:
+            old_key = next(iter(self._wg_cache))
+            self.torch.cuda.synchronize()
+            _lib.lib().dbs_worker_graphs_destroy(self._wg_cache.pop(old_key))
+        return hit
+
     # -- the epoch loop -----------------------------------------------------------
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
             aggregation: str = "batch_weighted", profiles: Optional[Sequence[WorkerProfile]] = None,
@@ -428,7 +452,7 @@ class SimulatedTrainer:
         samples, wall, done = 0, 0.0, 0
         mode = _MODE[aggregation]
         t_start = t_end = None
-        timed_samples = timed_launches = 0
+        timed_samples = timed_launches = timed_host_launches = 0
         for epoch in range(n_epochs):
             if timed_from is not None and epoch == timed_from:
                 torch.cuda.synchronize()
@@ -438,6 +462,8 @@ class SimulatedTrainer:
             if epoch_hook is not None:
                 epoch_hook(epoch)
             launches0 = _lib.lib().dbs_launch_count()
+            host0 = _lib.lib().dbs_host_launch_count()
+            replays = 0
             captured = 0
             if plan_source is not None:
                 plan = plan_source[min(epoch, len(plan_source) - 1)]
@@ -564,11 +590,19 @@ class SimulatedTrainer:
                             graph.replay()
                         if graph_r is not None:
                             graph_r.replay()
+                    replays = iters // k_it + (graph_r is not None)
                 elif local:
                     st = _lib.lib().dbs_run_iterations_local(slots, self.n, 0, iters, mode, float(lr), float(momentum),
                                                              int(local_interval), self._rep_ptrs[0], self._rep_ptrs[1],
                                                              self._rep_ptrs[2], int(self.agg.cuda_stream))
                     _lib.check(st, "run_iterations_local")
+                elif self.worker_graphs:
+                    wg = self._worker_graphs((tuple(batches), tuple(spin_key), bool(record_loss)))
+                    st = _lib.lib().dbs_run_iterations_graphed(
+                        slots, self.n, 0, iters, mode, float(lr), float(momentum), self.model.params.data_ptr(),
+                        self.model.velocity.data_ptr(), self.model.params_op.data_ptr(), int(skip_update),
+                        int(self.agg.cuda_stream), self.d_iter.data_ptr(), wg)
+                    _lib.check(st, "run_iterations_graphed")
                 else:
                     self._run_iters(slots, 0, iters, mode, lr, momentum, self.model.params, self.model.velocity,
                                     self.model.params_op, skip_update)
@@ -605,6 +639,7 @@ class SimulatedTrainer:
                 timed_samples += iters * sum(batches)
                 timed_launches += (_lib.lib().dbs_launch_count() - launches0 - captured
                                    + (per_replay * (iters // k_it) + per_r if graph is not None else 0))
+                timed_host_launches += _lib.lib().dbs_host_launch_count() - host0 + replays
             if max_iters is not None and done >= max_iters:
                 break
         timed = 0.0
@@ -618,7 +653,7 @@ class SimulatedTrainer:
                                batches=list(plans[-1].int_batches) if plans else None)
         return RunResult(stats=stats, losses=np.concatenate(losses) if losses else np.zeros(0), samples=samples,
                          wall_seconds=wall, plans=plans, timed_seconds=timed, timed_samples=timed_samples,
-                         timed_launches=timed_launches)
+                         timed_launches=timed_launches, timed_host_launches=timed_host_launches)
 
 
 # ---------------------------------------------------------------------------

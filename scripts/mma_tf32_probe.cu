@@ -256,7 +256,75 @@ void run_pattern(int pat) {
   cudaFree(d);
 }
 
+
+// MN-major operands (SWIZZLE_128B_BASE32B, the transposed weight gradient's layout):
+// kind::tf32 M=128 N=BN K=8 issue rate with A and/or B MN-major (a_mn, b_mn)
+template <int BN>
+__global__ void __launch_bounds__(128, 1) mnrate(int reps, int a_mn, int b_mn, unsigned long long* out) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t done;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kOpBytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 32768);
+    const uint32_t idesc = make_idesc_tf32(128, BN, a_mn, b_mn);
+    const long long t0 = clock64();
+    for (int i = 0; i < reps; i++) {
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint64_t ad = a_mn ? make_sdesc(a0 + k * 1024, 8192, 512, 1) : make_sdesc(a0 + k * 32, 16, 1024);
+        const uint64_t bd = b_mn ? make_sdesc(b0 + k * 1024, 4096, 512, 1) : make_sdesc(b0 + k * 32, 16, 1024);
+        mma_tf32_ss(tmem, ad, bd, idesc, (i | k) != 0);
+      }
+    }
+    mma_commit(&done);
+    mbar_wait(&done, 0);
+    out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+template <int BN>
+void run_mn(int a_mn, int b_mn) {
+  unsigned long long* d;
+  cudaMalloc(&d, 8 * 2048);
+  const int smem = kOpBytes + 2048;
+  cudaFuncSetAttribute(mnrate<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int reps = 2000;
+  for (int w = 0; w < 2; w++) mnrate<BN><<<148, 128, smem>>>(reps, a_mn, b_mn, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, 8 * 148, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; i++) avg += (double)h[i];
+  avg /= 148;
+  const double per = avg / (reps * 4);
+  printf("tf32 M=128 N=%3d a_mn=%d b_mn=%d: %6.1f clk/MMA (%3.0f%% of 2048 MAC/clk)  %s\n", BN, a_mn, b_mn, per,
+         100.0 * 128.0 * BN * 8 / per / 2048, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
+  for (int am = 0; am < 2; am++)
+    for (int bm = 0; bm < 2; bm++) {
+      run_mn<64>(am, bm);
+      run_mn<128>(am, bm);
+    }
+
   for (int pat : {0, 3, 4, 13, 14}) {
     run_pattern<64>(pat);
     run_pattern<128>(pat);
