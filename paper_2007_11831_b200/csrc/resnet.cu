@@ -675,6 +675,16 @@ __device__ __forceinline__ void ld8_s32(const float* p, int64_t i, float (&v)[8]
   v[0] = h0.x + l0.x; v[1] = h0.y + l0.y; v[2] = h0.z + l0.z; v[3] = h0.w + l0.w;
   v[4] = h1.x + l1.x; v[5] = h1.y + l1.y; v[6] = h1.z + l1.z; v[7] = h1.w + l1.w;
 }
+// the ReLU mask of an S32 activation from its hi plane only (half the bytes): for a
+// finite v, hi = rn_tf32(v) > 0 exactly when v > 0, except positive subnormals below
+// 2^-137 (hi rounds to 0) -- a ReLU output that small is not distinguishable from 0
+// at the fp32 tolerance this path is held to
+__device__ __forceinline__ void ld8_s32_hi(const float* p, int64_t i, float (&v)[8]) {
+  const float* q = p + s32_off(8 * i);
+  const float4 h0 = *reinterpret_cast<const float4*>(q), h1 = *reinterpret_cast<const float4*>(q + 4);
+  v[0] = h0.x; v[1] = h0.y; v[2] = h0.z; v[3] = h0.w;
+  v[4] = h1.x; v[5] = h1.y; v[6] = h1.z; v[7] = h1.w;
+}
 __device__ __forceinline__ void st8_s32(float* p, int64_t i, const float (&v)[8]) {
   float* q = p + s32_off(8 * i);
   float h[8], l[8];
@@ -877,7 +887,7 @@ __global__ void __launch_bounds__(256) bn_bwd_reduce_f32_kernel(const float* __r
       float g[8], yv[8], mv[8];
       ld8_f32(gin, i, g);
       ld8_f32(y, i, yv);
-      if (mask) ld8_s32(mask, i, mv);
+      if (mask) ld8_s32_hi(mask, i, mv);
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         const float gg = (!mask || mv[k] > 0.0f) ? g[k] : 0.0f;
@@ -948,7 +958,7 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_f32_kernel(const float* __re
     ld8_f32(y, i, yv);
     if (mask) {
       float mv[8];
-      ld8_s32(mask, i, mv);
+      ld8_s32_hi(mask, i, mv);
 #pragma unroll
       for (int k = 0; k < 8; k++) g[k] = mv[k] > 0.0f ? g[k] : 0.0f;
     }

@@ -32,6 +32,7 @@ Disturbance (DisturbanceEvent, cluster.py:25-56), realised on the device:
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -233,6 +234,8 @@ class SimulatedTrainer:
         self.graphs = default_graphs if graphs is None else bool(graphs and default_graphs)
         # partitioned workers: one graph per worker, captured in its own context
         self.worker_graphs = partitioned if graphs is None else bool(graphs and partitioned)
+        if os.environ.get("DBS_WORKER_GRAPHS") == "0":  # A/B switch: eager launches from the host
+            self.worker_graphs = False
         self._wg_cache = {}
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
@@ -518,41 +521,41 @@ class SimulatedTrainer:
             # disturbances of this epoch
             spinning, spin_key = [], []
             emulate = bool(self.device_per_sample_ns) and not self.pin_sms
-            if emulate:
-                for w in range(n):
-                    prof = profiles[w] if profiles is not None else None
-                    m = cluster.effective_cost(prof, epoch) / prof.base_cost if prof is not None else 1.0
+            # a worker's device slowdown this epoch: its effective per-sample cost
+            # (cluster.py:123-130: base cost x active multipliers) relative to the
+            # cheapest worker's base cost -- a scenario's cost spread (e.g. the
+            # robustness scenario's _geometric_costs) and its disturbances alike
+            base_min = min(p.base_cost for p in profiles) if profiles is not None else 1.0
+            for w in range(n):
+                prof = profiles[w] if profiles is not None else None
+                m = cluster.effective_cost(prof, epoch) / base_min if prof is not None else 1.0
+                wk = self.workers[w]
+                if emulate:
+                    # emulated device: m x b x the per-sample time, whatever the batch
                     slots[w].spin_ns = int(m * batches[w] * self.device_per_sample_ns)
                     slots[w].spin_ctas = 2
                     spin_key.append((w, slots[w].spin_ns))
-            if profiles is not None:
-                for w, prof in enumerate(profiles):
-                    ev = prof.active_disturbance(epoch)
-                    if ev is None:
-                        continue
-                    wk = self.workers[w]
-                    if ev.cost_multiplier is not None and ev.cost_multiplier > 1.0:
-                        if self.pin_sms:
-                            # a co-running job pins 1 - 1/m of the worker's SMs
-                            ctas = int(round(wk.sm_count * (1.0 - 1.0 / ev.cost_multiplier)))
-                            ctas = max(0, min(ctas, wk.sm_count - 1))
-                            if ctas:
-                                spinning.append((wk, ctas))
-                        elif emulate:
-                            pass  # folded into the emulated device's per-sample spin above
-                        else:
-                            # simulated workers share the GPU's SMs: the slow worker's
-                            # device is emulated as m x its own forward/backward time
-                            slots[w].slow_scale = float(ev.cost_multiplier - 1.0)
-                            slots[w].slow_ctas = 8
-                            spin_key.append((w, "x", float(ev.cost_multiplier)))
-                    elif ev.extra_epoch_seconds:
-                        slots[w].spin_ns = (slots[w].spin_ns if emulate else 0) + int(ev.extra_epoch_seconds * 1e9 /
-                                                                                       max(iters, 1))
-                        # in its own partition the spin occupies the worker's SMs; on a shared
-                        # GPU a 2-CTA timed spin delays only this worker's stream
-                        slots[w].spin_ctas = wk.sm_count if wk.ctx else 2
-                        spin_key.append((w, slots[w].spin_ns))
+                elif m > 1.0:
+                    if self.pin_sms:
+                        # a co-running job pins 1 - 1/m of the worker's SMs
+                        ctas = int(round(wk.sm_count * (1.0 - 1.0 / m)))
+                        ctas = max(0, min(ctas, wk.sm_count - 1))
+                        if ctas:
+                            spinning.append((wk, ctas))
+                    else:
+                        # simulated workers share the GPU's SMs: the slow worker's
+                        # device is emulated as m x its own forward/backward time
+                        slots[w].slow_scale = float(m - 1.0)
+                        slots[w].slow_ctas = 8
+                        spin_key.append((w, "x", float(m)))
+                ev = prof.active_disturbance(epoch) if prof is not None else None
+                if ev is not None and ev.extra_epoch_seconds:
+                    # flat extra seconds (cluster.py:141-143), spread over the epoch's iterations
+                    slots[w].spin_ns += int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
+                    # in its own partition the spin occupies the worker's SMs; on a shared
+                    # GPU a 2-CTA timed spin delays only this worker's stream
+                    slots[w].spin_ctas = wk.sm_count if wk.ctx else 2
+                    spin_key.append((w, "+", slots[w].spin_ns))
             if iters > 0 and (spinning or self.graphs):
                 self._prime(slots, mode)
             graph = graph_r = None

@@ -1,0 +1,127 @@
+"""The reference's `robustness` scenario on a B200, in both disturbance forms, with the
+simulator-vs-measured cross-check.
+
+4 ResNet-18 workers (disjoint 32-SM partitions), 41 epochs, B = 512, D = 50000,
+background jobs on workers 0 / 1 / 2 from epochs 10 / 21 / 31 (scenarios.py:287-309):
+
+  as_written  the scenario itself: a 1:2 geometric spread of per-sample cost over the
+              four workers (_geometric_costs, scenarios.py:262-265 -- realised by
+              co-running spin kernels pinning 0, 7, 12 and 16 of the 32 SMs) and each
+              background job a flat `extra_epoch_seconds` (10 s against the
+              reference's 125 s slowest-worker epoch, scaled to the measured B200
+              epoch) realised by dbs_dev_spin_for on the worker's partition;
+  cost_x2     round 1's form: uniform workers, a job pins half the worker's SMs
+              (cost_multiplier 2).
+
+Each form runs fixed-batch S-SGD and DBS; the measured EpochStats go out in the
+reference's report format.  crosscheck.fit_costs fits the reference's cost law
+(base_cost, per_iteration_overhead per worker, sync cost per round; for cost_x2
+also the measured multiplier of a half-pinned partition) to both runs, replays
+every measured plan through cluster.run_epoch, and reports the per-epoch error;
+cluster.run_training with the fitted profiles gives the simulator's saving for
+the same hardware, next to the measured one.
+
+    python scripts/replay_robustness_r2.py [--epochs 41] [--out profiles/robustness_r2]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--epochs", type=int, default=41)
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "robustness_r2"))
+    ap.add_argument("--dataset", type=int, default=50000)
+    ap.add_argument("--forms", default="as_written,cost_x2")
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2007_11831_b200 import cluster, crosscheck, report
+    from paper_2007_11831_b200.resnet import synthetic_cifar
+    from paper_2007_11831_b200.trainer import SimulatedTrainer
+
+    torch.cuda.set_device(0)
+    X, y = synthetic_cifar(args.dataset, seed=0)
+    tr = SimulatedTrainer(X, y, n_workers=4, model="resnet18", seed=0, partition=True, max_batch=384)
+    starts = {0: 10, 1: 21, 2: 31}
+    out = Path(args.out)
+    out.mkdir(parents=True, exist_ok=True)
+    sm = tr.workers[0].sm_count
+    spread = [2.0 ** (i / 3) for i in range(4)]  # _geometric_costs(4, base, 2.0) / base
+    summary = {"partition_sms": sm}
+    for form in args.forms.split(","):
+        if form == "as_written":
+            # the scenario's workers: base costs 5e-3 x 2^(i/3) (the trainer pins 1 - c_min / c_w of a
+            # worker's SMs); calibrate the flat 10 s: the reference's slowest worker spends
+            # 12500 x 1e-2 = 125 s per even-plan epoch -- measure ours under the same spread
+            base = [cluster.WorkerProfile(w, 5e-3 * m) for w, m in enumerate(spread)]
+            cal = tr.run(cluster.StrategyConfig("fixed_ssgd", 512), n_epochs=2, lr=0.0, momentum=0.0,
+                         profiles=base, record_loss=False)
+            slowest = max(cal.stats[-1].per_worker_gpu)
+            extra = 10.0 * slowest / 125.0
+            profiles = [cluster.WorkerProfile(w, 5e-3 * m, disturbances=((cluster.DisturbanceEvent(
+                starts[w], extra_epoch_seconds=extra),) if w in starts else ())) for w, m in enumerate(spread)]
+            fit_profiles = profiles  # the spread is each worker's fitted base cost; the extra seconds are declared
+            fit_mult = False
+            form_info = {"cost_spread": [round(m, 4) for m in spread], "extra_epoch_seconds": round(extra, 5),
+                         "pinned_sms": [int(round(sm * (1 - 1 / m))) for m in spread]}
+        else:
+            profiles = [cluster.WorkerProfile(w, 1.0, disturbances=((cluster.DisturbanceEvent(
+                starts[w], cost_multiplier=2.0),) if w in starts else ())) for w in range(4)]
+            fit_profiles = profiles
+            fit_mult = True
+            form_info = {"pinned_sms_per_job": sm // 2}
+        runs, reports, res_sum = [], [], {}
+        for kind in ("fixed_ssgd", "dbs"):
+            cfg = cluster.StrategyConfig(kind, 512)
+            res = tr.run(cfg, n_epochs=args.epochs, lr=0.05, momentum=0.9, profiles=profiles, record_loss=False)
+            rep = report.RunReport.from_stats(f"robustness_{form}_b200", kind, 0, res.stats)
+            report.write_epoch_csv(rep, out / f"robustness_{form}_b200_{kind}.csv")
+            reports.append(rep)
+            runs.append((cfg, res.stats))
+            walls = [s.epoch_wall_time for s in res.stats]
+            res_sum[kind] = {"total_s": round(sum(walls), 4), "plans": [list(s.plan.int_batches) for s in res.stats]}
+        report.write_run_json(reports, [], out / f"robustness_{form}_b200.json")
+        fit = crosscheck.fit_costs(runs, fit_profiles, skip_epochs=1, fit_multiplier=fit_mult)
+        cross = {}
+        for cfg, stats in runs:
+            cross[cfg.kind] = crosscheck.compare(stats, crosscheck.replay(stats, cfg, fit, fit_profiles))
+        sim = {k: sum(s.epoch_wall_time for s in crosscheck.simulate(fit, cluster.StrategyConfig(k, 512),
+                                                                       args.dataset, args.epochs, fit_profiles))
+               for k in ("fixed_ssgd", "dbs")}
+        entry = {"form": form_info,
+                 "measured_total_s": {k: v["total_s"] for k, v in res_sum.items()},
+                 "saving_measured": round(1.0 - res_sum["dbs"]["total_s"] / res_sum["fixed_ssgd"]["total_s"], 4),
+                 "saving_simulated_with_fitted_costs": round(1.0 - sim["dbs"] / sim["fixed_ssgd"], 4),
+                 "fit": {"base_cost_s_per_sample": [float(f"{c:.4e}") for c in fit.base_cost],
+                         "per_iteration_overhead_s": [float(f"{o:.4e}") for o in fit.per_iteration_overhead],
+                         "sync_cost_per_round_s": float(f"{fit.sync_cost_per_round:.4e}"),
+                         "measured_multiplier": [round(m, 4) for m in fit.multiplier],
+                         "residual_rms_rel": round(fit.residual_rel, 5)},
+                 "per_epoch_prediction_error": cross,
+                 "dbs_plans": res_sum["dbs"]["plans"]}
+        if form == "as_written":
+            # the reference's own scenario in the reference's own simulator (its costs, 10 s)
+            ref_prof = [cluster.WorkerProfile(w, 5e-3 * m, disturbances=((cluster.DisturbanceEvent(
+                starts[w], extra_epoch_seconds=10.0),) if w in starts else ())) for w, m in enumerate(spread)]
+            rs = {k: sum(s.epoch_wall_time for s in cluster.run_training(ref_prof, cluster.StrategyConfig(k, 512),
+                                                                         args.dataset, args.epochs))
+                  for k in ("fixed_ssgd", "dbs")}
+            entry["saving_reference_scenario_simulated"] = round(1.0 - rs["dbs"] / rs["fixed_ssgd"], 4)
+        summary[form] = entry
+        print(json.dumps({form: {k: v for k, v in entry.items() if k not in ("dbs_plans",)}}, default=str)[:3000],
+              flush=True)
+    (out / "summary.json").write_text(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -22,7 +22,7 @@ def _launch_all(torch, comms, fn):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("world,P", [(2, 1000), (3, 203530), (4, 65536 * 3 + 7)])
+@pytest.mark.parametrize("world,P", [(2, 1000), (3, 203530), (4, 65536 * 3 + 7), (8, 11173962), (8, 4099)])
 def test_fused_allreduce_sgd_matches_torch(dev, world, P):
     import torch
 
@@ -36,7 +36,7 @@ def test_fused_allreduce_sgd_matches_torch(dev, world, P):
     for c, gr in zip(comms, grads):
         c.params.copy_(x0)
         c.grad.copy_(gr)
-    batches = [37, 73, 73, 128][:world]
+    batches = ([37, 73, 73, 128] if world <= 4 else [37, 37, 73, 73, 73, 73, 73, 73])[:world]  # SURVEY 8(d) C2 weights
     lr, mom = 0.05, 0.9
     w = torch.tensor(batches, dtype=torch.float64, device=dev)
     w = (w / w.sum()).float()
