@@ -502,7 +502,75 @@ def aux_rooflines(tr, peaks):
                             "unit": "GB/s", "frac": round(byt / t / 1e9 / peaks["hbm_gbs"], 4),
                             "bytes_per_launch": byt, "avg_launch_us": round(t * 1e6, 2),
                             "launch": f"{n} worker gradients x {P} fp32 parameters"}
+    if tr.kind != 0 and tr.depth == 18 and tr.precision == _lib.PREC_F32 and tr.workers and tr.workers[0].ctx:
+        out.update(bn_rooflines(tr, peaks))
     return out
+
+
+def bn_rooflines(tr, peaks, reps=20):
+    """The fp32-class BatchNorm passes (resnet.cu; the network's own kernels through
+    dbs_dev_bn_*_s32) at the bench's largest BN shape (b per worker x 32 x 32 x 64),
+    timed where the bench runs them -- inside worker 0's SM partition, eager launches
+    between CUDA events on the partition's stream -- against the copy bandwidth the
+    same partition reaches (the repartition gather with an identity index: 8 B per
+    element).  Bytes per element: forward 4 (y) + 8 (S32 out); backward 12 (reduce:
+    g, y, mask hi plane) + 24 (apply: g, y, mask, S32 dy, g_out)."""
+    import torch
+
+    from paper_2007_11831_b200 import _lib
+
+    L = _lib.lib()
+    wk = tr.workers[0]
+    M, C = tr.max_batch // tr.n * 1024, 64
+    dev = tr.dev
+    g0 = torch.Generator(device=dev).manual_seed(0)
+    y = torch.randn(M, C, device=dev, generator=g0)
+    acc = torch.cat([y.double().sum(0), (y.double() ** 2).sum(0)]).contiguous()
+    gamma, beta = torch.ones(C, device=dev), torch.zeros(C, device=dev)
+    mean, invstd = torch.empty(C, device=dev), torch.empty(C, device=dev)
+    out = torch.empty(M, 2 * C, device=dev)
+    g = torch.randn(M, C, device=dev, generator=g0)
+    dgam, dbet = torch.zeros(C, device=dev), torch.zeros(C, device=dev)
+    dy, gout = torch.empty(M, 2 * C, device=dev), torch.empty(M, C, device=dev)
+    idx = torch.arange(M, device=dev)
+    cp = torch.empty_like(y)
+    h = int(wk.stream.cuda_stream)
+    fns = {
+        "copy": lambda: L.dbs_dev_gather_rows(y.data_ptr(), idx.data_ptr(), M, 4 * C, cp.data_ptr(), h),
+        "bn_forward": lambda: L.dbs_dev_bn_apply_s32(y.data_ptr(), acc.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
+                                                    C, M, 1, mean.data_ptr(), invstd.data_ptr(), out.data_ptr(), h),
+        "bn_backward": lambda: L.dbs_dev_bn_backward_s32(g.data_ptr(), out.data_ptr(), y.data_ptr(), mean.data_ptr(),
+                                                        invstd.data_ptr(), gamma.data_ptr(), C, M, dgam.data_ptr(),
+                                                        dbet.data_ptr(), dy.data_ptr(), gout.data_ptr(), h),
+    }
+    byts = {"copy": 8.0 * M * C + 8.0 * M, "bn_forward": 12.0 * M * C, "bn_backward": 36.0 * M * C}
+    res = {}
+    torch.cuda.synchronize()
+    _lib.check(L.dbs_partition_push(wk.ctx), "partition_push")
+    try:
+        for name, fn in fns.items():
+            for _ in range(3):
+                assert fn() == 0, _lib.last_error()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(wk.stream)
+            for _ in range(reps):
+                fn()
+            e1.record(wk.stream)
+            torch.cuda.synchronize()
+            res[name] = e0.elapsed_time(e1) / 1e3 / reps
+    finally:
+        _lib.check(L.dbs_partition_pop(wk.ctx), "partition_pop")
+    copy_gbs = byts["copy"] / res["copy"] / 1e9
+    out_ = {}
+    for name in ("bn_forward", "bn_backward"):
+        a = byts[name] / res[name] / 1e9
+        out_[name] = {"bound": "hbm", "achieved": round(a, 1), "peak": round(copy_gbs, 1), "unit": "GB/s",
+                      "frac": round(a / copy_gbs, 4), "frac_of_full_gpu_hbm": round(a / peaks["hbm_gbs"], 4),
+                      "bytes_per_launch": byts[name], "avg_launch_us": round(res[name] * 1e6, 2),
+                      "launch": f"M = {M} rows x C = {C} (b = {M // 1024} x 32 x 32), inside a {wk.sm_count}-SM "
+                                "partition; peak = the copy bandwidth measured in the same partition",
+                      "partition_copy_GBps": round(copy_gbs, 1)}
+    return out_
 
 
 def disturbance_desc(wl):

@@ -398,6 +398,17 @@ int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H
                          int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw, void* stream);
 /* fp32-class forms: S32 operands (NHWC activations, [Cout][k][k][Cin] weights,
  * channels multiples of 32), fp32 outputs (y, dx; dw accumulated atomically) */
+/* Stand-alone fp32-class BatchNorm passes (the network's own kernels; unit tests and
+ * per-kernel rooflines).  acc = [sum C | sum of squares C] (fp64) of y [M][C] fp32;
+ * out / dy / mask in the S32 operand format.  Forward: out = act(gamma yhat + beta),
+ * mean / invstd written.  Backward: g masked by (mask > 0) when mask != NULL;
+ * dgamma += sum g yhat, dbeta += sum g (fp32 atomics; zero them first); dy = the
+ * BatchNorm input gradient; g_out (optional) = the masked g. */
+int dbs_dev_bn_apply_s32(const float* d_y, const double* d_acc, const float* d_gamma, const float* d_beta, int32_t C,
+                         int64_t M, int32_t relu, float* d_mean, float* d_invstd, float* d_out, void* stream);
+int dbs_dev_bn_backward_s32(const float* d_g, const float* d_mask, const float* d_y, const float* d_mean,
+                            const float* d_invstd, const float* d_gamma, int32_t C, int64_t M, float* d_dgamma,
+                            float* d_dbeta, float* d_dy, float* d_gout, void* stream);
 int dbs_dev_conv2d_fwd_s32(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
                            int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_y, void* stream);
 int dbs_dev_conv2d_dgrad_s32(const void* d_dy, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,

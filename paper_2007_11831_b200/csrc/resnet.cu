@@ -2279,6 +2279,57 @@ extern "C" int dbs_dev_conv2d_dgrad(const void* d_dy, int32_t N, int32_t H, int3
                        static_cast<uint16_t*>(d_dx), 0, as_stream(stream));
 }
 
+// Stand-alone fp32-class BatchNorm passes (the kernels the network runs; for unit tests
+// and the bench's per-kernel HBM rooflines).  Forward: batch statistics from the conv
+// epilogue's fp64 column sums acc [sum C | sum of squares C] -> mean / invstd, out (S32)
+// = act(gamma (y - mean) invstd + beta).  Backward: g (fp32; zeroed where the S32 ReLU
+// output `mask` is not positive, when given) -> dbeta += sum g, dgamma += sum g yhat,
+// dy (S32) = the BatchNorm input gradient, g_out (fp32, optional) = the masked g.
+extern "C" int dbs_dev_bn_apply_s32(const float* d_y, const double* d_acc, const float* d_gamma, const float* d_beta,
+                                    int32_t C, int64_t M, int32_t relu, float* d_mean, float* d_invstd, float* d_out,
+                                    void* stream) {
+  DBS_REQUIRE(d_y && d_acc && d_gamma && d_beta && d_mean && d_invstd && d_out && C % 32 == 0 && C <= 2048 && M > 0,
+              DBS_ERR_ARGUMENT, "bn_apply_s32: C %% 32 == 0, C <= 2048, M > 0");
+  cudaStream_t s = as_stream(stream);
+  const int64_t total = M * (C / 8);
+  const size_t smem = (size_t)2 * C * sizeof(float);
+  DBS_CUDA_TRY(launch_pdl(bn_apply_f32_kernel, dim3(grid_one_wave(bn_apply_f32_kernel, total, 256, smem)), dim3(256),
+                          smem, s, d_y, d_acc, d_mean, d_invstd, d_gamma, d_beta, static_cast<const float*>(nullptr),
+                          static_cast<const float*>(nullptr), static_cast<const double*>(nullptr),
+                          static_cast<float*>(nullptr), static_cast<float*>(nullptr),
+                          static_cast<const float*>(nullptr), static_cast<const float*>(nullptr), relu, (int)C, M,
+                          d_out, static_cast<float*>(nullptr), static_cast<float*>(nullptr), 0.0f));
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
+extern "C" int dbs_dev_bn_backward_s32(const float* d_g, const float* d_mask, const float* d_y, const float* d_mean,
+                                       const float* d_invstd, const float* d_gamma, int32_t C, int64_t M,
+                                       float* d_dgamma, float* d_dbeta, float* d_dy, float* d_gout, void* stream) {
+  DBS_REQUIRE(d_g && d_y && d_mean && d_invstd && d_gamma && d_dgamma && d_dbeta && d_dy && C % 32 == 0 &&
+                  C <= 2048 && M > 0,
+              DBS_ERR_ARGUMENT, "bn_backward_s32: C %% 32 == 0, C <= 2048, M > 0");
+  cudaStream_t s = as_stream(stream);
+  const int cv = C / 8;
+  const int rows_per_pass = 256 / cv;
+  DBS_REQUIRE(rows_per_pass >= 1, DBS_ERR_ARGUMENT, "bn_backward_s32: C too large");
+  int blocks = (int)((M + rows_per_pass - 1) / rows_per_pass);
+  const int cap = current_sm_count() * resident_per_sm(bn_bwd_reduce_f32_kernel, 256, 0);
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_reduce_f32_kernel, dim3(blocks), dim3(256), 0, s, d_g, d_mask, d_y, d_mean, d_invstd,
+                          (int)C, M, d_dgamma, d_dbeta));
+  DBS_LAUNCH_CHECK();
+  const int64_t total = M * cv;
+  const size_t smem = (size_t)3 * C * sizeof(float);
+  DBS_CUDA_TRY(launch_pdl(bn_bwd_apply_f32_kernel, dim3(grid_one_wave(bn_bwd_apply_f32_kernel, total, 256, smem)),
+                          dim3(256), smem, s, d_g, d_mask, d_y, d_mean, d_invstd, d_gamma,
+                          static_cast<const float*>(d_dgamma), static_cast<const float*>(d_dbeta), (int)C, M, d_dy,
+                          d_gout));
+  DBS_LAUNCH_CHECK();
+  return DBS_OK;
+}
+
 // fp32-class (3xTF32) forms: S32 x / w / dy operands (rows of 32-multiples), fp32 outputs
 extern "C" int dbs_dev_conv2d_fwd_s32(const void* d_x, int32_t N, int32_t H, int32_t W, int32_t Cin, const void* d_w,
                                       int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_y, void* stream) {

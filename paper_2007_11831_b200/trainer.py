@@ -237,6 +237,7 @@ class SimulatedTrainer:
         if os.environ.get("DBS_WORKER_GRAPHS") == "0":  # A/B switch: eager launches from the host
             self.worker_graphs = False
         self._wg_cache = {}
+        self._wg_retired = []
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
         self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
@@ -363,7 +364,10 @@ class SimulatedTrainer:
             slots[w].loss = None
             slots[w].stamps = st_scratch[2 * w:].data_ptr()
             slots[w].seconds = sec_scratch.data_ptr()
-        self._run_iters(slots, 0, 1, mode, 0.0, 0.0, p, v, pb, 0, it_scratch if self.graphs else None)
+        # device-indexed (d_iter) whenever graphs will run: the iteration-index kernels (iter_increment,
+        # MLP row staging) must be loaded too
+        self._run_iters(slots, 0, 1, mode, 0.0, 0.0, p, v, pb, 0,
+                        it_scratch if (self.graphs or self.worker_graphs) else None)
         for w in range(self.n):
             slots[w].loss, slots[w].stamps, slots[w].seconds = saved[w]
         torch.cuda.synchronize()
@@ -394,7 +398,9 @@ class SimulatedTrainer:
 
     def _worker_graphs(self, key):
         """The per-worker graph set of a plan (captured by the library on first use);
-        the last few plans' sets are kept, older ones released."""
+        the last few plans' sets are kept, older ones released after the epoch's final
+        synchronisation (never here: a disturbance spin kernel may be running, and a
+        device-wide sync would wait for it forever)."""
         hit = self._wg_cache.pop(key, None)
         if hit is None:
             h = ctypes.c_void_p()
@@ -402,10 +408,13 @@ class SimulatedTrainer:
             hit = h
         self._wg_cache[key] = hit  # most recent last
         while len(self._wg_cache) > 8:
-            old_key = next(iter(self._wg_cache))
-            self.torch.cuda.synchronize()
-            _lib.lib().dbs_worker_graphs_destroy(self._wg_cache.pop(old_key))
+            self._wg_retired.append(self._wg_cache.pop(next(iter(self._wg_cache))))
         return hit
+
+    def _release_retired_graphs(self):
+        """After a device-wide sync: the evicted graph sets are no longer in flight."""
+        while self._wg_retired:
+            _lib.lib().dbs_worker_graphs_destroy(self._wg_retired.pop())
 
     # -- the epoch loop -----------------------------------------------------------
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
@@ -623,6 +632,7 @@ class SimulatedTrainer:
             if record_loss and iters > 0:
                 self._loss_host[:, :iters].copy_(self.loss_buf[:, :iters], non_blocking=True)
             torch.cuda.synchronize()
+            self._release_retired_graphs()
             ep_wall = start.elapsed_time(end) / 1e3
             if planner is not None:
                 secs = planner.seconds()

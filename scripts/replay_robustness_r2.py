@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--out", default=str(ROOT / "profiles" / "robustness_r2"))
     ap.add_argument("--dataset", type=int, default=50000)
     ap.add_argument("--forms", default="as_written,cost_x2")
+    ap.add_argument("--starts", default="10,21,31", help="epochs at which workers 0, 1, 2 get a background job")
     args = ap.parse_args()
 
     import torch
@@ -52,7 +53,7 @@ def main():
     torch.cuda.set_device(0)
     X, y = synthetic_cifar(args.dataset, seed=0)
     tr = SimulatedTrainer(X, y, n_workers=4, model="resnet18", seed=0, partition=True, max_batch=384)
-    starts = {0: 10, 1: 21, 2: 31}
+    starts = {w: int(e) for w, e in enumerate(args.starts.split(","))}
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
     sm = tr.workers[0].sm_count

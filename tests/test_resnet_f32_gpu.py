@@ -279,3 +279,47 @@ def test_conv_s32_halo_variant(dev):
                         "-k", "conv_s32_fwd_dgrad_wgrad and 64-64-3-1"],
                        env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("M,C", [(170 * 1024, 64), (4 * 256, 128), (37, 512)])
+def test_bn_passes_s32_vs_fp64(dev, M, C):
+    """The stand-alone BatchNorm passes (the network's own kernels) vs float64 torch:
+    batch-statistics forward + ReLU into S32, and the backward through ReLU + BN."""
+    import torch
+
+    from paper_2007_11831_b200 import _lib
+
+    L = _lib.lib()
+    s = _lib.stream_handle()
+    g0 = torch.Generator(device=dev).manual_seed(M + C)
+    y = torch.randn(M, C, device=dev, generator=g0) * 3 + 1
+    gamma = torch.rand(C, device=dev, generator=g0) + 0.5
+    beta = torch.randn(C, device=dev, generator=g0)
+    acc = torch.cat([y.double().sum(0), (y.double() ** 2).sum(0)]).contiguous()
+    mean, invstd = torch.empty(C, device=dev), torch.empty(C, device=dev)
+    out = torch.empty(M, 2 * C, device=dev)
+    assert L.dbs_dev_bn_apply_s32(y.data_ptr(), acc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), C, M, 1,
+                                  mean.data_ptr(), invstd.data_ptr(), out.data_ptr(), s) == 0, _lib.last_error()
+    yd = y.double().requires_grad_(True)
+    gd, bd = gamma.double().requires_grad_(True), beta.double().requires_grad_(True)
+    mu = yd.mean(0)
+    var = ((yd - mu) ** 2).mean(0)
+    z = torch.relu(gd * (yd - mu) / torch.sqrt(var + 1e-5) + bd)
+    o = out.view(M, C // 32, 2, 32)
+    got = (o[:, :, 0, :] + o[:, :, 1, :]).reshape(M, C)
+    torch.cuda.synchronize()
+    assert _rel(got, z.detach()) <= 1e-6
+    g = torch.randn(M, C, device=dev, generator=g0)
+    z.backward(g.double())
+    dgamma, dbeta = torch.zeros(C, device=dev), torch.zeros(C, device=dev)
+    dy = torch.empty(M, 2 * C, device=dev)
+    gout = torch.empty(M, C, device=dev)
+    assert L.dbs_dev_bn_backward_s32(g.data_ptr(), out.data_ptr(), y.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                                     gamma.data_ptr(), C, M, dgamma.data_ptr(), dbeta.data_ptr(), dy.data_ptr(),
+                                     gout.data_ptr(), s) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    d = dy.view(M, C // 32, 2, 32)
+    got_dy = (d[:, :, 0, :] + d[:, :, 1, :]).reshape(M, C)
+    assert _rel(got_dy, yd.grad) <= 1e-5
+    assert _rel(dgamma, gd.grad) <= 1e-5 and _rel(dbeta, bd.grad) <= 1e-5
+    assert torch.equal(gout, torch.where(got > 0, g, torch.zeros_like(g)))

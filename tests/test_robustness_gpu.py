@@ -29,3 +29,24 @@ def test_robustness_replay_short(dev, tmp_path):
     assert summary["dbs"]["epoch_wall_s"][6] < summary["fixed_ssgd"]["epoch_wall_s"][6]
     rows = list(csv.DictReader(open(tmp_path / "robustness_b200_dbs.csv")))
     assert len(rows) == 7 * 4 and {"epoch", "worker_id", "t_gpu", "t_w"} <= set(rows[0])
+
+
+def test_robustness_r2_both_forms_and_crosscheck(dev, tmp_path):
+    """The robustness scenario in both disturbance forms (the scenario as written: a 1:2
+    base-cost spread + flat extra seconds; and cost x2 jobs), with the cost-law fit and
+    the per-epoch replay through cluster.run_epoch.  Many distinct DBS plans with
+    SM-pinning spins running: the per-worker graph cache evicts without a device sync."""
+    r = subprocess.run([sys.executable, str(ROOT / "scripts" / "replay_robustness_r2.py"), "--epochs", "8",
+                        "--dataset", "12000", "--starts", "2,4,6", "--out", str(tmp_path)],
+                       capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    summary = json.loads((tmp_path / "summary.json").read_text())
+    for form in ("as_written", "cost_x2"):
+        e = summary[form]
+        assert e["measured_total_s"]["dbs"] > 0 and e["measured_total_s"]["fixed_ssgd"] > 0
+        assert all(c > 0 for c in e["fit"]["base_cost_s_per_sample"])
+        for kind in ("fixed_ssgd", "dbs"):
+            assert e["per_epoch_prediction_error"][kind]["epochs"] == 7
+        rows = list(csv.DictReader(open(tmp_path / f"robustness_{form}_b200_dbs.csv")))
+        assert len(rows) == 8 * 4
+    assert 1.0 < summary["cost_x2"]["fit"]["measured_multiplier"][0] < 3.0
