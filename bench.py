@@ -512,8 +512,8 @@ def bn_rooflines(tr, peaks, reps=20):
     dbs_dev_bn_*_s32) at the bench's largest BN shape (b per worker x 32 x 32 x 64),
     timed where the bench runs them -- inside worker 0's SM partition, eager launches
     between CUDA events on the partition's stream -- against the copy bandwidth the
-    same partition reaches (the repartition gather with an identity index: 8 B per
-    element).  Bytes per element: forward 4 (y) + 8 (S32 out); backward 12 (reduce:
+    same partition reaches (the repartition gather with an identity index over the
+    same bytes in 16 KB rows).  Bytes per element: forward 4 (y) + 8 (S32 out); backward 12 (reduce:
     g, y, mask hi plane) + 24 (apply: g, y, mask, S32 dy, g_out)."""
     import torch
 
@@ -532,18 +532,21 @@ def bn_rooflines(tr, peaks, reps=20):
     g = torch.randn(M, C, device=dev, generator=g0)
     dgam, dbet = torch.zeros(C, device=dev), torch.zeros(C, device=dev)
     dy, gout = torch.empty(M, 2 * C, device=dev), torch.empty(M, C, device=dev)
-    idx = torch.arange(M, device=dev)
+    # the copy reference: the same bytes as y moved by the repartition gather in 16 KB rows
+    # (its efficient regime; 256-byte rows would understate the partition's bandwidth)
+    cp_rows = M * C * 4 // 16384
+    idx = torch.arange(cp_rows, device=dev)
     cp = torch.empty_like(y)
     h = int(wk.stream.cuda_stream)
     fns = {
-        "copy": lambda: L.dbs_dev_gather_rows(y.data_ptr(), idx.data_ptr(), M, 4 * C, cp.data_ptr(), h),
+        "copy": lambda: L.dbs_dev_gather_rows(y.data_ptr(), idx.data_ptr(), cp_rows, 16384, cp.data_ptr(), h),
         "bn_forward": lambda: L.dbs_dev_bn_apply_s32(y.data_ptr(), acc.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
                                                     C, M, 1, mean.data_ptr(), invstd.data_ptr(), out.data_ptr(), h),
         "bn_backward": lambda: L.dbs_dev_bn_backward_s32(g.data_ptr(), out.data_ptr(), y.data_ptr(), mean.data_ptr(),
                                                         invstd.data_ptr(), gamma.data_ptr(), C, M, dgam.data_ptr(),
                                                         dbet.data_ptr(), dy.data_ptr(), gout.data_ptr(), h),
     }
-    byts = {"copy": 8.0 * M * C + 8.0 * M, "bn_forward": 12.0 * M * C, "bn_backward": 36.0 * M * C}
+    byts = {"copy": 2.0 * cp_rows * 16384 + 8.0 * cp_rows, "bn_forward": 12.0 * M * C, "bn_backward": 36.0 * M * C}
     res = {}
     torch.cuda.synchronize()
     _lib.check(L.dbs_partition_push(wk.ctx), "partition_push")

@@ -475,6 +475,11 @@ int dbs_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, in
 typedef struct dbs_worker_graphs dbs_worker_graphs;
 int dbs_worker_graphs_create(int32_t n, dbs_worker_graphs** out);
 int dbs_worker_graphs_destroy(dbs_worker_graphs* g);
+/* Capture the graph set (nothing runs); called before the epoch's disturbance spins
+ * start (capturing may load kernels, which must not wait behind a spinning kernel). */
+int dbs_worker_graphs_capture(const dbs_worker_slot* workers, int32_t n, int32_t mode, float lr, float momentum,
+                              float* d_params, float* d_velocity, void* d_params_shadow, int32_t skip_update,
+                              void* agg_stream, int64_t* d_iter, dbs_worker_graphs* graphs);
 int dbs_run_iterations_graphed(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                float lr, float momentum, float* d_params, float* d_velocity, void* d_params_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_worker_graphs* graphs);

@@ -19,6 +19,7 @@
 //            "shard written" to all peers and waits for theirs, so the kernel
 //            completes only when every rank's parameters are whole.
 // NCCL is not involved; torch.distributed only carries the IPC handles.
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -108,8 +109,8 @@ __device__ __forceinline__ uint32_t bf16_bits(float f) {
 
 // mode 0: gradient all-reduce + SGD;  mode 1: parameter averaging
 // BF16: also push the bf16 operand shadow (an S32-shadow communicator refreshes its own)
-template <int MODE, bool BF16>
-__global__ void __launch_bounds__(kThreads, 2) fused_kernel(PeerTable T, int rank, int world, int64_t shard4,
+template <int MODE, bool BF16, int kUnroll>
+__global__ void __launch_bounds__(kThreads) fused_kernel(PeerTable T, int rank, int world, int64_t shard4,
                                                          float lr, float mom, float4* __restrict__ vel,
                                                          uint32_t gen) {
   uint32_t* my_sig = T.signal[rank];
@@ -121,9 +122,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(PeerTable T, int ran
   }
   __syncthreads();
   // ---- phase 1: reduce my shard, update, push to every peer -----------------
-  // kUnroll float4s per thread and trip, every peer's loads issued before any use:
+  // kUnroll float4s per thread and trip, every peer's loads issued before any use
   // up to 8 x kUnroll 16-byte NVLink reads in flight per thread (latency-bound otherwise)
-  constexpr int kUnroll = 2;
   const int64_t base4 = (int64_t)rank * shard4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < shard4; i0 += stride * kUnroll) {
@@ -196,6 +196,25 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(PeerTable T, int ran
   }
 }
 
+// float4s per thread and trip / resident CTAs per SM (DBS_COMM_UNROLL, DBS_COMM_CTAS:
+// measurement switches; defaults are the measured configuration)
+int comm_unroll() {
+  static const int u = [] {
+    const char* e = getenv("DBS_COMM_UNROLL");
+    const int v = e ? atoi(e) : 1;
+    return (v == 1 || v == 2 || v == 4) ? v : 1;
+  }();
+  return u;
+}
+int comm_ctas_per_sm() {
+  static const int c = [] {
+    const char* e = getenv("DBS_COMM_CTAS");
+    const int v = e ? atoi(e) : 2;
+    return (v >= 1 && v <= 8) ? v : 2;
+  }();
+  return c;
+}
+
 int ipc_handle_size() { return (int)sizeof(cudaIpcMemHandle_t); }
 
 size_t block_layout(int64_t P, size_t* off_param, size_t* off_bf16, size_t* off_sig) {
@@ -231,18 +250,30 @@ int launch_fused(dbs_comm* c, const int64_t* batch_sizes, int32_t mode, int kind
   c->gen += 1;
   const int64_t shard4 = c->shard / 4;
   const bool bf = c->shadow_prec == DBS_PREC_BF16;
+  const int u = comm_unroll();
+#define DBS_COMM_LAUNCH(K, B, U)                                                                                     \
+  fused_kernel<K, B, U><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, K == 0 ? lr : 0.f,     \
+                                                     K == 0 ? mom : 0.f,                                          \
+                                                     K == 0 ? reinterpret_cast<float4*>(vel) : nullptr, c->gen)
+#define DBS_COMM_LAUNCH_U(K, B) \
+  do {                          \
+    if (u == 1)                 \
+      DBS_COMM_LAUNCH(K, B, 1); \
+    else if (u == 4)            \
+      DBS_COMM_LAUNCH(K, B, 4); \
+    else                        \
+      DBS_COMM_LAUNCH(K, B, 2); \
+  } while (0)
   if (kind == 0 && bf)
-    fused_kernel<0, true><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, lr, mom,
-                                                        reinterpret_cast<float4*>(vel), c->gen);
+    DBS_COMM_LAUNCH_U(0, true);
   else if (kind == 0)
-    fused_kernel<0, false><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, lr, mom,
-                                                         reinterpret_cast<float4*>(vel), c->gen);
+    DBS_COMM_LAUNCH_U(0, false);
   else if (bf)
-    fused_kernel<1, true><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, 0.f, 0.f, nullptr,
-                                                        c->gen);
+    DBS_COMM_LAUNCH_U(1, true);
   else
-    fused_kernel<1, false><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, 0.f, 0.f, nullptr,
-                                                         c->gen);
+    DBS_COMM_LAUNCH_U(1, false);
+#undef DBS_COMM_LAUNCH_U
+#undef DBS_COMM_LAUNCH
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
@@ -265,8 +296,9 @@ static int comm_new(int32_t rank, int32_t world, int64_t P, dbs_comm** out) {
   c->shard = c->P / world;
   size_t op, ob, os;
   c->block_bytes = block_layout(c->P, &op, &ob, &os);
-  const int64_t want = (c->shard / 4 + 2 * kThreads - 1) / (2 * kThreads);  // 2 float4 per thread and trip
-  const int64_t cap = (int64_t)num_sms() * 2;  // 2 x 256 threads x 2 float4 x (W peers + x + v) in flight per SM
+  const int64_t per = (int64_t)kThreads * comm_unroll();  // float4s per CTA and trip
+  const int64_t want = (c->shard / 4 + per - 1) / per;
+  const int64_t cap = (int64_t)num_sms() * comm_ctas_per_sm();
   c->grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   *out = c;
   return DBS_OK;

@@ -433,7 +433,8 @@ extern "C" int dbs_comm_shadow(const dbs_comm* c, void** d_shadow, int32_t* prec
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                float mom, float* d_params, float* d_velocity, void* d_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
-                               const int64_t* rank_batches, dbs_worker_graphs* graphs = nullptr);
+                               const int64_t* rank_batches, dbs_worker_graphs* graphs = nullptr,
+                               bool capture_only = false);
 
 namespace dbs {
 long long launch_count();
@@ -476,6 +477,18 @@ extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t
                              agg_stream, d_iter, nullptr, nullptr);
 }
 
+// Capture (and instantiate) the per-worker graphs without running anything: done
+// before an epoch's disturbance kernels start, since capturing may load kernels
+// lazily and a module load would wait behind a spin kernel that owns SMs.
+extern "C" int dbs_worker_graphs_capture(const dbs_worker_slot* w, int32_t n, int32_t mode, float lr, float mom,
+                                         float* d_params, float* d_velocity, void* d_params_shadow,
+                                         int32_t skip_update, void* agg_stream, int64_t* d_iter,
+                                         dbs_worker_graphs* graphs) {
+  DBS_REQUIRE(graphs, DBS_ERR_ARGUMENT, "worker_graphs_capture: null graphs");
+  return run_iterations_impl(w, n, 0, 0, mode, lr, mom, d_params, d_velocity, d_params_shadow, skip_update,
+                             agg_stream, d_iter, nullptr, nullptr, graphs, true);
+}
+
 extern "C" int dbs_run_iterations_graphed(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                           float lr, float mom, float* d_params, float* d_velocity,
                                           void* d_params_shadow, int32_t skip_update, void* agg_stream,
@@ -510,7 +523,7 @@ extern "C" int dbs_run_iterations_comm(const dbs_worker_slot* w, int32_t n, int6
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                float mom, float* d_params, float* d_velocity, void* d_shadow,
                                int32_t skip_update, void* agg_stream, int64_t* d_iter, dbs_comm* comm,
-                               const int64_t* rank_batches, dbs_worker_graphs* graphs) {
+                               const int64_t* rank_batches, dbs_worker_graphs* graphs, bool capture_only) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0, DBS_ERR_ARGUMENT, "run_iterations: bad arguments");
   for (int i = 0; i < n; i++)
     DBS_REQUIRE(w[i].model && (w[i].model_kind == DBS_MODEL_MLP || w[i].model_kind == DBS_MODEL_RESNET18),
@@ -609,6 +622,7 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
       if (st) return st;
       if (st_pop) return st_pop;
     }
+    if (capture_only) return DBS_OK;
   }
   DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
   for (int64_t t = t0; t < t1; t++) {

@@ -272,6 +272,7 @@ class SimulatedTrainer:
         self._graph_cache = {}
         self.graph_iters = 8  # iterations per captured graph
         self._primed = False
+        self._primed_batches = None
 
     # -- helpers --------------------------------------------------------------
     def _scratch(self, w: int, b: int):
@@ -565,8 +566,21 @@ class SimulatedTrainer:
                     # GPU a 2-CTA timed spin delays only this worker's stream
                     slots[w].spin_ctas = wk.sm_count if wk.ctx else 2
                     spin_key.append((w, "+", slots[w].spin_ns))
+            if iters > 0 and spinning and not self.worker_graphs and tuple(batches) != self._primed_batches:
+                # eager launches behind a running spin: a new plan may select kernel
+                # instantiations not loaded yet (lazy loading would wait behind the spin)
+                self._primed = False
             if iters > 0 and (spinning or self.graphs):
                 self._prime(slots, mode)
+                self._primed_batches = tuple(batches)
+            wg = None
+            if self.worker_graphs and iters > 0 and not local:
+                # capture this plan's per-worker graphs now, before any spin starts
+                wg = self._worker_graphs((tuple(batches), tuple(spin_key), bool(record_loss)))
+                _lib.check(_lib.lib().dbs_worker_graphs_capture(
+                    slots, self.n, mode, float(lr), float(momentum), self.model.params.data_ptr(),
+                    self.model.velocity.data_ptr(), self.model.params_op.data_ptr(), int(skip_update),
+                    int(self.agg.cuda_stream), self.d_iter.data_ptr(), wg), "worker_graphs_capture")
             graph = graph_r = None
             per_replay = per_r = 0
             k_it = 1
@@ -608,8 +622,7 @@ class SimulatedTrainer:
                                                              int(local_interval), self._rep_ptrs[0], self._rep_ptrs[1],
                                                              self._rep_ptrs[2], int(self.agg.cuda_stream))
                     _lib.check(st, "run_iterations_local")
-                elif self.worker_graphs:
-                    wg = self._worker_graphs((tuple(batches), tuple(spin_key), bool(record_loss)))
+                elif wg is not None:
                     st = _lib.lib().dbs_run_iterations_graphed(
                         slots, self.n, 0, iters, mode, float(lr), float(momentum), self.model.params.data_ptr(),
                         self.model.velocity.data_ptr(), self.model.params_op.data_ptr(), int(skip_update),
@@ -862,7 +875,15 @@ class DistributedTrainer(SimulatedTrainer):
             rank_batches = np.asarray([sum(batches[r * n_loc:(r + 1) * n_loc]) for r in range(self.world)],
                                       dtype=np.int64)
             if iters > 0:
+                # a new plan: load its kernels before the spin starts -- decided on the GLOBAL
+                # plan (identical on every rank), since the prime runs the collective kernel
+                any_spin = profiles is not None and any(
+                    (lambda ev: ev is not None and ev.cost_multiplier is not None and ev.cost_multiplier > 1.0)(
+                        p.active_disturbance(epoch)) for p in profiles)
+                if any_spin and tuple(batches) != self._primed_batches:
+                    self._primed = False
                 self._prime_comm(slots, mode, rank_batches)
+                self._primed_batches = tuple(batches)
             cur = torch.cuda.current_stream()
             for wk, ctas in spinning:
                 wk.spin_stream.wait_stream(cur)
