@@ -504,6 +504,13 @@ int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* batch_size
 int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                              float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
                              void* const* d_params_shadow, void* agg_stream);
+/* The same with one CUDA graph per worker (forward/backward + its local step, captured
+ * in its own partition's context); d_iters[n] are per-worker device iteration counters
+ * (zero them at the epoch start); capture_only = 1 captures without running. */
+int dbs_run_iterations_local_graphed(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                     float lr, float mom, int32_t sync_interval, float* const* d_params,
+                                     float* const* d_velocity, void* const* d_params_shadow, void* agg_stream,
+                                     int64_t* d_iters, dbs_worker_graphs* graphs, int32_t capture_only);
 /* The same across GPUs (one process per GPU): after the local average of every
  * sync round, d_params[0] -- which must be the communicator's parameter block --
  * is averaged across ranks with rank weights = rank_batches[r] (the ranks' batch

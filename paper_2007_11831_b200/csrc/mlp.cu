@@ -687,7 +687,8 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
 static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                 float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
                                 void* const* d_shadows, void* agg_stream, dbs_comm* comm,
-                                const int64_t* rank_batches);
+                                const int64_t* rank_batches, dbs_worker_graphs* graphs = nullptr,
+                                int64_t* d_iters = nullptr, bool capture_only = false);
 
 extern "C" int dbs_run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                         float lr, float mom, int32_t sync_interval, float* const* d_params,
@@ -711,10 +712,25 @@ extern "C" int dbs_run_iterations_local_comm(const dbs_worker_slot* w, int32_t n
                               agg_stream, comm, rank_batches);
 }
 
+// Per-worker CUDA graphs for local SGD (graphs != NULL): worker i's block -- forward /
+// backward reading its own device iteration counter d_iters[i], its local momentum
+// step, the counter increment -- is captured once in its partition's context and
+// replayed each iteration; the periodic averaging stays on the aggregation stream.
+extern "C" int dbs_run_iterations_local_graphed(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1,
+                                                int32_t mode, float lr, float mom, int32_t sync_interval,
+                                                float* const* d_params, float* const* d_velocity,
+                                                void* const* d_params_shadow, void* agg_stream, int64_t* d_iters,
+                                                dbs_worker_graphs* graphs, int32_t capture_only) {
+  DBS_REQUIRE(graphs && d_iters, DBS_ERR_ARGUMENT, "run_iterations_local_graphed: graphs and d_iters required");
+  return run_iterations_local(w, n, t0, t1, mode, lr, mom, sync_interval, d_params, d_velocity, d_params_shadow,
+                              agg_stream, nullptr, nullptr, graphs, d_iters, capture_only != 0);
+}
+
 static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,
                                 float mom, int32_t sync_interval, float* const* d_params, float* const* d_velocity,
                                 void* const* d_shadows, void* agg_stream, dbs_comm* comm,
-                                const int64_t* rank_batches) {
+                                const int64_t* rank_batches, dbs_worker_graphs* graphs, int64_t* d_iters,
+                                bool capture_only) {
   DBS_REQUIRE(w && n >= 1 && n <= 64 && t1 >= t0 && sync_interval >= 1 && d_params && d_velocity && d_shadows,
               DBS_ERR_ARGUMENT, "run_iterations_local: bad arguments");
   for (int i = 0; i < n; i++)
@@ -731,15 +747,9 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
   for (int i = 0; i < n; i++) batches[i] = w[i].batch;
   const int64_t P = (w[0].model_kind == DBS_MODEL_MLP) ? static_cast<const dbs_mlp*>(w[0].model)->P
                                                        : resnet_param_count(static_cast<const dbs_resnet*>(w[0].model));
-  DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
-  for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(as_stream(w[i].stream), ev[n], 0));
-  for (int64_t t = t0; t < t1; t++) {
-    const bool sync = ((t + 1) % sync_interval) == 0;
-    for (int i = 0; i < n; i++) {
-      cudaStream_t s = as_stream(w[i].stream);
-      st = ctx_push(w[i].ctx);
-      if (st) return st;
-      st = [&]() -> int {
+  // worker i's part of local iteration t on stream s (its partition's context current);
+  // dev: iteration index from d_iters[i] (graph capture), incremented at the end
+  auto issue_local = [&](int i, cudaStream_t s, int64_t t, bool dev) -> int {
         if (w[i].stamps) {
           st = stamp(w[i].stamps, 0, s);
           if (st) return st;
@@ -749,15 +759,27 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
           if (st) return st;
         }
         const int64_t b = w[i].batch;
-        const char* x = static_cast<const char*>(w[i].x_shard) + t * b * slot_row_bytes(w[i]);
-        if (w[i].model_kind == DBS_MODEL_MLP) {
-          dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
-          st = mlp_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, b, w[i].grad,
-                           w[i].loss ? w[i].loss + t : w[i].loss_scratch, s, nullptr, 0);
+        if (dev) {
+          if (w[i].model_kind == DBS_MODEL_MLP) {
+            dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
+            st = mlp_fwd_bwd(m, d_shadows[i], d_params[i], w[i].x_shard, w[i].y_shard, b, w[i].grad,
+                             w[i].loss ? w[i].loss : w[i].loss_scratch, s, d_iters + i, w[i].loss ? 1 : 0);
+          } else {
+            dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
+            st = resnet_fwd_bwd(m, d_shadows[i], d_params[i], w[i].x_shard, w[i].y_shard, d_iters + i, b,
+                                w[i].grad, w[i].loss, s);
+          }
         } else {
-          dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
-          st = resnet_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,
-                              w[i].loss ? w[i].loss + t : nullptr, s);
+          const char* x = static_cast<const char*>(w[i].x_shard) + t * b * slot_row_bytes(w[i]);
+          if (w[i].model_kind == DBS_MODEL_MLP) {
+            dbs_mlp* m = static_cast<dbs_mlp*>(w[i].model);
+            st = mlp_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, b, w[i].grad,
+                             w[i].loss ? w[i].loss + t : w[i].loss_scratch, s, nullptr, 0);
+          } else {
+            dbs_resnet* m = static_cast<dbs_resnet*>(w[i].model);
+            st = resnet_fwd_bwd(m, d_shadows[i], d_params[i], x, w[i].y_shard + t * b, nullptr, b, w[i].grad,
+                                w[i].loss ? w[i].loss + t : nullptr, s);
+          }
         }
         if (st) return st;
         if (w[i].stamps) {
@@ -778,6 +800,60 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
         st = dbs_dev_aggregate_sgd_f32_ex(&g, &one, 1, DBS_AGG_UNIFORM, P, lr, mom, d_params[i], d_velocity[i],
                                           d_shadows[i], prec, s);
         if (st) return st;
+        if (dev) {
+          st = iter_increment(d_iters + i, s);
+          if (st) return st;
+        }
+        return DBS_OK;
+  };
+  if (graphs) {
+    DBS_REQUIRE(graphs->n == n, DBS_ERR_ARGUMENT, "run_iterations_local: graph set for %d workers", graphs->n);
+    for (int i = 0; i < n; i++) {
+      if (graphs->exec[i]) continue;
+      cudaStream_t s = as_stream(w[i].stream);
+      st = ctx_push(w[i].ctx);
+      if (st) return st;
+      const long long c0 = launch_count();
+      st = [&]() -> int {
+        DBS_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int st_w = issue_local(i, s, 0, true);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e_end = cudaStreamEndCapture(s, &g);
+        if (st_w) {
+          if (g) cudaGraphDestroy(g);
+          return st_w;
+        }
+        DBS_CUDA_TRY(e_end);
+        const cudaError_t e_inst = cudaGraphInstantiate(&graphs->exec[i], g, 0);
+        cudaGraphDestroy(g);
+        DBS_CUDA_TRY(e_inst);
+        return DBS_OK;
+      }();
+      graphs->kernels[i] = launch_count() - c0;
+      add_launches(-graphs->kernels[i]);
+      const int st_pop = ctx_pop(w[i].ctx);
+      if (st) return st;
+      if (st_pop) return st_pop;
+    }
+    if (capture_only) return DBS_OK;
+  }
+  DBS_CUDA_TRY(cudaEventRecord(ev[n], agg));
+  for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(as_stream(w[i].stream), ev[n], 0));
+  for (int64_t t = t0; t < t1; t++) {
+    const bool sync = ((t + 1) % sync_interval) == 0;
+    for (int i = 0; i < n; i++) {
+      cudaStream_t s = as_stream(w[i].stream);
+      st = ctx_push(w[i].ctx);
+      if (st) return st;
+      st = [&]() -> int {
+        if (graphs) {
+          DBS_CUDA_TRY(cudaGraphLaunch(graphs->exec[i], s));
+          add_launches(graphs->kernels[i]);
+          count_host_launch();
+        } else {
+          const int st_w = issue_local(i, s, t, false);
+          if (st_w) return st_w;
+        }
         if (sync) DBS_CUDA_TRY(cudaEventRecord(ev[i], s));
         return DBS_OK;
       }();

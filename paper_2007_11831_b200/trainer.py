@@ -581,6 +581,17 @@ class SimulatedTrainer:
                     slots, self.n, mode, float(lr), float(momentum), self.model.params.data_ptr(),
                     self.model.velocity.data_ptr(), self.model.params_op.data_ptr(), int(skip_update),
                     int(self.agg.cuda_stream), self.d_iter.data_ptr(), wg), "worker_graphs_capture")
+            elif self.worker_graphs and iters > 0 and local:
+                # local SGD: per-worker graphs over the replicas (their addresses are part of the key)
+                if getattr(self, "_local_iters", None) is None or self._local_iters.numel() != n:
+                    self._local_iters = torch.zeros(n, dtype=torch.int64, device=self.dev)
+                self._local_iters.zero_()
+                wg = self._worker_graphs(("local", tuple(batches), tuple(spin_key), bool(record_loss), float(lr),
+                                          float(momentum), self._rep_ptrs[0][0]))
+                _lib.check(_lib.lib().dbs_run_iterations_local_graphed(
+                    slots, self.n, 0, 0, mode, float(lr), float(momentum), int(local_interval), self._rep_ptrs[0],
+                    self._rep_ptrs[1], self._rep_ptrs[2], int(self.agg.cuda_stream), self._local_iters.data_ptr(),
+                    wg, 1), "worker_graphs_capture (local)")
             graph = graph_r = None
             per_replay = per_r = 0
             k_it = 1
@@ -617,6 +628,12 @@ class SimulatedTrainer:
                         if graph_r is not None:
                             graph_r.replay()
                     replays = iters // k_it + (graph_r is not None)
+                elif local and wg is not None:
+                    st = _lib.lib().dbs_run_iterations_local_graphed(
+                        slots, self.n, 0, iters, mode, float(lr), float(momentum), int(local_interval),
+                        self._rep_ptrs[0], self._rep_ptrs[1], self._rep_ptrs[2], int(self.agg.cuda_stream),
+                        self._local_iters.data_ptr(), wg, 0)
+                    _lib.check(st, "run_iterations_local_graphed")
                 elif local:
                     st = _lib.lib().dbs_run_iterations_local(slots, self.n, 0, iters, mode, float(lr), float(momentum),
                                                              int(local_interval), self._rep_ptrs[0], self._rep_ptrs[1],

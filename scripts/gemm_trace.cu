@@ -9,7 +9,9 @@ int main(int argc, char** argv) {
   // gemm_trace M N K            plain GEMM
   // gemm_trace conv N H C       3x3 stride-1 C->C conv forward on an N x H x H x C map
   // gemm_trace f32conv N H C    the same conv, fp32 class (3xTF32 on S32 operands)
-  const bool f32 = argc > 1 && argv[1][0] == 'f';
+  // gemm_trace wgrad N H C       the fp32-class weight gradient of the same conv
+  const bool wgrad = argc > 1 && argv[1][0] == 'w';
+  const bool f32 = argc > 1 && (argv[1][0] == 'f' || wgrad);
   const bool conv = argc > 1 && (argv[1][0] == 'c' || f32);
   const int o = conv ? 1 : 0;
   long M = argc > 1 + o ? atol(argv[1 + o]) : 131072, N = argc > 2 + o ? atol(argv[2 + o]) : 64, K = argc > 3 + o ? atol(argv[3 + o]) : 64;
@@ -20,6 +22,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&a, abytes); cudaMalloc(&b, bbytes); cudaMalloc(&d, dbytes);
   cudaMemset(a, 0x3c, abytes); cudaMemset(b, 0x3c, bbytes);
   auto run = [&]() {
+    if (wgrad) return dbs_dev_conv2d_wgrad_s32(a, a, (int)M, (int)N, (int)N, (int)K, (int)K, 3, 1, 1, (float*)d, nullptr);
     if (f32) return dbs_dev_conv2d_fwd_s32(a, (int)M, (int)N, (int)N, (int)K, b, (int)K, 3, 1, 1, (float*)d, nullptr);
     return conv ? dbs_dev_conv2d_fwd(a, (int)M, (int)N, (int)N, (int)K, b, (int)K, 3, 1, 1, d, nullptr)
                 : dbs_dev_gemm_bf16(a, 0, K, b, 0, K, d, N, M, N, K, DBS_EPI_BF16, nullptr, nullptr, nullptr);

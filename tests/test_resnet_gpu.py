@@ -243,3 +243,31 @@ def test_partition_worker_graphs_match_eager(dev):
     assert np.abs(out[0][0] - out[1][0]).max() <= 10 * noise + 1e-5
     pn = np.linalg.norm(out[1][1] - out[2][1])
     assert np.linalg.norm(out[0][1] - out[1][1]) <= 10 * pn + 1e-6 * np.linalg.norm(out[1][1])
+
+
+def test_partition_worker_graphs_local_sgd(dev):
+    """Local SGD with periodic averaging (config 4) in SM partitions: the per-worker
+    graphs (forward/backward + local step, per-worker device iteration counters) agree
+    with eager launches to the run-to-run noise."""
+    import numpy as np
+
+    from paper_2007_11831_b200 import cluster, resnet
+    from paper_2007_11831_b200.trainer import SimulatedTrainer
+
+    X, y = resnet.synthetic_cifar(3000, seed=1)
+    prof = [cluster.WorkerProfile(0, 1.0, disturbances=(cluster.DisturbanceEvent(0, cost_multiplier=2.0),)),
+            cluster.WorkerProfile(1, 1.0), cluster.WorkerProfile(2, 1.0)]
+    cfg = cluster.StrategyConfig("model_averaging", 96, sync_interval=2)
+    out = []
+    for graphs in (True, False, False):
+        tr = SimulatedTrainer(X, y, n_workers=3, model="resnet18", seed=0, partition=True, max_batch=96)
+        tr.worker_graphs = graphs
+        res = tr.run(cfg, n_epochs=2, lr=0.05, momentum=0.9, profiles=prof, max_iters=6)
+        out.append((res.losses.copy(), tr.model.params.detach().cpu().numpy().astype(np.float64)))
+        del tr
+    assert len(out[0][0]) == 6 and np.all(np.isfinite(out[0][0]))
+    assert abs(out[0][0][0] - out[1][0][0]) <= 1e-6 * abs(out[1][0][0])
+    noise = np.abs(out[1][0] - out[2][0]).max()
+    assert np.abs(out[0][0] - out[1][0]).max() <= 10 * noise + 1e-5
+    pn = np.linalg.norm(out[1][1] - out[2][1])
+    assert np.linalg.norm(out[0][1] - out[1][1]) <= 10 * pn + 1e-6 * np.linalg.norm(out[1][1])
