@@ -540,6 +540,7 @@ class SimulatedTrainer:
                 prof = profiles[w] if profiles is not None else None
                 m = cluster.effective_cost(prof, epoch) / base_min if prof is not None else 1.0
                 wk = self.workers[w]
+                pinned = 0
                 if emulate:
                     # emulated device: m x b x the per-sample time, whatever the batch
                     slots[w].spin_ns = int(m * batches[w] * self.device_per_sample_ns)
@@ -552,6 +553,7 @@ class SimulatedTrainer:
                         ctas = max(0, min(ctas, wk.sm_count - 1))
                         if ctas:
                             spinning.append((wk, ctas))
+                            pinned = ctas
                     else:
                         # simulated workers share the GPU's SMs: the slow worker's
                         # device is emulated as m x its own forward/backward time
@@ -562,9 +564,10 @@ class SimulatedTrainer:
                 if ev is not None and ev.extra_epoch_seconds:
                     # flat extra seconds (cluster.py:141-143), spread over the epoch's iterations
                     slots[w].spin_ns += int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
-                    # in its own partition the spin occupies the worker's SMs; on a shared
-                    # GPU a 2-CTA timed spin delays only this worker's stream
-                    slots[w].spin_ctas = wk.sm_count if wk.ctx else 2
+                    # in its own partition the spin occupies the worker's free SMs (one wave:
+                    # the SMs a co-running pinning spin holds are not available to it); on a
+                    # shared GPU a 2-CTA timed spin delays only this worker's stream
+                    slots[w].spin_ctas = max(1, wk.sm_count - pinned) if wk.ctx else 2
                     spin_key.append((w, "+", slots[w].spin_ns))
             if iters > 0 and spinning and not self.worker_graphs and tuple(batches) != self._primed_batches:
                 # eager launches behind a running spin: a new plan may select kernel
