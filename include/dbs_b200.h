@@ -491,6 +491,12 @@ int dbs_run_iterations_graphed(const dbs_worker_slot* workers, int32_t n, int64_
 int dbs_run_iterations_comm(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                             float lr, float momentum, dbs_comm* comm, const int64_t* rank_batches,
                             float* d_velocity_shard, void* agg_stream, int64_t* d_iter);
+/* The multi-GPU form with per-worker graphs (see dbs_run_iterations_graphed);
+ * capture_only = 1 captures the set without running (before the epoch's spins). */
+int dbs_run_iterations_comm_graphed(const dbs_worker_slot* workers, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                                    float lr, float momentum, dbs_comm* comm, const int64_t* rank_batches,
+                                    float* d_velocity_shard, void* agg_stream, int64_t* d_iter,
+                                    dbs_worker_graphs* graphs, int32_t capture_only);
 /* fp32 weighted reduce out = sum_i w_i g_i (DBS_AGG_*), no step. */
 int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* batch_sizes, int64_t n, int32_t mode, int64_t P,
                           float* d_out, void* stream);

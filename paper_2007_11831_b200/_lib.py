@@ -141,6 +141,8 @@ SIGNATURES = {
                                           c_i32, c_vp, c_vp, c_vp]),
     "dbs_run_iterations_local_graphed": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt,
                                                  c_flt, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "dbs_run_iterations_comm_graphed": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt,
+                                                c_vp, P_i64, c_vp, c_vp, c_vp, c_vp, c_i32]),
     "dbs_worker_graphs_create": (c_i32, [c_i32, ctypes.POINTER(c_vp)]),
     "dbs_worker_graphs_destroy": (c_i32, [c_vp]),
     "dbs_run_iterations_comm": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp,

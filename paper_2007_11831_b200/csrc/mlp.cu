@@ -503,9 +503,33 @@ extern "C" int dbs_run_iterations_graphed(const dbs_worker_slot* w, int32_t n, i
 // one worker, whose gradient is written there directly) and the fused NVLink
 // all-reduce + momentum SGD with per-rank weights rank_batches[r] = sum of
 // that rank's worker batches.  Parameters live in the communicator's blocks.
+static int run_iterations_comm(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                               float lr, float mom, dbs_comm* comm, const int64_t* rank_batches,
+                               float* d_velocity_shard, void* agg_stream, int64_t* d_iter,
+                               dbs_worker_graphs* graphs, bool capture_only);
+
 extern "C" int dbs_run_iterations_comm(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
                                        float lr, float mom, dbs_comm* comm, const int64_t* rank_batches,
                                        float* d_velocity_shard, void* agg_stream, int64_t* d_iter) {
+  return run_iterations_comm(w, n, t0, t1, mode, lr, mom, comm, rank_batches, d_velocity_shard, agg_stream, d_iter,
+                             nullptr, false);
+}
+
+// the multi-GPU form with per-worker graphs (capture_only = 1: capture, run nothing)
+extern "C" int dbs_run_iterations_comm_graphed(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1,
+                                               int32_t mode, float lr, float mom, dbs_comm* comm,
+                                               const int64_t* rank_batches, float* d_velocity_shard,
+                                               void* agg_stream, int64_t* d_iter, dbs_worker_graphs* graphs,
+                                               int32_t capture_only) {
+  DBS_REQUIRE(graphs && d_iter, DBS_ERR_ARGUMENT, "run_iterations_comm_graphed: graphs and d_iter required");
+  return run_iterations_comm(w, n, t0, t1, mode, lr, mom, comm, rank_batches, d_velocity_shard, agg_stream, d_iter,
+                             graphs, capture_only != 0);
+}
+
+static int run_iterations_comm(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode,
+                               float lr, float mom, dbs_comm* comm, const int64_t* rank_batches,
+                               float* d_velocity_shard, void* agg_stream, int64_t* d_iter,
+                               dbs_worker_graphs* graphs, bool capture_only) {
   DBS_REQUIRE(comm && rank_batches && d_velocity_shard, DBS_ERR_ARGUMENT, "run_iterations_comm: null argument");
   float *g = nullptr, *p = nullptr;
   void* sh = nullptr;
@@ -517,7 +541,7 @@ extern "C" int dbs_run_iterations_comm(const dbs_worker_slot* w, int32_t n, int6
   DBS_REQUIRE(n >= 1 && prec == slot_precision(w[0]), DBS_ERR_ARGUMENT,
               "run_iterations_comm: the communicator's shadow precision differs from the model's");
   return run_iterations_impl(w, n, t0, t1, mode, lr, mom, p, d_velocity_shard, sh, 0, agg_stream, d_iter, comm,
-                             rank_batches);
+                             rank_batches, graphs, capture_only);
 }
 
 static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, int64_t t1, int32_t mode, float lr,

@@ -904,6 +904,15 @@ class DistributedTrainer(SimulatedTrainer):
                     self._primed = False
                 self._prime_comm(slots, mode, rank_batches)
                 self._primed_batches = tuple(batches)
+            wg = None
+            if self.worker_graphs and iters > 0 and not local:
+                # this plan's per-worker graphs, captured before any spin starts
+                self.d_iter.zero_()
+                wg = self._worker_graphs(("comm", tuple(batches), tuple((w, slots[w].spin_ns) for w in range(n_loc))))
+                _lib.check(_lib.lib().dbs_run_iterations_comm_graphed(
+                    slots, n_loc, 0, 0, mode, float(lr), float(momentum), self.comm.h,
+                    rank_batches.ctypes.data_as(_lib.P_i64), self.comm.velocity.data_ptr(), int(self.agg.cuda_stream),
+                    self.d_iter.data_ptr(), wg, 1), "worker_graphs_capture (comm)")
             cur = torch.cuda.current_stream()
             for wk, ctas in spinning:
                 wk.spin_stream.wait_stream(cur)
@@ -920,6 +929,12 @@ class DistributedTrainer(SimulatedTrainer):
                     rep_ptrs[1], rep_ptrs[2], self.comm.h, rank_batches.ctypes.data_as(_lib.P_i64),
                     int(self.agg.cuda_stream))
                 _lib.check(st, "run_iterations_local_comm")
+            elif iters > 0 and wg is not None:
+                st = _lib.lib().dbs_run_iterations_comm_graphed(
+                    slots, n_loc, 0, iters, mode, float(lr), float(momentum), self.comm.h,
+                    rank_batches.ctypes.data_as(_lib.P_i64), self.comm.velocity.data_ptr(), int(self.agg.cuda_stream),
+                    self.d_iter.data_ptr(), wg, 0)
+                _lib.check(st, "run_iterations_comm_graphed")
             elif iters > 0:
                 st = _lib.lib().dbs_run_iterations_comm(slots, n_loc, 0, iters, mode, float(lr), float(momentum),
                                                         self.comm.h, rank_batches.ctypes.data_as(_lib.P_i64),
@@ -931,6 +946,7 @@ class DistributedTrainer(SimulatedTrainer):
                 self.agg.wait_stream(wk.spin_stream)
             cur.wait_stream(self.agg)
             torch.cuda.synchronize()
+            self._release_retired_graphs()
             ep_wall = max_over_ranks(start.elapsed_time(end) / 1e3, self.group)
             secs = tuple(gather_worker_times(self.seconds.cpu().tolist(), self.group))
             slowest = max(secs)
