@@ -18,6 +18,7 @@ struct Shape {
   cuuint64_t dims[4];
   cuuint32_t box[4];
   int coord_mode;  // 0: 2-D rows walk; 1: 4-D conv walk (tile over h, n); 2: 4-D halo walk (h0-1, w-1)
+  int swz32 = 0;   // 1: CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (the MN-major tf32 operand layout)
 };
 
 template <int kSlots>
@@ -92,6 +93,9 @@ int main(int argc, char** argv) {
       {"4D  {64,32,4,1} conv 16 KB", 4, {64, 32, 32, 128}, {64, 32, 4, 1}, 1},
       {"4D  {64,32,6,1} halo 24 KB", 4, {64, 32, 32, 128}, {64, 32, 6, 1}, 2},
       {"4D  {64,16,8,1} conv 16 KB", 4, {64, 16, 16, 512}, {64, 16, 8, 1}, 1},
+      {"2D  {64 x 32 rows}  4 KB atom32", 2, {64, 131072}, {64, 32}, 0, 1},
+      {"2D  {64 x 128 rows} 16 KB atom32", 2, {64, 131072}, {64, 128}, 0, 1},
+      {"4D  {64,32,4,1} 16 KB atom32", 4, {64, 32, 32, 128}, {64, 32, 4, 1}, 1, 1},
   };
   cudaFuncSetAttribute(tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -110,7 +114,9 @@ int main(int argc, char** argv) {
     }
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sh.rank, buf, sh.dims, strides, sh.box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     sh.swz32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       printf("%s: encode failed %d\n", sh.name, (int)r);
