@@ -475,6 +475,17 @@ int dbs_run_iterations(const dbs_worker_slot* workers, int32_t n, int64_t t0, in
 typedef struct dbs_worker_graphs dbs_worker_graphs;
 int dbs_worker_graphs_create(int32_t n, dbs_worker_graphs** out);
 int dbs_worker_graphs_destroy(dbs_worker_graphs* g);
+/* Device-side epoch loop for workers sharing one context: one CUDA graph whose
+ * `while` conditional node replays the captured iteration (every worker's forward /
+ * backward, the update, *d_iter += 1) while *d_iter < *d_total.  Per epoch: zero
+ * d_iter, set d_total = T >= 1, one dbs_epoch_graph_launch.  A graph is valid for one
+ * plan (batches, spins, model scratch). */
+typedef struct dbs_epoch_graph dbs_epoch_graph;
+int dbs_epoch_graph_create(const dbs_worker_slot* workers, int32_t n, int32_t mode, float lr, float momentum,
+                           float* d_params, float* d_velocity, void* d_params_shadow, int32_t skip_update,
+                           void* agg_stream, int64_t* d_iter, const int64_t* d_total, dbs_epoch_graph** out);
+int dbs_epoch_graph_launch(dbs_epoch_graph* g, int64_t iters, void* stream);
+int dbs_epoch_graph_destroy(dbs_epoch_graph* g);
 /* Capture the graph set (nothing runs); called before the epoch's disturbance spins
  * start (capturing may load kernels, which must not wait behind a spinning kernel). */
 int dbs_worker_graphs_capture(const dbs_worker_slot* workers, int32_t n, int32_t mode, float lr, float momentum,

@@ -143,6 +143,10 @@ SIGNATURES = {
                                                  c_flt, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
     "dbs_run_iterations_comm_graphed": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt,
                                                 c_vp, P_i64, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "dbs_epoch_graph_create": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i32, c_flt, c_flt, c_vp, c_vp, c_vp, c_i32,
+                                       c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    "dbs_epoch_graph_launch": (c_i32, [c_vp, c_i64, c_vp]),
+    "dbs_epoch_graph_destroy": (c_i32, [c_vp]),
     "dbs_worker_graphs_create": (c_i32, [c_i32, ctypes.POINTER(c_vp)]),
     "dbs_worker_graphs_destroy": (c_i32, [c_vp]),
     "dbs_run_iterations_comm": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp,

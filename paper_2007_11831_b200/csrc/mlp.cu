@@ -477,6 +477,97 @@ extern "C" int dbs_run_iterations(const dbs_worker_slot* w, int32_t n, int64_t t
                              agg_stream, d_iter, nullptr, nullptr);
 }
 
+// ---------------------------------------------------------------------------
+// Device-side epoch loop (single-context workers: C1, ResNet on one GPU without
+// partitions): ONE CUDA graph per plan whose `while` conditional node runs the
+// captured iteration (every worker's forward/backward, the update, the iteration
+// counter increment) until *d_iter reaches *d_total -- one graph launch per epoch,
+// no host launch and no inter-graph gap per iteration.
+// ---------------------------------------------------------------------------
+struct dbs_epoch_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long kernels_per_iter = 0;
+};
+
+namespace dbs {
+namespace {
+__global__ void epoch_cond_kernel(cudaGraphConditionalHandle h, const int64_t* __restrict__ d_iter,
+                                  const int64_t* __restrict__ d_total) {
+  cudaGraphSetConditional(h, (*d_iter < *d_total) ? 1u : 0u);
+}
+}  // namespace
+}  // namespace dbs
+
+extern "C" int dbs_epoch_graph_destroy(dbs_epoch_graph* e) {
+  if (!e) return DBS_OK;
+  if (e->exec) cudaGraphExecDestroy(e->exec);
+  if (e->graph) cudaGraphDestroy(e->graph);
+  delete e;
+  return DBS_OK;
+}
+
+extern "C" int dbs_epoch_graph_create(const dbs_worker_slot* w, int32_t n, int32_t mode, float lr, float mom,
+                                      float* d_params, float* d_velocity, void* d_params_shadow,
+                                      int32_t skip_update, void* agg_stream, int64_t* d_iter,
+                                      const int64_t* d_total, dbs_epoch_graph** out) {
+  DBS_REQUIRE(w && n >= 1 && d_iter && d_total && out, DBS_ERR_ARGUMENT, "epoch_graph_create: bad arguments");
+  for (int i = 0; i < n; i++)
+    DBS_REQUIRE(w[i].ctx == nullptr, DBS_ERR_ARGUMENT, "epoch_graph_create: workers must share one context");
+  dbs_epoch_graph* e = new dbs_epoch_graph();
+  cudaStream_t agg = as_stream(agg_stream);
+  const long long c0 = launch_count();
+  int st = [&]() -> int {
+    DBS_CUDA_TRY(cudaGraphCreate(&e->graph, 0));
+    cudaGraphConditionalHandle h;
+    DBS_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, e->graph, 1u, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    DBS_CUDA_TRY(cudaGraphAddNode(&node, e->graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    DBS_CUDA_TRY(cudaStreamBeginCaptureToGraph(agg, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    int st_i = run_iterations_impl(w, n, 0, 1, mode, lr, mom, d_params, d_velocity, d_params_shadow, skip_update,
+                                   agg_stream, d_iter, nullptr, nullptr);
+    if (st_i == DBS_OK) {
+      dbs::epoch_cond_kernel<<<1, 1, 0, agg>>>(h, d_iter, d_total);
+      const cudaError_t e_l = cudaGetLastError();
+      if (e_l != cudaSuccess) {
+        set_error("epoch_graph_create: %s", cudaGetErrorString(e_l));
+        st_i = DBS_ERR_CUDA;
+      }
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t e_end = cudaStreamEndCapture(agg, &captured);
+    if (st_i) return st_i;
+    DBS_CUDA_TRY(e_end);
+    DBS_CUDA_TRY(cudaGraphInstantiate(&e->exec, e->graph, 0));
+    return DBS_OK;
+  }();
+  e->kernels_per_iter = launch_count() - c0;
+  add_launches(-e->kernels_per_iter);  // recorded, not executed
+  if (st) {
+    dbs_epoch_graph_destroy(e);
+    *out = nullptr;
+    return st;
+  }
+  e->kernels_per_iter += 1;  // the condition kernel
+  *out = e;
+  return DBS_OK;
+}
+
+// One epoch: *d_iter must be 0 and *d_total = iters >= 1 (set on `stream` before)
+extern "C" int dbs_epoch_graph_launch(dbs_epoch_graph* e, int64_t iters, void* stream) {
+  DBS_REQUIRE(e && e->exec && iters >= 1, DBS_ERR_ARGUMENT, "epoch_graph_launch: bad arguments");
+  DBS_CUDA_TRY(cudaGraphLaunch(e->exec, as_stream(stream)));
+  add_launches(e->kernels_per_iter * iters);
+  count_host_launch();
+  return DBS_OK;
+}
+
 // Capture (and instantiate) the per-worker graphs without running anything: done
 // before an epoch's disturbance kernels start, since capturing may load kernels
 // lazily and a module load would wait behind a spin kernel that owns SMs.

@@ -238,6 +238,11 @@ class SimulatedTrainer:
             self.worker_graphs = False
         self._wg_cache = {}
         self._wg_retired = []
+        # shared-context workers: the device-side epoch loop (a `while` conditional graph)
+        self.epoch_graphs = os.environ.get("DBS_EPOCH_GRAPH", "1") != "0"
+        self._eg_cache = {}
+        self._eg_retired = []
+        self.d_total = torch.zeros(1, dtype=torch.int64, device=self.dev)
         # SM-pinning disturbance only when each worker owns its SMs (one GPU per
         # worker, or green-context partitions); otherwise the proportional slow-down
         self.pin_sms = (n_workers == 1 or partition) if pin_sms is None else bool(pin_sms)
@@ -416,6 +421,32 @@ class SimulatedTrainer:
         """After a device-wide sync: the evicted graph sets are no longer in flight."""
         while self._wg_retired:
             _lib.lib().dbs_worker_graphs_destroy(self._wg_retired.pop())
+        while self._eg_retired:
+            _lib.lib().dbs_epoch_graph_destroy(self._eg_retired.pop())
+
+    def _epoch_graph(self, key, slots, mode, lr, mom, skip):
+        """The device-side epoch loop of a plan (dbs_epoch_graph_create: the iteration
+        captured once into a `while` conditional node), or None when the driver cannot
+        build one (the iteration graphs below are used instead)."""
+        hit = self._eg_cache.pop(key, None)
+        if hit is None:
+            h = ctypes.c_void_p()
+            st = _lib.lib().dbs_epoch_graph_create(slots, self.n, mode, float(lr), float(mom),
+                                                   self.model.params.data_ptr(), self.model.velocity.data_ptr(),
+                                                   self.model.params_op.data_ptr(), int(skip),
+                                                   int(self.agg.cuda_stream), self.d_iter.data_ptr(),
+                                                   self.d_total.data_ptr(), ctypes.byref(h))
+            if st != 0:
+                import warnings
+
+                warnings.warn(f"device-side epoch loop unavailable ({_lib.last_error()}); using iteration graphs")
+                self.epoch_graphs = False
+                return None
+            hit = h
+        self._eg_cache[key] = hit
+        while len(self._eg_cache) > 8:
+            self._eg_retired.append(self._eg_cache.pop(next(iter(self._eg_cache))))
+        return hit
 
     # -- the epoch loop -----------------------------------------------------------
     def run(self, config: StrategyConfig, n_epochs: int, lr: float = 0.05, momentum: float = 0.5,
@@ -596,9 +627,16 @@ class SimulatedTrainer:
                     self._rep_ptrs[1], self._rep_ptrs[2], int(self.agg.cuda_stream), self._local_iters.data_ptr(),
                     wg, 1), "worker_graphs_capture (local)")
             graph = graph_r = None
+            egraph = None
             per_replay = per_r = 0
             k_it = 1
-            if self.graphs and iters > 0 and not local:
+            if self.graphs and iters > 0 and not local and self.epoch_graphs:
+                key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
+                       bool(record_loss))
+                egraph = self._epoch_graph(key, slots, mode, lr, momentum, skip_update)
+                if egraph is not None:
+                    self.d_total.fill_(iters)  # the loop's trip count (d_iter is 0)
+            if self.graphs and iters > 0 and not local and egraph is None:
                 key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
                        bool(record_loss))
                 # a plan seen before gets k-iteration graphs; a new one (DBS re-plans move
@@ -624,7 +662,11 @@ class SimulatedTrainer:
             end = torch.cuda.Event(enable_timing=True)
             start.record(self.agg)
             if iters > 0:
-                if graph is not None:
+                if egraph is not None:
+                    _lib.check(_lib.lib().dbs_epoch_graph_launch(egraph, iters, int(self.agg.cuda_stream)),
+                               "epoch_graph_launch")
+                    replays = 0  # counted by the library
+                elif graph is not None:
                     with torch.cuda.stream(self.agg):
                         for _ in range(iters // k_it):
                             graph.replay()
