@@ -398,6 +398,8 @@ int dbs_dev_conv2d_wgrad(const void* d_dy, const void* d_x, int32_t N, int32_t H
                          int32_t Cout, int32_t k, int32_t stride, int32_t pad, float* d_dw, void* stream);
 /* fp32-class forms: S32 operands (NHWC activations, [Cout][k][k][Cin] weights,
  * channels multiples of 32), fp32 outputs (y, dx; dw accumulated atomically) */
+/* *d_iter += 1 on the stream (the device iteration counter of graph-replayed loops). */
+int dbs_dev_iter_increment(int64_t* d_iter, void* stream);
 /* Stand-alone fp32-class BatchNorm passes (the network's own kernels; unit tests and
  * per-kernel rooflines).  acc = [sum C | sum of squares C] (fp64) of y [M][C] fp32;
  * out / dy / mask in the S32 operand format.  Forward: out = act(gamma yhat + beta),

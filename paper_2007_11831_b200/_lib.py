@@ -132,6 +132,7 @@ SIGNATURES = {
                                        c_vp, c_vp, c_i32, c_vp]),
     "dbs_run_iterations": (c_i32, [ctypes.POINTER(WorkerSlot), c_i32, c_i64, c_i64, c_i32, c_flt, c_flt, c_vp, c_vp,
                                    c_vp, c_i32, c_vp, c_vp]),
+    "dbs_dev_iter_increment": (c_i32, [c_vp, c_vp]),
     "dbs_dev_bn_apply_s32": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "dbs_dev_bn_backward_s32": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp,
                                         c_vp]),

@@ -421,6 +421,9 @@ int64_t slot_row_bytes(const dbs_worker_slot& w) {
   return resnet_row_bytes(static_cast<const dbs_resnet*>(w.model));
 }
 int iter_increment(int64_t* d_iter, cudaStream_t s);
+int aggregate_sgd_f32_iter(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                           float step, float mom, float* d_x, float* d_v, void* d_shadow, int32_t shadow_prec,
+                           void* stream, int64_t* d_iter);
 }  // namespace dbs
 
 extern "C" int dbs_dev_aggregate_f32(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode, int64_t P,
@@ -764,10 +767,12 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
       if (st_pop) return st_pop;
     }
     for (int i = 0; i < n; i++) DBS_CUDA_TRY(cudaStreamWaitEvent(agg, ev[i], 0));
+    bool iter_done = false;  // the update kernel advanced d_iter itself
     if (!skip_update && comm == nullptr) {
-      st = dbs_dev_aggregate_sgd_f32_ex(grads, batches, n, mode, P, lr, mom, d_params, d_velocity, d_shadow, prec,
-                                        agg_stream);
+      st = aggregate_sgd_f32_iter(grads, batches, n, mode, P, lr, mom, d_params, d_velocity, d_shadow, prec,
+                                  agg_stream, d_iter);
       if (st) return st;
+      iter_done = d_iter != nullptr;
     } else if (!skip_update) {
       float* cg = nullptr;
       st = dbs_comm_buffers(comm, &cg, nullptr, nullptr);
@@ -783,7 +788,7 @@ static int run_iterations_impl(const dbs_worker_slot* w, int32_t n, int64_t t0, 
         if (st) return st;
       }
     }
-    if (d_iter) {
+    if (d_iter && !iter_done) {
       st = iter_increment(d_iter, agg);
       if (st) return st;
     }
@@ -912,13 +917,9 @@ static int run_iterations_local(const dbs_worker_slot* w, int32_t n, int64_t t0,
         // the worker's own momentum-SGD step on its replica
         const float* g = w[i].grad;
         const int64_t one = 1;
-        st = dbs_dev_aggregate_sgd_f32_ex(&g, &one, 1, DBS_AGG_UNIFORM, P, lr, mom, d_params[i], d_velocity[i],
-                                          d_shadows[i], prec, s);
+        st = aggregate_sgd_f32_iter(&g, &one, 1, DBS_AGG_UNIFORM, P, lr, mom, d_params[i], d_velocity[i],
+                                    d_shadows[i], prec, s, dev ? d_iters + i : nullptr);
         if (st) return st;
-        if (dev) {
-          st = iter_increment(d_iters + i, s);
-          if (st) return st;
-        }
         return DBS_OK;
   };
   if (graphs) {

@@ -2119,6 +2119,11 @@ int iter_increment(int64_t* d_iter, cudaStream_t s) {
 
 }  // namespace dbs
 
+extern "C" int dbs_dev_iter_increment(int64_t* d_iter, void* stream) {
+  DBS_REQUIRE(d_iter, DBS_ERR_ARGUMENT, "iter_increment: null counter");
+  return iter_increment(d_iter, as_stream(stream));
+}
+
 extern "C" int dbs_resnet_create_ex2(int32_t depth, int32_t image, int64_t max_batch, int32_t classes,
                                      int32_t precision, dbs_resnet** out) {
   DBS_REQUIRE(out && max_batch > 0, DBS_ERR_ARGUMENT, "resnet_create: need max_batch > 0");

@@ -113,7 +113,11 @@ __device__ __forceinline__ void store_shadow(void* sh, int64_t p, const float4 x
 template <int PREC>
 __global__ void __launch_bounds__(256) aggregate_sgd_f32_kernel(AggArgs a, int64_t P4, float step, float mom,
                                                                 float4* __restrict__ x, float4* __restrict__ v,
-                                                                void* __restrict__ xb) {
+                                                                void* __restrict__ xb, int64_t* __restrict__ d_iter) {
+  // the iteration counter of device-indexed iterations: every reader of this
+  // iteration has finished before this kernel starts, the next iteration's start after
+  // it ends (one kernel less per iteration than a separate increment)
+  if (d_iter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *d_iter += 1;
   // weights straight from the parameter bank (no local-memory array)
 #define W(i) ((a.mode == DBS_AGG_BATCH_WEIGHTED) ? (float)a.w[i] : 1.0f / (float)a.n)
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P4; p += (int64_t)gridDim.x * blockDim.x) {
@@ -231,9 +235,23 @@ extern "C" int dbs_dev_aggregate_sgd_f64(const double* const* d_grads, const int
   return DBS_OK;
 }
 
+namespace dbs {
+int aggregate_sgd_f32_iter(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                           float step, float mom, float* d_x, float* d_v, void* d_shadow, int32_t shadow_prec,
+                           void* stream, int64_t* d_iter);
+}
+
 extern "C" int dbs_dev_aggregate_sgd_f32_ex(const float* const* d_grads, const int64_t* b, int64_t n,
                                             int32_t mode, int64_t P, float step, float mom, float* d_x,
                                             float* d_v, void* d_shadow, int32_t shadow_prec, void* stream) {
+  return dbs::aggregate_sgd_f32_iter(d_grads, b, n, mode, P, step, mom, d_x, d_v, d_shadow, shadow_prec, stream,
+                                     nullptr);
+}
+
+// the same, also advancing the device iteration counter d_iter (when not null)
+int dbs::aggregate_sgd_f32_iter(const float* const* d_grads, const int64_t* b, int64_t n, int32_t mode, int64_t P,
+                                float step, float mom, float* d_x, float* d_v, void* d_shadow, int32_t shadow_prec,
+                                void* stream, int64_t* d_iter) {
   AggArgs a;
   int st = make_args(a, (const void* const*)d_grads, b, n, mode);
   if (st) return st;
@@ -246,10 +264,10 @@ extern "C" int dbs_dev_aggregate_sgd_f32_ex(const float* const* d_grads, const i
   const int64_t P4 = P / 4;
   if (shadow_prec == DBS_PREC_F32)
     aggregate_sgd_f32_kernel<DBS_PREC_F32><<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
-        a, P4, step, mom, (float4*)d_x, (float4*)d_v, d_shadow);
+        a, P4, step, mom, (float4*)d_x, (float4*)d_v, d_shadow, d_iter);
   else
     aggregate_sgd_f32_kernel<DBS_PREC_BF16><<<grid_for(P4, 256), 256, 0, as_stream(stream)>>>(
-        a, P4, step, mom, (float4*)d_x, (float4*)d_v, d_shadow);
+        a, P4, step, mom, (float4*)d_x, (float4*)d_v, d_shadow, d_iter);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }

@@ -374,6 +374,9 @@ class SimulatedTrainer:
         # MLP row staging) must be loaded too
         self._run_iters(slots, 0, 1, mode, 0.0, 0.0, p, v, pb, 0,
                         it_scratch if (self.graphs or self.worker_graphs) else None)
+        # (the update kernel advances the counter itself; the stand-alone increment other
+        # paths launch -- multi-GPU, skip_update -- is loaded here too)
+        _lib.check(_lib.lib().dbs_dev_iter_increment(it_scratch.data_ptr(), _lib.stream_handle()), "iter_increment")
         for w in range(self.n):
             slots[w].loss, slots[w].stamps, slots[w].seconds = saved[w]
         torch.cuda.synchronize()
@@ -630,9 +633,13 @@ class SimulatedTrainer:
             egraph = None
             per_replay = per_r = 0
             k_it = 1
-            if self.graphs and iters > 0 and not local and self.epoch_graphs:
-                key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
-                       bool(record_loss))
+            key = (tuple(batches), tuple(spin_key), mode, float(lr), float(momentum), bool(skip_update),
+                   bool(record_loss))
+            if (self.graphs and iters > 0 and not local and self.epoch_graphs and
+                    ((key, 1) in self._graph_cache or key in self._eg_cache)):
+                # a plan seen before: the device-side epoch loop (building one -- capture plus
+                # instantiation of the conditional graph -- is not worth it for a plan that
+                # may live one epoch, as DBS re-plans by a sample or two)
                 egraph = self._epoch_graph(key, slots, mode, lr, momentum, skip_update)
                 if egraph is not None:
                     self.d_total.fill_(iters)  # the loop's trip count (d_iter is 0)
