@@ -923,18 +923,32 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
       }
     }
     const uint32_t a_bytes = am >= 5 ? (uint32_t)a_groups * 8192u : C::kABytes;
+    // transposed weight gradient, K-paired (p.pair_a == 5): each box covers the k-block pair
+    // (i, i + 1) = 64 pixels, landing in ring slots s, s + 1 as per group [hi 64 rows | lo 64
+    // rows] (A) and [hi groups | lo groups] of 64 rows (B) -- half the TMA operations of the
+    // producer-bound 64-channel weight gradient; the MMA issuer addresses the pair layout
+    const bool kp5 = am == 5 && p.pair_a == 5;
     for (int i = 0; i < num_k; i++, it++) {
       const int L = kb_begin + i;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
       if (it < 12) GEMM_TRACE(100 + it);
-      mbar_arrive_expect_tx(&full[s], a_bytes + C::kBBytes);
+      if (kp5 && (i & 1)) {
+        mbar_arrive(&full[s]);  // its bytes completed on slot s - 1's barrier
+        if (k_pix) pc.advance(gk);
+        continue;
+      }
+      if (kp5) mbar_wait(&empty[s + 1], (((it + 1) / kStages) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], (a_bytes + C::kBBytes) * (kp5 ? 2u : 1u));
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
       if (am >= 5) {
         const ConvGeom& g = p.ga;
         for (int gq = 0; gq < a_groups; gq++) {
-          if (am == 6) {
+          if (kp5) {
+            tma_load_5d(a + gq * 16384, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
+                        pc.oh * g.stride + at_r[gq] - g.pad, pc.n, 2 * (at_c[gq] / 32));
+          } else if (am == 6) {
             const int cu = at_c[gq] * 4;
             tma_load_im2col_4d(a + gq * 8192, tmA, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
                                pc.n, (uint16_t)at_s[gq], (uint16_t)at_r[gq]);
@@ -1282,13 +1296,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // adjacent (group stride LBO = 8 KB), SWIZZLE_128B_BASE32B (4-row K groups 512 B apart)
     // A: MN-major groups [hi | lo] per 32 columns (group stride 8 KB); B: [all hi | all lo]
     // (MN-major groups 4 KB apart), so B_hi:B_lo is ONE N = 2 BN operand
-    const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), 8192, 512, 1) : make_sdesc(smem_u32(sA), 16, 1024);
+    // (K-paired transposed weight gradient: 64-row groups, group strides doubled, lo planes
+    // 8 KB after hi, the odd k-block of a pair 32 rows (4 KB) into the pair's groups)
+    const bool kp5 = p.a_mode == 5 && p.pair_a == 5;
+    const uint64_t a_desc0 = a_mn ? make_sdesc(smem_u32(sA), kp5 ? 16384 : 8192, 512, 1)
+                                  : make_sdesc(smem_u32(sA), 16, 1024);
     // (B mode 2, the 4-D-box weight-gradient operand, keeps [hi | lo] per group: 3 MMAs per k-step)
     const bool b_pairs = p.b_mode == 2;
-    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), b_pairs ? 8192 : 4096, 512, 1)
+    const uint64_t b_desc0 = b_mn ? make_sdesc(smem_u32(sB), (b_pairs || kp5) ? 8192 : 4096, 512, 1)
                                   : make_sdesc(smem_u32(sB), 16, 1024);
     const uint32_t b_lo = b_pairs ? 4096u >> 4 : 0u;
-    const uint32_t a_lo = a_mn ? 4096u >> 4 : (uint32_t)(kBM * 128) >> 4;  // lo half offset, 16-byte units
+    const uint32_t a_lo = a_mn ? (kp5 ? 8192u : 4096u) >> 4 : (uint32_t)(kBM * 128) >> 4;  // lo half, 16-byte units
     const uint32_t a_kstep = a_mn ? 64u : 2u, b_kstep = b_mn ? 64u : 2u;  // UMMA_K = 8: 8 K rows / 32 B
     const uint32_t idesc2 = make_idesc_tf32(kBM, 2 * BN, a_mn, b_mn);  // A_hi x [B_hi | B_lo]
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -1307,7 +1325,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it < 12) GEMM_TRACE(112 + it);
         tc_fence_after();
         const uint32_t d_main = d_buf + (i % kMains) * CT::kPairCols;  // [main | correction] pair
-        const uint64_t a_hi = a_desc0 + (uint64_t)((s * kSlotA) >> 4), b_hi = b_desc0 + (uint64_t)((s * kSlotB) >> 4);
+        const uint32_t a_off = kp5 ? (uint32_t)((s & ~1) * kSlotA + (s & 1) * 4096) : (uint32_t)(s * kSlotA);
+        const uint32_t b_off = kp5 ? (uint32_t)((s & ~1) * kSlotB + (s & 1) * 4096) : (uint32_t)(s * kSlotB);
+        const uint64_t a_hi = a_desc0 + (uint64_t)(a_off >> 4), b_hi = b_desc0 + (uint64_t)(b_off >> 4);
         if (!b_pairs) {
 #pragma unroll
           for (int k = 0; k < 4; k++) {
@@ -1972,14 +1992,14 @@ int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, 
 // per group [hi 32 rows x 128 B | lo 32 rows x 128 B] (SWIZZLE_128B_ATOM_32B)
 // (hilo_outer: {64 units, K rows, groups, hi/lo} -> [all hi groups | all lo groups], the B form)
 int make_tmap_s32_mn(CUtensorMap* tm, const void* base, uint64_t mn, uint64_t krows, uint64_t ld, uint32_t groups,
-                     bool hilo_outer = false) {
+                     bool hilo_outer = false, uint32_t box_k = 32) {
   EncodeTiledFn fn = encode_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && ld % 32 == 0 && groups >= 1 && groups <= 8, DBS_ERR_ARGUMENT,
               "S32 MN-major view: aligned base, ld %% 32 == 0");
   cuuint64_t dims[4] = {64, krows, 2, (mn + 31) / 32};
   cuuint64_t strides[3] = {ld * 8, 128, 256};
-  cuuint32_t box[4] = {64, 32, 2, groups};
+  cuuint32_t box[4] = {64, box_k, 2, groups};
   if (hilo_outer) {
     dims[2] = (mn + 31) / 32;
     dims[3] = 2;
@@ -2412,10 +2432,15 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
       st = make_tmap_im2col(&ta, c.a, t4, -c.ga.pad, c.ga.pad - (c.ga.R - 1), 32, c.ga.stride, kMnSwz);
       p.a_mode = 6;
     } else {
+      // K-paired (64-pixel boxes) when the tile and ring allow it: BN = 64 (4 ring stages),
+      // an even k-block count, 64-pixel windows that are whole rows
+      const bool kp5 = kpair_enabled() && bn == 64 && CfgTf<64>::kStages % 2 == 0 && ((c.K + 31) / 32) % 2 == 0 &&
+                       pixel_box_fits(c.ga.OH, c.ga.OW, 64) && c.b_mode == 1;
       int bw, bh, bnn;
-      st = pixel_box(c.ga.OH, c.ga.OW, 32, bw, bh, bnn);
+      st = pixel_box(c.ga.OH, c.ga.OW, kp5 ? 64 : 32, bw, bh, bnn);
       if (st) return st;
       st = make_tmap_nhwc_pair(&ta, c.a, t4, bw, bh, bnn, c.ga.stride, kMnSwz);
+      p.pair_a = kp5 ? 5 : 0;
     }
   } else if (c.a_mode == 1) {
     DBS_REQUIRE(c.lda % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: lda %% 32");
@@ -2458,7 +2483,8 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
     st = DBS_OK;
   } else if (c.b_mode == 1) {
     DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
-    st = make_tmap_s32_mn(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, (uint32_t)(bn / 32), true);
+    st = make_tmap_s32_mn(&tb, c.b, (uint64_t)c.N, (uint64_t)c.K, (uint64_t)c.ldb, (uint32_t)(bn / 32), true,
+                          p.pair_a == 5 ? 64u : 32u);
   } else {
     DBS_REQUIRE(c.ldb % 32 == 0, DBS_ERR_ARGUMENT, "conv_gemm_tf: ldb %% 32");
     st = make_tmap_kpair(&tb, c.b, (uint64_t)(4 * ceil32(c.K)), (uint64_t)c.N, (uint64_t)(4 * c.ldb), (uint32_t)bn);
@@ -2468,6 +2494,7 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
   int splits = c.splits > 0 ? c.splits : 1;
   if (splits > num_l) splits = num_l;
   p.kb_per_split = (num_l + splits - 1) / splits;
+  if (p.pair_a == 5 && (p.kb_per_split & 1)) p.kb_per_split++;  // K pairs never straddle split-K slices
   splits = (num_l + p.kb_per_split - 1) / p.kb_per_split;
   DBS_REQUIRE(splits == 1 || c.epi == DBS_EPI_F32_ATOMIC, DBS_ERR_ARGUMENT, "split-K needs the atomic epilogue");
   return dispatch(ta, tb, p, bn, splits, s, false, true);
