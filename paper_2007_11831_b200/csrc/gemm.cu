@@ -1011,6 +1011,12 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
                                pc.n, (uint16_t)b_s, (uint16_t)b_r);
             tma_load_im2col_4d(b + kLoB + j * 4096, tmB, &full[s], cu + 64, pc.ow * g.stride - g.pad,
                                pc.oh * g.stride - g.pad, pc.n, (uint16_t)b_s, (uint16_t)b_r);
+          } else if (p.pair_b == 2) {
+            // all BN / 32 groups of the tile (one tap, consecutive channels) in ONE box
+            // {64, 32 pixels, 2 x BN / 32 sub-blocks}: [hi g | lo g] per group as below
+            if (j == 0)
+              tma_load_5d(b, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad, pc.oh * g.stride + b_r - g.pad, pc.n,
+                          2 * (b_c0 / 32));
           } else {
             // one {64, 32 pixels, hi/lo} box per group: [hi g | lo g] pairs (group stride 8 KB),
             // the un-fused layout (3 MMAs per k-step, see the issuer) -- half the TMA operations
@@ -1971,14 +1977,15 @@ int make_tmap_kpair(CUtensorMap* tm, const void* base, uint64_t K, uint64_t rows
 // NHWC activation viewed as {64 c, W, H, N, C / 64 channel blocks}: one box of
 // {64, bw, bh, bn, 2} fills two consecutive ring slots (two channel blocks of one tap)
 int make_tmap_nhwc_pair(CUtensorMap* tm, const void* base, const ConvTensor& t, int bw, int bh, int bn, int stride,
-                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, int subblocks = 2) {
   EncodeTiledFn fn = encode_fn();
   DBS_REQUIRE(fn != nullptr, DBS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   DBS_REQUIRE(((uintptr_t)base & 15) == 0 && t.C % 128 == 0, DBS_ERR_ARGUMENT,
               "conv pair TMA: aligned base and C %% 128 == 0 required");
   cuuint64_t dims[5] = {64, (cuuint64_t)t.W, (cuuint64_t)t.H, (cuuint64_t)t.N, (cuuint64_t)t.C / 64};
   cuuint64_t strides[4] = {(cuuint64_t)t.C * 2, (cuuint64_t)t.W * t.C * 2, (cuuint64_t)t.H * t.W * t.C * 2, 128};
-  cuuint32_t box[5] = {64, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn, 2};
+  cuuint32_t box[5] = {64, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn,
+                       (cuuint32_t)subblocks};
   cuuint32_t es[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -2462,7 +2469,14 @@ int conv_gemm_tf(const ConvCall& c, cudaStream_t s) {
       int bw, bh, bnn;
       st = pixel_box(c.gb.OH, c.gb.OW, 32, bw, bh, bnn);
       if (st) return st;
-      st = make_tmap_nhwc_pair(&tb, c.b, t4, bw, bh, bnn, c.gb.stride, kMnSwz);  // {64, 32 pixels, hi/lo}
+      // one box for all BN / 32 channel groups of a tile (DBS_WGRAD_MERGE=0: one per group)
+      static const bool merge = [] {
+        const char* e = getenv("DBS_WGRAD_MERGE");
+        return !(e && e[0] == '0');
+      }();
+      p.pair_b = (merge && bn / 32 >= 2) ? 2 : 0;
+      st = make_tmap_nhwc_pair(&tb, c.b, t4, bw, bh, bnn, c.gb.stride, kMnSwz,
+                               p.pair_b == 2 ? 2 * (bn / 32) : 2);  // {64, 32 pixels, hi/lo (x groups)}
     }
   } else if (c.b_mode == 3) {
     // filter [Cout][R*S][Cin] S32 read as the flipped, transposed filter: the MN-major
