@@ -323,3 +323,19 @@ def test_bn_passes_s32_vs_fp64(dev, M, C):
     assert _rel(got_dy, yd.grad) <= 1e-5
     assert _rel(dgamma, gd.grad) <= 1e-5 and _rel(dbeta, bd.grad) <= 1e-5
     assert torch.equal(gout, torch.where(got > 0, g, torch.zeros_like(g)))
+
+
+def test_conv_s32_unmerged_wgrad_boxes(dev):
+    """The weight gradient with one TMA box per channel group (DBS_WGRAD_MERGE=0; read once
+    per process: run in a child) on the 128+-channel shapes, same 5e-6 bound."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBS_WGRAD_MERGE="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", str(Path(__file__).resolve()),
+                        "-k", "conv_s32_fwd_dgrad_wgrad and (128-128 or 256-256 or 512-512)"],
+                       env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
