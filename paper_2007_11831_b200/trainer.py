@@ -957,7 +957,8 @@ class DistributedTrainer(SimulatedTrainer):
             if self.worker_graphs and iters > 0 and not local:
                 # this plan's per-worker graphs, captured before any spin starts
                 self.d_iter.zero_()
-                wg = self._worker_graphs(("comm", tuple(batches), tuple((w, slots[w].spin_ns) for w in range(n_loc))))
+                wg = self._worker_graphs(("comm", tuple(batches), tuple((w, slots[w].spin_ns) for w in range(n_loc)),
+                                          bool(record_loss)))
                 _lib.check(_lib.lib().dbs_run_iterations_comm_graphed(
                     slots, n_loc, 0, 0, mode, float(lr), float(momentum), self.comm.h,
                     rank_batches.ctypes.data_as(_lib.P_i64), self.comm.velocity.data_ptr(), int(self.agg.cuda_stream),
