@@ -6,9 +6,9 @@
 // is repacked contiguously in HBM so every iteration reads a dense slice.
 //
 // Algorithmic bytes per row: 2 * row_bytes (+ 8 B of index).  Mapping: one warp
-// per row (several rows per CTA, grid-stride over rows), 16-byte vector loads
-// and stores with 4 independent requests in flight per lane; rows that are not
-// 16-byte aligned fall back to 4-byte or byte copies.
+// per row (several rows per CTA, grid-stride over rows), 32-byte vector loads
+// and stores (LDG/STG.256) with 4 independent requests in flight per lane; rows
+// that are not 32-byte aligned fall back to 16-byte, 4-byte or byte copies.
 #include "common.cuh"
 
 namespace dbs {
@@ -16,6 +16,13 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kUnroll = 4;
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) { return __ldcs(p); }
+__device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+__device__ __forceinline__ V8 ld_stream(const V8* p) { return ldg8_cs(p); }
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(int* p, const int& v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(V8* p, const V8& v) { stg8_cs(p, v); }
 
 template <typename V>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -31,11 +38,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     for (; c + 32 * (kUnroll - 1) < vec_per_row; c += 32 * kUnroll) {
       V v[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) v[u] = __ldcs(s + c + 32 * u);
+      for (int u = 0; u < kUnroll; u++) v[u] = ld_stream(s + c + 32 * u);
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) __stcs(d + c + 32 * u, v[u]);
+      for (int u = 0; u < kUnroll; u++) st_stream(d + c + 32 * u, v[u]);
     }
-    for (; c < vec_per_row; c += 32) __stcs(d + c, __ldcs(s + c));
+    for (; c < vec_per_row; c += 32) st_stream(d + c, ld_stream(s + c));
   }
 }
 
@@ -132,7 +139,10 @@ extern "C" int dbs_dev_gather_rows(const void* d_src, const int64_t* d_idx, int6
   cudaStream_t s = as_stream(stream);
   const int grid = grid_for_rows(rows);
   const uintptr_t align = (uintptr_t)d_src | (uintptr_t)d_dst;
-  if (row_bytes % 16 == 0 && align % 16 == 0) {
+  if (row_bytes % 32 == 0 && align % 32 == 0) {
+    gather_rows_kernel<V8><<<grid, kWarpsPerBlock * 32, 0, s>>>((const V8*)d_src, d_idx, rows, row_bytes / 32,
+                                                                (V8*)d_dst);
+  } else if (row_bytes % 16 == 0 && align % 16 == 0) {
     gather_rows_kernel<int4><<<grid, kWarpsPerBlock * 32, 0, s>>>(
         (const int4*)d_src, d_idx, rows, row_bytes / 16, (int4*)d_dst);
   } else if (row_bytes % 4 == 0 && align % 4 == 0) {

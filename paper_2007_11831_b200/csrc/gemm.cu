@@ -117,15 +117,15 @@ __device__ __forceinline__ float tf32_rn(float x) {
 // 32 consecutive logical values -> one S32 block (256 contiguous bytes at `blk`)
 __device__ __forceinline__ void store_s32x32(float* blk, const float (&x)[32]) {
 #pragma unroll
-  for (int j = 0; j < 32; j += 4) {
-    float h[4], l[4];
+  for (int j = 0; j < 32; j += 8) {
+    float h[8], l[8];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < 8; u++) {
       h[u] = tf32_rn(x[j + u]);
       l[u] = tf32_rn(x[j + u] - h[u]);
     }
-    *reinterpret_cast<float4*>(blk + j) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(blk + 32 + j) = make_float4(l[0], l[1], l[2], l[3]);
+    stg8(blk + j, v8_of(h));  // 256-bit stores (the block is 256-byte aligned)
+    stg8(blk + 32 + j, v8_of(l));
   }
 }
 __device__ __forceinline__ bool is_s32_epi(int epi) {
@@ -347,6 +347,14 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int64_t row,
 #pragma unroll
       for (int j = 0; j < 32; j += 4)
         atomicAdd(reinterpret_cast<float4*>(d + j), make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]));
+    } else if (((reinterpret_cast<uintptr_t>(d)) & 31) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float o[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) o[u] = x[j + u];
+        stg8(d + j, v8_of(o));
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);

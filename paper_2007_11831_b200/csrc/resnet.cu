@@ -660,31 +660,28 @@ __device__ __forceinline__ float rn_tf32(float x) {
 }
 __device__ __forceinline__ int64_t s32_off(int64_t e) { return 2 * (e & ~int64_t(31)) + (e & 31); }
 // elements 8 i .. 8 i + 7
-__device__ __forceinline__ void ld8_f32(const float* p, int64_t i, float (&v)[8]) {
-  const float4 a = reinterpret_cast<const float4*>(p)[2 * i], b = reinterpret_cast<const float4*>(p)[2 * i + 1];
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+// 256-bit global accesses (LDG/STG.256, sm_100): one instruction per 8 floats
+__device__ __forceinline__ void ldg8f(const float* q, float (&v)[8]) {
+  asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(q));
 }
-__device__ __forceinline__ void st8_f32(float* p, int64_t i, const float (&v)[8]) {
-  reinterpret_cast<float4*>(p)[2 * i] = make_float4(v[0], v[1], v[2], v[3]);
-  reinterpret_cast<float4*>(p)[2 * i + 1] = make_float4(v[4], v[5], v[6], v[7]);
+__device__ __forceinline__ void stg8f(float* q, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
 }
+__device__ __forceinline__ void ld8_f32(const float* p, int64_t i, float (&v)[8]) { ldg8f(p + 8 * i, v); }
+__device__ __forceinline__ void st8_f32(float* p, int64_t i, const float (&v)[8]) { stg8f(p + 8 * i, v); }
 __device__ __forceinline__ void ld8_s32(const float* p, int64_t i, float (&v)[8]) {
   const float* q = p + s32_off(8 * i);
-  const float4 h0 = *reinterpret_cast<const float4*>(q), h1 = *reinterpret_cast<const float4*>(q + 4);
-  const float4 l0 = *reinterpret_cast<const float4*>(q + 32), l1 = *reinterpret_cast<const float4*>(q + 36);
-  v[0] = h0.x + l0.x; v[1] = h0.y + l0.y; v[2] = h0.z + l0.z; v[3] = h0.w + l0.w;
-  v[4] = h1.x + l1.x; v[5] = h1.y + l1.y; v[6] = h1.z + l1.z; v[7] = h1.w + l1.w;
+  float l[8];
+  ldg8f(q, v);
+  ldg8f(q + 32, l);
+#pragma unroll
+  for (int k = 0; k < 8; k++) v[k] += l[k];
 }
-// the ReLU mask of an S32 activation from its hi plane only (half the bytes): for a
-// finite v, hi = rn_tf32(v) > 0 exactly when v > 0, except positive subnormals below
-// 2^-137 (hi rounds to 0) -- a ReLU output that small is not distinguishable from 0
-// at the fp32 tolerance this path is held to
-__device__ __forceinline__ void ld8_s32_hi(const float* p, int64_t i, float (&v)[8]) {
-  const float* q = p + s32_off(8 * i);
-  const float4 h0 = *reinterpret_cast<const float4*>(q), h1 = *reinterpret_cast<const float4*>(q + 4);
-  v[0] = h0.x; v[1] = h0.y; v[2] = h0.z; v[3] = h0.w;
-  v[4] = h1.x; v[5] = h1.y; v[6] = h1.z; v[7] = h1.w;
-}
+__device__ __forceinline__ void ld8_s32_hi(const float* p, int64_t i, float (&v)[8]) { ldg8f(p + s32_off(8 * i), v); }
 __device__ __forceinline__ void st8_s32(float* p, int64_t i, const float (&v)[8]) {
   float* q = p + s32_off(8 * i);
   float h[8], l[8];
@@ -693,10 +690,8 @@ __device__ __forceinline__ void st8_s32(float* p, int64_t i, const float (&v)[8]
     h[k] = rn_tf32(v[k]);
     l[k] = rn_tf32(v[k] - h[k]);
   }
-  *reinterpret_cast<float4*>(q) = make_float4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<float4*>(q + 4) = make_float4(h[4], h[5], h[6], h[7]);
-  *reinterpret_cast<float4*>(q + 32) = make_float4(l[0], l[1], l[2], l[3]);
-  *reinterpret_cast<float4*>(q + 36) = make_float4(l[4], l[5], l[6], l[7]);
+  stg8f(q, h);
+  stg8f(q + 32, l);
 }
 __device__ __forceinline__ void st1_s32(float* p, int64_t e, float v) {
   const float h = rn_tf32(v);
