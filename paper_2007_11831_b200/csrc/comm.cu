@@ -198,6 +198,84 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(PeerTable T, int rank, 
   }
 }
 
+// peer memory, fetched again (.cv), 256 bits per load
+__device__ __forceinline__ V8 ldg8_cv(const void* p) {
+  V8 r;
+  asm volatile("ld.global.cv.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]),
+                 "=r"(r.v[7])
+               : "l"(p));
+  return r;
+}
+
+// The same exchange over 8 floats per thread and trip with 256-bit loads / stores
+// (LDG/STG.256: twice the bytes in flight per request of the float4 form; the shards
+// are whole 32-element blocks, so every unit is 32-byte aligned)
+template <int MODE, bool BF16>
+__global__ void __launch_bounds__(kThreads) fused8_kernel(PeerTable T, int rank, int world, int64_t shard8, float lr,
+                                                          float mom, float* __restrict__ vel, uint32_t gen) {
+  uint32_t* my_sig = T.signal[rank];
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int j = 0; j < world; j++) st_release_sys(T.signal[j] + rank, gen);
+    wait_flags(my_sig, world, gen, my_sig + 48);
+  }
+  __syncthreads();
+  const int64_t base8 = (int64_t)rank * shard8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < shard8; i += stride) {
+    const int64_t p8 = base8 + i;
+    V8 g[kMaxRanks];
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; j++) {
+      if (j >= world) break;
+      // every peer's load before any use; this rank's own buffer was written by this GPU
+      // (earlier kernels), so a plain streaming load suffices there
+      const float* src = (MODE == 0 ? T.grad[j] : T.param[j]) + 8 * p8;
+      g[j] = j == rank ? ldg8_cs(src) : ldg8_cv(src);
+    }
+    float x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; j++) {
+      if (j >= world) break;
+      const float w = T.w[j];
+#pragma unroll
+      for (int k = 0; k < 8; k++) x[k] = fmaf(w, f8(g[j], k), x[k]);
+    }
+    if (MODE == 0) {
+      const V8 vq = ldg8(vel + 8 * i), xq = ldg8(T.param[rank] + 8 * p8);
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        v[k] = fmaf(mom, f8(vq, k), x[k]);
+        x[k] = fmaf(-lr, v[k], f8(xq, k));
+      }
+      stg8(vel + 8 * i, v8_of(v));
+    }
+    const V8 xo = v8_of(x);
+    const uint4 xb = make_uint4(bf16_bits(x[0]) | (bf16_bits(x[1]) << 16), bf16_bits(x[2]) | (bf16_bits(x[3]) << 16),
+                                bf16_bits(x[4]) | (bf16_bits(x[5]) << 16), bf16_bits(x[6]) | (bf16_bits(x[7]) << 16));
+#pragma unroll
+    for (int j = 0; j < kMaxRanks; j++) {
+      if (j >= world) break;
+      const int jj = (rank + j) % world;  // stagger the peers to spread NVLink traffic
+      stg8(T.param[jj] + 8 * p8, xo);
+      if (BF16) reinterpret_cast<uint4*>(T.param_bf16[jj])[p8] = xb;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t arrived = atomicAdd(my_sig + 32, 1u) + 1u;
+    if (arrived == gen * gridDim.x) {
+      for (int j = 0; j < world; j++) st_release_sys(T.signal[j] + 16 + rank, gen);
+      wait_flags(my_sig + 16, world, gen, my_sig + 48);
+    }
+  }
+}
+
 // float4s per thread and trip / resident CTAs per SM (DBS_COMM_UNROLL, DBS_COMM_CTAS:
 // measurement switches; defaults are the measured configuration)
 int comm_unroll() {
@@ -215,6 +293,15 @@ int comm_ctas_per_sm() {
     return (v >= 1 && v <= 8) ? v : 2;
   }();
   return c;
+}
+
+// 256-bit exchange kernel (fused8_kernel) unless DBS_COMM_WIDE=0 (measurement switch)
+bool comm_wide() {
+  static const bool on = [] {
+    const char* e = getenv("DBS_COMM_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int ipc_handle_size() { return (int)sizeof(cudaIpcMemHandle_t); }
@@ -253,6 +340,23 @@ int launch_fused(dbs_comm* c, const int64_t* batch_sizes, int32_t mode, int kind
   const int64_t shard4 = c->shard / 4;
   const bool bf = c->shadow_prec == DBS_PREC_BF16;
   const int u = comm_unroll();
+  if (comm_wide() && (kind != 0 || ((uintptr_t)vel % 32) == 0)) {
+    const int64_t shard8 = c->shard / 8;
+#define DBS_COMM_LAUNCH8(K, B)                                                                                        \
+  fused8_kernel<K, B><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard8, K == 0 ? lr : 0.f,         \
+                                                   K == 0 ? mom : 0.f, K == 0 ? vel : nullptr, c->gen)
+    if (kind == 0 && bf)
+      DBS_COMM_LAUNCH8(0, true);
+    else if (kind == 0)
+      DBS_COMM_LAUNCH8(0, false);
+    else if (bf)
+      DBS_COMM_LAUNCH8(1, true);
+    else
+      DBS_COMM_LAUNCH8(1, false);
+#undef DBS_COMM_LAUNCH8
+    DBS_LAUNCH_CHECK();
+    return DBS_OK;
+  }
 #define DBS_COMM_LAUNCH(K, B, U)                                                                                     \
   fused_kernel<K, B, U><<<c->grid, kThreads, 0, s>>>(c->table, c->rank, c->world, shard4, K == 0 ? lr : 0.f,     \
                                                      K == 0 ? mom : 0.f,                                          \
