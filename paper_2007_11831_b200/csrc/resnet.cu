@@ -18,7 +18,8 @@
 //             bf16 accumulation of the shortcut gradient -> wgrad = dY^T im2col(X)
 //             (split-K, fp32 atomics into the flat gradient)
 // BatchNorm uses the worker's own batch statistics (local BN, as in DDP without
-// SyncBN); running statistics are not tracked (training throughput path).
+// SyncBN); the f32 mode also keeps torch-style running statistics
+// (dbs_resnet_running_stats).
 #include <math.h>
 #include <stdlib.h>
 

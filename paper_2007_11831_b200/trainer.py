@@ -940,7 +940,9 @@ class DistributedTrainer(SimulatedTrainer):
                             spinning.append((wk, ctas))
                     elif ev is not None and ev.extra_epoch_seconds:
                         slots[w].spin_ns = int(ev.extra_epoch_seconds * 1e9 / max(iters, 1))
-                        slots[w].spin_ctas = self.workers[w].sm_count
+                        # own partition: the whole partition; shared GPU: a 2-CTA timed spin that
+                        # delays only this worker's stream
+                        slots[w].spin_ctas = self.workers[w].sm_count if self.workers[w].ctx else 2
             rank_batches = np.asarray([sum(batches[r * n_loc:(r + 1) * n_loc]) for r in range(self.world)],
                                       dtype=np.int64)
             if iters > 0:
