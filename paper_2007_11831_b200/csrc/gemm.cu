@@ -93,6 +93,9 @@ struct GemmParams {
   int64_t halo_tiles;   // halo variant: images x tiles per image
   int d_trans;          // F32 atomic epilogue: D stored transposed (d[n * ldd + m])
   int b_wide;           // flipped-filter B (mode 3): one 4-D box per k-block covers all BN / 64 channel blocks
+  int dbg;              // measurement only (DBS_GEMM_DBG, S32 path): 1 = no TMA loads, 2 = no MMAs, 4 = no epilogue work
+  int tf_nbuf;          // S32, BN = 128: 1 = one TMEM buffer of two main accumulators, 2 = two buffers
+                        //   of one main each (tile j's epilogue overlaps tile j + 1's MMAs)
 };
 
 // two floats -> packed bf16x2 (lo in bits 0..15), one round-to-nearest-even
@@ -947,6 +950,12 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
         continue;
       }
       if (kp5) mbar_wait(&empty[s + 1], (((it + 1) / kStages) & 1) ^ 1);
+      if (p.dbg & 1) {  // attribution run: the ring without its loads
+        mbar_arrive(&full[s]);  // (K-paired: the odd k-block arrives on its own slot above)
+        if (tap_k) tc.advance(p.ga);
+        if (k_pix) pc.advance(gk);
+        continue;
+      }
       mbar_arrive_expect_tx(&full[s], (a_bytes + C::kBBytes) * (kp5 ? 2u : 1u));
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
@@ -1083,6 +1092,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kMains = kTf ? CT::kMains : 1;
   constexpr uint32_t kBufCols = kTf ? CT::kBufCols : kAccCols;
   constexpr int kNumBuf = kTf ? CT::kNumBuf : 2;  // accumulator buffers (tile j uses j % kNumBuf)
+  // S32 BN = 128: the buffer split is chosen per launch (p.tf_nbuf); mains is 1, 2 or 4
+  constexpr bool kRtBuf = kTf && BN >= 128;
+  const int nbuf = kRtBuf ? p.tf_nbuf : kNumBuf;
+  const int mains = kRtBuf ? (p.tf_nbuf == 2 ? 1 : kMains) : kMains;
+  const uint32_t bufcols = kRtBuf ? 512u / (uint32_t)p.tf_nbuf : kBufCols;
   constexpr uint32_t kTmemCols = kHalo ? H::kTmemCols : (kTf ? 512u : C::kTmemCols);
   constexpr uint32_t kSlotA = kHT ? HT::kASlotBytes : (kHalo ? H::kSlotBytes : (kTf ? CT::kABytes : C::kABytes));
   constexpr uint32_t kSlotB = kHT ? HT::kBBytes : (kHalo ? 0u : (kTf ? CT::kBBytes : C::kBBytes));
@@ -1328,31 +1342,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kb_begin, cls;
       const int num_k = decode(t, m0, n0, kb_begin, cls);
       if (num_k == 0) continue;
-      const int b = kNumBuf == 1 ? 0 : (int)(j & 1);
-      mbar_wait(&acc_empty[b], (kNumBuf == 1 ? (j & 1) : ((j >> 1) & 1)) ^ 1);
+      const int b = nbuf == 1 ? 0 : (int)(j & 1);
+      mbar_wait(&acc_empty[b], (nbuf == 1 ? (j & 1) : ((j >> 1) & 1)) ^ 1);
       if (j < 10) GEMM_TRACE(12 + j);
       tc_fence_after();
-      const uint32_t d_buf = tmem_base + b * kBufCols;
+      const uint32_t d_buf = tmem_base + b * bufcols;
       for (int i = 0; i < num_k; i++, it++) {
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
         if (it < 12) GEMM_TRACE(112 + it);
         tc_fence_after();
-        const uint32_t d_main = d_buf + (i % kMains) * CT::kPairCols;  // [main | correction] pair
+        const uint32_t d_main = d_buf + (i & (mains - 1)) * CT::kPairCols;  // [main | correction] pair
         const uint32_t a_off = kp5 ? (uint32_t)((s & ~1) * kSlotA + (s & 1) * 4096) : (uint32_t)(s * kSlotA);
         const uint32_t b_off = kp5 ? (uint32_t)((s & ~1) * kSlotB + (s & 1) * 4096) : (uint32_t)(s * kSlotB);
         const uint64_t a_hi = a_desc0 + (uint64_t)(a_off >> 4), b_hi = b_desc0 + (uint64_t)(b_off >> 4);
-        if (!b_pairs) {
+        if (p.dbg & 2) {
+          // attribution run: the ring without its MMAs
+        } else if (!b_pairs) {
 #pragma unroll
           for (int k = 0; k < 4; k++) {
-            const uint32_t acc = (i < kMains && k == 0) ? 0u : 1u;
+            const uint32_t acc = (i < mains && k == 0) ? 0u : 1u;
             mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc2, acc);
             mma_tf32_ss(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
           }
         } else {
 #pragma unroll
           for (int k = 0; k < 4; k++) {
-            const uint32_t acc = (i < kMains && k == 0) ? 0u : 1u;
+            const uint32_t acc = (i < mains && k == 0) ? 0u : 1u;
             mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc, acc);
             mma_tf32_ss(d_main + BN, a_hi + k * a_kstep, b_hi + b_lo + k * b_kstep, idesc, acc);
             mma_tf32_ss(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
@@ -1425,11 +1441,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     int kb_begin, cls = -1;
     const int tile_k = kHT ? 9 * p.ga.cblocks : (kHalo ? 1 : decode(t, m0, n0, kb_begin, cls));
     if (tile_k == 0) continue;
-    const int nmain = tile_k < kMains ? tile_k : kMains;  // S32: main accumulators this tile wrote
+    const int nmain = tile_k < mains ? tile_k : mains;  // S32: main accumulators this tile wrote
     (void)nmain;
     const OutMap& om = cls >= 0 ? p.cls_omap[cls] : p.omap;
-    const int b = kNumBuf == 1 ? 0 : (int)(tj & 1);
-    mbar_wait(&acc_full[b], kNumBuf == 1 ? (tj & 1) : ((tj >> 1) & 1));
+    const int b = nbuf == 1 ? 0 : (int)(tj & 1);
+    mbar_wait(&acc_full[b], nbuf == 1 ? (tj & 1) : ((tj >> 1) & 1));
+    if (p.dbg & 4) {  // attribution run: no epilogue work
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      tj++;
+      continue;
+    }
     if (warp == 2 && lane == 0 && tj < 10) GEMM_TRACE(32 + tj);
     tc_fence_after();
     int64_t row = m0 + q * 32 + lane;
@@ -1451,7 +1474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i = rem / om.OW, jj = rem - i * om.OW;
       orow = (img * om.H + 2 * i + om.a) * om.W + 2 * jj + om.b;
     }
-    const uint32_t lane_addr = tmem_base + b * kBufCols + ((uint32_t)(q * 32) << 16);
+    const uint32_t lane_addr = tmem_base + b * bufcols + ((uint32_t)(q * 32) << 16);
     const bool stats = (p.sum_part != nullptr);
     // S32: fold the other main accumulators and the correction accumulator of chunk c
     // into r (fp32 adds, round to nearest; the corrections last)
@@ -2095,6 +2118,19 @@ void* current_ctx() {
   return c;
 }
 
+// S32 BN = 128 double buffering: largest k-step count per main accumulator
+// (DBS_TF_DB_STEPS).  288 = the steps a main takes in the 512-channel 3x3 convs with two
+// mains (K = 4608), so double buffering (K <= 2304 here: the 64 -> 128 .. 256 -> 256
+// convs) adds no error beyond the worst single-buffer case; 128 -> 128 3x3 forward
+// 172 -> 153 us in a 48-SM partition (profiles/r2/tf_double_buffer.txt)
+int tf_db_steps() {
+  static const int v = [] {
+    const char* e = getenv("DBS_TF_DB_STEPS");
+    return e ? atoi(e) : 288;
+  }();
+  return v;
+}
+
 template <int BN, bool kHalo = false, bool kTf = false>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits, cudaStream_t s) {
   constexpr size_t kSmem = (kHalo && kTf) ? HaloTfCfg::kSmem
@@ -2111,6 +2147,23 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, in
   }
   GemmParams q = p;
   q.splits = splits;
+  static const int dbg = [] {
+    const char* e = getenv("DBS_GEMM_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  q.dbg = kTf ? dbg : 0;
+  if (kTf && BN >= 128) {
+    // two accumulator buffers (one main each) when a tile accumulates at most
+    // tf_db_steps() k-steps into its main; else one buffer of two mains (the tensor
+    // core's in-TMEM accumulation truncates: fewer steps per accumulator = less error)
+    int kbt = (int)((p.K + 31) / 32);
+    if (splits > 1) kbt = p.kb_per_split;
+    if (p.nclass > 0) {
+      kbt = 0;
+      for (int c = 0; c < p.nclass; c++) kbt = p.cls_kb[c] > kbt ? p.cls_kb[c] : kbt;
+    }
+    q.tf_nbuf = 4 * kbt <= tf_db_steps() ? 2 : 1;
+  }
 
   // persistent: one CTA per SM of the current (possibly green) context
   const int64_t tiles = kHalo ? p.halo_tiles
