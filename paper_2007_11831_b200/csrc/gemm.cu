@@ -890,6 +890,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
 // hi/lo dimension of stride 128 B, so ONE box fetches both halves (except im2col
 // maps: two boxes).  The MMA issuer then runs (A hi, B hi), (A hi, B lo), (A lo, B hi).
 template <int BN>
+// (called by the whole producer warp: one elected lane issues each TMA / arrive)
 __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMap* tmA, const CUtensorMap* tmB,
                                            uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
                                            int64_t num_tiles, int64_t m_tiles, int64_t n_tiles, int num_k_total) {
@@ -943,43 +944,43 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
       const int L = kb_begin + i;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-      if (it < 12) GEMM_TRACE(100 + it);
+      if ((threadIdx.x & 31) == 0 && it - 36u < 12u) GEMM_TRACE(100 + (it - 36));  // (trace window: ring positions 36..47)
       if (kp5 && (i & 1)) {
-        mbar_arrive(&full[s]);  // its bytes completed on slot s - 1's barrier
+        mbar_arrive_w(&full[s]);  // its bytes completed on slot s - 1's barrier
         if (k_pix) pc.advance(gk);
         continue;
       }
       if (kp5) mbar_wait(&empty[s + 1], (((it + 1) / kStages) & 1) ^ 1);
       if (p.dbg & 1) {  // attribution run: the ring without its loads
-        mbar_arrive(&full[s]);  // (K-paired: the odd k-block arrives on its own slot above)
+        mbar_arrive_w(&full[s]);  // (K-paired: the odd k-block arrives on its own slot above)
         if (tap_k) tc.advance(p.ga);
         if (k_pix) pc.advance(gk);
         continue;
       }
-      mbar_arrive_expect_tx(&full[s], (a_bytes + C::kBBytes) * (kp5 ? 2u : 1u));
+      mbar_arrive_expect_tx_w(&full[s], (a_bytes + C::kBBytes) * (kp5 ? 2u : 1u));
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
       if (am >= 5) {
         const ConvGeom& g = p.ga;
         for (int gq = 0; gq < a_groups; gq++) {
           if (kp5) {
-            tma_load_5d(a + gq * 16384, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
+            tma_load_5d_w(a + gq * 16384, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
                         pc.oh * g.stride + at_r[gq] - g.pad, pc.n, 2 * (at_c[gq] / 32));
           } else if (am == 6) {
             const int cu = at_c[gq] * 4;
-            tma_load_im2col_4d(a + gq * 8192, tmA, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+            tma_load_im2col_4d_w(a + gq * 8192, tmA, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
                                pc.n, (uint16_t)at_s[gq], (uint16_t)at_r[gq]);
-            tma_load_im2col_4d(a + gq * 8192 + 4096, tmA, &full[s], cu + 64, pc.ow * g.stride - g.pad,
+            tma_load_im2col_4d_w(a + gq * 8192 + 4096, tmA, &full[s], cu + 64, pc.ow * g.stride - g.pad,
                                pc.oh * g.stride - g.pad, pc.n, (uint16_t)at_s[gq], (uint16_t)at_r[gq]);
           } else {
-            tma_load_5d(a + gq * 8192, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
+            tma_load_5d_w(a + gq * 8192, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
                         pc.oh * g.stride + at_r[gq] - g.pad, pc.n, 2 * (at_c[gq] / 32));
           }
         }
       } else if (am == 0) {
-        tma_load_3d(a, tmA, &full[s], 0, (int32_t)m0, 2 * L);  // {64, 128 rows, hi/lo}
+        tma_load_3d_w(a, tmA, &full[s], 0, (int32_t)m0, 2 * L);  // {64, 128 rows, hi/lo}
       } else if (am == 1) {
-        tma_load_4d(a, tmA, &full[s], 0, L * 32, 0, (int32_t)(m0 / 32));  // {64, 32 k, hi/lo, 4 groups}
+        tma_load_4d_w(a, tmA, &full[s], 0, L * 32, 0, (int32_t)(m0 / 32));  // {64, 32 k, hi/lo, 4 groups}
       } else if (am == 4) {
         const ConvGeom& g = p.ga;
         int h0, w0, oh, ow;
@@ -994,8 +995,8 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
           h0 = a_oh * g.stride - g.pad;
           w0 = a_ow * g.stride - g.pad;
         }
-        tma_load_im2col_4d(a, tmA, &full[s], tc.cb * 128, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
-        tma_load_im2col_4d(a + kBM * 128, tmA, &full[s], tc.cb * 128 + 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+        tma_load_im2col_4d_w(a, tmA, &full[s], tc.cb * 128, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+        tma_load_im2col_4d_w(a + kBM * 128, tmA, &full[s], tc.cb * 128 + 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
       } else {
         const ConvGeom& g = p.ga;
         int ah, aw;
@@ -1006,17 +1007,17 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
           ah = a_oh * g.stride + tc.r - g.pad;
           aw = a_ow * g.stride + tc.sx - g.pad;
         }
-        tma_load_5d(a, tmA, &full[s], 0, aw, ah, a_n, 2 * tc.cb);  // {64, pixels..., hi/lo}
+        tma_load_5d_w(a, tmA, &full[s], 0, aw, ah, a_n, 2 * tc.cb);  // {64, pixels..., hi/lo}
       }
       // B lands as [B_hi (BN columns) | B_lo (BN columns)]: one N = 2 BN operand
       if (bm == 0) {
-        tma_load_3d(b, tmB, &full[s], 0, (int32_t)n0, 2 * L);  // {64, BN rows, hi/lo}
+        tma_load_3d_w(b, tmB, &full[s], 0, (int32_t)n0, 2 * L);  // {64, BN rows, hi/lo}
       } else if (bm == 1) {
-        tma_load_4d(b, tmB, &full[s], 0, L * 32, (int32_t)(n0 / 32), 0);  // {64, 32 k, groups, hi/lo}
+        tma_load_4d_w(b, tmB, &full[s], 0, L * 32, (int32_t)(n0 / 32), 0);  // {64, 32 k, groups, hi/lo}
       } else if (bm == 3) {
         const ConvGeom& g = p.ga;
         const int rs_flip = tp.n > 0 ? (int)tp.rs[tc.rs] : (g.R - 1 - tc.r) * g.S + (g.S - 1 - tc.sx);
-        tma_load_5d(b, tmB, &full[s], 0, tc.cb * 32, (int32_t)(n0 / 32), 0, rs_flip);  // {64, 32 k, groups, hi/lo, rs}
+        tma_load_5d_w(b, tmB, &full[s], 0, tc.cb * 32, (int32_t)(n0 / 32), 0, rs_flip);  // {64, 32 k, groups, hi/lo, rs}
       } else {
         const ConvGeom& g = p.gb;
         constexpr uint32_t kLoB = BN * 128;
@@ -1024,20 +1025,20 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
         for (int j = 0; j < BN / 32; j++) {
           const int cu = (b_c0 / 32 + j) * 128;
           if (bm == 4) {
-            tma_load_im2col_4d(b + j * 4096, tmB, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+            tma_load_im2col_4d_w(b + j * 4096, tmB, &full[s], cu, pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
                                pc.n, (uint16_t)b_s, (uint16_t)b_r);
-            tma_load_im2col_4d(b + kLoB + j * 4096, tmB, &full[s], cu + 64, pc.ow * g.stride - g.pad,
+            tma_load_im2col_4d_w(b + kLoB + j * 4096, tmB, &full[s], cu + 64, pc.ow * g.stride - g.pad,
                                pc.oh * g.stride - g.pad, pc.n, (uint16_t)b_s, (uint16_t)b_r);
           } else if (p.pair_b == 2) {
             // all BN / 32 groups of the tile (one tap, consecutive channels) in ONE box
             // {64, 32 pixels, 2 x BN / 32 sub-blocks}: [hi g | lo g] per group as below
             if (j == 0)
-              tma_load_5d(b, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad, pc.oh * g.stride + b_r - g.pad, pc.n,
+              tma_load_5d_w(b, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad, pc.oh * g.stride + b_r - g.pad, pc.n,
                           2 * (b_c0 / 32));
           } else {
             // one {64, 32 pixels, hi/lo} box per group: [hi g | lo g] pairs (group stride 8 KB),
             // the un-fused layout (3 MMAs per k-step, see the issuer) -- half the TMA operations
-            tma_load_5d(b + j * 8192, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad,
+            tma_load_5d_w(b + j * 8192, tmB, &full[s], 0, pc.ow * g.stride + b_s - g.pad,
                         pc.oh * g.stride + b_r - g.pad, pc.n, 2 * (b_c0 / 32 + j));
           }
         }
@@ -1097,7 +1098,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nbuf = kRtBuf ? p.tf_nbuf : kNumBuf;
   const int mains = kRtBuf ? (p.tf_nbuf == 2 ? 1 : kMains) : kMains;
   const uint32_t bufcols = kRtBuf ? 512u / (uint32_t)p.tf_nbuf : kBufCols;
-  constexpr uint32_t kTmemCols = kHalo ? H::kTmemCols : (kTf ? 512u : C::kTmemCols);
+  constexpr uint32_t kTmemCols = kTf ? 512u : (kHalo ? H::kTmemCols : C::kTmemCols);  // (S32 halo: 2 x 256 columns too)
   constexpr uint32_t kSlotA = kHT ? HT::kASlotBytes : (kHalo ? H::kSlotBytes : (kTf ? CT::kABytes : C::kABytes));
   constexpr uint32_t kSlotB = kHT ? HT::kBBytes : (kHalo ? 0u : (kTf ? CT::kBBytes : C::kBBytes));
   constexpr uint32_t kBRes = (kHalo && !kHT) ? H::kBResBytes : 0u;
@@ -1153,12 +1154,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if constexpr (kTf) {
+    if (tmem_base != 0u) __trap();  // the S32 issuers address the whole-TMEM allocation from 0
+  }
   // everything above overlapped the previous kernel's tail; operands and outputs only from here
   pdl_trigger_and_wait();
   if (threadIdx.x == 0) GEMM_TRACE(1);
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 || kTf) {  // (S32 paths: the whole warp, one elected lane issues; see produce_tf)
    // ---------------- TMA producer ----------------
    uint32_t it = 0;  // ring position, continuous across tiles
    uint32_t pt = 0;
@@ -1170,25 +1174,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t a_bytes = 2u * (uint32_t)(p.halo_rows * W1) * 128u;
     uint32_t ia = 0;
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      if (pt < 10) GEMM_TRACE(2 + pt);
+      if (lane == 0 && pt < 10) GEMM_TRACE(2 + pt);
       pt++;
       const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
       const int P0 = (int)(t - (int64_t)img * p.halo_tpi) * kBM;
       for (int cb = 0; cb < g.cblocks; cb++, ia++) {
         const int sa = (int)(ia & 1);
         mbar_wait(&a_empty[sa], ((ia >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&a_full[sa], a_bytes);
-        tma_load_5d(sA + sa * kSlotA, &tmA, &a_full[sa], 0, -1, P0 / W1 - 1, img, 2 * cb);  // {64, W+1, rows, 1, hi/lo}
+        mbar_arrive_expect_tx_w(&a_full[sa], a_bytes);
+        tma_load_5d_w(sA + sa * kSlotA, &tmA, &a_full[sa], 0, -1, P0 / W1 - 1, img, 2 * cb);  // {64, W+1, rows, 1, hi/lo}
         for (int tap = 0; tap < 9; tap++, it++) {
           const int s = (int)(it % kStages);
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-          if (it < 12) GEMM_TRACE(100 + it);
-          mbar_arrive_expect_tx(&full[s], kSlotB);
+          if (lane == 0 && it < 12) GEMM_TRACE(100 + it);
+          mbar_arrive_expect_tx_w(&full[s], kSlotB);
           uint8_t* b = sB + s * kSlotB;
           if (p.b_mode == 0) {
-            tma_load_3d(b, &tmB, &full[s], 0, 0, 2 * (tap * g.cblocks + cb));  // {64, 64 rows, hi/lo}
+            tma_load_3d_w(b, &tmB, &full[s], 0, 0, 2 * (tap * g.cblocks + cb));  // {64, 64 rows, hi/lo}
           } else {  // flipped filter of the input gradient, MN-major {64, 32 k, groups, hi/lo, rs}
-            tma_load_5d(b, &tmB, &full[s], 0, cb * 32, 0, 0, 8 - tap);
+            tma_load_5d_w(b, &tmB, &full[s], 0, cb * 32, 0, 0, 8 - tap);
           }
         }
       }
@@ -1226,7 +1230,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    // (S32 streamed path: the whole warp runs the issuer loop and one elected lane issues,
+    // so the descriptors / TMEM addresses stay warp-uniform -- see mma_tf32_ss_warp)
+    if (lane == 0 || kTf) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = kTf ? make_idesc_tf32(kBM, BN, a_mn, b_mn) : make_idesc_bf16(kBM, BN, a_mn, b_mn);
     uint32_t it = 0, j = 0;
@@ -1242,9 +1248,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int b = (int)(j & 1);
         mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
-        if (j < 10) GEMM_TRACE(12 + j);
+        if (lane == 0 && j < 10) GEMM_TRACE(12 + j);
         tc_fence_after();
-        const uint32_t d_buf = tmem_base + b * kBufCols;
+        const uint32_t d_buf = b * kBufCols;  // (whole-TMEM allocation at address 0)
         const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
         const int off = ((int)(t - (int64_t)img * p.halo_tpi) * kBM) % W1;
         int i = 0;  // logical k-block of the tile (main accumulator round robin)
@@ -1257,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int tap = 0; tap < 9; tap++, it++, i++) {
             const int s = (int)(it % kStages);
             mbar_wait(&full[s], (it / kStages) & 1);
-            if (it < 12) GEMM_TRACE(112 + it);
+            if (lane == 0 && it < 12) GEMM_TRACE(112 + it);
             tc_fence_after();
             const int r = tap / 3, sx = tap - 3 * (tap / 3);
             const uint64_t a_hi = a_slot + (uint64_t)((off + r * W1 + sx) * 8);  // 128-byte rows
@@ -1266,16 +1272,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; k++) {
               const uint32_t acc = (i < kMains && k == 0) ? 0u : 1u;
-              mma_tf32_ss(d_main, a_hi + k * 2, b_hi + k * b_kstep, idesc2, acc);
-              mma_tf32_ss(d_main + BN, a_hi + a_lo + k * 2, b_hi + k * b_kstep, idesc1, 1u);
+              mma_tf32_ss_warp(d_main, a_hi + k * 2, b_hi + k * b_kstep, idesc2, acc);
+              mma_tf32_ss_warp(d_main + BN, a_hi + a_lo + k * 2, b_hi + k * b_kstep, idesc1, 1u);
             }
-            mma_commit(&empty[s]);
-            if (it < 12) GEMM_TRACE(64 + it);
+            mma_commit_warp(&empty[s]);
+            if (lane == 0 && it < 12) GEMM_TRACE(64 + it);
           }
-          mma_commit(&a_empty[sa]);
+          mma_commit_warp(&a_empty[sa]);
         }
-        mma_commit(&acc_full[b]);
-        if (j < 10) GEMM_TRACE(22 + j);
+        mma_commit_warp(&acc_full[b]);
+        if (lane == 0 && j < 10) GEMM_TRACE(22 + j);
         j++;
       }
     } else if constexpr (kHalo) {
@@ -1344,13 +1350,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (num_k == 0) continue;
       const int b = nbuf == 1 ? 0 : (int)(j & 1);
       mbar_wait(&acc_empty[b], (nbuf == 1 ? (j & 1) : ((j >> 1) & 1)) ^ 1);
-      if (j < 10) GEMM_TRACE(12 + j);
+      if (lane == 0 && j < 10) GEMM_TRACE(12 + j);
       tc_fence_after();
-      const uint32_t d_buf = tmem_base + b * bufcols;
+      const uint32_t d_buf = b * bufcols;  // (the 512-column allocation starts at TMEM address 0)
       for (int i = 0; i < num_k; i++, it++) {
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
-        if (it < 12) GEMM_TRACE(112 + it);
+        if (lane == 0 && it - 36u < 12u) GEMM_TRACE(112 + (it - 36));
         tc_fence_after();
         const uint32_t d_main = d_buf + (i & (mains - 1)) * CT::kPairCols;  // [main | correction] pair
         const uint32_t a_off = kp5 ? (uint32_t)((s & ~1) * kSlotA + (s & 1) * 4096) : (uint32_t)(s * kSlotA);
@@ -1362,23 +1368,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const uint32_t acc = (i < mains && k == 0) ? 0u : 1u;
-            mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc2, acc);
-            mma_tf32_ss(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
+            mma_tf32_ss_warp(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc2, acc);
+            mma_tf32_ss_warp(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
           }
         } else {
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const uint32_t acc = (i < mains && k == 0) ? 0u : 1u;
-            mma_tf32_ss(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc, acc);
-            mma_tf32_ss(d_main + BN, a_hi + k * a_kstep, b_hi + b_lo + k * b_kstep, idesc, acc);
-            mma_tf32_ss(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
+            mma_tf32_ss_warp(d_main, a_hi + k * a_kstep, b_hi + k * b_kstep, idesc, acc);
+            mma_tf32_ss_warp(d_main + BN, a_hi + k * a_kstep, b_hi + b_lo + k * b_kstep, idesc, acc);
+            mma_tf32_ss_warp(d_main + BN, a_hi + a_lo + k * a_kstep, b_hi + k * b_kstep, idesc, 1u);
           }
         }
-        mma_commit(&empty[s]);
+        mma_commit_warp(&empty[s]);
+        if (lane == 0 && it - 36u < 12u) GEMM_TRACE(64 + (it - 36));
       }
       // (a short tile, num_k < kMains, leaves the higher mains unwritten: the epilogue skips them)
-      mma_commit(&acc_full[b]);
-      if (j < 10) GEMM_TRACE(22 + j);
+      mma_commit_warp(&acc_full[b]);
+      if (lane == 0 && j < 10) GEMM_TRACE(22 + j);
       j++;
     }
     } else {

@@ -1497,15 +1497,16 @@ bool halo_ok(const Conv& c) {
   }();
   return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 && halo_fits(c.OH, c.OW);
 }
-// the fp32-class (S32) halo variant (gemm.cu HaloTfCfg): same shape, W <= 32.
-// Off by default (DBS_HALO_TF=1 enables it): it moves 22 KB per k-block instead of
-// 48 KB, but the streamed kernel is not ingest-bound -- traced in-kernel, both spend
-// ~600 cycles issuing one k-block's 8 MMAs (+ ~220 waiting on the ring) -- so the
-// halo's 1/(W + 1) junk positions made it 10% slower.
+// the fp32-class (S32) halo variant (gemm.cu HaloTfCfg): same shape, W <= 32.  On by
+// default (DBS_HALO_TF=0 disables it): it moves 22 KB per k-block instead of the
+// streamed kernel's 48 KB, whose two TMA boxes take the SM's TMA unit ~1000 cycles per
+// k-block.  (It lost while the MMAs were issued from one lane -- ~80 cycles of
+// uniform-register waterfall per instruction; with the warp-wide issue the worker
+// step drops 11.87 -> 11.00 ms, profiles/r2/mma_issue.txt.)
 bool halo_tf_ok(const Conv& c) {
   static const bool enabled = [] {
     const char* e = getenv("DBS_HALO_TF");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return enabled && c.k == 3 && c.stride == 1 && c.pad == 1 && c.cin == 64 && c.cout == 64 &&
          halo_tf_fits(c.OH, c.OW);

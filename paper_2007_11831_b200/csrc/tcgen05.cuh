@@ -96,6 +96,52 @@ __device__ __forceinline__ void tma_load_im2col_4d(void* dst, const void* desc, 
       : "memory");
 }
 
+// Warp-wide forms of the producer's instructions: called by a whole converged warp,
+// one elected lane issues, so the coordinates / addresses stay warp-uniform (from a
+// single lane every operand went through an R2UR / ELECT / BRA.U.ANY waterfall)
+#define DBS_ELECT_ASM(body) "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e " body "\n\t}"
+__device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+  asm volatile(DBS_ELECT_ASM("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;") ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+  asm volatile(DBS_ELECT_ASM("mbarrier.arrive.shared::cta.b64 _, [%0];") ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_w(void* dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1,
+                                              int32_t c2) {
+  asm volatile(DBS_ELECT_ASM(
+                   "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                   "%5}], [%2];") ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_w(void* dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1,
+                                              int32_t c2, int32_t c3) {
+  asm volatile(DBS_ELECT_ASM(
+                   "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                   "%5, %6}], [%2];") ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_w(void* dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1,
+                                              int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile(DBS_ELECT_ASM(
+                   "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                   "%5, %6, %7}], [%2];") ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col_4d_w(void* dst, const void* desc, uint64_t* bar, int32_t c0,
+                                                     int32_t w, int32_t h, int32_t n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(DBS_ELECT_ASM(
+                   "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+                   "%4, %5, %6}], [%2], {%7, %8};") ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(w), "r"(h), "r"(n), "h"(off_w),
+               "h"(off_h)
+               : "memory");
+}
+
 // ---- clusters / CTA pairs ---------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -202,6 +248,31 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t tmem_d, uint64_t adesc, uin
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
       "}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// The same, executed by a whole (converged) warp: one elected lane issues.  Called from
+// warp-uniform code, the operands stay in uniform registers -- issued from a single
+// lane (divergent code) every operand went through an R2UR / ELECT / BRA.U.ANY
+// waterfall per MMA, ~80 cycles of issue per instruction (profiles/r2/mma_issue.txt)
+__device__ __forceinline__ void mma_tf32_ss_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+      "}" ::"r"(smem_u32(bar))
       : "memory");
 }
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete

@@ -265,16 +265,17 @@ def test_bench_cpu_inputs_match_package(dev):
         assert all(np.array_equal(x, y) for x, y in zip(f(*args, seed=2), g(*args, seed=2)))
 
 
-def test_conv_s32_halo_variant(dev):
-    """The experimental fp32-class halo kernel (DBS_HALO_TF=1, read once per process:
-    run in a child) on the 64->64 3x3 shapes, fwd and dgrad at the same 5e-6 bound."""
+def test_conv_s32_streamed_variant(dev):
+    """The fp32-class 64->64 3x3 convs run the halo kernel by default; the streamed
+    kernel (DBS_HALO_TF=0, read once per process: run in a child) on the same shapes,
+    fwd and dgrad at the same 5e-6 bound."""
     import os
     import subprocess
     import sys
     from pathlib import Path
 
     root = Path(__file__).resolve().parent.parent
-    env = dict(os.environ, DBS_HALO_TF="1")
+    env = dict(os.environ, DBS_HALO_TF="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", str(Path(__file__).resolve()),
                         "-k", "conv_s32_fwd_dgrad_wgrad and 64-64-3-1"],
                        env=env, cwd=str(root), capture_output=True, text=True, timeout=600)
