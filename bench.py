@@ -412,7 +412,13 @@ def kernel_roofline(peaks, wl, precision, tr=None):
         rec = json.loads(tf.read_text()).get(f"{key}_{precision}")
         if rec:
             traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
-    kname = "gemm_bf16_kernel<64, false, true> (3xTF32)" if f32 else "gemm_bf16_kernel<64, true> (halo)"
+    if f32:
+        # (64 -> 64 3x3: the S32 halo kernel unless DBS_HALO_TF=0; wider convs: the streamed BN = 128 kernel)
+        halo = Co == 64 and C == 64 and k == 3 and stride == 1 and os.environ.get("DBS_HALO_TF", "1") != "0"
+        kname = ("gemm_bf16_kernel<64, true, true> (3xTF32, S32 halo)" if halo else
+                 f"gemm_bf16_kernel<{64 if Co <= 64 else 128}, false, true> (3xTF32)")
+    else:
+        kname = "gemm_bf16_kernel<64, true> (halo)" if Co == 64 else "gemm_bf16_kernel<128, false> (bf16)"
     return {"bound": "tensor", "kernel": f"{kname} implicit-GEMM conv {desc}, b={N} per worker, inside a "
                                          f"{sms}-SM partition",
             "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
