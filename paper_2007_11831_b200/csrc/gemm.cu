@@ -599,26 +599,26 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
     const bool tap_k = kTapK || (AM < 0 && (am == 2 || am == 4 || bm == 3));
     TapCursor tc{};
     if (tap_k) tc.init(p.ga, kb_begin);
-    if (num_k > 0) { GEMM_TRACE(2 + pt); pt++; }
+    if (num_k > 0) { if ((threadIdx.x & 31) == 0) GEMM_TRACE(2 + pt); pt++; }
     if ((p.pair_a | p.pair_b) == 0) {
     for (int i = 0; i < num_k; i++, it++) {
       const int kb = kb_begin + i;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-      if (it < 12) GEMM_TRACE(100 + it);
+      if ((threadIdx.x & 31) == 0 && it < 12) GEMM_TRACE(100 + it);
       // MN-major A: the upper 64 rows of the tile are skipped when they lie past
       // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
       // accumulator rows the epilogue masks
       const bool a_hi = (am != 1 && am < 5) || (m0 + 64 < p.M);
-      mbar_arrive_expect_tx(&full[s], (a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes);
+      mbar_arrive_expect_tx_w(&full[s], (a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes);
       const int32_t k0 = kb * kBK;
       uint8_t* a = sA + s * C::kABytes;
       uint8_t* b = sB + s * C::kBBytes;
       if (am == 0) {
-        tma_load_2d(a, tmA, &full[s], k0, (int32_t)m0);
+        tma_load_2d_w(a, tmA, &full[s], k0, (int32_t)m0);
       } else if (am == 1) {
-        tma_load_2d(a, tmA, &full[s], (int32_t)m0, k0);
-        if (a_hi) tma_load_2d(a + 8192, tmA, &full[s], (int32_t)m0 + 64, k0);
+        tma_load_2d_w(a, tmA, &full[s], (int32_t)m0, k0);
+        if (a_hi) tma_load_2d_w(a + 8192, tmA, &full[s], (int32_t)m0 + 64, k0);
       } else if (am >= 5) {
         // weight gradient, transposed: A[k = pixel][m = (r, s, c)] is the conv
         // input window of 64 output pixels at tap (r, s), channels c .. c + 63 --
@@ -628,10 +628,10 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         for (int j = 0; j < 2; j++) {
           if (j == 1 && !a_hi) break;
           if (am == 6)
-            tma_load_im2col_4d(a + j * 8192, tmA, &full[s], at_c[j], pc.ow * g.stride - g.pad,
+            tma_load_im2col_4d_w(a + j * 8192, tmA, &full[s], at_c[j], pc.ow * g.stride - g.pad,
                                pc.oh * g.stride - g.pad, pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
           else
-            tma_load_4d(a + j * 8192, tmA, &full[s], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
+            tma_load_4d_w(a + j * 8192, tmA, &full[s], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
                         pc.oh * g.stride + at_r[j] - g.pad, pc.n);
         }
         pc.advance(g);  // (only in the pixel-K branches: the producer thread is latency-critical)
@@ -654,7 +654,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
           h0 = a_oh * g.stride - g.pad;
           w0 = a_ow * g.stride - g.pad;
         }
-        tma_load_im2col_4d(a, tmA, &full[s], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+        tma_load_im2col_4d_w(a, tmA, &full[s], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
       } else {
         const ConvGeom& g = p.ga;
         const int cb = tc.cb;
@@ -668,13 +668,13 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
           ah = a_oh * g.stride + r - g.pad;
           aw = a_ow * g.stride + sx - g.pad;
         }
-        tma_load_4d(a, tmA, &full[s], cb * 64, aw, ah, a_n);
+        tma_load_4d_w(a, tmA, &full[s], cb * 64, aw, ah, a_n);
       }
       if (bm == 0) {
-        tma_load_2d(b, tmB, &full[s], k0, (int32_t)n0);
+        tma_load_2d_w(b, tmB, &full[s], k0, (int32_t)n0);
       } else if (bm == 1) {
 #pragma unroll
-        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, tmB, &full[s], (int32_t)n0 + 64 * j, k0);
+        for (int j = 0; j < BN / 64; j++) tma_load_2d_w(b + j * 8192, tmB, &full[s], (int32_t)n0 + 64 * j, k0);
       } else if (bm == 3) {
         // input gradient: the filter W[k][r][s][c] read in place as the flipped,
         // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
@@ -684,17 +684,17 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         const int r = tc.r, sx = tc.sx;
         const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
         if (p.b_wide) {
-          tma_load_4d(b, tmB, &full[s], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
+          tma_load_4d_w(b, tmB, &full[s], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
         } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
+          for (int j = 0; j < BN / 64; j++) tma_load_3d_w(b + j * 8192, tmB, &full[s], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
         }
       } else if (bm == 4) {
         const ConvGeom& g = p.gb;
         const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
-          tma_load_im2col_4d(b + j * 8192, tmB, &full[s], b_c0 + 64 * j, bow * g.stride - g.pad,
+          tma_load_im2col_4d_w(b + j * 8192, tmB, &full[s], b_c0 + 64 * j, bow * g.stride - g.pad,
                              boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
         pc.advance(g);
       } else {
@@ -702,7 +702,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
-          tma_load_4d(b + j * 8192, tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
+          tma_load_4d_w(b + j * 8192, tmB, &full[s], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
                       boh * g.stride + b_r - g.pad, bn_);
         pc.advance(g);
       }
@@ -715,15 +715,15 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
       const int s0 = (int)(it % kStages);
       for (int u = 0; u < npair; u++)
         mbar_wait(&empty[s0 + u], (((it + u) / kStages) & 1) ^ 1);
-      if (it < 12) GEMM_TRACE(100 + it);
+      if ((threadIdx.x & 31) == 0 && it < 12) GEMM_TRACE(100 + it);
       // MN-major A: the upper 64 rows of the tile are skipped when they lie past
       // M (e.g. the 64-channel weight gradient) -- their stale rows only reach
       // accumulator rows the epilogue masks
       const bool a_hi = (am != 1 && am < 5) || (m0 + 64 < p.M);
       // a pair's bytes all complete on full[s0]; full[s0 + 1] gets a plain
       // arrival (the MMA reaches slot s0 + 1 only after full[s0] completed)
-      mbar_arrive_expect_tx(&full[s0], npair * ((a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes));
-      mbar_arrive(&full[s0 + 1]);
+      mbar_arrive_expect_tx_w(&full[s0], npair * ((a_hi ? C::kABytes : C::kABytes / 2) + C::kBBytes));
+      mbar_arrive_w(&full[s0 + 1]);
       for (int u = 0; u < npair; u++) {
       const int s = s0 + u;
       const int kb = kb_begin + i + u;
@@ -741,18 +741,18 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
               if (j == 1 && !a_hi) break;
               uint8_t* aj = sA + (s0 + j) * C::kABytes;
               if (am == 6)
-                tma_load_im2col_4d(aj, tmA, &full[s0], at_c[j], pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
+                tma_load_im2col_4d_w(aj, tmA, &full[s0], at_c[j], pc.ow * g.stride - g.pad, pc.oh * g.stride - g.pad,
                                    pc.n, (uint16_t)at_s[j], (uint16_t)at_r[j]);
               else
-                tma_load_4d(aj, tmA, &full[s0], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
+                tma_load_4d_w(aj, tmA, &full[s0], at_c[j], pc.ow * g.stride + at_s[j] - g.pad,
                             pc.oh * g.stride + at_r[j] - g.pad, pc.n);
             }
             pc.advance(g);
             pc.advance(g);
           } else if (am == 0) {
-            tma_load_3d(a, tmA, &full[s0], 0, (int32_t)m0, kb);
+            tma_load_3d_w(a, tmA, &full[s0], 0, (int32_t)m0, kb);
           } else if (am == 1) {  // <= 64 rows: 128 k rows fill both halves of slot s0
-            tma_load_2d(a, tmA, &full[s0], (int32_t)m0, k0);
+            tma_load_2d_w(a, tmA, &full[s0], (int32_t)m0, k0);
           } else {
             const ConvGeom& g = p.ga;
             const int cb = tc.cb;
@@ -766,14 +766,14 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
               ah = a_oh * g.stride + r - g.pad;
               aw = a_ow * g.stride + sx - g.pad;
             }
-            tma_load_5d(a, tmA, &full[s0], 0, aw, ah, a_n, cb);
+            tma_load_5d_w(a, tmA, &full[s0], 0, aw, ah, a_n, cb);
           }
         }
       } else if (am == 0) {
-        tma_load_2d(a, tmA, &full[s0], k0, (int32_t)m0);
+        tma_load_2d_w(a, tmA, &full[s0], k0, (int32_t)m0);
       } else if (am == 1) {
-        tma_load_2d(a, tmA, &full[s0], (int32_t)m0, k0);
-        if (a_hi) tma_load_2d(a + 8192, tmA, &full[s0], (int32_t)m0 + 64, k0);
+        tma_load_2d_w(a, tmA, &full[s0], (int32_t)m0, k0);
+        if (a_hi) tma_load_2d_w(a + 8192, tmA, &full[s0], (int32_t)m0 + 64, k0);
       } else if (am == 4) {
         // im2col TMA: 128 consecutive output pixels (crossing rows / images) of
         // the window corner, shifted by the tap; the tensor map's bounding box
@@ -793,7 +793,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
           h0 = a_oh * g.stride - g.pad;
           w0 = a_ow * g.stride - g.pad;
         }
-        tma_load_im2col_4d(a, tmA, &full[s0], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
+        tma_load_im2col_4d_w(a, tmA, &full[s0], cb * 64, w0, h0, a_n, (uint16_t)ow, (uint16_t)oh);
       } else {
         const ConvGeom& g = p.ga;
         const int cb = tc.cb;
@@ -807,22 +807,22 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
           ah = a_oh * g.stride + r - g.pad;
           aw = a_ow * g.stride + sx - g.pad;
         }
-        tma_load_4d(a, tmA, &full[s0], cb * 64, aw, ah, a_n);
+        tma_load_4d_w(a, tmA, &full[s0], cb * 64, aw, ah, a_n);
       }
       if (p.pair_b) {
         if (u == 0) {
           if (bm == 0) {
-            tma_load_3d(b, tmB, &full[s0], 0, (int32_t)n0, kb);
+            tma_load_3d_w(b, tmB, &full[s0], 0, (int32_t)n0, kb);
           } else if (bm == 1) {  // BN = 64, MN-major: 128 k rows fill the B parts of slots s0, s0 + 1
-            tma_load_2d(b, tmB, &full[s0], (int32_t)n0, k0);
+            tma_load_2d_w(b, tmB, &full[s0], (int32_t)n0, k0);
           } else if (bm == 2 || bm == 4) {  // BN = 64: 128 output pixels in one box
             const ConvGeom& g = p.gb;
             const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
             if (bm == 4)
-              tma_load_im2col_4d(b, tmB, &full[s0], b_c0, bow * g.stride - g.pad, boh * g.stride - g.pad, bn_,
+              tma_load_im2col_4d_w(b, tmB, &full[s0], b_c0, bow * g.stride - g.pad, boh * g.stride - g.pad, bn_,
                                  (uint16_t)b_s, (uint16_t)b_r);
             else
-              tma_load_4d(b, tmB, &full[s0], b_c0, bow * g.stride + b_s - g.pad, boh * g.stride + b_r - g.pad, bn_);
+              tma_load_4d_w(b, tmB, &full[s0], b_c0, bow * g.stride + b_s - g.pad, boh * g.stride + b_r - g.pad, bn_);
             pc.advance(g);
             pc.advance(g);
           } else {  // mode 3, BN = 64: the two k-blocks are consecutive 64-row k ranges
@@ -832,16 +832,16 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
             const int r = tc.r, sx = tc.sx;
             const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
             if (p.b_wide)  // BN >= 128: all channel blocks x 128 k rows in one 4-D box (pair_b 3)
-              tma_load_4d(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
+              tma_load_4d_w(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
             else
-              tma_load_3d(b, tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
+              tma_load_3d_w(b, tmB, &full[s0], (int32_t)n0, rs_flip, cb * 64);
           }
         }
       } else if (bm == 0) {
-        tma_load_2d(b, tmB, &full[s0], k0, (int32_t)n0);
+        tma_load_2d_w(b, tmB, &full[s0], k0, (int32_t)n0);
       } else if (bm == 1) {
 #pragma unroll
-        for (int j = 0; j < BN / 64; j++) tma_load_2d(b + j * 8192, tmB, &full[s0], (int32_t)n0 + 64 * j, k0);
+        for (int j = 0; j < BN / 64; j++) tma_load_2d_w(b + j * 8192, tmB, &full[s0], (int32_t)n0 + 64 * j, k0);
       } else if (bm == 3) {
         // input gradient: the filter W[k][r][s][c] read in place as the flipped,
         // transposed filter Wt[c][R-1-r][S-1-s][k] -- MN-major boxes of 64 c x 64 k
@@ -851,17 +851,17 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         const int r = tc.r, sx = tc.sx;
         const int rs_flip = tp.n > 0 ? (int)tp.rs[rs] : (g.R - 1 - r) * g.S + (g.S - 1 - sx);
         if (p.b_wide) {
-          tma_load_4d(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
+          tma_load_4d_w(b, tmB, &full[s0], 0, cb * 64, (int32_t)(n0 >> 6), rs_flip);
         } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; j++) tma_load_3d(b + j * 8192, tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
+          for (int j = 0; j < BN / 64; j++) tma_load_3d_w(b + j * 8192, tmB, &full[s0], (int32_t)n0 + 64 * j, rs_flip, cb * 64);
         }
       } else if (bm == 4) {
         const ConvGeom& g = p.gb;
         const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
-          tma_load_im2col_4d(b + j * 8192, tmB, &full[s0], b_c0 + 64 * j, bow * g.stride - g.pad,
+          tma_load_im2col_4d_w(b + j * 8192, tmB, &full[s0], b_c0 + 64 * j, bow * g.stride - g.pad,
                              boh * g.stride - g.pad, bn_, (uint16_t)b_s, (uint16_t)b_r);
         pc.advance(g);
       } else {
@@ -869,7 +869,7 @@ __device__ __forceinline__ void produce(const GemmParams& p, const CUtensorMap* 
         const int bn_ = pc.n, boh = pc.oh, bow = pc.ow;
 #pragma unroll
         for (int j = 0; j < BN / 64; j++)
-          tma_load_4d(b + j * 8192, tmB, &full[s0], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
+          tma_load_4d_w(b + j * 8192, tmB, &full[s0], b_c0 + 64 * j, bow * g.stride + b_s - g.pad,
                       boh * g.stride + b_r - g.pad, bn_);
         pc.advance(g);
       }
@@ -1098,7 +1098,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nbuf = kRtBuf ? p.tf_nbuf : kNumBuf;
   const int mains = kRtBuf ? (p.tf_nbuf == 2 ? 1 : kMains) : kMains;
   const uint32_t bufcols = kRtBuf ? 512u / (uint32_t)p.tf_nbuf : kBufCols;
-  constexpr uint32_t kTmemCols = kTf ? 512u : (kHalo ? H::kTmemCols : C::kTmemCols);  // (S32 halo: 2 x 256 columns too)
+  // all 512 columns: the allocation then starts at TMEM address 0, a compile-time constant
+  // for the warp-wide issuers (a base read back from shared memory is not warp-uniform)
+  constexpr uint32_t kTmemCols = 512u;
   constexpr uint32_t kSlotA = kHT ? HT::kASlotBytes : (kHalo ? H::kSlotBytes : (kTf ? CT::kABytes : C::kABytes));
   constexpr uint32_t kSlotB = kHT ? HT::kBBytes : (kHalo ? 0u : (kTf ? CT::kBBytes : C::kBBytes));
   constexpr uint32_t kBRes = (kHalo && !kHT) ? H::kBResBytes : 0u;
@@ -1154,15 +1156,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if constexpr (kTf) {
-    if (tmem_base != 0u) __trap();  // the S32 issuers address the whole-TMEM allocation from 0
-  }
+  if (tmem_base != 0u) __trap();  // the issuers address the whole-TMEM allocation from 0
   // everything above overlapped the previous kernel's tail; operands and outputs only from here
   pdl_trigger_and_wait();
   if (threadIdx.x == 0) GEMM_TRACE(1);
 
   if (warp == 0) {
-    if (lane == 0 || kTf) {  // (S32 paths: the whole warp, one elected lane issues; see produce_tf)
+    {  // (the whole warp runs the producer; one elected lane issues each TMA / arrive)
    // ---------------- TMA producer ----------------
    uint32_t it = 0;  // ring position, continuous across tiles
    uint32_t pt = 0;
@@ -1199,28 +1199,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
    } else if constexpr (kHalo) {
     // the 9 filter taps, once per CTA
-    mbar_arrive_expect_tx(bres_full, H::kBResBytes);
+    mbar_arrive_expect_tx_w(bres_full, H::kBResBytes);
     for (int tap = 0; tap < 9; tap++) {
       uint8_t* b = sB + tap * H::kTapBytes;
       if (p.b_mode == 0) {
-        tma_load_2d(b, &tmB, bres_full, tap * 64, 0);
+        tma_load_2d_w(b, &tmB, bres_full, tap * 64, 0);
       } else {  // mode 3: flipped, transposed filter of the input gradient
-        tma_load_3d(b, &tmB, bres_full, 0, 8 - tap, 0);
+        tma_load_3d_w(b, &tmB, bres_full, 0, 8 - tap, 0);
       }
     }
     const ConvGeom& g = p.ga;
     const int W1 = g.OW + 1;
     const uint32_t halo_bytes = (uint32_t)(p.halo_rows * W1) * 128u;
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, it++) {
-      if (pt < 10) GEMM_TRACE(2 + pt);
+      if ((threadIdx.x & 31) == 0 && pt < 10) GEMM_TRACE(2 + pt);
       pt++;
       const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
       const int P0 = (int)(t - (int64_t)img * p.halo_tpi) * kBM;
       const int s = (int)(it % kStages);
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], halo_bytes);
+      mbar_arrive_expect_tx_w(&full[s], halo_bytes);
       // rows from one above the tile's first row, columns from -1 (zero fill)
-      tma_load_4d(sA + s * kSlotA, &tmA, &full[s], 0, -1, P0 / W1 - 1, img);
+      tma_load_4d_w(sA + s * kSlotA, &tmA, &full[s], 0, -1, P0 / W1 - 1, img);
     }
    } else if constexpr (kTf) {
    produce_tf<BN>(p, &tmA, &tmB, sA, sB, full, empty, num_tiles, m_tiles, n_tiles, num_k_total);
@@ -1230,9 +1230,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // (S32 streamed path: the whole warp runs the issuer loop and one elected lane issues,
-    // so the descriptors / TMEM addresses stay warp-uniform -- see mma_tf32_ss_warp)
-    if (lane == 0 || kTf) {
+    // (the whole warp runs the issuer loop and one elected lane issues, so the
+    // descriptors / TMEM addresses stay warp-uniform -- see mma_tf32_ss_warp)
+    {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = kTf ? make_idesc_tf32(kBM, BN, a_mn, b_mn) : make_idesc_bf16(kBM, BN, a_mn, b_mn);
     uint32_t it = 0, j = 0;
@@ -1297,11 +1297,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = (int)(j & 1);
         mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        GEMM_TRACE(12 + j);
-        const uint32_t d_tmem = tmem_base + b * kAccCols;
+        if ((threadIdx.x & 31) == 0) GEMM_TRACE(12 + j);
+        const uint32_t d_tmem = b * kAccCols;  // (whole-TMEM allocation at address 0)
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
-        if (j < 8) GEMM_TRACE(96 + 3 * j);
+        if ((threadIdx.x & 31) == 0 && j < 8) GEMM_TRACE(96 + 3 * j);
         tc_fence_after();
         const int img = (int)((uint32_t)t / (uint32_t)p.halo_tpi);
         const int off = ((int)(t - (int64_t)img * p.halo_tpi) * kBM) % W1;
@@ -1314,13 +1314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t b_t = b_desc0 + (uint64_t)((r * 3 + sx) * (H::kTapBytes >> 4));
 #pragma unroll
             for (int k = 0; k < kBK / 16; k++)
-              mma_bf16_ss(d_tmem, a_t + (uint64_t)(k * 2), b_t + (uint64_t)(k * b_kstep), idesc,
+              mma_bf16_ss_warp(d_tmem, a_t + (uint64_t)(k * 2), b_t + (uint64_t)(k * b_kstep), idesc,
                           (r | sx | k) != 0 ? 1u : 0u);
           }
         }
-        mma_commit(&empty[s]);
-        mma_commit(&acc_full[b]);
-        GEMM_TRACE(22 + j);
+        mma_commit_warp(&empty[s]);
+        mma_commit_warp(&acc_full[b]);
+        if ((threadIdx.x & 31) == 0) GEMM_TRACE(22 + j);
         j++;
       }
     } else {
@@ -1403,13 +1403,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (num_k == 0) continue;
       const int b = (int)(j & 1);
       mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
-      GEMM_TRACE(12 + j);
+      if ((threadIdx.x & 31) == 0) GEMM_TRACE(12 + j);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + b * kAccCols;
+      const uint32_t d_tmem = b * kAccCols;  // (whole-TMEM allocation at address 0)
       for (int i = 0; i < num_k; i++, it++) {
         const int s = (int)(it % kStages);
         mbar_wait(&full[s], (it / kStages) & 1);
-        if (it < 12) GEMM_TRACE(112 + it);
+        if ((threadIdx.x & 31) == 0 && it < 12) GEMM_TRACE(112 + it);
         tc_fence_after();
         // (pair_a == 2: an MN-major A of <= 64 rows whose paired box put k-block
         // kb + 1 in the unused upper half of slot s - 1)
@@ -1421,12 +1421,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t b_s = b_desc0 + (uint64_t)(b_off >> 4);
 #pragma unroll
         for (int k = 0; k < kBK / 16; k++)
-          mma_bf16_ss(d_tmem, a_s + (uint64_t)(k * a_kstep), b_s + (uint64_t)(k * b_kstep), idesc,
+          mma_bf16_ss_warp(d_tmem, a_s + (uint64_t)(k * a_kstep), b_s + (uint64_t)(k * b_kstep), idesc,
                       (i | k) != 0 ? 1u : 0u);
-        mma_commit(&empty[s]);
+        mma_commit_warp(&empty[s]);
       }
-      mma_commit(&acc_full[b]);
-      GEMM_TRACE(22 + j);
+      mma_commit_warp(&acc_full[b]);
+      if ((threadIdx.x & 31) == 0) GEMM_TRACE(22 + j);
       j++;
     }
     }

@@ -108,6 +108,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t 
 __device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
   asm volatile(DBS_ELECT_ASM("mbarrier.arrive.shared::cta.b64 _, [%0];") ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_w(void* dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1) {
+  asm volatile(DBS_ELECT_ASM(
+                   "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+                   "%4}], [%2];") ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_w(void* dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1,
                                               int32_t c2) {
   asm volatile(DBS_ELECT_ASM(
@@ -232,6 +239,19 @@ __device__ __forceinline__ void mma_bf16_ss(uint32_t tmem_d, uint64_t adesc, uin
       ".reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// warp-wide form (see mma_tf32_ss_warp)
+__device__ __forceinline__ void mma_bf16_ss_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
       "}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
