@@ -103,7 +103,7 @@ class ClockSampler:
     """SM clock + throttle reasons sampled in-process (NVML) DURING the timed region."""
 
     def __init__(self, index=0):
-        self.index, self.samples = index, []
+        self.index, self.samples, self.power = index, [], []
         self._stop = threading.Event()
         self._t = None
 
@@ -125,6 +125,10 @@ class ClockSampler:
                         sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                         r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                         self.samples.append((sm, [n for n, b in names if r & b]))
+                        try:
+                            self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1e3)
+                        except Exception:
+                            pass
                     except Exception:
                         pass
                     self._stop.wait(0.25)
@@ -140,8 +144,11 @@ class ClockSampler:
             self._t.join(timeout=5)
         sm = [s for s, _ in self.samples]
         reasons = sorted({r for _, rs in self.samples for r in rs})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": getattr(self, "max_mhz", None),
-                "reasons": reasons, "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": getattr(self, "max_mhz", None),
+               "reasons": reasons, "samples": len(sm)}
+        if self.power:
+            out["power_w"] = round(float(np.median(self.power)), 1)
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -952,6 +959,9 @@ def main():
         "cpu_baseline": cpu,
         "bf16_variant": variant,
         "clocks": dbs["clocks"],
+        # (the fixed-plan epochs' own timed region: on one GPU the emulated workers share one
+        # power budget, and balanced DBS epochs keep every partition busy)
+        "clocks_fixed": fixed["clocks"],
         "gpu_launches": int(dbs["launches"]),
         "host_launches_per_epoch": round(dbs["host_launches"] / max(len(dbs["stats"]), 1), 1),
     }
