@@ -13,6 +13,8 @@
 // previous epoch's per_worker_gpu) is read from %globaltimer by 1-thread stamp
 // kernels in the worker's stream and accumulated on the device, so the
 // controller never waits for the host.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace dbs {
@@ -34,7 +36,13 @@ __device__ __forceinline__ long long globaltimer() {
 // address would congest the L2 slice and slow every kernel on the GPU.
 // 1024 threads x ~64 live registers fill the register file, 200 KB the shared
 // memory: nothing else can be co-resident on a pinned SM.
-__global__ void __launch_bounds__(kSpinThreads, 1) spin_until_kernel(const volatile int32_t* stop) {
+// sleep = 1 (the default): the resident CTA holds the SM's registers and shared memory
+// but its threads sleep (__nanosleep) between polls -- the SMs are pinned exactly as
+// before at a fraction of the power.  On one GPU the emulated workers share ONE power
+// budget: an FMA-burning disturbance pushed the balanced DBS epochs into the power cap
+// (1852-1927 MHz vs 1965 in the fixed-plan epochs), a coupling separate devices do not
+// have.  sleep = 0 keeps the FMA spin (DBS_SPIN_SLEEP=0).
+__global__ void __launch_bounds__(kSpinThreads, 1) spin_until_kernel(const volatile int32_t* stop, int sleep) {
   extern __shared__ float buf[];
   __shared__ volatile int done;
   if (threadIdx.x == 0) done = 0;
@@ -43,6 +51,17 @@ __global__ void __launch_bounds__(kSpinThreads, 1) spin_until_kernel(const volat
   float acc[48];
 #pragma unroll
   for (int j = 0; j < 48; j++) acc[j] = threadIdx.x + j;
+  if (sleep) {
+    for (int it = 1;; it++) {
+      __nanosleep(1000);
+      buf[threadIdx.x + (it & 31) * kSpinThreads] = acc[it & 7];
+      if ((it & 3) == 0) {
+        if (threadIdx.x == 0 && (*stop || globaltimer() - t0 > kSpinSafetyNs)) done = 1;
+        __syncthreads();
+        if (done) break;
+      }
+    }
+  } else
   for (int it = 1;; it++) {
 #pragma unroll 4
     for (int k = 0; k < 8; k++)
@@ -145,7 +164,11 @@ extern "C" int dbs_dev_spin_until(int32_t num_ctas, const volatile int32_t* d_st
   if (num_ctas == 0) return DBS_OK;
   int st = set_spin_attrs();
   if (st) return st;
-  spin_until_kernel<<<num_ctas, kSpinThreads, kSpinSmem, as_stream(stream)>>>(d_stop);
+  static const int sleep = [] {
+    const char* e = getenv("DBS_SPIN_SLEEP");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  spin_until_kernel<<<num_ctas, kSpinThreads, kSpinSmem, as_stream(stream)>>>(d_stop, sleep);
   DBS_LAUNCH_CHECK();
   return DBS_OK;
 }
