@@ -1485,6 +1485,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool stats = (p.sum_part != nullptr);
     // S32: fold the other main accumulators and the correction accumulator of chunk c
     // into r (fp32 adds, round to nearest; the corrections last)
+    // (rc: pair 0's correction chunk, prefetched with the next main chunk -- one TMEM
+    // round trip instead of two on the epilogue's serial path; same summation order)
+    uint32_t rc[kTf ? 32 : 1];
+    auto prefetch_corr = [&](int c) {
+      if constexpr (kTf) tmem_ld_32x32b_x32(lane_addr + BN + c * 32, rc);
+    };
+    auto add_corr_pref = [&](int c, uint32_t (&r)[32]) {
+      if constexpr (kTf) {
+#pragma unroll
+        for (int k = 0; k < 32; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(rc[k]));
+        uint32_t r2[32];
+        for (int m = 1; m < nmain; m++) {
+          for (int half = 0; half < 2; half++) {
+            tmem_ld_32x32b_x32(lane_addr + m * CT::kPairCols + half * BN + c * 32, r2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; k++) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+          }
+        }
+      }
+    };
     auto add_corr = [&](int c, uint32_t (&r)[32]) {
       if constexpr (kTf) {
         // r holds pair 0's main chunk: add the other pairs' mains, then every correction
@@ -1563,7 +1584,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
                 pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
                 pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
-          if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+          if (prefetch) {
+            tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+            prefetch_corr(c + 1);
+          }
           __syncwarp();
           uint16_t* dbase = reinterpret_cast<uint16_t*>(p.d) + n_base + (lane & 3) * 8;
           if (!kHalo && !om.on) {
@@ -1593,7 +1617,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // instead of 32 scalar ones; the split-K slices all hit the same lines)
 #pragma unroll
           for (int k = 0; k < 32; k++) tr[lane * 33 + k] = valid ? __uint_as_float(r[k]) : 0.0f;
-          if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+          if (prefetch) {
+            tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+            prefetch_corr(c + 1);
+          }
           __syncwarp();
           const int rq = 4 * (lane & 7);
           const int64_t mrow = m0 + q * 32 + rq;
@@ -1613,7 +1640,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[k] = valid ? __uint_as_float(r[k]) : 0.0f;
             vo[k] = 0.0f;
           }
-          if (prefetch) tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+          if (prefetch) {
+            tmem_ld_32x32b_x32(lane_addr + (c + 1) * 32, r);
+            prefetch_corr(c + 1);
+          }
           if (valid) epilogue_chunk<BN, kTf>(p, orow, n_base, v, cnt, vo);
           if (p.colsum_part != nullptr) {
             const int64_t g = (m0 >> 5) + q;
@@ -1624,7 +1654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (prefetch) {
           tmem_ld_wait();
-          add_corr(c + 1, r);
+          add_corr_pref(c + 1, r);
         }
         if (last) break;
       }
