@@ -33,6 +33,10 @@ PER_FILE = {
     "problems.cu": ["-fmad=false"],
     "theory.cu": ["-fmad=false"],
 }
+# measurement builds only: DBS_GEMM_ATTRIB=1 compiles gemm.cu's DBS_GEMM_DBG attribution
+# switches in (they cost the production kernels registers; rebuild with force after toggling)
+if os.environ.get("DBS_GEMM_ATTRIB") == "1":
+    PER_FILE["gemm.cu"] = ["-DDBS_GEMM_ATTRIB"]
 
 
 def nvcc() -> str:

@@ -66,6 +66,15 @@ __device__ unsigned long long g_gemm_trace[1024 * 128];
   } while (0)
 #endif
 
+// Attribution switches (DBS_GEMM_DBG at run time) exist only in a -DDBS_GEMM_ATTRIB build:
+// the run-time checks alone cost the S32 kernels registers / local-memory spills (ResNet-18
+// worker step 10.8 -> 10.4 ms without them; the MLP epoch ~10%)
+#ifdef DBS_GEMM_ATTRIB
+#define DBS_GEMM_DBG_BIT(p, bit) (((p).dbg & (bit)) != 0)
+#else
+#define DBS_GEMM_DBG_BIT(p, bit) (false)
+#endif
+
 struct GemmParams {
   int64_t M, N, K;
   int a_mode, b_mode;
@@ -93,7 +102,8 @@ struct GemmParams {
   int64_t halo_tiles;   // halo variant: images x tiles per image
   int d_trans;          // F32 atomic epilogue: D stored transposed (d[n * ldd + m])
   int b_wide;           // flipped-filter B (mode 3): one 4-D box per k-block covers all BN / 64 channel blocks
-  int dbg;              // measurement only (DBS_GEMM_DBG, S32 path): 1 = no TMA loads, 2 = no MMAs, 4 = no epilogue work
+  int dbg;              // measurement only (DBS_GEMM_DBG in a -DDBS_GEMM_ATTRIB build, S32 path): 1 = no TMA
+                        //   loads, 2 = no MMAs, 4 = no epilogue work
   int tf_nbuf;          // S32, BN = 128: 1 = one TMEM buffer of two main accumulators, 2 = two buffers
                         //   of one main each (tile j's epilogue overlaps tile j + 1's MMAs)
 };
@@ -951,7 +961,7 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
         continue;
       }
       if (kp5) mbar_wait(&empty[s + 1], (((it + 1) / kStages) & 1) ^ 1);
-      if (p.dbg & 1) {  // attribution run: the ring without its loads
+      if DBS_GEMM_DBG_BIT(p, 1) {  // attribution run: the ring without its loads
         mbar_arrive_w(&full[s]);  // (K-paired: the odd k-block arrives on its own slot above)
         if (tap_k) tc.advance(p.ga);
         if (k_pix) pc.advance(gk);
@@ -1362,7 +1372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t a_off = kp5 ? (uint32_t)((s & ~1) * kSlotA + (s & 1) * 4096) : (uint32_t)(s * kSlotA);
         const uint32_t b_off = kp5 ? (uint32_t)((s & ~1) * kSlotB + (s & 1) * 4096) : (uint32_t)(s * kSlotB);
         const uint64_t a_hi = a_desc0 + (uint64_t)(a_off >> 4), b_hi = b_desc0 + (uint64_t)(b_off >> 4);
-        if (p.dbg & 2) {
+        if DBS_GEMM_DBG_BIT(p, 2) {
           // attribution run: the ring without its MMAs
         } else if (!b_pairs) {
 #pragma unroll
@@ -1453,7 +1463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const OutMap& om = cls >= 0 ? p.cls_omap[cls] : p.omap;
     const int b = nbuf == 1 ? 0 : (int)(tj & 1);
     mbar_wait(&acc_full[b], nbuf == 1 ? (tj & 1) : ((tj >> 1) & 1));
-    if (p.dbg & 4) {  // attribution run: no epilogue work
+    if DBS_GEMM_DBG_BIT(p, 4) {  // attribution run: no epilogue work
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
