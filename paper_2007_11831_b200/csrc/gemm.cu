@@ -972,7 +972,9 @@ __device__ __forceinline__ void produce_tf(const GemmParams& p, const CUtensorMa
       uint8_t* b = sB + s * C::kBBytes;
       if (am >= 5) {
         const ConvGeom& g = p.ga;
-        for (int gq = 0; gq < a_groups; gq++) {
+#pragma unroll
+        for (int gq = 0; gq < 4; gq++) {  // (constant trip count: at_* stay in registers)
+          if (gq >= a_groups) break;
           if (kp5) {
             tma_load_5d_w(a + gq * 16384, tmA, &full[s], 0, pc.ow * g.stride + at_s[gq] - g.pad,
                         pc.oh * g.stride + at_r[gq] - g.pad, pc.n, 2 * (at_c[gq] / 32));
