@@ -582,7 +582,9 @@ int dbs_dev_gather_means(const double* d_v, const int64_t* d_idx, int64_t n_draw
 /* ------------------------------------------------------------------------ */
 /* Occupy `num_ctas` SMs (one resident CTA per SM, max shared memory) until
  * *d_stop becomes non-zero: the co-running disturbance of the paper's
- * robustness experiments.  Launch it on its own stream. */
+ * robustness experiments.  Launch it on its own stream.  The resident CTAs hold
+ * their SMs' registers and shared memory but sleep between polls (low power;
+ * DBS_SPIN_SLEEP=0 selects an FMA-burning spin). */
 int dbs_dev_spin_until(int32_t num_ctas, const volatile int32_t* d_stop, void* stream);
 /* Occupy `num_ctas` SMs for `nanoseconds` (fixed extra work). */
 int dbs_dev_spin_for(int32_t num_ctas, int64_t nanoseconds, void* stream);
